@@ -1,0 +1,231 @@
+/*
+ * paro.h — C ABI of the B200-native PaRO sync + update step (libparo.so).
+ *
+ * PaRO (arXiv 2310.06003): N GPUs are split into g = N/M groups of M
+ * (§3.1).  Each model state — parameters P, gradients G,
+ * optimizer state OS — is left unsharded (N), sharded inside a group (I) or
+ * sharded over all GPUs (G) (§3.1.1).  The 14 codes allowed by
+ * Principle 1 (Table 1) are accepted.  One paro_step is the
+ * s = 1 mini-batch update of mixed-precision Adam: reduce the bf16
+ * gradients to the optimizer-state shard (intra-group reduce-scatter, inter-group
+ * reduce-scatter / all-reduce, or the HO-Ring reduce-scatter, P:343, P:353-355,
+ * P:385-410), run fused unscale + fp32-master Adam on the owned shard, cast to
+ * bf16 into the all-gather buffer and all-gather the parameters back to their
+ * residency.
+ *
+ * Conventions for every call
+ *  - Sizes are int64_t element counts.  bf16 values are 2-byte words.
+ *  - Return value is a paro_status_t.  On failure paro_last_error() returns a
+ *    thread-local message valid until the next call on the same thread.
+ *  - CUDA / NCCL / device-timeout failures are sticky on the context: every
+ *    later call on it returns the same status until paro_finalize.
+ *  - Device pointers are CUDA global-memory pointers on the context's device.
+ *  - Calls on one context or plan are not thread-safe.
+ *
+ * Numerics (readings R2, R4-R7): gradients are pre-scaled by 1/N
+ * when first read (x = RNE_bf16(g * 1/N)); every reduction hop is
+ * RNE_bf16(fp32(a) + fp32(b)) in the canonical ring order; Adam is the
+ * AdamW form in fp32 with IEEE-rounded operations and no FMA; the result is
+ * bit-identical to unsharded data parallel for every strategy and for the
+ * hierarchical topologies (HO-Ring, two-step, direct) at fixed (N, M, bucket).
+ */
+#ifndef PARO_H_
+#define PARO_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  PARO_OK = 0,
+  PARO_ERR_INVALID = 1,  /* bad argument, strategy or cluster shape          */
+  PARO_ERR_OOM = 2,      /* device or host allocation failed                  */
+  PARO_ERR_CUDA = 3,     /* CUDA runtime error (sticky)                       */
+  PARO_ERR_NCCL = 4,     /* NCCL error (sticky)                               */
+  PARO_ERR_STATE = 5,    /* call not valid in this context mode / state       */
+  PARO_ERR_TIMEOUT = 6   /* a device-side cross-GPU wait timed out (sticky)   */
+} paro_status_t;
+
+typedef struct paro_ctx* paro_ctx_t;
+typedef struct paro_plan* paro_plan_t;
+
+/* Opaque NCCL unique id (ncclUniqueId is 128 bytes). */
+typedef struct { char bytes[128]; } paro_uid_t;
+
+/* Caller-allocated optimizer state of one rank: three fp32 device arrays of
+ * paro_plan_info_t.os_numel elements each, laid out bucket-major over the
+ * rank's OS residency (DESIGN.md §4 "HBM layout").  K = 12 bytes per element
+ * (Table 2). */
+typedef struct { float* master; float* m; float* v; } paro_opt_state_t;
+
+/* Topologies of the world-reaching gradient reduce-scatter / parameter
+ * all-gather (used when G in {N, G}; G = I always runs RS_I then the inter op). */
+enum {
+  PARO_TOPO_HO_RING = 0,   /* HO-Ring: intra and inter rings overlap  */
+  PARO_TOPO_TWO_STEP = 1,  /* intra ring then inter ring   */
+  PARO_TOPO_FLAT_RING = 2, /* one ring over all N ranks; different bits  */
+  PARO_TOPO_DIRECT = 3,    /* NVSwitch one-shot hierarchical: same bits as 0 / 1 */
+  PARO_TOPO_NCCL = 4       /* NCCL collectives on split comms: perf comparator,
+                              NOT bit-exact (NCCL's reduction order)              */
+};
+
+typedef struct {
+  int64_t bucket_elems;  /* default 1<<26; rounded down to a multiple of N*64     */
+  int topology;          /* PARO_TOPO_*, default PARO_TOPO_HO_RING                 */
+  float beta1, beta2;    /* 0.9, 0.95 (R5)                                         */
+  float eps;             /* 1e-8                                                   */
+  float weight_decay;    /* 0.0 (AdamW form, R5)                                   */
+  float loss_scale;      /* 1.0; gradients are unscaled by 1/loss_scale in Adam    */
+  int comm_ctas;         /* CTAs of the collective kernels (default 64)           */
+  int pipeline_depth;    /* buckets in flight between reduce and gather (def. 2)  */
+  void* stream;          /* cudaStream_t the step is ordered on; NULL = ctx stream */
+} paro_opts_t;
+
+typedef struct {
+  int64_t psi;           /* sum of param sizes                              */
+  int64_t psi_pad;       /* psi rounded up to a multiple of N*64 (R21)              */
+  int64_t bucket_elems;  /* effective bucket size B                                 */
+  int64_t n_buckets;
+  int64_t p_numel, g_numel, os_numel;  /* per-rank residency sizes (elements)      */
+  int64_t mem_p_bytes, mem_g_bytes, mem_os_bytes;  /* Table 2 at psi_pad           */
+  int64_t workspace_bytes;             /* library staging per rank                 */
+  int64_t step_send_bytes_intra;       /* this rank, one step, counted from the    */
+  int64_t step_send_bytes_inter;       /*   transfers the kernels perform          */
+  int32_t n_rounds;                    /* collective rounds per step (all buckets) */
+  int32_t n_comm_launches;             /* collective kernel launches per step      */
+} paro_plan_info_t;
+
+typedef struct {
+  double grad_norm;      /* sqrt(sum (g_hat * s_g)^2) over unique elements (R8)     */
+  int32_t nonfinite;     /* 1 if any reduced gradient was inf/NaN (R9: flag only)   */
+  int64_t sent_intra, sent_inter;  /* bytes this rank sent in the last step         */
+  int32_t kernel_launches;         /* library kernels launched by the last step     */
+} paro_step_stats_t;
+
+/* Fill *o with the defaults listed above. */
+void paro_opts_default(paro_opts_t* o);
+
+/* ---- contexts ------------------------------------------------------------ */
+
+/* New NCCL unique id; call on rank 0 and broadcast (e.g. with torch.distributed). */
+paro_status_t paro_get_unique_id(paro_uid_t* out);
+
+/* One rank of a real N-GPU job (one process per GPU).  world_size = N,
+ * group_size = M must divide N ("group_size must divide n_gpus").
+ * Creates the NCCL world communicator from uid, its intra (color = group) and
+ * inter (color = position) splits, the streams, and maps peer memory.
+ * Collective: all ranks must call it. */
+paro_status_t paro_init(int world_size, int group_size, int rank, const paro_uid_t* uid,
+                        int device, paro_ctx_t* out);
+
+/* All N ranks emulated in this one process on one device (no NCCL, no peer
+ * memory): every collective round becomes one kernel over all ranks' data.
+ * Used for bit-exact tests of any split on one GPU. */
+paro_status_t paro_init_emulated(int world_size, int group_size, int device, paro_ctx_t* out);
+
+/* Planning-only context: no CUDA calls.  paro_plan / paro_plan_info /
+ * paro_shard_range / paro_rank_send_bytes work; buffers and steps do not. */
+paro_status_t paro_init_planner(int world_size, int group_size, paro_ctx_t* out);
+
+paro_status_t paro_finalize(paro_ctx_t ctx);
+
+/* ---- plans ------------------------------------------------------------------ */
+
+/* Validate `strategy` (3 letters over {N,I,G} in P/G/OS order, Table 1; error
+ * strings "invalid shard level 'X' at position k", "strategy 'GGN' violates
+ * Principle 1 (S_P>=S_OS and S_G>=S_OS)"), lay the n_params tensors of
+ * param_sizes out densely in the given order, cut buckets, build the
+ * position-major shard map (R1), the per-bucket collective schedule and the
+ * accounting, and allocate the plan's device buffers (flat gradient buffer,
+ * parameter buffer, G-residency buffer, staging).  Collective in real mode. */
+paro_status_t paro_plan(paro_ctx_t ctx, const char* strategy, const int64_t* param_sizes,
+                        int n_params, const paro_opts_t* opts, paro_plan_t* out);
+
+paro_status_t paro_plan_info(paro_plan_t plan, paro_plan_info_t* out);
+
+/* Flat element range [*begin, *end) of state (0 = P, 1 = G, 2 = OS) held by
+ * `rank` inside bucket `bucket` (position-major nested map, R1). */
+paro_status_t paro_shard_range(paro_plan_t plan, int state, int rank, int64_t bucket,
+                               int64_t* begin, int64_t* end);
+
+/* Bucket [*begin, *end) in the flat parameter space. */
+paro_status_t paro_bucket_range(paro_plan_t plan, int64_t bucket, int64_t* begin, int64_t* end);
+
+/* Bytes `rank` sends per step on intra- and inter-group links, counted from the
+ * plan's transfer list (pull model, a byte read by a peer from this
+ * rank's memory counts as sent by this rank). */
+paro_status_t paro_rank_send_bytes(paro_plan_t plan, int rank, int64_t* intra, int64_t* inter);
+
+/* Library-owned device buffers of `rank` (must be a local rank):
+ *   kind 0: flat gradient buffer, bf16, psi_pad elements (zero-padded tail).
+ *           Writing gradients here and passing grads = NULL to paro_step is
+ *           the zero-copy path.
+ *   kind 1: parameter buffer, bf16, p_numel elements (P residency, bucket-major).
+ *   kind 2: G-residency buffer, bf16, g_numel elements (NULL for G = N, whose
+ *           gradient residency is the flat gradient buffer). */
+paro_status_t paro_buffer(paro_plan_t plan, int rank, int kind, void** ptr);
+
+/* Initialise one local rank's optimizer state and parameter buffer from a full
+ * fp32 master vector `master_full` (device, psi elements; padding = 0):
+ * master = its OS residency slice, m = v = 0, param buffer = RNE_bf16 of the P
+ * residency slice.  Stream-ordered on the plan stream. */
+paro_status_t paro_opt_state_init(paro_plan_t plan, int rank, const float* master_full,
+                                  const paro_opt_state_t* st);
+
+/* Same, with master weights from the counter-based synthetic generator
+ * (paro_synth) instead of a vector: no psi-sized temporary. */
+paro_status_t paro_opt_state_init_synth(paro_plan_t plan, int rank, uint64_t seed,
+                                        const paro_opt_state_t* st);
+
+/* Fill a local rank's flat gradient buffer with synthetic bf16 gradients of
+ * (seed, rank, step). */
+paro_status_t paro_synth_grads(paro_plan_t plan, int rank, uint64_t seed, int64_t step);
+
+/* One s = 1 sync + update step, stream-ordered and asynchronous.
+ *  grads:  NULL = gradients already in each local rank's flat gradient buffer;
+ *          else n_params bf16 device pointers per local rank (rank-major in
+ *          emulated mode), packed into the flat buffer first.
+ *  params: NULL = the plan's parameter buffer is the destination (zero copy);
+ *          else per local rank: n_params bf16 pointers (P = N) or one pointer
+ *          to p_numel elements (P = I, G) that receive a copy after the step.
+ *  opt_state: one paro_opt_state_t per local rank (rank order).
+ *  lr: this step's learning rate; step: 1-based Adam t ("step must be >= 1"). */
+paro_status_t paro_step(paro_plan_t plan, const void* const* grads, void* const* params,
+                        const paro_opt_state_t* opt_state, float lr, int64_t step);
+
+/* Per-kernel timing over a region of steps (used by bench.py for the roofline):
+ * paro_profile_start allocates `max_launches` CUDA event pairs and brackets
+ * every following library kernel launch on the stream it runs on;
+ * paro_profile_stop synchronises, sums the per-launch durations by kind and
+ * stops recording.  Launches beyond max_launches are not timed. */
+typedef struct {
+  double adam_ms;        /* sum of fused-Adam kernel durations                    */
+  double comm_ms;        /* sum of collective (rounds / NCCL) launch durations    */
+  int64_t adam_launches, comm_launches;
+  int64_t adam_elems;    /* elements the timed Adam launches processed            */
+  int64_t comm_bytes;    /* bytes this rank sent in the timed collective launches */
+  int64_t steps;         /* paro_step calls inside the region                     */
+  int64_t kernel_launches; /* all library kernel launches inside the region       */
+} paro_profile_t;
+
+paro_status_t paro_profile_start(paro_plan_t plan, int max_launches);
+paro_status_t paro_profile_stop(paro_plan_t plan, paro_profile_t* out);
+
+/* Synchronise the plan stream and return the last step's statistics.
+ * Returns PARO_ERR_TIMEOUT if a cross-GPU wait timed out on the device. */
+paro_status_t paro_step_stats(paro_plan_t plan, paro_step_stats_t* out);
+
+paro_status_t paro_plan_destroy(paro_plan_t plan);
+
+/* Thread-local message of the last failed call on this thread. */
+const char* paro_last_error(void);
+
+/* Library version string ("paro-b200 <semver> sm_100a"). */
+const char* paro_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PARO_H_ */

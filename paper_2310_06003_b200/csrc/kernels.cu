@@ -1,0 +1,444 @@
+// kernels.cu — sm_100a kernels of the PaRO sync + update step.
+//
+// Nothing here is a dense contraction, so there are no tensor-core paths:
+// every kernel is HBM- or NVLink-bound streaming code.
+//  * rounds_kernel: fold tasks of a collective round; 128-bit coalesced loads
+//    (ld.global.cg: L1 bypass, peers' lines are never cached stale), one
+//    8-element unit per 16 B, grid barrier + release/acquire peer flags.
+//  * adam_kernel: 28 B/elem single pass (ghat 2 + master/m/v 12 read,
+//    master/m/v 12 + bf16 param 2 written), streaming cache hints, fp64 norm
+//    partials through warp shuffles.
+// Numerics follow DESIGN R2 / R5-R7: every fp32 op is an explicit _rn
+// intrinsic, so nvcc cannot contract them to FMA; bf16 rounding is cvt.rn.
+#include <cuda_bf16.h>
+
+#include <cstdint>
+
+#include "kernels.h"
+
+namespace paro {
+
+namespace {
+
+constexpr int kRoundsBlock = 256;
+constexpr int kAdamBlock = 256;
+constexpr uint64_t kTimeoutNs = 20ull * 1000 * 1000 * 1000;  // 20 s per wait
+
+// ------------------------------------------------------------- bf16 helpers
+__device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
+
+__device__ __forceinline__ uint32_t pack2_rn(float lo, float hi) {
+  __nv_bfloat162 r = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&r);
+}
+
+__device__ __forceinline__ void unpack8(const uint4& v, float f[8]) {
+  f[0] = bf_lo(v.x); f[1] = bf_hi(v.x); f[2] = bf_lo(v.y); f[3] = bf_hi(v.y);
+  f[4] = bf_lo(v.z); f[5] = bf_hi(v.z); f[6] = bf_lo(v.w); f[7] = bf_hi(v.w);
+}
+
+__device__ __forceinline__ uint4 pack8(const float f[8]) {
+  uint4 v;
+  v.x = pack2_rn(f[0], f[1]); v.y = pack2_rn(f[2], f[3]);
+  v.z = pack2_rn(f[4], f[5]); v.w = pack2_rn(f[6], f[7]);
+  return v;
+}
+
+// x <- RNE_bf16(fp32(x) * alpha)  (pack / pre-divide, R4)
+__device__ __forceinline__ void scale_round8(float f[8], float alpha) {
+  float t[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) t[e] = __fmul_rn(f[e], alpha);
+  uint4 p = pack8(t);
+  unpack8(p, f);
+}
+
+// acc <- RNE_bf16(fp32(acc) + fp32(x))  (one hop, R2)
+__device__ __forceinline__ void hop8(float acc[8], const float x[8]) {
+  float t[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) t[e] = __fadd_rn(acc[e], x[e]);
+  uint4 p = pack8(t);
+  unpack8(p, acc);
+}
+
+// ------------------------------------------------------------- sync helpers
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long ld_acquire_gpu(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Grid-wide barrier of this rank, then release/acquire flags with `peers`.
+// Returns false (and leaves a sticky error word) on timeout.
+__device__ bool grid_peer_barrier(const RoundsArgs& a, uint64_t peers, int bidx) {
+  __shared__ int s_ok;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int ok = 1;
+    volatile int* err = a.bar.err;
+    __threadfence();
+    const unsigned long long target = a.arrive_base + (unsigned long long)(bidx + 1) * gridDim.x;
+    const unsigned long long old = atomicAdd(a.bar.arrive, 1ull);
+    const uint64_t val = a.serial * 256ull + (uint64_t)bidx + 1ull;
+    if (old + 1 == target) {          // last CTA of this GPU: publish to peers
+      __threadfence_system();
+      for (int x = 0; x < 64; ++x)
+        if ((peers >> x) & 1ull) st_release_sys(a.bar.peer_slot[x], val);
+    }
+    const uint64_t t0 = globaltimer();
+    while (ok && ld_acquire_gpu(a.bar.arrive) < target) {
+      if (*err || globaltimer() - t0 > kTimeoutNs) { ok = 0; atomicExch((int*)err, 2); }
+      __nanosleep(64);
+    }
+    for (int x = 0; x < 64 && ok; ++x) {
+      if (!((peers >> x) & 1ull)) continue;
+      while (ld_acquire_sys(&a.bar.my_flags[x]) < val) {
+        if (*err || globaltimer() - t0 > kTimeoutNs) { ok = 0; atomicExch((int*)err, 2); break; }
+        __nanosleep(64);
+      }
+    }
+    s_ok = ok;
+  }
+  __syncthreads();
+  return s_ok != 0;
+}
+
+// ------------------------------------------------------------- fold tasks
+template <int NIN, int UNR>
+__device__ __forceinline__ void run_fold(const DTask* __restrict__ t, int64_t u0, int64_t u1, float alpha) {
+  const uint4* in[NIN];
+#pragma unroll
+  for (int i = 0; i < NIN; ++i) in[i] = reinterpret_cast<const uint4*>(t->in[i]);
+  uint4* dst = reinterpret_cast<uint4*>(t->dst);
+  const uint32_t raw = t->rawmask;
+  const int64_t stride = blockDim.x;
+  for (int64_t ub = u0 + threadIdx.x; ub < u1; ub += stride * UNR) {
+    uint4 v[UNR][NIN];
+#pragma unroll
+    for (int k = 0; k < UNR; ++k) {
+      const int64_t u = ub + k * stride;
+      if (u < u1) {
+#pragma unroll
+        for (int i = 0; i < NIN; ++i) v[k][i] = __ldcg(in[i] + u);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < UNR; ++k) {
+      const int64_t u = ub + k * stride;
+      if (u >= u1) break;
+      float acc[8];
+      unpack8(v[k][0], acc);
+      if (raw & 1u) scale_round8(acc, alpha);
+#pragma unroll
+      for (int i = 1; i < NIN; ++i) {
+        float x[8];
+        unpack8(v[k][i], x);
+        if ((raw >> i) & 1u) scale_round8(x, alpha);
+        hop8(acc, x);
+      }
+      __stcg(dst + u, pack8(acc));
+    }
+  }
+}
+
+__device__ __noinline__ void run_fold_generic(const DTask* __restrict__ t, int64_t u0, int64_t u1, float alpha) {
+  uint4* dst = reinterpret_cast<uint4*>(t->dst);
+  const int nin = t->nin;
+  const uint32_t raw = t->rawmask;
+  for (int64_t u = u0 + threadIdx.x; u < u1; u += blockDim.x) {
+    float acc[8];
+    unpack8(__ldcg(reinterpret_cast<const uint4*>(t->in[0]) + u), acc);
+    if (raw & 1u) scale_round8(acc, alpha);
+    for (int i = 1; i < nin; ++i) {
+      float x[8];
+      unpack8(__ldcg(reinterpret_cast<const uint4*>(t->in[i]) + u), x);
+      if ((raw >> i) & 1u) scale_round8(x, alpha);
+      hop8(acc, x);
+    }
+    __stcg(dst + u, pack8(acc));
+  }
+}
+
+__device__ __forceinline__ void run_task(const DTask* __restrict__ t, int64_t u0, int64_t u1, float alpha) {
+  switch (t->nin) {
+    case 1: run_fold<1, 4>(t, u0, u1, alpha); break;
+    case 2: run_fold<2, 4>(t, u0, u1, alpha); break;
+    case 3: run_fold<3, 2>(t, u0, u1, alpha); break;
+    case 4: run_fold<4, 2>(t, u0, u1, alpha); break;
+    default: run_fold_generic(t, u0, u1, alpha); break;
+  }
+}
+
+__global__ void __launch_bounds__(kRoundsBlock) rounds_kernel(const RoundsArgs a) {
+  if (a.bar.err && *(volatile int*)a.bar.err) return;   // sticky device error: do nothing
+  int bidx = 0;
+  for (int r = 0; r < a.nrounds; ++r) {
+    const DRound rd = a.rounds[r];
+    if (a.bar.my_flags && !grid_peer_barrier(a, rd.peers_before, bidx++)) return;
+    const int64_t U = rd.units;
+    const int64_t per = (U + gridDim.x - 1) / gridDim.x;
+    const int64_t b0 = min(U, (int64_t)blockIdx.x * per);
+    const int64_t b1 = min(U, b0 + per);
+    int64_t base = 0;
+    for (int ti = rd.t0; ti < rd.t1 && base < b1; ++ti) {
+      const DTask* t = a.tasks + ti;
+      const int64_t n8 = t->n8;
+      const int64_t s = max(b0, base), e = min(b1, base + n8);
+      if (s < e) run_task(t, s - base, e - base, a.alpha);
+      base += n8;
+    }
+  }
+  if (a.bar.my_flags && a.final_barrier) grid_peer_barrier(a, a.final_peers, bidx++);
+}
+
+// ------------------------------------------------------------- Adam
+struct AdamScal {
+  float b1, omb1, b2, omb2, step_size, bc2s, eps, decay, s_g, alpha;
+  int has_wd;
+};
+
+__device__ __forceinline__ float adam_elem(float g, float& w, float& m, float& v, const AdamScal& c,
+                                           double& nsq, int& bad, bool in_norm) {
+  const float gr = __fmul_rn(g, c.s_g);
+  if (!isfinite(g)) bad = 1;
+  if (in_norm) nsq += (double)gr * (double)gr;
+  float ww = w;
+  if (c.has_wd) ww = __fmul_rn(ww, c.decay);
+  const float m2 = __fadd_rn(__fmul_rn(c.b1, m), __fmul_rn(c.omb1, gr));
+  const float v2 = __fadd_rn(__fmul_rn(c.b2, v), __fmul_rn(c.omb2, __fmul_rn(gr, gr)));
+  const float d = __fadd_rn(__fdiv_rn(__fsqrt_rn(v2), c.bc2s), c.eps);
+  const float w2 = __fsub_rn(ww, __fmul_rn(c.step_size, __fdiv_rn(m2, d)));
+  w = w2;
+  m = m2;
+  v = v2;
+  return w2;
+}
+
+__device__ __forceinline__ void adam_unit(const AdamSeg& sg, int64_t u, const AdamScal& c, double& nsq,
+                                          int& bad) {
+  const uint4 gv = __ldcs(reinterpret_cast<const uint4*>(sg.ghat) + u);
+  const float4* mp = reinterpret_cast<const float4*>(sg.master) + 2 * u;
+  const float4* m1p = reinterpret_cast<const float4*>(sg.m) + 2 * u;
+  const float4* v1p = reinterpret_cast<const float4*>(sg.v) + 2 * u;
+  float4 w0 = __ldcs(mp), w1 = __ldcs(mp + 1);
+  float4 m0 = __ldcs(m1p), m1 = __ldcs(m1p + 1);
+  float4 v0 = __ldcs(v1p), v1 = __ldcs(v1p + 1);
+  float g[8];
+  unpack8(gv, g);
+  if (sg.raw) scale_round8(g, c.alpha);
+  float w[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+  float m[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
+  float v[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+  const bool in_norm = sg.in_norm != 0;
+#pragma unroll
+  for (int e = 0; e < 8; ++e) adam_elem(g[e], w[e], m[e], v[e], c, nsq, bad, in_norm);
+  __stcs(reinterpret_cast<float4*>(sg.master) + 2 * u, make_float4(w[0], w[1], w[2], w[3]));
+  __stcs(reinterpret_cast<float4*>(sg.master) + 2 * u + 1, make_float4(w[4], w[5], w[6], w[7]));
+  __stcs(reinterpret_cast<float4*>(sg.m) + 2 * u, make_float4(m[0], m[1], m[2], m[3]));
+  __stcs(reinterpret_cast<float4*>(sg.m) + 2 * u + 1, make_float4(m[4], m[5], m[6], m[7]));
+  __stcs(reinterpret_cast<float4*>(sg.v) + 2 * u, make_float4(v[0], v[1], v[2], v[3]));
+  __stcs(reinterpret_cast<float4*>(sg.v) + 2 * u + 1, make_float4(v[4], v[5], v[6], v[7]));
+  // the bf16 parameter goes straight into its all-gather / parameter slot
+  reinterpret_cast<uint4*>(sg.param)[u] = pack8(w);
+}
+
+__global__ void __launch_bounds__(kAdamBlock) adam_kernel(const AdamArgs a) {
+  const AdamScal c{a.b1, a.omb1, a.b2, a.omb2, a.step_size, a.bc2s, a.eps, a.decay, a.s_g, a.alpha, a.has_wd};
+  int64_t U = 0;
+  for (int i = 0; i < a.nseg; ++i) U += a.seg[i].n8;
+  const int64_t per = (U + gridDim.x - 1) / gridDim.x;
+  const int64_t b0 = min(U, (int64_t)blockIdx.x * per);
+  const int64_t b1 = min(U, b0 + per);
+  double nsq = 0.0;
+  int bad = 0;
+  int64_t base = 0;
+  for (int i = 0; i < a.nseg && base < b1; ++i) {
+    const AdamSeg sg = a.seg[i];
+    const int64_t s = max(b0, base) - base, e = min(b1, base + sg.n8) - base;
+    for (int64_t u = s + threadIdx.x; u < e; u += 2 * blockDim.x) {
+      const int64_t u2 = u + blockDim.x;
+      adam_unit(sg, u, c, nsq, bad);
+      if (u2 < e) adam_unit(sg, u2, c, nsq, bad);
+    }
+    base += sg.n8;
+  }
+  // block reduction of the norm partial: warp shuffles, then one warp
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) nsq += __shfl_xor_sync(0xffffffffu, nsq, o);
+  __shared__ double s_part[kAdamBlock / 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) s_part[wid] = nsq;
+  const int any_bad = __syncthreads_or(bad);
+  if (wid == 0) {
+    double x = (lane < (int)(blockDim.x / 32)) ? s_part[lane] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    if (lane == 0) {
+      a.partials[blockIdx.x] = x;
+      if (any_bad) atomicOr(a.nonfinite, 1);
+    }
+  }
+}
+
+// ------------------------------------------------------------- norm finalize
+__global__ void __launch_bounds__(1024) norm_finalize_kernel(const double* p, int n, double* out) {
+  __shared__ double sh[1024];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s += p[i];
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[0] = sh[0];
+}
+
+// ------------------------------------------------------------- pack / copy
+__global__ void __launch_bounds__(256) pack_kernel(const PackEntry* table) {
+  const PackEntry e = table[blockIdx.y];
+  const bool vec = (((uintptr_t)e.src | (uintptr_t)e.dst) & 15) == 0;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+  int64_t done = 0;
+  if (vec) {
+    const int64_t n8 = e.n / 8;
+    const uint4* s = reinterpret_cast<const uint4*>(e.src);
+    uint4* d = reinterpret_cast<uint4*>(e.dst);
+    for (int64_t i = tid; i < n8; i += nth) d[i] = __ldcs(s + i);
+    done = n8 * 8;
+  }
+  for (int64_t i = done + tid; i < e.n; i += nth) e.dst[i] = e.src[i];
+}
+
+// ------------------------------------------------------------- synthetic inputs
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  uint64_t z = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ uint16_t synth_grad_bits(uint64_t key, uint64_t i) {
+  const uint64_t h = splitmix64(key ^ i);
+  const uint32_t sign = (uint32_t)(h >> 63);
+  const uint32_t expo = 114u + (uint32_t)((h >> 8) % 5ull);
+  const uint32_t mant = (uint32_t)((h >> 16) & 0x7Full);
+  return (uint16_t)((sign << 15) | (expo << 7) | mant);
+}
+
+__device__ __forceinline__ float synth_master(uint64_t key, uint64_t i) {
+  const uint64_t h = splitmix64(key ^ i);
+  const uint32_t sign = (uint32_t)(h >> 63);
+  const uint32_t expo = 119u + (uint32_t)((h >> 8) % 5ull);
+  const uint32_t mant = (uint32_t)(h & 0x7FFFFFull);
+  return __uint_as_float((sign << 31) | (expo << 23) | mant);
+}
+
+__global__ void synth_grad_kernel(uint16_t* dst, int64_t psi, int64_t psi_pad, uint64_t key) {
+  const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < psi_pad / 8; u += nth) {
+    uint16_t b[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int64_t i = u * 8 + e;
+      b[e] = (i < psi) ? synth_grad_bits(key, (uint64_t)i) : (uint16_t)0;
+    }
+    uint4 v;
+    v.x = b[0] | ((uint32_t)b[1] << 16); v.y = b[2] | ((uint32_t)b[3] << 16);
+    v.z = b[4] | ((uint32_t)b[5] << 16); v.w = b[6] | ((uint32_t)b[7] << 16);
+    reinterpret_cast<uint4*>(dst)[u] = v;
+  }
+}
+
+__global__ void init_range_kernel(const float* src, uint64_t key, int64_t begin, int64_t n, int64_t psi,
+                                  float* master, float* m, float* v, uint16_t* pdst) {
+  const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += nth) {
+    const int64_t f = begin + i;
+    float val = 0.f;
+    if (f < psi) val = src ? src[f] : synth_master(key, (uint64_t)f);
+    if (master) {
+      master[i] = val;
+      m[i] = 0.f;
+      v[i] = 0.f;
+    }
+    if (pdst) {
+      __nv_bfloat16 b = __float2bfloat16_rn(val);
+      pdst[i] = *reinterpret_cast<uint16_t*>(&b);
+    }
+  }
+}
+
+}  // namespace
+
+// ------------------------------------------------------------- launchers
+int adam_grid() { return 148 * 8; }
+int adam_block() { return kAdamBlock; }
+
+cudaError_t launch_rounds(const RoundsArgs& a, int grid, int block, cudaStream_t s) {
+  rounds_kernel<<<grid, block > 0 ? block : kRoundsBlock, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_adam(const AdamArgs& a, int grid, cudaStream_t s) {
+  adam_kernel<<<grid, kAdamBlock, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_norm_finalize(const double* partials, int n, double* out, cudaStream_t s) {
+  norm_finalize_kernel<<<1, 1024, 0, s>>>(partials, n, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pack(const PackEntry* table, int n_entries, int64_t max_n, cudaStream_t s) {
+  if (n_entries <= 0) return cudaSuccess;
+  int64_t bx = (max_n / 8 + 255) / 256;
+  if (bx < 1) bx = 1;
+  if (bx > 512) bx = 512;
+  dim3 grid((unsigned)bx, (unsigned)n_entries);
+  pack_kernel<<<grid, 256, 0, s>>>(table);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_synth_grad(uint16_t* dst, int64_t psi, int64_t psi_pad, uint64_t key, cudaStream_t s) {
+  synth_grad_kernel<<<148 * 16, 256, 0, s>>>(dst, psi, psi_pad, key);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_init_range(const float* src, uint64_t key, int64_t begin, int64_t n, int64_t psi,
+                              float* master, float* m, float* v, uint16_t* pdst, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  init_range_kernel<<<(unsigned)blocks, 256, 0, s>>>(src, key, begin, n, psi, master, m, v, pdst);
+  return cudaGetLastError();
+}
+
+uint64_t splitmix64_host(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  uint64_t z = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+uint64_t synth_key(uint64_t seed, uint64_t tag, uint64_t rank, uint64_t step) {
+  return splitmix64_host(splitmix64_host(seed ^ tag) ^ ((rank << 32) | step));
+}
+
+}  // namespace paro

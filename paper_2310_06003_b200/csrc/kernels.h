@@ -1,0 +1,104 @@
+// kernels.h — device-side descriptors and launchers of the sm_100a kernels.
+//
+//  * rounds kernel: executes a collective's rounds of fold tasks
+//      dst = (((in0 (+) in1) (+) in2) ...),  a (+) b = RNE_bf16(fp32 a + fp32 b)
+//    reading peers' buffers over NVLink (real mode) with a grid + peer-flag
+//    barrier between rounds; or one round per launch over all emulated ranks.
+//  * adam kernel: fused unscale + fp32-master Adam + RNE bf16 cast into the
+//    parameter / all-gather buffer + fp64 grad-norm partials (warp shuffles),
+//    28 B of HBM traffic per element.
+//  * pack / unpack, norm finalize, synthetic inputs.
+#pragma once
+
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+namespace paro {
+
+constexpr int kDevMaxIn = 16;
+constexpr int kMaxAdamSegs = 16;
+constexpr int kHeaderBytes = 4096;   // per-rank region header: flags + counters
+
+struct DTask {
+  const uint16_t* in[kDevMaxIn];
+  uint16_t* dst;
+  int64_t n8;        // 8-element (16-byte) units
+  int32_t nin;
+  uint32_t rawmask;  // bit i: input i is a raw gradient -> RNE_bf16(g * alpha)
+};
+
+struct DRound {
+  int32_t t0, t1;        // task range
+  int64_t units;         // sum of n8
+  uint64_t peers_before; // barrier peer mask before this round (real mode)
+};
+
+// Region header layout (bytes): [0, 512) uint64 flags[64] indexed by sender;
+// [512] uint64 arrive counter; [520] int32 error word.
+struct BarrierCtx {
+  uint64_t* const* peer_slot;   // [N] device array: &flags_of_peer_x[me]
+  uint64_t* my_flags;           // NULL => emulated mode (no barriers)
+  unsigned long long* arrive;
+  int* err;
+};
+
+struct RoundsArgs {
+  const DRound* rounds;
+  const DTask* tasks;
+  int nrounds;
+  int final_barrier;
+  uint64_t final_peers;
+  float alpha;
+  uint64_t serial;              // launch serial (same sequence on every rank)
+  unsigned long long arrive_base;
+  BarrierCtx bar;
+};
+
+struct AdamSeg {
+  const uint16_t* ghat;
+  float* master;
+  float* m;
+  float* v;
+  uint16_t* param;
+  int64_t n8;
+  int32_t raw;       // ghat is a raw gradient (N = 1): scale by alpha first
+  int32_t in_norm;   // elements counted in the unique-element norm
+};
+
+struct AdamArgs {
+  AdamSeg seg[kMaxAdamSegs];
+  int nseg;
+  float alpha;
+  float b1, omb1, b2, omb2, step_size, bc2s, eps, decay, s_g;
+  int has_wd;
+  double* partials;  // [gridDim.x] block partial sums of (g * s_g)^2
+  int* nonfinite;
+};
+
+struct PackEntry {     // one tensor slice: src/dst element pointers + count
+  const uint16_t* src;
+  uint16_t* dst;
+  int64_t n;
+};
+
+// launchers (return cudaGetLastError())
+cudaError_t launch_rounds(const RoundsArgs& a, int grid, int block, cudaStream_t s);
+cudaError_t launch_adam(const AdamArgs& a, int grid, cudaStream_t s);
+cudaError_t launch_norm_finalize(const double* partials, int n, double* out, cudaStream_t s);
+cudaError_t launch_pack(const PackEntry* table, int n_entries, int64_t max_n, cudaStream_t s);
+cudaError_t launch_synth_grad(uint16_t* dst, int64_t psi, int64_t psi_pad, uint64_t key, cudaStream_t s);
+// init master/m/v over flat range [begin, begin+n) into os arrays at os_ptrs and
+// params (bf16) at pdst (may be null); src == null => synthetic master from key
+cudaError_t launch_init_range(const float* src, uint64_t key, int64_t begin, int64_t n, int64_t psi,
+                              float* master, float* m, float* v, uint16_t* pdst, cudaStream_t s);
+int adam_grid();
+int adam_block();
+
+// splitmix64 counter hash (paro_synth) — host copy for key derivation
+uint64_t splitmix64_host(uint64_t x);
+uint64_t synth_key(uint64_t seed, uint64_t tag, uint64_t rank, uint64_t step);
+constexpr uint64_t kTagGrad = 0x4752414400000000ull;
+constexpr uint64_t kTagMaster = 0x4D41535400000000ull;
+
+}  // namespace paro

@@ -1,0 +1,973 @@
+// paro_api.cpp — C ABI (include/paro.h) and the step engine.
+//
+// Engine per step (real or emulated mode), bucket b in order:
+//   comm stream:    reduce(b)            [rounds kernel; NVLink pull + hop]
+//   compute stream: adam(b)              [after reduce(b): fused Adam + bf16 cast]
+//   comm stream:    gather(b - D)        [after adam(b - D): in-place all-gather]
+// then the remaining gathers, the norm finalize (+ NCCL scalar all-reduce) and
+// the join back onto the caller's stream.  Every rank issues the same launch
+// sequence, so the in-kernel peer barriers pair up.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/paro.h"
+#include "kernels.h"
+#include "planner.h"
+
+using namespace paro;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+paro_status_t fail(paro_status_t st, const std::string& msg) {
+  g_last_error = msg;
+  return st;
+}
+
+enum Mode { MODE_REAL = 0, MODE_EMU = 1, MODE_PLANNER = 2 };
+
+}  // namespace
+
+struct paro_ctx {
+  int mode = MODE_PLANNER;
+  int N = 1, M = 1, rank = 0, device = -1;
+  cudaStream_t main = nullptr, comm = nullptr, comp = nullptr;
+  ncclComm_t world = nullptr, intra = nullptr, inter = nullptr;
+  paro_status_t sticky = PARO_OK;
+  std::string sticky_msg;
+  int sm_count = 148;
+};
+
+struct DevLaunch {
+  int64_t bytes = 0;       // bytes the local rank(s) send in this launch
+  int64_t round_off = 0;   // index into the plan's DRound array
+  int nrounds = 0;
+  int final_barrier = 0;
+  uint64_t final_peers = 0;
+};
+
+struct paro_plan {
+  paro_ctx* ctx = nullptr;
+  std::unique_ptr<Planner> pl;
+  paro_opts_t opts{};
+  std::vector<int> local;                 // local ranks (real: {rank}, emulated: all)
+  std::vector<char*> region;              // per local rank: device region base
+  std::vector<char*> peer_base;           // [N] base as addressable from this process
+  uint64_t** d_peer_slot = nullptr;       // real mode
+  DRound* d_rounds = nullptr;
+  DTask* d_tasks = nullptr;
+  std::vector<DevLaunch> red, gat;        // per bucket
+  double* d_partials = nullptr;
+  int partials_cap = 0;
+  double* d_norm = nullptr;
+  int* d_nonfinite = nullptr;
+  PackEntry* d_pack = nullptr;
+  PackEntry* h_pack = nullptr;            // pinned staging
+  int pack_cap = 0;
+  cudaEvent_t ev_fork = nullptr, ev_comm = nullptr, ev_comp = nullptr, ev_pack_staged = nullptr,
+              ev_unpack_staged = nullptr;
+  std::vector<cudaEvent_t> ev_red, ev_adam;
+  uint64_t serial = 1;
+  unsigned long long arrive_base = 0;
+  cudaStream_t last_stream = nullptr;
+  int last_launches = 0;
+  bool stepped = false;
+  // profiling (paro_profile_start / stop)
+  bool prof = false;
+  std::vector<cudaEvent_t> prof_ev;       // 2 per launch
+  std::vector<int> prof_kind;             // 0 adam, 1 comm
+  std::vector<int64_t> prof_amount;       // adam: elements; comm: bytes sent
+  int prof_used = 0;
+  int64_t prof_steps = 0, prof_launches = 0;
+};
+// (the C API also declares a *function* named paro_plan, which hides the tag in C++)
+using PlanT = struct paro_plan;
+
+namespace {
+
+#define CK(call)                                                                         \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess) return cuda_fail(ctx, #call, e_);                             \
+  } while (0)
+#define NK(call)                                                                         \
+  do {                                                                                   \
+    ncclResult_t r_ = (call);                                                            \
+    if (r_ != ncclSuccess) return nccl_fail(ctx, #call, r_);                             \
+  } while (0)
+
+paro_status_t cuda_fail(paro_ctx* ctx, const char* what, cudaError_t e) {
+  std::string m = std::string(what) + ": " + cudaGetErrorString(e);
+  if (ctx) {
+    ctx->sticky = (e == cudaErrorMemoryAllocation) ? PARO_ERR_OOM : PARO_ERR_CUDA;
+    ctx->sticky_msg = m;
+    if (e == cudaErrorMemoryAllocation) ctx->sticky = PARO_OK;  // OOM is not sticky
+    return fail(e == cudaErrorMemoryAllocation ? PARO_ERR_OOM : PARO_ERR_CUDA, m);
+  }
+  return fail(PARO_ERR_CUDA, m);
+}
+
+paro_status_t nccl_fail(paro_ctx* ctx, const char* what, ncclResult_t r) {
+  std::string m = std::string(what) + ": " + ncclGetErrorString(r);
+  if (ctx) {
+    ctx->sticky = PARO_ERR_NCCL;
+    ctx->sticky_msg = m;
+  }
+  return fail(PARO_ERR_NCCL, m);
+}
+
+paro_status_t check_ctx(paro_ctx* ctx) {
+  if (!ctx) return fail(PARO_ERR_INVALID, "null context");
+  if (ctx->sticky != PARO_OK) return fail(ctx->sticky, "sticky error: " + ctx->sticky_msg);
+  if (ctx->mode != MODE_PLANNER) {
+    cudaError_t e = cudaSetDevice(ctx->device);
+    if (e != cudaSuccess) return cuda_fail(ctx, "cudaSetDevice", e);
+  }
+  return PARO_OK;
+}
+
+bool is_local(const PlanT* p, int rank) {
+  for (int r : p->local)
+    if (r == rank) return true;
+  return false;
+}
+
+int local_index(const PlanT* p, int rank) {
+  for (size_t i = 0; i < p->local.size(); ++i)
+    if (p->local[i] == rank) return (int)i;
+  return -1;
+}
+
+char* data_ptr(const PlanT* p, int rank, int kind, int64_t off) {
+  const Planner& pl = *p->pl;
+  return p->peer_base[rank] + kHeaderBytes + 2 * (pl.buf_off[kind] + off);
+}
+
+DTask resolve(const PlanT* p, const Task& t) {
+  DTask d{};
+  d.nin = t.nin;
+  d.n8 = t.n / 8;
+  d.rawmask = 0;
+  for (int i = 0; i < t.nin; ++i) {
+    d.in[i] = reinterpret_cast<const uint16_t*>(data_ptr(p, t.in[i].rank, t.in[i].kind, t.in[i].off));
+    if (t.in[i].kind == BUF_GRAD) d.rawmask |= 1u << i;
+  }
+  d.dst = reinterpret_cast<uint16_t*>(data_ptr(p, t.dst.rank, t.dst.kind, t.dst.off));
+  return d;
+}
+
+// Build device round/task arrays for every bucket's launches.
+paro_status_t upload_schedule(PlanT* p) {
+  paro_ctx* ctx = p->ctx;
+  const Planner& pl = *p->pl;
+  std::vector<DRound> rounds;
+  std::vector<DTask> tasks;
+  auto build = [&](const Launch& L) {
+    DevLaunch dl;
+    dl.round_off = (int64_t)rounds.size();
+    if (L.empty()) return dl;
+    const int R = (int)L.rounds.size();
+    for (int r = 0; r < R; ++r) {
+      DRound d{};
+      d.t0 = (int32_t)tasks.size();
+      d.units = 0;
+      if (ctx->mode == MODE_REAL) {
+        for (const Task& t : L.rounds[r][ctx->rank]) {
+          tasks.push_back(resolve(p, t));
+          d.units += t.n / 8;
+        }
+        d.peers_before = L.barrier_peers(r, ctx->rank);
+      } else {
+        for (int x = 0; x < pl.N; ++x)
+          for (const Task& t : L.rounds[r][x]) {
+            tasks.push_back(resolve(p, t));
+            d.units += t.n / 8;
+          }
+        d.peers_before = 0;
+      }
+      d.t1 = (int32_t)tasks.size();
+      rounds.push_back(d);
+    }
+    dl.nrounds = R;
+    dl.final_barrier = L.final_barrier ? 1 : 0;
+    // bytes sent by the local rank(s): what peers read from them in this launch
+    for (int r = 0; r < R; ++r)
+      for (int x = 0; x < pl.N; ++x)
+        for (const Task& t : L.rounds[r][x])
+          for (int i = 0; i < t.nin; ++i) {
+            const int y = t.in[i].rank;
+            if (y != x && (ctx->mode != MODE_REAL || y == ctx->rank)) dl.bytes += 2 * t.n;
+          }
+    dl.final_peers = (ctx->mode == MODE_REAL) ? L.barrier_peers(R, ctx->rank) : 0;
+    return dl;
+  };
+  p->red.clear();
+  p->gat.clear();
+  for (const BucketSchedule& S : pl.sched) {
+    p->red.push_back(build(S.reduce));
+    p->gat.push_back(build(S.gather));
+  }
+  if (!rounds.empty()) {
+    CK(cudaMalloc(&p->d_rounds, rounds.size() * sizeof(DRound)));
+    CK(cudaMemcpy(p->d_rounds, rounds.data(), rounds.size() * sizeof(DRound), cudaMemcpyHostToDevice));
+  }
+  if (!tasks.empty()) {
+    CK(cudaMalloc(&p->d_tasks, tasks.size() * sizeof(DTask)));
+    CK(cudaMemcpy(p->d_tasks, tasks.data(), tasks.size() * sizeof(DTask), cudaMemcpyHostToDevice));
+  }
+  return PARO_OK;
+}
+
+// Record the start event of a timed launch; returns the slot or -1.
+int prof_begin(PlanT* p, cudaStream_t s, int kind, int64_t amount) {
+  if (!p->prof || 2 * (p->prof_used + 1) > (int)p->prof_ev.size()) return -1;
+  const int k = p->prof_used++;
+  p->prof_kind[k] = kind;
+  p->prof_amount[k] = amount;
+  cudaEventRecord(p->prof_ev[2 * k], s);
+  return k;
+}
+void prof_end(PlanT* p, cudaStream_t s, int k) {
+  if (k >= 0) cudaEventRecord(p->prof_ev[2 * k + 1], s);
+}
+
+int comm_grid(const PlanT* p) {
+  int g = p->opts.comm_ctas > 0 ? p->opts.comm_ctas : 64;
+  if (p->ctx->mode == MODE_REAL) {
+    if (g > p->ctx->sm_count) g = p->ctx->sm_count;   // co-residency of all CTAs (barriers)
+  } else {
+    g = p->ctx->sm_count * 2;
+  }
+  return g;
+}
+
+// Launch one collective (reduce or gather of one bucket) on the comm stream.
+paro_status_t run_launch(PlanT* p, const DevLaunch& dl, int* nlaunch) {
+  paro_ctx* ctx = p->ctx;
+  if (dl.nrounds == 0) return PARO_OK;
+  const int grid = comm_grid(p);
+  RoundsArgs a{};
+  a.tasks = p->d_tasks;
+  a.alpha = (float)(1.0 / (double)p->pl->N);
+  if (ctx->mode == MODE_REAL) {
+    char* hdr = p->region[0];
+    a.rounds = p->d_rounds + dl.round_off;
+    a.nrounds = dl.nrounds;
+    a.final_barrier = dl.final_barrier;
+    a.final_peers = dl.final_peers;
+    a.serial = p->serial++;
+    a.arrive_base = p->arrive_base;
+    a.bar.peer_slot = p->d_peer_slot;
+    a.bar.my_flags = reinterpret_cast<uint64_t*>(hdr);
+    a.bar.arrive = reinterpret_cast<unsigned long long*>(hdr + 512);
+    a.bar.err = reinterpret_cast<int*>(hdr + 520);
+    p->arrive_base += (unsigned long long)(dl.nrounds + dl.final_barrier) * grid;
+    const int k = prof_begin(p, ctx->comm, 1, dl.bytes);
+    CK(launch_rounds(a, grid, 0, ctx->comm));
+    prof_end(p, ctx->comm, k);
+    ++*nlaunch;
+  } else {
+    for (int r = 0; r < dl.nrounds; ++r) {
+      a.rounds = p->d_rounds + dl.round_off + r;
+      a.nrounds = 1;
+      const int k = prof_begin(p, ctx->comm, 1, r == 0 ? dl.bytes : 0);
+      CK(launch_rounds(a, grid, 0, ctx->comm));
+      prof_end(p, ctx->comm, k);
+      ++*nlaunch;
+    }
+  }
+  return PARO_OK;
+}
+
+ncclComm_t pick_comm(paro_ctx* ctx, NcclCall::Comm c) {
+  return c == NcclCall::INTRA ? ctx->intra : (c == NcclCall::INTER ? ctx->inter : ctx->world);
+}
+
+paro_status_t run_nccl(PlanT* p, const std::vector<NcclCall>& calls) {
+  paro_ctx* ctx = p->ctx;
+  for (const NcclCall& c : calls) {
+    void* send = data_ptr(p, c.send.rank, c.send.kind, c.send.off);
+    void* recv = data_ptr(p, c.recv.rank, c.recv.kind, c.recv.off);
+    ncclComm_t cm = pick_comm(ctx, c.comm);
+    if (c.kind == NcclCall::RS) NK(ncclReduceScatter(send, recv, c.count, ncclBfloat16, ncclAvg, cm, ctx->comm));
+    else if (c.kind == NcclCall::AG) NK(ncclAllGather(send, recv, c.count, ncclBfloat16, cm, ctx->comm));
+    else NK(ncclAllReduce(send, recv, c.count, ncclBfloat16, ncclAvg, cm, ctx->comm));
+  }
+  return PARO_OK;
+}
+
+void destroy_plan(PlanT* p) {
+  if (!p) return;
+  paro_ctx* ctx = p->ctx;
+  if (ctx && ctx->mode != MODE_PLANNER) {
+    cudaSetDevice(ctx->device);
+    if (p->stepped && p->last_stream) cudaStreamSynchronize(p->last_stream);
+    if (ctx->mode == MODE_REAL) {
+      for (int x = 0; x < (int)p->peer_base.size(); ++x)
+        if (x != ctx->rank && p->peer_base[x]) cudaIpcCloseMemHandle(p->peer_base[x]);
+    }
+    for (char* r : p->region) cudaFree(r);
+    cudaFree(p->d_peer_slot);
+    cudaFree(p->d_rounds);
+    cudaFree(p->d_tasks);
+    cudaFree(p->d_partials);
+    cudaFree(p->d_norm);
+    cudaFree(p->d_nonfinite);
+    cudaFree(p->d_pack);
+    if (p->h_pack) cudaFreeHost(p->h_pack);
+    for (cudaEvent_t e : {p->ev_fork, p->ev_comm, p->ev_comp, p->ev_pack_staged, p->ev_unpack_staged})
+      if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : p->prof_ev) cudaEventDestroy(e);
+    for (cudaEvent_t e : p->ev_red) cudaEventDestroy(e);
+    for (cudaEvent_t e : p->ev_adam) cudaEventDestroy(e);
+  }
+  delete p;
+}
+
+paro_status_t make_streams(paro_ctx* ctx) {
+  CK(cudaSetDevice(ctx->device));
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, ctx->device));
+  ctx->sm_count = prop.multiProcessorCount;
+  int lo = 0, hi = 0;
+  CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  CK(cudaStreamCreateWithFlags(&ctx->main, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithPriority(&ctx->comm, cudaStreamNonBlocking, hi));  // collectives first
+  CK(cudaStreamCreateWithFlags(&ctx->comp, cudaStreamNonBlocking));
+  return PARO_OK;
+}
+
+}  // namespace
+
+// ====================================================================== C ABI
+extern "C" {
+
+const char* paro_last_error(void) { return g_last_error.c_str(); }
+
+const char* paro_version(void) { return "paro-b200 0.1.0 sm_100a"; }
+
+void paro_opts_default(paro_opts_t* o) {
+  if (!o) return;
+  std::memset(o, 0, sizeof(*o));
+  o->bucket_elems = int64_t(1) << 26;
+  o->topology = PARO_TOPO_HO_RING;
+  o->beta1 = 0.9f;
+  o->beta2 = 0.95f;
+  o->eps = 1e-8f;
+  o->weight_decay = 0.0f;
+  o->loss_scale = 1.0f;
+  o->comm_ctas = 64;
+  o->pipeline_depth = 2;
+  o->stream = nullptr;
+}
+
+paro_status_t paro_get_unique_id(paro_uid_t* out) {
+  if (!out) return fail(PARO_ERR_INVALID, "null uid");
+  static_assert(sizeof(ncclUniqueId) <= sizeof(paro_uid_t), "uid size");
+  ncclUniqueId id;
+  ncclResult_t r = ncclGetUniqueId(&id);
+  if (r != ncclSuccess) return fail(PARO_ERR_NCCL, std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+  std::memset(out, 0, sizeof(*out));
+  std::memcpy(out->bytes, &id, sizeof(id));
+  return PARO_OK;
+}
+
+paro_status_t paro_init_planner(int world_size, int group_size, paro_ctx_t* out) {
+  if (!out) return fail(PARO_ERR_INVALID, "null out");
+  std::string e = validate_cluster(world_size, group_size);
+  if (!e.empty()) return fail(PARO_ERR_INVALID, e);
+  auto* c = new paro_ctx();
+  c->mode = MODE_PLANNER;
+  c->N = world_size;
+  c->M = group_size;
+  *out = c;
+  return PARO_OK;
+}
+
+paro_status_t paro_init_emulated(int world_size, int group_size, int device, paro_ctx_t* out) {
+  if (!out) return fail(PARO_ERR_INVALID, "null out");
+  std::string e = validate_cluster(world_size, group_size);
+  if (!e.empty()) return fail(PARO_ERR_INVALID, e);
+  if (world_size > kMaxAdamSegs) return fail(PARO_ERR_INVALID, "emulated mode supports world_size <= 16");
+  auto* c = new paro_ctx();
+  c->mode = MODE_EMU;
+  c->N = world_size;
+  c->M = group_size;
+  c->device = device;
+  paro_status_t st = make_streams(c);
+  if (st != PARO_OK) {
+    delete c;
+    return st;
+  }
+  *out = c;
+  return PARO_OK;
+}
+
+paro_status_t paro_init(int world_size, int group_size, int rank, const paro_uid_t* uid, int device,
+                        paro_ctx_t* out) {
+  if (!out || !uid) return fail(PARO_ERR_INVALID, "null argument");
+  std::string e = validate_cluster(world_size, group_size);
+  if (!e.empty()) return fail(PARO_ERR_INVALID, e);
+  if (rank < 0 || rank >= world_size) return fail(PARO_ERR_INVALID, "rank out of range");
+  auto* c = new paro_ctx();
+  c->mode = MODE_REAL;
+  c->N = world_size;
+  c->M = group_size;
+  c->rank = rank;
+  c->device = device;
+  paro_status_t st = make_streams(c);
+  if (st != PARO_OK) {
+    delete c;
+    return st;
+  }
+  if (world_size > 1) {
+    ncclUniqueId id;
+    std::memcpy(&id, uid->bytes, sizeof(id));
+    paro_ctx* ctx = c;
+    ncclResult_t r = ncclCommInitRank(&c->world, world_size, id, rank);
+    if (r != ncclSuccess) {
+      delete c;
+      return fail(PARO_ERR_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+    }
+    const int j = rank / group_size, p = rank % group_size;
+    NK(ncclCommSplit(c->world, j, p, &c->intra, nullptr));
+    NK(ncclCommSplit(c->world, p, j, &c->inter, nullptr));
+  }
+  *out = c;
+  return PARO_OK;
+}
+
+paro_status_t paro_finalize(paro_ctx_t ctx) {
+  if (!ctx) return PARO_OK;
+  if (ctx->mode != MODE_PLANNER) {
+    cudaSetDevice(ctx->device);
+    cudaDeviceSynchronize();
+    if (ctx->intra) ncclCommDestroy(ctx->intra);
+    if (ctx->inter) ncclCommDestroy(ctx->inter);
+    if (ctx->world) ncclCommDestroy(ctx->world);
+    for (cudaStream_t s : {ctx->main, ctx->comm, ctx->comp})
+      if (s) cudaStreamDestroy(s);
+  }
+  delete ctx;
+  return PARO_OK;
+}
+
+paro_status_t paro_plan(paro_ctx_t ctx, const char* strategy, const int64_t* param_sizes, int n_params,
+                        const paro_opts_t* opts, paro_plan_t* out) {
+  paro_status_t st = check_ctx(ctx);
+  if (st != PARO_OK) return st;
+  if (!strategy || !out || (n_params > 0 && !param_sizes) || n_params < 0)
+    return fail(PARO_ERR_INVALID, "null argument");
+  paro_opts_t o;
+  if (opts) o = *opts;
+  else paro_opts_default(&o);
+  if (o.topology == PARO_TOPO_NCCL && ctx->mode == MODE_EMU)
+    return fail(PARO_ERR_INVALID, "NCCL topology needs real ranks");
+  if (o.comm_ctas <= 0) o.comm_ctas = 64;
+  std::vector<int64_t> sizes(param_sizes, param_sizes + n_params);
+  PlanOptions po;
+  po.bucket_elems = o.bucket_elems > 0 ? o.bucket_elems : (int64_t(1) << 26);
+  po.topology = o.topology;
+  po.pipeline_depth = o.pipeline_depth > 0 ? o.pipeline_depth : 2;
+  auto* p = new PlanT();
+  p->ctx = ctx;
+  p->opts = o;
+  try {
+    p->pl.reset(new Planner(ctx->N, ctx->M, strategy, sizes, po));
+  } catch (const std::exception& ex) {
+    delete p;
+    return fail(PARO_ERR_INVALID, ex.what());
+  }
+  if (ctx->mode == MODE_PLANNER) {
+    *out = p;
+    return PARO_OK;
+  }
+  const Planner& pl = *p->pl;
+  const int N = pl.N;
+  const size_t region_bytes = kHeaderBytes + 2 * (size_t)pl.region_elems;
+  auto bail = [&](paro_status_t s) {
+    destroy_plan(p);
+    return s;
+  };
+#define PCK(call)                                                  \
+  do {                                                             \
+    cudaError_t e_ = (call);                                       \
+    if (e_ != cudaSuccess) return bail(cuda_fail(ctx, #call, e_)); \
+  } while (0)
+  if (ctx->mode == MODE_REAL) p->local = {ctx->rank};
+  else
+    for (int r = 0; r < N; ++r) p->local.push_back(r);
+  p->peer_base.assign(N, nullptr);
+  for (int r : p->local) {
+    char* base = nullptr;
+    PCK(cudaMalloc(&base, region_bytes));
+    PCK(cudaMemset(base, 0, region_bytes));
+    p->region.push_back(base);
+    p->peer_base[r] = base;
+  }
+  if (ctx->mode == MODE_REAL && N > 1) {
+    // exchange IPC handles of the symmetric regions over the world communicator
+    cudaIpcMemHandle_t h;
+    PCK(cudaIpcGetMemHandle(&h, p->region[0]));
+    char* d_h = nullptr;
+    PCK(cudaMalloc(&d_h, sizeof(h) * (N + 1)));
+    PCK(cudaMemcpy(d_h + sizeof(h) * N, &h, sizeof(h), cudaMemcpyHostToDevice));
+    ncclResult_t r = ncclAllGather(d_h + sizeof(h) * N, d_h, sizeof(h), ncclChar, ctx->world, ctx->main);
+    if (r != ncclSuccess) {
+      cudaFree(d_h);
+      return bail(nccl_fail(ctx, "ncclAllGather(ipc handles)", r));
+    }
+    PCK(cudaStreamSynchronize(ctx->main));
+    std::vector<cudaIpcMemHandle_t> hs(N);
+    PCK(cudaMemcpy(hs.data(), d_h, sizeof(h) * N, cudaMemcpyDeviceToHost));
+    cudaFree(d_h);
+    for (int x = 0; x < N; ++x) {
+      if (x == ctx->rank) continue;
+      void* ptr = nullptr;
+      PCK(cudaIpcOpenMemHandle(&ptr, hs[x], cudaIpcMemLazyEnablePeerAccess));
+      p->peer_base[x] = static_cast<char*>(ptr);
+    }
+    std::vector<uint64_t*> slots(64, nullptr);
+    for (int x = 0; x < N; ++x) slots[x] = reinterpret_cast<uint64_t*>(p->peer_base[x]) + ctx->rank;
+    PCK(cudaMalloc(&p->d_peer_slot, 64 * sizeof(uint64_t*)));
+    PCK(cudaMemcpy(p->d_peer_slot, slots.data(), 64 * sizeof(uint64_t*), cudaMemcpyHostToDevice));
+  }
+  {
+    paro_status_t s2 = upload_schedule(p);
+    if (s2 != PARO_OK) return bail(s2);
+  }
+  const int nb = (int)pl.buckets.size();
+  p->partials_cap = adam_grid() * (pl.N == 1 ? 1 : nb);
+  PCK(cudaMalloc(&p->d_partials, sizeof(double) * p->partials_cap));
+  PCK(cudaMalloc(&p->d_norm, sizeof(double)));
+  PCK(cudaMemset(p->d_norm, 0, sizeof(double)));
+  PCK(cudaMalloc(&p->d_nonfinite, sizeof(int)));
+  PCK(cudaMemset(p->d_nonfinite, 0, sizeof(int)));
+  p->pack_cap = std::max(1, n_params) * (int)p->local.size();
+  PCK(cudaMalloc(&p->d_pack, 2 * sizeof(PackEntry) * p->pack_cap));   // [pack | unpack]
+  PCK(cudaHostAlloc(&p->h_pack, 2 * sizeof(PackEntry) * p->pack_cap, cudaHostAllocDefault));
+  for (cudaEvent_t* e : {&p->ev_fork, &p->ev_comm, &p->ev_comp, &p->ev_pack_staged, &p->ev_unpack_staged})
+    PCK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+  p->ev_red.resize(nb);
+  p->ev_adam.resize(nb);
+  for (int b = 0; b < nb; ++b) {
+    PCK(cudaEventCreateWithFlags(&p->ev_red[b], cudaEventDisableTiming));
+    PCK(cudaEventCreateWithFlags(&p->ev_adam[b], cudaEventDisableTiming));
+  }
+  PCK(cudaDeviceSynchronize());
+#undef PCK
+  *out = p;
+  return PARO_OK;
+}
+
+paro_status_t paro_plan_info(paro_plan_t p, paro_plan_info_t* out) {
+  if (!p || !out) return fail(PARO_ERR_INVALID, "null argument");
+  const Planner& pl = *p->pl;
+  std::memset(out, 0, sizeof(*out));
+  out->psi = pl.psi;
+  out->psi_pad = pl.psi_pad;
+  out->bucket_elems = pl.B;
+  out->n_buckets = (int64_t)pl.buckets.size();
+  out->p_numel = pl.p_numel;
+  out->g_numel = pl.g_numel;
+  out->os_numel = pl.os_numel;
+  out->mem_p_bytes = pl.mem_bytes(0);
+  out->mem_g_bytes = pl.mem_bytes(1);
+  out->mem_os_bytes = pl.mem_bytes(2);
+  int64_t ws = 0;
+  for (int k = BUF_GHAT; k < BUF_NKINDS; ++k) ws += 2 * pl.buf_len[k];
+  out->workspace_bytes = ws + kHeaderBytes;
+  const int me = p->ctx->mode == MODE_REAL ? p->ctx->rank : 0;
+  out->step_send_bytes_intra = pl.send_intra[me];
+  out->step_send_bytes_inter = pl.send_inter[me];
+  out->n_rounds = pl.n_rounds;
+  out->n_comm_launches = pl.n_comm_launches;
+  return PARO_OK;
+}
+
+paro_status_t paro_shard_range(paro_plan_t p, int state, int rank, int64_t bucket, int64_t* begin,
+                               int64_t* end) {
+  if (!p || !begin || !end) return fail(PARO_ERR_INVALID, "null argument");
+  const Planner& pl = *p->pl;
+  if (state < 0 || state > 2) return fail(PARO_ERR_INVALID, "state must be 0 (P), 1 (G) or 2 (OS)");
+  if (rank < 0 || rank >= pl.N) return fail(PARO_ERR_INVALID, "rank out of range");
+  if (bucket < 0 || bucket >= (int64_t)pl.buckets.size()) return fail(PARO_ERR_INVALID, "bucket out of range");
+  const Level l = state == 0 ? pl.P : (state == 1 ? pl.G : pl.OS);
+  pl.residency(l, rank, bucket, begin, end);
+  return PARO_OK;
+}
+
+paro_status_t paro_bucket_range(paro_plan_t p, int64_t bucket, int64_t* begin, int64_t* end) {
+  if (!p || !begin || !end) return fail(PARO_ERR_INVALID, "null argument");
+  const Planner& pl = *p->pl;
+  if (bucket < 0 || bucket >= (int64_t)pl.buckets.size()) return fail(PARO_ERR_INVALID, "bucket out of range");
+  *begin = pl.buckets[bucket].first;
+  *end = *begin + pl.buckets[bucket].second;
+  return PARO_OK;
+}
+
+paro_status_t paro_rank_send_bytes(paro_plan_t p, int rank, int64_t* intra, int64_t* inter) {
+  if (!p || !intra || !inter) return fail(PARO_ERR_INVALID, "null argument");
+  if (rank < 0 || rank >= p->pl->N) return fail(PARO_ERR_INVALID, "rank out of range");
+  *intra = p->pl->send_intra[rank];
+  *inter = p->pl->send_inter[rank];
+  return PARO_OK;
+}
+
+paro_status_t paro_buffer(paro_plan_t p, int rank, int kind, void** ptr) {
+  if (!p || !ptr) return fail(PARO_ERR_INVALID, "null argument");
+  paro_ctx* ctx = p->ctx;
+  if (ctx->mode == MODE_PLANNER) return fail(PARO_ERR_STATE, "planning-only context has no buffers");
+  if (!is_local(p, rank)) return fail(PARO_ERR_INVALID, "rank is not local to this process");
+  const Planner& pl = *p->pl;
+  if (kind == 0) *ptr = data_ptr(p, rank, BUF_GRAD, 0);
+  else if (kind == 1) *ptr = data_ptr(p, rank, BUF_PARAM, 0);
+  else if (kind == 2) *ptr = (pl.G == LV_N) ? nullptr : data_ptr(p, rank, BUF_GSHARD, 0);
+  else return fail(PARO_ERR_INVALID, "kind must be 0, 1 or 2");
+  return PARO_OK;
+}
+
+static paro_status_t opt_init_impl(paro_plan_t p, int rank, const float* src, uint64_t key,
+                                   const paro_opt_state_t* st) {
+  paro_ctx* ctx = p->ctx;
+  paro_status_t s = check_ctx(ctx);
+  if (s != PARO_OK) return s;
+  if (ctx->mode == MODE_PLANNER) return fail(PARO_ERR_STATE, "planning-only context");
+  if (!st || !st->master || !st->m || !st->v) return fail(PARO_ERR_INVALID, "null opt state");
+  if (!is_local(p, rank)) return fail(PARO_ERR_INVALID, "rank is not local to this process");
+  const Planner& pl = *p->pl;
+  uint16_t* pbuf = reinterpret_cast<uint16_t*>(data_ptr(p, rank, BUF_PARAM, 0));
+  for (size_t b = 0; b < pl.buckets.size(); ++b) {
+    int64_t ob, oe, pb, pe;
+    pl.residency(pl.OS, rank, b, &ob, &oe);
+    pl.residency(pl.P, rank, b, &pb, &pe);
+    const int64_t os_off = pl.buckets[b].first / pl.divl(pl.OS);
+    const int64_t p_off = pl.buckets[b].first / pl.divl(pl.P);
+    CK(launch_init_range(src, key, ob, oe - ob, pl.psi, st->master + os_off, st->m + os_off, st->v + os_off,
+                         nullptr, ctx->main));
+    CK(launch_init_range(src, key, pb, pe - pb, pl.psi, nullptr, nullptr, nullptr, pbuf + p_off, ctx->main));
+  }
+  CK(cudaStreamSynchronize(ctx->main));
+  return PARO_OK;
+}
+
+paro_status_t paro_opt_state_init(paro_plan_t p, int rank, const float* master_full, const paro_opt_state_t* st) {
+  if (!p) return fail(PARO_ERR_INVALID, "null plan");
+  if (!master_full) return fail(PARO_ERR_INVALID, "null master vector");
+  return opt_init_impl(p, rank, master_full, 0, st);
+}
+
+paro_status_t paro_opt_state_init_synth(paro_plan_t p, int rank, uint64_t seed, const paro_opt_state_t* st) {
+  if (!p) return fail(PARO_ERR_INVALID, "null plan");
+  return opt_init_impl(p, rank, nullptr, synth_key(seed, kTagMaster, 0, 0), st);
+}
+
+paro_status_t paro_synth_grads(paro_plan_t p, int rank, uint64_t seed, int64_t step) {
+  if (!p) return fail(PARO_ERR_INVALID, "null plan");
+  paro_ctx* ctx = p->ctx;
+  paro_status_t s = check_ctx(ctx);
+  if (s != PARO_OK) return s;
+  if (ctx->mode == MODE_PLANNER) return fail(PARO_ERR_STATE, "planning-only context");
+  if (!is_local(p, rank)) return fail(PARO_ERR_INVALID, "rank is not local to this process");
+  uint16_t* g = reinterpret_cast<uint16_t*>(data_ptr(p, rank, BUF_GRAD, 0));
+  CK(launch_synth_grad(g, p->pl->psi, p->pl->psi_pad, synth_key(seed, kTagGrad, (uint64_t)rank, (uint64_t)step),
+                       ctx->main));
+  CK(cudaStreamSynchronize(ctx->main));
+  return PARO_OK;
+}
+
+paro_status_t paro_step(paro_plan_t p, const void* const* grads, void* const* params,
+                        const paro_opt_state_t* opt_state, float lr, int64_t step) {
+  if (!p) return fail(PARO_ERR_INVALID, "null plan");
+  paro_ctx* ctx = p->ctx;
+  paro_status_t s = check_ctx(ctx);
+  if (s != PARO_OK) return s;
+  if (ctx->mode == MODE_PLANNER) return fail(PARO_ERR_STATE, "planning-only context cannot step");
+  if (step < 1) return fail(PARO_ERR_INVALID, "step must be >= 1");
+  if (!opt_state) return fail(PARO_ERR_INVALID, "null opt_state");
+  const Planner& pl = *p->pl;
+  const int nl = (int)p->local.size();
+  const int np = (int)pl.param_sizes.size();
+  for (int i = 0; i < nl; ++i)
+    if (!opt_state[i].master || !opt_state[i].m || !opt_state[i].v)
+      return fail(PARO_ERR_INVALID, "null opt_state array");
+  if (grads) {
+    for (int i = 0; i < nl * np; ++i)
+      if (!grads[i] && pl.param_sizes[i % np] > 0) return fail(PARO_ERR_INVALID, "null gradient pointer");
+  }
+  cudaStream_t S = p->opts.stream ? static_cast<cudaStream_t>(p->opts.stream) : ctx->main;
+  int launches = 0;
+
+  // ---- host scalars of canonical Adam (double, rounded once: R6)
+  const double b1 = p->opts.beta1, b2 = p->opts.beta2, dlr = lr;
+  AdamArgs aa{};
+  aa.alpha = (float)(1.0 / (double)pl.N);
+  aa.b1 = (float)b1;
+  aa.omb1 = (float)(1.0 - b1);
+  aa.b2 = (float)b2;
+  aa.omb2 = (float)(1.0 - b2);
+  aa.step_size = (float)(dlr / (1.0 - std::pow(b1, (double)step)));
+  aa.bc2s = (float)std::sqrt(1.0 - std::pow(b2, (double)step));
+  aa.eps = p->opts.eps;
+  aa.has_wd = p->opts.weight_decay != 0.0f;
+  aa.decay = (float)(1.0 - dlr * (double)p->opts.weight_decay);
+  aa.s_g = (float)(1.0 / (double)p->opts.loss_scale);
+  aa.nonfinite = p->d_nonfinite;
+
+  CK(cudaEventRecord(p->ev_fork, S));
+  CK(cudaStreamWaitEvent(ctx->comm, p->ev_fork, 0));
+  CK(cudaStreamWaitEvent(ctx->comp, p->ev_fork, 0));
+
+  // ---- pack (per-parameter gradients -> flat gradient buffer)
+  if (grads) {
+    CK(cudaEventSynchronize(p->ev_pack_staged));   // staging buffer free again
+    int k = 0;
+    int64_t maxn = 0;
+    for (int li = 0; li < nl; ++li) {
+      const int r = p->local[li];
+      for (int i = 0; i < np; ++i) {
+        if (pl.param_sizes[i] == 0) continue;
+        p->h_pack[k].src = static_cast<const uint16_t*>(grads[li * np + i]);
+        p->h_pack[k].dst = reinterpret_cast<uint16_t*>(data_ptr(p, r, BUF_GRAD, pl.param_offsets[i]));
+        p->h_pack[k].n = pl.param_sizes[i];
+        maxn = std::max(maxn, pl.param_sizes[i]);
+        ++k;
+      }
+    }
+    CK(cudaMemcpyAsync(p->d_pack, p->h_pack, sizeof(PackEntry) * k, cudaMemcpyHostToDevice, ctx->comp));
+    CK(cudaEventRecord(p->ev_pack_staged, ctx->comp));
+    CK(launch_pack(p->d_pack, k, maxn, ctx->comp));
+    ++launches;
+    CK(cudaEventRecord(p->ev_comp, ctx->comp));
+    CK(cudaStreamWaitEvent(ctx->comm, p->ev_comp, 0));
+  }
+  CK(cudaMemsetAsync(p->d_nonfinite, 0, sizeof(int), ctx->comp));
+
+  const int nb = (int)pl.buckets.size();
+  const int grid = adam_grid();
+  int n_adam = 0;
+  auto adam_bucket = [&](int b0, int b1) -> paro_status_t {
+    // one Adam launch over buckets [b0, b1) and every local rank
+    aa.nseg = 0;
+    for (int li = 0; li < nl; ++li) {
+      const int r = p->local[li];
+      const int j = r / pl.M;
+      const bool uniq = (pl.OS == LV_G) || (pl.OS == LV_I && j == 0) || (pl.OS == LV_N && r == 0);
+      const BucketSchedule& S0 = pl.sched[b0];
+      int64_t len = 0;
+      for (int b = b0; b < b1; ++b) len += pl.sched[b].os_len;
+      AdamSeg& sg = aa.seg[aa.nseg++];
+      sg.ghat = reinterpret_cast<const uint16_t*>(data_ptr(p, S0.ghat[r].rank, S0.ghat[r].kind, S0.ghat[r].off));
+      sg.master = opt_state[li].master + S0.os_off[r];
+      sg.m = opt_state[li].m + S0.os_off[r];
+      sg.v = opt_state[li].v + S0.os_off[r];
+      sg.param = reinterpret_cast<uint16_t*>(data_ptr(p, S0.param[r].rank, S0.param[r].kind, S0.param[r].off));
+      sg.n8 = len / 8;
+      sg.raw = (pl.N == 1) ? 1 : 0;
+      sg.in_norm = uniq ? 1 : 0;
+    }
+    aa.partials = p->d_partials + (int64_t)n_adam * grid;
+    int64_t elems = 0;
+    for (int i = 0; i < aa.nseg; ++i) elems += 8 * aa.seg[i].n8;
+    const int pk = prof_begin(p, ctx->comp, 0, elems);
+    CK(launch_adam(aa, grid, ctx->comp));
+    prof_end(p, ctx->comp, pk);
+    ++n_adam;
+    ++launches;
+    return PARO_OK;
+  };
+
+  if (pl.N == 1) {
+    paro_status_t s2 = adam_bucket(0, nb);   // contiguous: one launch over all buckets
+    if (s2 != PARO_OK) return s2;
+  } else {
+    const int D = std::max(1, p->opts.pipeline_depth);
+    const bool nccl = pl.opt.topology == PARO_TOPO_NCCL;
+    auto do_gather = [&](int b) -> paro_status_t {
+      CK(cudaStreamWaitEvent(ctx->comm, p->ev_adam[b], 0));
+      if (nccl) {
+        const int k = prof_begin(p, ctx->comm, 1, 0);
+        paro_status_t s3 = run_nccl(p, pl.sched[b].nccl_gather[ctx->rank]);
+        prof_end(p, ctx->comm, k);
+        if (s3 != PARO_OK) return s3;
+        if (!pl.sched[b].nccl_gather[ctx->rank].empty()) ++launches;
+        return PARO_OK;
+      }
+      return run_launch(p, p->gat[b], &launches);
+    };
+    for (int b = 0; b < nb; ++b) {
+      if (pl.nslots > 0 && b >= pl.nslots) CK(cudaStreamWaitEvent(ctx->comm, p->ev_adam[b - pl.nslots], 0));
+      if (nccl) {
+        const int k = prof_begin(p, ctx->comm, 1, 0);
+        paro_status_t s3 = run_nccl(p, pl.sched[b].nccl_reduce[ctx->rank]);
+        prof_end(p, ctx->comm, k);
+        if (s3 != PARO_OK) return s3;
+        ++launches;
+      } else {
+        paro_status_t s3 = run_launch(p, p->red[b], &launches);
+        if (s3 != PARO_OK) return s3;
+      }
+      CK(cudaEventRecord(p->ev_red[b], ctx->comm));
+      CK(cudaStreamWaitEvent(ctx->comp, p->ev_red[b], 0));
+      paro_status_t s4 = adam_bucket(b, b + 1);
+      if (s4 != PARO_OK) return s4;
+      CK(cudaEventRecord(p->ev_adam[b], ctx->comp));
+      if (b >= D) {
+        paro_status_t s5 = do_gather(b - D);
+        if (s5 != PARO_OK) return s5;
+      }
+    }
+    for (int b = std::max(0, nb - D); b < nb; ++b) {
+      paro_status_t s5 = do_gather(b);
+      if (s5 != PARO_OK) return s5;
+    }
+  }
+  // ---- grad norm: ordered fp64 finalize, then scalar all-reduce (R8, R23)
+  CK(launch_norm_finalize(p->d_partials, n_adam * grid, p->d_norm, ctx->comp));
+  ++launches;
+  CK(cudaEventRecord(p->ev_comp, ctx->comp));
+  CK(cudaStreamWaitEvent(ctx->comm, p->ev_comp, 0));
+  if (ctx->mode == MODE_REAL && pl.N > 1) {
+    NK(ncclAllReduce(p->d_norm, p->d_norm, 1, ncclDouble, ncclSum, ctx->world, ctx->comm));
+    NK(ncclAllReduce(p->d_nonfinite, p->d_nonfinite, 1, ncclInt32, ncclMax, ctx->world, ctx->comm));
+    launches += 2;
+  }
+  // ---- unpack into caller parameter tensors
+  if (params) {
+    int k = 0;
+    int64_t maxn = 0;
+    CK(cudaEventSynchronize(p->ev_unpack_staged));
+    PackEntry* hu = p->h_pack + p->pack_cap;
+    PackEntry* du = p->d_pack + p->pack_cap;
+    for (int li = 0; li < nl; ++li) {
+      const int r = p->local[li];
+      if (pl.P == LV_N) {
+        for (int i = 0; i < np; ++i) {
+          if (pl.param_sizes[i] == 0) continue;
+          hu[k].src = reinterpret_cast<const uint16_t*>(data_ptr(p, r, BUF_PARAM, pl.param_offsets[i]));
+          hu[k].dst = static_cast<uint16_t*>(params[li * np + i]);
+          hu[k].n = pl.param_sizes[i];
+          maxn = std::max(maxn, pl.param_sizes[i]);
+          ++k;
+        }
+      } else {
+        hu[k].src = reinterpret_cast<const uint16_t*>(data_ptr(p, r, BUF_PARAM, 0));
+        hu[k].dst = static_cast<uint16_t*>(params[li]);
+        hu[k].n = pl.p_numel;
+        maxn = std::max(maxn, pl.p_numel);
+        ++k;
+      }
+    }
+    if (k > 0) {
+      CK(cudaMemcpyAsync(du, hu, sizeof(PackEntry) * k, cudaMemcpyHostToDevice, ctx->comm));
+      CK(cudaEventRecord(p->ev_unpack_staged, ctx->comm));
+      CK(launch_pack(du, k, maxn, ctx->comm));
+      ++launches;
+    }
+  }
+  CK(cudaEventRecord(p->ev_comm, ctx->comm));
+  CK(cudaStreamWaitEvent(S, p->ev_comm, 0));
+  p->last_stream = S;
+  p->last_launches = launches;
+  p->stepped = true;
+  if (p->prof) {
+    ++p->prof_steps;
+    p->prof_launches += launches;
+  }
+  return PARO_OK;
+}
+
+paro_status_t paro_profile_start(paro_plan_t p, int max_launches) {
+  if (!p) return fail(PARO_ERR_INVALID, "null plan");
+  paro_ctx* ctx = p->ctx;
+  paro_status_t s = check_ctx(ctx);
+  if (s != PARO_OK) return s;
+  if (ctx->mode == MODE_PLANNER) return fail(PARO_ERR_STATE, "planning-only context");
+  if (max_launches < 1) return fail(PARO_ERR_INVALID, "max_launches must be >= 1");
+  for (cudaEvent_t e : p->prof_ev) cudaEventDestroy(e);
+  p->prof_ev.assign(2 * (size_t)max_launches, nullptr);
+  for (auto& e : p->prof_ev) CK(cudaEventCreate(&e));
+  p->prof_kind.assign(max_launches, 0);
+  p->prof_amount.assign(max_launches, 0);
+  p->prof_used = 0;
+  p->prof_steps = 0;
+  p->prof_launches = 0;
+  p->prof = true;
+  return PARO_OK;
+}
+
+paro_status_t paro_profile_stop(paro_plan_t p, paro_profile_t* out) {
+  if (!p || !out) return fail(PARO_ERR_INVALID, "null argument");
+  paro_ctx* ctx = p->ctx;
+  paro_status_t s = check_ctx(ctx);
+  if (s != PARO_OK) return s;
+  std::memset(out, 0, sizeof(*out));
+  CK(cudaDeviceSynchronize());
+  for (int k = 0; k < p->prof_used; ++k) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, p->prof_ev[2 * k], p->prof_ev[2 * k + 1]));
+    if (p->prof_kind[k] == 0) {
+      out->adam_ms += ms;
+      out->adam_launches += 1;
+      out->adam_elems += p->prof_amount[k];
+    } else {
+      out->comm_ms += ms;
+      out->comm_launches += 1;
+      out->comm_bytes += p->prof_amount[k];
+    }
+  }
+  out->steps = p->prof_steps;
+  out->kernel_launches = p->prof_launches;
+  p->prof = false;
+  for (cudaEvent_t e : p->prof_ev) cudaEventDestroy(e);
+  p->prof_ev.clear();
+  p->prof_used = 0;
+  return PARO_OK;
+}
+
+paro_status_t paro_step_stats(paro_plan_t p, paro_step_stats_t* out) {
+  if (!p || !out) return fail(PARO_ERR_INVALID, "null argument");
+  paro_ctx* ctx = p->ctx;
+  paro_status_t s = check_ctx(ctx);
+  if (s != PARO_OK) return s;
+  if (ctx->mode == MODE_PLANNER) return fail(PARO_ERR_STATE, "planning-only context");
+  std::memset(out, 0, sizeof(*out));
+  if (!p->stepped) return fail(PARO_ERR_STATE, "no step has run on this plan");
+  CK(cudaStreamSynchronize(p->last_stream));
+  for (char* r : p->region) {
+    int err = 0;
+    CK(cudaMemcpy(&err, r + 520, sizeof(int), cudaMemcpyDeviceToHost));
+    if (err) {
+      ctx->sticky = PARO_ERR_TIMEOUT;
+      ctx->sticky_msg = "a cross-GPU wait timed out on the device (peer never arrived)";
+      return fail(PARO_ERR_TIMEOUT, ctx->sticky_msg);
+    }
+  }
+  double nsq = 0;
+  int nf = 0;
+  CK(cudaMemcpy(&nsq, p->d_norm, sizeof(double), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(&nf, p->d_nonfinite, sizeof(int), cudaMemcpyDeviceToHost));
+  out->grad_norm = std::sqrt(nsq);
+  out->nonfinite = nf;
+  const int me = ctx->mode == MODE_REAL ? ctx->rank : 0;
+  out->sent_intra = p->pl->send_intra[me];
+  out->sent_inter = p->pl->send_inter[me];
+  out->kernel_launches = p->last_launches;
+  return PARO_OK;
+}
+
+paro_status_t paro_plan_destroy(paro_plan_t p) {
+  destroy_plan(p);
+  return PARO_OK;
+}
+
+}  // extern "C"

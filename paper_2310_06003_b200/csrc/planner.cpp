@@ -1,0 +1,655 @@
+// planner.cpp — see planner.h.  Host only.
+//
+// Schedules are written in the pull model used by the sm_100a kernels: in a
+// round, a rank READS its ring predecessor's partial (over NVLink in real
+// mode) and writes its own result locally.  The arithmetic each element sees
+// is exactly the ring of the paper in canonical order R2:
+// the chain for block c starts at member c+1 and ends at its owner c.
+#include "planner.h"
+
+#include <algorithm>
+#include <functional>
+#include <stdexcept>
+
+namespace paro {
+
+namespace {
+
+constexpr int64_t kQuantum = 64;      // elements per shard granule (R21)
+constexpr int64_t kAlignElems = 128;  // 256-byte alignment of buffer kinds
+
+int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
+
+Ref at(Ref r, int64_t d) {
+  r.off += d;
+  return r;
+}
+
+struct Piece {
+  int64_t src_off;  // offset in the contribution's address space
+  int64_t len;
+  int64_t blk_off;  // offset inside the dense block (stage / dest space)
+};
+
+using PieceFn = std::function<std::vector<Piece>(int c)>;
+using ContribFn = std::function<Ref(int q, int c, const Piece& pc)>;
+using BaseFn = std::function<Ref(int q, int slot)>;
+
+struct FinalIn {   // inputs of a ring RS's final hop at member q, per piece
+  std::vector<Piece> pieces;
+  std::vector<Ref> pin;   // partial from the predecessor (rank == -1: none, k == 1)
+  std::vector<Ref> own;   // own contribution
+};
+
+Task make_task(int64_t n, std::initializer_list<Ref> ins, Ref dst) {
+  Task t;
+  t.n = n;
+  t.nin = 0;
+  for (const Ref& r : ins) {
+    if (r.rank < 0) continue;
+    t.in[t.nin++] = r;
+  }
+  t.dst = dst;
+  return t;
+}
+
+// Ring reduce-scatter body over `ranks` (k members): emits the non-final hops
+// 0..k-3 at rounds round0 + h and returns each member's final-hop inputs.
+std::vector<FinalIn> ring_rs_body(Launch& L, const std::vector<int>& ranks, const PieceFn& pieces,
+                                  const ContribFn& contrib, const BaseFn& stage, int round0) {
+  const int k = (int)ranks.size();
+  for (int t = 0; t + 2 < k; ++t) {
+    for (int q = 0; q < k; ++q) {
+      const int c = ((q - t - 2) % k + k) % k;
+      const int pred = (q - 1 + k) % k;
+      for (const Piece& pc : pieces(c)) {
+        Ref in0 = (t == 0) ? contrib(pred, c, pc) : at(stage(pred, (t - 1) % 2), pc.blk_off);
+        Ref in1 = contrib(q, c, pc);
+        L.add(round0 + t, ranks[q], make_task(pc.len, {in0, in1}, at(stage(q, t % 2), pc.blk_off)));
+      }
+    }
+  }
+  std::vector<FinalIn> fin(k);
+  for (int q = 0; q < k; ++q) {
+    const int pred = (q - 1 + k) % k;
+    fin[q].pieces = pieces(q);
+    for (const Piece& pc : fin[q].pieces) {
+      Ref pin;
+      if (k == 2) pin = contrib(pred, q, pc);
+      else if (k > 2) pin = at(stage(pred, (k - 3) % 2), pc.blk_off);
+      fin[q].pin.push_back(pin);
+      fin[q].own.push_back(contrib(q, q, pc));
+    }
+  }
+  return fin;
+}
+
+// Plain ring RS: body + final hop at round0 + k - 2 into dest(q) (block space).
+void ring_rs(Launch& L, const std::vector<int>& ranks, const PieceFn& pieces, const ContribFn& contrib,
+             const BaseFn& stage, const std::function<Ref(int q)>& dest, int round0) {
+  const int k = (int)ranks.size();
+  auto fin = ring_rs_body(L, ranks, pieces, contrib, stage, round0);
+  const int rf = round0 + std::max(0, k - 2);
+  for (int q = 0; q < k; ++q) {
+    for (size_t i = 0; i < fin[q].pieces.size(); ++i) {
+      const Piece& pc = fin[q].pieces[i];
+      Ref d = at(dest(q), pc.blk_off);
+      const Ref& own = fin[q].own[i];
+      if (k == 1 && own.rank == d.rank && own.kind == d.kind && own.off == d.off) continue;
+      L.add(rf, ranks[q], make_task(pc.len, {fin[q].pin[i], own}, d));
+    }
+  }
+}
+
+// Ring all-gather in place: member q owns block q in base(q); round t copies
+// block (q-1-t) from the predecessor (P:358 ring order, pull form).
+void ring_ag(Launch& L, const std::vector<int>& ranks, const PieceFn& pieces,
+             const std::function<Ref(int q)>& base, int round0) {
+  const int k = (int)ranks.size();
+  for (int t = 0; t + 1 < k; ++t) {
+    for (int q = 0; q < k; ++q) {
+      const int c = ((q - 1 - t) % k + k) % k;
+      const int pred = (q - 1 + k) % k;
+      for (const Piece& pc : pieces(c))
+        L.add(round0 + t, ranks[q], make_task(pc.len, {at(base(pred), pc.src_off)}, at(base(q), pc.src_off)));
+    }
+  }
+}
+
+}  // namespace
+
+// ----------------------------------------------------------------- Launch
+void Launch::add(int round, int rank, const Task& t) {
+  if ((int)rounds.size() <= round) rounds.resize(round + 1, std::vector<std::vector<Task>>(n_ranks));
+  rounds[round][rank].push_back(t);
+}
+
+std::vector<int> Launch::reads(int r, int rank) const {
+  std::vector<int> out;
+  if (r < 0 || r >= (int)rounds.size()) return out;
+  for (const Task& t : rounds[r][rank])
+    for (int i = 0; i < t.nin; ++i)
+      if (t.in[i].rank != rank && std::find(out.begin(), out.end(), t.in[i].rank) == out.end())
+        out.push_back(t.in[i].rank);
+  return out;
+}
+
+uint64_t Launch::barrier_peers(int r, int rank) const {
+  uint64_t m = 0;
+  for (int rr = r - 1; rr <= r; ++rr) {
+    if (rr < 0 || rr >= (int)rounds.size()) continue;
+    for (int x : reads(rr, rank)) m |= uint64_t(1) << x;
+    for (int x = 0; x < n_ranks; ++x) {
+      if (x == rank) continue;
+      auto rx = reads(rr, x);
+      if (std::find(rx.begin(), rx.end(), rank) != rx.end()) m |= uint64_t(1) << x;
+    }
+  }
+  return m;
+}
+
+// ----------------------------------------------------------------- validation
+Level parse_level(char c) {
+  if (c == 'N') return LV_N;
+  if (c == 'I') return LV_I;
+  if (c == 'G') return LV_G;
+  throw std::invalid_argument("bad level");
+}
+
+std::string validate_strategy(const std::string& code) {
+  if (code.size() != 3) return "strategy code must have 3 characters";
+  for (int i = 0; i < 3; ++i) {
+    char c = code[i];
+    if (c != 'N' && c != 'I' && c != 'G')
+      return std::string("invalid shard level '") + c + "' at position " + std::to_string(i + 1);
+  }
+  // Principle 1: OS at least as finely sharded as P and G.
+  Level p = parse_level(code[0]), g = parse_level(code[1]), o = parse_level(code[2]);
+  if (o < p || o < g)
+    return "strategy '" + code + "' violates Principle 1 (S_P>=S_OS and S_G>=S_OS)";
+  return "";
+}
+
+std::string validate_cluster(int N, int M) {
+  if (N < 1 || M < 1) return "n_gpus and group_size must be >= 1";
+  if (N > 64) return "n_gpus must be <= 64";
+  if (N % M != 0) return "group_size must divide n_gpus";
+  return "";
+}
+
+// ----------------------------------------------------------------- Planner
+Planner::Planner(int N_, int M_, const std::string& code_, const std::vector<int64_t>& sizes,
+                 const PlanOptions& opt_)
+    : N(N_), M(M_), g(0), code(code_), opt(opt_), param_sizes(sizes) {
+  std::string e = validate_cluster(N, M);
+  if (!e.empty()) throw std::invalid_argument(e);
+  e = validate_strategy(code);
+  if (!e.empty()) throw std::invalid_argument(e);
+  g = N / M;
+  P = parse_level(code[0]);
+  G = parse_level(code[1]);
+  OS = parse_level(code[2]);
+  for (int64_t s : sizes)
+    if (s < 0) throw std::invalid_argument("param sizes must be >= 0");
+  if (opt.topology < 0 || opt.topology > 4) throw std::invalid_argument("unknown topology");
+  if (opt.topology == 3 && (M > kMaxIn || g > kMaxIn))
+    throw std::invalid_argument("direct topology needs group_size and n_groups <= 16");
+  if (opt.pipeline_depth < 1) opt.pipeline_depth = 1;
+  layout();
+  build_schedule();
+  count_bytes();
+}
+
+void Planner::residency(Level l, int r, int64_t b, int64_t* begin, int64_t* end) const {
+  const int64_t s = buckets[b].first, n = buckets[b].second;
+  const int j = grp(r), p = pos(r);
+  if (l == LV_N) {
+    *begin = s;
+    *end = s + n;
+  } else if (l == LV_I) {
+    const int64_t c = n / M;
+    *begin = s + p * c;
+    *end = *begin + c;
+  } else {
+    const int64_t c = n / N;
+    *begin = s + int64_t(seg(j, p)) * c;
+    *end = *begin + c;
+  }
+}
+
+int64_t Planner::mem_bytes(int state) const {
+  if (state == 0) return 2 * p_numel;
+  if (state == 1) return 2 * (G == LV_N ? psi_pad : g_numel);
+  return 12 * os_numel;
+}
+
+void Planner::layout() {
+  const int64_t unit = int64_t(N) * kQuantum;
+  psi = 0;
+  param_offsets.clear();
+  for (int64_t s : param_sizes) {
+    param_offsets.push_back(psi);
+    psi += s;
+  }
+  psi_pad = ceil_div(psi, unit) * unit;
+  B = std::max(unit, (opt.bucket_elems / unit) * unit);
+  buckets.clear();
+  for (int64_t s = 0; s < psi_pad; s += B) buckets.push_back({s, std::min(B, psi_pad - s)});
+  p_numel = psi_pad / divl(P);
+  g_numel = (G == LV_N) ? 0 : psi_pad / divl(G);
+  os_numel = psi_pad / divl(OS);
+  if (G != OS && N > 1) {
+    nslots = opt.pipeline_depth + 1;
+    ghat_slot = B / divl(OS);
+  }
+  const int64_t C = B / N;
+  stage_i_len = B / M;       // largest intra block: a whole chunk (RS_I)
+  stage_e_len = C;
+  p1_len = B / M;
+  sown_len = C;
+  buf_len[BUF_GRAD] = psi_pad;
+  buf_len[BUF_PARAM] = p_numel;
+  buf_len[BUF_GSHARD] = g_numel;
+  buf_len[BUF_GHAT] = int64_t(nslots) * ghat_slot;
+  buf_len[BUF_STAGE_I] = (N > 1) ? 4 * stage_i_len : 0;
+  buf_len[BUF_STAGE_E] = (N > 1) ? 4 * stage_e_len : 0;
+  buf_len[BUF_P1] = (N > 1) ? 2 * p1_len : 0;
+  buf_len[BUF_SOWN] = (N > 1) ? 2 * sown_len : 0;
+  int64_t off = 0;
+  for (int k = 0; k < BUF_NKINDS; ++k) {
+    buf_off[k] = off;
+    off += round_up(buf_len[k], kAlignElems);
+  }
+  region_elems = off;
+}
+
+void Planner::build_schedule() {
+  sched.assign(buckets.size(), BucketSchedule());
+  const int topo = opt.topology;
+  // primitive names (reporting; mirrors oracle.accounting.step_ops)
+  grad_ops.clear();
+  rest_ops.clear();
+  if (G == LV_I) {
+    grad_ops = {"RS_I", OS == LV_G ? "RS_E" : "AR_E"};
+  } else {
+    grad_ops = {"HO_RS"};
+    if (OS == LV_I) grad_ops.push_back("AG_E");
+    if (OS == LV_N) grad_ops.push_back("HO_AG");
+  }
+  if (OS != P) rest_ops = {OS == LV_G ? (P == LV_I ? "AG_E" : "HO_AG") : "AG_I"};
+
+  for (size_t b = 0; b < buckets.size(); ++b) {
+    BucketSchedule& S = sched[b];
+    const int64_t s = buckets[b].first, n = buckets[b].second;
+    const int64_t C = n / N, chunk = n / M;
+    const int par = int(b % 2);
+    S.reduce.n_ranks = S.gather.n_ranks = N;
+    S.nccl_reduce.assign(N, {});
+    S.nccl_gather.assign(N, {});
+
+    auto grad = [&](int r, int64_t o) { return Ref{r, BUF_GRAD, s + o}; };
+    auto gshard = [&](int r, int64_t o) { return Ref{r, BUF_GSHARD, s / divl(G) + o}; };
+    auto ghat_base = [&](int r) {
+      if (G == OS) return Ref{r, BUF_GSHARD, s / divl(G)};
+      return Ref{r, BUF_GHAT, int64_t(b % nslots) * ghat_slot};
+    };
+    auto param_base = [&](int r) { return Ref{r, BUF_PARAM, s / divl(P)}; };
+    auto stage_i = [&](int r, int slot) { return Ref{r, BUF_STAGE_I, int64_t(par * 2 + slot) * stage_i_len}; };
+    auto stage_e = [&](int r, int slot) { return Ref{r, BUF_STAGE_E, int64_t(par * 2 + slot) * stage_e_len}; };
+    auto p1 = [&](int r) { return Ref{r, BUF_P1, int64_t(par) * p1_len}; };
+    auto sown = [&](int r) { return Ref{r, BUF_SOWN, int64_t(par) * sown_len}; };
+    // where the reduced segment of rank r lands (OS-residency layout of g_hat)
+    auto dest_seg = [&](int r) {
+      const int j = grp(r), p = pos(r);
+      if (OS == LV_G) return ghat_base(r);
+      if (OS == LV_I) return at(ghat_base(r), int64_t(j) * C);
+      return at(ghat_base(r), int64_t(seg(j, p)) * C);
+    };
+    auto group_ranks = [&](int j) {
+      std::vector<int> v;
+      for (int p = 0; p < M; ++p) v.push_back(rank_of(j, p));
+      return v;
+    };
+    auto pos_ranks = [&](int p) {
+      std::vector<int> v;
+      for (int j = 0; j < g; ++j) v.push_back(rank_of(j, p));
+      return v;
+    };
+    auto one = [](int64_t off, int64_t len) { return std::vector<Piece>{{off, len, 0}}; };
+
+    // ---- world-reaching RS producing g_hat segments at dest_seg (G in {N, G})
+    auto emit_world_rs = [&](Launch& L) -> int {   // returns rounds used
+      if (topo == 0) {  // HO-Ring RS (R16/R17)
+        const int R1 = (g > 1 && M > 1) ? M - 1 : 0;
+        const int R2 = std::max(M - 1, g - 1);
+        if (R1 > 0) {
+          for (int j = 0; j < g; ++j) {
+            auto pieces = [&, j](int c) {
+              std::vector<Piece> v;
+              const int64_t base = int64_t(c) * g * C;
+              if (j > 0) v.push_back({base, int64_t(j) * C, 0});
+              if (j < g - 1) v.push_back({base + int64_t(j + 1) * C, int64_t(g - 1 - j) * C, int64_t(j) * C});
+              return v;
+            };
+            auto gr = group_ranks(j);
+            ring_rs(L, gr, pieces, [&, gr](int q, int, const Piece& pc) { return grad(gr[q], pc.src_off); },
+                    [&, gr](int q, int slot) { return stage_i(gr[q], slot); },
+                    [&, gr](int q) { return p1(gr[q]); }, 0);
+          }
+        }
+        // phase 2: inter ring (i) concurrent with intra own-segment ring (ii)
+        std::vector<FinalIn> intra_fin(N), inter_fin(N);
+        if (M > 1) {
+          for (int j = 0; j < g; ++j) {
+            auto gr = group_ranks(j);
+            auto fin = ring_rs_body(L, gr, [&, j](int c) { return one(int64_t(seg(j, c)) * C, C); },
+                                    [&, gr](int q, int, const Piece& pc) { return grad(gr[q], pc.src_off); },
+                                    [&, gr](int q, int slot) { return stage_i(gr[q], slot); }, R1);
+            for (int q = 0; q < M; ++q) intra_fin[gr[q]] = fin[q];
+          }
+        }
+        if (g > 1) {
+          for (int p = 0; p < M; ++p) {
+            auto pr = pos_ranks(p);
+            auto contrib = [&, pr, p](int q, int c, const Piece&) {
+              if (M > 1) return at(p1(pr[q]), int64_t(c < q ? c : c - 1) * C);
+              return grad(pr[q], int64_t(seg(c, p)) * C);
+            };
+            // non-final inter hops at rounds R1 + h (h <= g-3); the final hop is emitted below
+            auto fin = ring_rs_body(L, pr, [&](int) { return one(0, C); }, contrib,
+                                    [&, pr](int q, int slot) { return stage_e(pr[q], slot); }, R1);
+            for (int q = 0; q < g; ++q) inter_fin[pr[q]] = fin[q];
+          }
+        }
+        const int rlast = R1 + R2 - 1;
+        for (int r = 0; r < N; ++r) {
+          Ref d = dest_seg(r);
+          if (g == 1) {
+            L.add(rlast, r, make_task(C, {intra_fin[r].pin[0], intra_fin[r].own[0]}, d));
+          } else if (M == 1) {
+            L.add(rlast, r, make_task(C, {inter_fin[r].pin[0], grad(r, int64_t(seg(grp(r), 0)) * C)}, d));
+          } else if (M - 1 == R2) {   // fused: ((intra_in (+) x_own) (+) inter_in)
+            L.add(rlast, r, make_task(C, {intra_fin[r].pin[0], intra_fin[r].own[0], inter_fin[r].pin[0]}, d));
+          } else {                    // intra ring finished earlier: stash S, combine last
+            L.add(R1 + M - 2, r, make_task(C, {intra_fin[r].pin[0], intra_fin[r].own[0]}, sown(r)));
+            L.add(rlast, r, make_task(C, {inter_fin[r].pin[0], sown(r)}, d));
+          }
+        }
+        return R1 + R2;
+      }
+      if (topo == 1) {  // two-step: RS_I into P1, then RS_E
+        for (int j = 0; j < g; ++j) {
+          auto gr = group_ranks(j);
+          ring_rs(L, gr, [&](int c) { return one(int64_t(c) * chunk, chunk); },
+                  [&, gr](int q, int, const Piece& pc) { return grad(gr[q], pc.src_off); },
+                  [&, gr](int q, int slot) { return stage_i(gr[q], slot); },
+                  [&, gr](int q) { return p1(gr[q]); }, 0);
+        }
+        const int r0 = std::max(1, M - 1);
+        for (int p = 0; p < M; ++p) {
+          auto pr = pos_ranks(p);
+          ring_rs(L, pr, [&](int c) { return one(int64_t(c) * C, C); },
+                  [&, pr](int q, int, const Piece& pc) { return at(p1(pr[q]), pc.src_off); },
+                  [&, pr](int q, int slot) { return stage_e(pr[q], slot); },
+                  [&, pr](int q) { return dest_seg(pr[q]); }, r0);
+        }
+        return r0 + std::max(1, g - 1);
+      }
+      if (topo == 2) {  // flat ring over all ranks
+        std::vector<int> all;
+        for (int r = 0; r < N; ++r) all.push_back(r);
+        ring_rs(L, all, [&](int c) { return one(int64_t(seg(grp(c), pos(c))) * C, C); },
+                [&](int q, int, const Piece& pc) { return grad(q, pc.src_off); },
+                [&](int q, int slot) { return stage_i(q, slot); }, [&](int q) { return dest_seg(q); }, 0);
+        return N - 1;
+      }
+      // topo == 3: direct hierarchical one-shot (NVSwitch): same canonical order
+      int rr = 0;
+      if (M > 1) {
+        for (int r = 0; r < N; ++r) {
+          const int j = grp(r), p = pos(r);
+          Task t;
+          t.n = (g == 1) ? C : chunk;
+          t.nin = M;
+          for (int i = 0; i < M; ++i) {   // R_M(p; ...): p+1, p+2, ..., p
+            const int pp = (p + 1 + i) % M;
+            t.in[i] = grad(rank_of(j, pp), int64_t(p) * chunk);
+          }
+          t.dst = (g == 1) ? dest_seg(r) : p1(r);
+          L.add(0, r, t);
+        }
+        rr = 1;
+      }
+      if (g > 1) {
+        for (int r = 0; r < N; ++r) {
+          const int j = grp(r), p = pos(r);
+          Task t;
+          t.n = C;
+          t.nin = g;
+          for (int i = 0; i < g; ++i) {   // R_g(j; ...): j+1, ..., j
+            const int jj = (j + 1 + i) % g;
+            t.in[i] = (M > 1) ? at(p1(rank_of(jj, p)), int64_t(j) * C)
+                              : grad(rank_of(jj, p), int64_t(seg(j, p)) * C);
+          }
+          t.dst = dest_seg(r);
+          L.add(rr, r, t);
+        }
+        rr += 1;
+      }
+      return rr;
+    };
+
+    // ---- world-reaching AG of segments in place in a bucket-layout buffer
+    auto emit_world_ag = [&](Launch& L, const std::function<Ref(int)>& base, int round0) {
+      if (topo == 0) {  // HO-Ring AG
+        for (int j = 0; j < g; ++j) {
+          auto gr = group_ranks(j);
+          ring_ag(L, gr, [&, j](int c) { return one(int64_t(seg(j, c)) * C, C); },
+                  [&, gr](int q) { return base(gr[q]); }, round0);
+        }
+        for (int p = 0; p < M; ++p) {
+          auto pr = pos_ranks(p);
+          ring_ag(L, pr, [&, p](int c) { return one(int64_t(seg(c, p)) * C, C); },
+                  [&, pr](int q) { return base(pr[q]); }, round0);
+        }
+        if (g > 1 && M > 1) {
+          const int rb = round0 + std::max(M - 1, g - 1);
+          for (int j = 0; j < g; ++j) {
+            auto gr = group_ranks(j);
+            auto pieces = [&, j](int c) {
+              std::vector<Piece> v;
+              const int64_t cb = int64_t(c) * g * C;
+              if (j > 0) v.push_back({cb, int64_t(j) * C, 0});
+              if (j < g - 1) v.push_back({cb + int64_t(j + 1) * C, int64_t(g - 1 - j) * C, 0});
+              return v;
+            };
+            ring_ag(L, gr, pieces, [&, gr](int q) { return base(gr[q]); }, rb);
+          }
+        }
+      } else if (topo == 1) {  // AG_E then AG_I
+        for (int p = 0; p < M; ++p) {
+          auto pr = pos_ranks(p);
+          ring_ag(L, pr, [&, p](int c) { return one(int64_t(seg(c, p)) * C, C); },
+                  [&, pr](int q) { return base(pr[q]); }, round0);
+        }
+        for (int j = 0; j < g; ++j) {
+          auto gr = group_ranks(j);
+          ring_ag(L, gr, [&](int c) { return one(int64_t(c) * chunk, chunk); },
+                  [&, gr](int q) { return base(gr[q]); }, round0 + (g - 1));
+        }
+      } else if (topo == 2) {
+        std::vector<int> all;
+        for (int r = 0; r < N; ++r) all.push_back(r);
+        ring_ag(L, all, [&](int c) { return one(int64_t(seg(grp(c), pos(c))) * C, C); }, base, round0);
+      } else {  // direct: inter segments, then intra chunks
+        int rr = round0;
+        if (g > 1) {
+          for (int r = 0; r < N; ++r) {
+            const int j = grp(r), p = pos(r);
+            for (int x = 0; x < g; ++x) {
+              if (x == j) continue;
+              const int64_t o = int64_t(seg(x, p)) * C;
+              L.add(rr, r, make_task(C, {at(base(rank_of(x, p)), o)}, at(base(r), o)));
+            }
+          }
+          ++rr;
+        }
+        if (M > 1) {
+          for (int r = 0; r < N; ++r) {
+            const int j = grp(r), p = pos(r);
+            for (int c = 0; c < M; ++c) {
+              if (c == p) continue;
+              const int64_t o = int64_t(c) * chunk;
+              L.add(rr, r, make_task(chunk, {at(base(rank_of(j, c)), o)}, at(base(r), o)));
+            }
+          }
+        }
+      }
+    };
+    // AG_E in place in a chunk-layout buffer (segment j of chunk p at j*C)
+    auto emit_ag_e = [&](Launch& L, const std::function<Ref(int)>& base, int round0) {
+      for (int p = 0; p < M; ++p) {
+        auto pr = pos_ranks(p);
+        ring_ag(L, pr, [&](int c) { return one(int64_t(c) * C, C); }, [&, pr](int q) { return base(pr[q]); },
+                round0);
+      }
+    };
+    auto emit_ag_i = [&](Launch& L, const std::function<Ref(int)>& base, int round0) {
+      for (int j = 0; j < g; ++j) {
+        auto gr = group_ranks(j);
+        ring_ag(L, gr, [&](int c) { return one(int64_t(c) * chunk, chunk); },
+                [&, gr](int q) { return base(gr[q]); }, round0);
+      }
+    };
+
+    if (N > 1 && topo != 4) {
+      Launch& L = S.reduce;
+      if (G == LV_I) {
+        for (int j = 0; j < g; ++j) {   // RS_I into the G residency
+          auto gr = group_ranks(j);
+          ring_rs(L, gr, [&](int c) { return one(int64_t(c) * chunk, chunk); },
+                  [&, gr](int q, int, const Piece& pc) { return grad(gr[q], pc.src_off); },
+                  [&, gr](int q, int slot) { return stage_i(gr[q], slot); },
+                  [&, gr](int q) { return gshard(gr[q], 0); }, 0);
+        }
+        const int r0 = std::max(1, M - 1);
+        for (int p = 0; p < M; ++p) {   // RS_E; in place for OS = I (all-reduce)
+          auto pr = pos_ranks(p);
+          ring_rs(L, pr, [&](int c) { return one(int64_t(c) * C, C); },
+                  [&, pr](int q, int, const Piece& pc) { return gshard(pr[q], pc.src_off); },
+                  [&, pr](int q, int slot) { return stage_e(pr[q], slot); },
+                  [&, pr](int q) { return dest_seg(pr[q]); }, r0);
+        }
+        if (OS == LV_I) emit_ag_e(L, [&](int r) { return ghat_base(r); }, r0 + std::max(1, g - 1));
+      } else {
+        int used = emit_world_rs(L);
+        if (OS == LV_I) emit_ag_e(L, [&](int r) { return ghat_base(r); }, used);
+        if (OS == LV_N) emit_world_ag(L, [&](int r) { return ghat_base(r); }, used);
+      }
+      // ---- parameter restore
+      Launch& Lg = S.gather;
+      if (OS == LV_G && P == LV_I) emit_ag_e(Lg, param_base, 0);
+      if (OS == LV_G && P == LV_N) emit_world_ag(Lg, param_base, 0);
+      if (OS == LV_I && P == LV_N) emit_ag_i(Lg, param_base, 0);
+      // drop rounds that ended up empty for every rank (degenerate splits)
+      for (Launch* Lp : {&S.reduce, &S.gather}) {
+        std::vector<std::vector<std::vector<Task>>> kept;
+        for (auto& rnd : Lp->rounds) {
+          bool any = false;
+          for (auto& v : rnd) any = any || !v.empty();
+          if (any) kept.push_back(rnd);
+        }
+        Lp->rounds.swap(kept);
+      }
+    } else if (N > 1 && topo == 4) {  // NCCL comparator
+      for (int r = 0; r < N; ++r) {
+        auto& red = S.nccl_reduce[r];
+        auto& gat = S.nccl_gather[r];
+        const int j = grp(r);
+        if (G == LV_I) {
+          red.push_back({NcclCall::RS, NcclCall::INTRA, grad(r, 0), gshard(r, 0), chunk});
+          if (OS == LV_G) red.push_back({NcclCall::RS, NcclCall::INTER, gshard(r, 0), dest_seg(r), C});
+          else red.push_back({NcclCall::AR, NcclCall::INTER, gshard(r, 0), gshard(r, 0), chunk});
+        } else {
+          red.push_back({NcclCall::RS, NcclCall::INTRA, grad(r, 0), p1(r), chunk});
+          red.push_back({NcclCall::RS, NcclCall::INTER, p1(r), dest_seg(r), C});
+          if (OS == LV_I) red.push_back({NcclCall::AG, NcclCall::INTER, dest_seg(r), ghat_base(r), C});
+          if (OS == LV_N) {
+            Ref cb = at(ghat_base(r), int64_t(pos(r)) * chunk);
+            red.push_back({NcclCall::AG, NcclCall::INTER, dest_seg(r), cb, C});
+            red.push_back({NcclCall::AG, NcclCall::INTRA, cb, ghat_base(r), chunk});
+          }
+        }
+        if (OS == LV_G && P == LV_I)
+          gat.push_back({NcclCall::AG, NcclCall::INTER, at(param_base(r), int64_t(j) * C), param_base(r), C});
+        if (OS == LV_G && P == LV_N) {
+          Ref cb = at(param_base(r), int64_t(pos(r)) * chunk);
+          gat.push_back({NcclCall::AG, NcclCall::INTER, at(cb, int64_t(j) * C), cb, C});
+          gat.push_back({NcclCall::AG, NcclCall::INTRA, cb, param_base(r), chunk});
+        }
+        if (OS == LV_I && P == LV_N)
+          gat.push_back({NcclCall::AG, NcclCall::INTRA, at(param_base(r), int64_t(pos(r)) * chunk),
+                         param_base(r), chunk});
+      }
+    }
+
+    // ---- Adam placement per rank
+    S.os_len = n / divl(OS);
+    S.ghat.resize(N);
+    S.param.resize(N);
+    S.os_off.resize(N);
+    for (int r = 0; r < N; ++r) {
+      const int j = grp(r), p = pos(r);
+      S.os_off[r] = s / divl(OS);
+      S.ghat[r] = (N == 1) ? grad(r, 0) : ghat_base(r);
+      Ref pb = param_base(r);
+      if (P == OS) S.param[r] = pb;
+      else if (P == LV_I) S.param[r] = at(pb, int64_t(j) * C);              // OS = G
+      else if (OS == LV_G) S.param[r] = at(pb, int64_t(seg(j, p)) * C);     // P = N
+      else S.param[r] = at(pb, int64_t(p) * chunk);                         // P = N, OS = I
+    }
+  }
+  // the last collective launch of a step ends with a barrier: afterwards no
+  // peer reads this rank's buffers, so the caller may overwrite gradients.
+  for (int b = (int)sched.size() - 1; b >= 0; --b) {
+    if (!sched[b].gather.empty()) { sched[b].gather.final_barrier = true; break; }
+    if (!sched[b].reduce.empty()) { sched[b].reduce.final_barrier = true; break; }
+  }
+}
+
+void Planner::count_bytes() {
+  send_intra.assign(N, 0);
+  send_inter.assign(N, 0);
+  n_rounds = 0;
+  n_comm_launches = 0;
+  for (const BucketSchedule& S : sched) {
+    for (const Launch* L : {&S.reduce, &S.gather}) {
+      if (L->empty()) continue;
+      ++n_comm_launches;
+      n_rounds += (int)L->rounds.size();
+      for (const auto& rnd : L->rounds)
+        for (int x = 0; x < N; ++x)
+          for (const Task& t : rnd[x])
+            for (int i = 0; i < t.nin; ++i) {
+              const int y = t.in[i].rank;
+              if (y == x) continue;
+              (grp(x) == grp(y) ? send_intra[y] : send_inter[y]) += 2 * t.n;
+            }
+    }
+    // NCCL comparator: ring-algorithm volumes of each call (perf only)
+    for (int r = 0; r < N && opt.topology == 4; ++r) {
+      for (const auto* calls : {&S.nccl_reduce[r], &S.nccl_gather[r]}) {
+        for (const NcclCall& c : *calls) {
+          const int k = (c.comm == NcclCall::INTRA) ? M : (c.comm == NcclCall::INTER ? g : N);
+          const int64_t per = (c.kind == NcclCall::AR) ? 2 * (k - 1) * (c.count / k) : (k - 1) * c.count;
+          (c.comm == NcclCall::INTRA ? send_intra[r] : send_inter[r]) += 2 * per;
+        }
+        if (!calls->empty()) ++n_comm_launches;
+      }
+    }
+  }
+  if (opt.topology == 4) n_comm_launches /= std::max(1, N);
+}
+
+}  // namespace paro

@@ -1,0 +1,137 @@
+// planner.h — host-only PaRO planner: strategy validation, flat layout,
+// buckets, position-major shard map, per-bucket collective schedule (as
+// symbolic pull-model transfer lists for every rank), and byte/memory
+// accounting.  No CUDA here: the planning-only context uses it on a CPU box.
+//
+// Paper: P = PAPER.md line.  Strategy codes and Principle 1: P:240-243,
+// Table 1 P:266-298.  Shard levels N/I/G: P:185-188.  Schedules: P:333-363.
+// HO-Ring: P:385-410.  Memory: Table 2 P:416-439.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace paro {
+
+enum Level : int { LV_N = 0, LV_I = 1, LV_G = 2 };
+
+// Buffers of one rank, all bf16, carved from one symmetric allocation so a
+// (rank, kind, offset) triple names the same bytes on every rank.
+enum BufKind : int {
+  BUF_GRAD = 0,    // flat gradients, psi_pad (raw: scaled by 1/N when read)
+  BUF_PARAM,       // parameter residency, p_numel
+  BUF_GSHARD,      // gradient residency (G = I or G), g_numel
+  BUF_GHAT,        // reduced-gradient slots when G != OS
+  BUF_STAGE_I,     // intra-ring partials: 2 parities x 2 slots
+  BUF_STAGE_E,     // inter-ring partials: 2 parities x 2 slots
+  BUF_P1,          // HO phase-1 / direct phase-1 output: 2 parities
+  BUF_SOWN,        // own-group partial (HO phase 2): 2 parities
+  BUF_NKINDS
+};
+
+constexpr int kMaxIn = 16;   // max inputs of one fold task
+
+struct Ref {
+  int32_t rank = -1;
+  int32_t kind = -1;
+  int64_t off = 0;           // element offset inside the buffer kind
+};
+
+// dst = (((in0 (+) in1) (+) in2) ...), (+) = RNE_bf16(fp32 + fp32); inputs
+// that reference BUF_GRAD are first scaled: RNE_bf16(fp32(g) * alpha).
+// nin == 1 is a copy (or a pack when the input is raw).
+struct Task {
+  int64_t n = 0;             // elements (multiple of 8)
+  int32_t nin = 0;
+  Ref in[kMaxIn];
+  Ref dst;
+};
+
+// One collective launch = rounds; round r holds, for every rank, its tasks.
+struct Launch {
+  std::vector<std::vector<std::vector<Task>>> rounds;  // [round][rank][task]
+  bool final_barrier = false;
+  int n_ranks = 0;
+  void add(int round, int rank, const Task& t);
+  bool empty() const { return rounds.empty(); }
+  // ranks `rank` reads from in round r (excluding itself)
+  std::vector<int> reads(int r, int rank) const;
+  // symmetric barrier peer set before round r (r == rounds.size(): final)
+  uint64_t barrier_peers(int r, int rank) const;
+};
+
+// NCCL comparator call (PARO_TOPO_NCCL): not bit-exact, perf only.
+struct NcclCall {
+  enum Kind { RS, AG, AR } kind;
+  enum Comm { WORLD, INTRA, INTER } comm;
+  Ref send, recv;            // for the local rank (rank field = owner)
+  int64_t count;             // recv count (RS), send count (AG), count (AR)
+};
+
+struct BucketSchedule {
+  Launch reduce;             // gradient reduction to the OS residency
+  Launch gather;             // parameter restore to the P residency
+  std::vector<std::vector<NcclCall>> nccl_reduce, nccl_gather;  // [rank][call]
+  // Adam input/output per rank for this bucket
+  std::vector<Ref> ghat;     // reduced gradient at the OS residency start
+  std::vector<Ref> param;    // parameter-buffer position of the OS residency
+  std::vector<int64_t> os_off;   // offset in the rank's opt-state arrays
+  int64_t os_len = 0;
+};
+
+struct PlanOptions {
+  int64_t bucket_elems = int64_t(1) << 26;
+  int topology = 0;          // PARO_TOPO_*
+  int pipeline_depth = 2;
+};
+
+class Planner {
+ public:
+  // Throws std::invalid_argument with the user-facing message.
+  Planner(int N, int M, const std::string& code, const std::vector<int64_t>& sizes,
+          const PlanOptions& opt);
+
+  int N, M, g;
+  Level P, G, OS;
+  std::string code;
+  PlanOptions opt;
+  int64_t psi = 0, psi_pad = 0, B = 0;
+  std::vector<std::pair<int64_t, int64_t>> buckets;   // (start, size)
+  std::vector<int64_t> param_sizes, param_offsets;
+  int64_t p_numel = 0, g_numel = 0, os_numel = 0;
+  int nslots = 0;                                      // BUF_GHAT slots
+  int64_t ghat_slot = 0;                               // elements per slot
+  int64_t buf_len[BUF_NKINDS] = {0};                   // elements per kind
+  int64_t buf_off[BUF_NKINDS] = {0};                   // element offset in the region
+  int64_t region_elems = 0;                            // symmetric region (bf16 elems)
+  int64_t stage_i_len = 0, stage_e_len = 0, p1_len = 0, sown_len = 0;
+
+  std::vector<BucketSchedule> sched;
+  std::vector<std::string> grad_ops, rest_ops;        // primitives (for reporting)
+  std::vector<int64_t> send_intra, send_inter;        // bytes per rank per step
+  int n_rounds = 0, n_comm_launches = 0;
+
+  static int div(Level l, int N, int M) { return l == LV_N ? 1 : (l == LV_I ? M : N); }
+  int divl(Level l) const { return div(l, N, M); }
+  int rank_of(int j, int p) const { return j * M + p; }
+  int grp(int r) const { return r / M; }
+  int pos(int r) const { return r % M; }
+  int seg(int j, int p) const { return p * g + j; }
+
+  // flat [begin, end) of `level` residency of rank r in bucket b (R1)
+  void residency(Level l, int r, int64_t b, int64_t* begin, int64_t* end) const;
+  int64_t mem_bytes(int state) const;   // 0 P, 1 G, 2 OS (Table 2 at psi_pad)
+
+ private:
+  void layout();
+  void build_schedule();
+  void count_bytes();
+};
+
+Level parse_level(char c);
+// Validation helpers shared by the C API (messages follow S:63).
+std::string validate_strategy(const std::string& code);   // "" if OK
+std::string validate_cluster(int N, int M);               // "" if OK
+
+}  // namespace paro

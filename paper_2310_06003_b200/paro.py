@@ -1,0 +1,238 @@
+"""ctypes binding of libparo.so (include/paro.h).  Argument marshalling only:
+every step of the PaRO sync + update path runs in the library's kernels.
+
+The functions keep the C names (paro_init, paro_plan, paro_step, ...); the
+small `Context` / `Plan` classes below only hold handles and turn status
+codes into exceptions.  There is no CPU fallback: if the shared library is
+missing this module raises at import time.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libparo.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
+
+_lib = C.CDLL(LIB_PATH)
+
+# ---------------------------------------------------------------- constants
+PARO_OK, PARO_ERR_INVALID, PARO_ERR_OOM, PARO_ERR_CUDA, PARO_ERR_NCCL, PARO_ERR_STATE, PARO_ERR_TIMEOUT = range(7)
+TOPO = {"ho": 0, "two_step": 1, "flat": 2, "direct": 3, "nccl": 4}
+STATE = {"P": 0, "G": 1, "OS": 2}
+
+
+class ParoError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"[paro status {status}] {msg}")
+        self.status = status
+
+
+# ---------------------------------------------------------------- structs
+class paro_uid_t(C.Structure):
+    _fields_ = [("bytes", C.c_char * 128)]
+
+
+class paro_opt_state_t(C.Structure):
+    _fields_ = [("master", C.c_void_p), ("m", C.c_void_p), ("v", C.c_void_p)]
+
+
+class paro_opts_t(C.Structure):
+    _fields_ = [("bucket_elems", C.c_int64), ("topology", C.c_int), ("beta1", C.c_float),
+                ("beta2", C.c_float), ("eps", C.c_float), ("weight_decay", C.c_float),
+                ("loss_scale", C.c_float), ("comm_ctas", C.c_int), ("pipeline_depth", C.c_int),
+                ("stream", C.c_void_p)]
+
+
+class paro_plan_info_t(C.Structure):
+    _fields_ = [("psi", C.c_int64), ("psi_pad", C.c_int64), ("bucket_elems", C.c_int64),
+                ("n_buckets", C.c_int64), ("p_numel", C.c_int64), ("g_numel", C.c_int64),
+                ("os_numel", C.c_int64), ("mem_p_bytes", C.c_int64), ("mem_g_bytes", C.c_int64),
+                ("mem_os_bytes", C.c_int64), ("workspace_bytes", C.c_int64),
+                ("step_send_bytes_intra", C.c_int64), ("step_send_bytes_inter", C.c_int64),
+                ("n_rounds", C.c_int32), ("n_comm_launches", C.c_int32)]
+
+
+class paro_step_stats_t(C.Structure):
+    _fields_ = [("grad_norm", C.c_double), ("nonfinite", C.c_int32), ("sent_intra", C.c_int64),
+                ("sent_inter", C.c_int64), ("kernel_launches", C.c_int32)]
+
+
+class paro_profile_t(C.Structure):
+    _fields_ = [("adam_ms", C.c_double), ("comm_ms", C.c_double), ("adam_launches", C.c_int64),
+                ("comm_launches", C.c_int64), ("adam_elems", C.c_int64), ("comm_bytes", C.c_int64),
+                ("steps", C.c_int64), ("kernel_launches", C.c_int64)]
+
+
+_vp = C.c_void_p
+_i64 = C.c_int64
+_st = C.c_int
+
+
+def _sig(name, restype, *argtypes):
+    f = getattr(_lib, name)
+    f.restype = restype
+    f.argtypes = list(argtypes)
+    return f
+
+
+paro_opts_default = _sig("paro_opts_default", None, C.POINTER(paro_opts_t))
+paro_get_unique_id = _sig("paro_get_unique_id", _st, C.POINTER(paro_uid_t))
+paro_init = _sig("paro_init", _st, C.c_int, C.c_int, C.c_int, C.POINTER(paro_uid_t), C.c_int, C.POINTER(_vp))
+paro_init_emulated = _sig("paro_init_emulated", _st, C.c_int, C.c_int, C.c_int, C.POINTER(_vp))
+paro_init_planner = _sig("paro_init_planner", _st, C.c_int, C.c_int, C.POINTER(_vp))
+paro_finalize = _sig("paro_finalize", _st, _vp)
+paro_plan = _sig("paro_plan", _st, _vp, C.c_char_p, C.POINTER(_i64), C.c_int, C.POINTER(paro_opts_t),
+                 C.POINTER(_vp))
+paro_plan_info = _sig("paro_plan_info", _st, _vp, C.POINTER(paro_plan_info_t))
+paro_shard_range = _sig("paro_shard_range", _st, _vp, C.c_int, C.c_int, _i64, C.POINTER(_i64), C.POINTER(_i64))
+paro_bucket_range = _sig("paro_bucket_range", _st, _vp, _i64, C.POINTER(_i64), C.POINTER(_i64))
+paro_rank_send_bytes = _sig("paro_rank_send_bytes", _st, _vp, C.c_int, C.POINTER(_i64), C.POINTER(_i64))
+paro_buffer = _sig("paro_buffer", _st, _vp, C.c_int, C.c_int, C.POINTER(_vp))
+paro_opt_state_init = _sig("paro_opt_state_init", _st, _vp, C.c_int, _vp, C.POINTER(paro_opt_state_t))
+paro_opt_state_init_synth = _sig("paro_opt_state_init_synth", _st, _vp, C.c_int, C.c_uint64,
+                                 C.POINTER(paro_opt_state_t))
+paro_synth_grads = _sig("paro_synth_grads", _st, _vp, C.c_int, C.c_uint64, _i64)
+paro_step = _sig("paro_step", _st, _vp, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(paro_opt_state_t),
+                 C.c_float, _i64)
+paro_step_stats = _sig("paro_step_stats", _st, _vp, C.POINTER(paro_step_stats_t))
+paro_plan_destroy = _sig("paro_plan_destroy", _st, _vp)
+paro_profile_start = _sig("paro_profile_start", _st, _vp, C.c_int)
+paro_profile_stop = _sig("paro_profile_stop", _st, _vp, C.POINTER(paro_profile_t))
+paro_last_error = _sig("paro_last_error", C.c_char_p)
+paro_version = _sig("paro_version", C.c_char_p)
+
+EXPORTED = ["paro_opts_default", "paro_get_unique_id", "paro_init", "paro_init_emulated",
+            "paro_init_planner", "paro_finalize", "paro_plan", "paro_plan_info", "paro_shard_range",
+            "paro_bucket_range", "paro_rank_send_bytes", "paro_buffer", "paro_opt_state_init",
+            "paro_opt_state_init_synth", "paro_synth_grads", "paro_step", "paro_step_stats",
+            "paro_plan_destroy", "paro_last_error", "paro_version", "paro_profile_start",
+            "paro_profile_stop"]
+
+
+def check(status):
+    if status != PARO_OK:
+        raise ParoError(status, paro_last_error().decode())
+    return status
+
+
+# ---------------------------------------------------------------- helpers
+def make_opts(bucket_elems=1 << 26, topology="ho", beta1=0.9, beta2=0.95, eps=1e-8, weight_decay=0.0,
+              loss_scale=1.0, comm_ctas=64, pipeline_depth=2, stream=None):
+    o = paro_opts_t()
+    paro_opts_default(C.byref(o))
+    o.bucket_elems = int(bucket_elems)
+    o.topology = TOPO[topology] if isinstance(topology, str) else int(topology)
+    o.beta1, o.beta2, o.eps = beta1, beta2, eps
+    o.weight_decay, o.loss_scale = weight_decay, loss_scale
+    o.comm_ctas, o.pipeline_depth = int(comm_ctas), int(pipeline_depth)
+    o.stream = stream
+    return o
+
+
+def unique_id():
+    u = paro_uid_t()
+    check(paro_get_unique_id(C.byref(u)))
+    return bytes(u.bytes)
+
+
+class Context:
+    """paro_init (real rank), paro_init_emulated (all ranks, one device) or
+    paro_init_planner (host only)."""
+
+    def __init__(self, world_size, group_size, mode="planner", rank=0, device=0, uid=None):
+        h = _vp()
+        if mode == "planner":
+            check(paro_init_planner(world_size, group_size, C.byref(h)))
+        elif mode == "emulated":
+            check(paro_init_emulated(world_size, group_size, device, C.byref(h)))
+        elif mode == "real":
+            u = paro_uid_t()
+            u.bytes = uid
+            check(paro_init(world_size, group_size, rank, C.byref(u), device, C.byref(h)))
+        else:
+            raise ValueError(mode)
+        self.h, self.mode, self.N, self.M, self.rank = h, mode, world_size, group_size, rank
+
+    def close(self):
+        if self.h:
+            paro_finalize(self.h)
+            self.h = None
+
+
+class Plan:
+    def __init__(self, ctx: Context, strategy: str, param_sizes, **opts):
+        self.ctx = ctx
+        self.sizes = [int(s) for s in param_sizes]
+        arr = (_i64 * max(1, len(self.sizes)))(*self.sizes)
+        self.opts = make_opts(**opts)
+        h = _vp()
+        check(paro_plan(ctx.h, strategy.encode(), arr, len(self.sizes), C.byref(self.opts), C.byref(h)))
+        self.h = h
+        self.strategy = strategy
+
+    def info(self):
+        i = paro_plan_info_t()
+        check(paro_plan_info(self.h, C.byref(i)))
+        return {k: getattr(i, k) for k, _ in paro_plan_info_t._fields_}
+
+    def shard_range(self, state, rank, bucket):
+        b, e = _i64(), _i64()
+        check(paro_shard_range(self.h, STATE[state] if isinstance(state, str) else state, rank, bucket,
+                               C.byref(b), C.byref(e)))
+        return b.value, e.value
+
+    def bucket_range(self, bucket):
+        b, e = _i64(), _i64()
+        check(paro_bucket_range(self.h, bucket, C.byref(b), C.byref(e)))
+        return b.value, e.value
+
+    def send_bytes(self, rank):
+        a, b = _i64(), _i64()
+        check(paro_rank_send_bytes(self.h, rank, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
+    def buffer(self, rank, kind):
+        p = _vp()
+        check(paro_buffer(self.h, rank, kind, C.byref(p)))
+        return p.value
+
+    def opt_state_init(self, rank, st, master_full_ptr=None, seed=None):
+        s = paro_opt_state_t(*st)
+        if master_full_ptr is not None:
+            check(paro_opt_state_init(self.h, rank, master_full_ptr, C.byref(s)))
+        else:
+            check(paro_opt_state_init_synth(self.h, rank, int(seed), C.byref(s)))
+
+    def synth_grads(self, rank, seed, step):
+        check(paro_synth_grads(self.h, rank, int(seed), int(step)))
+
+    def step(self, opt_states, lr, step, grads=None, params=None):
+        """opt_states: list (per local rank) of (master, m, v) device pointers;
+        grads / params: None (zero-copy flat buffers) or flat lists of pointers."""
+        n = len(opt_states)
+        sts = (paro_opt_state_t * n)(*[paro_opt_state_t(*s) for s in opt_states])
+        gp = (_vp * len(grads))(*grads) if grads is not None else None
+        pp = (_vp * len(params))(*params) if params is not None else None
+        check(paro_step(self.h, gp, pp, sts, float(lr), int(step)))
+
+    def stats(self):
+        s = paro_step_stats_t()
+        check(paro_step_stats(self.h, C.byref(s)))
+        return {k: getattr(s, k) for k, _ in paro_step_stats_t._fields_}
+
+    def profile_start(self, max_launches):
+        check(paro_profile_start(self.h, int(max_launches)))
+
+    def profile_stop(self):
+        s = paro_profile_t()
+        check(paro_profile_stop(self.h, C.byref(s)))
+        return {k: getattr(s, k) for k, _ in paro_profile_t._fields_}
+
+    def close(self):
+        if self.h:
+            paro_plan_destroy(self.h)
+            self.h = None

@@ -1,0 +1,136 @@
+"""C-ABI tests that need no GPU: the library loads, exports every symbol
+include/paro.h declares, and its host planner agrees bit-exactly with the
+oracle (shard maps, per-rank bytes counted from the transfer lists, memory
+accounting, error strings)."""
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+from oracle import accounting as A
+from oracle import layout as L
+from oracle import numerics as nm
+from oracle import step as ST
+from oracle import strategy as S
+from paper_2310_06003_b200 import paro
+from paro_synth import grad_bits, llama_param_sizes, master_f32
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_exports_every_declared_symbol():
+    hdr = open(os.path.join(ROOT, "include", "paro.h")).read()
+    declared = set(re.findall(r"\b(paro_[a-z_]+)\s*\(", hdr))
+    out = subprocess.run(["nm", "-D", "--defined-only", paro.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r" T (paro_[a-z_]+)$", out, re.M))
+    assert declared, "no declarations parsed"
+    assert declared <= exported, declared - exported
+    assert set(paro.EXPORTED) == declared
+
+
+def test_library_is_sm100a():
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", paro.LIB_PATH],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_error_strings():
+    ctx = paro.Context(8, 4)
+    for code, msg in [("XGG", "invalid shard level 'X' at position 1"),
+                      ("GGN", "strategy 'GGN' violates Principle 1 (S_P>=S_OS and S_G>=S_OS)"),
+                      ("IG", "strategy code must have 3 characters")]:
+        with pytest.raises(paro.ParoError, match=re.escape(msg)):
+            paro.Plan(ctx, code, [1024])
+    with pytest.raises(paro.ParoError, match="group_size must divide n_gpus"):
+        paro.Context(9, 4)
+    ctx.close()
+
+
+def test_all_27_codes_accept_exactly_table1():
+    ctx = paro.Context(4, 2)
+    ok = []
+    for code in S.enumerate_all():
+        try:
+            paro.Plan(ctx, code, [4096]).close()
+            ok.append(code)
+        except paro.ParoError:
+            pass
+    assert sorted(ok) == sorted(S.TABLE1_ROWS)
+    ctx.close()
+
+
+SPLITS = [(8, 4), (8, 2), (4, 2), (9, 3), (8, 1), (8, 8), (2, 1), (1, 1), (12, 3), (6, 2), (16, 4)]
+
+
+@pytest.mark.parametrize("N,M", SPLITS)
+def test_shard_ranges_and_memory_match_oracle(N, M):
+    sizes = [3000, 517, 64, 9000, 7]
+    B = N * 64 * 4
+    lay = L.Layout(sizes, N, M, B)
+    ctx = paro.Context(N, M)
+    for code in S.paro_strategies():
+        pl = paro.Plan(ctx, code, sizes, bucket_elems=B)
+        info = pl.info()
+        assert info["psi"] == lay.psi and info["psi_pad"] == lay.psi_pad
+        assert info["n_buckets"] == len(lay.buckets) and info["bucket_elems"] == lay.B
+        for b in range(len(lay.buckets)):
+            assert pl.bucket_range(b) == (lay.buckets[b][0], sum(lay.buckets[b]))
+            for r in range(N):
+                for st, lvl in zip(("P", "G", "OS"), code):
+                    assert pl.shard_range(st, r, b) == lay.residency(lvl, r, b)
+        mp, mg, mo = A.memory_strategy(code, N, M, lay.psi_pad)
+        assert (info["mem_p_bytes"], info["mem_g_bytes"], info["mem_os_bytes"]) == (mp, mg, mo)
+        assert info["p_numel"] == lay.shard_numel(code[0])
+        assert info["os_numel"] == lay.shard_numel(code[2])
+        pl.close()
+    ctx.close()
+
+
+@pytest.mark.parametrize("N,M", SPLITS)
+def test_send_bytes_match_oracle_simulator(N, M):
+    """Bytes counted from the library's transfer lists == the oracle's round
+    simulator (HO-Ring, two-step and flat topologies), bit-exact."""
+    sizes = [3000, 517, 64, 9000, 7]
+    B = N * 64 * 4
+    lay = L.Layout(sizes, N, M, B)
+    grads = [grad_bits(r, 1, 0, lay.psi) for r in range(N)]
+    w0 = master_f32(0, lay.psi)
+    ctx = paro.Context(N, M)
+    for code in S.paro_strategies():
+        for topo in ("ho", "two_step", "flat"):
+            pl = paro.Plan(ctx, code, sizes, bucket_elems=B, topology=topo)
+            res = ST.strategy_step(code, lay, grads, ST.init_state(w0, lay, code), nm.AdamScalars(1e-3, 1),
+                                   topology=topo)
+            for r in range(N):
+                assert pl.send_bytes(r) == (2 * res.sent[r][0], 2 * res.sent[r][1]), (code, topo, r)
+            pl.close()
+    ctx.close()
+
+
+@pytest.mark.parametrize("N,M", [(8, 4), (8, 2), (4, 2), (8, 1), (8, 8), (16, 4)])
+def test_direct_topology_bytes_equal_closed_form(N, M):
+    ctx = paro.Context(N, M)
+    for code in S.paro_strategies():
+        pl = paro.Plan(ctx, code, [N * 64 * 16], bucket_elems=N * 64 * 4, topology="direct")
+        a, b = A.step_units_per_rank(code, N, M, N * 64 * 16)
+        for r in range(N):
+            assert pl.send_bytes(r) == (2 * a, 2 * b), code
+        pl.close()
+    ctx.close()
+
+
+def test_llama7b_plan_accounting():
+    sizes = llama_param_sizes("7B")
+    assert len(sizes) == 291 and sum(sizes) == 6_738_415_616
+    ctx = paro.Context(8, 4)
+    for code in S.paro_strategies():
+        pl = paro.Plan(ctx, code, sizes, bucket_elems=1 << 26)
+        info = pl.info()
+        assert info["psi_pad"] == 6_738_415_616 and info["n_buckets"] == 101
+        a, b = A.step_units_per_rank(code, 8, 4, info["psi_pad"])
+        for r in range(8):
+            assert pl.send_bytes(r) == (2 * a, 2 * b)
+        pl.close()
+    ctx.close()

@@ -1,0 +1,273 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Emulated mode runs all N ranks of a split on one B200 (each collective round
+is one kernel over every rank's buffers), so any (N, M) is checked bit for bit.
+Bar (BASELINE.json north_star): shard maps / bytes exact; fp32
+masters, m, v and bf16 params bit-exact (the 1e-5 relative / 1-ulp fallback
+is never needed); NaN compared by isnan; grad norm rel 1e-12.
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import layout as L
+from oracle import numerics as nm
+from oracle import step as ST
+from oracle import strategy as S
+from paro_synth import SEED, edge_grad_bits, grad_bits, master_f32, ragged_param_sizes
+
+from devmem import d2h, h2d
+
+pytestmark = pytest.mark.gpu
+
+LR = 3e-4
+
+
+def _paro():
+    from paper_2310_06003_b200 import paro
+    return paro
+
+
+class EmuRun:
+    """All ranks of one split on cuda:0 through the C ABI."""
+
+    def __init__(self, N, M, code, sizes, B, topo="ho", depth=2, wd=0.0, loss_scale=1.0):
+        paro = _paro()
+        self.ctx = paro.Context(N, M, mode="emulated", device=0)
+        self.pl = paro.Plan(self.ctx, code, sizes, bucket_elems=B, topology=topo, pipeline_depth=depth,
+                            weight_decay=wd, loss_scale=loss_scale)
+        self.info = self.pl.info()
+        self.N, self.code, self.sizes = N, code, sizes
+        n = self.info["os_numel"]
+        self.st = [tuple(torch.empty(n, dtype=torch.float32, device="cuda") for _ in range(3)) for _ in range(N)]
+        for r in range(N):
+            self.pl.opt_state_init(r, [t.data_ptr() for t in self.st[r]], seed=SEED)
+
+    def ptrs(self):
+        return [[t.data_ptr() for t in s] for s in self.st]
+
+    def set_grads(self, t, kind="synth"):
+        for r in range(self.N):
+            if kind == "synth":
+                self.pl.synth_grads(r, SEED, t)
+            else:
+                g = np.zeros(self.info["psi_pad"], np.uint16)
+                g[:self.info["psi"]] = edge_grad_bits(kind, self.info["psi"], rank=r, step=t)
+                h2d(self.pl.buffer(r, 0), g)
+
+    def step(self, t, **kw):
+        self.pl.step(self.ptrs(), LR, t, **kw)
+        return self.pl.stats()
+
+    def state(self, r):
+        torch.cuda.synchronize()
+        out = {k: self.st[r][i].cpu().numpy() for i, k in enumerate(("master", "m", "v"))}
+        out["param"] = d2h(self.pl.buffer(r, 1), self.info["p_numel"], np.uint16)
+        return out
+
+    def close(self):
+        self.pl.close()
+        self.ctx.close()
+
+
+def _oracle_grads(N, psi, t, kind="synth"):
+    if kind == "synth":
+        return [grad_bits(r, t, 0, psi) for r in range(N)]
+    return [edge_grad_bits(kind, psi, rank=r, step=t) for r in range(N)]
+
+
+def _assert_same(got, ref, what):
+    if ref.dtype == np.uint16:
+        gf, rf = nm.f32_from_bf16_bits(got), nm.f32_from_bf16_bits(ref)
+    else:
+        gf, rf = got, ref
+    nan_g, nan_r = np.isnan(gf), np.isnan(rf)
+    assert np.array_equal(nan_g, nan_r), f"{what}: NaN pattern differs"
+    ok = ~nan_r
+    bad = np.nonzero(gf[ok] != rf[ok])[0]
+    assert bad.size == 0, f"{what}: {bad.size} mismatches, first at {bad[0]}: {gf[ok][bad[0]]} vs {rf[ok][bad[0]]}"
+
+
+def _dp_reference(lay, steps, kind="synth", wd=0.0, loss_scale=1.0):
+    w0 = master_f32(0, lay.psi)
+    w = ST.pad_flat(w0, lay.psi_pad, np.float32)
+    m, v = np.zeros_like(w), np.zeros_like(w)
+    norms = []
+    for t in range(1, steps + 1):
+        sc = nm.AdamScalars(LR, t, weight_decay=wd, loss_scale=loss_scale)
+        w, m, v, p, gh = ST.dp_step(lay, _oracle_grads(lay.N, lay.psi, t, kind), w, m, v, sc)
+        norms.append(nm.grad_sq_sum(gh, sc.s_g))
+    return w, m, v, p, norms
+
+
+def _check_against_dp(run, lay, ref):
+    w, m, v, p, _ = ref
+    pl_, _, ol = run.code
+    for r in range(lay.N):
+        st = run.state(r)
+        _assert_same(st["master"], ST.shard_of(w, lay, ol, r), f"rank {r} master")
+        _assert_same(st["m"], ST.shard_of(m, lay, ol, r), f"rank {r} m")
+        _assert_same(st["v"], ST.shard_of(v, lay, ol, r), f"rank {r} v")
+        _assert_same(st["param"], ST.shard_of(p, lay, pl_, r), f"rank {r} param")
+
+
+# --------------------------------------------------------------------- generator
+def test_synth_generator_matches_host():
+    run = EmuRun(1, 1, "NNN", [100_003], 1 << 16)
+    run.set_grads(3)
+    g = d2h(run.pl.buffer(0, 0), run.info["psi_pad"], np.uint16)
+    assert np.array_equal(g[:100_003], grad_bits(0, 3, 0, 100_003))
+    assert not g[100_003:].any()
+    st = run.state(0)
+    assert np.array_equal(st["master"][:100_003], master_f32(0, 100_003))
+    assert np.array_equal(st["param"][:100_003], nm.bf16_bits_from_f32(master_f32(0, 100_003)))
+    run.close()
+
+
+# --------------------------------------------------------------------- N = 1
+@pytest.mark.parametrize("wd,ls", [(0.0, 1.0), (0.1, 4.0)])
+def test_n1_ten_steps_bit_exact(wd, ls):
+    sizes = [50_000, 4096, 12_345]
+    lay = L.Layout(sizes, 1, 1, 1 << 14)
+    run = EmuRun(1, 1, "NNN", sizes, 1 << 14, wd=wd, loss_scale=ls)
+    ref = _dp_reference(lay, 10, wd=wd, loss_scale=ls)
+    for t in range(1, 11):
+        run.set_grads(t)
+        stats = run.step(t)
+        assert abs(stats["grad_norm"] ** 2 - ref[4][t - 1]) <= 1e-12 * ref[4][t - 1]
+    _check_against_dp(run, lay, ref)
+    run.close()
+
+
+# --------------------------------------------------------------------- all strategies
+CONFIG_4M = dict(sizes=[1 << 22], B=1 << 18)   # BASELINE config 1: 2^22 params, 16 buckets
+
+
+@pytest.mark.parametrize("topo", ["ho", "two_step", "direct"])
+def test_4m_2x4_every_strategy_one_step(topo):
+    N, M = 8, 4
+    lay = L.Layout(CONFIG_4M["sizes"], N, M, CONFIG_4M["B"])
+    ref = _dp_reference(lay, 1)
+    for code in S.paro_strategies():
+        run = EmuRun(N, M, code, CONFIG_4M["sizes"], CONFIG_4M["B"], topo=topo)
+        run.set_grads(1)
+        stats = run.step(1)
+        assert abs(stats["grad_norm"] ** 2 - ref[4][0]) <= 1e-12 * ref[4][0]
+        _check_against_dp(run, lay, ref)
+        run.close()
+
+
+@pytest.mark.parametrize("N,M", [(8, 2), (4, 2), (8, 1), (8, 8), (6, 3), (2, 2), (2, 1), (9, 3)])
+@pytest.mark.parametrize("topo", ["ho", "two_step", "direct"])
+def test_splits_every_strategy_ragged(N, M, topo):
+    sizes = ragged_param_sizes() + [N * 64 * 7 + 3]
+    B = N * 64 * 3
+    lay = L.Layout(sizes, N, M, B)
+    ref = _dp_reference(lay, 2)
+    for code in S.paro_strategies():
+        run = EmuRun(N, M, code, sizes, B, topo=topo)
+        for t in (1, 2):
+            run.set_grads(t)
+            run.step(t)
+        _check_against_dp(run, lay, ref)
+        run.close()
+
+
+def test_flat_ring_matches_oracle_flat_simulation():
+    N, M = 8, 4
+    sizes = [N * 64 * 20]
+    B = N * 64 * 6
+    lay = L.Layout(sizes, N, M, B)
+    grads = _oracle_grads(N, lay.psi, 1)
+    w0 = master_f32(0, lay.psi)
+    for code in ("NNN", "NNG", "GGG", "IGG"):
+        res = ST.strategy_step(code, lay, grads, ST.init_state(w0, lay, code), nm.AdamScalars(LR, 1),
+                               topology="flat")
+        run = EmuRun(N, M, code, sizes, B, topo="flat")
+        run.set_grads(1)
+        run.step(1)
+        for r in range(N):
+            st = run.state(r)
+            for k in ("master", "m", "v", "param"):
+                _assert_same(st[k], res.state[r][k], f"{code} rank {r} {k}")
+        run.close()
+
+
+@pytest.mark.parametrize("code", ["IIG", "NNN", "III", "GGG"])
+def test_4m_2x4_ten_steps(code):
+    N, M = 8, 4
+    lay = L.Layout(CONFIG_4M["sizes"], N, M, CONFIG_4M["B"])
+    ref = _dp_reference(lay, 10)
+    run = EmuRun(N, M, code, CONFIG_4M["sizes"], CONFIG_4M["B"])
+    for t in range(1, 11):
+        run.set_grads(t)
+        run.step(t)
+    _check_against_dp(run, lay, ref)
+    run.close()
+
+
+@pytest.mark.parametrize("kind", ["zeros", "smallint", "specials", "nearmax"])
+def test_edge_inputs(kind):
+    N, M = 4, 2
+    sizes = [N * 64 * 10 + 5]
+    B = N * 64 * 4
+    lay = L.Layout(sizes, N, M, B)
+    ref = _dp_reference(lay, 1, kind=kind)
+    for code in ("NNN", "IIG", "INI", "GGG"):
+        run = EmuRun(N, M, code, sizes, B)
+        run.set_grads(1, kind=kind)
+        stats = run.step(1)
+        assert stats["nonfinite"] == (1 if kind in ("specials", "nearmax") else 0)
+        _check_against_dp(run, lay, ref)
+        run.close()
+
+
+def test_pack_and_unpack_paths_and_depth_determinism():
+    """Per-parameter gradient pointers (pack) and per-parameter outputs (unpack)
+    give the same bits as the zero-copy path; pipeline depth 1 vs 4 identical."""
+    N, M = 4, 2
+    sizes = [1000, 64, 4096 + 8, 777]
+    B = N * 64 * 4
+    lay = L.Layout(sizes, N, M, B)
+    ref = _dp_reference(lay, 1)
+    grads = _oracle_grads(N, lay.psi, 1)
+    for code in ("NNN", "NIG", "IGG"):
+        outs = []
+        for depth, use_ptrs in ((1, False), (4, True)):
+            run = EmuRun(N, M, code, sizes, B, depth=depth)
+            gkeep, gptrs, pkeep, pptrs = [], [], [], []
+            for r in range(N):
+                for i, s in enumerate(sizes):
+                    o = lay.param_offsets[i]
+                    tg = torch.from_numpy(grads[r][o:o + s].view(np.int16).copy()).cuda()
+                    gkeep.append(tg)
+                    gptrs.append(tg.data_ptr())
+                if code[0] == "N":
+                    for s in sizes:
+                        tp = torch.zeros(s, dtype=torch.int16, device="cuda")
+                        pkeep.append(tp)
+                        pptrs.append(tp.data_ptr())
+                else:
+                    tp = torch.zeros(run.info["p_numel"], dtype=torch.int16, device="cuda")
+                    pkeep.append(tp)
+                    pptrs.append(tp.data_ptr())
+            if use_ptrs:
+                run.step(1, grads=gptrs, params=pptrs)
+            else:
+                run.set_grads(1)
+                run.step(1)
+            _check_against_dp(run, lay, ref)
+            if use_ptrs:
+                torch.cuda.synchronize()
+                for r in range(N):
+                    st = run.state(r)
+                    if code[0] == "N":
+                        got = np.concatenate([t.cpu().numpy().view(np.uint16)
+                                              for t in pkeep[r * len(sizes):(r + 1) * len(sizes)]])
+                        assert np.array_equal(got, st["param"][:lay.psi])
+                    else:
+                        assert np.array_equal(pkeep[r].cpu().numpy().view(np.uint16), st["param"])
+            outs.append([run.state(r)["master"] for r in range(N)])
+            run.close()
+        for a, b in zip(*outs):
+            assert np.array_equal(a, b)
