@@ -18,6 +18,8 @@ used (R2, R5-R7):
 """
 from __future__ import annotations
 
+import math
+
 import numpy as np
 
 F32 = np.float32
@@ -89,7 +91,10 @@ def pack(grad_bits, alpha: float) -> np.ndarray:
 class AdamScalars:
     """Per-step host scalars of canonical Adam (R5, R6).
 
-    Every value is computed in double precision and rounded once to fp32.
+    The hyperparameters are fp32 values (lr, beta1, beta2, eps, weight_decay,
+    loss_scale are each rounded to fp32 first, as an fp32 optimizer API
+    receives them); every derived scalar is then computed in double precision
+    from those fp32 values and rounded once to fp32:
     step_size = lr / (1 - beta1^t);  bc2s = sqrt(1 - beta2^t);
     decay = 1 - lr * weight_decay;  s_g = 1 / loss_scale (unscale, R4).
     """
@@ -98,13 +103,15 @@ class AdamScalars:
                  loss_scale=1.0, clip_coef=1.0):
         if step < 1:
             raise ValueError("step must be >= 1")
-        lr, b1, b2 = float(lr), float(beta1), float(beta2)
+        f = lambda x: float(F32(x))
+        lr, b1, b2 = f(lr), f(beta1), f(beta2)
+        weight_decay, loss_scale, eps = f(weight_decay), f(loss_scale), f(eps)
         self.b1 = F32(b1)
         self.omb1 = F32(1.0 - b1)
         self.b2 = F32(b2)
         self.omb2 = F32(1.0 - b2)
         self.step_size = F32(lr / (1.0 - b1 ** step))
-        self.bc2s = F32((1.0 - b2 ** step) ** 0.5)
+        self.bc2s = F32(math.sqrt(1.0 - b2 ** step))
         self.eps = F32(eps)
         self.wd = float(weight_decay)
         self.decay = F32(1.0 - lr * float(weight_decay))
