@@ -198,6 +198,7 @@ Planner::Planner(int N_, int M_, const std::string& code_, const std::vector<int
   if (opt.pipeline_depth < 1) opt.pipeline_depth = 1;
   layout();
   build_schedule();
+  validate_refs();
   count_bytes();
 }
 
@@ -239,7 +240,7 @@ void Planner::layout() {
   p_numel = psi_pad / divl(P);
   g_numel = (G == LV_N) ? 0 : psi_pad / divl(G);
   os_numel = psi_pad / divl(OS);
-  if (G != OS && N > 1) {
+  if ((G != OS || G == LV_N) && N > 1) {   // reduced gradient needs its own slots
     nslots = opt.pipeline_depth + 1;
     ghat_slot = B / divl(OS);
   }
@@ -291,7 +292,7 @@ void Planner::build_schedule() {
     auto grad = [&](int r, int64_t o) { return Ref{r, BUF_GRAD, s + o}; };
     auto gshard = [&](int r, int64_t o) { return Ref{r, BUF_GSHARD, s / divl(G) + o}; };
     auto ghat_base = [&](int r) {
-      if (G == OS) return Ref{r, BUF_GSHARD, s / divl(G)};
+      if (G == OS && G != LV_N) return Ref{r, BUF_GSHARD, s / divl(G)};
       return Ref{r, BUF_GHAT, int64_t(b % nslots) * ghat_slot};
     };
     auto param_base = [&](int r) { return Ref{r, BUF_PARAM, s / divl(P)}; };
@@ -615,6 +616,32 @@ void Planner::build_schedule() {
   for (int b = (int)sched.size() - 1; b >= 0; --b) {
     if (!sched[b].gather.empty()) { sched[b].gather.final_barrier = true; break; }
     if (!sched[b].reduce.empty()) { sched[b].reduce.final_barrier = true; break; }
+  }
+}
+
+// Every transfer must stay inside its buffer kind (caught on the CPU, before
+// any kernel could fault on a bad schedule).
+void Planner::validate_refs() const {
+  auto ok = [&](const Ref& r, int64_t n) {
+    return r.rank >= 0 && r.rank < N && r.kind >= 0 && r.kind < BUF_NKINDS && r.off >= 0 &&
+           r.off + n <= buf_len[r.kind] && r.off % 8 == 0;
+  };
+  for (size_t b = 0; b < sched.size(); ++b) {
+    const BucketSchedule& S = sched[b];
+    for (const Launch* L : {&S.reduce, &S.gather})
+      for (const auto& rnd : L->rounds)
+        for (const auto& v : rnd)
+          for (const Task& t : v) {
+            if (t.n <= 0 || t.n % 8 != 0 || t.nin < 1 || t.nin > kMaxIn)
+              throw std::logic_error("bad task shape in bucket " + std::to_string(b));
+            for (int i = 0; i < t.nin; ++i)
+              if (!ok(t.in[i], t.n)) throw std::logic_error("task input out of range in bucket " + std::to_string(b));
+            if (!ok(t.dst, t.n)) throw std::logic_error("task output out of range in bucket " + std::to_string(b));
+          }
+    if (N > 1)
+      for (int r = 0; r < N; ++r)
+        if (!ok(S.ghat[r], S.os_len) || !ok(S.param[r], S.os_len))
+          throw std::logic_error("adam range out of range in bucket " + std::to_string(b));
   }
 }
 

@@ -127,6 +127,7 @@ class Planner {
   void layout();
   void build_schedule();
   void count_bytes();
+  void validate_refs() const;
 };
 
 Level parse_level(char c);

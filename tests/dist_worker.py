@@ -1,0 +1,80 @@
+"""Worker for the real multi-GPU parity test (launched by test_gpu_multi.py via
+torchrun, one process per GPU).  Each rank runs real-mode paro_step (NCCL
+bootstrap, peer-memory collectives) for every strategy / topology requested
+and saves its state shards; the parent compares them with the oracle.
+
+Also usable as a standalone smoke: torchrun --nproc-per-node 2 tests/dist_worker.py OUT
+"""
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+from paro_synth import SEED  # noqa: E402
+
+
+def main():
+    out = sys.argv[1]
+    cfg = json.loads(sys.argv[2]) if len(sys.argv) > 2 else {}
+    rank = int(os.environ["RANK"])
+    world = int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2310_06003_b200 import paro
+    splits = cfg.get("splits", [world])
+    codes = cfg.get("codes", ["NNN", "IIG", "NIG", "IGG", "GGG", "III", "INI", "NNG"])
+    topos = cfg.get("topos", ["ho", "two_step", "direct"])
+    sizes = cfg.get("sizes", [world * 64 * 40 + 24, 333])
+    B = cfg.get("bucket", world * 64 * 12)
+    steps = cfg.get("steps", 2)
+    for M in splits:
+        uid = paro.unique_id() if rank == 0 else bytes(128)
+        t = torch.tensor(list(uid), dtype=torch.uint8)
+        dist.broadcast(t, 0)
+        ctx = paro.Context(world, M, mode="real", rank=rank, device=local, uid=bytes(t.tolist()))
+        for code in codes:
+            for topo in topos:
+                pl = paro.Plan(ctx, code, sizes, bucket_elems=B, topology=topo)
+                info = pl.info()
+                st = [torch.empty(info["os_numel"], dtype=torch.float32, device="cuda") for _ in range(3)]
+                ptrs = [[x.data_ptr() for x in st]]
+                pl.opt_state_init(rank, ptrs[0], seed=SEED)
+                stats = None
+                for s in range(1, steps + 1):
+                    pl.synth_grads(rank, SEED, s)
+                    pl.step(ptrs, 3e-4, s)
+                    stats = pl.stats()
+                torch.cuda.synchronize()
+                pbuf = torch.empty(info["p_numel"], dtype=torch.int16, device="cuda")
+                _copy(pbuf, pl.buffer(rank, 1))
+                tag = f"{M}_{code}_{topo}_r{rank}"
+                np.savez(os.path.join(out, tag + ".npz"), master=st[0].cpu().numpy(), m=st[1].cpu().numpy(),
+                         v=st[2].cpu().numpy(), param=pbuf.cpu().numpy().view(np.uint16))
+                with open(os.path.join(out, tag + ".json"), "w") as f:
+                    json.dump({"stats": stats, "send": pl.send_bytes(rank)}, f)
+                pl.close()
+        ctx.close()
+        dist.barrier()
+    dist.destroy_process_group()
+
+
+def _copy(dst, src_ptr):
+    import ctypes
+    import glob
+    import nvidia.cuda_runtime as cr
+    path = glob.glob(os.path.join(list(cr.__path__)[0], "lib", "libcudart.so*"))[0]
+    rt = ctypes.CDLL(path)
+    rt.cudaMemcpy.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int]
+    assert rt.cudaMemcpy(ctypes.c_void_p(dst.data_ptr()), ctypes.c_void_p(src_ptr),
+                         dst.numel() * dst.element_size(), 3) == 0
+
+
+if __name__ == "__main__":
+    main()
