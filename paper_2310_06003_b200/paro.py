@@ -136,7 +136,7 @@ def make_opts(bucket_elems=1 << 26, topology="ho", beta1=0.9, beta2=0.95, eps=1e
 def unique_id():
     u = paro_uid_t()
     check(paro_get_unique_id(C.byref(u)))
-    return bytes(u.bytes)
+    return C.string_at(C.addressof(u), 128)   # raw 128 bytes (the id contains NULs)
 
 
 class Context:
@@ -151,7 +151,8 @@ class Context:
             check(paro_init_emulated(world_size, group_size, device, C.byref(h)))
         elif mode == "real":
             u = paro_uid_t()
-            u.bytes = uid
+            assert uid is not None and len(uid) == 128, "uid must be the 128 raw bytes of unique_id()"
+            C.memmove(C.addressof(u), bytes(uid), 128)
             check(paro_init(world_size, group_size, rank, C.byref(u), device, C.byref(h)))
         else:
             raise ValueError(mode)

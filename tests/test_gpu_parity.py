@@ -213,11 +213,15 @@ def test_edge_inputs(kind):
     B = N * 64 * 4
     lay = L.Layout(sizes, N, M, B)
     ref = _dp_reference(lay, 1, kind=kind)
+    gh = ST.dp_step(lay, _oracle_grads(N, lay.psi, 1, kind), *ref[:3], nm.AdamScalars(LR, 1))[4]
+    expect_nonfinite = int(not np.all(np.isfinite(nm.f32_from_bf16_bits(gh))))
+    if kind == "specials":
+        assert expect_nonfinite == 1
     for code in ("NNN", "IIG", "INI", "GGG"):
         run = EmuRun(N, M, code, sizes, B)
         run.set_grads(1, kind=kind)
         stats = run.step(1)
-        assert stats["nonfinite"] == (1 if kind in ("specials", "nearmax") else 0)
+        assert stats["nonfinite"] == expect_nonfinite
         _check_against_dp(run, lay, ref)
         run.close()
 
