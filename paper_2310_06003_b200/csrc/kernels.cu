@@ -91,7 +91,7 @@ __device__ bool grid_peer_barrier(const RoundsArgs& a, uint64_t peers, int bidx)
   if (threadIdx.x == 0) {
     int ok = 1;
     volatile int* err = a.bar.err;
-    __threadfence();
+    __threadfence_system();   // this CTA's stores (incl. remote NVLink stores) are visible system-wide
     const unsigned long long target = a.arrive_base + (unsigned long long)(bidx + 1) * gridDim.x;
     const unsigned long long old = atomicAdd(a.bar.arrive, 1ull);
     const uint64_t val = a.serial * 256ull + (uint64_t)bidx + 1ull;

@@ -198,16 +198,26 @@ paro_status_t upload_schedule(PlanT* p) {
       rounds.push_back(d);
     }
     dl.nrounds = R;
-    dl.final_barrier = L.final_barrier ? 1 : 0;
+    dl.final_barrier = (L.final_barrier || L.final_all) ? 1 : 0;
     // bytes sent by the local rank(s): what peers read from them in this launch
     for (int r = 0; r < R; ++r)
       for (int x = 0; x < pl.N; ++x)
-        for (const Task& t : L.rounds[r][x])
+        for (const Task& t : L.rounds[r][x]) {
           for (int i = 0; i < t.nin; ++i) {
             const int y = t.in[i].rank;
             if (y != x && (ctx->mode != MODE_REAL || y == ctx->rank)) dl.bytes += 2 * t.n;
           }
-    dl.final_peers = (ctx->mode == MODE_REAL) ? L.barrier_peers(R, ctx->rank) : 0;
+          if (t.dst.rank != x && (ctx->mode != MODE_REAL || x == ctx->rank)) dl.bytes += 2 * t.n;
+        }
+    dl.final_peers = 0;
+    if (ctx->mode == MODE_REAL) {
+      if (L.final_all) {
+        for (int x = 0; x < pl.N; ++x)
+          if (x != ctx->rank) dl.final_peers |= uint64_t(1) << x;
+      } else {
+        dl.final_peers = L.barrier_peers(R, ctx->rank);
+      }
+    }
     return dl;
   };
   p->red.clear();
@@ -367,6 +377,7 @@ void paro_opts_default(paro_opts_t* o) {
   o->loss_scale = 1.0f;
   o->comm_ctas = 64;
   o->pipeline_depth = 2;
+  o->pull_transport = 0;
   o->stream = nullptr;
 }
 
@@ -478,6 +489,7 @@ paro_status_t paro_plan(paro_ctx_t ctx, const char* strategy, const int64_t* par
   po.bucket_elems = o.bucket_elems > 0 ? o.bucket_elems : (int64_t(1) << 26);
   po.topology = o.topology;
   po.pipeline_depth = o.pipeline_depth > 0 ? o.pipeline_depth : 2;
+  po.push = o.pull_transport == 0;
   auto* p = new PlanT();
   p->ctx = ctx;
   p->opts = o;

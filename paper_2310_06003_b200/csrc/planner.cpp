@@ -54,67 +54,119 @@ Task make_task(int64_t n, std::initializer_list<Ref> ins, Ref dst) {
   return t;
 }
 
-// Ring reduce-scatter body over `ranks` (k members): emits the non-final hops
-// 0..k-3 at rounds round0 + h and returns each member's final-hop inputs.
-std::vector<FinalIn> ring_rs_body(Launch& L, const std::vector<int>& ranks, const PieceFn& pieces,
-                                  const ContribFn& contrib, const BaseFn& stage, int round0) {
+// Ring reduce-scatter body over `ranks` (k members).
+//  pull: member q READS its predecessor's partial (or raw contribution at the
+//        first hop) and writes locally; non-final hops at round0 + t, t <= k-3;
+//        the final hop may run from round0 + k - 2.
+//  push: member q combines the partial its predecessor WROTE into q's stage
+//        with its own contribution and STORES the result into its successor's
+//        stage; hops at round0 + t, t <= k-2; the final (local) fold may run
+//        from round0 + k - 1.
+// Either way block c's chain is c+1, c+2, ..., c (canonical order R2).
+struct RingBody {
+  std::vector<FinalIn> fin;
+  int final_off = 0;   // earliest final-fold round, relative to round0
+};
+
+RingBody ring_rs_body(Launch& L, bool push, const std::vector<int>& ranks, const PieceFn& pieces,
+                      const ContribFn& contrib, const BaseFn& stage, int round0) {
   const int k = (int)ranks.size();
-  for (int t = 0; t + 2 < k; ++t) {
-    for (int q = 0; q < k; ++q) {
-      const int c = ((q - t - 2) % k + k) % k;
-      const int pred = (q - 1 + k) % k;
-      for (const Piece& pc : pieces(c)) {
-        Ref in0 = (t == 0) ? contrib(pred, c, pc) : at(stage(pred, (t - 1) % 2), pc.blk_off);
-        Ref in1 = contrib(q, c, pc);
-        L.add(round0 + t, ranks[q], make_task(pc.len, {in0, in1}, at(stage(q, t % 2), pc.blk_off)));
+  RingBody rb;
+  rb.fin.resize(k);
+  if (k == 1) {
+    rb.fin[0].pieces = pieces(0);
+    for (const Piece& pc : rb.fin[0].pieces) {
+      rb.fin[0].pin.push_back(Ref{});
+      rb.fin[0].own.push_back(contrib(0, 0, pc));
+    }
+    rb.final_off = 0;
+    return rb;
+  }
+  if (!push) {
+    for (int t = 0; t + 2 < k; ++t) {
+      for (int q = 0; q < k; ++q) {
+        const int c = ((q - t - 2) % k + k) % k;
+        const int pred = (q - 1 + k) % k;
+        for (const Piece& pc : pieces(c)) {
+          Ref in0 = (t == 0) ? contrib(pred, c, pc) : at(stage(pred, (t - 1) % 2), pc.blk_off);
+          L.add(round0 + t, ranks[q], make_task(pc.len, {in0, contrib(q, c, pc)}, at(stage(q, t % 2), pc.blk_off)));
+        }
       }
     }
-  }
-  std::vector<FinalIn> fin(k);
-  for (int q = 0; q < k; ++q) {
-    const int pred = (q - 1 + k) % k;
-    fin[q].pieces = pieces(q);
-    for (const Piece& pc : fin[q].pieces) {
-      Ref pin;
-      if (k == 2) pin = contrib(pred, q, pc);
-      else if (k > 2) pin = at(stage(pred, (k - 3) % 2), pc.blk_off);
-      fin[q].pin.push_back(pin);
-      fin[q].own.push_back(contrib(q, q, pc));
+    for (int q = 0; q < k; ++q) {
+      const int pred = (q - 1 + k) % k;
+      rb.fin[q].pieces = pieces(q);
+      for (const Piece& pc : rb.fin[q].pieces) {
+        rb.fin[q].pin.push_back(k == 2 ? contrib(pred, q, pc) : at(stage(pred, (k - 3) % 2), pc.blk_off));
+        rb.fin[q].own.push_back(contrib(q, q, pc));
+      }
     }
+    rb.final_off = k - 2;
+    return rb;
   }
-  return fin;
-}
-
-// Plain ring RS: body + final hop at round0 + k - 2 into dest(q) (block space).
-void ring_rs(Launch& L, const std::vector<int>& ranks, const PieceFn& pieces, const ContribFn& contrib,
-             const BaseFn& stage, const std::function<Ref(int q)>& dest, int round0) {
-  const int k = (int)ranks.size();
-  auto fin = ring_rs_body(L, ranks, pieces, contrib, stage, round0);
-  const int rf = round0 + std::max(0, k - 2);
-  for (int q = 0; q < k; ++q) {
-    for (size_t i = 0; i < fin[q].pieces.size(); ++i) {
-      const Piece& pc = fin[q].pieces[i];
-      Ref d = at(dest(q), pc.blk_off);
-      const Ref& own = fin[q].own[i];
-      if (k == 1 && own.rank == d.rank && own.kind == d.kind && own.off == d.off) continue;
-      L.add(rf, ranks[q], make_task(pc.len, {fin[q].pin[i], own}, d));
-    }
-  }
-}
-
-// Ring all-gather in place: member q owns block q in base(q); round t copies
-// block (q-1-t) from the predecessor (P:358 ring order, pull form).
-void ring_ag(Launch& L, const std::vector<int>& ranks, const PieceFn& pieces,
-             const std::function<Ref(int q)>& base, int round0) {
-  const int k = (int)ranks.size();
   for (int t = 0; t + 1 < k; ++t) {
     for (int q = 0; q < k; ++q) {
       const int c = ((q - 1 - t) % k + k) % k;
-      const int pred = (q - 1 + k) % k;
-      for (const Piece& pc : pieces(c))
-        L.add(round0 + t, ranks[q], make_task(pc.len, {at(base(pred), pc.src_off)}, at(base(q), pc.src_off)));
+      const int succ = (q + 1) % k;
+      for (const Piece& pc : pieces(c)) {
+        Ref d = at(stage(succ, t % 2), pc.blk_off);
+        if (t == 0) L.add(round0, ranks[q], make_task(pc.len, {contrib(q, c, pc)}, d));
+        else L.add(round0 + t, ranks[q], make_task(pc.len, {at(stage(q, (t - 1) % 2), pc.blk_off), contrib(q, c, pc)}, d));
+      }
     }
   }
+  for (int q = 0; q < k; ++q) {
+    rb.fin[q].pieces = pieces(q);
+    for (const Piece& pc : rb.fin[q].pieces) {
+      rb.fin[q].pin.push_back(at(stage(q, (k - 2) % 2), pc.blk_off));
+      rb.fin[q].own.push_back(contrib(q, q, pc));
+    }
+  }
+  rb.final_off = k - 1;
+  return rb;
+}
+
+// Plain ring RS: body + final fold into dest(q) (block space).  Returns rounds used.
+int ring_rs(Launch& L, bool push, const std::vector<int>& ranks, const PieceFn& pieces,
+            const ContribFn& contrib, const BaseFn& stage, const std::function<Ref(int q)>& dest, int round0) {
+  const int k = (int)ranks.size();
+  RingBody rb = ring_rs_body(L, push, ranks, pieces, contrib, stage, round0);
+  bool any = false;
+  for (int q = 0; q < k; ++q) {
+    for (size_t i = 0; i < rb.fin[q].pieces.size(); ++i) {
+      const Piece& pc = rb.fin[q].pieces[i];
+      Ref d = at(dest(q), pc.blk_off);
+      const Ref& own = rb.fin[q].own[i];
+      if (k == 1 && own.rank == d.rank && own.kind == d.kind && own.off == d.off) continue;
+      L.add(round0 + rb.final_off, ranks[q], make_task(pc.len, {rb.fin[q].pin[i], own}, d));
+      any = true;
+    }
+  }
+  return (k == 1 && !any) ? 0 : rb.final_off + 1;
+}
+
+// Ring all-gather in place: member q owns block q in base(q).
+//  pull: round t, q copies block (q-1-t) from its predecessor;
+//  push: round t, q stores block (q-t) into its successor.  Returns k - 1.
+int ring_ag(Launch& L, bool push, const std::vector<int>& ranks, const PieceFn& pieces,
+            const std::function<Ref(int q)>& base, int round0) {
+  const int k = (int)ranks.size();
+  for (int t = 0; t + 1 < k; ++t) {
+    for (int q = 0; q < k; ++q) {
+      if (!push) {
+        const int c = ((q - 1 - t) % k + k) % k;
+        const int pred = (q - 1 + k) % k;
+        for (const Piece& pc : pieces(c))
+          L.add(round0 + t, ranks[q], make_task(pc.len, {at(base(pred), pc.src_off)}, at(base(q), pc.src_off)));
+      } else {
+        const int c = ((q - t) % k + k) % k;
+        const int succ = (q + 1) % k;
+        for (const Piece& pc : pieces(c))
+          L.add(round0 + t, ranks[q], make_task(pc.len, {at(base(q), pc.src_off)}, at(base(succ), pc.src_off)));
+      }
+    }
+  }
+  return k - 1;
 }
 
 }  // namespace
@@ -126,12 +178,16 @@ void Launch::add(int round, int rank, const Task& t) {
 }
 
 std::vector<int> Launch::reads(int r, int rank) const {
+  // every other rank whose memory `rank` reads (pull) or writes (push) in round r
   std::vector<int> out;
   if (r < 0 || r >= (int)rounds.size()) return out;
-  for (const Task& t : rounds[r][rank])
-    for (int i = 0; i < t.nin; ++i)
-      if (t.in[i].rank != rank && std::find(out.begin(), out.end(), t.in[i].rank) == out.end())
-        out.push_back(t.in[i].rank);
+  auto add = [&](int x) {
+    if (x != rank && std::find(out.begin(), out.end(), x) == out.end()) out.push_back(x);
+  };
+  for (const Task& t : rounds[r][rank]) {
+    for (int i = 0; i < t.nin; ++i) add(t.in[i].rank);
+    add(t.dst.rank);
+  }
   return out;
 }
 
@@ -249,6 +305,7 @@ void Planner::layout() {
   stage_e_len = C;
   p1_len = B / M;
   sown_len = C;
+  land_len = int64_t(M - 1) * (B / M) + int64_t(g - 1) * C;
   buf_len[BUF_GRAD] = psi_pad;
   buf_len[BUF_PARAM] = p_numel;
   buf_len[BUF_GSHARD] = g_numel;
@@ -257,6 +314,7 @@ void Planner::layout() {
   buf_len[BUF_STAGE_E] = (N > 1) ? 4 * stage_e_len : 0;
   buf_len[BUF_P1] = (N > 1) ? 2 * p1_len : 0;
   buf_len[BUF_SOWN] = (N > 1) ? 2 * sown_len : 0;
+  buf_len[BUF_LAND] = (N > 1 && opt.topology == 3 && opt.push) ? 2 * land_len : 0;
   int64_t off = 0;
   for (int k = 0; k < BUF_NKINDS; ++k) {
     buf_off[k] = off;
@@ -280,6 +338,7 @@ void Planner::build_schedule() {
   }
   if (OS != P) rest_ops = {OS == LV_G ? (P == LV_I ? "AG_E" : "HO_AG") : "AG_I"};
 
+  const bool push = opt.push;
   for (size_t b = 0; b < buckets.size(); ++b) {
     BucketSchedule& S = sched[b];
     const int64_t s = buckets[b].first, n = buckets[b].second;
@@ -319,232 +378,302 @@ void Planner::build_schedule() {
     };
     auto one = [](int64_t off, int64_t len) { return std::vector<Piece>{{off, len, 0}}; };
 
-    // ---- world-reaching RS producing g_hat segments at dest_seg (G in {N, G})
-    auto emit_world_rs = [&](Launch& L) -> int {   // returns rounds used
+    auto land_i = [&](int r, int slot) {
+      return Ref{r, BUF_LAND, int64_t(par) * land_len + int64_t(slot) * chunk};
+    };
+    auto land_e = [&](int r, int slot) {
+      return Ref{r, BUF_LAND, int64_t(par) * land_len + int64_t(M - 1) * chunk + int64_t(slot) * C};
+    };
+    // foreign-group segments of chunk c for group j: 1 or 2 contiguous pieces
+    auto foreign_pieces = [&](int j, int c) {
+      std::vector<Piece> v;
+      const int64_t base = int64_t(c) * g * C;
+      if (j > 0) v.push_back({base, int64_t(j) * C, 0});
+      if (j < g - 1) v.push_back({base + int64_t(j + 1) * C, int64_t(g - 1 - j) * C, int64_t(j) * C});
+      return v;
+    };
+
+    // ---- world-reaching RS producing g_hat segments at dest_seg (G in {N, G}).
+    // Returns rounds used.
+    auto emit_world_rs = [&](Launch& L, int round0) -> int {
       if (topo == 0) {  // HO-Ring RS (R16/R17)
-        const int R1 = (g > 1 && M > 1) ? M - 1 : 0;
-        const int R2 = std::max(M - 1, g - 1);
-        if (R1 > 0) {
+        int R1 = 0;
+        if (g > 1 && M > 1) {   // phase 1: intra ring RS of the foreign-group segments
           for (int j = 0; j < g; ++j) {
-            auto pieces = [&, j](int c) {
-              std::vector<Piece> v;
-              const int64_t base = int64_t(c) * g * C;
-              if (j > 0) v.push_back({base, int64_t(j) * C, 0});
-              if (j < g - 1) v.push_back({base + int64_t(j + 1) * C, int64_t(g - 1 - j) * C, int64_t(j) * C});
-              return v;
-            };
             auto gr = group_ranks(j);
-            ring_rs(L, gr, pieces, [&, gr](int q, int, const Piece& pc) { return grad(gr[q], pc.src_off); },
-                    [&, gr](int q, int slot) { return stage_i(gr[q], slot); },
-                    [&, gr](int q) { return p1(gr[q]); }, 0);
+            R1 = ring_rs(L, push, gr, [&, j](int c) { return foreign_pieces(j, c); },
+                         [&, gr](int q, int, const Piece& pc) { return grad(gr[q], pc.src_off); },
+                         [&, gr](int q, int slot) { return stage_i(gr[q], slot); },
+                         [&, gr](int q) { return p1(gr[q]); }, round0);
           }
         }
-        // phase 2: inter ring (i) concurrent with intra own-segment ring (ii)
+        // phase 2: inter ring (i) concurrent with the intra own-segment ring (ii)
         std::vector<FinalIn> intra_fin(N), inter_fin(N);
+        int off_i = 0, off_e = 0;
         if (M > 1) {
           for (int j = 0; j < g; ++j) {
             auto gr = group_ranks(j);
-            auto fin = ring_rs_body(L, gr, [&, j](int c) { return one(int64_t(seg(j, c)) * C, C); },
-                                    [&, gr](int q, int, const Piece& pc) { return grad(gr[q], pc.src_off); },
-                                    [&, gr](int q, int slot) { return stage_i(gr[q], slot); }, R1);
-            for (int q = 0; q < M; ++q) intra_fin[gr[q]] = fin[q];
+            auto rb = ring_rs_body(L, push, gr, [&, j](int c) { return one(int64_t(seg(j, c)) * C, C); },
+                                   [&, gr](int q, int, const Piece& pc) { return grad(gr[q], pc.src_off); },
+                                   [&, gr](int q, int slot) { return stage_i(gr[q], slot); }, round0 + R1);
+            off_i = rb.final_off;
+            for (int q = 0; q < M; ++q) intra_fin[gr[q]] = rb.fin[q];
           }
         }
         if (g > 1) {
           for (int p = 0; p < M; ++p) {
             auto pr = pos_ranks(p);
             auto contrib = [&, pr, p](int q, int c, const Piece&) {
-              if (M > 1) return at(p1(pr[q]), int64_t(c < q ? c : c - 1) * C);
-              return grad(pr[q], int64_t(seg(c, p)) * C);
+              if (M > 1 && c != q) return at(p1(pr[q]), int64_t(c < q ? c : c - 1) * C);
+              return grad(pr[q], int64_t(seg(c, p)) * C);   // M == 1, or the own segment
             };
-            // non-final inter hops at rounds R1 + h (h <= g-3); the final hop is emitted below
-            auto fin = ring_rs_body(L, pr, [&](int) { return one(0, C); }, contrib,
-                                    [&, pr](int q, int slot) { return stage_e(pr[q], slot); }, R1);
-            for (int q = 0; q < g; ++q) inter_fin[pr[q]] = fin[q];
+            auto rb = ring_rs_body(L, push, pr, [&](int) { return one(0, C); }, contrib,
+                                   [&, pr](int q, int slot) { return stage_e(pr[q], slot); }, round0 + R1);
+            off_e = rb.final_off;
+            for (int q = 0; q < g; ++q) inter_fin[pr[q]] = rb.fin[q];
           }
         }
-        const int rlast = R1 + R2 - 1;
+        const int rf = round0 + R1 + std::max(off_i, off_e);
         for (int r = 0; r < N; ++r) {
           Ref d = dest_seg(r);
           if (g == 1) {
-            L.add(rlast, r, make_task(C, {intra_fin[r].pin[0], intra_fin[r].own[0]}, d));
+            L.add(rf, r, make_task(C, {intra_fin[r].pin[0], intra_fin[r].own[0]}, d));
           } else if (M == 1) {
-            L.add(rlast, r, make_task(C, {inter_fin[r].pin[0], grad(r, int64_t(seg(grp(r), 0)) * C)}, d));
-          } else if (M - 1 == R2) {   // fused: ((intra_in (+) x_own) (+) inter_in)
-            L.add(rlast, r, make_task(C, {intra_fin[r].pin[0], intra_fin[r].own[0], inter_fin[r].pin[0]}, d));
-          } else {                    // intra ring finished earlier: stash S, combine last
-            L.add(R1 + M - 2, r, make_task(C, {intra_fin[r].pin[0], intra_fin[r].own[0]}, sown(r)));
-            L.add(rlast, r, make_task(C, {inter_fin[r].pin[0], sown(r)}, d));
+            L.add(rf, r, make_task(C, {inter_fin[r].pin[0], inter_fin[r].own[0]}, d));
+          } else if (round0 + R1 + off_i == rf) {   // fused: ((intra_in (+) x_own) (+) inter_in)
+            L.add(rf, r, make_task(C, {intra_fin[r].pin[0], intra_fin[r].own[0], inter_fin[r].pin[0]}, d));
+          } else {   // intra ring finished earlier: stash S_j, combine it last
+            L.add(round0 + R1 + off_i, r, make_task(C, {intra_fin[r].pin[0], intra_fin[r].own[0]}, sown(r)));
+            L.add(rf, r, make_task(C, {inter_fin[r].pin[0], sown(r)}, d));
           }
         }
-        return R1 + R2;
+        return rf - round0 + 1;
       }
       if (topo == 1) {  // two-step: RS_I into P1, then RS_E
+        int r1 = 0;
         for (int j = 0; j < g; ++j) {
           auto gr = group_ranks(j);
-          ring_rs(L, gr, [&](int c) { return one(int64_t(c) * chunk, chunk); },
-                  [&, gr](int q, int, const Piece& pc) { return grad(gr[q], pc.src_off); },
-                  [&, gr](int q, int slot) { return stage_i(gr[q], slot); },
-                  [&, gr](int q) { return p1(gr[q]); }, 0);
+          r1 = ring_rs(L, push, gr, [&](int c) { return one(int64_t(c) * chunk, chunk); },
+                       [&, gr](int q, int, const Piece& pc) { return grad(gr[q], pc.src_off); },
+                       [&, gr](int q, int slot) { return stage_i(gr[q], slot); },
+                       [&, gr](int q) { return p1(gr[q]); }, round0);
         }
-        const int r0 = std::max(1, M - 1);
+        int r2 = 0;
         for (int p = 0; p < M; ++p) {
           auto pr = pos_ranks(p);
-          ring_rs(L, pr, [&](int c) { return one(int64_t(c) * C, C); },
-                  [&, pr](int q, int, const Piece& pc) { return at(p1(pr[q]), pc.src_off); },
-                  [&, pr](int q, int slot) { return stage_e(pr[q], slot); },
-                  [&, pr](int q) { return dest_seg(pr[q]); }, r0);
+          r2 = ring_rs(L, push, pr, [&](int c) { return one(int64_t(c) * C, C); },
+                       [&, pr](int q, int, const Piece& pc) { return at(p1(pr[q]), pc.src_off); },
+                       [&, pr](int q, int slot) { return stage_e(pr[q], slot); },
+                       [&, pr](int q) { return dest_seg(pr[q]); }, round0 + r1);
         }
-        return r0 + std::max(1, g - 1);
+        return r1 + r2;
       }
       if (topo == 2) {  // flat ring over all ranks
         std::vector<int> all;
         for (int r = 0; r < N; ++r) all.push_back(r);
-        ring_rs(L, all, [&](int c) { return one(int64_t(seg(grp(c), pos(c))) * C, C); },
-                [&](int q, int, const Piece& pc) { return grad(q, pc.src_off); },
-                [&](int q, int slot) { return stage_i(q, slot); }, [&](int q) { return dest_seg(q); }, 0);
-        return N - 1;
+        return ring_rs(L, push, all, [&](int c) { return one(int64_t(seg(grp(c), pos(c))) * C, C); },
+                       [&](int q, int, const Piece& pc) { return grad(q, pc.src_off); },
+                       [&](int q, int slot) { return stage_i(q, slot); }, [&](int q) { return dest_seg(q); },
+                       round0);
       }
-      // topo == 3: direct hierarchical one-shot (NVSwitch): same canonical order
-      int rr = 0;
+      // topo == 3: direct hierarchical (NVSwitch all-to-all): same canonical order.
+      // Intra: S_j[chunk p] = R_M(p; x_(j,p+1), ..., x_(j,p)); inter: R_g(j; S_(j+1), ..., S_j).
+      int rr = round0;
       if (M > 1) {
-        for (int r = 0; r < N; ++r) {
-          const int j = grp(r), p = pos(r);
-          Task t;
-          t.n = (g == 1) ? C : chunk;
-          t.nin = M;
-          for (int i = 0; i < M; ++i) {   // R_M(p; ...): p+1, p+2, ..., p
-            const int pp = (p + 1 + i) % M;
-            t.in[i] = grad(rank_of(j, pp), int64_t(p) * chunk);
+        const int64_t n1 = (g == 1) ? C : chunk;
+        if (!push) {
+          for (int r = 0; r < N; ++r) {
+            const int j = grp(r), p = pos(r);
+            Task t;
+            t.n = n1;
+            t.nin = M;
+            for (int i = 0; i < M; ++i) t.in[i] = grad(rank_of(j, (p + 1 + i) % M), int64_t(p) * chunk);
+            t.dst = (g == 1) ? dest_seg(r) : p1(r);
+            L.add(rr, r, t);
           }
-          t.dst = (g == 1) ? dest_seg(r) : p1(r);
-          L.add(0, r, t);
+          rr += 1;
+        } else {
+          for (int r = 0; r < N; ++r) {     // every rank stores its chunk-p share into owner p's landing slot
+            const int j = grp(r), pp = pos(r);
+            for (int p = 0; p < M; ++p) {
+              if (p == pp) continue;
+              const int slot = ((pp - p - 1) % M + M) % M;
+              L.add(rr, r, make_task(n1, {grad(r, int64_t(p) * chunk)}, land_i(rank_of(j, p), slot)));
+            }
+          }
+          for (int r = 0; r < N; ++r) {     // owner folds the landed shares in canonical order
+            const int p = pos(r);
+            Task t;
+            t.n = n1;
+            t.nin = M;
+            for (int i = 0; i < M - 1; ++i) t.in[i] = land_i(r, i);
+            t.in[M - 1] = grad(r, int64_t(p) * chunk);
+            t.dst = (g == 1) ? dest_seg(r) : p1(r);
+            L.add(rr + 1, r, t);
+          }
+          rr += 2;
         }
-        rr = 1;
       }
       if (g > 1) {
-        for (int r = 0; r < N; ++r) {
-          const int j = grp(r), p = pos(r);
-          Task t;
-          t.n = C;
-          t.nin = g;
-          for (int i = 0; i < g; ++i) {   // R_g(j; ...): j+1, ..., j
-            const int jj = (j + 1 + i) % g;
-            t.in[i] = (M > 1) ? at(p1(rank_of(jj, p)), int64_t(j) * C)
-                              : grad(rank_of(jj, p), int64_t(seg(j, p)) * C);
+        auto spart = [&](int r, int jj) {   // group partial of segment (jj, p) held by r = (j, p)
+          return (M > 1) ? at(p1(r), int64_t(jj) * C) : grad(r, int64_t(seg(jj, pos(r))) * C);
+        };
+        if (!push) {
+          for (int r = 0; r < N; ++r) {
+            const int j = grp(r), p = pos(r);
+            Task t;
+            t.n = C;
+            t.nin = g;
+            for (int i = 0; i < g; ++i) t.in[i] = spart(rank_of((j + 1 + i) % g, p), j);
+            t.dst = dest_seg(r);
+            L.add(rr, r, t);
           }
-          t.dst = dest_seg(r);
-          L.add(rr, r, t);
+          rr += 1;
+        } else {
+          for (int r = 0; r < N; ++r) {
+            const int j = grp(r), p = pos(r);
+            for (int jo = 0; jo < g; ++jo) {
+              if (jo == j) continue;
+              const int slot = ((j - jo - 1) % g + g) % g;
+              L.add(rr, r, make_task(C, {spart(r, jo)}, land_e(rank_of(jo, p), slot)));
+            }
+          }
+          for (int r = 0; r < N; ++r) {
+            const int j = grp(r);
+            Task t;
+            t.n = C;
+            t.nin = g;
+            for (int i = 0; i < g - 1; ++i) t.in[i] = land_e(r, i);
+            t.in[g - 1] = spart(r, j);
+            t.dst = dest_seg(r);
+            L.add(rr + 1, r, t);
+          }
+          rr += 2;
         }
-        rr += 1;
       }
-      return rr;
+      return rr - round0;
     };
 
-    // ---- world-reaching AG of segments in place in a bucket-layout buffer
-    auto emit_world_ag = [&](Launch& L, const std::function<Ref(int)>& base, int round0) {
+    // ---- world-reaching AG of segments in place in a bucket-layout buffer.  Returns rounds used.
+    auto emit_world_ag = [&](Launch& L, const std::function<Ref(int)>& base, int round0) -> int {
       if (topo == 0) {  // HO-Ring AG
         for (int j = 0; j < g; ++j) {
           auto gr = group_ranks(j);
-          ring_ag(L, gr, [&, j](int c) { return one(int64_t(seg(j, c)) * C, C); },
+          ring_ag(L, push, gr, [&, j](int c) { return one(int64_t(seg(j, c)) * C, C); },
                   [&, gr](int q) { return base(gr[q]); }, round0);
         }
         for (int p = 0; p < M; ++p) {
           auto pr = pos_ranks(p);
-          ring_ag(L, pr, [&, p](int c) { return one(int64_t(seg(c, p)) * C, C); },
+          ring_ag(L, push, pr, [&, p](int c) { return one(int64_t(seg(c, p)) * C, C); },
                   [&, pr](int q) { return base(pr[q]); }, round0);
         }
+        const int ra = std::max(M - 1, g - 1);
         if (g > 1 && M > 1) {
-          const int rb = round0 + std::max(M - 1, g - 1);
           for (int j = 0; j < g; ++j) {
             auto gr = group_ranks(j);
-            auto pieces = [&, j](int c) {
-              std::vector<Piece> v;
-              const int64_t cb = int64_t(c) * g * C;
-              if (j > 0) v.push_back({cb, int64_t(j) * C, 0});
-              if (j < g - 1) v.push_back({cb + int64_t(j + 1) * C, int64_t(g - 1 - j) * C, 0});
-              return v;
-            };
-            ring_ag(L, gr, pieces, [&, gr](int q) { return base(gr[q]); }, rb);
+            ring_ag(L, push, gr, [&, j](int c) { auto v = foreign_pieces(j, c); for (auto& pc : v) pc.blk_off = 0; return v; },
+                    [&, gr](int q) { return base(gr[q]); }, round0 + ra);
           }
+          return ra + M - 1;
         }
-      } else if (topo == 1) {  // AG_E then AG_I
+        return ra;
+      }
+      if (topo == 1) {  // AG_E then AG_I
         for (int p = 0; p < M; ++p) {
           auto pr = pos_ranks(p);
-          ring_ag(L, pr, [&, p](int c) { return one(int64_t(seg(c, p)) * C, C); },
+          ring_ag(L, push, pr, [&, p](int c) { return one(int64_t(seg(c, p)) * C, C); },
                   [&, pr](int q) { return base(pr[q]); }, round0);
         }
         for (int j = 0; j < g; ++j) {
           auto gr = group_ranks(j);
-          ring_ag(L, gr, [&](int c) { return one(int64_t(c) * chunk, chunk); },
+          ring_ag(L, push, gr, [&](int c) { return one(int64_t(c) * chunk, chunk); },
                   [&, gr](int q) { return base(gr[q]); }, round0 + (g - 1));
         }
-      } else if (topo == 2) {
+        return (g - 1) + (M - 1);
+      }
+      if (topo == 2) {
         std::vector<int> all;
         for (int r = 0; r < N; ++r) all.push_back(r);
-        ring_ag(L, all, [&](int c) { return one(int64_t(seg(grp(c), pos(c))) * C, C); }, base, round0);
-      } else {  // direct: inter segments, then intra chunks
-        int rr = round0;
-        if (g > 1) {
-          for (int r = 0; r < N; ++r) {
-            const int j = grp(r), p = pos(r);
-            for (int x = 0; x < g; ++x) {
-              if (x == j) continue;
+        return ring_ag(L, push, all, [&](int c) { return one(int64_t(seg(grp(c), pos(c))) * C, C); }, base,
+                       round0);
+      }
+      // direct: inter segments, then intra chunks
+      int rr = round0;
+      if (g > 1) {
+        for (int r = 0; r < N; ++r) {
+          const int j = grp(r), p = pos(r);
+          for (int x = 0; x < g; ++x) {
+            if (x == j) continue;
+            if (!push) {
               const int64_t o = int64_t(seg(x, p)) * C;
               L.add(rr, r, make_task(C, {at(base(rank_of(x, p)), o)}, at(base(r), o)));
+            } else {
+              const int64_t o = int64_t(seg(j, p)) * C;
+              L.add(rr, r, make_task(C, {at(base(r), o)}, at(base(rank_of(x, p)), o)));
             }
           }
-          ++rr;
         }
-        if (M > 1) {
-          for (int r = 0; r < N; ++r) {
-            const int j = grp(r), p = pos(r);
-            for (int c = 0; c < M; ++c) {
-              if (c == p) continue;
+        ++rr;
+      }
+      if (M > 1) {
+        for (int r = 0; r < N; ++r) {
+          const int j = grp(r), p = pos(r);
+          for (int c = 0; c < M; ++c) {
+            if (c == p) continue;
+            if (!push) {
               const int64_t o = int64_t(c) * chunk;
               L.add(rr, r, make_task(chunk, {at(base(rank_of(j, c)), o)}, at(base(r), o)));
+            } else {
+              const int64_t o = int64_t(p) * chunk;
+              L.add(rr, r, make_task(chunk, {at(base(r), o)}, at(base(rank_of(j, c)), o)));
             }
           }
         }
+        ++rr;
       }
+      return rr - round0;
     };
     // AG_E in place in a chunk-layout buffer (segment j of chunk p at j*C)
-    auto emit_ag_e = [&](Launch& L, const std::function<Ref(int)>& base, int round0) {
+    auto emit_ag_e = [&](Launch& L, const std::function<Ref(int)>& base, int round0) -> int {
+      int used = 0;
       for (int p = 0; p < M; ++p) {
         auto pr = pos_ranks(p);
-        ring_ag(L, pr, [&](int c) { return one(int64_t(c) * C, C); }, [&, pr](int q) { return base(pr[q]); },
-                round0);
+        used = ring_ag(L, push, pr, [&](int c) { return one(int64_t(c) * C, C); },
+                       [&, pr](int q) { return base(pr[q]); }, round0);
       }
+      return used;
     };
-    auto emit_ag_i = [&](Launch& L, const std::function<Ref(int)>& base, int round0) {
+    auto emit_ag_i = [&](Launch& L, const std::function<Ref(int)>& base, int round0) -> int {
+      int used = 0;
       for (int j = 0; j < g; ++j) {
         auto gr = group_ranks(j);
-        ring_ag(L, gr, [&](int c) { return one(int64_t(c) * chunk, chunk); },
-                [&, gr](int q) { return base(gr[q]); }, round0);
+        used = ring_ag(L, push, gr, [&](int c) { return one(int64_t(c) * chunk, chunk); },
+                       [&, gr](int q) { return base(gr[q]); }, round0);
       }
+      return used;
     };
 
     if (N > 1 && topo != 4) {
       Launch& L = S.reduce;
       if (G == LV_I) {
+        int r1 = 0, r2 = 0;
         for (int j = 0; j < g; ++j) {   // RS_I into the G residency
           auto gr = group_ranks(j);
-          ring_rs(L, gr, [&](int c) { return one(int64_t(c) * chunk, chunk); },
-                  [&, gr](int q, int, const Piece& pc) { return grad(gr[q], pc.src_off); },
-                  [&, gr](int q, int slot) { return stage_i(gr[q], slot); },
-                  [&, gr](int q) { return gshard(gr[q], 0); }, 0);
+          r1 = ring_rs(L, push, gr, [&](int c) { return one(int64_t(c) * chunk, chunk); },
+                       [&, gr](int q, int, const Piece& pc) { return grad(gr[q], pc.src_off); },
+                       [&, gr](int q, int slot) { return stage_i(gr[q], slot); },
+                       [&, gr](int q) { return gshard(gr[q], 0); }, 0);
         }
-        const int r0 = std::max(1, M - 1);
         for (int p = 0; p < M; ++p) {   // RS_E; in place for OS = I (all-reduce)
           auto pr = pos_ranks(p);
-          ring_rs(L, pr, [&](int c) { return one(int64_t(c) * C, C); },
-                  [&, pr](int q, int, const Piece& pc) { return gshard(pr[q], pc.src_off); },
-                  [&, pr](int q, int slot) { return stage_e(pr[q], slot); },
-                  [&, pr](int q) { return dest_seg(pr[q]); }, r0);
+          r2 = ring_rs(L, push, pr, [&](int c) { return one(int64_t(c) * C, C); },
+                       [&, pr](int q, int, const Piece& pc) { return gshard(pr[q], pc.src_off); },
+                       [&, pr](int q, int slot) { return stage_e(pr[q], slot); },
+                       [&, pr](int q) { return dest_seg(pr[q]); }, r1);
         }
-        if (OS == LV_I) emit_ag_e(L, [&](int r) { return ghat_base(r); }, r0 + std::max(1, g - 1));
+        if (OS == LV_I) emit_ag_e(L, [&](int r) { return ghat_base(r); }, r1 + r2);
       } else {
-        int used = emit_world_rs(L);
+        int used = emit_world_rs(L, 0);
         if (OS == LV_I) emit_ag_e(L, [&](int r) { return ghat_base(r); }, used);
         if (OS == LV_N) emit_world_ag(L, [&](int r) { return ghat_base(r); }, used);
       }
@@ -562,6 +691,13 @@ void Planner::build_schedule() {
           if (any) kept.push_back(rnd);
         }
         Lp->rounds.swap(kept);
+        // a launch whose last round stores into peers ends with a barrier so the
+        // data has landed before the peer's next kernel reads it
+        if (!Lp->rounds.empty()) {
+          for (int r = 0; r < N; ++r)
+            for (const Task& t : Lp->rounds.back()[r])
+              if (t.dst.rank != r) Lp->final_barrier = true;
+        }
       }
     } else if (N > 1 && topo == 4) {  // NCCL comparator
       for (int r = 0; r < N; ++r) {
@@ -611,11 +747,12 @@ void Planner::build_schedule() {
       else S.param[r] = at(pb, int64_t(p) * chunk);                         // P = N, OS = I
     }
   }
-  // the last collective launch of a step ends with a barrier: afterwards no
-  // peer reads this rank's buffers, so the caller may overwrite gradients.
+  // the last collective launch of a step ends with a barrier among ALL ranks:
+  // afterwards no peer reads or writes this rank's buffers, so the caller may
+  // overwrite gradients and read parameters.
   for (int b = (int)sched.size() - 1; b >= 0; --b) {
-    if (!sched[b].gather.empty()) { sched[b].gather.final_barrier = true; break; }
-    if (!sched[b].reduce.empty()) { sched[b].reduce.final_barrier = true; break; }
+    if (!sched[b].gather.empty()) { sched[b].gather.final_all = true; break; }
+    if (!sched[b].reduce.empty()) { sched[b].reduce.final_all = true; break; }
   }
 }
 
@@ -657,12 +794,15 @@ void Planner::count_bytes() {
       n_rounds += (int)L->rounds.size();
       for (const auto& rnd : L->rounds)
         for (int x = 0; x < N; ++x)
-          for (const Task& t : rnd[x])
-            for (int i = 0; i < t.nin; ++i) {
+          for (const Task& t : rnd[x]) {
+            for (int i = 0; i < t.nin; ++i) {   // pull: y's bytes travel to x
               const int y = t.in[i].rank;
               if (y == x) continue;
               (grp(x) == grp(y) ? send_intra[y] : send_inter[y]) += 2 * t.n;
             }
+            const int z = t.dst.rank;            // push: x's bytes travel to z
+            if (z != x) (grp(x) == grp(z) ? send_intra[x] : send_inter[x]) += 2 * t.n;
+          }
     }
     // NCCL comparator: ring-algorithm volumes of each call (perf only)
     for (int r = 0; r < N && opt.topology == 4; ++r) {

@@ -27,6 +27,7 @@ enum BufKind : int {
   BUF_STAGE_E,     // inter-ring partials: 2 parities x 2 slots
   BUF_P1,          // HO phase-1 / direct phase-1 output: 2 parities
   BUF_SOWN,        // own-group partial (HO phase 2): 2 parities
+  BUF_LAND,        // direct push landing slots: 2 parities x ((M-1) chunks + (g-1) segments)
   BUF_NKINDS
 };
 
@@ -51,11 +52,12 @@ struct Task {
 // One collective launch = rounds; round r holds, for every rank, its tasks.
 struct Launch {
   std::vector<std::vector<std::vector<Task>>> rounds;  // [round][rank][task]
-  bool final_barrier = false;
+  bool final_barrier = false;   // barrier with the peers touched in the last round
+  bool final_all = false;       // barrier with every rank (end of the step)
   int n_ranks = 0;
   void add(int round, int rank, const Task& t);
   bool empty() const { return rounds.empty(); }
-  // ranks `rank` reads from in round r (excluding itself)
+  // other ranks whose memory `rank` reads or writes in round r
   std::vector<int> reads(int r, int rank) const;
   // symmetric barrier peer set before round r (r == rounds.size(): final)
   uint64_t barrier_peers(int r, int rank) const;
@@ -84,6 +86,7 @@ struct PlanOptions {
   int64_t bucket_elems = int64_t(1) << 26;
   int topology = 0;          // PARO_TOPO_*
   int pipeline_depth = 2;
+  bool push = true;          // push (remote stores) or pull (remote loads) transport
 };
 
 class Planner {
@@ -105,7 +108,7 @@ class Planner {
   int64_t buf_len[BUF_NKINDS] = {0};                   // elements per kind
   int64_t buf_off[BUF_NKINDS] = {0};                   // element offset in the region
   int64_t region_elems = 0;                            // symmetric region (bf16 elems)
-  int64_t stage_i_len = 0, stage_e_len = 0, p1_len = 0, sown_len = 0;
+  int64_t stage_i_len = 0, stage_e_len = 0, p1_len = 0, sown_len = 0, land_len = 0;
 
   std::vector<BucketSchedule> sched;
   std::vector<std::string> grad_ops, rest_ops;        // primitives (for reporting)

@@ -31,6 +31,7 @@ def main():
     splits = cfg.get("splits", [world])
     codes = cfg.get("codes", ["NNN", "IIG", "NIG", "IGG", "GGG", "III", "INI", "NNG"])
     topos = cfg.get("topos", ["ho", "two_step", "direct"])
+    transports = cfg.get("transports", ["push"])
     sizes = cfg.get("sizes", [world * 64 * 40 + 24, 333])
     B = cfg.get("bucket", world * 64 * 12)
     steps = cfg.get("steps", 2)
@@ -39,9 +40,9 @@ def main():
         t = torch.tensor(list(uid), dtype=torch.uint8)
         dist.broadcast(t, 0)
         ctx = paro.Context(world, M, mode="real", rank=rank, device=local, uid=bytes(t.tolist()))
-        for code in codes:
-            for topo in topos:
-                pl = paro.Plan(ctx, code, sizes, bucket_elems=B, topology=topo)
+        for code, topo, tr in [(c, t_, x) for c in codes for t_ in topos for x in transports]:
+            if True:
+                pl = paro.Plan(ctx, code, sizes, bucket_elems=B, topology=topo, transport=tr)
                 info = pl.info()
                 st = [torch.empty(info["os_numel"], dtype=torch.float32, device="cuda") for _ in range(3)]
                 ptrs = [[x.data_ptr() for x in st]]
@@ -54,7 +55,7 @@ def main():
                 torch.cuda.synchronize()
                 pbuf = torch.empty(info["p_numel"], dtype=torch.int16, device="cuda")
                 _copy(pbuf, pl.buffer(rank, 1))
-                tag = f"{M}_{code}_{topo}_r{rank}"
+                tag = f"{M}_{code}_{topo}_{tr}_r{rank}"
                 np.savez(os.path.join(out, tag + ".npz"), master=st[0].cpu().numpy(), m=st[1].cpu().numpy(),
                          v=st[2].cpu().numpy(), param=pbuf.cpu().numpy().view(np.uint16))
                 with open(os.path.join(out, tag + ".json"), "w") as f:

@@ -99,8 +99,8 @@ def test_send_bytes_match_oracle_simulator(N, M):
     w0 = master_f32(0, lay.psi)
     ctx = paro.Context(N, M)
     for code in S.paro_strategies():
-        for topo in ("ho", "two_step", "flat"):
-            pl = paro.Plan(ctx, code, sizes, bucket_elems=B, topology=topo)
+        for topo, tr in [(a, b) for a in ("ho", "two_step", "flat") for b in ("push", "pull")]:
+            pl = paro.Plan(ctx, code, sizes, bucket_elems=B, topology=topo, transport=tr)
             res = ST.strategy_step(code, lay, grads, ST.init_state(w0, lay, code), nm.AdamScalars(1e-3, 1),
                                    topology=topo)
             for r in range(N):
@@ -113,11 +113,12 @@ def test_send_bytes_match_oracle_simulator(N, M):
 def test_direct_topology_bytes_equal_closed_form(N, M):
     ctx = paro.Context(N, M)
     for code in S.paro_strategies():
-        pl = paro.Plan(ctx, code, [N * 64 * 16], bucket_elems=N * 64 * 4, topology="direct")
-        a, b = A.step_units_per_rank(code, N, M, N * 64 * 16)
-        for r in range(N):
-            assert pl.send_bytes(r) == (2 * a, 2 * b), code
-        pl.close()
+        for tr in ("push", "pull"):
+            pl = paro.Plan(ctx, code, [N * 64 * 16], bucket_elems=N * 64 * 4, topology="direct", transport=tr)
+            a, b = A.step_units_per_rank(code, N, M, N * 64 * 16)
+            for r in range(N):
+                assert pl.send_bytes(r) == (2 * a, 2 * b), code
+            pl.close()
     ctx.close()
 
 

@@ -40,7 +40,7 @@ def test_real_ranks_match_oracle(tmp_path):
     cfg = {"splits": splits, "steps": 2, "sizes": [world * 64 * 40 + 24, 333], "bucket": world * 64 * 12,
            "codes": ["NNN", "NNI", "NNG", "NII", "NIG", "NGG", "INI", "ING", "III", "IIG", "IGG", "GNG",
                      "GIG", "GGG"],
-           "topos": ["ho", "two_step", "direct"]}
+           "topos": ["ho", "two_step", "direct"], "transports": ["push", "pull"]}
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr=127.0.0.1", "--master-port=29517", os.path.join(ROOT, "tests", "dist_worker.py"),
            str(tmp_path), json.dumps(cfg)]
@@ -52,8 +52,9 @@ def test_real_ranks_match_oracle(tmp_path):
         norm = nm.grad_sq_sum(gh)
         for code in cfg["codes"]:
             for topo in cfg["topos"]:
+              for tr in cfg["transports"]:
                 for rank in range(world):
-                    tag = f"{M}_{code}_{topo}_r{rank}"
+                    tag = f"{M}_{code}_{topo}_{tr}_r{rank}"
                     d = np.load(tmp_path / (tag + ".npz"))
                     meta = json.load(open(tmp_path / (tag + ".json")))
                     assert np.array_equal(d["master"], ST.shard_of(w, lay, code[2], rank)), tag

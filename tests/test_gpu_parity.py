@@ -31,11 +31,11 @@ def _paro():
 class EmuRun:
     """All ranks of one split on cuda:0 through the C ABI."""
 
-    def __init__(self, N, M, code, sizes, B, topo="ho", depth=2, wd=0.0, loss_scale=1.0):
+    def __init__(self, N, M, code, sizes, B, topo="ho", depth=2, wd=0.0, loss_scale=1.0, transport="push"):
         paro = _paro()
         self.ctx = paro.Context(N, M, mode="emulated", device=0)
         self.pl = paro.Plan(self.ctx, code, sizes, bucket_elems=B, topology=topo, pipeline_depth=depth,
-                            weight_decay=wd, loss_scale=loss_scale)
+                            weight_decay=wd, loss_scale=loss_scale, transport=transport)
         self.info = self.pl.info()
         self.N, self.code, self.sizes = N, code, sizes
         n = self.info["os_numel"]
@@ -143,13 +143,14 @@ def test_n1_ten_steps_bit_exact(wd, ls):
 CONFIG_4M = dict(sizes=[1 << 22], B=1 << 18)   # BASELINE config 1: 2^22 params, 16 buckets
 
 
+@pytest.mark.parametrize("transport", ["push", "pull"])
 @pytest.mark.parametrize("topo", ["ho", "two_step", "direct"])
-def test_4m_2x4_every_strategy_one_step(topo):
+def test_4m_2x4_every_strategy_one_step(topo, transport):
     N, M = 8, 4
     lay = L.Layout(CONFIG_4M["sizes"], N, M, CONFIG_4M["B"])
     ref = _dp_reference(lay, 1)
     for code in S.paro_strategies():
-        run = EmuRun(N, M, code, CONFIG_4M["sizes"], CONFIG_4M["B"], topo=topo)
+        run = EmuRun(N, M, code, CONFIG_4M["sizes"], CONFIG_4M["B"], topo=topo, transport=transport)
         run.set_grads(1)
         stats = run.step(1)
         assert abs(stats["grad_norm"] ** 2 - ref[4][0]) <= 1e-12 * ref[4][0]
@@ -157,15 +158,16 @@ def test_4m_2x4_every_strategy_one_step(topo):
         run.close()
 
 
+@pytest.mark.parametrize("transport", ["push", "pull"])
 @pytest.mark.parametrize("N,M", [(8, 2), (4, 2), (8, 1), (8, 8), (6, 3), (2, 2), (2, 1), (9, 3)])
 @pytest.mark.parametrize("topo", ["ho", "two_step", "direct"])
-def test_splits_every_strategy_ragged(N, M, topo):
+def test_splits_every_strategy_ragged(N, M, topo, transport):
     sizes = ragged_param_sizes() + [N * 64 * 7 + 3]
     B = N * 64 * 3
     lay = L.Layout(sizes, N, M, B)
     ref = _dp_reference(lay, 2)
     for code in S.paro_strategies():
-        run = EmuRun(N, M, code, sizes, B, topo=topo)
+        run = EmuRun(N, M, code, sizes, B, topo=topo, transport=transport)
         for t in (1, 2):
             run.set_grads(t)
             run.step(t)
@@ -173,7 +175,8 @@ def test_splits_every_strategy_ragged(N, M, topo):
         run.close()
 
 
-def test_flat_ring_matches_oracle_flat_simulation():
+@pytest.mark.parametrize("transport", ["push", "pull"])
+def test_flat_ring_matches_oracle_flat_simulation(transport):
     N, M = 8, 4
     sizes = [N * 64 * 20]
     B = N * 64 * 6
@@ -183,7 +186,7 @@ def test_flat_ring_matches_oracle_flat_simulation():
     for code in ("NNN", "NNG", "GGG", "IGG"):
         res = ST.strategy_step(code, lay, grads, ST.init_state(w0, lay, code), nm.AdamScalars(LR, 1),
                                topology="flat")
-        run = EmuRun(N, M, code, sizes, B, topo="flat")
+        run = EmuRun(N, M, code, sizes, B, topo="flat", transport=transport)
         run.set_grads(1)
         run.step(1)
         for r in range(N):
