@@ -1,0 +1,106 @@
+#!/usr/bin/env python
+"""Diagnostic sweep (not the bench contract): under torchrun, time paro_step for
+a grid of (strategy, topology, transport, comm_ctas, bucket) on one job and
+print one JSON line per point (rank 0).  Usage:
+
+  torchrun --nproc-per-node 2 tools/sweep.py --model 7B --grid '{"strategy":["IIG"],"comm_ctas":[32,64,148]}'
+"""
+import argparse
+import itertools
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+from paro_synth import SEED, llama_param_sizes  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--model", default="7B")
+    ap.add_argument("--steps", type=int, default=4)
+    ap.add_argument("--warmup", type=int, default=2)
+    ap.add_argument("--group-size", type=int, default=0)
+    ap.add_argument("--grid", default="{}")
+    a = ap.parse_args()
+    grid = {"strategy": ["IIG"], "topology": ["ho"], "transport": ["push"], "comm_ctas": [64],
+            "bucket": [1 << 26], "depth": [2]}
+    grid.update(json.loads(a.grid))
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("cpu:gloo,cuda:nccl", rank=rank, world_size=world)
+    from paper_2310_06003_b200 import paro
+    M = a.group_size or (world // 2 if world >= 4 else 1)
+    uid = paro.unique_id() if rank == 0 else bytes(128)
+    if world > 1:
+        t = torch.tensor(list(uid), dtype=torch.uint8)
+        dist.broadcast(t, 0)
+        uid = bytes(t.tolist())
+    ctx = paro.Context(world, M, mode="real", rank=rank, device=local, uid=uid)
+    sizes = llama_param_sizes(a.model)
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    keys = list(grid.keys())
+    for vals in itertools.product(*[grid[k] for k in keys]):
+        cfg = dict(zip(keys, vals))
+        try:
+            plan = paro.Plan(ctx, cfg["strategy"], sizes, bucket_elems=cfg["bucket"], topology=cfg["topology"],
+                             comm_ctas=cfg["comm_ctas"], pipeline_depth=cfg["depth"], stream=stream.cuda_stream,
+                             transport=cfg["transport"])
+        except Exception as e:  # noqa: BLE001
+            if rank == 0:
+                print(json.dumps({"cfg": cfg, "error": str(e)}), flush=True)
+            continue
+        info = plan.info()
+        st = [torch.empty(info["os_numel"], dtype=torch.float32, device="cuda") for _ in range(3)]
+        ptrs = [[x.data_ptr() for x in st]]
+        plan.opt_state_init(rank, ptrs[0], seed=SEED)
+        plan.synth_grads(rank, SEED, 1)
+        s = 0
+        for _ in range(a.warmup):
+            s += 1
+            plan.step(ptrs, 3e-4, s)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        plan.profile_start((info["n_comm_launches"] + info["n_buckets"] + 8) * a.steps + 64)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(a.steps):
+            s += 1
+            plan.step(ptrs, 3e-4, s)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        prof = plan.profile_stop()
+        ms = e0.elapsed_time(e1) / a.steps
+        tt = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        if rank == 0:
+            print(json.dumps({"cfg": cfg, "groups": f"{world // M}x{M}", "ms": round(float(tt.item()), 3),
+                              "Gparam_s": round(info["psi"] / float(tt.item()) / 1e6, 1),
+                              "adam_ms": round(prof["adam_ms"] / a.steps, 3),
+                              "comm_ms": round(prof["comm_ms"] / a.steps, 3),
+                              "comm_launch_us": round(1000 * prof["comm_ms"] / max(1, prof["comm_launches"]), 1),
+                              "comm_GBps": round(prof["comm_bytes"] / max(1e-9, prof["comm_ms"]) / 1e6, 1),
+                              "adam_GBps": round(28 * prof["adam_elems"] / max(1e-9, prof["adam_ms"]) / 1e6, 1),
+                              "send_bytes": info["step_send_bytes_intra"] + info["step_send_bytes_inter"]}),
+                  flush=True)
+        del st
+        plan.close()
+        torch.cuda.empty_cache()
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
