@@ -176,15 +176,15 @@ __device__ __noinline__ void run_fold_generic(const DTask* __restrict__ t, int64
 
 __device__ __forceinline__ void run_task(const DTask* __restrict__ t, int64_t u0, int64_t u1, float alpha) {
   switch (t->nin) {
-    case 1: run_fold<1, 4>(t, u0, u1, alpha); break;
-    case 2: run_fold<2, 4>(t, u0, u1, alpha); break;
-    case 3: run_fold<3, 2>(t, u0, u1, alpha); break;
-    case 4: run_fold<4, 2>(t, u0, u1, alpha); break;
+    case 1: run_fold<1, 2>(t, u0, u1, alpha); break;
+    case 2: run_fold<2, 2>(t, u0, u1, alpha); break;
+    case 3: run_fold<3, 1>(t, u0, u1, alpha); break;
+    case 4: run_fold<4, 1>(t, u0, u1, alpha); break;
     default: run_fold_generic(t, u0, u1, alpha); break;
   }
 }
 
-__global__ void __launch_bounds__(kRoundsBlock) rounds_kernel(const RoundsArgs a) {
+__global__ void __launch_bounds__(kRoundsBlock, 4) rounds_kernel(const RoundsArgs a) {
   if (a.bar.err && *(volatile int*)a.bar.err) return;   // sticky device error: do nothing
   int bidx = 0;
   for (int r = 0; r < a.nrounds; ++r) {
@@ -231,16 +231,29 @@ __device__ __forceinline__ float adam_elem(float g, float& w, float& m, float& v
 
 __device__ __forceinline__ void adam_unit(const AdamSeg& sg, int64_t u, const AdamScal& c, double& nsq,
                                           int& bad) {
-  const uint4 gv = __ldcs(reinterpret_cast<const uint4*>(sg.ghat) + u);
+  uint4 gv[kAdamMaxIn];
+#pragma unroll
+  for (int i = 0; i < kAdamMaxIn; ++i)
+    if (i < sg.gnin) gv[i] = __ldcs(reinterpret_cast<const uint4*>(sg.gin[i]) + u);
   const float4* mp = reinterpret_cast<const float4*>(sg.master) + 2 * u;
   const float4* m1p = reinterpret_cast<const float4*>(sg.m) + 2 * u;
   const float4* v1p = reinterpret_cast<const float4*>(sg.v) + 2 * u;
-  float4 w0 = __ldcs(mp), w1 = __ldcs(mp + 1);
-  float4 m0 = __ldcs(m1p), m1 = __ldcs(m1p + 1);
-  float4 v0 = __ldcs(v1p), v1 = __ldcs(v1p + 1);
+  const float4 w0 = __ldcs(mp), w1 = __ldcs(mp + 1);
+  const float4 m0 = __ldcs(m1p), m1 = __ldcs(m1p + 1);
+  const float4 v0 = __ldcs(v1p), v1 = __ldcs(v1p + 1);
+  // g_hat: fused final hop(s) of the reduction, canonical order (R2)
   float g[8];
-  unpack8(gv, g);
-  if (sg.raw) scale_round8(g, c.alpha);
+  unpack8(gv[0], g);
+  if (sg.graw & 1u) scale_round8(g, c.alpha);
+#pragma unroll
+  for (int i = 1; i < kAdamMaxIn; ++i) {
+    if (i < sg.gnin) {
+      float x[8];
+      unpack8(gv[i], x);
+      if ((sg.graw >> i) & 1u) scale_round8(x, c.alpha);
+      hop8(g, x);
+    }
+  }
   float w[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
   float m[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
   float v[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
@@ -257,7 +270,7 @@ __device__ __forceinline__ void adam_unit(const AdamSeg& sg, int64_t u, const Ad
   reinterpret_cast<uint4*>(sg.param)[u] = pack8(w);
 }
 
-__global__ void __launch_bounds__(kAdamBlock) adam_kernel(const AdamArgs a) {
+__global__ void __launch_bounds__(kAdamBlock, 3) adam_kernel(const AdamArgs a) {
   const AdamScal c{a.b1, a.omb1, a.b2, a.omb2, a.step_size, a.bc2s, a.eps, a.decay, a.s_g, a.alpha, a.has_wd};
   int64_t U = 0;
   for (int i = 0; i < a.nseg; ++i) U += a.seg[i].n8;
@@ -268,14 +281,11 @@ __global__ void __launch_bounds__(kAdamBlock) adam_kernel(const AdamArgs a) {
   int bad = 0;
   int64_t base = 0;
   for (int i = 0; i < a.nseg && base < b1; ++i) {
-    const AdamSeg sg = a.seg[i];
-    const int64_t s = max(b0, base) - base, e = min(b1, base + sg.n8) - base;
-    for (int64_t u = s + threadIdx.x; u < e; u += 2 * blockDim.x) {
-      const int64_t u2 = u + blockDim.x;
-      adam_unit(sg, u, c, nsq, bad);
-      if (u2 < e) adam_unit(sg, u2, c, nsq, bad);
-    }
-    base += sg.n8;
+    const AdamSeg& sg = a.seg[i];
+    const int64_t n8 = sg.n8;
+    const int64_t s = max(b0, base) - base, e = min(b1, base + n8) - base;
+    for (int64_t u = s + threadIdx.x; u < e; u += blockDim.x) adam_unit(sg, u, c, nsq, bad);
+    base += n8;
   }
   // block reduction of the norm partial: warp shuffles, then one warp
 #pragma unroll

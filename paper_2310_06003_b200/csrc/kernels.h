@@ -17,7 +17,7 @@
 namespace paro {
 
 constexpr int kDevMaxIn = 16;
-constexpr int kMaxAdamSegs = 16;
+constexpr int kMaxAdamSegs = 16;  // emulated ranks per Adam launch
 constexpr int kHeaderBytes = 4096;   // per-rank region header: flags + counters
 
 struct DTask {
@@ -55,14 +55,20 @@ struct RoundsArgs {
   BarrierCtx bar;
 };
 
+constexpr int kAdamMaxIn = 4;
+
 struct AdamSeg {
-  const uint16_t* ghat;
+  // g_hat = fold(gin[0..gnin-1]) with the hop operator: 1 input = a
+  // materialised g_hat (or the raw local gradient at N = 1); 2-4 inputs =
+  // the final reduction hop fused into the update (push transport, OS = G)
+  const uint16_t* gin[kAdamMaxIn];
   float* master;
   float* m;
   float* v;
   uint16_t* param;
   int64_t n8;
-  int32_t raw;       // ghat is a raw gradient (N = 1): scale by alpha first
+  int32_t gnin;
+  uint32_t graw;     // bit i: gin[i] is a raw gradient -> RNE_bf16(g * alpha)
   int32_t in_norm;   // elements counted in the unique-element norm
 };
 

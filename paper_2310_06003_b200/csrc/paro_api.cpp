@@ -778,13 +778,18 @@ paro_status_t paro_step(paro_plan_t p, const void* const* grads, void* const* pa
       int64_t len = 0;
       for (int b = b0; b < b1; ++b) len += pl.sched[b].os_len;
       AdamSeg& sg = aa.seg[aa.nseg++];
-      sg.ghat = reinterpret_cast<const uint16_t*>(data_ptr(p, S0.ghat[r].rank, S0.ghat[r].kind, S0.ghat[r].off));
+      sg.gnin = (int)S0.ghat_in[r].size();
+      sg.graw = 0;
+      for (int i = 0; i < sg.gnin; ++i) {
+        const Ref& x = S0.ghat_in[r][i];
+        sg.gin[i] = reinterpret_cast<const uint16_t*>(data_ptr(p, x.rank, x.kind, x.off));
+        if (x.kind == BUF_GRAD) sg.graw |= 1u << i;
+      }
       sg.master = opt_state[li].master + S0.os_off[r];
       sg.m = opt_state[li].m + S0.os_off[r];
       sg.v = opt_state[li].v + S0.os_off[r];
       sg.param = reinterpret_cast<uint16_t*>(data_ptr(p, S0.param[r].rank, S0.param[r].kind, S0.param[r].off));
       sg.n8 = len / 8;
-      sg.raw = (pl.N == 1) ? 1 : 0;
       sg.in_norm = uniq ? 1 : 0;
     }
     aa.partials = p->d_partials + (int64_t)n_adam * grid;
@@ -817,7 +822,10 @@ paro_status_t paro_step(paro_plan_t p, const void* const* grads, void* const* pa
       return run_launch(p, p->gat[b], &launches);
     };
     for (int b = 0; b < nb; ++b) {
+      // staging sets / g_hat slots are reused kStageSets / nslots buckets later:
+      // the Adam that reads them (fused final hop) must be done first
       if (pl.nslots > 0 && b >= pl.nslots) CK(cudaStreamWaitEvent(ctx->comm, p->ev_adam[b - pl.nslots], 0));
+      if (b >= kStageSets) CK(cudaStreamWaitEvent(ctx->comm, p->ev_adam[b - kStageSets], 0));
       if (nccl) {
         const int k = prof_begin(p, ctx->comm, 1, 0);
         paro_status_t s3 = run_nccl(p, pl.sched[b].nccl_reduce[ctx->rank]);

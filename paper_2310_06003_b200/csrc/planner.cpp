@@ -246,6 +246,16 @@ Planner::Planner(int N_, int M_, const std::string& code_, const std::vector<int
   P = parse_level(code[0]);
   G = parse_level(code[1]);
   OS = parse_level(code[2]);
+  // Degenerate splits: with M == 1 a group is one GPU (I == N); with g == 1 a
+  // group is the world (I == G).  Same residencies, same bits, no copy rounds.
+  auto norm = [&](Level l) {
+    if (l == LV_I && M == 1) return LV_N;
+    if (l == LV_I && g == 1) return LV_G;
+    return l;
+  };
+  P = norm(P);
+  G = norm(G);
+  OS = norm(OS);
   for (int64_t s : sizes)
     if (s < 0) throw std::invalid_argument("param sizes must be >= 0");
   if (opt.topology < 0 || opt.topology > 4) throw std::invalid_argument("unknown topology");
@@ -310,11 +320,11 @@ void Planner::layout() {
   buf_len[BUF_PARAM] = p_numel;
   buf_len[BUF_GSHARD] = g_numel;
   buf_len[BUF_GHAT] = int64_t(nslots) * ghat_slot;
-  buf_len[BUF_STAGE_I] = (N > 1) ? 4 * stage_i_len : 0;
-  buf_len[BUF_STAGE_E] = (N > 1) ? 4 * stage_e_len : 0;
-  buf_len[BUF_P1] = (N > 1) ? 2 * p1_len : 0;
-  buf_len[BUF_SOWN] = (N > 1) ? 2 * sown_len : 0;
-  buf_len[BUF_LAND] = (N > 1 && opt.topology == 3 && opt.push) ? 2 * land_len : 0;
+  buf_len[BUF_STAGE_I] = (N > 1) ? 2 * kStageSets * stage_i_len : 0;
+  buf_len[BUF_STAGE_E] = (N > 1) ? 2 * kStageSets * stage_e_len : 0;
+  buf_len[BUF_P1] = (N > 1) ? kStageSets * p1_len : 0;
+  buf_len[BUF_SOWN] = (N > 1) ? kStageSets * sown_len : 0;
+  buf_len[BUF_LAND] = (N > 1 && opt.topology == 3 && opt.push) ? kStageSets * land_len : 0;
   int64_t off = 0;
   for (int k = 0; k < BUF_NKINDS; ++k) {
     buf_off[k] = off;
@@ -343,7 +353,7 @@ void Planner::build_schedule() {
     BucketSchedule& S = sched[b];
     const int64_t s = buckets[b].first, n = buckets[b].second;
     const int64_t C = n / N, chunk = n / M;
-    const int par = int(b % 2);
+    const int par = int(b % kStageSets);
     S.reduce.n_ranks = S.gather.n_ranks = N;
     S.nccl_reduce.assign(N, {});
     S.nccl_gather.assign(N, {});
@@ -357,6 +367,7 @@ void Planner::build_schedule() {
     auto param_base = [&](int r) { return Ref{r, BUF_PARAM, s / divl(P)}; };
     auto stage_i = [&](int r, int slot) { return Ref{r, BUF_STAGE_I, int64_t(par * 2 + slot) * stage_i_len}; };
     auto stage_e = [&](int r, int slot) { return Ref{r, BUF_STAGE_E, int64_t(par * 2 + slot) * stage_e_len}; };
+    (void)stage_e;
     auto p1 = [&](int r) { return Ref{r, BUF_P1, int64_t(par) * p1_len}; };
     auto sown = [&](int r) { return Ref{r, BUF_SOWN, int64_t(par) * sown_len}; };
     // where the reduced segment of rank r lands (OS-residency layout of g_hat)
@@ -691,6 +702,28 @@ void Planner::build_schedule() {
           if (any) kept.push_back(rnd);
         }
         Lp->rounds.swap(kept);
+        // Push transport, OS = G: the last fold of the reduction (the owner's
+        // final hop) moves into the Adam kernel, which reads its inputs (all
+        // local) directly: g_hat is never written to / re-read from HBM.
+        if (Lp == &S.reduce && push && OS == LV_G && !Lp->rounds.empty()) {
+          S.ghat_in.assign(N, {});
+          auto& last = Lp->rounds.back();
+          for (int r = 0; r < N; ++r) {
+            const Ref d = dest_seg(r);
+            for (size_t i = 0; i < last[r].size(); ++i) {
+              const Task& t = last[r][i];
+              if (t.dst.rank == d.rank && t.dst.kind == d.kind && t.dst.off == d.off && t.n == C &&
+                  t.nin <= kMaxAdamIn) {
+                for (int k = 0; k < t.nin; ++k) S.ghat_in[r].push_back(t.in[k]);
+                last[r].erase(last[r].begin() + i);
+                break;
+              }
+            }
+          }
+          bool any = false;
+          for (auto& v : last) any = any || !v.empty();
+          if (!any) Lp->rounds.pop_back();
+        }
         // a launch whose last round stores into peers ends with a barrier so the
         // data has landed before the peer's next kernel reads it
         if (!Lp->rounds.empty()) {
@@ -740,6 +773,7 @@ void Planner::build_schedule() {
       const int j = grp(r), p = pos(r);
       S.os_off[r] = s / divl(OS);
       S.ghat[r] = (N == 1) ? grad(r, 0) : ghat_base(r);
+      if (S.ghat_in.size() != (size_t)N || S.ghat_in[r].empty()) S.ghat_in.resize(N), S.ghat_in[r] = {S.ghat[r]};
       Ref pb = param_base(r);
       if (P == OS) S.param[r] = pb;
       else if (P == LV_I) S.param[r] = at(pb, int64_t(j) * C);              // OS = G
@@ -775,10 +809,11 @@ void Planner::validate_refs() const {
               if (!ok(t.in[i], t.n)) throw std::logic_error("task input out of range in bucket " + std::to_string(b));
             if (!ok(t.dst, t.n)) throw std::logic_error("task output out of range in bucket " + std::to_string(b));
           }
-    if (N > 1)
-      for (int r = 0; r < N; ++r)
-        if (!ok(S.ghat[r], S.os_len) || !ok(S.param[r], S.os_len))
-          throw std::logic_error("adam range out of range in bucket " + std::to_string(b));
+    for (int r = 0; r < N; ++r) {
+      if (!ok(S.param[r], S.os_len)) throw std::logic_error("adam output out of range in bucket " + std::to_string(b));
+      for (const Ref& x : S.ghat_in[r])
+        if (!ok(x, S.os_len)) throw std::logic_error("adam input out of range in bucket " + std::to_string(b));
+    }
   }
 }
 

@@ -32,6 +32,8 @@ enum BufKind : int {
 };
 
 constexpr int kMaxIn = 16;   // max inputs of one fold task
+constexpr int kStageSets = 3;
+constexpr int kMaxAdamIn = 4;  // max fold inputs of the fused final hop in Adam  // rotation of per-bucket staging sets (reuse distance)
 
 struct Ref {
   int32_t rank = -1;
@@ -77,6 +79,9 @@ struct BucketSchedule {
   std::vector<std::vector<NcclCall>> nccl_reduce, nccl_gather;  // [rank][call]
   // Adam input/output per rank for this bucket
   std::vector<Ref> ghat;     // reduced gradient at the OS residency start
+  // Adam's g_hat = fold(ghat_in[r]) (1 input = materialised g_hat; up to 3 when
+  // the final reduction hop is fused into the Adam kernel)
+  std::vector<std::vector<Ref>> ghat_in;
   std::vector<Ref> param;    // parameter-buffer position of the OS residency
   std::vector<int64_t> os_off;   // offset in the rank's opt-state arrays
   int64_t os_len = 0;
