@@ -166,7 +166,10 @@ paro_status_t paro_rank_send_bytes(paro_plan_t plan, int rank, int64_t* intra, i
  *           the zero-copy path.
  *   kind 1: parameter buffer, bf16, p_numel elements (P residency, bucket-major).
  *   kind 2: G-residency buffer, bf16, g_numel elements (NULL for G = N, whose
- *           gradient residency is the flat gradient buffer). */
+ *           gradient residency is the flat gradient buffer).
+ *   kind 3: reduced-gradient slots (bf16; slot b % (pipeline_depth+1) holds
+ *           bucket b's g_hat at the OS residency) or NULL when g_hat lives in
+ *           the G-residency buffer or is consumed directly by Adam. */
 paro_status_t paro_buffer(paro_plan_t plan, int rank, int kind, void** ptr);
 
 /* Initialise one local rank's optimizer state and parameter buffer from a full
@@ -196,6 +199,14 @@ paro_status_t paro_synth_grads(paro_plan_t plan, int rank, uint64_t seed, int64_
  *  lr: this step's learning rate; step: 1-based Adam t ("step must be >= 1"). */
 paro_status_t paro_step(paro_plan_t plan, const void* const* grads, void* const* params,
                         const paro_opt_state_t* opt_state, float lr, int64_t step);
+
+/* Collective only (no optimizer): run the plan's gradient-reduction launches
+ * (what = 0) or parameter all-gather launches (what = 1) for every bucket,
+ * stream-ordered like paro_step.  With strategy NNN, what = 0 is a
+ * hierarchical all-reduce of the flat gradient buffer (gradients pre-scaled by
+ * 1/N, i.e. the average) on the plan's topology: the HO-Ring all-reduce of
+ * BASELINE config 5.  Requires a real or emulated context. */
+paro_status_t paro_collective(paro_plan_t plan, int what);
 
 /* Per-kernel timing over a region of steps (used by bench.py for the roofline):
  * paro_profile_start allocates `max_launches` CUDA event pairs and brackets

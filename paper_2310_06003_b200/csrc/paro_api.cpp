@@ -644,7 +644,8 @@ paro_status_t paro_buffer(paro_plan_t p, int rank, int kind, void** ptr) {
   if (kind == 0) *ptr = data_ptr(p, rank, BUF_GRAD, 0);
   else if (kind == 1) *ptr = data_ptr(p, rank, BUF_PARAM, 0);
   else if (kind == 2) *ptr = (pl.G == LV_N) ? nullptr : data_ptr(p, rank, BUF_GSHARD, 0);
-  else return fail(PARO_ERR_INVALID, "kind must be 0, 1 or 2");
+  else if (kind == 3) *ptr = pl.buf_len[BUF_GHAT] ? data_ptr(p, rank, BUF_GHAT, 0) : nullptr;
+  else return fail(PARO_ERR_INVALID, "kind must be 0, 1, 2 or 3");
   return PARO_OK;
 }
 
@@ -899,6 +900,42 @@ paro_status_t paro_step(paro_plan_t p, const void* const* grads, void* const* pa
   p->last_stream = S;
   p->last_launches = launches;
   p->stepped = true;
+  if (p->prof) {
+    ++p->prof_steps;
+    p->prof_launches += launches;
+  }
+  return PARO_OK;
+}
+
+paro_status_t paro_collective(paro_plan_t p, int what) {
+  if (!p) return fail(PARO_ERR_INVALID, "null plan");
+  paro_ctx* ctx = p->ctx;
+  paro_status_t s = check_ctx(ctx);
+  if (s != PARO_OK) return s;
+  if (ctx->mode == MODE_PLANNER) return fail(PARO_ERR_STATE, "planning-only context");
+  if (what != 0 && what != 1) return fail(PARO_ERR_INVALID, "what must be 0 (reduce) or 1 (gather)");
+  const Planner& pl = *p->pl;
+  cudaStream_t S = p->opts.stream ? static_cast<cudaStream_t>(p->opts.stream) : ctx->main;
+  int launches = 0;
+  CK(cudaEventRecord(p->ev_fork, S));
+  CK(cudaStreamWaitEvent(ctx->comm, p->ev_fork, 0));
+  const bool nccl = pl.opt.topology == PARO_TOPO_NCCL;
+  for (size_t b = 0; b < pl.buckets.size() && pl.N > 1; ++b) {
+    if (nccl) {
+      const auto& calls = what == 0 ? pl.sched[b].nccl_reduce[ctx->rank] : pl.sched[b].nccl_gather[ctx->rank];
+      const int k = prof_begin(p, ctx->comm, 1, 0);
+      paro_status_t s3 = run_nccl(p, calls);
+      prof_end(p, ctx->comm, k);
+      if (s3 != PARO_OK) return s3;
+      ++launches;
+    } else {
+      paro_status_t s3 = run_launch(p, what == 0 ? p->red[b] : p->gat[b], &launches);
+      if (s3 != PARO_OK) return s3;
+    }
+  }
+  CK(cudaEventRecord(p->ev_comm, ctx->comm));
+  CK(cudaStreamWaitEvent(S, p->ev_comm, 0));
+  p->last_stream = S;
   if (p->prof) {
     ++p->prof_steps;
     p->prof_launches += launches;

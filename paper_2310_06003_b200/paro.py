@@ -100,6 +100,7 @@ paro_step = _sig("paro_step", _st, _vp, C.POINTER(_vp), C.POINTER(_vp), C.POINTE
                  C.c_float, _i64)
 paro_step_stats = _sig("paro_step_stats", _st, _vp, C.POINTER(paro_step_stats_t))
 paro_plan_destroy = _sig("paro_plan_destroy", _st, _vp)
+paro_collective = _sig("paro_collective", _st, _vp, C.c_int)
 paro_profile_start = _sig("paro_profile_start", _st, _vp, C.c_int)
 paro_profile_stop = _sig("paro_profile_stop", _st, _vp, C.POINTER(paro_profile_t))
 paro_last_error = _sig("paro_last_error", C.c_char_p)
@@ -110,7 +111,7 @@ EXPORTED = ["paro_opts_default", "paro_get_unique_id", "paro_init", "paro_init_e
             "paro_bucket_range", "paro_rank_send_bytes", "paro_buffer", "paro_opt_state_init",
             "paro_opt_state_init_synth", "paro_synth_grads", "paro_step", "paro_step_stats",
             "paro_plan_destroy", "paro_last_error", "paro_version", "paro_profile_start",
-            "paro_profile_stop"]
+            "paro_profile_stop", "paro_collective"]
 
 
 def check(status):
@@ -225,6 +226,9 @@ class Plan:
         s = paro_step_stats_t()
         check(paro_step_stats(self.h, C.byref(s)))
         return {k: getattr(s, k) for k, _ in paro_step_stats_t._fields_}
+
+    def collective(self, what=0):
+        check(paro_collective(self.h, int(what)))
 
     def profile_start(self, max_launches):
         check(paro_profile_start(self.h, int(max_launches)))

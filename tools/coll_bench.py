@@ -1,0 +1,81 @@
+#!/usr/bin/env python
+"""All-reduce bus bandwidth sweep (BASELINE config 5): our HO-Ring / flat ring /
+two-step / direct all-reduce (paro_collective on an NNN plan: hierarchical
+RS + AG with the bf16 hop arithmetic) against torch.distributed.all_reduce
+(NCCL) on the same bf16 size.  busbw = S * 2(N-1)/N / t (nccl-tests convention).
+Run under torchrun; prints one JSON line per point on rank 0."""
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--sizes-mb", default="1,4,16,64,256,1024,4096")
+    ap.add_argument("--topos", default="ho,flat,two_step,direct")
+    ap.add_argument("--group-size", type=int, default=0)
+    ap.add_argument("--iters", type=int, default=10)
+    ap.add_argument("--comm-ctas", type=int, default=148)
+    ap.add_argument("--transport", default="push")
+    a = ap.parse_args()
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist.init_process_group("cpu:gloo,cuda:nccl", rank=rank, world_size=world)
+    from paper_2310_06003_b200 import paro
+    M = a.group_size or (world // 2 if world >= 4 else 1)
+    uid = paro.unique_id() if rank == 0 else bytes(128)
+    t = torch.tensor(list(uid), dtype=torch.uint8)
+    dist.broadcast(t, 0)
+    ctx = paro.Context(world, M, mode="real", rank=rank, device=local, uid=bytes(t.tolist()))
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+
+    def timeit(fn):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(a.iters):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = torch.tensor([e0.elapsed_time(e1) / a.iters], dtype=torch.float64, device="cuda")
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        return float(ms.item())
+
+    for mb in [int(x) for x in a.sizes_mb.split(",")]:
+        nbytes = mb << 20
+        elems = nbytes // 2
+        row = {"bytes": nbytes, "groups": f"{world // M}x{M}", "n_gpus": world}
+        for topo in a.topos.split(","):
+            bucket = min(elems, 1 << 28)
+            pl = paro.Plan(ctx, "NNN", [elems], bucket_elems=bucket, topology=topo, comm_ctas=a.comm_ctas,
+                           stream=stream.cuda_stream, transport=a.transport)
+            pl.synth_grads(rank, 1234, 1)
+            ms = timeit(lambda: pl.collective(0))
+            row[topo] = {"ms": round(ms, 4), "busbw_GBps": round(nbytes * 2 * (world - 1) / world / (ms / 1e3) / 1e9, 1)}
+            pl.close()
+        x = torch.ones(elems, dtype=torch.bfloat16, device="cuda")
+        ms = timeit(lambda: dist.all_reduce(x))
+        row["nccl_allreduce"] = {"ms": round(ms, 4),
+                                 "busbw_GBps": round(nbytes * 2 * (world - 1) / world / (ms / 1e3) / 1e9, 1)}
+        del x
+        torch.cuda.empty_cache()
+        if rank == 0:
+            print(json.dumps(row), flush=True)
+    ctx.close()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
