@@ -20,7 +20,7 @@ namespace paro {
 
 namespace {
 
-constexpr int kRoundsBlock = 256;
+constexpr int kRoundsBlock = 512;
 constexpr int kAdamBlock = 256;
 constexpr uint64_t kTimeoutNs = 20ull * 1000 * 1000 * 1000;  // 20 s per wait
 
@@ -119,20 +119,25 @@ __device__ bool grid_peer_barrier(const RoundsArgs& a, uint64_t peers, int bidx)
 }
 
 // ------------------------------------------------------------- fold tasks
+// Each task is spread over the whole grid, grid-stride interleaved (every
+// warp touches consecutive 16-byte units; measured on B200: interleaving beats
+// per-CTA contiguous slices, tools/p2p_bw.cu), UNR independent 128-bit loads
+// per input in flight per thread before any use.
 template <int NIN, int UNR>
-__device__ __forceinline__ void run_fold(const DTask* __restrict__ t, int64_t u0, int64_t u1, float alpha) {
+__device__ __forceinline__ void run_fold(const DTask* __restrict__ t, float alpha) {
   const uint4* in[NIN];
 #pragma unroll
   for (int i = 0; i < NIN; ++i) in[i] = reinterpret_cast<const uint4*>(t->in[i]);
   uint4* dst = reinterpret_cast<uint4*>(t->dst);
   const uint32_t raw = t->rawmask;
-  const int64_t stride = blockDim.x;
-  for (int64_t ub = u0 + threadIdx.x; ub < u1; ub += stride * UNR) {
+  const int64_t n8 = t->n8;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t ub = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; ub < n8; ub += stride * UNR) {
     uint4 v[UNR][NIN];
 #pragma unroll
     for (int k = 0; k < UNR; ++k) {
       const int64_t u = ub + k * stride;
-      if (u < u1) {
+      if (u < n8) {
 #pragma unroll
         for (int i = 0; i < NIN; ++i) v[k][i] = __ldcg(in[i] + u);
       }
@@ -140,7 +145,11 @@ __device__ __forceinline__ void run_fold(const DTask* __restrict__ t, int64_t u0
 #pragma unroll
     for (int k = 0; k < UNR; ++k) {
       const int64_t u = ub + k * stride;
-      if (u >= u1) break;
+      if (u >= n8) break;
+      if (NIN == 1 && !(raw & 1u)) {   // plain copy (all-gather hop): no unpack
+        __stcg(dst + u, v[k][0]);
+        continue;
+      }
       float acc[8];
       unpack8(v[k][0], acc);
       if (raw & 1u) scale_round8(acc, alpha);
@@ -156,11 +165,13 @@ __device__ __forceinline__ void run_fold(const DTask* __restrict__ t, int64_t u0
   }
 }
 
-__device__ __noinline__ void run_fold_generic(const DTask* __restrict__ t, int64_t u0, int64_t u1, float alpha) {
+__device__ __noinline__ void run_fold_generic(const DTask* __restrict__ t, float alpha) {
   uint4* dst = reinterpret_cast<uint4*>(t->dst);
   const int nin = t->nin;
   const uint32_t raw = t->rawmask;
-  for (int64_t u = u0 + threadIdx.x; u < u1; u += blockDim.x) {
+  const int64_t n8 = t->n8;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n8; u += stride) {
     float acc[8];
     unpack8(__ldcg(reinterpret_cast<const uint4*>(t->in[0]) + u), acc);
     if (raw & 1u) scale_round8(acc, alpha);
@@ -174,34 +185,23 @@ __device__ __noinline__ void run_fold_generic(const DTask* __restrict__ t, int64
   }
 }
 
-__device__ __forceinline__ void run_task(const DTask* __restrict__ t, int64_t u0, int64_t u1, float alpha) {
+__device__ __forceinline__ void run_task(const DTask* __restrict__ t, float alpha) {
   switch (t->nin) {
-    case 1: run_fold<1, 2>(t, u0, u1, alpha); break;
-    case 2: run_fold<2, 2>(t, u0, u1, alpha); break;
-    case 3: run_fold<3, 1>(t, u0, u1, alpha); break;
-    case 4: run_fold<4, 1>(t, u0, u1, alpha); break;
-    default: run_fold_generic(t, u0, u1, alpha); break;
+    case 1: run_fold<1, 4>(t, alpha); break;
+    case 2: run_fold<2, 2>(t, alpha); break;
+    case 3: run_fold<3, 1>(t, alpha); break;
+    case 4: run_fold<4, 1>(t, alpha); break;
+    default: run_fold_generic(t, alpha); break;
   }
 }
 
-__global__ void __launch_bounds__(kRoundsBlock, 4) rounds_kernel(const RoundsArgs a) {
+__global__ void __launch_bounds__(kRoundsBlock, 2) rounds_kernel(const RoundsArgs a) {
   if (a.bar.err && *(volatile int*)a.bar.err) return;   // sticky device error: do nothing
   int bidx = 0;
   for (int r = 0; r < a.nrounds; ++r) {
     const DRound rd = a.rounds[r];
     if (a.bar.my_flags && !grid_peer_barrier(a, rd.peers_before, bidx++)) return;
-    const int64_t U = rd.units;
-    const int64_t per = (U + gridDim.x - 1) / gridDim.x;
-    const int64_t b0 = min(U, (int64_t)blockIdx.x * per);
-    const int64_t b1 = min(U, b0 + per);
-    int64_t base = 0;
-    for (int ti = rd.t0; ti < rd.t1 && base < b1; ++ti) {
-      const DTask* t = a.tasks + ti;
-      const int64_t n8 = t->n8;
-      const int64_t s = max(b0, base), e = min(b1, base + n8);
-      if (s < e) run_task(t, s - base, e - base, a.alpha);
-      base += n8;
-    }
+    for (int ti = rd.t0; ti < rd.t1; ++ti) run_task(a.tasks + ti, a.alpha);
   }
   if (a.bar.my_flags && a.final_barrier) grid_peer_barrier(a, a.final_peers, bidx++);
 }

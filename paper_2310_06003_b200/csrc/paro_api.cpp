@@ -251,7 +251,7 @@ void prof_end(PlanT* p, cudaStream_t s, int k) {
 }
 
 int comm_grid(const PlanT* p) {
-  int g = p->opts.comm_ctas > 0 ? p->opts.comm_ctas : 64;
+  int g = p->opts.comm_ctas > 0 ? p->opts.comm_ctas : 148;
   if (p->ctx->mode == MODE_REAL) {
     if (g > p->ctx->sm_count) g = p->ctx->sm_count;   // co-residency of all CTAs (barriers)
   } else {
@@ -375,7 +375,7 @@ void paro_opts_default(paro_opts_t* o) {
   o->eps = 1e-8f;
   o->weight_decay = 0.0f;
   o->loss_scale = 1.0f;
-  o->comm_ctas = 64;
+  o->comm_ctas = 148;
   o->pipeline_depth = 2;
   o->pull_transport = 0;
   o->stream = nullptr;
@@ -483,7 +483,7 @@ paro_status_t paro_plan(paro_ctx_t ctx, const char* strategy, const int64_t* par
   else paro_opts_default(&o);
   if (o.topology == PARO_TOPO_NCCL && ctx->mode == MODE_EMU)
     return fail(PARO_ERR_INVALID, "NCCL topology needs real ranks");
-  if (o.comm_ctas <= 0) o.comm_ctas = 64;
+  if (o.comm_ctas <= 0) o.comm_ctas = 148;
   std::vector<int64_t> sizes(param_sizes, param_sizes + n_params);
   PlanOptions po;
   po.bucket_elems = o.bucket_elems > 0 ? o.bucket_elems : (int64_t(1) << 26);
