@@ -198,7 +198,7 @@ paro_status_t upload_schedule(PlanT* p) {
       rounds.push_back(d);
     }
     dl.nrounds = R;
-    dl.final_barrier = (L.final_barrier || L.final_all) ? 1 : 0;
+    dl.final_barrier = L.final_barrier ? 1 : 0;
     // bytes sent by the local rank(s): what peers read from them in this launch
     for (int r = 0; r < R; ++r)
       for (int x = 0; x < pl.N; ++x)
@@ -209,15 +209,7 @@ paro_status_t upload_schedule(PlanT* p) {
           }
           if (t.dst.rank != x && (ctx->mode != MODE_REAL || x == ctx->rank)) dl.bytes += 2 * t.n;
         }
-    dl.final_peers = 0;
-    if (ctx->mode == MODE_REAL) {
-      if (L.final_all) {
-        for (int x = 0; x < pl.N; ++x)
-          if (x != ctx->rank) dl.final_peers |= uint64_t(1) << x;
-      } else {
-        dl.final_peers = L.barrier_peers(R, ctx->rank);
-      }
-    }
+    dl.final_peers = (ctx->mode == MODE_REAL) ? L.barrier_peers(R, ctx->rank) : 0;
     return dl;
   };
   p->red.clear();
@@ -263,7 +255,7 @@ int comm_grid(const PlanT* p) {
 // Launch one collective (reduce or gather of one bucket) on the comm stream.
 paro_status_t run_launch(PlanT* p, const DevLaunch& dl, int* nlaunch) {
   paro_ctx* ctx = p->ctx;
-  if (dl.nrounds == 0) return PARO_OK;
+  if (dl.nrounds == 0 && (!dl.final_barrier || ctx->mode != MODE_REAL)) return PARO_OK;
   const int grid = comm_grid(p);
   RoundsArgs a{};
   a.tasks = p->d_tasks;
@@ -857,6 +849,18 @@ paro_status_t paro_step(paro_plan_t p, const void* const* grads, void* const* pa
   ++launches;
   CK(cudaEventRecord(p->ev_comp, ctx->comp));
   CK(cudaStreamWaitEvent(ctx->comm, p->ev_comp, 0));
+  // ---- step-end barrier with every peer: after it no peer reads (fused Adam,
+  // pull rounds) or writes (push rounds) this rank's buffers any more, so the
+  // caller may overwrite its gradients and read its parameters.
+  if (ctx->mode == MODE_REAL && pl.N > 1 && pl.opt.topology != PARO_TOPO_NCCL) {
+    DevLaunch fin;
+    fin.nrounds = 0;
+    fin.final_barrier = 1;
+    for (int x = 0; x < pl.N; ++x)
+      if (x != ctx->rank) fin.final_peers |= uint64_t(1) << x;
+    paro_status_t s6 = run_launch(p, fin, &launches);
+    if (s6 != PARO_OK) return s6;
+  }
   if (ctx->mode == MODE_REAL && pl.N > 1) {
     NK(ncclAllReduce(p->d_norm, p->d_norm, 1, ncclDouble, ncclSum, ctx->world, ctx->comm));
     NK(ncclAllReduce(p->d_nonfinite, p->d_nonfinite, 1, ncclInt32, ncclMax, ctx->world, ctx->comm));

@@ -193,6 +193,7 @@ std::vector<int> Launch::reads(int r, int rank) const {
 
 uint64_t Launch::barrier_peers(int r, int rank) const {
   uint64_t m = 0;
+  if (r >= (int)rounds.size() && !final_extra.empty()) m |= final_extra[rank];
   for (int rr = r - 1; rr <= r; ++rr) {
     if (rr < 0 || rr >= (int)rounds.size()) continue;
     for (int x : reads(rr, rank)) m |= uint64_t(1) << x;
@@ -702,11 +703,14 @@ void Planner::build_schedule() {
           if (any) kept.push_back(rnd);
         }
         Lp->rounds.swap(kept);
-        // Push transport, OS = G: the last fold of the reduction (the owner's
-        // final hop) moves into the Adam kernel, which reads its inputs (all
-        // local) directly: g_hat is never written to / re-read from HBM.
-        if (Lp == &S.reduce && push && OS == LV_G && !Lp->rounds.empty()) {
+        // OS = G: the last fold of the reduction (the owner's final hop) moves
+        // into the Adam kernel, which reads its inputs directly (push: all
+        // local; pull: the predecessor's partial over NVLink): g_hat is never
+        // written to / re-read from HBM.  The launch then ends with a barrier
+        // that also covers the ranks the fused Adam reads (final_extra).
+        if (Lp == &S.reduce && OS == LV_G && !Lp->rounds.empty()) {
           S.ghat_in.assign(N, {});
+          Lp->final_extra.assign(N, 0);
           auto& last = Lp->rounds.back();
           for (int r = 0; r < N; ++r) {
             const Ref d = dest_seg(r);
@@ -720,9 +724,16 @@ void Planner::build_schedule() {
               }
             }
           }
+          for (int r = 0; r < N; ++r)
+            for (const Ref& x : S.ghat_in[r])
+              if (x.rank != r) {
+                Lp->final_extra[r] |= uint64_t(1) << x.rank;
+                Lp->final_extra[x.rank] |= uint64_t(1) << r;
+              }
           bool any = false;
           for (auto& v : last) any = any || !v.empty();
           if (!any) Lp->rounds.pop_back();
+          Lp->final_barrier = true;
         }
         // a launch whose last round stores into peers ends with a barrier so the
         // data has landed before the peer's next kernel reads it
@@ -731,6 +742,7 @@ void Planner::build_schedule() {
             for (const Task& t : Lp->rounds.back()[r])
               if (t.dst.rank != r) Lp->final_barrier = true;
         }
+        if (Lp->final_extra.empty()) Lp->final_extra.assign(N, 0);
       }
     } else if (N > 1 && topo == 4) {  // NCCL comparator
       for (int r = 0; r < N; ++r) {
@@ -780,13 +792,6 @@ void Planner::build_schedule() {
       else if (OS == LV_G) S.param[r] = at(pb, int64_t(seg(j, p)) * C);     // P = N
       else S.param[r] = at(pb, int64_t(p) * chunk);                         // P = N, OS = I
     }
-  }
-  // the last collective launch of a step ends with a barrier among ALL ranks:
-  // afterwards no peer reads or writes this rank's buffers, so the caller may
-  // overwrite gradients and read parameters.
-  for (int b = (int)sched.size() - 1; b >= 0; --b) {
-    if (!sched[b].gather.empty()) { sched[b].gather.final_all = true; break; }
-    if (!sched[b].reduce.empty()) { sched[b].reduce.final_all = true; break; }
   }
 }
 
@@ -839,6 +844,10 @@ void Planner::count_bytes() {
             if (z != x) (grp(x) == grp(z) ? send_intra[x] : send_inter[x]) += 2 * t.n;
           }
     }
+    // fused final hop: the Adam kernel reads these inputs (pull: over NVLink)
+    for (int x = 0; x < N && (int)S.ghat_in.size() == N; ++x)
+      for (const Ref& y : S.ghat_in[x])
+        if (y.rank != x) (grp(x) == grp(y.rank) ? send_intra[y.rank] : send_inter[y.rank]) += 2 * S.os_len;
     // NCCL comparator: ring-algorithm volumes of each call (perf only)
     for (int r = 0; r < N && opt.topology == 4; ++r) {
       for (const auto* calls : {&S.nccl_reduce[r], &S.nccl_gather[r]}) {

@@ -55,10 +55,10 @@ struct Task {
 struct Launch {
   std::vector<std::vector<std::vector<Task>>> rounds;  // [round][rank][task]
   bool final_barrier = false;   // barrier with the peers touched in the last round
-  bool final_all = false;       // barrier with every rank (end of the step)
+  std::vector<uint64_t> final_extra;  // per rank: extra final-barrier peers (fused Adam reads)
   int n_ranks = 0;
   void add(int round, int rank, const Task& t);
-  bool empty() const { return rounds.empty(); }
+  bool empty() const { return rounds.empty() && !final_barrier; }
   // other ranks whose memory `rank` reads or writes in round r
   std::vector<int> reads(int r, int rank) const;
   // symmetric barrier peer set before round r (r == rounds.size(): final)
