@@ -221,6 +221,11 @@ typedef struct {
   int64_t comm_bytes;    /* bytes this rank sent in the timed collective launches */
   int64_t steps;         /* paro_step calls inside the region                     */
   int64_t kernel_launches; /* all library kernel launches inside the region       */
+  /* device-side globaltimer trace of the first (up to 512) collective launches
+   * of the region (real mode): time in peer/grid barriers before each round,
+   * in the rounds' data movement, and in the launch-final barrier */
+  int64_t traced_launches;
+  double traced_barrier_ms, traced_work_ms, traced_final_ms;
 } paro_profile_t;
 
 paro_status_t paro_profile_start(paro_plan_t plan, int max_launches);

@@ -195,15 +195,25 @@ __device__ __forceinline__ void run_task(const DTask* __restrict__ t, float alph
   }
 }
 
+__device__ __forceinline__ void trace_stamp(const RoundsArgs& a, int slot) {
+  if (a.trace && threadIdx.x == 0 && slot < kTraceSlots)
+    a.trace[(size_t)blockIdx.x * kTraceSlots + slot] = globaltimer();
+}
+
 __global__ void __launch_bounds__(kRoundsBlock, 2) rounds_kernel(const RoundsArgs a) {
   if (a.bar.err && *(volatile int*)a.bar.err) return;   // sticky device error: do nothing
   int bidx = 0;
+  trace_stamp(a, 0);
   for (int r = 0; r < a.nrounds; ++r) {
     const DRound rd = a.rounds[r];
     if (a.bar.my_flags && !grid_peer_barrier(a, rd.peers_before, bidx++)) return;
+    trace_stamp(a, 1 + 2 * r);
     for (int ti = rd.t0; ti < rd.t1; ++ti) run_task(a.tasks + ti, a.alpha);
+    __syncthreads();
+    trace_stamp(a, 2 + 2 * r);
   }
   if (a.bar.my_flags && a.final_barrier) grid_peer_barrier(a, a.final_peers, bidx++);
+  trace_stamp(a, kTraceSlots - 1);
 }
 
 // ------------------------------------------------------------- Adam

@@ -43,7 +43,10 @@ struct BarrierCtx {
   int* err;
 };
 
+constexpr int kTraceSlots = 64;   // per CTA per traced launch: start, (barrier exit, work end) x rounds, end
+
 struct RoundsArgs {
+  uint64_t* trace;              // profiling: [gridDim][kTraceSlots] globaltimer stamps, or NULL
   const DRound* rounds;
   const DTask* tasks;
   int nrounds;

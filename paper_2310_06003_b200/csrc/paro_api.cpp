@@ -88,6 +88,9 @@ struct paro_plan {
   std::vector<int64_t> prof_amount;       // adam: elements; comm: bytes sent
   int prof_used = 0;
   int64_t prof_steps = 0, prof_launches = 0;
+  uint64_t* d_trace = nullptr;            // [kTraceLaunches][grid][kTraceSlots]
+  std::vector<int> trace_nrounds;         // rounds of each traced launch
+  int trace_grid = 0;
 };
 // (the C API also declares a *function* named paro_plan, which hides the tag in C++)
 using PlanT = struct paro_plan;
@@ -242,6 +245,8 @@ void prof_end(PlanT* p, cudaStream_t s, int k) {
   if (k >= 0) cudaEventRecord(p->prof_ev[2 * k + 1], s);
 }
 
+constexpr int kTraceLaunches = 512;
+
 int comm_grid(const PlanT* p) {
   int g = p->opts.comm_ctas > 0 ? p->opts.comm_ctas : 148;
   if (p->ctx->mode == MODE_REAL) {
@@ -274,6 +279,11 @@ paro_status_t run_launch(PlanT* p, const DevLaunch& dl, int* nlaunch) {
     a.bar.err = reinterpret_cast<int*>(hdr + 520);
     p->arrive_base += (unsigned long long)(dl.nrounds + dl.final_barrier) * grid;
     const int k = prof_begin(p, ctx->comm, 1, dl.bytes);
+    if (p->prof && p->d_trace && (int)p->trace_nrounds.size() < kTraceLaunches) {
+      a.trace = p->d_trace + (size_t)p->trace_nrounds.size() * grid * kTraceSlots;
+      p->trace_nrounds.push_back(dl.nrounds);
+      p->trace_grid = grid;
+    }
     CK(launch_rounds(a, grid, 0, ctx->comm));
     prof_end(p, ctx->comm, k);
     ++*nlaunch;
@@ -329,6 +339,7 @@ void destroy_plan(PlanT* p) {
     for (cudaEvent_t e : {p->ev_fork, p->ev_comm, p->ev_comp, p->ev_pack_staged, p->ev_unpack_staged})
       if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : p->prof_ev) cudaEventDestroy(e);
+    cudaFree(p->d_trace);
     for (cudaEvent_t e : p->ev_red) cudaEventDestroy(e);
     for (cudaEvent_t e : p->ev_adam) cudaEventDestroy(e);
   }
@@ -962,6 +973,10 @@ paro_status_t paro_profile_start(paro_plan_t p, int max_launches) {
   p->prof_used = 0;
   p->prof_steps = 0;
   p->prof_launches = 0;
+  if (ctx->mode == MODE_REAL && !p->d_trace) {
+    CK(cudaMalloc(&p->d_trace, sizeof(uint64_t) * kTraceLaunches * ctx->sm_count * kTraceSlots));
+  }
+  p->trace_nrounds.clear();
   p->prof = true;
   return PARO_OK;
 }
@@ -988,6 +1003,31 @@ paro_status_t paro_profile_stop(paro_plan_t p, paro_profile_t* out) {
   }
   out->steps = p->prof_steps;
   out->kernel_launches = p->prof_launches;
+  // device-side trace of the first collective launches: where the time goes
+  if (!p->trace_nrounds.empty()) {
+    const int G = p->trace_grid;
+    std::vector<uint64_t> tr((size_t)p->trace_nrounds.size() * G * kTraceSlots);
+    CK(cudaMemcpy(tr.data(), p->d_trace, tr.size() * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    double bar = 0, work = 0, fin = 0;
+    for (size_t l = 0; l < p->trace_nrounds.size(); ++l) {
+      const uint64_t* t = tr.data() + l * G * kTraceSlots;
+      auto mx = [&](int slot) { uint64_t m = 0; for (int b = 0; b < G; ++b) m = std::max(m, t[b * kTraceSlots + slot]); return m; };
+      auto mn = [&](int slot) { uint64_t m = ~0ull; for (int b = 0; b < G; ++b) m = std::min(m, t[b * kTraceSlots + slot]); return m; };
+      uint64_t prev = mn(0);
+      const int R = std::min(p->trace_nrounds[l], (kTraceSlots - 2) / 2);
+      for (int r = 0; r < R; ++r) {
+        const uint64_t be = mx(1 + 2 * r), we = mx(2 + 2 * r);
+        bar += (double)(be - prev);
+        work += (double)(we - be);
+        prev = we;
+      }
+      fin += (double)(mx(kTraceSlots - 1) - prev);
+    }
+    out->traced_launches = (int64_t)p->trace_nrounds.size();
+    out->traced_barrier_ms = bar * 1e-6;
+    out->traced_work_ms = work * 1e-6;
+    out->traced_final_ms = fin * 1e-6;
+  }
   p->prof = false;
   for (cudaEvent_t e : p->prof_ev) cudaEventDestroy(e);
   p->prof_ev.clear();

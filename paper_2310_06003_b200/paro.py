@@ -64,7 +64,8 @@ class paro_step_stats_t(C.Structure):
 class paro_profile_t(C.Structure):
     _fields_ = [("adam_ms", C.c_double), ("comm_ms", C.c_double), ("adam_launches", C.c_int64),
                 ("comm_launches", C.c_int64), ("adam_elems", C.c_int64), ("comm_bytes", C.c_int64),
-                ("steps", C.c_int64), ("kernel_launches", C.c_int64)]
+                ("steps", C.c_int64), ("kernel_launches", C.c_int64), ("traced_launches", C.c_int64),
+                ("traced_barrier_ms", C.c_double), ("traced_work_ms", C.c_double), ("traced_final_ms", C.c_double)]
 
 
 _vp = C.c_void_p

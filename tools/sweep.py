@@ -28,7 +28,7 @@ def main():
     ap.add_argument("--group-size", type=int, default=0)
     ap.add_argument("--grid", default="{}")
     a = ap.parse_args()
-    grid = {"strategy": ["IIG"], "topology": ["ho"], "transport": ["push"], "comm_ctas": [64],
+    grid = {"strategy": ["IIG"], "topology": ["ho"], "transport": ["pull"], "comm_ctas": [148],
             "bucket": [1 << 26], "depth": [2]}
     grid.update(json.loads(a.grid))
     rank = int(os.environ.get("RANK", "0"))
@@ -92,7 +92,9 @@ def main():
                               "comm_launch_us": round(1000 * prof["comm_ms"] / max(1, prof["comm_launches"]), 1),
                               "comm_GBps": round(prof["comm_bytes"] / max(1e-9, prof["comm_ms"]) / 1e6, 1),
                               "adam_GBps": round(28 * prof["adam_elems"] / max(1e-9, prof["adam_ms"]) / 1e6, 1),
-                              "send_bytes": info["step_send_bytes_intra"] + info["step_send_bytes_inter"]}),
+                              "send_bytes": info["step_send_bytes_intra"] + info["step_send_bytes_inter"],
+                              "trace": {k: round(prof[k], 3) for k in ("traced_launches", "traced_barrier_ms",
+                                                                      "traced_work_ms", "traced_final_ms")}}),
                   flush=True)
         del st
         plan.close()
