@@ -187,8 +187,8 @@ __device__ __noinline__ void run_fold_generic(const DTask* __restrict__ t, float
 
 __device__ __forceinline__ void run_task(const DTask* __restrict__ t, float alpha) {
   switch (t->nin) {
-    case 1: run_fold<1, 4>(t, alpha); break;
-    case 2: run_fold<2, 2>(t, alpha); break;
+    case 1: run_fold<1, 2>(t, alpha); break;
+    case 2: run_fold<2, 1>(t, alpha); break;
     case 3: run_fold<3, 1>(t, alpha); break;
     case 4: run_fold<4, 1>(t, alpha); break;
     default: run_fold_generic(t, alpha); break;
@@ -200,7 +200,7 @@ __device__ __forceinline__ void trace_stamp(const RoundsArgs& a, int slot) {
     a.trace[(size_t)blockIdx.x * kTraceSlots + slot] = globaltimer();
 }
 
-__global__ void __launch_bounds__(kRoundsBlock, 2) rounds_kernel(const RoundsArgs a) {
+__global__ void __maxnreg__(48) rounds_kernel(const RoundsArgs a) {
   if (a.bar.err && *(volatile int*)a.bar.err) return;   // sticky device error: do nothing
   int bidx = 0;
   trace_stamp(a, 0);
@@ -416,8 +416,17 @@ cudaError_t launch_rounds(const RoundsArgs& a, int grid, int block, cudaStream_t
   return cudaGetLastError();
 }
 
-cudaError_t launch_adam(const AdamArgs& a, int grid, cudaStream_t s) {
-  adam_kernel<<<grid, kAdamBlock, 0, s>>>(a);
+cudaError_t launch_adam(const AdamArgs& a, int grid, cudaStream_t s, int cap_two_per_sm) {
+  // With collectives running concurrently, Adam is capped at two CTAs per SM
+  // (an 80 KB shared-memory reservation) so a 512-thread collective CTA always
+  // fits beside it (registers: 2 x 256 x 80 + 512 x 48 = 64K).
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(adam_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  adam_kernel<<<grid, kAdamBlock, cap_two_per_sm ? 80 * 1024 : 0, s>>>(a);
   return cudaGetLastError();
 }
 

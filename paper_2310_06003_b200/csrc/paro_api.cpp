@@ -800,7 +800,7 @@ paro_status_t paro_step(paro_plan_t p, const void* const* grads, void* const* pa
     int64_t elems = 0;
     for (int i = 0; i < aa.nseg; ++i) elems += 8 * aa.seg[i].n8;
     const int pk = prof_begin(p, ctx->comp, 0, elems);
-    CK(launch_adam(aa, grid, ctx->comp));
+    CK(launch_adam(aa, grid, ctx->comp, (ctx->mode == MODE_REAL && pl.N > 1) ? 1 : 0));
     prof_end(p, ctx->comp, pk);
     ++n_adam;
     ++launches;
