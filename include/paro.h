@@ -80,8 +80,9 @@ typedef struct {
   float loss_scale;      /* 1.0; gradients are unscaled by 1/loss_scale in Adam    */
   int comm_ctas;         /* CTAs of the collective kernels (default 64)           */
   int pipeline_depth;    /* buckets in flight between reduce and gather (def. 2)  */
-  int pull_transport;    /* 0 (default): peers STORE into each other's buffers     *
-                          * (push); 1: ranks LOAD from peers (pull).  Same bits.   */
+  int pull_transport;    /* 1 (default): ranks LOAD their ring predecessor's data   *
+                          * over NVLink (pull); 0: ranks STORE into their          *
+                          * successor's buffers (push).  Same bits either way.     */
   void* stream;          /* cudaStream_t the step is ordered on; NULL = ctx stream */
 } paro_opts_t;
 

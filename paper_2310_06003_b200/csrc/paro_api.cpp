@@ -380,7 +380,7 @@ void paro_opts_default(paro_opts_t* o) {
   o->loss_scale = 1.0f;
   o->comm_ctas = 148;
   o->pipeline_depth = 2;
-  o->pull_transport = 0;
+  o->pull_transport = 1;
   o->stream = nullptr;
 }
 

@@ -123,7 +123,7 @@ def check(status):
 
 # ---------------------------------------------------------------- helpers
 def make_opts(bucket_elems=1 << 26, topology="ho", beta1=0.9, beta2=0.95, eps=1e-8, weight_decay=0.0,
-              loss_scale=1.0, comm_ctas=148, pipeline_depth=2, stream=None, transport="push"):
+              loss_scale=1.0, comm_ctas=148, pipeline_depth=2, stream=None, transport="pull"):
     o = paro_opts_t()
     paro_opts_default(C.byref(o))
     o.bucket_elems = int(bucket_elems)
