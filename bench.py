@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--bucket", type=int, default=1 << 26)
     ap.add_argument("--comm-ctas", type=int, default=148)
     ap.add_argument("--depth", type=int, default=2)
+    ap.add_argument("--transport", default="pull", choices=["pull", "push"])
+    ap.add_argument("--adam-impl", default="auto", choices=["auto", "lsu"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -207,7 +209,8 @@ def run_ours(args):
     stream = torch.cuda.Stream()          # a real (non-legacy) stream the steps are ordered on
     torch.cuda.set_stream(stream)
     plan = paro.Plan(ctx, args.strategy, sizes, bucket_elems=args.bucket, topology=args.topology,
-                     comm_ctas=args.comm_ctas, pipeline_depth=args.depth, stream=stream.cuda_stream)
+                     comm_ctas=args.comm_ctas, pipeline_depth=args.depth, stream=stream.cuda_stream,
+                     transport=args.transport, adam_impl=args.adam_impl)
     info = plan.info()
     st = [torch.empty(info["os_numel"], dtype=torch.float32, device="cuda") for _ in range(3)]
     ptrs = [[t.data_ptr() for t in st]]
@@ -329,6 +332,7 @@ def run_ours(args):
                        "n_tensors": len(sizes), "strategy": args.strategy, "groups": f"{N // M}x{M}",
                        "topology": args.topology, "bucket_elems": info["bucket_elems"],
                        "n_buckets": info["n_buckets"], "comm_ctas": args.comm_ctas, "pipeline_depth": args.depth,
+                       "transport": args.transport, "adam_impl": args.adam_impl,
                        "l2": "no flush: per-step inputs (13.5 GB grads + 81 GB/div(OS) state) >> 126 MB L2",
                        "intra_inter_gap": "not emulated: one NVSwitch box, intra/inter are labels"},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,

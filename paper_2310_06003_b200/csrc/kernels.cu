@@ -315,6 +315,154 @@ __global__ void __launch_bounds__(kAdamBlock, 3) adam_kernel(const AdamArgs a) {
   }
 }
 
+// ------------------------------------------------------------- Adam, TMA pipeline
+// Same arithmetic as adam_kernel, but the operand streams are moved by the
+// bulk-copy engine (cp.async.bulk, the non-tensor TMA path) into a ring of
+// shared-memory stages guarded by mbarriers: one thread keeps kStages-1 tiles
+// (up to ~170 KB per SM) in flight while 16 warps compute on the current one,
+// so memory-level parallelism no longer costs registers.  Persistent grid:
+// one CTA per SM, tiles dealt round-robin.  Inputs must be local memory.
+constexpr int kTmaThreads = 512;
+constexpr int kTmaTile = kTmaThreads * 8;   // elements per tile (8 per thread)
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+struct TileRef {
+  int seg;
+  int64_t start;   // element offset inside the segment
+  int n;           // elements in this tile (multiple of 8)
+};
+
+__device__ __forceinline__ bool tile_of(const AdamArgs& a, int64_t t, TileRef& out) {
+  for (int i = 0; i < a.nseg; ++i) {
+    const int64_t n = a.seg[i].n8 * 8;
+    const int64_t nt = (n + kTmaTile - 1) / kTmaTile;
+    if (t < nt) {
+      out.seg = i;
+      out.start = t * kTmaTile;
+      out.n = (int)min((int64_t)kTmaTile, n - out.start);
+      return true;
+    }
+    t -= nt;
+  }
+  return false;
+}
+
+__global__ void __launch_bounds__(kTmaThreads, 1) adam_tma_kernel(const AdamArgs a, int gnin_max, int stages) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ uint64_t full_bar[4];
+  const AdamScal c{a.b1, a.omb1, a.b2, a.omb2, a.step_size, a.bc2s, a.eps, a.decay, a.s_g, a.alpha, a.has_wd};
+  const size_t g_bytes = (size_t)kTmaTile * 2, f_bytes = (size_t)kTmaTile * 4;
+  const size_t stage_bytes = gnin_max * g_bytes + 3 * f_bytes;
+  int64_t total = 0;
+  for (int i = 0; i < a.nseg; ++i) total += (a.seg[i].n8 * 8 + kTmaTile - 1) / kTmaTile;
+  const int64_t mine = (total > blockIdx.x) ? (total - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s) mbar_init(&full_bar[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int64_t k) {   // thread 0: load tile k of this CTA into stage k % stages
+    TileRef tr;
+    tile_of(a, blockIdx.x + k * gridDim.x, tr);
+    const AdamSeg& sg = a.seg[tr.seg];
+    const int s = (int)(k % stages);
+    unsigned char* base = smem + s * stage_bytes;
+    const uint32_t gb = (uint32_t)tr.n * 2, fb = (uint32_t)tr.n * 4;
+    mbar_expect_tx(&full_bar[s], sg.gnin * gb + 3 * fb);
+    for (int i = 0; i < sg.gnin; ++i) bulk_g2s(base + i * g_bytes, sg.gin[i] + tr.start, gb, &full_bar[s]);
+    unsigned char* fbase = base + gnin_max * g_bytes;
+    bulk_g2s(fbase, sg.master + tr.start, fb, &full_bar[s]);
+    bulk_g2s(fbase + f_bytes, sg.m + tr.start, fb, &full_bar[s]);
+    bulk_g2s(fbase + 2 * f_bytes, sg.v + tr.start, fb, &full_bar[s]);
+  };
+  if (threadIdx.x == 0)
+    for (int64_t k = 0; k < min((int64_t)stages, mine); ++k) issue(k);
+  double nsq = 0.0;
+  int bad = 0;
+  for (int64_t k = 0; k < mine; ++k) {
+    const int s = (int)(k % stages);
+    mbar_wait(&full_bar[s], (uint32_t)((k / stages) & 1));
+    TileRef tr;
+    tile_of(a, blockIdx.x + k * gridDim.x, tr);
+    const AdamSeg& sg = a.seg[tr.seg];
+    const unsigned char* base = smem + s * stage_bytes;
+    const int e0 = threadIdx.x * 8;
+    if (e0 < tr.n) {
+      float g[8];
+      unpack8(*reinterpret_cast<const uint4*>(base + e0 * 2), g);
+      if (sg.graw & 1u) scale_round8(g, c.alpha);
+      for (int i = 1; i < sg.gnin; ++i) {
+        float x[8];
+        unpack8(*reinterpret_cast<const uint4*>(base + i * g_bytes + e0 * 2), x);
+        if ((sg.graw >> i) & 1u) scale_round8(x, c.alpha);
+        hop8(g, x);
+      }
+      const float* fw = reinterpret_cast<const float*>(base + gnin_max * g_bytes);
+      const float4 w0 = *reinterpret_cast<const float4*>(fw + e0), w1 = *reinterpret_cast<const float4*>(fw + e0 + 4);
+      const float4 m0 = *reinterpret_cast<const float4*>(fw + kTmaTile + e0);
+      const float4 m1 = *reinterpret_cast<const float4*>(fw + kTmaTile + e0 + 4);
+      const float4 v0 = *reinterpret_cast<const float4*>(fw + 2 * kTmaTile + e0);
+      const float4 v1 = *reinterpret_cast<const float4*>(fw + 2 * kTmaTile + e0 + 4);
+      float w[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+      float m[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
+      float v[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+      const bool in_norm = sg.in_norm != 0;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) adam_elem(g[e], w[e], m[e], v[e], c, nsq, bad, in_norm);
+      const int64_t o = tr.start + e0;
+      __stcs(reinterpret_cast<float4*>(sg.master + o), make_float4(w[0], w[1], w[2], w[3]));
+      __stcs(reinterpret_cast<float4*>(sg.master + o) + 1, make_float4(w[4], w[5], w[6], w[7]));
+      __stcs(reinterpret_cast<float4*>(sg.m + o), make_float4(m[0], m[1], m[2], m[3]));
+      __stcs(reinterpret_cast<float4*>(sg.m + o) + 1, make_float4(m[4], m[5], m[6], m[7]));
+      __stcs(reinterpret_cast<float4*>(sg.v + o), make_float4(v[0], v[1], v[2], v[3]));
+      __stcs(reinterpret_cast<float4*>(sg.v + o) + 1, make_float4(v[4], v[5], v[6], v[7]));
+      *reinterpret_cast<uint4*>(sg.param + o) = pack8(w);
+    }
+    __syncthreads();   // every thread is done with stage s: refill it
+    if (threadIdx.x == 0 && k + stages < mine) issue(k + stages);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) nsq += __shfl_xor_sync(0xffffffffu, nsq, o);
+  __shared__ double s_part[kTmaThreads / 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) s_part[wid] = nsq;
+  const int any_bad = __syncthreads_or(bad);
+  if (wid == 0) {
+    double x = (lane < (int)(blockDim.x / 32)) ? s_part[lane] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    if (lane == 0) {
+      a.partials[blockIdx.x] = x;
+      if (any_bad) atomicOr(a.nonfinite, 1);
+    }
+  }
+}
+
 // ------------------------------------------------------------- norm finalize
 __global__ void __launch_bounds__(1024) norm_finalize_kernel(const double* p, int n, double* out) {
   __shared__ double sh[1024];
@@ -427,6 +575,25 @@ cudaError_t launch_adam(const AdamArgs& a, int grid, cudaStream_t s, int cap_two
     attr_set = true;
   }
   adam_kernel<<<grid, kAdamBlock, cap_two_per_sm ? 80 * 1024 : 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+// TMA pipeline: persistent grid (one CTA per SM); stages sized to ~200 KB.
+cudaError_t launch_adam_tma(const AdamArgs& a, int sms, cudaStream_t s) {
+  int gmax = 1;
+  for (int i = 0; i < a.nseg; ++i) gmax = a.seg[i].gnin > gmax ? a.seg[i].gnin : gmax;
+  const size_t stage = (size_t)kTmaTile * (2 * gmax + 12);
+  int stages = (int)((200 * 1024) / stage);
+  if (stages > 4) stages = 4;
+  if (stages < 2) stages = 2;
+  const size_t smem = stage * stages;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(adam_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  adam_tma_kernel<<<sms, kTmaThreads, smem, s>>>(a, gmax, stages);
   return cudaGetLastError();
 }
 

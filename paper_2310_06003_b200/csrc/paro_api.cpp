@@ -155,6 +155,15 @@ char* data_ptr(const PlanT* p, int rank, int kind, int64_t off) {
   return p->peer_base[rank] + kHeaderBytes + 2 * (pl.buf_off[kind] + off);
 }
 
+// which rank's region a resolved device pointer belongs to (-1: none)
+int data_rank(const PlanT* p, const void* ptr) {
+  const char* c = static_cast<const char*>(ptr);
+  const size_t bytes = kHeaderBytes + 2 * (size_t)p->pl->region_elems;
+  for (int r = 0; r < (int)p->peer_base.size(); ++r)
+    if (p->peer_base[r] && c >= p->peer_base[r] && c < p->peer_base[r] + bytes) return r;
+  return -1;
+}
+
 DTask resolve(const PlanT* p, const Task& t) {
   DTask d{};
   d.nin = t.nin;
@@ -381,6 +390,7 @@ void paro_opts_default(paro_opts_t* o) {
   o->comm_ctas = 148;
   o->pipeline_depth = 2;
   o->pull_transport = 1;
+  o->adam_impl = 0;
   o->stream = nullptr;
 }
 
@@ -767,6 +777,7 @@ paro_status_t paro_step(paro_plan_t p, const void* const* grads, void* const* pa
     CK(cudaStreamWaitEvent(ctx->comm, p->ev_comp, 0));
   }
   CK(cudaMemsetAsync(p->d_nonfinite, 0, sizeof(int), ctx->comp));
+  CK(cudaMemsetAsync(p->d_partials, 0, sizeof(double) * p->partials_cap, ctx->comp));
 
   const int nb = (int)pl.buckets.size();
   const int grid = adam_grid();
@@ -800,7 +811,14 @@ paro_status_t paro_step(paro_plan_t p, const void* const* grads, void* const* pa
     int64_t elems = 0;
     for (int i = 0; i < aa.nseg; ++i) elems += 8 * aa.seg[i].n8;
     const int pk = prof_begin(p, ctx->comp, 0, elems);
-    CK(launch_adam(aa, grid, ctx->comp, (ctx->mode == MODE_REAL && pl.N > 1) ? 1 : 0));
+    // TMA-pipelined Adam when every operand is in local memory (bulk copies
+    // are not used on NVLink peer addresses); otherwise the LSU kernel.
+    bool all_local = p->opts.adam_impl != 1;
+    for (int i = 0; i < aa.nseg && all_local; ++i)
+      for (int k = 0; k < aa.seg[i].gnin; ++k)
+        if (ctx->mode == MODE_REAL && data_rank(p, aa.seg[i].gin[k]) != ctx->rank) all_local = false;
+    if (all_local) CK(launch_adam_tma(aa, ctx->sm_count, ctx->comp));
+    else CK(launch_adam(aa, grid, ctx->comp, (ctx->mode == MODE_REAL && pl.N > 1) ? 1 : 0));
     prof_end(p, ctx->comp, pk);
     ++n_adam;
     ++launches;

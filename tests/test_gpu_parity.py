@@ -31,11 +31,12 @@ def _paro():
 class EmuRun:
     """All ranks of one split on cuda:0 through the C ABI."""
 
-    def __init__(self, N, M, code, sizes, B, topo="ho", depth=2, wd=0.0, loss_scale=1.0, transport="push"):
+    def __init__(self, N, M, code, sizes, B, topo="ho", depth=2, wd=0.0, loss_scale=1.0, transport="push",
+                 adam_impl="auto"):
         paro = _paro()
         self.ctx = paro.Context(N, M, mode="emulated", device=0)
         self.pl = paro.Plan(self.ctx, code, sizes, bucket_elems=B, topology=topo, pipeline_depth=depth,
-                            weight_decay=wd, loss_scale=loss_scale, transport=transport)
+                            weight_decay=wd, loss_scale=loss_scale, transport=transport, adam_impl=adam_impl)
         self.info = self.pl.info()
         self.N, self.code, self.sizes = N, code, sizes
         n = self.info["os_numel"]
@@ -125,11 +126,12 @@ def test_synth_generator_matches_host():
 
 
 # --------------------------------------------------------------------- N = 1
+@pytest.mark.parametrize("adam_impl", ["auto", "lsu"])
 @pytest.mark.parametrize("wd,ls", [(0.0, 1.0), (0.1, 4.0)])
-def test_n1_ten_steps_bit_exact(wd, ls):
-    sizes = [50_000, 4096, 12_345]
+def test_n1_ten_steps_bit_exact(wd, ls, adam_impl):
+    sizes = [50_000, 4096, 12_345, 3 * 4096 * 148 + 8]   # > one tile per CTA, ragged tail
     lay = L.Layout(sizes, 1, 1, 1 << 14)
-    run = EmuRun(1, 1, "NNN", sizes, 1 << 14, wd=wd, loss_scale=ls)
+    run = EmuRun(1, 1, "NNN", sizes, 1 << 14, wd=wd, loss_scale=ls, adam_impl=adam_impl)
     ref = _dp_reference(lay, 10, wd=wd, loss_scale=ls)
     for t in range(1, 11):
         run.set_grads(t)
@@ -196,12 +198,13 @@ def test_flat_ring_matches_oracle_flat_simulation(transport):
         run.close()
 
 
+@pytest.mark.parametrize("adam_impl", ["auto", "lsu"])
 @pytest.mark.parametrize("code", ["IIG", "NNN", "III", "GGG"])
-def test_4m_2x4_ten_steps(code):
+def test_4m_2x4_ten_steps(code, adam_impl):
     N, M = 8, 4
     lay = L.Layout(CONFIG_4M["sizes"], N, M, CONFIG_4M["B"])
     ref = _dp_reference(lay, 10)
-    run = EmuRun(N, M, code, CONFIG_4M["sizes"], CONFIG_4M["B"])
+    run = EmuRun(N, M, code, CONFIG_4M["sizes"], CONFIG_4M["B"], adam_impl=adam_impl)
     for t in range(1, 11):
         run.set_grads(t)
         run.step(t)

@@ -29,12 +29,14 @@ def main():
     ap.add_argument("--grid", default="{}")
     a = ap.parse_args()
     grid = {"strategy": ["IIG"], "topology": ["ho"], "transport": ["pull"], "comm_ctas": [148],
-            "bucket": [1 << 26], "depth": [2]}
+            "bucket": [1 << 26], "depth": [2], "adam_impl": ["auto"]}
     grid.update(json.loads(a.grid))
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
+    if world == 1:
+        pass
     if world > 1:
         dist.init_process_group("cpu:gloo,cuda:nccl", rank=rank, world_size=world)
     from paper_2310_06003_b200 import paro
@@ -54,7 +56,7 @@ def main():
         try:
             plan = paro.Plan(ctx, cfg["strategy"], sizes, bucket_elems=cfg["bucket"], topology=cfg["topology"],
                              comm_ctas=cfg["comm_ctas"], pipeline_depth=cfg["depth"], stream=stream.cuda_stream,
-                             transport=cfg["transport"])
+                             transport=cfg["transport"], adam_impl=cfg["adam_impl"])
         except Exception as e:  # noqa: BLE001
             if rank == 0:
                 print(json.dumps({"cfg": cfg, "error": str(e)}), flush=True)
