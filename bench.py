@@ -258,11 +258,18 @@ def run_ours(args):
     adam_ms = prof["adam_ms"] / max(1, prof["adam_launches"])
     comm_ms = prof["comm_ms"] / max(1, prof["comm_launches"])
     if prof["adam_ms"] >= prof["comm_ms"] or prof["comm_launches"] == 0:
-        alg = 28.0 * prof["adam_elems"] / max(1, prof["adam_launches"])
+        elems_per_launch = prof["adam_elems"] / max(1, prof["adam_launches"])
+        alg = 28.0 * elems_per_launch
         ach = alg / (adam_ms / 1000.0) / 1e9
         peak = float(peaks["hbm_gbs"])
-        roof = {"bound": "hbm", "kernel": "adam_kernel (fused unscale+Adam+bf16 cast+norm)", "achieved": ach,
-                "peak": peak, "unit": "GB/s", "frac": ach / peak, "traffic": traffic.get("adam_kernel"),
+        # which Adam kernel ran: TMA pipeline when every operand is local (N = 1, push), else LSU
+        kname = "adam_tma_kernel" if args.adam_impl == "auto" and (N == 1 or args.transport == "push") \
+            else "adam_kernel"
+        tr = traffic.get(kname)
+        roof = {"bound": "hbm", "kernel": f"{kname} (fused unscale+Adam+bf16 cast+norm)", "achieved": ach,
+                "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                "traffic": (tr["dram_bytes_per_elem"] * elems_per_launch) if tr else None,
+                "traffic_source": tr["source"] if tr else None,
                 "algorithmic_bytes_per_launch": alg, "launch_ms": adam_ms, "peak_source": peak_kind,
                 "share_of_step": prof["adam_ms"] / max(1e-9, ms * args.steps)}
     else:
@@ -271,7 +278,7 @@ def run_ours(args):
         peak = 770.0
         roof = {"bound": "nvlink", "kernel": "rounds_kernel (collective rounds, NVLink pull + hop)",
                 "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
-                "traffic": traffic.get("rounds_kernel"), "algorithmic_bytes_per_launch": alg,
+                "traffic": None, "algorithmic_bytes_per_launch": alg,
                 "launch_ms": comm_ms, "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s/dir",
                 "share_of_step": prof["comm_ms"] / max(1e-9, ms * args.steps)}
 
