@@ -263,8 +263,7 @@ def run_ours(args):
         ach = alg / (adam_ms / 1000.0) / 1e9
         peak = float(peaks["hbm_gbs"])
         # which Adam kernel ran: TMA pipeline when every operand is local (N = 1, push), else LSU
-        kname = "adam_tma_kernel" if args.adam_impl == "auto" and (N == 1 or args.transport == "push") \
-            else "adam_kernel"
+        kname = "adam_tma_kernel" if args.adam_impl == "auto" else "adam_kernel"
         tr = traffic.get(kname)
         roof = {"bound": "hbm", "kernel": f"{kname} (fused unscale+Adam+bf16 cast+norm)", "achieved": ach,
                 "peak": peak, "unit": "GB/s", "frac": ach / peak,

@@ -83,8 +83,9 @@ typedef struct {
   int pull_transport;    /* 1 (default): ranks LOAD their ring predecessor's data   *
                           * over NVLink (pull); 0: ranks STORE into their          *
                           * successor's buffers (push).  Same bits either way.     */
-  int adam_impl;         /* 0 (default): TMA bulk-copy pipeline when every operand  *
-                          * is local, else LSU kernel; 1: always the LSU kernel     */
+  int adam_impl;         /* 0 (default): TMA bulk-copy pipeline (cp.async.bulk +    *
+                          * mbarrier stages; also pulls NVLink-peer operands);      *
+                          * 1: the LSU (ld.global) kernel                           */
   void* stream;          /* cudaStream_t the step is ordered on; NULL = ctx stream */
 } paro_opts_t;
 

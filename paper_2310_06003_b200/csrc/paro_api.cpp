@@ -811,13 +811,9 @@ paro_status_t paro_step(paro_plan_t p, const void* const* grads, void* const* pa
     int64_t elems = 0;
     for (int i = 0; i < aa.nseg; ++i) elems += 8 * aa.seg[i].n8;
     const int pk = prof_begin(p, ctx->comp, 0, elems);
-    // TMA-pipelined Adam when every operand is in local memory (bulk copies
-    // are not used on NVLink peer addresses); otherwise the LSU kernel.
-    bool all_local = p->opts.adam_impl != 1;
-    for (int i = 0; i < aa.nseg && all_local; ++i)
-      for (int k = 0; k < aa.seg[i].gnin; ++k)
-        if (ctx->mode == MODE_REAL && data_rank(p, aa.seg[i].gin[k]) != ctx->rank) all_local = false;
-    if (all_local) CK(launch_adam_tma(aa, ctx->sm_count, ctx->comp));
+    // TMA-pipelined Adam (bulk copies also pull the fused hop's NVLink-peer
+    // inputs: tools/tma_peer_test.cu measured 782 GB/s); LSU kernel on request.
+    if (p->opts.adam_impl != 1) CK(launch_adam_tma(aa, ctx->sm_count, ctx->comp));
     else CK(launch_adam(aa, grid, ctx->comp, (ctx->mode == MODE_REAL && pl.N > 1) ? 1 : 0));
     prof_end(p, ctx->comp, pk);
     ++n_adam;
