@@ -43,7 +43,7 @@ def parse():
     ap.add_argument("--strategy", default="IIG")
     ap.add_argument("--group-size", type=int, default=0, help="M; default N/2 for N>=4, else 1")
     ap.add_argument("--topology", default="ho", choices=["ho", "two_step", "flat", "direct", "nccl"])
-    ap.add_argument("--bucket", type=int, default=1 << 26)
+    ap.add_argument("--bucket", type=int, default=1 << 28)
     ap.add_argument("--comm-ctas", type=int, default=148)
     ap.add_argument("--depth", type=int, default=2)
     ap.add_argument("--transport", default="pull", choices=["pull", "push"])
