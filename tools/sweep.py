@@ -27,6 +27,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=2)
     ap.add_argument("--group-size", type=int, default=0)
     ap.add_argument("--grid", default="{}")
+    ap.add_argument("--collective-only", action="store_true",
+                    help="time paro_collective(reduce) + paro_collective(gather) per step, no Adam")
     a = ap.parse_args()
     grid = {"strategy": ["IIG"], "topology": ["ho"], "transport": ["pull"], "comm_ctas": [148],
             "bucket": [1 << 26], "depth": [2], "adam_impl": ["auto"]}
@@ -67,9 +69,15 @@ def main():
         plan.opt_state_init(rank, ptrs[0], seed=SEED)
         plan.synth_grads(rank, SEED, 1)
         s = 0
+        def one_step(s):
+            if a.collective_only:
+                plan.collective(0)
+                plan.collective(1)
+            else:
+                plan.step(ptrs, 3e-4, s)
         for _ in range(a.warmup):
             s += 1
-            plan.step(ptrs, 3e-4, s)
+            one_step(s)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -78,7 +86,7 @@ def main():
         e0.record(stream)
         for _ in range(a.steps):
             s += 1
-            plan.step(ptrs, 3e-4, s)
+            one_step(s)
         e1.record(stream)
         torch.cuda.synchronize()
         prof = plan.profile_stop()
