@@ -48,6 +48,7 @@ def parse():
     ap.add_argument("--depth", type=int, default=2)
     ap.add_argument("--transport", default="pull", choices=["pull", "push"])
     ap.add_argument("--adam-impl", default="auto", choices=["auto", "lsu"])
+    ap.add_argument("--comm-impl", default="tma", choices=["tma", "lsu"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -210,7 +211,7 @@ def run_ours(args):
     torch.cuda.set_stream(stream)
     plan = paro.Plan(ctx, args.strategy, sizes, bucket_elems=args.bucket, topology=args.topology,
                      comm_ctas=args.comm_ctas, pipeline_depth=args.depth, stream=stream.cuda_stream,
-                     transport=args.transport, adam_impl=args.adam_impl)
+                     transport=args.transport, adam_impl=args.adam_impl, comm_impl=args.comm_impl)
     info = plan.info()
     st = [torch.empty(info["os_numel"], dtype=torch.float32, device="cuda") for _ in range(3)]
     ptrs = [[t.data_ptr() for t in st]]
@@ -275,7 +276,8 @@ def run_ours(args):
         alg = prof["comm_bytes"] / max(1, prof["comm_launches"])
         ach = alg / (comm_ms / 1000.0) / 1e9
         peak = 770.0
-        roof = {"bound": "nvlink", "kernel": "rounds_kernel (collective rounds, NVLink pull + hop)",
+        roof = {"bound": "nvlink", "kernel": ("rounds_tma_kernel" if args.comm_impl == "tma" else "rounds_kernel")
+                + " (collective rounds: NVLink pull + hop)",
                 "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
                 "traffic": None, "algorithmic_bytes_per_launch": alg,
                 "launch_ms": comm_ms, "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s/dir",
@@ -338,7 +340,7 @@ def run_ours(args):
                        "n_tensors": len(sizes), "strategy": args.strategy, "groups": f"{N // M}x{M}",
                        "topology": args.topology, "bucket_elems": info["bucket_elems"],
                        "n_buckets": info["n_buckets"], "comm_ctas": args.comm_ctas, "pipeline_depth": args.depth,
-                       "transport": args.transport, "adam_impl": args.adam_impl,
+                       "transport": args.transport, "adam_impl": args.adam_impl, "comm_impl": args.comm_impl,
                        "l2": "no flush: per-step inputs (13.5 GB grads + 81 GB/div(OS) state) >> 126 MB L2",
                        "intra_inter_gap": "not emulated: one NVSwitch box, intra/inter are labels"},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,

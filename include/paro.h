@@ -86,6 +86,8 @@ typedef struct {
   int adam_impl;         /* 0 (default): TMA bulk-copy pipeline (cp.async.bulk +    *
                           * mbarrier stages; also pulls NVLink-peer operands);      *
                           * 1: the LSU (ld.global) kernel                           */
+  int comm_impl;         /* 0 (default): collective rounds move operands with TMA  *
+                          * bulk copies into shared memory; 1: LSU kernel           */
   void* stream;          /* cudaStream_t the step is ordered on; NULL = ctx stream */
 } paro_opts_t;
 

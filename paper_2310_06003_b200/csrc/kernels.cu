@@ -463,6 +463,119 @@ __global__ void __launch_bounds__(kTmaThreads, 1) adam_tma_kernel(const AdamArgs
   }
 }
 
+// ------------------------------------------------------------- rounds, TMA pipeline
+// The collective rounds with the operand streams moved by the bulk-copy engine:
+// for every tile (4096 elements) of a fold task, one thread issues
+// cp.async.bulk for each input — NVLink-peer or local — into a 4-stage
+// shared-memory ring (mbarrier complete_tx); 8 warps fold from shared memory
+// and store the result.  Memory-level parallelism no longer costs registers,
+// so the kernel keeps NVLink busy beside the Adam kernel.  Tasks with more
+// than kRtMaxIn inputs (direct topology, large M or g) use the LSU path.
+constexpr int kRtThreads = 256;
+constexpr int kRtTileE = 4096;
+constexpr int kRtTileB = kRtTileE * 2;
+constexpr int kRtStages = 4;
+constexpr int kRtMaxIn = 3;
+
+__device__ __forceinline__ bool rt_tile(const RoundsArgs& a, const DRound& rd, int64_t t, const DTask*& task,
+                                        int64_t& e0, int& ne) {
+  for (int ti = rd.t0; ti < rd.t1; ++ti) {
+    const DTask* tk = a.tasks + ti;
+    if (tk->nin > kRtMaxIn) continue;
+    const int64_t n = tk->n8 * 8;
+    const int64_t nt = (n + kRtTileE - 1) / kRtTileE;
+    if (t < nt) {
+      task = tk;
+      e0 = t * kRtTileE;
+      ne = (int)min((int64_t)kRtTileE, n - e0);
+      return true;
+    }
+    t -= nt;
+  }
+  return false;
+}
+
+__global__ void __launch_bounds__(kRtThreads) rounds_tma_kernel(const RoundsArgs a, int max_in) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ uint64_t bars[kRtStages];
+  if (a.bar.err && *(volatile int*)a.bar.err) return;   // sticky device error: do nothing
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kRtStages; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const size_t stage_bytes = (size_t)max_in * kRtTileB;
+  uint32_t cnt = 0;   // tiles this CTA has consumed so far (stage = cnt % S, parity = cnt / S)
+  int bidx = 0;
+  trace_stamp(a, 0);
+  for (int r = 0; r < a.nrounds; ++r) {
+    const DRound rd = a.rounds[r];
+    if (a.bar.my_flags && !grid_peer_barrier(a, rd.peers_before, bidx++)) return;
+    // order the peers' released (generic-proxy) writes before our async-proxy reads
+    if (threadIdx.x == 0) asm volatile("fence.proxy.async;" ::: "memory");
+    trace_stamp(a, 1 + 2 * r);
+    int64_t total = 0;
+    for (int ti = rd.t0; ti < rd.t1; ++ti) {
+      const DTask* tk = a.tasks + ti;
+      if (tk->nin <= kRtMaxIn) total += (tk->n8 * 8 + kRtTileE - 1) / kRtTileE;
+    }
+    const int64_t mine = (total > blockIdx.x) ? (total - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    auto issue = [&](int64_t k) {
+      const DTask* tk;
+      int64_t e0;
+      int ne;
+      rt_tile(a, rd, blockIdx.x + k * gridDim.x, tk, e0, ne);
+      const uint32_t slot = (cnt + (uint32_t)k) % kRtStages;
+      unsigned char* base = smem + slot * stage_bytes;
+      const uint32_t bytes = (uint32_t)ne * 2;
+      mbar_expect_tx(&bars[slot], bytes * tk->nin);
+      for (int i = 0; i < tk->nin; ++i) bulk_g2s(base + i * kRtTileB, tk->in[i] + e0, bytes, &bars[slot]);
+    };
+    if (threadIdx.x == 0)
+      for (int64_t k = 0; k < min((int64_t)kRtStages, mine); ++k) issue(k);
+    for (int64_t k = 0; k < mine; ++k) {
+      const uint32_t c = cnt + (uint32_t)k;
+      const uint32_t slot = c % kRtStages;
+      mbar_wait(&bars[slot], (c / kRtStages) & 1u);
+      const DTask* tk;
+      int64_t e0;
+      int ne;
+      rt_tile(a, rd, blockIdx.x + k * gridDim.x, tk, e0, ne);
+      const unsigned char* base = smem + slot * stage_bytes;
+      const int nin = tk->nin;
+      const uint32_t raw = tk->rawmask;
+      uint4* dst = reinterpret_cast<uint4*>(tk->dst + e0);
+      for (int u = threadIdx.x; u < ne / 8; u += kRtThreads) {
+        const uint4 v0 = reinterpret_cast<const uint4*>(base)[u];
+        if (nin == 1 && !(raw & 1u)) {
+          __stcg(dst + u, v0);
+          continue;
+        }
+        float acc[8];
+        unpack8(v0, acc);
+        if (raw & 1u) scale_round8(acc, a.alpha);
+        for (int i = 1; i < nin; ++i) {
+          float x[8];
+          unpack8(reinterpret_cast<const uint4*>(base + i * kRtTileB)[u], x);
+          if ((raw >> i) & 1u) scale_round8(x, a.alpha);
+          hop8(acc, x);
+        }
+        __stcg(dst + u, pack8(acc));
+      }
+      __syncthreads();   // stage consumed by every thread: refill it
+      if (threadIdx.x == 0 && k + kRtStages < mine) issue(k + kRtStages);
+    }
+    cnt += (uint32_t)mine;
+    // tasks with many inputs: LSU path over the whole grid
+    for (int ti = rd.t0; ti < rd.t1; ++ti)
+      if (a.tasks[ti].nin > kRtMaxIn) run_task(a.tasks + ti, a.alpha);
+    __syncthreads();
+    trace_stamp(a, 2 + 2 * r);
+  }
+  if (a.bar.my_flags && a.final_barrier) grid_peer_barrier(a, a.final_peers, bidx++);
+  trace_stamp(a, kTraceSlots - 1);
+}
+
 // ------------------------------------------------------------- norm finalize
 __global__ void __launch_bounds__(1024) norm_finalize_kernel(const double* p, int n, double* out) {
   __shared__ double sh[1024];
@@ -564,6 +677,20 @@ cudaError_t launch_rounds(const RoundsArgs& a, int grid, int block, cudaStream_t
   return cudaGetLastError();
 }
 
+cudaError_t launch_rounds_tma(const RoundsArgs& a, int grid, int max_in, cudaStream_t s) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(rounds_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         kRtStages * kRtMaxIn * kRtTileB);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  if (max_in < 1) max_in = 1;
+  if (max_in > kRtMaxIn) max_in = kRtMaxIn;
+  rounds_tma_kernel<<<grid, kRtThreads, (size_t)kRtStages * max_in * kRtTileB, s>>>(a, max_in);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_adam(const AdamArgs& a, int grid, cudaStream_t s, int cap_two_per_sm) {
   // With collectives running concurrently, Adam is capped at two CTAs per SM
   // (an 80 KB shared-memory reservation) so a 512-thread collective CTA always
@@ -579,11 +706,11 @@ cudaError_t launch_adam(const AdamArgs& a, int grid, cudaStream_t s, int cap_two
 }
 
 // TMA pipeline: persistent grid (one CTA per SM); stages sized to ~200 KB.
-cudaError_t launch_adam_tma(const AdamArgs& a, int sms, cudaStream_t s) {
+cudaError_t launch_adam_tma(const AdamArgs& a, int sms, cudaStream_t s, int smem_budget_kb) {
   int gmax = 1;
   for (int i = 0; i < a.nseg; ++i) gmax = a.seg[i].gnin > gmax ? a.seg[i].gnin : gmax;
   const size_t stage = (size_t)kTmaTile * (2 * gmax + 12);
-  int stages = (int)((200 * 1024) / stage);
+  int stages = (int)(((size_t)smem_budget_kb * 1024) / stage);
   if (stages > 4) stages = 4;
   if (stages < 2) stages = 2;
   const size_t smem = stage * stages;

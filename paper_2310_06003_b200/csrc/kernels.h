@@ -94,7 +94,8 @@ struct PackEntry {     // one tensor slice: src/dst element pointers + count
 // launchers (return cudaGetLastError())
 cudaError_t launch_rounds(const RoundsArgs& a, int grid, int block, cudaStream_t s);
 cudaError_t launch_adam(const AdamArgs& a, int grid, cudaStream_t s, int cap_two_per_sm);
-cudaError_t launch_adam_tma(const AdamArgs& a, int sms, cudaStream_t s);
+cudaError_t launch_adam_tma(const AdamArgs& a, int sms, cudaStream_t s, int smem_budget_kb);
+cudaError_t launch_rounds_tma(const RoundsArgs& a, int grid, int max_in, cudaStream_t s);
 cudaError_t launch_norm_finalize(const double* partials, int n, double* out, cudaStream_t s);
 cudaError_t launch_pack(const PackEntry* table, int n_entries, int64_t max_n, cudaStream_t s);
 cudaError_t launch_synth_grad(uint16_t* dst, int64_t psi, int64_t psi_pad, uint64_t key, cudaStream_t s);

@@ -48,6 +48,7 @@ struct paro_ctx {
 };
 
 struct DevLaunch {
+  int max_in = 1;          // largest fold input count (TMA stage sizing)
   int64_t bytes = 0;       // bytes the local rank(s) send in this launch
   int64_t round_off = 0;   // index into the plan's DRound array
   int nrounds = 0;
@@ -207,6 +208,7 @@ paro_status_t upload_schedule(PlanT* p) {
         d.peers_before = 0;
       }
       d.t1 = (int32_t)tasks.size();
+      for (int ti = d.t0; ti < d.t1; ++ti) dl.max_in = std::max(dl.max_in, std::min(3, (int)tasks[ti].nin));
       rounds.push_back(d);
     }
     dl.nrounds = R;
@@ -293,7 +295,8 @@ paro_status_t run_launch(PlanT* p, const DevLaunch& dl, int* nlaunch) {
       p->trace_nrounds.push_back(dl.nrounds);
       p->trace_grid = grid;
     }
-    CK(launch_rounds(a, grid, 0, ctx->comm));
+    if (p->opts.comm_impl == 0) CK(launch_rounds_tma(a, grid, dl.max_in, ctx->comm));
+    else CK(launch_rounds(a, grid, 0, ctx->comm));
     prof_end(p, ctx->comm, k);
     ++*nlaunch;
   } else {
@@ -301,7 +304,8 @@ paro_status_t run_launch(PlanT* p, const DevLaunch& dl, int* nlaunch) {
       a.rounds = p->d_rounds + dl.round_off + r;
       a.nrounds = 1;
       const int k = prof_begin(p, ctx->comm, 1, r == 0 ? dl.bytes : 0);
-      CK(launch_rounds(a, grid, 0, ctx->comm));
+      if (p->opts.comm_impl == 0) CK(launch_rounds_tma(a, grid, dl.max_in, ctx->comm));
+      else CK(launch_rounds(a, grid, 0, ctx->comm));
       prof_end(p, ctx->comm, k);
       ++*nlaunch;
     }
@@ -391,6 +395,7 @@ void paro_opts_default(paro_opts_t* o) {
   o->pipeline_depth = 2;
   o->pull_transport = 1;
   o->adam_impl = 0;
+  o->comm_impl = 0;
   o->stream = nullptr;
 }
 
@@ -813,7 +818,10 @@ paro_status_t paro_step(paro_plan_t p, const void* const* grads, void* const* pa
     const int pk = prof_begin(p, ctx->comp, 0, elems);
     // TMA-pipelined Adam (bulk copies also pull the fused hop's NVLink-peer
     // inputs: tools/tma_peer_test.cu measured 782 GB/s); LSU kernel on request.
-    if (p->opts.adam_impl != 1) CK(launch_adam_tma(aa, ctx->sm_count, ctx->comp));
+    // while collectives run beside it (real N > 1) Adam keeps ~120 KB of shared
+    // memory per SM so the TMA collective kernel (<= 96 KB) fits on the same SM
+    if (p->opts.adam_impl != 1)
+      CK(launch_adam_tma(aa, ctx->sm_count, ctx->comp, (ctx->mode == MODE_REAL && pl.N > 1) ? 120 : 200));
     else CK(launch_adam(aa, grid, ctx->comp, (ctx->mode == MODE_REAL && pl.N > 1) ? 1 : 0));
     prof_end(p, ctx->comp, pk);
     ++n_adam;

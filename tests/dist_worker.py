@@ -32,6 +32,7 @@ def main():
     codes = cfg.get("codes", ["NNN", "IIG", "NIG", "IGG", "GGG", "III", "INI", "NNG"])
     topos = cfg.get("topos", ["ho", "two_step", "direct"])
     transports = cfg.get("transports", ["push"])
+    comm_impl = cfg.get("comm_impl", "tma")
     sizes = cfg.get("sizes", [world * 64 * 40 + 24, 333])
     B = cfg.get("bucket", world * 64 * 12)
     steps = cfg.get("steps", 2)
@@ -42,7 +43,7 @@ def main():
         ctx = paro.Context(world, M, mode="real", rank=rank, device=local, uid=bytes(t.tolist()))
         for code, topo, tr in [(c, t_, x) for c in codes for t_ in topos for x in transports]:
             if True:
-                pl = paro.Plan(ctx, code, sizes, bucket_elems=B, topology=topo, transport=tr)
+                pl = paro.Plan(ctx, code, sizes, bucket_elems=B, topology=topo, transport=tr, comm_impl=comm_impl)
                 info = pl.info()
                 st = [torch.empty(info["os_numel"], dtype=torch.float32, device="cuda") for _ in range(3)]
                 ptrs = [[x.data_ptr() for x in st]]

@@ -32,11 +32,12 @@ class EmuRun:
     """All ranks of one split on cuda:0 through the C ABI."""
 
     def __init__(self, N, M, code, sizes, B, topo="ho", depth=2, wd=0.0, loss_scale=1.0, transport="push",
-                 adam_impl="auto"):
+                 adam_impl="auto", comm_impl="tma"):
         paro = _paro()
         self.ctx = paro.Context(N, M, mode="emulated", device=0)
         self.pl = paro.Plan(self.ctx, code, sizes, bucket_elems=B, topology=topo, pipeline_depth=depth,
-                            weight_decay=wd, loss_scale=loss_scale, transport=transport, adam_impl=adam_impl)
+                            weight_decay=wd, loss_scale=loss_scale, transport=transport, adam_impl=adam_impl,
+                            comm_impl=comm_impl)
         self.info = self.pl.info()
         self.N, self.code, self.sizes = N, code, sizes
         n = self.info["os_numel"]
@@ -145,14 +146,16 @@ def test_n1_ten_steps_bit_exact(wd, ls, adam_impl):
 CONFIG_4M = dict(sizes=[1 << 22], B=1 << 18)   # BASELINE config 1: 2^22 params, 16 buckets
 
 
+@pytest.mark.parametrize("comm_impl", ["tma", "lsu"])
 @pytest.mark.parametrize("transport", ["push", "pull"])
 @pytest.mark.parametrize("topo", ["ho", "two_step", "direct"])
-def test_4m_2x4_every_strategy_one_step(topo, transport):
+def test_4m_2x4_every_strategy_one_step(topo, transport, comm_impl):
     N, M = 8, 4
     lay = L.Layout(CONFIG_4M["sizes"], N, M, CONFIG_4M["B"])
     ref = _dp_reference(lay, 1)
     for code in S.paro_strategies():
-        run = EmuRun(N, M, code, CONFIG_4M["sizes"], CONFIG_4M["B"], topo=topo, transport=transport)
+        run = EmuRun(N, M, code, CONFIG_4M["sizes"], CONFIG_4M["B"], topo=topo, transport=transport,
+                     comm_impl=comm_impl)
         run.set_grads(1)
         stats = run.step(1)
         assert abs(stats["grad_norm"] ** 2 - ref[4][0]) <= 1e-12 * ref[4][0]

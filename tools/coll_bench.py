@@ -23,7 +23,8 @@ def main():
     ap.add_argument("--group-size", type=int, default=0)
     ap.add_argument("--iters", type=int, default=10)
     ap.add_argument("--comm-ctas", type=int, default=148)
-    ap.add_argument("--transport", default="push")
+    ap.add_argument("--transport", default="pull")
+    ap.add_argument("--comm-impl", default="tma")
     a = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -60,7 +61,7 @@ def main():
         for topo in a.topos.split(","):
             bucket = min(elems, 1 << 28)
             pl = paro.Plan(ctx, "NNN", [elems], bucket_elems=bucket, topology=topo, comm_ctas=a.comm_ctas,
-                           stream=stream.cuda_stream, transport=a.transport)
+                           stream=stream.cuda_stream, transport=a.transport, comm_impl=a.comm_impl)
             pl.synth_grads(rank, 1234, 1)
             ms = timeit(lambda: pl.collective(0))
             row[topo] = {"ms": round(ms, 4), "busbw_GBps": round(nbytes * 2 * (world - 1) / world / (ms / 1e3) / 1e9, 1)}
