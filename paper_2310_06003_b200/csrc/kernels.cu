@@ -672,12 +672,33 @@ __global__ void init_range_kernel(const float* src, uint64_t key, int64_t begin,
 int adam_grid() { return 148 * 8; }
 int adam_block() { return kAdamBlock; }
 
+// All kernels that may share an SM prefer the maximum shared-memory carveout,
+// so the SM never has to drain to re-split L1/shared between a collective CTA
+// and an Adam CTA.
+static cudaError_t set_carveouts() {
+  static bool done = false;
+  if (done) return cudaSuccess;
+  const void* fns[] = {(const void*)rounds_kernel, (const void*)rounds_tma_kernel, (const void*)adam_kernel,
+                       (const void*)adam_tma_kernel};
+  for (const void* f : fns) {
+    cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                         (int)cudaSharedmemCarveoutMaxShared);
+    if (e != cudaSuccess) return e;
+  }
+  done = true;
+  return cudaSuccess;
+}
+
 cudaError_t launch_rounds(const RoundsArgs& a, int grid, int block, cudaStream_t s) {
+  cudaError_t e = set_carveouts();
+  if (e != cudaSuccess) return e;
   rounds_kernel<<<grid, block > 0 ? block : kRoundsBlock, 0, s>>>(a);
   return cudaGetLastError();
 }
 
 cudaError_t launch_rounds_tma(const RoundsArgs& a, int grid, int max_in, cudaStream_t s) {
+  cudaError_t ec = set_carveouts();
+  if (ec != cudaSuccess) return ec;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(rounds_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -692,6 +713,8 @@ cudaError_t launch_rounds_tma(const RoundsArgs& a, int grid, int max_in, cudaStr
 }
 
 cudaError_t launch_adam(const AdamArgs& a, int grid, cudaStream_t s, int cap_two_per_sm) {
+  cudaError_t ec = set_carveouts();
+  if (ec != cudaSuccess) return ec;
   // With collectives running concurrently, Adam is capped at two CTAs per SM
   // (an 80 KB shared-memory reservation) so a 512-thread collective CTA always
   // fits beside it (registers: 2 x 256 x 80 + 512 x 48 = 64K).
@@ -707,6 +730,8 @@ cudaError_t launch_adam(const AdamArgs& a, int grid, cudaStream_t s, int cap_two
 
 // TMA pipeline: persistent grid (one CTA per SM); stages sized to ~200 KB.
 cudaError_t launch_adam_tma(const AdamArgs& a, int sms, cudaStream_t s, int smem_budget_kb) {
+  cudaError_t ec = set_carveouts();
+  if (ec != cudaSuccess) return ec;
   int gmax = 1;
   for (int i = 0; i < a.nseg; ++i) gmax = a.seg[i].gnin > gmax ? a.seg[i].gnin : gmax;
   const size_t stage = (size_t)kTmaTile * (2 * gmax + 12);
