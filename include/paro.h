@@ -88,6 +88,11 @@ typedef struct {
                           * 1: the LSU (ld.global) kernel                           */
   int comm_impl;         /* 0 (default): collective rounds move operands with TMA  *
                           * bulk copies into shared memory; 1: LSU kernel           */
+  float inter_gbps;      /* > 0: emulate a slow inter-group link — each rank's     *
+                          * inter-group transfers are paced to this many GB/s (TMA *
+                          * rounds kernel; the final hop is then not fused into    *
+                          * Adam).  0 (default): no pacing.  One NVSwitch box has  *
+                          * no real intra/inter gap.                */
   void* stream;          /* cudaStream_t the step is ordered on; NULL = ctx stream */
 } paro_opts_t;
 

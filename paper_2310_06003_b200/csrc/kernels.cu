@@ -520,11 +520,17 @@ __global__ void __launch_bounds__(kRtThreads) rounds_tma_kernel(const RoundsArgs
       if (tk->nin <= kRtMaxIn) total += (tk->n8 * 8 + kRtTileE - 1) / kRtTileE;
     }
     const int64_t mine = (total > blockIdx.x) ? (total - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    const uint64_t t_round = globaltimer();
+    double inter_sent = 0.0;   // bytes of inter-group tiles this CTA has issued in this round
     auto issue = [&](int64_t k) {
       const DTask* tk;
       int64_t e0;
       int ne;
       rt_tile(a, rd, blockIdx.x + k * gridDim.x, tk, e0, ne);
+      if (tk->inter && a.inter_bytes_per_ns > 0.0) {   // token bucket: emulated slow inter link
+        inter_sent += (double)ne * 2.0;
+        while (inter_sent > (double)(globaltimer() - t_round) * a.inter_bytes_per_ns) __nanosleep(256);
+      }
       const uint32_t slot = (cnt + (uint32_t)k) % kRtStages;
       unsigned char* base = smem + slot * stage_bytes;
       const uint32_t bytes = (uint32_t)ne * 2;

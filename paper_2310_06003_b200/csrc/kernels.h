@@ -26,6 +26,8 @@ struct DTask {
   int64_t n8;        // 8-element (16-byte) units
   int32_t nin;
   uint32_t rawmask;  // bit i: input i is a raw gradient -> RNE_bf16(g * alpha)
+  int32_t inter;     // 1: the task moves data across groups (paced by inter_gbps)
+  int32_t pad_;
 };
 
 struct DRound {
@@ -53,6 +55,7 @@ struct RoundsArgs {
   int final_barrier;
   uint64_t final_peers;
   float alpha;
+  double inter_bytes_per_ns;    // per-CTA pacing of inter-group tiles (0 = off)
   uint64_t serial;              // launch serial (same sequence on every rank)
   unsigned long long arrive_base;
   BarrierCtx bar;

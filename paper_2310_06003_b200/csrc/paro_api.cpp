@@ -165,16 +165,20 @@ int data_rank(const PlanT* p, const void* ptr) {
   return -1;
 }
 
-DTask resolve(const PlanT* p, const Task& t) {
+DTask resolve(const PlanT* p, const Task& t, int executing_rank) {
   DTask d{};
   d.nin = t.nin;
   d.n8 = t.n / 8;
   d.rawmask = 0;
+  d.inter = 0;
+  const int M = p->pl->M;
   for (int i = 0; i < t.nin; ++i) {
     d.in[i] = reinterpret_cast<const uint16_t*>(data_ptr(p, t.in[i].rank, t.in[i].kind, t.in[i].off));
     if (t.in[i].kind == BUF_GRAD) d.rawmask |= 1u << i;
+    if (t.in[i].rank / M != executing_rank / M) d.inter = 1;
   }
   d.dst = reinterpret_cast<uint16_t*>(data_ptr(p, t.dst.rank, t.dst.kind, t.dst.off));
+  if (t.dst.rank / M != executing_rank / M) d.inter = 1;
   return d;
 }
 
@@ -195,14 +199,14 @@ paro_status_t upload_schedule(PlanT* p) {
       d.units = 0;
       if (ctx->mode == MODE_REAL) {
         for (const Task& t : L.rounds[r][ctx->rank]) {
-          tasks.push_back(resolve(p, t));
+          tasks.push_back(resolve(p, t, ctx->rank));
           d.units += t.n / 8;
         }
         d.peers_before = L.barrier_peers(r, ctx->rank);
       } else {
         for (int x = 0; x < pl.N; ++x)
           for (const Task& t : L.rounds[r][x]) {
-            tasks.push_back(resolve(p, t));
+            tasks.push_back(resolve(p, t, x));
             d.units += t.n / 8;
           }
         d.peers_before = 0;
@@ -276,6 +280,10 @@ paro_status_t run_launch(PlanT* p, const DevLaunch& dl, int* nlaunch) {
   RoundsArgs a{};
   a.tasks = p->d_tasks;
   a.alpha = (float)(1.0 / (double)p->pl->N);
+  // emulated intra/inter gap: this rank's inter-group transfers are paced to
+  // inter_gbps, spread evenly over the CTAs (real mode, TMA rounds kernel)
+  a.inter_bytes_per_ns = (ctx->mode == MODE_REAL && p->opts.inter_gbps > 0.f)
+                             ? (double)p->opts.inter_gbps / (double)grid : 0.0;
   if (ctx->mode == MODE_REAL) {
     char* hdr = p->region[0];
     a.rounds = p->d_rounds + dl.round_off;
@@ -396,6 +404,7 @@ void paro_opts_default(paro_opts_t* o) {
   o->pull_transport = 1;
   o->adam_impl = 0;
   o->comm_impl = 0;
+  o->inter_gbps = 0.f;
   o->stream = nullptr;
 }
 
@@ -508,6 +517,7 @@ paro_status_t paro_plan(paro_ctx_t ctx, const char* strategy, const int64_t* par
   po.topology = o.topology;
   po.pipeline_depth = o.pipeline_depth > 0 ? o.pipeline_depth : 2;
   po.push = o.pull_transport == 0;
+  po.fuse_final = !(o.inter_gbps > 0.f);   // paced runs keep every transfer in the rounds kernel
   auto* p = new PlanT();
   p->ctx = ctx;
   p->opts = o;

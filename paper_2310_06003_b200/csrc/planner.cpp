@@ -708,7 +708,7 @@ void Planner::build_schedule() {
         // local; pull: the predecessor's partial over NVLink): g_hat is never
         // written to / re-read from HBM.  The launch then ends with a barrier
         // that also covers the ranks the fused Adam reads (final_extra).
-        if (Lp == &S.reduce && OS == LV_G && !Lp->rounds.empty()) {
+        if (Lp == &S.reduce && OS == LV_G && opt.fuse_final && !Lp->rounds.empty()) {
           S.ghat_in.assign(N, {});
           Lp->final_extra.assign(N, 0);
           auto& last = Lp->rounds.back();

@@ -92,6 +92,7 @@ struct PlanOptions {
   int topology = 0;          // PARO_TOPO_*
   int pipeline_depth = 2;
   bool push = true;          // push (remote stores) or pull (remote loads) transport
+  bool fuse_final = true;    // OS = G: fold the owner's last reduction hop into Adam
 };
 
 class Planner {

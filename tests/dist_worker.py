@@ -33,6 +33,7 @@ def main():
     topos = cfg.get("topos", ["ho", "two_step", "direct"])
     transports = cfg.get("transports", ["push"])
     comm_impl = cfg.get("comm_impl", "tma")
+    inter_gbps = cfg.get("inter_gbps", 0.0)
     sizes = cfg.get("sizes", [world * 64 * 40 + 24, 333])
     B = cfg.get("bucket", world * 64 * 12)
     steps = cfg.get("steps", 2)
@@ -43,7 +44,8 @@ def main():
         ctx = paro.Context(world, M, mode="real", rank=rank, device=local, uid=bytes(t.tolist()))
         for code, topo, tr in [(c, t_, x) for c in codes for t_ in topos for x in transports]:
             if True:
-                pl = paro.Plan(ctx, code, sizes, bucket_elems=B, topology=topo, transport=tr, comm_impl=comm_impl)
+                pl = paro.Plan(ctx, code, sizes, bucket_elems=B, topology=topo, transport=tr, comm_impl=comm_impl,
+                               inter_gbps=inter_gbps)
                 info = pl.info()
                 st = [torch.empty(info["os_numel"], dtype=torch.float32, device="cuda") for _ in range(3)]
                 ptrs = [[x.data_ptr() for x in st]]

@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--comm-ctas", type=int, default=148)
     ap.add_argument("--transport", default="pull")
     ap.add_argument("--comm-impl", default="tma")
+    ap.add_argument("--inter-gbps", type=float, default=0.0, help="emulated inter-group link (0 = off)")
     a = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -57,11 +58,12 @@ def main():
     for mb in [int(x) for x in a.sizes_mb.split(",")]:
         nbytes = mb << 20
         elems = nbytes // 2
-        row = {"bytes": nbytes, "groups": f"{world // M}x{M}", "n_gpus": world}
+        row = {"bytes": nbytes, "groups": f"{world // M}x{M}", "n_gpus": world, "inter_gbps": a.inter_gbps}
         for topo in a.topos.split(","):
             bucket = min(elems, 1 << 28)
             pl = paro.Plan(ctx, "NNN", [elems], bucket_elems=bucket, topology=topo, comm_ctas=a.comm_ctas,
-                           stream=stream.cuda_stream, transport=a.transport, comm_impl=a.comm_impl)
+                           stream=stream.cuda_stream, transport=a.transport, comm_impl=a.comm_impl,
+                           inter_gbps=a.inter_gbps)
             pl.synth_grads(rank, 1234, 1)
             ms = timeit(lambda: pl.collective(0))
             row[topo] = {"ms": round(ms, 4), "busbw_GBps": round(nbytes * 2 * (world - 1) / world / (ms / 1e3) / 1e9, 1)}
