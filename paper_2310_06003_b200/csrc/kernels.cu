@@ -528,7 +528,7 @@ __global__ void __launch_bounds__(kRtThreads) rounds_tma_kernel(const RoundsArgs
       int ne;
       rt_tile(a, rd, blockIdx.x + k * gridDim.x, tk, e0, ne);
       if (tk->inter && a.inter_bytes_per_ns > 0.0) {   // token bucket: emulated slow inter link
-        inter_sent += (double)ne * 2.0;
+        inter_sent += (double)ne * 2.0 * (double)tk->inter;
         while (inter_sent > (double)(globaltimer() - t_round) * a.inter_bytes_per_ns) __nanosleep(256);
       }
       const uint32_t slot = (cnt + (uint32_t)k) % kRtStages;

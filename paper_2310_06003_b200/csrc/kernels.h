@@ -26,7 +26,7 @@ struct DTask {
   int64_t n8;        // 8-element (16-byte) units
   int32_t nin;
   uint32_t rawmask;  // bit i: input i is a raw gradient -> RNE_bf16(g * alpha)
-  int32_t inter;     // 1: the task moves data across groups (paced by inter_gbps)
+  int32_t inter;     // operands (inputs + dst) on another group's GPU: paced by inter_gbps
   int32_t pad_;
 };
 

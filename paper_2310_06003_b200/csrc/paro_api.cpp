@@ -175,10 +175,10 @@ DTask resolve(const PlanT* p, const Task& t, int executing_rank) {
   for (int i = 0; i < t.nin; ++i) {
     d.in[i] = reinterpret_cast<const uint16_t*>(data_ptr(p, t.in[i].rank, t.in[i].kind, t.in[i].off));
     if (t.in[i].kind == BUF_GRAD) d.rawmask |= 1u << i;
-    if (t.in[i].rank / M != executing_rank / M) d.inter = 1;
+    if (t.in[i].rank / M != executing_rank / M) d.inter += 1;
   }
   d.dst = reinterpret_cast<uint16_t*>(data_ptr(p, t.dst.rank, t.dst.kind, t.dst.off));
-  if (t.dst.rank / M != executing_rank / M) d.inter = 1;
+  if (t.dst.rank / M != executing_rank / M) d.inter += 1;
   return d;
 }
 
