@@ -67,8 +67,10 @@ enum {
   PARO_TOPO_TWO_STEP = 1,  /* intra ring then inter ring   */
   PARO_TOPO_FLAT_RING = 2, /* one ring over all N ranks; different bits  */
   PARO_TOPO_DIRECT = 3,    /* NVSwitch one-shot hierarchical: same bits as 0 / 1 */
-  PARO_TOPO_NCCL = 4       /* NCCL collectives on split comms: perf comparator,
+  PARO_TOPO_NCCL = 4,      /* NCCL collectives on split comms: perf comparator,
                               NOT bit-exact (NCCL's reduction order)              */
+  PARO_TOPO_H_RING = 5     /* H-Ring all-gather with one leader per group (P:146-147,
+                              P:401-402); its reduce-scatter runs two-step        */
 };
 
 typedef struct {

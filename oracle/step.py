@@ -106,7 +106,8 @@ def strategy_step(code, lay: Layout, grads, state, sc: AdamScalars, topology="ho
     the world-reaching gradient reduce-scatter and parameter all-gather used
     when G in {N, G}: "ho" (HO-Ring), "two_step" or
     "flat" (ring over all ranks, P:399 -- a different, still deterministic
-    accumulation order).  G = I always runs RS_I then the inter op (Fig 2/3).
+    accumulation order) or "h_ring" (H-Ring all-gather with one leader per
+    group, P:401-402 / S:378; its reduce-scatter is two-step).  G = I always runs RS_I then the inter op (Fig 2/3).
     """
     pl, gl, ol = validate(code)
     N, M = lay.N, lay.M
@@ -126,7 +127,7 @@ def strategy_step(code, lay: Layout, grads, state, sc: AdamScalars, topology="ho
             if topology == "ho":
                 seg_out, tr, S = C.rs_ho_ring(geo, X, hop)
                 grp_partial = None
-            elif topology == "two_step":
+            elif topology in ("two_step", "h_ring"):   # H-Ring plans reduce two-step
                 seg_out, tr, grp_partial = C.rs_two_step(geo, X, hop)
             elif topology == "flat":
                 seg_out, tr = C.rs_flat_ring(geo, X, hop)
@@ -222,6 +223,8 @@ def _ag(geo, Z, topology):
         return C.ag_two_step(geo, Z)
     if topology == "flat":
         return C.ag_flat_ring(geo, Z)
+    if topology == "h_ring":
+        return C.ag_h_ring(geo, Z)
     raise ValueError(topology)
 
 

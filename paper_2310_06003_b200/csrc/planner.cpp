@@ -259,7 +259,7 @@ Planner::Planner(int N_, int M_, const std::string& code_, const std::vector<int
   OS = norm(OS);
   for (int64_t s : sizes)
     if (s < 0) throw std::invalid_argument("param sizes must be >= 0");
-  if (opt.topology < 0 || opt.topology > 4) throw std::invalid_argument("unknown topology");
+  if (opt.topology < 0 || opt.topology > 5) throw std::invalid_argument("unknown topology");
   if (opt.topology == 3 && (M > kMaxIn || g > kMaxIn))
     throw std::invalid_argument("direct topology needs group_size and n_groups <= 16");
   if (opt.pipeline_depth < 1) opt.pipeline_depth = 1;
@@ -461,7 +461,7 @@ void Planner::build_schedule() {
         }
         return rf - round0 + 1;
       }
-      if (topo == 1) {  // two-step: RS_I into P1, then RS_E
+      if (topo == 1 || topo == 5) {  // two-step: RS_I into P1, then RS_E; H-Ring plans reduce this way
         int r1 = 0;
         for (int j = 0; j < g; ++j) {
           auto gr = group_ranks(j);
@@ -608,6 +608,43 @@ void Planner::build_schedule() {
         for (int r = 0; r < N; ++r) all.push_back(r);
         return ring_ag(L, push, all, [&](int c) { return one(int64_t(seg(grp(c), pos(c))) * C, C); }, base,
                        round0);
+      }
+      if (topo == 5) {  // H-Ring AG: one leader (position 0) per group
+        for (int j = 0; j < g; ++j) {   // phase 1: intra ring AG of the own segments
+          auto gr = group_ranks(j);
+          ring_ag(L, push, gr, [&, j](int c) { return one(int64_t(seg(j, c)) * C, C); },
+                  [&, gr](int q) { return base(gr[q]); }, round0);
+        }
+        int rr = round0 + (M - 1);
+        if (g > 1) {
+          std::vector<int> leaders;
+          for (int j = 0; j < g; ++j) leaders.push_back(rank_of(j, 0));
+          // phase 2: leaders' inter ring AG of whole group blocks (M strided segments each)
+          ring_ag(L, push, leaders,
+                  [&](int c) {
+                    std::vector<Piece> v;
+                    for (int p = 0; p < M; ++p) v.push_back({int64_t(seg(c, p)) * C, C, 0});
+                    return v;
+                  },
+                  [&](int q) { return base(leaders[q]); }, rr);
+          rr += g - 1;
+          // phase 3: chain broadcast of the foreign-group blocks down the positions
+          for (int t = 0; t + 1 < M; ++t) {
+            for (int j = 0; j < g; ++j) {
+              const int src = rank_of(j, t), dst = rank_of(j, t + 1);
+              for (int x = 0; x < g; ++x) {
+                if (x == j) continue;
+                for (int p = 0; p < M; ++p) {
+                  const int64_t o = int64_t(seg(x, p)) * C;
+                  if (!push) L.add(rr + t, dst, make_task(C, {at(base(src), o)}, at(base(dst), o)));
+                  else L.add(rr + t, src, make_task(C, {at(base(src), o)}, at(base(dst), o)));
+                }
+              }
+            }
+          }
+          rr += M - 1;
+        }
+        return rr - round0;
       }
       // direct: inter segments, then intra chunks
       int rr = round0;

@@ -99,7 +99,7 @@ def test_send_bytes_match_oracle_simulator(N, M):
     w0 = master_f32(0, lay.psi)
     ctx = paro.Context(N, M)
     for code in S.paro_strategies():
-        for topo, tr in [(a, b) for a in ("ho", "two_step", "flat") for b in ("push", "pull")]:
+        for topo, tr in [(a, b) for a in ("ho", "two_step", "flat", "h_ring") for b in ("push", "pull")]:
             pl = paro.Plan(ctx, code, sizes, bucket_elems=B, topology=topo, transport=tr)
             res = ST.strategy_step(code, lay, grads, ST.init_state(w0, lay, code), nm.AdamScalars(1e-3, 1),
                                    topology=topo)

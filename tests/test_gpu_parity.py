@@ -148,7 +148,7 @@ CONFIG_4M = dict(sizes=[1 << 22], B=1 << 18)   # BASELINE config 1: 2^22 params,
 
 @pytest.mark.parametrize("comm_impl", ["tma", "lsu"])
 @pytest.mark.parametrize("transport", ["push", "pull"])
-@pytest.mark.parametrize("topo", ["ho", "two_step", "direct"])
+@pytest.mark.parametrize("topo", ["ho", "two_step", "direct", "h_ring"])
 def test_4m_2x4_every_strategy_one_step(topo, transport, comm_impl):
     N, M = 8, 4
     lay = L.Layout(CONFIG_4M["sizes"], N, M, CONFIG_4M["B"])

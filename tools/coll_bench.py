@@ -26,6 +26,9 @@ def main():
     ap.add_argument("--transport", default="pull")
     ap.add_argument("--comm-impl", default="tma")
     ap.add_argument("--inter-gbps", type=float, default=0.0, help="emulated inter-group link (0 = off)")
+    ap.add_argument("--op", default="ar", choices=["ar", "ag"],
+                    help="ar: gradient all-reduce (NNN plan, reduce launches); ag: parameter all-gather "
+                         "(NNG plan, gather launches) as in the paper's section 4.4")
     a = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -59,19 +62,26 @@ def main():
         nbytes = mb << 20
         elems = nbytes // 2
         row = {"bytes": nbytes, "groups": f"{world // M}x{M}", "n_gpus": world, "inter_gbps": a.inter_gbps}
+        factor = 2 * (world - 1) / world if a.op == "ar" else (world - 1) / world
+        code, what = ("NNN", 0) if a.op == "ar" else ("NNG", 1)
         for topo in a.topos.split(","):
             bucket = min(elems, 1 << 28)
-            pl = paro.Plan(ctx, "NNN", [elems], bucket_elems=bucket, topology=topo, comm_ctas=a.comm_ctas,
+            pl = paro.Plan(ctx, code, [elems], bucket_elems=bucket, topology=topo, comm_ctas=a.comm_ctas,
                            stream=stream.cuda_stream, transport=a.transport, comm_impl=a.comm_impl,
                            inter_gbps=a.inter_gbps)
             pl.synth_grads(rank, 1234, 1)
-            ms = timeit(lambda: pl.collective(0))
-            row[topo] = {"ms": round(ms, 4), "busbw_GBps": round(nbytes * 2 * (world - 1) / world / (ms / 1e3) / 1e9, 1)}
+            ms = timeit(lambda: pl.collective(what))
+            row[topo] = {"ms": round(ms, 4), "busbw_GBps": round(nbytes * factor / (ms / 1e3) / 1e9, 1)}
             pl.close()
         x = torch.ones(elems, dtype=torch.bfloat16, device="cuda")
-        ms = timeit(lambda: dist.all_reduce(x))
-        row["nccl_allreduce"] = {"ms": round(ms, 4),
-                                 "busbw_GBps": round(nbytes * 2 * (world - 1) / world / (ms / 1e3) / 1e9, 1)}
+        if a.op == "ar":
+            ms = timeit(lambda: dist.all_reduce(x))
+        else:
+            part = x[rank * (elems // world):(rank + 1) * (elems // world)]
+            ms = timeit(lambda: dist.all_gather_into_tensor(x, part))
+        row["nccl_" + ("allreduce" if a.op == "ar" else "allgather")] = {
+            "ms": round(ms, 4), "busbw_GBps": round(nbytes * factor / (ms / 1e3) / 1e9, 1)}
+        row["op"] = a.op
         del x
         torch.cuda.empty_cache()
         if rank == 0:
