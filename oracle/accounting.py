@@ -171,3 +171,33 @@ def step_units_per_rank(code, N, M, psi):
         tot[0] += a
         tot[1] += b
     return tuple(tot)
+
+
+# ----------------------------------------------------------------- gradient accumulation
+def accum_ops(code):
+    """Primitives of a mini-batch step with s > 1 micro-batches (R27).
+
+    Returns (per_micro_batch_ops, once_ops): the G-level reduction each
+    micro-batch pays (G = G: HO_RS, P:343; G = I: RS_I, P:353/P:369;
+    G = N: none, local accumulation), and the rest of the step paid once
+    (G = I: RS_E or AR_E; G = N: the whole s = 1 reduction),
+    followed by the parameter restore of step_ops.
+    """
+    p, g, o = validate(code)
+    grad, rest = step_ops(code)
+    if g == "G":
+        return ["HO_RS"], rest
+    if g == "I":
+        return ["RS_I"], grad[1:] + rest
+    return [], grad + rest
+
+
+def accum_units_per_rank(code, N, M, psi, s):
+    """Per-rank (intra, inter) parameter units of one mini-batch step with s micro-batches."""
+    per_mb, once = accum_ops(code)
+    tot = [Fr(0), Fr(0)]
+    for prim, mult in [(x, s) for x in per_mb] + [(x, 1) for x in once]:
+        a, b = primitive_units(prim, N, M, psi)
+        tot[0] += mult * a
+        tot[1] += mult * b
+    return tuple(tot)

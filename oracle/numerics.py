@@ -97,12 +97,16 @@ class AdamScalars:
     from those fp32 values and rounded once to fp32:
     step_size = lr / (1 - beta1^t);  bc2s = sqrt(1 - beta2^t);
     decay = 1 - lr * weight_decay;  s_g = 1 / loss_scale (unscale, R4).
+    With gradient accumulation over s micro-batches the accumulated sum is
+    turned into the mini-batch mean here: s_g = 1 / (loss_scale * s) (R27).
     """
 
     def __init__(self, lr, step, beta1=0.9, beta2=0.95, eps=1e-8, weight_decay=0.0,
-                 loss_scale=1.0, clip_coef=1.0):
+                 loss_scale=1.0, clip_coef=1.0, accum_steps=1):
         if step < 1:
             raise ValueError("step must be >= 1")
+        if accum_steps < 1:
+            raise ValueError("accum_steps must be >= 1")
         f = lambda x: float(F32(x))
         lr, b1, b2 = f(lr), f(beta1), f(beta2)
         weight_decay, loss_scale, eps = f(weight_decay), f(loss_scale), f(eps)
@@ -115,7 +119,7 @@ class AdamScalars:
         self.eps = F32(eps)
         self.wd = float(weight_decay)
         self.decay = F32(1.0 - lr * float(weight_decay))
-        self.s_g = F32((1.0 / float(loss_scale)) * float(clip_coef))
+        self.s_g = F32((1.0 / (float(loss_scale) * accum_steps)) * float(clip_coef))
 
 
 def adam_update(master, m, v, ghat_bits, sc: AdamScalars):

@@ -79,6 +79,54 @@ def dp_step(lay: Layout, grads, master, m, v, sc: AdamScalars):
     return w2, m2, v2, pb, ghat
 
 
+def dp_accum_step(lay: Layout, grads_mb, master, m, v, sc: AdamScalars, g_level):
+    """Unsharded data parallel with gradient accumulation (plain definition, R27).
+
+    grads_mb[k][r]: rank r's flat bf16 gradient of micro-batch k (k = 1..s).
+    The micro-batch sum is taken where the strategy keeps its gradient shard
+    (P:344), so the result depends on the G level only:
+      G = G: g_hat = Acc_k CanonReduce(x_k)
+      G = I: S_j'  = Acc_k R_M(p; x_(j', 0..M-1), k);  g_hat = R_g(j; S_0..S_{g-1})
+      G = N: y_r   = Acc_k x_(r, k);                    g_hat = CanonReduce(y)
+    with Acc_k y_k = ((y_1 (+) y_2) (+) ...) (+) y_s and x = RNE_bf16(g / N).
+    Then canonical Adam with sc built with accum_steps = s.
+    """
+    N, M = lay.N, lay.M
+    geo = C.Geometry(N, M)
+    X_mb = [[pack(pad_flat(gr, lay.psi_pad, np.uint16), 1.0 / N) for gr in grads] for grads in grads_mb]
+
+    def acc(ys):
+        out = ys[0]
+        for y in ys[1:]:
+            out = hop(out, y)
+        return out
+
+    if g_level == "N":
+        Y = [acc([X[r] for X in X_mb]) for r in range(N)]
+    ghat = np.zeros(lay.psi_pad, np.uint16)
+    for (s, n) in lay.buckets:
+        segn = n // N
+        for r in range(N):
+            j, p = geo.jp(r)
+            k = geo.seg(j, p)
+            a, b = s + k * segn, s + (k + 1) * segn
+            if g_level == "G":
+                per_mb = []
+                for X in X_mb:
+                    S = [canonical_fold([X[geo.r(jj, pp)][a:b] for pp in range(M)], p) for jj in range(geo.g)]
+                    per_mb.append(canonical_fold(S, j))
+                ghat[a:b] = acc(per_mb)
+            elif g_level == "I":
+                S = [acc([canonical_fold([X[geo.r(jj, pp)][a:b] for pp in range(M)], p) for X in X_mb])
+                     for jj in range(geo.g)]
+                ghat[a:b] = canonical_fold(S, j)
+            else:
+                S = [canonical_fold([Y[geo.r(jj, pp)][a:b] for pp in range(M)], p) for jj in range(geo.g)]
+                ghat[a:b] = canonical_fold(S, j)
+    w2, m2, v2, pb = adam_update(master, m, v, ghat, sc)
+    return w2, m2, v2, pb, ghat
+
+
 class StepResult:
     def __init__(self, N):
         self.state = {}
@@ -109,39 +157,106 @@ def strategy_step(code, lay: Layout, grads, state, sc: AdamScalars, topology="ho
     accumulation order) or "h_ring" (H-Ring all-gather with one leader per
     group, P:401-402 / S:378; its reduce-scatter is two-step).  G = I always runs RS_I then the inter op (Fig 2/3).
     """
+    return _simulate(code, lay, [grads], state, sc, topology, accumulate=False)
+
+
+def strategy_accum_step(code, lay: Layout, grads_mb, state, sc: AdamScalars, topology="ho"):
+    """One mini-batch step with gradient accumulation over s = len(grads_mb)
+    micro-batches (§3.3; "each GPU maintains a gradient shard
+    that accumulates gradients generated by each micro-batch").
+
+    grads_mb[k][r] is rank r's flat bf16 gradient of micro-batch k.  Per
+    micro-batch the gradient is reduced only to the G residency and added to
+    the rank's accumulator there (reading R27):
+      G = G: HO-Ring (or two-step / flat) RS of the micro-batch (P:343);
+      G = I: intra-group RS_I ("synchronized through the
+             intra-group reduce-scatter");
+      G = N: nothing is exchanged; each rank accumulates its full gradient.
+    Accumulator: acc_1 = r_1, acc_k = acc_{k-1} (+) r_k (the hop operator, G is
+    2 bytes).  After the last micro-batch the rest of the reduction runs
+    once on the accumulator (G = I: RS_E / AR_E, "performing an
+    inter-group reduce-scatter operation only once"; G = N: the s = 1 reduction
+    with the accumulator as input), then Adam and the parameter restore as in
+    strategy_step.  The mean over micro-batches is folded into the unscale
+    factor: pass AdamScalars(..., accum_steps=s).
+    """
+    return _simulate(code, lay, grads_mb, state, sc, topology, accumulate=True)
+
+
+def _simulate(code, lay, grads_mb, state, sc, topology, accumulate):
     pl, gl, ol = validate(code)
     N, M = lay.N, lay.M
     geo = C.Geometry(N, M)
     alpha = 1.0 / N
     grad_ops, rest_ops = step_ops(code)
     res = StepResult(N)
-    X_full = [pack(pad_flat(gr, lay.psi_pad, np.uint16), alpha) for gr in grads]
+    X_mb = [[pack(pad_flat(gr, lay.psi_pad, np.uint16), alpha) for gr in grads] for grads in grads_mb]
     new = {r: {"master": [], "m": [], "v": [], "param": []} for r in range(N)}
     ghat_os = {r: [] for r in range(N)}
     gshard = {r: [] for r in range(N)}
+
+    def world_rs(X):
+        if topology == "ho":
+            seg_out, tr, _S = C.rs_ho_ring(geo, X, hop)
+            return seg_out, tr, None
+        if topology in ("two_step", "h_ring"):   # H-Ring plans reduce two-step
+            return C.rs_two_step(geo, X, hop)
+        if topology == "flat":
+            seg_out, tr = C.rs_flat_ring(geo, X, hop)
+            return seg_out, tr, None
+        raise ValueError(topology)
+
+    def intra_rs(X):
+        Y, r1 = C.rs_intra(geo, X, hop)
+        t = C.Trace(M)
+        t.extend(r1)
+        return Y, t
+
+    def inter_rs(Y):
+        seg_out, r2 = C.rs_inter(geo, Y, hop)
+        t = C.Trace(M)
+        t.extend(r2)
+        return seg_out, t
+
     for b, (s, n) in enumerate(lay.buckets):
         segn = n // N
-        X = {r: [X_full[r][s + k * segn: s + (k + 1) * segn] for k in range(N)] for r in range(N)}
-        # ---- gradient reduction to the OS residency
-        if grad_ops[0] == "HO_RS":
-            if topology == "ho":
-                seg_out, tr, S = C.rs_ho_ring(geo, X, hop)
-                grp_partial = None
-            elif topology in ("two_step", "h_ring"):   # H-Ring plans reduce two-step
-                seg_out, tr, grp_partial = C.rs_two_step(geo, X, hop)
-            elif topology == "flat":
-                seg_out, tr = C.rs_flat_ring(geo, X, hop)
-                grp_partial = None
+        segs = lambda full, r: [full[r][s + k * segn: s + (k + 1) * segn] for k in range(N)]
+        grp_partial = None
+        if not accumulate:
+            (X_full,) = X_mb
+            X = {r: segs(X_full, r) for r in range(N)}
+            # ---- gradient reduction to the OS residency
+            if grad_ops[0] == "HO_RS":
+                seg_out, tr, grp_partial = world_rs(X)
+                _add_trace(res, tr)
+            else:  # RS_I then RS_E / AR_E
+                grp_partial, t1 = intra_rs(X)
+                seg_out, t2 = inter_rs(grp_partial)
+                _add_trace(res, t1)
+                _add_trace(res, t2)
+        else:
+            acc = None
+            for X_full in X_mb:
+                X = {r: segs(X_full, r) for r in range(N)}
+                if gl == "G":
+                    red, tr, _ = world_rs(X)
+                    _add_trace(res, tr)
+                elif gl == "I":
+                    red, tr = intra_rs(X)
+                    _add_trace(res, tr)
+                else:
+                    red = {r: np.concatenate(X[r]) for r in range(N)}
+                acc = red if acc is None else {r: hop(acc[r], red[r]) for r in range(N)}
+            if gl == "G":
+                seg_out = acc
+            elif gl == "I":
+                grp_partial = acc
+                seg_out, tr = inter_rs(acc)
+                _add_trace(res, tr)
             else:
-                raise ValueError(topology)
-            _add_trace(res, tr)
-        else:  # RS_I then RS_E / AR_E
-            grp_partial, r1 = C.rs_intra(geo, X, hop)
-            seg_out, r2 = C.rs_inter(geo, grp_partial, hop)
-            t = C.Trace(M)
-            t.extend(r1)
-            t.extend(r2)
-            _add_trace(res, t)
+                seg_out, tr, _ = world_rs({r: [acc[r][k * segn:(k + 1) * segn] for k in range(N)]
+                                           for r in range(N)})
+                _add_trace(res, tr)
         # per-rank g_hat over the OS residency
         if ol == "G":
             gh = {r: seg_out[r] for r in range(N)}
@@ -152,10 +267,10 @@ def strategy_step(code, lay: Layout, grads, state, sc: AdamScalars, topology="ho
             _add_trace(res, t)
             gh = {r: np.concatenate(ch[r]) for r in range(N)}
         else:  # OS = N: HO-Ring all-gather of g_hat (all-reduce = RS + AG)
-            segs, t = _ag(geo, seg_out, topology)
+            segs_, t = _ag(geo, seg_out, topology)
             _add_trace(res, t)
-            gh = {r: np.concatenate([segs[r][k] for k in range(N)]) for r in range(N)}
-        # G residency (s = 1): the value the strategy keeps as its gradient shard
+            gh = {r: np.concatenate([segs_[r][k] for k in range(N)]) for r in range(N)}
+        # G residency: the value the strategy keeps as its gradient shard
         for r in range(N):
             if gl == "G":
                 gshard[r].append(seg_out[r])
@@ -184,9 +299,9 @@ def strategy_step(code, lay: Layout, grads, state, sc: AdamScalars, topology="ho
             _add_trace(res, t)
             pres = {r: np.concatenate(ch[r]) for r in range(N)}
         elif rest_ops == ["HO_AG"]:
-            segs, t = _ag(geo, adam_out, topology)
+            segs_, t = _ag(geo, adam_out, topology)
             _add_trace(res, t)
-            pres = {r: np.concatenate([segs[r][k] for k in range(N)]) for r in range(N)}
+            pres = {r: np.concatenate([segs_[r][k] for k in range(N)]) for r in range(N)}
         elif rest_ops == ["AG_I"]:
             ch, rounds = C.ag_intra(geo, adam_out)
             t = C.Trace(M)
