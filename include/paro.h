@@ -95,6 +95,9 @@ typedef struct {
                           * rounds kernel; the final hop is then not fused into    *
                           * Adam).  0 (default): no pacing.  One NVSwitch box has  *
                           * no real intra/inter gap.                */
+  int grad_accum;        /* 1: enable paro_accumulate (gradient accumulation over  *
+                          * s > 1 micro-batches); G = N plans then own  *
+                          * a psi_pad bf16 accumulator.  0 (default): off.         */
   void* stream;          /* cudaStream_t the step is ordered on; NULL = ctx stream */
 } paro_opts_t;
 
@@ -110,6 +113,10 @@ typedef struct {
   int64_t step_send_bytes_inter;       /*   transfers the kernels perform          */
   int32_t n_rounds;                    /* collective rounds per step (all buckets) */
   int32_t n_comm_launches;             /* collective kernel launches per step      */
+  /* grad_accum plans: this rank's bytes per paro_accumulate call, and per      *
+   * paro_step that follows accumulation (0 otherwise)                         */
+  int64_t accum_send_bytes_intra, accum_send_bytes_inter;
+  int64_t accum_step_send_bytes_intra, accum_step_send_bytes_inter;
 } paro_plan_info_t;
 
 typedef struct {
@@ -173,6 +180,13 @@ paro_status_t paro_bucket_range(paro_plan_t plan, int64_t bucket, int64_t* begin
  * rank's memory counts as sent by this rank). */
 paro_status_t paro_rank_send_bytes(paro_plan_t plan, int rank, int64_t* intra, int64_t* inter);
 
+/* grad_accum plans: bytes `rank` sends per paro_accumulate call (*acc_*) and
+ * in the paro_step that follows accumulation (*step_*), per link class,
+ * counted from the transfer lists like paro_rank_send_bytes.  PARO_ERR_STATE
+ * if the plan was made with grad_accum = 0. */
+paro_status_t paro_rank_accum_send_bytes(paro_plan_t plan, int rank, int64_t* acc_intra, int64_t* acc_inter,
+                                         int64_t* step_intra, int64_t* step_inter);
+
 /* Library-owned device buffers of `rank` (must be a local rank):
  *   kind 0: flat gradient buffer, bf16, psi_pad elements (zero-padded tail).
  *           Writing gradients here and passing grads = NULL to paro_step is
@@ -182,7 +196,9 @@ paro_status_t paro_rank_send_bytes(paro_plan_t plan, int rank, int64_t* intra, i
  *           gradient residency is the flat gradient buffer).
  *   kind 3: reduced-gradient slots (bf16; slot b % (pipeline_depth+1) holds
  *           bucket b's g_hat at the OS residency) or NULL when g_hat lives in
- *           the G-residency buffer or is consumed directly by Adam. */
+ *           the G-residency buffer or is consumed directly by Adam.
+ *   kind 4: the G = N gradient accumulator (bf16, psi_pad elements; grad_accum
+ *           plans with G = N only, else NULL). */
 paro_status_t paro_buffer(paro_plan_t plan, int rank, int kind, void** ptr);
 
 /* Initialise one local rank's optimizer state and parameter buffer from a full
@@ -209,9 +225,27 @@ paro_status_t paro_synth_grads(paro_plan_t plan, int rank, uint64_t seed, int64_
  *          else per local rank: n_params bf16 pointers (P = N) or one pointer
  *          to p_numel elements (P = I, G) that receive a copy after the step.
  *  opt_state: one paro_opt_state_t per local rank (rank order).
- *  lr: this step's learning rate; step: 1-based Adam t ("step must be >= 1"). */
+ *  lr: this step's learning rate; step: 1-based Adam t ("step must be >= 1").
+ *  After paro_accumulate calls, grads must be NULL: the step consumes the
+ *  accumulator ("grads must be NULL after paro_accumulate"). */
 paro_status_t paro_step(paro_plan_t plan, const void* const* grads, void* const* params,
                         const paro_opt_state_t* opt_state, float lr, int64_t step);
+
+/* Gradient accumulation (§3.3; R27).  Adds one
+ * micro-batch's gradients at the G residency: G = G reduces the micro-batch
+ * over all ranks (HO-Ring RS), G = I inside the group (RS_I, P:353,
+ * P:369), G = N only locally; the result is folded into the rank's bf16
+ * accumulator, acc = acc (+) r (first call: acc = r).  After s >= 1 calls the
+ * next paro_step (grads must be NULL) finishes the reduction from the
+ * accumulator once (G = I: the inter-group RS / AR, "only once"), runs
+ * Adam on the mini-batch mean (unscale 1/(loss_scale * s)) and the parameter
+ * all-gather, and resets s.  Per-rank bytes: paro_plan_info_t.accum_*.
+ *  grads: NULL = the micro-batch is in each local rank's flat gradient buffer
+ *         (paro_buffer kind 0); else n_params bf16 device pointers per local
+ *         rank, packed first.  The gradient buffer may be overwritten once the
+ *         call's work has completed on the stream.
+ * Errors: PARO_ERR_STATE if the plan was made with grad_accum = 0. */
+paro_status_t paro_accumulate(paro_plan_t plan, const void* const* grads);
 
 /* Collective only (no optimizer): run the plan's gradient-reduction launches
  * (what = 0) or parameter all-gather launches (what = 1) for every bucket,

@@ -67,6 +67,9 @@ struct paro_plan {
   DRound* d_rounds = nullptr;
   DTask* d_tasks = nullptr;
   std::vector<DevLaunch> red, gat;        // per bucket
+  std::vector<DevLaunch> acc_first, acc_next, red_acc;   // gradient accumulation (per bucket)
+  int64_t acc_count = 0;                  // micro-batches accumulated since the last step
+  bool last_step_acc = false;             // the last step consumed an accumulator
   double* d_partials = nullptr;
   int partials_cap = 0;
   double* d_norm = nullptr;
@@ -165,7 +168,9 @@ int data_rank(const PlanT* p, const void* ptr) {
   return -1;
 }
 
-DTask resolve(const PlanT* p, const Task& t, int executing_rank) {
+// acc_kind >= 0: a task writing that buffer kind also folds its old contents in
+// as the last input (gradient accumulation: acc = acc (+) r, R27)
+DTask resolve(const PlanT* p, const Task& t, int executing_rank, int acc_kind) {
   DTask d{};
   d.nin = t.nin;
   d.n8 = t.n / 8;
@@ -179,6 +184,10 @@ DTask resolve(const PlanT* p, const Task& t, int executing_rank) {
   }
   d.dst = reinterpret_cast<uint16_t*>(data_ptr(p, t.dst.rank, t.dst.kind, t.dst.off));
   if (t.dst.rank / M != executing_rank / M) d.inter += 1;
+  if (acc_kind >= 0 && t.dst.kind == acc_kind) {
+    d.in[d.nin++] = d.dst;
+    if (t.dst.rank / M != executing_rank / M) d.inter += 1;
+  }
   return d;
 }
 
@@ -188,7 +197,7 @@ paro_status_t upload_schedule(PlanT* p) {
   const Planner& pl = *p->pl;
   std::vector<DRound> rounds;
   std::vector<DTask> tasks;
-  auto build = [&](const Launch& L) {
+  auto build = [&](const Launch& L, int acc_kind) {
     DevLaunch dl;
     dl.round_off = (int64_t)rounds.size();
     if (L.empty()) return dl;
@@ -199,20 +208,21 @@ paro_status_t upload_schedule(PlanT* p) {
       d.units = 0;
       if (ctx->mode == MODE_REAL) {
         for (const Task& t : L.rounds[r][ctx->rank]) {
-          tasks.push_back(resolve(p, t, ctx->rank));
+          tasks.push_back(resolve(p, t, ctx->rank, acc_kind));
           d.units += t.n / 8;
         }
         d.peers_before = L.barrier_peers(r, ctx->rank);
       } else {
         for (int x = 0; x < pl.N; ++x)
           for (const Task& t : L.rounds[r][x]) {
-            tasks.push_back(resolve(p, t, x));
+            tasks.push_back(resolve(p, t, x, acc_kind));
             d.units += t.n / 8;
           }
         d.peers_before = 0;
       }
       d.t1 = (int32_t)tasks.size();
       for (int ti = d.t0; ti < d.t1; ++ti) dl.max_in = std::max(dl.max_in, std::min(3, (int)tasks[ti].nin));
+      (void)acc_kind;
       rounds.push_back(d);
     }
     dl.nrounds = R;
@@ -232,9 +242,17 @@ paro_status_t upload_schedule(PlanT* p) {
   };
   p->red.clear();
   p->gat.clear();
+  p->acc_first.clear();
+  p->acc_next.clear();
+  p->red_acc.clear();
   for (const BucketSchedule& S : pl.sched) {
-    p->red.push_back(build(S.reduce));
-    p->gat.push_back(build(S.gather));
+    p->red.push_back(build(S.reduce, -1));
+    p->gat.push_back(build(S.gather, -1));
+    if (pl.opt.accum) {
+      p->acc_first.push_back(build(S.accum, -1));
+      p->acc_next.push_back(build(S.accum, pl.acc_kind));
+      p->red_acc.push_back(build(S.reduce_acc, -1));
+    }
   }
   if (!rounds.empty()) {
     CK(cudaMalloc(&p->d_rounds, rounds.size() * sizeof(DRound)));
@@ -321,6 +339,50 @@ paro_status_t run_launch(PlanT* p, const DevLaunch& dl, int* nlaunch) {
   return PARO_OK;
 }
 
+// Per-parameter caller gradients -> each local rank's flat gradient buffer
+// (compute stream; the comm stream waits for it).
+paro_status_t pack_grads(PlanT* p, const void* const* grads, int* launches) {
+  paro_ctx* ctx = p->ctx;
+  const Planner& pl = *p->pl;
+  const int nl = (int)p->local.size();
+  const int np = (int)pl.param_sizes.size();
+  CK(cudaEventSynchronize(p->ev_pack_staged));   // staging buffer free again
+  int k = 0;
+  int64_t maxn = 0;
+  for (int li = 0; li < nl; ++li) {
+    const int r = p->local[li];
+    for (int i = 0; i < np; ++i) {
+      if (pl.param_sizes[i] == 0) continue;
+      p->h_pack[k].src = static_cast<const uint16_t*>(grads[li * np + i]);
+      p->h_pack[k].dst = reinterpret_cast<uint16_t*>(data_ptr(p, r, BUF_GRAD, pl.param_offsets[i]));
+      p->h_pack[k].n = pl.param_sizes[i];
+      maxn = std::max(maxn, pl.param_sizes[i]);
+      ++k;
+    }
+  }
+  CK(cudaMemcpyAsync(p->d_pack, p->h_pack, sizeof(PackEntry) * k, cudaMemcpyHostToDevice, ctx->comp));
+  CK(cudaEventRecord(p->ev_pack_staged, ctx->comp));
+  CK(launch_pack(p->d_pack, k, maxn, ctx->comp));
+  ++*launches;
+  CK(cudaEventRecord(p->ev_comp, ctx->comp));
+  CK(cudaStreamWaitEvent(ctx->comm, p->ev_comp, 0));
+  return PARO_OK;
+}
+
+// Step-end barrier with every peer (real mode, N > 1): after it no peer reads
+// (fused Adam, pull rounds) or writes (push rounds) this rank's buffers any
+// more, so the caller may overwrite its gradients and read its parameters.
+paro_status_t all_peer_barrier(PlanT* p, int* launches) {
+  paro_ctx* ctx = p->ctx;
+  if (ctx->mode != MODE_REAL || p->pl->N <= 1 || p->pl->opt.topology == PARO_TOPO_NCCL) return PARO_OK;
+  DevLaunch fin;
+  fin.nrounds = 0;
+  fin.final_barrier = 1;
+  for (int x = 0; x < p->pl->N; ++x)
+    if (x != ctx->rank) fin.final_peers |= uint64_t(1) << x;
+  return run_launch(p, fin, launches);
+}
+
 ncclComm_t pick_comm(paro_ctx* ctx, NcclCall::Comm c) {
   return c == NcclCall::INTRA ? ctx->intra : (c == NcclCall::INTER ? ctx->inter : ctx->world);
 }
@@ -405,6 +467,7 @@ void paro_opts_default(paro_opts_t* o) {
   o->adam_impl = 0;
   o->comm_impl = 0;
   o->inter_gbps = 0.f;
+  o->grad_accum = 0;
   o->stream = nullptr;
 }
 
@@ -518,6 +581,7 @@ paro_status_t paro_plan(paro_ctx_t ctx, const char* strategy, const int64_t* par
   po.pipeline_depth = o.pipeline_depth > 0 ? o.pipeline_depth : 2;
   po.push = o.pull_transport == 0;
   po.fuse_final = !(o.inter_gbps > 0.f);   // paced runs keep every transfer in the rounds kernel
+  po.accum = o.grad_accum != 0;
   auto* p = new PlanT();
   p->ctx = ctx;
   p->opts = o;
@@ -631,6 +695,12 @@ paro_status_t paro_plan_info(paro_plan_t p, paro_plan_info_t* out) {
   out->step_send_bytes_inter = pl.send_inter[me];
   out->n_rounds = pl.n_rounds;
   out->n_comm_launches = pl.n_comm_launches;
+  if (pl.opt.accum) {
+    out->accum_send_bytes_intra = pl.acc_send_intra[me];
+    out->accum_send_bytes_inter = pl.acc_send_inter[me];
+    out->accum_step_send_bytes_intra = pl.accstep_send_intra[me];
+    out->accum_step_send_bytes_inter = pl.accstep_send_inter[me];
+  }
   return PARO_OK;
 }
 
@@ -663,6 +733,18 @@ paro_status_t paro_rank_send_bytes(paro_plan_t p, int rank, int64_t* intra, int6
   return PARO_OK;
 }
 
+paro_status_t paro_rank_accum_send_bytes(paro_plan_t p, int rank, int64_t* acc_intra, int64_t* acc_inter,
+                                         int64_t* step_intra, int64_t* step_inter) {
+  if (!p || !acc_intra || !acc_inter || !step_intra || !step_inter) return fail(PARO_ERR_INVALID, "null argument");
+  if (rank < 0 || rank >= p->pl->N) return fail(PARO_ERR_INVALID, "rank out of range");
+  if (!p->pl->opt.accum) return fail(PARO_ERR_STATE, "plan was created without grad_accum");
+  *acc_intra = p->pl->acc_send_intra[rank];
+  *acc_inter = p->pl->acc_send_inter[rank];
+  *step_intra = p->pl->accstep_send_intra[rank];
+  *step_inter = p->pl->accstep_send_inter[rank];
+  return PARO_OK;
+}
+
 paro_status_t paro_buffer(paro_plan_t p, int rank, int kind, void** ptr) {
   if (!p || !ptr) return fail(PARO_ERR_INVALID, "null argument");
   paro_ctx* ctx = p->ctx;
@@ -673,7 +755,8 @@ paro_status_t paro_buffer(paro_plan_t p, int rank, int kind, void** ptr) {
   else if (kind == 1) *ptr = data_ptr(p, rank, BUF_PARAM, 0);
   else if (kind == 2) *ptr = (pl.G == LV_N) ? nullptr : data_ptr(p, rank, BUF_GSHARD, 0);
   else if (kind == 3) *ptr = pl.buf_len[BUF_GHAT] ? data_ptr(p, rank, BUF_GHAT, 0) : nullptr;
-  else return fail(PARO_ERR_INVALID, "kind must be 0, 1, 2 or 3");
+  else if (kind == 4) *ptr = pl.buf_len[BUF_GACC] ? data_ptr(p, rank, BUF_GACC, 0) : nullptr;
+  else return fail(PARO_ERR_INVALID, "kind must be 0, 1, 2, 3 or 4");
   return PARO_OK;
 }
 
@@ -745,6 +828,10 @@ paro_status_t paro_step(paro_plan_t p, const void* const* grads, void* const* pa
     for (int i = 0; i < nl * np; ++i)
       if (!grads[i] && pl.param_sizes[i % np] > 0) return fail(PARO_ERR_INVALID, "null gradient pointer");
   }
+  // after paro_accumulate the step consumes the accumulator (R27)
+  const int64_t n_acc = p->acc_count;
+  if (n_acc > 0 && grads) return fail(PARO_ERR_INVALID, "grads must be NULL after paro_accumulate");
+  const std::vector<DevLaunch>& red = n_acc > 0 ? p->red_acc : p->red;
   cudaStream_t S = p->opts.stream ? static_cast<cudaStream_t>(p->opts.stream) : ctx->main;
   int launches = 0;
 
@@ -761,7 +848,7 @@ paro_status_t paro_step(paro_plan_t p, const void* const* grads, void* const* pa
   aa.eps = p->opts.eps;
   aa.has_wd = p->opts.weight_decay != 0.0f;
   aa.decay = (float)(1.0 - dlr * (double)p->opts.weight_decay);
-  aa.s_g = (float)(1.0 / (double)p->opts.loss_scale);
+  aa.s_g = (float)(1.0 / ((double)p->opts.loss_scale * (double)(n_acc > 0 ? n_acc : 1)));
   aa.nonfinite = p->d_nonfinite;
 
   CK(cudaEventRecord(p->ev_fork, S));
@@ -770,26 +857,8 @@ paro_status_t paro_step(paro_plan_t p, const void* const* grads, void* const* pa
 
   // ---- pack (per-parameter gradients -> flat gradient buffer)
   if (grads) {
-    CK(cudaEventSynchronize(p->ev_pack_staged));   // staging buffer free again
-    int k = 0;
-    int64_t maxn = 0;
-    for (int li = 0; li < nl; ++li) {
-      const int r = p->local[li];
-      for (int i = 0; i < np; ++i) {
-        if (pl.param_sizes[i] == 0) continue;
-        p->h_pack[k].src = static_cast<const uint16_t*>(grads[li * np + i]);
-        p->h_pack[k].dst = reinterpret_cast<uint16_t*>(data_ptr(p, r, BUF_GRAD, pl.param_offsets[i]));
-        p->h_pack[k].n = pl.param_sizes[i];
-        maxn = std::max(maxn, pl.param_sizes[i]);
-        ++k;
-      }
-    }
-    CK(cudaMemcpyAsync(p->d_pack, p->h_pack, sizeof(PackEntry) * k, cudaMemcpyHostToDevice, ctx->comp));
-    CK(cudaEventRecord(p->ev_pack_staged, ctx->comp));
-    CK(launch_pack(p->d_pack, k, maxn, ctx->comp));
-    ++launches;
-    CK(cudaEventRecord(p->ev_comp, ctx->comp));
-    CK(cudaStreamWaitEvent(ctx->comm, p->ev_comp, 0));
+    paro_status_t sp = pack_grads(p, grads, &launches);
+    if (sp != PARO_OK) return sp;
   }
   CK(cudaMemsetAsync(p->d_nonfinite, 0, sizeof(int), ctx->comp));
   CK(cudaMemsetAsync(p->d_partials, 0, sizeof(double) * p->partials_cap, ctx->comp));
@@ -808,10 +877,11 @@ paro_status_t paro_step(paro_plan_t p, const void* const* grads, void* const* pa
       int64_t len = 0;
       for (int b = b0; b < b1; ++b) len += pl.sched[b].os_len;
       AdamSeg& sg = aa.seg[aa.nseg++];
-      sg.gnin = (int)S0.ghat_in[r].size();
+      const std::vector<Ref>& gin = (n_acc > 0) ? S0.ghat_in_acc[r] : S0.ghat_in[r];
+      sg.gnin = (int)gin.size();
       sg.graw = 0;
       for (int i = 0; i < sg.gnin; ++i) {
-        const Ref& x = S0.ghat_in[r][i];
+        const Ref& x = gin[i];
         sg.gin[i] = reinterpret_cast<const uint16_t*>(data_ptr(p, x.rank, x.kind, x.off));
         if (x.kind == BUF_GRAD) sg.graw |= 1u << i;
       }
@@ -869,7 +939,7 @@ paro_status_t paro_step(paro_plan_t p, const void* const* grads, void* const* pa
         if (s3 != PARO_OK) return s3;
         ++launches;
       } else {
-        paro_status_t s3 = run_launch(p, p->red[b], &launches);
+        paro_status_t s3 = run_launch(p, red[b], &launches);
         if (s3 != PARO_OK) return s3;
       }
       CK(cudaEventRecord(p->ev_red[b], ctx->comm));
@@ -892,16 +962,9 @@ paro_status_t paro_step(paro_plan_t p, const void* const* grads, void* const* pa
   ++launches;
   CK(cudaEventRecord(p->ev_comp, ctx->comp));
   CK(cudaStreamWaitEvent(ctx->comm, p->ev_comp, 0));
-  // ---- step-end barrier with every peer: after it no peer reads (fused Adam,
-  // pull rounds) or writes (push rounds) this rank's buffers any more, so the
-  // caller may overwrite its gradients and read its parameters.
-  if (ctx->mode == MODE_REAL && pl.N > 1 && pl.opt.topology != PARO_TOPO_NCCL) {
-    DevLaunch fin;
-    fin.nrounds = 0;
-    fin.final_barrier = 1;
-    for (int x = 0; x < pl.N; ++x)
-      if (x != ctx->rank) fin.final_peers |= uint64_t(1) << x;
-    paro_status_t s6 = run_launch(p, fin, &launches);
+  // ---- step-end barrier with every peer
+  {
+    paro_status_t s6 = all_peer_barrier(p, &launches);
     if (s6 != PARO_OK) return s6;
   }
   if (ctx->mode == MODE_REAL && pl.N > 1) {
@@ -947,10 +1010,52 @@ paro_status_t paro_step(paro_plan_t p, const void* const* grads, void* const* pa
   p->last_stream = S;
   p->last_launches = launches;
   p->stepped = true;
+  p->last_step_acc = n_acc > 0;
+  p->acc_count = 0;
   if (p->prof) {
     ++p->prof_steps;
     p->prof_launches += launches;
   }
+  return PARO_OK;
+}
+
+paro_status_t paro_accumulate(paro_plan_t p, const void* const* grads) {
+  if (!p) return fail(PARO_ERR_INVALID, "null plan");
+  paro_ctx* ctx = p->ctx;
+  paro_status_t s = check_ctx(ctx);
+  if (s != PARO_OK) return s;
+  if (ctx->mode == MODE_PLANNER) return fail(PARO_ERR_STATE, "planning-only context cannot accumulate");
+  const Planner& pl = *p->pl;
+  if (!pl.opt.accum) return fail(PARO_ERR_STATE, "plan was created without grad_accum");
+  const int nl = (int)p->local.size();
+  const int np = (int)pl.param_sizes.size();
+  if (grads) {
+    for (int i = 0; i < nl * np; ++i)
+      if (!grads[i] && pl.param_sizes[i % np] > 0) return fail(PARO_ERR_INVALID, "null gradient pointer");
+  }
+  cudaStream_t S = p->opts.stream ? static_cast<cudaStream_t>(p->opts.stream) : ctx->main;
+  int launches = 0;
+  CK(cudaEventRecord(p->ev_fork, S));
+  CK(cudaStreamWaitEvent(ctx->comm, p->ev_fork, 0));
+  CK(cudaStreamWaitEvent(ctx->comp, p->ev_fork, 0));
+  if (grads) {
+    paro_status_t sp = pack_grads(p, grads, &launches);
+    if (sp != PARO_OK) return sp;
+  }
+  const std::vector<DevLaunch>& acc = (p->acc_count == 0) ? p->acc_first : p->acc_next;
+  for (size_t b = 0; b < pl.buckets.size(); ++b) {
+    paro_status_t s3 = run_launch(p, acc[b], &launches);
+    if (s3 != PARO_OK) return s3;
+  }
+  {
+    paro_status_t s6 = all_peer_barrier(p, &launches);   // peers are done reading our gradients
+    if (s6 != PARO_OK) return s6;
+  }
+  CK(cudaEventRecord(p->ev_comm, ctx->comm));
+  CK(cudaStreamWaitEvent(S, p->ev_comm, 0));
+  p->last_stream = S;
+  ++p->acc_count;
+  if (p->prof) p->prof_launches += launches;
   return PARO_OK;
 }
 
@@ -1092,8 +1197,8 @@ paro_status_t paro_step_stats(paro_plan_t p, paro_step_stats_t* out) {
   out->grad_norm = std::sqrt(nsq);
   out->nonfinite = nf;
   const int me = ctx->mode == MODE_REAL ? ctx->rank : 0;
-  out->sent_intra = p->pl->send_intra[me];
-  out->sent_inter = p->pl->send_inter[me];
+  out->sent_intra = p->last_step_acc ? p->pl->accstep_send_intra[me] : p->pl->send_intra[me];
+  out->sent_inter = p->last_step_acc ? p->pl->accstep_send_inter[me] : p->pl->send_inter[me];
   out->kernel_launches = p->last_launches;
   return PARO_OK;
 }

@@ -263,6 +263,10 @@ Planner::Planner(int N_, int M_, const std::string& code_, const std::vector<int
   if (opt.topology == 3 && (M > kMaxIn || g > kMaxIn))
     throw std::invalid_argument("direct topology needs group_size and n_groups <= 16");
   if (opt.pipeline_depth < 1) opt.pipeline_depth = 1;
+  if (opt.accum && opt.topology == 4)
+    throw std::invalid_argument("gradient accumulation is not available with the NCCL comparator topology");
+  if (opt.accum && opt.topology == 3 && (M >= kMaxIn || g >= kMaxIn))
+    throw std::invalid_argument("gradient accumulation with the direct topology needs group_size and n_groups < 16");
   layout();
   build_schedule();
   validate_refs();
@@ -326,6 +330,8 @@ void Planner::layout() {
   buf_len[BUF_P1] = (N > 1) ? kStageSets * p1_len : 0;
   buf_len[BUF_SOWN] = (N > 1) ? kStageSets * sown_len : 0;
   buf_len[BUF_LAND] = (N > 1 && opt.topology == 3 && opt.push) ? kStageSets * land_len : 0;
+  buf_len[BUF_GACC] = (opt.accum && G == LV_N) ? psi_pad : 0;
+  acc_kind = !opt.accum ? -1 : (G == LV_N ? BUF_GACC : BUF_GSHARD);
   int64_t off = 0;
   for (int k = 0; k < BUF_NKINDS; ++k) {
     buf_off[k] = off;
@@ -355,11 +361,12 @@ void Planner::build_schedule() {
     const int64_t s = buckets[b].first, n = buckets[b].second;
     const int64_t C = n / N, chunk = n / M;
     const int par = int(b % kStageSets);
-    S.reduce.n_ranks = S.gather.n_ranks = N;
+    S.reduce.n_ranks = S.gather.n_ranks = S.accum.n_ranks = S.reduce_acc.n_ranks = N;
     S.nccl_reduce.assign(N, {});
     S.nccl_gather.assign(N, {});
 
-    auto grad = [&](int r, int64_t o) { return Ref{r, BUF_GRAD, s + o}; };
+    int src_kind = BUF_GRAD;   // BUF_GACC while emitting the G = N post-accumulation reduction
+    auto grad = [&](int r, int64_t o) { return Ref{r, src_kind, s + o}; };
     auto gshard = [&](int r, int64_t o) { return Ref{r, BUF_GSHARD, s / divl(G) + o}; };
     auto ghat_base = [&](int r) {
       if (G == OS && G != LV_N) return Ref{r, BUF_GSHARD, s / divl(G)};
@@ -702,29 +709,58 @@ void Planner::build_schedule() {
       return used;
     };
 
+    // RS_I of the gradients into the G residency.  Returns rounds used.
+    auto emit_rs_i = [&](Launch& L, int round0) -> int {
+      int r1 = 0;
+      for (int j = 0; j < g; ++j) {
+        auto gr = group_ranks(j);
+        r1 = ring_rs(L, push, gr, [&](int c) { return one(int64_t(c) * chunk, chunk); },
+                     [&, gr](int q, int, const Piece& pc) { return grad(gr[q], pc.src_off); },
+                     [&, gr](int q, int slot) { return stage_i(gr[q], slot); },
+                     [&, gr](int q) { return gshard(gr[q], 0); }, round0);
+      }
+      return r1;
+    };
+    // RS_E from the G residency; in place + AG_E for OS = I (all-reduce)
+    auto emit_rs_e = [&](Launch& L, int round0) {
+      int r2 = 0;
+      for (int p = 0; p < M; ++p) {
+        auto pr = pos_ranks(p);
+        r2 = ring_rs(L, push, pr, [&](int c) { return one(int64_t(c) * C, C); },
+                     [&, pr](int q, int, const Piece& pc) { return gshard(pr[q], pc.src_off); },
+                     [&, pr](int q, int slot) { return stage_e(pr[q], slot); },
+                     [&, pr](int q) { return dest_seg(pr[q]); }, round0);
+      }
+      if (OS == LV_I) emit_ag_e(L, [&](int r) { return ghat_base(r); }, round0 + r2);
+    };
+    // G in {N, G}: world RS (+ AG_E / world AG of g_hat for OS = I / N)
+    auto emit_world_reduce = [&](Launch& L) {
+      int used = emit_world_rs(L, 0);
+      if (OS == LV_I) emit_ag_e(L, [&](int r) { return ghat_base(r); }, used);
+      if (OS == LV_N) emit_world_ag(L, [&](int r) { return ghat_base(r); }, used);
+    };
+
     if (N > 1 && topo != 4) {
       Launch& L = S.reduce;
       if (G == LV_I) {
-        int r1 = 0, r2 = 0;
-        for (int j = 0; j < g; ++j) {   // RS_I into the G residency
-          auto gr = group_ranks(j);
-          r1 = ring_rs(L, push, gr, [&](int c) { return one(int64_t(c) * chunk, chunk); },
-                       [&, gr](int q, int, const Piece& pc) { return grad(gr[q], pc.src_off); },
-                       [&, gr](int q, int slot) { return stage_i(gr[q], slot); },
-                       [&, gr](int q) { return gshard(gr[q], 0); }, 0);
-        }
-        for (int p = 0; p < M; ++p) {   // RS_E; in place for OS = I (all-reduce)
-          auto pr = pos_ranks(p);
-          r2 = ring_rs(L, push, pr, [&](int c) { return one(int64_t(c) * C, C); },
-                       [&, pr](int q, int, const Piece& pc) { return gshard(pr[q], pc.src_off); },
-                       [&, pr](int q, int slot) { return stage_e(pr[q], slot); },
-                       [&, pr](int q) { return dest_seg(pr[q]); }, r1);
-        }
-        if (OS == LV_I) emit_ag_e(L, [&](int r) { return ghat_base(r); }, r1 + r2);
+        emit_rs_e(L, emit_rs_i(L, 0));
       } else {
-        int used = emit_world_rs(L, 0);
-        if (OS == LV_I) emit_ag_e(L, [&](int r) { return ghat_base(r); }, used);
-        if (OS == LV_N) emit_world_ag(L, [&](int r) { return ghat_base(r); }, used);
+        emit_world_reduce(L);
+      }
+      // ---- gradient accumulation (R27): per micro-batch only the
+      // G-level reduction, into the accumulator; the rest once, from it
+      if (opt.accum) {
+        if (G == LV_G) {
+          emit_world_rs(S.accum, 0);          // lands in the G residency (dest_seg)
+        } else if (G == LV_I) {
+          emit_rs_i(S.accum, 0);
+          emit_rs_e(S.reduce_acc, 0);
+        } else {
+          for (int r = 0; r < N; ++r) S.accum.add(0, r, make_task(n, {grad(r, 0)}, Ref{r, BUF_GACC, s}));
+          src_kind = BUF_GACC;
+          emit_world_reduce(S.reduce_acc);
+          src_kind = BUF_GRAD;
+        }
       }
       // ---- parameter restore
       Launch& Lg = S.gather;
@@ -732,7 +768,9 @@ void Planner::build_schedule() {
       if (OS == LV_G && P == LV_N) emit_world_ag(Lg, param_base, 0);
       if (OS == LV_I && P == LV_N) emit_ag_i(Lg, param_base, 0);
       // drop rounds that ended up empty for every rank (degenerate splits)
-      for (Launch* Lp : {&S.reduce, &S.gather}) {
+      for (Launch* Lp : {&S.reduce, &S.gather, &S.accum, &S.reduce_acc}) {
+        const bool is_red = (Lp == &S.reduce || Lp == &S.reduce_acc);
+        std::vector<std::vector<Ref>>& gin = (Lp == &S.reduce_acc) ? S.ghat_in_acc : S.ghat_in;
         std::vector<std::vector<std::vector<Task>>> kept;
         for (auto& rnd : Lp->rounds) {
           bool any = false;
@@ -745,8 +783,8 @@ void Planner::build_schedule() {
         // local; pull: the predecessor's partial over NVLink): g_hat is never
         // written to / re-read from HBM.  The launch then ends with a barrier
         // that also covers the ranks the fused Adam reads (final_extra).
-        if (Lp == &S.reduce && OS == LV_G && opt.fuse_final && !Lp->rounds.empty()) {
-          S.ghat_in.assign(N, {});
+        if (is_red && OS == LV_G && opt.fuse_final && !Lp->rounds.empty()) {
+          gin.assign(N, {});
           Lp->final_extra.assign(N, 0);
           auto& last = Lp->rounds.back();
           for (int r = 0; r < N; ++r) {
@@ -755,14 +793,14 @@ void Planner::build_schedule() {
               const Task& t = last[r][i];
               if (t.dst.rank == d.rank && t.dst.kind == d.kind && t.dst.off == d.off && t.n == C &&
                   t.nin <= kMaxAdamIn) {
-                for (int k = 0; k < t.nin; ++k) S.ghat_in[r].push_back(t.in[k]);
+                for (int k = 0; k < t.nin; ++k) gin[r].push_back(t.in[k]);
                 last[r].erase(last[r].begin() + i);
                 break;
               }
             }
           }
           for (int r = 0; r < N; ++r)
-            for (const Ref& x : S.ghat_in[r])
+            for (const Ref& x : gin[r])
               if (x.rank != r) {
                 Lp->final_extra[r] |= uint64_t(1) << x.rank;
                 Lp->final_extra[x.rank] |= uint64_t(1) << r;
@@ -781,6 +819,12 @@ void Planner::build_schedule() {
         }
         if (Lp->final_extra.empty()) Lp->final_extra.assign(N, 0);
       }
+    } else if (N == 1 && opt.accum) {   // one rank: the accumulation is a local fold
+      S.accum.add(0, 0, make_task(n, {grad(0, 0)}, Ref{0, acc_kind, s}));
+      S.accum.final_extra.assign(1, 0);
+      S.reduce_acc.final_extra.assign(1, 0);
+      S.reduce.final_extra.assign(1, 0);
+      S.gather.final_extra.assign(1, 0);
     } else if (N > 1 && topo == 4) {  // NCCL comparator
       for (int r = 0; r < N; ++r) {
         auto& red = S.nccl_reduce[r];
@@ -823,6 +867,10 @@ void Planner::build_schedule() {
       S.os_off[r] = s / divl(OS);
       S.ghat[r] = (N == 1) ? grad(r, 0) : ghat_base(r);
       if (S.ghat_in.size() != (size_t)N || S.ghat_in[r].empty()) S.ghat_in.resize(N), S.ghat_in[r] = {S.ghat[r]};
+      if (opt.accum && (S.ghat_in_acc.size() != (size_t)N || S.ghat_in_acc[r].empty())) {
+        S.ghat_in_acc.resize(N);
+        S.ghat_in_acc[r] = {(N == 1) ? Ref{r, acc_kind, s} : ghat_base(r)};   // materialised g_hat
+      }
       Ref pb = param_base(r);
       if (P == OS) S.param[r] = pb;
       else if (P == LV_I) S.param[r] = at(pb, int64_t(j) * C);              // OS = G
@@ -841,11 +889,12 @@ void Planner::validate_refs() const {
   };
   for (size_t b = 0; b < sched.size(); ++b) {
     const BucketSchedule& S = sched[b];
-    for (const Launch* L : {&S.reduce, &S.gather})
+    for (const Launch* L : {&S.reduce, &S.gather, &S.accum, &S.reduce_acc})
       for (const auto& rnd : L->rounds)
         for (const auto& v : rnd)
           for (const Task& t : v) {
-            if (t.n <= 0 || t.n % 8 != 0 || t.nin < 1 || t.nin > kMaxIn)
+            if (t.n <= 0 || t.n % 8 != 0 || t.nin < 1 || t.nin > kMaxIn ||
+                (L == &S.accum && t.dst.kind == acc_kind && t.nin + 1 > kMaxIn))
               throw std::logic_error("bad task shape in bucket " + std::to_string(b));
             for (int i = 0; i < t.nin; ++i)
               if (!ok(t.in[i], t.n)) throw std::logic_error("task input out of range in bucket " + std::to_string(b));
@@ -855,13 +904,41 @@ void Planner::validate_refs() const {
       if (!ok(S.param[r], S.os_len)) throw std::logic_error("adam output out of range in bucket " + std::to_string(b));
       for (const Ref& x : S.ghat_in[r])
         if (!ok(x, S.os_len)) throw std::logic_error("adam input out of range in bucket " + std::to_string(b));
+      for (size_t i = 0; opt.accum && i < S.ghat_in_acc[r].size(); ++i)
+        if (!ok(S.ghat_in_acc[r][i], S.os_len))
+          throw std::logic_error("adam input out of range in bucket " + std::to_string(b));
     }
   }
 }
 
 void Planner::count_bytes() {
+  // bytes each rank sends (pull: what peers read from it; push: what it stores
+  // into peers) over a list of launches plus the fused-Adam peer reads
+  auto count = [&](std::initializer_list<const Launch*> Ls, const std::vector<std::vector<Ref>>* gin,
+                   int64_t os_len, std::vector<int64_t>& si, std::vector<int64_t>& se) {
+    for (const Launch* L : Ls)
+      for (const auto& rnd : L->rounds)
+        for (int x = 0; x < N; ++x)
+          for (const Task& t : rnd[x]) {
+            for (int i = 0; i < t.nin; ++i) {   // pull: y's bytes travel to x
+              const int y = t.in[i].rank;
+              if (y == x) continue;
+              (grp(x) == grp(y) ? si[y] : se[y]) += 2 * t.n;
+            }
+            const int z = t.dst.rank;            // push: x's bytes travel to z
+            if (z != x) (grp(x) == grp(z) ? si[x] : se[x]) += 2 * t.n;
+          }
+    // fused final hop: the Adam kernel reads these inputs (pull: over NVLink)
+    for (int x = 0; gin && x < N && (int)gin->size() == N; ++x)
+      for (const Ref& y : (*gin)[x])
+        if (y.rank != x) (grp(x) == grp(y.rank) ? si[y.rank] : se[y.rank]) += 2 * os_len;
+  };
   send_intra.assign(N, 0);
   send_inter.assign(N, 0);
+  acc_send_intra.assign(N, 0);
+  acc_send_inter.assign(N, 0);
+  accstep_send_intra.assign(N, 0);
+  accstep_send_inter.assign(N, 0);
   n_rounds = 0;
   n_comm_launches = 0;
   for (const BucketSchedule& S : sched) {
@@ -869,22 +946,12 @@ void Planner::count_bytes() {
       if (L->empty()) continue;
       ++n_comm_launches;
       n_rounds += (int)L->rounds.size();
-      for (const auto& rnd : L->rounds)
-        for (int x = 0; x < N; ++x)
-          for (const Task& t : rnd[x]) {
-            for (int i = 0; i < t.nin; ++i) {   // pull: y's bytes travel to x
-              const int y = t.in[i].rank;
-              if (y == x) continue;
-              (grp(x) == grp(y) ? send_intra[y] : send_inter[y]) += 2 * t.n;
-            }
-            const int z = t.dst.rank;            // push: x's bytes travel to z
-            if (z != x) (grp(x) == grp(z) ? send_intra[x] : send_inter[x]) += 2 * t.n;
-          }
     }
-    // fused final hop: the Adam kernel reads these inputs (pull: over NVLink)
-    for (int x = 0; x < N && (int)S.ghat_in.size() == N; ++x)
-      for (const Ref& y : S.ghat_in[x])
-        if (y.rank != x) (grp(x) == grp(y.rank) ? send_intra[y.rank] : send_inter[y.rank]) += 2 * S.os_len;
+    count({&S.reduce, &S.gather}, &S.ghat_in, S.os_len, send_intra, send_inter);
+    if (opt.accum) {
+      count({&S.accum}, nullptr, 0, acc_send_intra, acc_send_inter);
+      count({&S.reduce_acc, &S.gather}, &S.ghat_in_acc, S.os_len, accstep_send_intra, accstep_send_inter);
+    }
     // NCCL comparator: ring-algorithm volumes of each call (perf only)
     for (int r = 0; r < N && opt.topology == 4; ++r) {
       for (const auto* calls : {&S.nccl_reduce[r], &S.nccl_gather[r]}) {

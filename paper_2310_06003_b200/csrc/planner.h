@@ -28,6 +28,7 @@ enum BufKind : int {
   BUF_P1,          // HO phase-1 / direct phase-1 output: 2 parities
   BUF_SOWN,        // own-group partial (HO phase 2): 2 parities
   BUF_LAND,        // direct push landing slots: 2 parities x ((M-1) chunks + (g-1) segments)
+  BUF_GACC,        // G = N gradient accumulator (psi_pad; only for grad_accum plans)
   BUF_NKINDS
 };
 
@@ -85,6 +86,12 @@ struct BucketSchedule {
   std::vector<Ref> param;    // parameter-buffer position of the OS residency
   std::vector<int64_t> os_off;   // offset in the rank's opt-state arrays
   int64_t os_len = 0;
+  // gradient accumulation (R27): `accum` reduces one micro-batch to
+  // the G residency and writes the accumulator (the engine appends the
+  // accumulator as the last fold input from the second micro-batch on);
+  // `reduce_acc` finishes the reduction from the accumulator after the last one
+  Launch accum, reduce_acc;
+  std::vector<std::vector<Ref>> ghat_in_acc;
 };
 
 struct PlanOptions {
@@ -93,6 +100,7 @@ struct PlanOptions {
   int pipeline_depth = 2;
   bool push = true;          // push (remote stores) or pull (remote loads) transport
   bool fuse_final = true;    // OS = G: fold the owner's last reduction hop into Adam
+  bool accum = false;        // build the gradient-accumulation launches (s > 1)
 };
 
 class Planner {
@@ -119,6 +127,9 @@ class Planner {
   std::vector<BucketSchedule> sched;
   std::vector<std::string> grad_ops, rest_ops;        // primitives (for reporting)
   std::vector<int64_t> send_intra, send_inter;        // bytes per rank per step
+  std::vector<int64_t> acc_send_intra, acc_send_inter;        // per accumulated micro-batch
+  std::vector<int64_t> accstep_send_intra, accstep_send_inter;  // per step after accumulation
+  int acc_kind = -1;                                  // accumulator buffer (GSHARD / GACC)
   int n_rounds = 0, n_comm_launches = 0;
 
   static int div(Level l, int N, int M) { return l == LV_N ? 1 : (l == LV_I ? M : N); }

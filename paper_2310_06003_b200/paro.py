@@ -45,7 +45,7 @@ class paro_opts_t(C.Structure):
                 ("beta2", C.c_float), ("eps", C.c_float), ("weight_decay", C.c_float),
                 ("loss_scale", C.c_float), ("comm_ctas", C.c_int), ("pipeline_depth", C.c_int),
                 ("pull_transport", C.c_int), ("adam_impl", C.c_int), ("comm_impl", C.c_int),
-                ("inter_gbps", C.c_float), ("stream", C.c_void_p)]
+                ("inter_gbps", C.c_float), ("grad_accum", C.c_int), ("stream", C.c_void_p)]
 
 
 class paro_plan_info_t(C.Structure):
@@ -54,7 +54,9 @@ class paro_plan_info_t(C.Structure):
                 ("os_numel", C.c_int64), ("mem_p_bytes", C.c_int64), ("mem_g_bytes", C.c_int64),
                 ("mem_os_bytes", C.c_int64), ("workspace_bytes", C.c_int64),
                 ("step_send_bytes_intra", C.c_int64), ("step_send_bytes_inter", C.c_int64),
-                ("n_rounds", C.c_int32), ("n_comm_launches", C.c_int32)]
+                ("n_rounds", C.c_int32), ("n_comm_launches", C.c_int32),
+                ("accum_send_bytes_intra", C.c_int64), ("accum_send_bytes_inter", C.c_int64),
+                ("accum_step_send_bytes_intra", C.c_int64), ("accum_step_send_bytes_inter", C.c_int64)]
 
 
 class paro_step_stats_t(C.Structure):
@@ -93,6 +95,8 @@ paro_plan_info = _sig("paro_plan_info", _st, _vp, C.POINTER(paro_plan_info_t))
 paro_shard_range = _sig("paro_shard_range", _st, _vp, C.c_int, C.c_int, _i64, C.POINTER(_i64), C.POINTER(_i64))
 paro_bucket_range = _sig("paro_bucket_range", _st, _vp, _i64, C.POINTER(_i64), C.POINTER(_i64))
 paro_rank_send_bytes = _sig("paro_rank_send_bytes", _st, _vp, C.c_int, C.POINTER(_i64), C.POINTER(_i64))
+paro_rank_accum_send_bytes = _sig("paro_rank_accum_send_bytes", _st, _vp, C.c_int, C.POINTER(_i64),
+                                  C.POINTER(_i64), C.POINTER(_i64), C.POINTER(_i64))
 paro_buffer = _sig("paro_buffer", _st, _vp, C.c_int, C.c_int, C.POINTER(_vp))
 paro_opt_state_init = _sig("paro_opt_state_init", _st, _vp, C.c_int, _vp, C.POINTER(paro_opt_state_t))
 paro_opt_state_init_synth = _sig("paro_opt_state_init_synth", _st, _vp, C.c_int, C.c_uint64,
@@ -100,6 +104,7 @@ paro_opt_state_init_synth = _sig("paro_opt_state_init_synth", _st, _vp, C.c_int,
 paro_synth_grads = _sig("paro_synth_grads", _st, _vp, C.c_int, C.c_uint64, _i64)
 paro_step = _sig("paro_step", _st, _vp, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(paro_opt_state_t),
                  C.c_float, _i64)
+paro_accumulate = _sig("paro_accumulate", _st, _vp, C.POINTER(_vp))
 paro_step_stats = _sig("paro_step_stats", _st, _vp, C.POINTER(paro_step_stats_t))
 paro_plan_destroy = _sig("paro_plan_destroy", _st, _vp)
 paro_collective = _sig("paro_collective", _st, _vp, C.c_int)
@@ -113,7 +118,8 @@ EXPORTED = ["paro_opts_default", "paro_get_unique_id", "paro_init", "paro_init_e
             "paro_bucket_range", "paro_rank_send_bytes", "paro_buffer", "paro_opt_state_init",
             "paro_opt_state_init_synth", "paro_synth_grads", "paro_step", "paro_step_stats",
             "paro_plan_destroy", "paro_last_error", "paro_version", "paro_profile_start",
-            "paro_profile_stop", "paro_collective"]
+            "paro_profile_stop", "paro_collective", "paro_accumulate",
+            "paro_rank_accum_send_bytes"]
 
 
 def check(status):
@@ -125,7 +131,7 @@ def check(status):
 # ---------------------------------------------------------------- helpers
 def make_opts(bucket_elems=1 << 26, topology="ho", beta1=0.9, beta2=0.95, eps=1e-8, weight_decay=0.0,
               loss_scale=1.0, comm_ctas=148, pipeline_depth=2, stream=None, transport="pull", adam_impl="auto",
-              comm_impl="tma", inter_gbps=0.0):
+              comm_impl="tma", inter_gbps=0.0, grad_accum=False):
     o = paro_opts_t()
     paro_opts_default(C.byref(o))
     o.bucket_elems = int(bucket_elems)
@@ -137,6 +143,7 @@ def make_opts(bucket_elems=1 << 26, topology="ho", beta1=0.9, beta2=0.95, eps=1e
     o.adam_impl = {"auto": 0, "lsu": 1}[adam_impl]
     o.comm_impl = {"tma": 0, "lsu": 1}[comm_impl]
     o.inter_gbps = float(inter_gbps)
+    o.grad_accum = 1 if grad_accum else 0
     o.stream = stream
     return o
 
@@ -204,6 +211,12 @@ class Plan:
         check(paro_rank_send_bytes(self.h, rank, C.byref(a), C.byref(b)))
         return a.value, b.value
 
+    def accum_send_bytes(self, rank):
+        """((intra, inter) per paro_accumulate call, (intra, inter) of the step after it)."""
+        v = [_i64() for _ in range(4)]
+        check(paro_rank_accum_send_bytes(self.h, rank, *[C.byref(x) for x in v]))
+        return (v[0].value, v[1].value), (v[2].value, v[3].value)
+
     def buffer(self, rank, kind):
         p = _vp()
         check(paro_buffer(self.h, rank, kind, C.byref(p)))
@@ -227,6 +240,12 @@ class Plan:
         gp = (_vp * len(grads))(*grads) if grads is not None else None
         pp = (_vp * len(params))(*params) if params is not None else None
         check(paro_step(self.h, gp, pp, sts, float(lr), int(step)))
+
+    def accumulate(self, grads=None):
+        """paro_accumulate: add one micro-batch (grads: None = the flat gradient
+        buffers, else a flat list of per-parameter pointers, rank-major)."""
+        gp = (_vp * len(grads))(*grads) if grads is not None else None
+        check(paro_accumulate(self.h, gp))
 
     def stats(self):
         s = paro_step_stats_t()

@@ -37,6 +37,7 @@ def main():
     sizes = cfg.get("sizes", [world * 64 * 40 + 24, 333])
     B = cfg.get("bucket", world * 64 * 12)
     steps = cfg.get("steps", 2)
+    accum = cfg.get("accum", 0)          # > 0: that many micro-batches per step (paro_accumulate)
     for M in splits:
         uid = paro.unique_id() if rank == 0 else bytes(128)
         t = torch.tensor(list(uid), dtype=torch.uint8)
@@ -45,14 +46,19 @@ def main():
         for code, topo, tr in [(c, t_, x) for c in codes for t_ in topos for x in transports]:
             if True:
                 pl = paro.Plan(ctx, code, sizes, bucket_elems=B, topology=topo, transport=tr, comm_impl=comm_impl,
-                               inter_gbps=inter_gbps)
+                               inter_gbps=inter_gbps, grad_accum=accum > 0)
                 info = pl.info()
                 st = [torch.empty(info["os_numel"], dtype=torch.float32, device="cuda") for _ in range(3)]
                 ptrs = [[x.data_ptr() for x in st]]
                 pl.opt_state_init(rank, ptrs[0], seed=SEED)
                 stats = None
                 for s in range(1, steps + 1):
-                    pl.synth_grads(rank, SEED, s)
+                    if accum:
+                        for k in range(accum):
+                            pl.synth_grads(rank, SEED, (s << 8) | (k + 1))
+                            pl.accumulate()
+                    else:
+                        pl.synth_grads(rank, SEED, s)
                     pl.step(ptrs, 3e-4, s)
                     stats = pl.stats()
                 torch.cuda.synchronize()

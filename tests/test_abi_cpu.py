@@ -135,3 +135,45 @@ def test_llama7b_plan_accounting():
             assert pl.send_bytes(r) == (2 * a, 2 * b)
         pl.close()
     ctx.close()
+
+
+@pytest.mark.parametrize("N,M", [(8, 4), (8, 2), (4, 2), (9, 3), (8, 1), (8, 8), (1, 1)])
+def test_accumulation_bytes_match_oracle_simulator(N, M):
+    """grad_accum plans: s * (bytes per paro_accumulate) + (bytes of the step
+    after it) == the oracle's simulated mini-batch with s micro-batches, for
+    s = 1 and s = 3 (pins both per-call numbers), every strategy and topology."""
+    sizes = [3000, 517, 64, 9000, 7]
+    B = N * 64 * 4
+    lay = L.Layout(sizes, N, M, B)
+    w0 = master_f32(0, lay.psi)
+    zero = [np.zeros(lay.psi, np.uint16) for _ in range(N)]
+    ctx = paro.Context(N, M)
+    for code in S.paro_strategies():
+        for topo, tr in [("ho", "pull"), ("ho", "push"), ("two_step", "pull"), ("flat", "pull"), ("direct", "push")]:
+            pl = paro.Plan(ctx, code, sizes, bucket_elems=B, topology=topo, transport=tr, grad_accum=True)
+            for s in (1, 3):
+                res = ST.strategy_accum_step(code, lay, [zero] * s, ST.init_state(w0, lay, code),
+                                             nm.AdamScalars(1e-3, 1, accum_steps=s),
+                                             topology="two_step" if topo == "direct" else topo)
+                for r in range(N):
+                    (ai, ae), (si, se) = pl.accum_send_bytes(r)
+                    if topo == "direct":    # one-shot: bytes follow the closed form, not the ring trace
+                        per_mb, once = A.accum_ops(code)
+                        assert (s * ai + si, s * ae + se) == tuple(2 * x for x in A.accum_units_per_rank(
+                            code, N, M, lay.psi_pad, s)), (code, r)
+                    else:
+                        assert (s * ai + si, s * ae + se) == (2 * res.sent[r][0], 2 * res.sent[r][1]), \
+                            (code, topo, tr, s, r)
+            pl.close()
+    ctx.close()
+
+
+def test_accumulate_needs_grad_accum_plan():
+    ctx = paro.Context(4, 2)
+    pl = paro.Plan(ctx, "IIG", [4096])
+    with pytest.raises(paro.ParoError, match="grad_accum"):
+        pl.accum_send_bytes(0)
+    with pytest.raises(paro.ParoError, match="NCCL"):
+        paro.Plan(ctx, "IIG", [4096], topology="nccl", grad_accum=True)
+    pl.close()
+    ctx.close()

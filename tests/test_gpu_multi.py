@@ -24,20 +24,27 @@ def _ngpu():
     return torch.cuda.device_count() if torch.cuda.is_available() else 0
 
 
-def _dp(lay, steps):
+def _dp(lay, steps, accum=0, g_level="N"):
     w = ST.pad_flat(master_f32(0, lay.psi), lay.psi_pad, np.float32)
     m, v = np.zeros_like(w), np.zeros_like(w)
     for t in range(1, steps + 1):
-        w, m, v, p, gh = ST.dp_step(lay, [grad_bits(r, t, 0, lay.psi) for r in range(lay.N)], w, m, v,
-                                    nm.AdamScalars(3e-4, t))
-    return w, m, v, p, gh
+        if accum:
+            mb = [[grad_bits(r, (t << 8) | (k + 1), 0, lay.psi) for r in range(lay.N)] for k in range(accum)]
+            w, m, v, p, gh = ST.dp_accum_step(lay, mb, w, m, v, nm.AdamScalars(3e-4, t, accum_steps=accum),
+                                              g_level)
+            sg = nm.AdamScalars(3e-4, t, accum_steps=accum).s_g
+        else:
+            w, m, v, p, gh = ST.dp_step(lay, [grad_bits(r, t, 0, lay.psi) for r in range(lay.N)], w, m, v,
+                                        nm.AdamScalars(3e-4, t))
+            sg = np.float32(1.0)
+    return w, m, v, p, nm.grad_sq_sum(gh, sg)
 
 
 CODES = ["NNN", "NNI", "NNG", "NII", "NIG", "NGG", "INI", "ING", "III", "IIG", "IGG", "GNG", "GIG", "GGG"]
 
 
 @pytest.mark.skipif(_ngpu() < 2, reason="needs >= 2 GPUs")
-@pytest.mark.parametrize("variant", ["default", "paced_lsu"])
+@pytest.mark.parametrize("variant", ["default", "paced_lsu", "accum"])
 def test_real_ranks_match_oracle(tmp_path, variant):
     world = min(_ngpu(), 4)
     splits = [m for m in range(1, world + 1) if world % m == 0]
@@ -46,6 +53,8 @@ def test_real_ranks_match_oracle(tmp_path, variant):
     if variant == "paced_lsu":   # emulated slow inter link (no fused hop) and the LSU kernels: same bits
         cfg.update({"codes": ["NNN", "IIG", "GGG", "NIG"], "topos": ["ho", "flat"], "transports": ["pull"],
                     "inter_gbps": 50.0, "comm_impl": "lsu"})
+    if variant == "accum":       # gradient accumulation, s = 3 micro-batches per step (NEXT-1)
+        cfg.update({"accum": 3, "topos": ["ho", "two_step"], "transports": ["pull", "push"]})
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr=127.0.0.1", "--master-port=29517", os.path.join(ROOT, "tests", "dist_worker.py"),
            str(tmp_path), json.dumps(cfg)]
@@ -53,9 +62,9 @@ def test_real_ranks_match_oracle(tmp_path, variant):
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     for M in splits:
         lay = L.Layout(cfg["sizes"], world, M, cfg["bucket"])
-        w, m, v, p, gh = _dp(lay, 2)
-        norm = nm.grad_sq_sum(gh)
+        refs = {gl: _dp(lay, 2, cfg.get("accum", 0), gl) for gl in "NIG"}
         for code in cfg["codes"]:
+            w, m, v, p, norm = refs[code[1]]
             for topo in cfg["topos"]:
               if topo == "flat":   # different (deterministic) order: compare with the oracle's flat ring
                   continue

@@ -32,12 +32,15 @@ class EmuRun:
     """All ranks of one split on cuda:0 through the C ABI."""
 
     def __init__(self, N, M, code, sizes, B, topo="ho", depth=2, wd=0.0, loss_scale=1.0, transport="push",
-                 adam_impl="auto", comm_impl="tma"):
+                 adam_impl="auto", comm_impl="tma", grad_accum=False, mode="emulated"):
         paro = _paro()
-        self.ctx = paro.Context(N, M, mode="emulated", device=0)
+        if mode == "emulated":
+            self.ctx = paro.Context(N, M, mode="emulated", device=0)
+        else:   # one real rank (N = 1): the bench's launch configuration
+            self.ctx = paro.Context(1, 1, mode="real", rank=0, device=0, uid=paro.unique_id())
         self.pl = paro.Plan(self.ctx, code, sizes, bucket_elems=B, topology=topo, pipeline_depth=depth,
                             weight_decay=wd, loss_scale=loss_scale, transport=transport, adam_impl=adam_impl,
-                            comm_impl=comm_impl)
+                            comm_impl=comm_impl, grad_accum=grad_accum)
         self.info = self.pl.info()
         self.N, self.code, self.sizes = N, code, sizes
         n = self.info["os_numel"]
@@ -284,3 +287,111 @@ def test_pack_and_unpack_paths_and_depth_determinism():
             run.close()
         for a, b in zip(*outs):
             assert np.array_equal(a, b)
+
+
+
+# --------------------------------------------------------------------- gradient accumulation (NEXT-1)
+def _mb_id(t, k):
+    return (t << 8) | (k + 1)     # synthetic-gradient counter of micro-batch k of step t
+
+
+def _accum_reference(lay, steps, s, g_level, loss_scale=1.0):
+    w = ST.pad_flat(master_f32(0, lay.psi), lay.psi_pad, np.float32)
+    m, v = np.zeros_like(w), np.zeros_like(w)
+    norms = []
+    for t in range(1, steps + 1):
+        mb = [[grad_bits(r, _mb_id(t, k), 0, lay.psi) for r in range(lay.N)] for k in range(s)]
+        sc = nm.AdamScalars(LR, t, loss_scale=loss_scale, accum_steps=s)
+        w, m, v, p, gh = ST.dp_accum_step(lay, mb, w, m, v, sc, g_level)
+        norms.append(nm.grad_sq_sum(gh, sc.s_g))
+    return w, m, v, p, norms
+
+
+def _run_accum(run, steps, s):
+    stats = []
+    for t in range(1, steps + 1):
+        for k in range(s):
+            for r in range(run.N):
+                run.pl.synth_grads(r, SEED, _mb_id(t, k))
+            run.pl.accumulate()
+        stats.append(run.step(t))
+    return stats
+
+
+@pytest.mark.parametrize("topo,transport", [("ho", "pull"), ("ho", "push"), ("two_step", "pull"),
+                                            ("direct", "pull")])
+def test_accumulation_every_strategy_2x4(topo, transport):
+    """BASELINE config 1 shape (2 groups x 4, 16 buckets) with s = 3 micro-batches,
+    two mini-batch steps: every strategy bit-exact vs dp_accum_step (R27)."""
+    N, M, s = 8, 4, 3
+    sizes = [N * 64 * 40 + 24, 1000]
+    B = N * 64 * 8
+    lay = L.Layout(sizes, N, M, B)
+    refs = {gl: _accum_reference(lay, 2, s, gl) for gl in "NIG"}
+    for code in S.paro_strategies():
+        run = EmuRun(N, M, code, sizes, B, topo=topo, transport=transport, grad_accum=True)
+        stats = _run_accum(run, 2, s)
+        ref = refs[code[1]]
+        _check_against_dp(run, lay, ref)
+        assert abs(stats[-1]["grad_norm"] ** 2 - ref[4][-1]) <= 1e-12 * ref[4][-1]
+        (ai, ae), (si, se) = run.pl.accum_send_bytes(0)
+        assert (stats[-1]["sent_intra"], stats[-1]["sent_inter"]) == (si, se)
+        run.close()
+
+
+@pytest.mark.parametrize("N,M", [(8, 2), (8, 1), (8, 8), (9, 3), (2, 1)])
+def test_accumulation_splits(N, M):
+    s = 2
+    sizes = ragged_param_sizes() + [N * 64 * 9]
+    B = N * 64 * 4
+    lay = L.Layout(sizes, N, M, B)
+    refs = {gl: _accum_reference(lay, 1, s, gl) for gl in "NIG"}
+    for code in ("NNN", "NIG", "IIG", "IGG", "III", "GGG", "NNI"):
+        run = EmuRun(N, M, code, sizes, B, grad_accum=True, transport="pull")
+        _run_accum(run, 1, s)
+        _check_against_dp(run, lay, refs[code[1]])
+        run.close()
+
+
+def test_accumulation_single_gpu_real_mode():
+    """N = 1 in the bench's configuration (one real rank): local accumulation,
+    loss scale 4, s = 4, three steps."""
+    sizes = [1 << 16, 3 * 4096 + 8, 517]
+    B = 1 << 14
+    lay = L.Layout(sizes, 1, 1, B)
+    ref = _accum_reference(lay, 3, 4, "N", loss_scale=4.0)
+    for code in ("IIG", "NNN"):
+        run = EmuRun(1, 1, code, sizes, B, grad_accum=True, loss_scale=4.0, mode="real")
+        stats = _run_accum(run, 3, 4)
+        _check_against_dp(run, lay, ref)
+        assert abs(stats[-1]["grad_norm"] ** 2 - ref[4][-1]) <= 1e-12 * ref[4][-1]
+        run.close()
+
+
+def test_accumulation_with_one_micro_batch_is_the_plain_step():
+    N, M = 8, 4
+    sizes = [N * 64 * 24]
+    B = N * 64 * 8
+    lay = L.Layout(sizes, N, M, B)
+    ref = _dp_reference(lay, 1)
+    for code in ("IIG", "NIG", "GGG", "NNN"):
+        run = EmuRun(N, M, code, sizes, B, grad_accum=True, transport="pull")
+        run.set_grads(1)
+        run.pl.accumulate()
+        run.step(1)
+        _check_against_dp(run, lay, ref)
+        run.close()
+
+
+def test_step_after_accumulate_rejects_grads():
+    run = EmuRun(2, 1, "IIG", [4096], 1024, grad_accum=True)
+    run.set_grads(1)
+    run.pl.accumulate()
+    paro = _paro()
+    with pytest.raises(paro.ParoError, match="grads must be NULL"):
+        run.pl.step(run.ptrs(), LR, 1, grads=[run.pl.buffer(0, 0)] * 2)
+    run.close()
+    plain = EmuRun(2, 1, "IIG", [4096], 1024)
+    with pytest.raises(paro.ParoError, match="grad_accum"):
+        plain.pl.accumulate()
+    plain.close()
