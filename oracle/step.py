@@ -18,12 +18,14 @@ residency.  Tests require the two to agree bit for bit (same (N, M, B)).
 """
 from __future__ import annotations
 
+import math
+
 import numpy as np
 
 from . import collectives as C
 from .accounting import step_ops
 from .layout import Layout
-from .numerics import (AdamScalars, adam_update, bf16_bits_from_f32, canonical_fold,
+from .numerics import (F32, AdamScalars, adam_update, bf16_bits_from_f32, canonical_fold,
                        f32_from_bf16_bits, hop, pack)
 from .strategy import validate
 
@@ -55,12 +57,8 @@ def init_state(master_full, lay: Layout, code, ranks=None):
     return out
 
 
-def dp_step(lay: Layout, grads, master, m, v, sc: AdamScalars):
-    """Unsharded data parallel with the canonical order (full-length arrays, Psi_pad).
-
-    grads: list of N flat bf16-bit arrays (length Psi or Psi_pad).
-    Returns (master, m, v, param_bits, g_hat_bits).
-    """
+def dp_reduce(lay: Layout, grads):
+    """g_hat = CanonReduce(RNE_bf16(grad_r / N)) over the N ranks (R2, R4), as bf16 bits."""
     N = lay.N
     geo = C.Geometry(N, lay.M)
     alpha = 1.0 / N
@@ -75,8 +73,56 @@ def dp_step(lay: Layout, grads, master, m, v, sc: AdamScalars):
             S = [canonical_fold([X[geo.r(jj, pp)][a:b] for pp in range(lay.M)], p)
                  for jj in range(geo.g)]
             ghat[a:b] = canonical_fold(S, j)
+    return ghat
+
+
+def dp_step(lay: Layout, grads, master, m, v, sc: AdamScalars):
+    """Unsharded data parallel with the canonical order (full-length arrays, Psi_pad).
+
+    grads: list of N flat bf16-bit arrays (length Psi or Psi_pad).
+    Returns (master, m, v, param_bits, g_hat_bits).
+    """
+    ghat = dp_reduce(lay, grads)
     w2, m2, v2, pb = adam_update(master, m, v, ghat, sc)
     return w2, m2, v2, pb, ghat
+
+
+def clip_coef(norm_sq, clip_norm):
+    """Global-norm clipping coefficient (reading R28; the formula of
+    torch.nn.utils.clip_grad_norm_): min(1, clip_norm / (||g|| + 1e-6)), in
+    double; 1 when clipping is off (clip_norm <= 0)."""
+    if clip_norm <= 0.0:
+        return 1.0
+    return min(1.0, float(F32(clip_norm)) / (math.sqrt(norm_sq) + 1e-6))
+
+
+def dp_clip_step(lay: Layout, grads, master, m, v, lr, step, clip_norm=0.0, skip_nonfinite=False,
+                 accum_steps=1, **adam_kw):
+    """Two-phase step with global-norm clipping and non-finite skip (NEXT-3, R28).
+
+    Phase 1 reduces every gradient and takes the norm of the unscaled
+    gradient, ||fp32(g_hat) * s_g|| (s_g = 1 / (loss_scale * accum_steps)),
+    over all elements; phase 2 runs Adam with the unscale factor
+    s_g' = fp32(s_g_double * clip_coef).  With skip_nonfinite and any
+    non-finite g_hat the step leaves master, m, v and the parameters unchanged.
+    Returns (master, m, v, param_bits, g_hat_bits, norm_sq, coef, skipped).
+    """
+    ghat = dp_reduce(lay, grads)
+    return clip_update(ghat, master, m, v, lr, step, clip_norm, skip_nonfinite, accum_steps, adam_kw)
+
+
+def clip_update(ghat, master, m, v, lr, step, clip_norm, skip_nonfinite, accum_steps, adam_kw):
+    sc0 = AdamScalars(lr, step, accum_steps=accum_steps, **adam_kw)
+    g = f32_from_bf16_bits(ghat) * sc0.s_g
+    norm_sq = float(np.sum(g.astype(np.float64) ** 2))
+    nonfinite = not bool(np.all(np.isfinite(g)))
+    if skip_nonfinite and nonfinite:
+        return (np.array(master, np.float32), np.array(m, np.float32), np.array(v, np.float32),
+                bf16_bits_from_f32(master), ghat, norm_sq, 1.0, True)
+    coef = clip_coef(norm_sq, clip_norm) if np.isfinite(norm_sq) else 1.0
+    sc = AdamScalars(lr, step, accum_steps=accum_steps, clip_coef=coef, **adam_kw)
+    w2, m2, v2, pb = adam_update(master, m, v, ghat, sc)
+    return w2, m2, v2, pb, ghat, norm_sq, coef, False
 
 
 def dp_accum_step(lay: Layout, grads_mb, master, m, v, sc: AdamScalars, g_level):
