@@ -95,6 +95,15 @@ typedef struct {
                           * rounds kernel; the final hop is then not fused into    *
                           * Adam).  0 (default): no pacing.  One NVSwitch box has  *
                           * no real intra/inter gap.                */
+  float clip_norm;       /* > 0: clip the global gradient norm to this value       *
+                          * (coef = min(1, clip / (||g|| + 1e-6)), the formula of  *
+                          * torch clip_grad_norm_; R28).  0 = off.       */
+  int skip_nonfinite;    /* 1: a step whose reduced gradient has an inf/NaN leaves *
+                          * master, m, v and the parameters unchanged.  0 = flag   *
+                          * only (default).  clip_norm > 0 or skip_nonfinite = 1   *
+                          * selects the two-phase step: every bucket is reduced    *
+                          * and the norm all-reduced before the first update, and  *
+                          * the reduced gradient stays resident (psi/div(OS) bf16) */
   int grad_accum;        /* 1: enable paro_accumulate (gradient accumulation over  *
                           * s > 1 micro-batches); G = N plans then own  *
                           * a psi_pad bf16 accumulator.  0 (default): off.         */

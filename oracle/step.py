@@ -115,7 +115,7 @@ def clip_update(ghat, master, m, v, lr, step, clip_norm, skip_nonfinite, accum_s
     sc0 = AdamScalars(lr, step, accum_steps=accum_steps, **adam_kw)
     g = f32_from_bf16_bits(ghat) * sc0.s_g
     norm_sq = float(np.sum(g.astype(np.float64) ** 2))
-    nonfinite = not bool(np.all(np.isfinite(g)))
+    nonfinite = not bool(np.all(np.isfinite(f32_from_bf16_bits(ghat))))   # R9: a non-finite g_hat
     if skip_nonfinite and nonfinite:
         return (np.array(master, np.float32), np.array(m, np.float32), np.array(v, np.float32),
                 bf16_bits_from_f32(master), ghat, norm_sq, 1.0, True)

@@ -280,8 +280,12 @@ __device__ __forceinline__ void adam_unit(const AdamSeg& sg, int64_t u, const Ad
   reinterpret_cast<uint4*>(sg.param)[u] = pack8(w);
 }
 
+__device__ __forceinline__ float unscale_of(const AdamArgs& a) { return a.s_g_dev ? *a.s_g_dev : a.s_g; }
+
 __global__ void __launch_bounds__(kAdamBlock, 3) adam_kernel(const AdamArgs a) {
-  const AdamScal c{a.b1, a.omb1, a.b2, a.omb2, a.step_size, a.bc2s, a.eps, a.decay, a.s_g, a.alpha, a.has_wd};
+  if (a.skip && *a.skip) return;   // two-phase step: non-finite gradients, update skipped
+  const AdamScal c{a.b1, a.omb1, a.b2, a.omb2, a.step_size, a.bc2s, a.eps, a.decay, unscale_of(a), a.alpha,
+                   a.has_wd};
   int64_t U = 0;
   for (int i = 0; i < a.nseg; ++i) U += a.seg[i].n8;
   const int64_t per = (U + gridDim.x - 1) / gridDim.x;
@@ -375,7 +379,9 @@ __device__ __forceinline__ bool tile_of(const AdamArgs& a, int64_t t, TileRef& o
 __global__ void __launch_bounds__(kTmaThreads, 1) adam_tma_kernel(const AdamArgs a, int gnin_max, int stages) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ uint64_t full_bar[4];
-  const AdamScal c{a.b1, a.omb1, a.b2, a.omb2, a.step_size, a.bc2s, a.eps, a.decay, a.s_g, a.alpha, a.has_wd};
+  if (a.skip && *a.skip) return;   // two-phase step: non-finite gradients, update skipped
+  const AdamScal c{a.b1, a.omb1, a.b2, a.omb2, a.step_size, a.bc2s, a.eps, a.decay, unscale_of(a), a.alpha,
+                   a.has_wd};
   const size_t g_bytes = (size_t)kTmaTile * 2, f_bytes = (size_t)kTmaTile * 4;
   const size_t stage_bytes = gnin_max * g_bytes + 3 * f_bytes;
   int64_t total = 0;
@@ -582,6 +588,69 @@ __global__ void __launch_bounds__(kRtThreads) rounds_tma_kernel(const RoundsArgs
   trace_stamp(a, kTraceSlots - 1);
 }
 
+// ------------------------------------------------------------- two-phase step (R28)
+// Phase 1: sum (fold(gin) * s_g)^2 and the non-finite flag over the segments,
+// same partition and block reduction as adam_kernel (2 B read per element).
+__global__ void __launch_bounds__(kAdamBlock) grad_norm_kernel(const AdamArgs a) {
+  int64_t U = 0;
+  for (int i = 0; i < a.nseg; ++i) U += a.seg[i].n8;
+  const int64_t per = (U + gridDim.x - 1) / gridDim.x;
+  const int64_t b0 = min(U, (int64_t)blockIdx.x * per);
+  const int64_t b1 = min(U, b0 + per);
+  double nsq = 0.0;
+  int bad = 0;
+  int64_t base = 0;
+  for (int i = 0; i < a.nseg && base < b1; ++i) {
+    const AdamSeg& sg = a.seg[i];
+    const int64_t n8 = sg.n8;
+    const int64_t s = max(b0, base) - base, e = min(b1, base + n8) - base;
+    if (sg.in_norm) {
+      for (int64_t u = s + threadIdx.x; u < e; u += blockDim.x) {
+        float g[8];
+        unpack8(__ldcs(reinterpret_cast<const uint4*>(sg.gin[0]) + u), g);
+        if (sg.graw & 1u) scale_round8(g, a.alpha);
+        for (int k = 1; k < sg.gnin; ++k) {
+          float x[8];
+          unpack8(__ldcs(reinterpret_cast<const uint4*>(sg.gin[k]) + u), x);
+          if ((sg.graw >> k) & 1u) scale_round8(x, a.alpha);
+          hop8(g, x);
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          if (!isfinite(g[q])) bad = 1;
+          const float gr = __fmul_rn(g[q], a.s_g);
+          nsq += (double)gr * (double)gr;
+        }
+      }
+    }
+    base += n8;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) nsq += __shfl_xor_sync(0xffffffffu, nsq, o);
+  __shared__ double s_part[kAdamBlock / 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) s_part[wid] = nsq;
+  const int any_bad = __syncthreads_or(bad);
+  if (wid == 0) {
+    double x = (lane < (int)(blockDim.x / 32)) ? s_part[lane] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    if (lane == 0) {
+      a.partials[blockIdx.x] = x;
+      if (any_bad) atomicOr(a.nonfinite, 1);
+    }
+  }
+}
+
+__global__ void clip_scale_kernel(const double* norm_sq, const int* nonfinite, double clip, double base,
+                                  int skip_nonfinite, float* s_g_out, int* skip_out) {
+  const double n = sqrt(*norm_sq);
+  double coef = 1.0;
+  if (clip > 0.0 && isfinite(n)) coef = fmin(1.0, clip / (n + 1e-6));
+  *s_g_out = (float)(base * coef);
+  *skip_out = (skip_nonfinite && *nonfinite) ? 1 : 0;
+}
+
 // ------------------------------------------------------------- norm finalize
 __global__ void __launch_bounds__(1024) norm_finalize_kernel(const double* p, int n, double* out) {
   __shared__ double sh[1024];
@@ -757,6 +826,17 @@ cudaError_t launch_adam_tma(const AdamArgs& a, int sms, cudaStream_t s, int smem
 
 cudaError_t launch_norm_finalize(const double* partials, int n, double* out, cudaStream_t s) {
   norm_finalize_kernel<<<1, 1024, 0, s>>>(partials, n, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_grad_norm(const AdamArgs& a, int grid, cudaStream_t s) {
+  grad_norm_kernel<<<grid, kAdamBlock, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_clip_scale(const double* norm_sq, const int* nonfinite, double clip, double base,
+                              int skip_nonfinite, float* s_g_out, int* skip_out, cudaStream_t s) {
+  clip_scale_kernel<<<1, 1, 0, s>>>(norm_sq, nonfinite, clip, base, skip_nonfinite, s_g_out, skip_out);
   return cudaGetLastError();
 }
 

@@ -86,6 +86,11 @@ struct AdamArgs {
   int has_wd;
   double* partials;  // [gridDim.x] block partial sums of (g * s_g)^2
   int* nonfinite;
+  // two-phase step (clipping / non-finite skip, R28): when set, the unscale
+  // factor is read from the device (computed from the global norm) and the
+  // update is skipped entirely while *skip != 0
+  const float* s_g_dev;
+  const int* skip;
 };
 
 struct PackEntry {     // one tensor slice: src/dst element pointers + count
@@ -100,6 +105,13 @@ cudaError_t launch_adam(const AdamArgs& a, int grid, cudaStream_t s, int cap_two
 cudaError_t launch_adam_tma(const AdamArgs& a, int sms, cudaStream_t s, int smem_budget_kb);
 cudaError_t launch_rounds_tma(const RoundsArgs& a, int grid, int max_in, cudaStream_t s);
 cudaError_t launch_norm_finalize(const double* partials, int n, double* out, cudaStream_t s);
+// phase 1 of the two-phase step: block partials of sum (fold(gin) * s_g)^2 and
+// the non-finite flag, 2 bytes read per element, no update
+cudaError_t launch_grad_norm(const AdamArgs& a, int grid, cudaStream_t s);
+// between the phases: s_g_out = fp32(base * coef), coef = min(1, clip / (sqrt(norm_sq) + 1e-6))
+// (1 if clip <= 0 or the norm is not finite); skip_out = skip_nonfinite && *nonfinite
+cudaError_t launch_clip_scale(const double* norm_sq, const int* nonfinite, double clip, double base,
+                              int skip_nonfinite, float* s_g_out, int* skip_out, cudaStream_t s);
 cudaError_t launch_pack(const PackEntry* table, int n_entries, int64_t max_n, cudaStream_t s);
 cudaError_t launch_synth_grad(uint16_t* dst, int64_t psi, int64_t psi_pad, uint64_t key, cudaStream_t s);
 // init master/m/v over flat range [begin, begin+n) into os arrays at os_ptrs and

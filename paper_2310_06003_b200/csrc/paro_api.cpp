@@ -74,6 +74,8 @@ struct paro_plan {
   int partials_cap = 0;
   double* d_norm = nullptr;
   int* d_nonfinite = nullptr;
+  float* d_sg = nullptr;                  // two-phase step: device unscale factor (clip)
+  int* d_skip = nullptr;                  // two-phase step: skip the update
   PackEntry* d_pack = nullptr;
   PackEntry* h_pack = nullptr;            // pinned staging
   int pack_cap = 0;
@@ -417,6 +419,8 @@ void destroy_plan(PlanT* p) {
     cudaFree(p->d_partials);
     cudaFree(p->d_norm);
     cudaFree(p->d_nonfinite);
+    cudaFree(p->d_sg);
+    cudaFree(p->d_skip);
     cudaFree(p->d_pack);
     if (p->h_pack) cudaFreeHost(p->h_pack);
     for (cudaEvent_t e : {p->ev_fork, p->ev_comm, p->ev_comp, p->ev_pack_staged, p->ev_unpack_staged})
@@ -468,6 +472,8 @@ void paro_opts_default(paro_opts_t* o) {
   o->comm_impl = 0;
   o->inter_gbps = 0.f;
   o->grad_accum = 0;
+  o->clip_norm = 0.f;
+  o->skip_nonfinite = 0;
   o->stream = nullptr;
 }
 
@@ -582,6 +588,9 @@ paro_status_t paro_plan(paro_ctx_t ctx, const char* strategy, const int64_t* par
   po.push = o.pull_transport == 0;
   po.fuse_final = !(o.inter_gbps > 0.f);   // paced runs keep every transfer in the rounds kernel
   po.accum = o.grad_accum != 0;
+  if (o.clip_norm < 0.f) return fail(PARO_ERR_INVALID, "clip_norm must be >= 0");
+  po.two_phase = o.clip_norm > 0.f || o.skip_nonfinite != 0;
+  if (po.two_phase) po.fuse_final = false;   // g_hat is materialised for the norm pass
   auto* p = new PlanT();
   p->ctx = ctx;
   p->opts = o;
@@ -656,6 +665,9 @@ paro_status_t paro_plan(paro_ctx_t ctx, const char* strategy, const int64_t* par
   PCK(cudaMemset(p->d_norm, 0, sizeof(double)));
   PCK(cudaMalloc(&p->d_nonfinite, sizeof(int)));
   PCK(cudaMemset(p->d_nonfinite, 0, sizeof(int)));
+  PCK(cudaMalloc(&p->d_sg, sizeof(float)));
+  PCK(cudaMalloc(&p->d_skip, sizeof(int)));
+  PCK(cudaMemset(p->d_skip, 0, sizeof(int)));
   p->pack_cap = std::max(1, n_params) * (int)p->local.size();
   PCK(cudaMalloc(&p->d_pack, 2 * sizeof(PackEntry) * p->pack_cap));   // [pack | unpack]
   PCK(cudaHostAlloc(&p->h_pack, 2 * sizeof(PackEntry) * p->pack_cap, cudaHostAllocDefault));
@@ -848,7 +860,8 @@ paro_status_t paro_step(paro_plan_t p, const void* const* grads, void* const* pa
   aa.eps = p->opts.eps;
   aa.has_wd = p->opts.weight_decay != 0.0f;
   aa.decay = (float)(1.0 - dlr * (double)p->opts.weight_decay);
-  aa.s_g = (float)(1.0 / ((double)p->opts.loss_scale * (double)(n_acc > 0 ? n_acc : 1)));
+  const double sg_base = 1.0 / ((double)p->opts.loss_scale * (double)(n_acc > 0 ? n_acc : 1));
+  aa.s_g = (float)sg_base;
   aa.nonfinite = p->d_nonfinite;
 
   CK(cudaEventRecord(p->ev_fork, S));
@@ -866,8 +879,14 @@ paro_status_t paro_step(paro_plan_t p, const void* const* grads, void* const* pa
   const int nb = (int)pl.buckets.size();
   const int grid = adam_grid();
   int n_adam = 0;
-  auto adam_bucket = [&](int b0, int b1) -> paro_status_t {
-    // one Adam launch over buckets [b0, b1) and every local rank
+  // two-phase step (clipping / non-finite skip, R28): phase 1 reduces every
+  // bucket and takes the norm, the clip scale is formed on the device, phase 2
+  // updates (Adam reads the scale and the skip flag from device memory)
+  const bool two = pl.opt.two_phase;
+  aa.s_g_dev = two ? p->d_sg : nullptr;
+  aa.skip = two ? p->d_skip : nullptr;
+  auto adam_bucket = [&](int b0, int b1, bool norm_only = false) -> paro_status_t {
+    // one Adam (or phase-1 norm) launch over buckets [b0, b1) and every local rank
     aa.nseg = 0;
     for (int li = 0; li < nl; ++li) {
       const int r = p->local[li];
@@ -890,9 +909,15 @@ paro_status_t paro_step(paro_plan_t p, const void* const* grads, void* const* pa
       sg.v = opt_state[li].v + S0.os_off[r];
       sg.param = reinterpret_cast<uint16_t*>(data_ptr(p, S0.param[r].rank, S0.param[r].kind, S0.param[r].off));
       sg.n8 = len / 8;
-      sg.in_norm = uniq ? 1 : 0;
+      sg.in_norm = (uniq && (norm_only || !two)) ? 1 : 0;
     }
     aa.partials = p->d_partials + (int64_t)n_adam * grid;
+    if (norm_only) {
+      CK(launch_grad_norm(aa, grid, ctx->comp));
+      ++n_adam;
+      ++launches;
+      return PARO_OK;
+    }
     int64_t elems = 0;
     for (int i = 0; i < aa.nseg; ++i) elems += 8 * aa.seg[i].n8;
     const int pk = prof_begin(p, ctx->comp, 0, elems);
@@ -909,9 +934,36 @@ paro_status_t paro_step(paro_plan_t p, const void* const* grads, void* const* pa
     return PARO_OK;
   };
 
+  // grad norm: ordered fp64 finalize, then scalar all-reduces (R8, R23)
+  auto norm_reduce = [&]() -> paro_status_t {
+    CK(launch_norm_finalize(p->d_partials, n_adam * grid, p->d_norm, ctx->comp));
+    ++launches;
+    CK(cudaEventRecord(p->ev_comp, ctx->comp));
+    CK(cudaStreamWaitEvent(ctx->comm, p->ev_comp, 0));
+    if (ctx->mode == MODE_REAL && pl.N > 1) {
+      NK(ncclAllReduce(p->d_norm, p->d_norm, 1, ncclDouble, ncclSum, ctx->world, ctx->comm));
+      NK(ncclAllReduce(p->d_nonfinite, p->d_nonfinite, 1, ncclInt32, ncclMax, ctx->world, ctx->comm));
+      launches += 2;
+    }
+    return PARO_OK;
+  };
+
   if (pl.N == 1) {
+    if (two) {
+      paro_status_t s1 = adam_bucket(0, nb, true);
+      if (s1 == PARO_OK) s1 = norm_reduce();
+      if (s1 != PARO_OK) return s1;
+      CK(launch_clip_scale(p->d_norm, p->d_nonfinite, (double)p->opts.clip_norm, sg_base,
+                           p->opts.skip_nonfinite, p->d_sg, p->d_skip, ctx->comp));
+      ++launches;
+      n_adam = 0;   // phase 2 reuses the partial slots (its norm flags are off)
+    }
     paro_status_t s2 = adam_bucket(0, nb);   // contiguous: one launch over all buckets
     if (s2 != PARO_OK) return s2;
+    if (!two) {
+      paro_status_t s3 = norm_reduce();
+      if (s3 != PARO_OK) return s3;
+    }
   } else {
     const int D = std::max(1, p->opts.pipeline_depth);
     const bool nccl = pl.opt.topology == PARO_TOPO_NCCL;
@@ -927,11 +979,7 @@ paro_status_t paro_step(paro_plan_t p, const void* const* grads, void* const* pa
       }
       return run_launch(p, p->gat[b], &launches);
     };
-    for (int b = 0; b < nb; ++b) {
-      // staging sets / g_hat slots are reused kStageSets / nslots buckets later:
-      // the Adam that reads them (fused final hop) must be done first
-      if (pl.nslots > 0 && b >= pl.nslots) CK(cudaStreamWaitEvent(ctx->comm, p->ev_adam[b - pl.nslots], 0));
-      if (b >= kStageSets) CK(cudaStreamWaitEvent(ctx->comm, p->ev_adam[b - kStageSets], 0));
+    auto do_reduce = [&](int b) -> paro_status_t {
       if (nccl) {
         const int k = prof_begin(p, ctx->comm, 1, 0);
         paro_status_t s3 = run_nccl(p, pl.sched[b].nccl_reduce[ctx->rank]);
@@ -944,6 +992,33 @@ paro_status_t paro_step(paro_plan_t p, const void* const* grads, void* const* pa
       }
       CK(cudaEventRecord(p->ev_red[b], ctx->comm));
       CK(cudaStreamWaitEvent(ctx->comp, p->ev_red[b], 0));
+      return PARO_OK;
+    };
+    if (two) {
+      // phase 1: every reduction (g_hat stays resident: one slot per bucket), norm per bucket
+      for (int b = 0; b < nb; ++b) {
+        paro_status_t s3 = do_reduce(b);
+        if (s3 == PARO_OK) s3 = adam_bucket(b, b + 1, true);
+        if (s3 != PARO_OK) return s3;
+      }
+      paro_status_t s4 = norm_reduce();
+      if (s4 != PARO_OK) return s4;
+      CK(cudaEventRecord(p->ev_comm, ctx->comm));
+      CK(cudaStreamWaitEvent(ctx->comp, p->ev_comm, 0));
+      CK(launch_clip_scale(p->d_norm, p->d_nonfinite, (double)p->opts.clip_norm, sg_base,
+                           p->opts.skip_nonfinite, p->d_sg, p->d_skip, ctx->comp));
+      ++launches;
+      n_adam = 0;   // phase 2 reuses the partial slots (its norm flags are off)
+    }
+    for (int b = 0; b < nb; ++b) {
+      if (!two) {
+        // staging sets / g_hat slots are reused kStageSets / nslots buckets later:
+        // the Adam that reads them (fused final hop) must be done first
+        if (pl.nslots > 0 && b >= pl.nslots) CK(cudaStreamWaitEvent(ctx->comm, p->ev_adam[b - pl.nslots], 0));
+        if (b >= kStageSets) CK(cudaStreamWaitEvent(ctx->comm, p->ev_adam[b - kStageSets], 0));
+        paro_status_t s3 = do_reduce(b);
+        if (s3 != PARO_OK) return s3;
+      }
       paro_status_t s4 = adam_bucket(b, b + 1);
       if (s4 != PARO_OK) return s4;
       CK(cudaEventRecord(p->ev_adam[b], ctx->comp));
@@ -956,21 +1031,17 @@ paro_status_t paro_step(paro_plan_t p, const void* const* grads, void* const* pa
       paro_status_t s5 = do_gather(b);
       if (s5 != PARO_OK) return s5;
     }
+    if (!two) {
+      paro_status_t s6 = norm_reduce();
+      if (s6 != PARO_OK) return s6;
+    }
   }
-  // ---- grad norm: ordered fp64 finalize, then scalar all-reduce (R8, R23)
-  CK(launch_norm_finalize(p->d_partials, n_adam * grid, p->d_norm, ctx->comp));
-  ++launches;
   CK(cudaEventRecord(p->ev_comp, ctx->comp));
   CK(cudaStreamWaitEvent(ctx->comm, p->ev_comp, 0));
   // ---- step-end barrier with every peer
   {
     paro_status_t s6 = all_peer_barrier(p, &launches);
     if (s6 != PARO_OK) return s6;
-  }
-  if (ctx->mode == MODE_REAL && pl.N > 1) {
-    NK(ncclAllReduce(p->d_norm, p->d_norm, 1, ncclDouble, ncclSum, ctx->world, ctx->comm));
-    NK(ncclAllReduce(p->d_nonfinite, p->d_nonfinite, 1, ncclInt32, ncclMax, ctx->world, ctx->comm));
-    launches += 2;
   }
   // ---- unpack into caller parameter tensors
   if (params) {

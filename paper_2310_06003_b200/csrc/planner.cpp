@@ -312,7 +312,8 @@ void Planner::layout() {
   g_numel = (G == LV_N) ? 0 : psi_pad / divl(G);
   os_numel = psi_pad / divl(OS);
   if ((G != OS || G == LV_N) && N > 1) {   // reduced gradient needs its own slots
-    nslots = opt.pipeline_depth + 1;
+    // two-phase step: all of g_hat is reduced before the first update
+    nslots = opt.two_phase ? (int)buckets.size() : opt.pipeline_depth + 1;
     ghat_slot = B / divl(OS);
   }
   const int64_t C = B / N;

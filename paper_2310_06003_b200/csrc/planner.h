@@ -101,6 +101,7 @@ struct PlanOptions {
   bool push = true;          // push (remote stores) or pull (remote loads) transport
   bool fuse_final = true;    // OS = G: fold the owner's last reduction hop into Adam
   bool accum = false;        // build the gradient-accumulation launches (s > 1)
+  bool two_phase = false;    // clipping / skip: every bucket's g_hat stays resident until Adam (R28)
 };
 
 class Planner {

@@ -45,7 +45,8 @@ class paro_opts_t(C.Structure):
                 ("beta2", C.c_float), ("eps", C.c_float), ("weight_decay", C.c_float),
                 ("loss_scale", C.c_float), ("comm_ctas", C.c_int), ("pipeline_depth", C.c_int),
                 ("pull_transport", C.c_int), ("adam_impl", C.c_int), ("comm_impl", C.c_int),
-                ("inter_gbps", C.c_float), ("grad_accum", C.c_int), ("stream", C.c_void_p)]
+                ("inter_gbps", C.c_float), ("clip_norm", C.c_float), ("skip_nonfinite", C.c_int),
+                ("grad_accum", C.c_int), ("stream", C.c_void_p)]
 
 
 class paro_plan_info_t(C.Structure):
@@ -131,7 +132,7 @@ def check(status):
 # ---------------------------------------------------------------- helpers
 def make_opts(bucket_elems=1 << 26, topology="ho", beta1=0.9, beta2=0.95, eps=1e-8, weight_decay=0.0,
               loss_scale=1.0, comm_ctas=148, pipeline_depth=2, stream=None, transport="pull", adam_impl="auto",
-              comm_impl="tma", inter_gbps=0.0, grad_accum=False):
+              comm_impl="tma", inter_gbps=0.0, grad_accum=False, clip_norm=0.0, skip_nonfinite=False):
     o = paro_opts_t()
     paro_opts_default(C.byref(o))
     o.bucket_elems = int(bucket_elems)
@@ -144,6 +145,8 @@ def make_opts(bucket_elems=1 << 26, topology="ho", beta1=0.9, beta2=0.95, eps=1e
     o.comm_impl = {"tma": 0, "lsu": 1}[comm_impl]
     o.inter_gbps = float(inter_gbps)
     o.grad_accum = 1 if grad_accum else 0
+    o.clip_norm = float(clip_norm)
+    o.skip_nonfinite = 1 if skip_nonfinite else 0
     o.stream = stream
     return o
 

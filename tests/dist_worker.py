@@ -38,6 +38,7 @@ def main():
     B = cfg.get("bucket", world * 64 * 12)
     steps = cfg.get("steps", 2)
     accum = cfg.get("accum", 0)          # > 0: that many micro-batches per step (paro_accumulate)
+    clip = cfg.get("clip_norm", 0.0)     # > 0: two-phase step with global-norm clipping
     for M in splits:
         uid = paro.unique_id() if rank == 0 else bytes(128)
         t = torch.tensor(list(uid), dtype=torch.uint8)
@@ -46,7 +47,7 @@ def main():
         for code, topo, tr in [(c, t_, x) for c in codes for t_ in topos for x in transports]:
             if True:
                 pl = paro.Plan(ctx, code, sizes, bucket_elems=B, topology=topo, transport=tr, comm_impl=comm_impl,
-                               inter_gbps=inter_gbps, grad_accum=accum > 0)
+                               inter_gbps=inter_gbps, grad_accum=accum > 0, clip_norm=clip)
                 info = pl.info()
                 st = [torch.empty(info["os_numel"], dtype=torch.float32, device="cuda") for _ in range(3)]
                 ptrs = [[x.data_ptr() for x in st]]

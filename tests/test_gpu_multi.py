@@ -24,11 +24,16 @@ def _ngpu():
     return torch.cuda.device_count() if torch.cuda.is_available() else 0
 
 
-def _dp(lay, steps, accum=0, g_level="N"):
+def _dp(lay, steps, accum=0, g_level="N", clip=0.0):
     w = ST.pad_flat(master_f32(0, lay.psi), lay.psi_pad, np.float32)
     m, v = np.zeros_like(w), np.zeros_like(w)
     for t in range(1, steps + 1):
-        if accum:
+        if clip:
+            w, m, v, p, gh, nsq = ST.dp_clip_step(lay, [grad_bits(r, t, 0, lay.psi) for r in range(lay.N)],
+                                                  w, m, v, 3e-4, t, clip_norm=clip)[:6]
+            assert ST.clip_coef(nsq, clip) < 1.0
+            sg = np.float32(1.0)
+        elif accum:
             mb = [[grad_bits(r, (t << 8) | (k + 1), 0, lay.psi) for r in range(lay.N)] for k in range(accum)]
             w, m, v, p, gh = ST.dp_accum_step(lay, mb, w, m, v, nm.AdamScalars(3e-4, t, accum_steps=accum),
                                               g_level)
@@ -44,7 +49,7 @@ CODES = ["NNN", "NNI", "NNG", "NII", "NIG", "NGG", "INI", "ING", "III", "IIG", "
 
 
 @pytest.mark.skipif(_ngpu() < 2, reason="needs >= 2 GPUs")
-@pytest.mark.parametrize("variant", ["default", "paced_lsu", "accum"])
+@pytest.mark.parametrize("variant", ["default", "paced_lsu", "accum", "clip"])
 def test_real_ranks_match_oracle(tmp_path, variant):
     world = min(_ngpu(), 4)
     splits = [m for m in range(1, world + 1) if world % m == 0]
@@ -55,6 +60,8 @@ def test_real_ranks_match_oracle(tmp_path, variant):
                     "inter_gbps": 50.0, "comm_impl": "lsu"})
     if variant == "accum":       # gradient accumulation, s = 3 micro-batches per step (NEXT-1)
         cfg.update({"accum": 3, "topos": ["ho", "two_step"], "transports": ["pull", "push"]})
+    if variant == "clip":        # two-phase step with an active global-norm clip (NEXT-3)
+        cfg.update({"clip_norm": 0.05, "topos": ["ho", "nccl"], "transports": ["pull"]})
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr=127.0.0.1", "--master-port=29517", os.path.join(ROOT, "tests", "dist_worker.py"),
            str(tmp_path), json.dumps(cfg)]
@@ -62,12 +69,12 @@ def test_real_ranks_match_oracle(tmp_path, variant):
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     for M in splits:
         lay = L.Layout(cfg["sizes"], world, M, cfg["bucket"])
-        refs = {gl: _dp(lay, 2, cfg.get("accum", 0), gl) for gl in "NIG"}
+        refs = {gl: _dp(lay, 2, cfg.get("accum", 0), gl, cfg.get("clip_norm", 0.0)) for gl in "NIG"}
         for code in cfg["codes"]:
             w, m, v, p, norm = refs[code[1]]
             for topo in cfg["topos"]:
-              if topo == "flat":   # different (deterministic) order: compare with the oracle's flat ring
-                  continue
+              if topo in ("flat", "nccl"):   # other reduction orders: flat = the oracle's flat ring,
+                  continue                   # nccl = NCCL's (perf comparator; it must only run)
               for tr in cfg["transports"]:
                 for rank in range(world):
                     tag = f"{M}_{code}_{topo}_{tr}_r{rank}"

@@ -32,7 +32,8 @@ class EmuRun:
     """All ranks of one split on cuda:0 through the C ABI."""
 
     def __init__(self, N, M, code, sizes, B, topo="ho", depth=2, wd=0.0, loss_scale=1.0, transport="push",
-                 adam_impl="auto", comm_impl="tma", grad_accum=False, mode="emulated"):
+                 adam_impl="auto", comm_impl="tma", grad_accum=False, mode="emulated", clip_norm=0.0,
+                 skip_nonfinite=False):
         paro = _paro()
         if mode == "emulated":
             self.ctx = paro.Context(N, M, mode="emulated", device=0)
@@ -40,7 +41,8 @@ class EmuRun:
             self.ctx = paro.Context(1, 1, mode="real", rank=0, device=0, uid=paro.unique_id())
         self.pl = paro.Plan(self.ctx, code, sizes, bucket_elems=B, topology=topo, pipeline_depth=depth,
                             weight_decay=wd, loss_scale=loss_scale, transport=transport, adam_impl=adam_impl,
-                            comm_impl=comm_impl, grad_accum=grad_accum)
+                            comm_impl=comm_impl, grad_accum=grad_accum, clip_norm=clip_norm,
+                            skip_nonfinite=skip_nonfinite)
         self.info = self.pl.info()
         self.N, self.code, self.sizes = N, code, sizes
         n = self.info["os_numel"]
@@ -395,3 +397,96 @@ def test_step_after_accumulate_rejects_grads():
     with pytest.raises(paro.ParoError, match="grad_accum"):
         plain.pl.accumulate()
     plain.close()
+
+
+# --------------------------------------------------------------------- clipping / skip (NEXT-3)
+def _clip_reference(lay, steps, clip, skip=False, kind="synth", accum=0):
+    w = ST.pad_flat(master_f32(0, lay.psi), lay.psi_pad, np.float32)
+    m, v = np.zeros_like(w), np.zeros_like(w)
+    out = []
+    for t in range(1, steps + 1):
+        if accum:
+            mb = [[grad_bits(r, _mb_id(t, k), 0, lay.psi) for r in range(lay.N)] for k in range(accum)]
+            gh = ST.dp_accum_step(lay, mb, w, m, v, nm.AdamScalars(LR, t, accum_steps=accum), accum_glevel)[4]
+            res = ST.clip_update(gh, w, m, v, LR, t, clip, skip, accum, {})
+        else:
+            res = ST.dp_clip_step(lay, _oracle_grads(lay.N, lay.psi, t, kind), w, m, v, LR, t, clip_norm=clip,
+                                  skip_nonfinite=skip)
+        w, m, v = res[0], res[1], res[2]
+        out.append(res)
+    last = out[-1]
+    return (w, m, v, last[3], [r[5] for r in out]), out
+
+
+accum_glevel = "G"
+
+
+@pytest.mark.parametrize("topo,transport", [("ho", "pull"), ("ho", "push"), ("two_step", "pull")])
+def test_clipping_every_strategy_2x4(topo, transport):
+    N, M = 8, 4
+    sizes = [N * 64 * 40 + 24, 1000]
+    B = N * 64 * 8
+    lay = L.Layout(sizes, N, M, B)
+    clip = 0.05                       # below the synthetic gradient norm: the coefficient is active
+    ref, per = _clip_reference(lay, 3, clip)
+    assert all(r[6] < 1.0 for r in per)
+    for code in S.paro_strategies():
+        run = EmuRun(N, M, code, sizes, B, topo=topo, transport=transport, clip_norm=clip)
+        for t in range(1, 4):
+            run.set_grads(t)
+            st = run.step(t)
+            assert abs(st["grad_norm"] ** 2 - per[t - 1][5]) <= 1e-12 * per[t - 1][5]
+        _check_against_dp(run, lay, ref)
+        run.close()
+
+
+def test_clipping_single_gpu_real_mode_and_accumulation():
+    sizes = [1 << 16, 3 * 4096 + 8]
+    B = 1 << 14
+    lay = L.Layout(sizes, 1, 1, B)
+    ref, per = _clip_reference(lay, 3, 0.02)
+    assert per[0][6] < 1.0
+    run = EmuRun(1, 1, "NNN", sizes, B, clip_norm=0.02, mode="real")
+    for t in range(1, 4):
+        run.set_grads(t)
+        run.step(t)
+    _check_against_dp(run, lay, ref)
+    run.close()
+    # accumulation + clipping, 2x4 emulated, G = G strategy
+    N, M = 8, 4
+    sizes = [N * 64 * 24]
+    lay = L.Layout(sizes, N, M, N * 64 * 8)
+    ref, per = _clip_reference(lay, 2, 0.01, accum=3)
+    assert per[0][6] < 1.0
+    for code in ("IGG", "GGG"):
+        run = EmuRun(N, M, code, sizes, N * 64 * 8, clip_norm=0.01, grad_accum=True, transport="pull")
+        _run_accum(run, 2, 3)
+        _check_against_dp(run, lay, ref)
+        run.close()
+
+
+def test_nonfinite_skip_leaves_state_unchanged():
+    N, M = 8, 2
+    sizes = [N * 64 * 30]
+    B = N * 64 * 8
+    lay = L.Layout(sizes, N, M, B)
+    for code in ("NNN", "IIG", "NIG", "GGG"):
+        run = EmuRun(N, M, code, sizes, B, skip_nonfinite=True, transport="pull")
+        run.set_grads(1)
+        run.step(1)
+        before = [run.state(r) for r in range(N)]
+        run.set_grads(2, kind="specials")
+        st = run.step(2)
+        assert st["nonfinite"] == 1
+        for r in range(N):
+            after = run.state(r)
+            for k in ("master", "m", "v", "param"):
+                assert np.array_equal(after[k], before[r][k]), (code, r, k)
+        run.set_grads(3)       # a finite step afterwards updates again: t = 3 over t = 1's state
+        run.step(3)
+        w = ST.pad_flat(master_f32(0, lay.psi), lay.psi_pad, np.float32)
+        z = np.zeros_like(w)
+        w1, m1, v1 = ST.dp_step(lay, _oracle_grads(N, lay.psi, 1), w, z, z, nm.AdamScalars(LR, 1))[:3]
+        ref = ST.dp_step(lay, _oracle_grads(N, lay.psi, 3), w1, m1, v1, nm.AdamScalars(LR, 3))
+        _check_against_dp(run, lay, ref)
+        run.close()
