@@ -104,6 +104,8 @@ typedef struct {
                           * selects the two-phase step: every bucket is reduced    *
                           * and the norm all-reduced before the first update, and  *
                           * the reduced gradient stays resident (psi/div(OS) bf16) */
+  int gather_windows;    /* > 0: that many library window slots of bucket_elems    *
+                          * bf16 each for paro_gather_window (P = I or G only).    */
   int grad_accum;        /* 1: enable paro_accumulate (gradient accumulation over  *
                           * s > 1 micro-batches); G = N plans then own  *
                           * a psi_pad bf16 accumulator.  0 (default): off.         */
@@ -196,6 +198,27 @@ paro_status_t paro_rank_send_bytes(paro_plan_t plan, int rank, int64_t* intra, i
 paro_status_t paro_rank_accum_send_bytes(paro_plan_t plan, int rank, int64_t* acc_intra, int64_t* acc_inter,
                                          int64_t* step_intra, int64_t* step_inter);
 
+/* Forward / backward parameter all-gather ("model parameters are
+ * ... intra-group sharded"; "each GPU obtains a complete replica of
+ * model parameters through the intra-group all-gather operation", P:341;
+ * Table 3 columns Forward / Backward A-G(P)).  Assembles bucket `bucket`'s
+ * full bf16 parameters (flat layout of paro_bucket_range) of local `rank`
+ * into window slot `slot` and returns its device address in *out: P = I
+ * gathers inside the group (ring AG_I), P = G over all ranks on the plan's
+ * topology (HO-Ring by default).  Bit copies: the window equals the bucket
+ * slice of the full model's bf16 parameters after the last step.
+ * Stream-ordered on `stream` (NULL = the plan stream), so a caller can
+ * prefetch bucket b+1 on a side stream while computing on bucket b; the
+ * window may be reused once the caller's reads of it are stream-ordered
+ * before the next gather into the same slot.  Collective over the ranks the
+ * level spans.  P = N (or N = 1): no transfer, *out points into the
+ * parameter buffer.  Emulated mode: rank 0, all ranks gather at once.
+ * Errors: PARO_ERR_STATE if the plan has no windows (gather_windows = 0). */
+paro_status_t paro_gather_window(paro_plan_t plan, int rank, int64_t bucket, int slot, void* stream, void** out);
+
+/* Bytes `rank` sends to gather every bucket once through paro_gather_window. */
+paro_status_t paro_rank_gather_send_bytes(paro_plan_t plan, int rank, int64_t* intra, int64_t* inter);
+
 /* Library-owned device buffers of `rank` (must be a local rank):
  *   kind 0: flat gradient buffer, bf16, psi_pad elements (zero-padded tail).
  *           Writing gradients here and passing grads = NULL to paro_step is
@@ -207,7 +230,9 @@ paro_status_t paro_rank_accum_send_bytes(paro_plan_t plan, int rank, int64_t* ac
  *           bucket b's g_hat at the OS residency) or NULL when g_hat lives in
  *           the G-residency buffer or is consumed directly by Adam.
  *   kind 4: the G = N gradient accumulator (bf16, psi_pad elements; grad_accum
- *           plans with G = N only, else NULL). */
+ *           plans with G = N only, else NULL).
+ *   kind 5: parameter-gather window slot 0 (gather_windows x bucket_elems bf16,
+ *           slot w at + 2 * w * bucket_elems bytes; NULL without windows). */
 paro_status_t paro_buffer(paro_plan_t plan, int rank, int kind, void** ptr);
 
 /* Initialise one local rank's optimizer state and parameter buffer from a full

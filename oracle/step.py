@@ -377,6 +377,43 @@ def _simulate(code, lay, grads_mb, state, sc, topology, accumulate):
     return res
 
 
+def param_gather(code, lay: Layout, params, topology="ho"):
+    """Forward / backward parameter all-gather of every bucket (P:195-196,
+    P:338; Table 3 A-G(P) columns), simulated round by round.
+
+    params[r]: rank r's bf16 parameter residency (bucket-major, as init_state /
+    strategy_step keep it).  P = I: intra-group ring AG (AG_I); P = G: the
+    world AG on `topology`; P = N: nothing moves.  Returns (full[r] = the
+    gathered flat bf16 parameters of rank r, sent[r] = [intra, inter] units).
+    """
+    pl, _, _ = validate(code)
+    N, M = lay.N, lay.M
+    geo = C.Geometry(N, M)
+    res = StepResult(N)
+    full = {r: [] for r in range(N)}
+    for b, (s, n) in enumerate(lay.buckets):
+        own = {}
+        for r in range(N):
+            off = _offset_in_shard(lay, pl, r, b)
+            a, e = lay.residency(pl, r, b)
+            own[r] = params[r][off:off + (e - a)]
+        if pl == "N":
+            got = own
+        elif pl == "I":
+            ch, rounds = C.ag_intra(geo, own)
+            t = C.Trace(M)
+            t.extend(rounds)
+            _add_trace(res, t)
+            got = {r: np.concatenate(ch[r]) for r in range(N)}
+        else:
+            segs, t = _ag(geo, own, topology)
+            _add_trace(res, t)
+            got = {r: np.concatenate([segs[r][k] for k in range(N)]) for r in range(N)}
+        for r in range(N):
+            full[r].append(got[r])
+    return {r: np.concatenate(full[r]) for r in range(N)}, res.sent
+
+
 def _ag(geo, Z, topology):
     if topology == "ho":
         return C.ag_ho_ring(geo, Z)

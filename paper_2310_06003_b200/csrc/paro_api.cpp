@@ -68,6 +68,7 @@ struct paro_plan {
   DTask* d_tasks = nullptr;
   std::vector<DevLaunch> red, gat;        // per bucket
   std::vector<DevLaunch> acc_first, acc_next, red_acc;   // gradient accumulation (per bucket)
+  std::vector<std::vector<DevLaunch>> win;  // [window slot][bucket]: forward/backward parameter gather
   int64_t acc_count = 0;                  // micro-batches accumulated since the last step
   bool last_step_acc = false;             // the last step consumed an accumulator
   double* d_partials = nullptr;
@@ -172,19 +173,22 @@ int data_rank(const PlanT* p, const void* ptr) {
 
 // acc_kind >= 0: a task writing that buffer kind also folds its old contents in
 // as the last input (gradient accumulation: acc = acc (+) r, R27)
-DTask resolve(const PlanT* p, const Task& t, int executing_rank, int acc_kind) {
+DTask resolve(const PlanT* p, const Task& t, int executing_rank, int acc_kind, int64_t win_shift = 0) {
   DTask d{};
+  auto ptr_of = [&](const Ref& x) {
+    return data_ptr(p, x.rank, x.kind, x.off + (x.kind == BUF_WIN ? win_shift : 0));
+  };
   d.nin = t.nin;
   d.n8 = t.n / 8;
   d.rawmask = 0;
   d.inter = 0;
   const int M = p->pl->M;
   for (int i = 0; i < t.nin; ++i) {
-    d.in[i] = reinterpret_cast<const uint16_t*>(data_ptr(p, t.in[i].rank, t.in[i].kind, t.in[i].off));
+    d.in[i] = reinterpret_cast<const uint16_t*>(ptr_of(t.in[i]));
     if (t.in[i].kind == BUF_GRAD) d.rawmask |= 1u << i;
     if (t.in[i].rank / M != executing_rank / M) d.inter += 1;
   }
-  d.dst = reinterpret_cast<uint16_t*>(data_ptr(p, t.dst.rank, t.dst.kind, t.dst.off));
+  d.dst = reinterpret_cast<uint16_t*>(ptr_of(t.dst));
   if (t.dst.rank / M != executing_rank / M) d.inter += 1;
   if (acc_kind >= 0 && t.dst.kind == acc_kind) {
     d.in[d.nin++] = d.dst;
@@ -199,7 +203,7 @@ paro_status_t upload_schedule(PlanT* p) {
   const Planner& pl = *p->pl;
   std::vector<DRound> rounds;
   std::vector<DTask> tasks;
-  auto build = [&](const Launch& L, int acc_kind) {
+  auto build = [&](const Launch& L, int acc_kind, int64_t win_shift = 0) {
     DevLaunch dl;
     dl.round_off = (int64_t)rounds.size();
     if (L.empty()) return dl;
@@ -210,14 +214,14 @@ paro_status_t upload_schedule(PlanT* p) {
       d.units = 0;
       if (ctx->mode == MODE_REAL) {
         for (const Task& t : L.rounds[r][ctx->rank]) {
-          tasks.push_back(resolve(p, t, ctx->rank, acc_kind));
+          tasks.push_back(resolve(p, t, ctx->rank, acc_kind, win_shift));
           d.units += t.n / 8;
         }
         d.peers_before = L.barrier_peers(r, ctx->rank);
       } else {
         for (int x = 0; x < pl.N; ++x)
           for (const Task& t : L.rounds[r][x]) {
-            tasks.push_back(resolve(p, t, x, acc_kind));
+            tasks.push_back(resolve(p, t, x, acc_kind, win_shift));
             d.units += t.n / 8;
           }
         d.peers_before = 0;
@@ -247,9 +251,11 @@ paro_status_t upload_schedule(PlanT* p) {
   p->acc_first.clear();
   p->acc_next.clear();
   p->red_acc.clear();
+  p->win.assign(pl.buf_len[BUF_WIN] > 0 ? pl.opt.windows : 0, {});
   for (const BucketSchedule& S : pl.sched) {
     p->red.push_back(build(S.reduce, -1));
     p->gat.push_back(build(S.gather, -1));
+    for (int w = 0; w < (int)p->win.size(); ++w) p->win[w].push_back(build(S.window, -1, int64_t(w) * pl.B));
     if (pl.opt.accum) {
       p->acc_first.push_back(build(S.accum, -1));
       p->acc_next.push_back(build(S.accum, pl.acc_kind));
@@ -474,6 +480,7 @@ void paro_opts_default(paro_opts_t* o) {
   o->grad_accum = 0;
   o->clip_norm = 0.f;
   o->skip_nonfinite = 0;
+  o->gather_windows = 0;
   o->stream = nullptr;
 }
 
@@ -591,6 +598,8 @@ paro_status_t paro_plan(paro_ctx_t ctx, const char* strategy, const int64_t* par
   if (o.clip_norm < 0.f) return fail(PARO_ERR_INVALID, "clip_norm must be >= 0");
   po.two_phase = o.clip_norm > 0.f || o.skip_nonfinite != 0;
   if (po.two_phase) po.fuse_final = false;   // g_hat is materialised for the norm pass
+  if (o.gather_windows < 0 || o.gather_windows > 64) return fail(PARO_ERR_INVALID, "gather_windows must be in [0, 64]");
+  po.windows = o.gather_windows;
   auto* p = new PlanT();
   p->ctx = ctx;
   p->opts = o;
@@ -757,6 +766,14 @@ paro_status_t paro_rank_accum_send_bytes(paro_plan_t p, int rank, int64_t* acc_i
   return PARO_OK;
 }
 
+paro_status_t paro_rank_gather_send_bytes(paro_plan_t p, int rank, int64_t* intra, int64_t* inter) {
+  if (!p || !intra || !inter) return fail(PARO_ERR_INVALID, "null argument");
+  if (rank < 0 || rank >= p->pl->N) return fail(PARO_ERR_INVALID, "rank out of range");
+  *intra = p->pl->win_send_intra[rank];
+  *inter = p->pl->win_send_inter[rank];
+  return PARO_OK;
+}
+
 paro_status_t paro_buffer(paro_plan_t p, int rank, int kind, void** ptr) {
   if (!p || !ptr) return fail(PARO_ERR_INVALID, "null argument");
   paro_ctx* ctx = p->ctx;
@@ -768,7 +785,8 @@ paro_status_t paro_buffer(paro_plan_t p, int rank, int kind, void** ptr) {
   else if (kind == 2) *ptr = (pl.G == LV_N) ? nullptr : data_ptr(p, rank, BUF_GSHARD, 0);
   else if (kind == 3) *ptr = pl.buf_len[BUF_GHAT] ? data_ptr(p, rank, BUF_GHAT, 0) : nullptr;
   else if (kind == 4) *ptr = pl.buf_len[BUF_GACC] ? data_ptr(p, rank, BUF_GACC, 0) : nullptr;
-  else return fail(PARO_ERR_INVALID, "kind must be 0, 1, 2, 3 or 4");
+  else if (kind == 5) *ptr = pl.buf_len[BUF_WIN] ? data_ptr(p, rank, BUF_WIN, 0) : nullptr;
+  else return fail(PARO_ERR_INVALID, "kind must be 0 .. 5");
   return PARO_OK;
 }
 
@@ -1126,6 +1144,38 @@ paro_status_t paro_accumulate(paro_plan_t p, const void* const* grads) {
   CK(cudaStreamWaitEvent(S, p->ev_comm, 0));
   p->last_stream = S;
   ++p->acc_count;
+  if (p->prof) p->prof_launches += launches;
+  return PARO_OK;
+}
+
+paro_status_t paro_gather_window(paro_plan_t p, int rank, int64_t bucket, int slot, void* stream, void** out) {
+  if (!p || !out) return fail(PARO_ERR_INVALID, "null argument");
+  paro_ctx* ctx = p->ctx;
+  paro_status_t s = check_ctx(ctx);
+  if (s != PARO_OK) return s;
+  if (ctx->mode == MODE_PLANNER) return fail(PARO_ERR_STATE, "planning-only context");
+  const Planner& pl = *p->pl;
+  if (!is_local(p, rank)) return fail(PARO_ERR_INVALID, "rank is not local to this process");
+  if (bucket < 0 || bucket >= (int64_t)pl.buckets.size()) return fail(PARO_ERR_INVALID, "bucket out of range");
+  if (pl.P == LV_N || pl.N == 1) {   // parameters are resident: the bucket is a view of the parameter buffer
+    *out = data_ptr(p, rank, BUF_PARAM, pl.buckets[bucket].first);
+    return PARO_OK;
+  }
+  if (p->win.empty()) return fail(PARO_ERR_STATE, "plan was created without gather_windows");
+  if (slot < 0 || slot >= (int)p->win.size()) return fail(PARO_ERR_INVALID, "window slot out of range");
+  if (ctx->mode == MODE_EMU && rank != p->local[0])
+    return fail(PARO_ERR_INVALID, "emulated mode gathers every rank at once: pass rank 0");
+  cudaStream_t S = stream ? static_cast<cudaStream_t>(stream)
+                          : (p->opts.stream ? static_cast<cudaStream_t>(p->opts.stream) : ctx->main);
+  int launches = 0;
+  CK(cudaEventRecord(p->ev_fork, S));
+  CK(cudaStreamWaitEvent(ctx->comm, p->ev_fork, 0));
+  paro_status_t s3 = run_launch(p, p->win[slot][bucket], &launches);
+  if (s3 != PARO_OK) return s3;
+  CK(cudaEventRecord(p->ev_comm, ctx->comm));
+  CK(cudaStreamWaitEvent(S, p->ev_comm, 0));
+  *out = data_ptr(p, rank, BUF_WIN, int64_t(slot) * pl.B);
+  p->last_stream = S;
   if (p->prof) p->prof_launches += launches;
   return PARO_OK;
 }

@@ -332,6 +332,7 @@ void Planner::layout() {
   buf_len[BUF_SOWN] = (N > 1) ? kStageSets * sown_len : 0;
   buf_len[BUF_LAND] = (N > 1 && opt.topology == 3 && opt.push) ? kStageSets * land_len : 0;
   buf_len[BUF_GACC] = (opt.accum && G == LV_N) ? psi_pad : 0;
+  buf_len[BUF_WIN] = (opt.windows > 0 && P != LV_N && N > 1) ? int64_t(opt.windows) * B : 0;
   acc_kind = !opt.accum ? -1 : (G == LV_N ? BUF_GACC : BUF_GSHARD);
   int64_t off = 0;
   for (int k = 0; k < BUF_NKINDS; ++k) {
@@ -362,7 +363,7 @@ void Planner::build_schedule() {
     const int64_t s = buckets[b].first, n = buckets[b].second;
     const int64_t C = n / N, chunk = n / M;
     const int par = int(b % kStageSets);
-    S.reduce.n_ranks = S.gather.n_ranks = S.accum.n_ranks = S.reduce_acc.n_ranks = N;
+    S.reduce.n_ranks = S.gather.n_ranks = S.accum.n_ranks = S.reduce_acc.n_ranks = S.window.n_ranks = N;
     S.nccl_reduce.assign(N, {});
     S.nccl_gather.assign(N, {});
 
@@ -765,11 +766,25 @@ void Planner::build_schedule() {
       }
       // ---- parameter restore
       Launch& Lg = S.gather;
+      // ---- forward/backward parameter all-gather into a window (P = I / G):
+      // round 0 copies the own P shard into its place, then the ring AG in place
+      // (P = I: AG_I, "intra-group all-gather"; P = G: the world AG)
+      if (opt.windows > 0 && P != LV_N) {
+        auto win = [&](int r) { return Ref{r, BUF_WIN, 0}; };
+        for (int r = 0; r < N; ++r) {
+          int64_t b0, e0;
+          residency(P, r, (int64_t)b, &b0, &e0);
+          S.window.add(0, r, make_task(e0 - b0, {param_base(r)}, at(win(r), b0 - s)));
+        }
+        if (P == LV_I) emit_ag_i(S.window, win, 1);
+        else emit_world_ag(S.window, win, 1);
+        S.window.final_barrier = true;   // peers are done reading the slot before it is reused
+      }
       if (OS == LV_G && P == LV_I) emit_ag_e(Lg, param_base, 0);
       if (OS == LV_G && P == LV_N) emit_world_ag(Lg, param_base, 0);
       if (OS == LV_I && P == LV_N) emit_ag_i(Lg, param_base, 0);
       // drop rounds that ended up empty for every rank (degenerate splits)
-      for (Launch* Lp : {&S.reduce, &S.gather, &S.accum, &S.reduce_acc}) {
+      for (Launch* Lp : {&S.reduce, &S.gather, &S.accum, &S.reduce_acc, &S.window}) {
         const bool is_red = (Lp == &S.reduce || Lp == &S.reduce_acc);
         std::vector<std::vector<Ref>>& gin = (Lp == &S.reduce_acc) ? S.ghat_in_acc : S.ghat_in;
         std::vector<std::vector<std::vector<Task>>> kept;
@@ -890,7 +905,7 @@ void Planner::validate_refs() const {
   };
   for (size_t b = 0; b < sched.size(); ++b) {
     const BucketSchedule& S = sched[b];
-    for (const Launch* L : {&S.reduce, &S.gather, &S.accum, &S.reduce_acc})
+    for (const Launch* L : {&S.reduce, &S.gather, &S.accum, &S.reduce_acc, &S.window})
       for (const auto& rnd : L->rounds)
         for (const auto& v : rnd)
           for (const Task& t : v) {
@@ -940,6 +955,8 @@ void Planner::count_bytes() {
   acc_send_inter.assign(N, 0);
   accstep_send_intra.assign(N, 0);
   accstep_send_inter.assign(N, 0);
+  win_send_intra.assign(N, 0);
+  win_send_inter.assign(N, 0);
   n_rounds = 0;
   n_comm_launches = 0;
   for (const BucketSchedule& S : sched) {
@@ -949,6 +966,7 @@ void Planner::count_bytes() {
       n_rounds += (int)L->rounds.size();
     }
     count({&S.reduce, &S.gather}, &S.ghat_in, S.os_len, send_intra, send_inter);
+    count({&S.window}, nullptr, 0, win_send_intra, win_send_inter);
     if (opt.accum) {
       count({&S.accum}, nullptr, 0, acc_send_intra, acc_send_inter);
       count({&S.reduce_acc, &S.gather}, &S.ghat_in_acc, S.os_len, accstep_send_intra, accstep_send_inter);

@@ -29,6 +29,7 @@ enum BufKind : int {
   BUF_SOWN,        // own-group partial (HO phase 2): 2 parities
   BUF_LAND,        // direct push landing slots: 2 parities x ((M-1) chunks + (g-1) segments)
   BUF_GACC,        // G = N gradient accumulator (psi_pad; only for grad_accum plans)
+  BUF_WIN,         // forward/backward parameter gather windows: n_windows x B (P = I or G)
   BUF_NKINDS
 };
 
@@ -92,6 +93,9 @@ struct BucketSchedule {
   // `reduce_acc` finishes the reduction from the accumulator after the last one
   Launch accum, reduce_acc;
   std::vector<std::vector<Ref>> ghat_in_acc;
+  // forward/backward parameter all-gather of the whole bucket into window slot
+  // 0; the engine shifts BUF_WIN refs to the slot used
+  Launch window;
 };
 
 struct PlanOptions {
@@ -102,6 +106,7 @@ struct PlanOptions {
   bool fuse_final = true;    // OS = G: fold the owner's last reduction hop into Adam
   bool accum = false;        // build the gradient-accumulation launches (s > 1)
   bool two_phase = false;    // clipping / skip: every bucket's g_hat stays resident until Adam (R28)
+  int windows = 0;           // parameter-gather window slots (0: none)
 };
 
 class Planner {
@@ -130,6 +135,7 @@ class Planner {
   std::vector<int64_t> send_intra, send_inter;        // bytes per rank per step
   std::vector<int64_t> acc_send_intra, acc_send_inter;        // per accumulated micro-batch
   std::vector<int64_t> accstep_send_intra, accstep_send_inter;  // per step after accumulation
+  std::vector<int64_t> win_send_intra, win_send_inter;          // per gather of every bucket once
   int acc_kind = -1;                                  // accumulator buffer (GSHARD / GACC)
   int n_rounds = 0, n_comm_launches = 0;
 

@@ -46,7 +46,7 @@ class paro_opts_t(C.Structure):
                 ("loss_scale", C.c_float), ("comm_ctas", C.c_int), ("pipeline_depth", C.c_int),
                 ("pull_transport", C.c_int), ("adam_impl", C.c_int), ("comm_impl", C.c_int),
                 ("inter_gbps", C.c_float), ("clip_norm", C.c_float), ("skip_nonfinite", C.c_int),
-                ("grad_accum", C.c_int), ("stream", C.c_void_p)]
+                ("gather_windows", C.c_int), ("grad_accum", C.c_int), ("stream", C.c_void_p)]
 
 
 class paro_plan_info_t(C.Structure):
@@ -98,6 +98,9 @@ paro_bucket_range = _sig("paro_bucket_range", _st, _vp, _i64, C.POINTER(_i64), C
 paro_rank_send_bytes = _sig("paro_rank_send_bytes", _st, _vp, C.c_int, C.POINTER(_i64), C.POINTER(_i64))
 paro_rank_accum_send_bytes = _sig("paro_rank_accum_send_bytes", _st, _vp, C.c_int, C.POINTER(_i64),
                                   C.POINTER(_i64), C.POINTER(_i64), C.POINTER(_i64))
+paro_gather_window = _sig("paro_gather_window", _st, _vp, C.c_int, _i64, C.c_int, _vp, C.POINTER(_vp))
+paro_rank_gather_send_bytes = _sig("paro_rank_gather_send_bytes", _st, _vp, C.c_int, C.POINTER(_i64),
+                                   C.POINTER(_i64))
 paro_buffer = _sig("paro_buffer", _st, _vp, C.c_int, C.c_int, C.POINTER(_vp))
 paro_opt_state_init = _sig("paro_opt_state_init", _st, _vp, C.c_int, _vp, C.POINTER(paro_opt_state_t))
 paro_opt_state_init_synth = _sig("paro_opt_state_init_synth", _st, _vp, C.c_int, C.c_uint64,
@@ -120,7 +123,7 @@ EXPORTED = ["paro_opts_default", "paro_get_unique_id", "paro_init", "paro_init_e
             "paro_opt_state_init_synth", "paro_synth_grads", "paro_step", "paro_step_stats",
             "paro_plan_destroy", "paro_last_error", "paro_version", "paro_profile_start",
             "paro_profile_stop", "paro_collective", "paro_accumulate",
-            "paro_rank_accum_send_bytes"]
+            "paro_rank_accum_send_bytes", "paro_gather_window", "paro_rank_gather_send_bytes"]
 
 
 def check(status):
@@ -132,7 +135,7 @@ def check(status):
 # ---------------------------------------------------------------- helpers
 def make_opts(bucket_elems=1 << 26, topology="ho", beta1=0.9, beta2=0.95, eps=1e-8, weight_decay=0.0,
               loss_scale=1.0, comm_ctas=148, pipeline_depth=2, stream=None, transport="pull", adam_impl="auto",
-              comm_impl="tma", inter_gbps=0.0, grad_accum=False, clip_norm=0.0, skip_nonfinite=False):
+              comm_impl="tma", inter_gbps=0.0, grad_accum=False, clip_norm=0.0, skip_nonfinite=False, gather_windows=0):
     o = paro_opts_t()
     paro_opts_default(C.byref(o))
     o.bucket_elems = int(bucket_elems)
@@ -147,6 +150,7 @@ def make_opts(bucket_elems=1 << 26, topology="ho", beta1=0.9, beta2=0.95, eps=1e
     o.grad_accum = 1 if grad_accum else 0
     o.clip_norm = float(clip_norm)
     o.skip_nonfinite = 1 if skip_nonfinite else 0
+    o.gather_windows = int(gather_windows)
     o.stream = stream
     return o
 
@@ -219,6 +223,17 @@ class Plan:
         v = [_i64() for _ in range(4)]
         check(paro_rank_accum_send_bytes(self.h, rank, *[C.byref(x) for x in v]))
         return (v[0].value, v[1].value), (v[2].value, v[3].value)
+
+    def gather_window(self, rank, bucket, slot=0, stream=None):
+        """paro_gather_window: device address of bucket `bucket`'s full bf16 parameters."""
+        out = _vp()
+        check(paro_gather_window(self.h, rank, int(bucket), int(slot), stream, C.byref(out)))
+        return out.value
+
+    def gather_send_bytes(self, rank):
+        a, b = _i64(), _i64()
+        check(paro_rank_gather_send_bytes(self.h, rank, C.byref(a), C.byref(b)))
+        return a.value, b.value
 
     def buffer(self, rank, kind):
         p = _vp()

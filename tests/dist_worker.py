@@ -39,6 +39,7 @@ def main():
     steps = cfg.get("steps", 2)
     accum = cfg.get("accum", 0)          # > 0: that many micro-batches per step (paro_accumulate)
     clip = cfg.get("clip_norm", 0.0)     # > 0: two-phase step with global-norm clipping
+    windows = cfg.get("windows", 0)      # > 0: also gather every bucket through paro_gather_window
     for M in splits:
         uid = paro.unique_id() if rank == 0 else bytes(128)
         t = torch.tensor(list(uid), dtype=torch.uint8)
@@ -47,7 +48,8 @@ def main():
         for code, topo, tr in [(c, t_, x) for c in codes for t_ in topos for x in transports]:
             if True:
                 pl = paro.Plan(ctx, code, sizes, bucket_elems=B, topology=topo, transport=tr, comm_impl=comm_impl,
-                               inter_gbps=inter_gbps, grad_accum=accum > 0, clip_norm=clip)
+                               inter_gbps=inter_gbps, grad_accum=accum > 0, clip_norm=clip,
+                               gather_windows=windows)
                 info = pl.info()
                 st = [torch.empty(info["os_numel"], dtype=torch.float32, device="cuda") for _ in range(3)]
                 ptrs = [[x.data_ptr() for x in st]]
@@ -66,8 +68,19 @@ def main():
                 pbuf = torch.empty(info["p_numel"], dtype=torch.int16, device="cuda")
                 _copy(pbuf, pl.buffer(rank, 1))
                 tag = f"{M}_{code}_{topo}_{tr}_r{rank}"
+                extra = {}
+                if windows:
+                    parts = []
+                    for b in range(info["n_buckets"]):
+                        b0, b1 = pl.bucket_range(b)
+                        ptr = pl.gather_window(rank, b, slot=b % windows)
+                        torch.cuda.synchronize()
+                        wb = torch.empty(b1 - b0, dtype=torch.int16, device="cuda")
+                        _copy(wb, ptr)
+                        parts.append(wb.cpu().numpy().view(np.uint16))
+                    extra["full"] = np.concatenate(parts)
                 np.savez(os.path.join(out, tag + ".npz"), master=st[0].cpu().numpy(), m=st[1].cpu().numpy(),
-                         v=st[2].cpu().numpy(), param=pbuf.cpu().numpy().view(np.uint16))
+                         v=st[2].cpu().numpy(), param=pbuf.cpu().numpy().view(np.uint16), **extra)
                 with open(os.path.join(out, tag + ".json"), "w") as f:
                     json.dump({"stats": stats, "send": pl.send_bytes(rank)}, f)
                 pl.close()

@@ -177,3 +177,23 @@ def test_accumulate_needs_grad_accum_plan():
         paro.Plan(ctx, "IIG", [4096], topology="nccl", grad_accum=True)
     pl.close()
     ctx.close()
+
+
+@pytest.mark.parametrize("N,M", [(8, 4), (8, 2), (4, 2), (9, 3), (8, 1), (8, 8)])
+def test_gather_window_bytes_match_oracle(N, M):
+    """Forward/backward parameter gathers (NEXT-2): bytes per full pass over
+    the buckets == the oracle's simulated AG rounds, every strategy / topology."""
+    sizes = [3000, 517, 64, 9000, 7]
+    B = N * 64 * 4
+    lay = L.Layout(sizes, N, M, B)
+    full = nm.bf16_bits_from_f32(ST.pad_flat(master_f32(0, lay.psi), lay.psi_pad, np.float32))
+    ctx = paro.Context(N, M)
+    for code in S.paro_strategies():
+        params = {r: ST.shard_of(full, lay, code[0], r) for r in range(N)}
+        for topo, tr in [("ho", "pull"), ("ho", "push"), ("two_step", "pull"), ("flat", "push"), ("h_ring", "pull")]:
+            pl = paro.Plan(ctx, code, sizes, bucket_elems=B, topology=topo, transport=tr, gather_windows=2)
+            _, sent = ST.param_gather(code, lay, params, topology=topo)
+            for r in range(N):
+                assert pl.gather_send_bytes(r) == (2 * sent[r][0], 2 * sent[r][1]), (code, topo, tr, r)
+            pl.close()
+    ctx.close()

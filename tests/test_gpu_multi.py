@@ -59,7 +59,7 @@ def test_real_ranks_match_oracle(tmp_path, variant):
         cfg.update({"codes": ["NNN", "IIG", "GGG", "NIG"], "topos": ["ho", "flat"], "transports": ["pull"],
                     "inter_gbps": 50.0, "comm_impl": "lsu"})
     if variant == "accum":       # gradient accumulation, s = 3 micro-batches per step (NEXT-1)
-        cfg.update({"accum": 3, "topos": ["ho", "two_step"], "transports": ["pull", "push"]})
+        cfg.update({"accum": 3, "topos": ["ho", "two_step"], "transports": ["pull", "push"], "windows": 2})
     if variant == "clip":        # two-phase step with an active global-norm clip (NEXT-3)
         cfg.update({"clip_norm": 0.05, "topos": ["ho", "nccl"], "transports": ["pull"]})
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
@@ -85,3 +85,5 @@ def test_real_ranks_match_oracle(tmp_path, variant):
                     assert np.array_equal(d["v"], ST.shard_of(v, lay, code[2], rank)), tag
                     assert np.array_equal(d["param"], ST.shard_of(p, lay, code[0], rank)), tag
                     assert abs(meta["stats"]["grad_norm"] ** 2 - norm) <= 1e-12 * norm, tag
+                    if "full" in d:      # forward/backward parameter gather: the full bf16 model
+                        assert np.array_equal(d["full"], p), tag

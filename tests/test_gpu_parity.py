@@ -490,3 +490,39 @@ def test_nonfinite_skip_leaves_state_unchanged():
         ref = ST.dp_step(lay, _oracle_grads(N, lay.psi, 3), w1, m1, v1, nm.AdamScalars(LR, 3))
         _check_against_dp(run, lay, ref)
         run.close()
+
+
+# --------------------------------------------------------------------- forward/backward parameter gather (NEXT-2)
+@pytest.mark.parametrize("topo,transport", [("ho", "pull"), ("ho", "push"), ("two_step", "pull"),
+                                            ("flat", "pull"), ("h_ring", "push")])
+def test_gather_windows_return_full_parameters(topo, transport):
+    """After a step, gathering every bucket into alternating windows gives each
+    rank the bucket slice of the full model's bf16 parameters, bit for bit."""
+    N, M = 8, 4
+    sizes = [N * 64 * 40 + 24, 1000]
+    B = N * 64 * 8
+    lay = L.Layout(sizes, N, M, B)
+    p_full = _dp_reference(lay, 1)[3]
+    for code in S.paro_strategies():
+        run = EmuRun(N, M, code, sizes, B, topo=topo, transport=transport)
+        run.pl.close()
+        paro = _paro()
+        run.pl = paro.Plan(run.ctx, code, sizes, bucket_elems=B, topology=topo, transport=transport,
+                           gather_windows=2)
+        for r in range(N):
+            run.pl.opt_state_init(r, [t.data_ptr() for t in run.st[r]], seed=SEED)
+        run.set_grads(1)
+        run.step(1)
+        for b in range(len(lay.buckets)):
+            s0, n = lay.buckets[b]
+            out = run.pl.gather_window(0, b, slot=b % 2)
+            for r in range(N):
+                if code[0] == "N":
+                    ptr = run.pl.buffer(r, 1) + 2 * s0
+                else:
+                    ptr = run.pl.buffer(r, 5) + 2 * (b % 2) * B
+                if r == 0:
+                    assert ptr == out
+                got = d2h(ptr, n, np.uint16)
+                assert np.array_equal(got, p_full[s0:s0 + n]), (code, b, r)
+        run.close()

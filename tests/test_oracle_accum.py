@@ -146,3 +146,31 @@ def test_accum_scalars():
     assert nm.AdamScalars(1e-3, 1).s_g == np.float32(1.0)
     with pytest.raises(ValueError):
         nm.AdamScalars(1e-3, 1, accum_steps=0)
+
+
+
+# ------------------------------------------------------------- forward/backward parameter gather (NEXT-2)
+@pytest.mark.parametrize("N,M", [(8, 4), (8, 2), (4, 2), (9, 3)])
+def test_param_gather_is_complete_and_matches_table3(N, M):
+    """Every rank ends with the full bf16 parameters (brute force), and the
+    per-rank bytes equal Table 3's Forward A-G(P) column per micro-batch
+    (P:454-490): MiCS / PaRO-IGG / PaRO-IIG gather intra-group (M-1)Psi/M;
+    ZeRO-3 gathers (N-1)Psi/N in total over all links (its flat-ring split
+    into intra / inter is a different topology, R14)."""
+    lay = L.Layout([N * 64 * 20 + 8, 77], N, M, bucket_elems=N * 64 * 4)
+    psi = lay.psi_pad
+    full = nm.bf16_bits_from_f32(ST.pad_flat(master_f32(0, lay.psi), psi, np.float32))
+    for code, meth in [("IGG", "PaRO-IGG"), ("IIG", "PaRO-IIG"), ("III", "MiCS"), ("GGG", "ZeRO-3"),
+                       ("GIG", None), ("NNN", None)]:
+        params = {r: ST.shard_of(full, lay, code[0], r) for r in range(N)}
+        got, sent = ST.param_gather(code, lay, params)
+        for r in range(N):
+            assert np.array_equal(got[r], full), (code, r)
+        if meth is None:
+            continue
+        t = A.table3(meth, N, M, 1, psi, corrected=True)["fwd_ag_p"]
+        for r in range(N):
+            if code[0] == "I":
+                assert tuple(Fr(x) for x in sent[r]) == (t[0] / N, t[1] / N)
+            else:
+                assert Fr(sum(sent[r])) == (t[0] + t[1]) / N
