@@ -513,6 +513,16 @@ def test_gather_windows_return_full_parameters(topo, transport):
             run.pl.opt_state_init(r, [t.data_ptr() for t in run.st[r]], seed=SEED)
         run.set_grads(1)
         run.step(1)
+        # the full model assembled from every rank's parameter residency (bit copies)
+        assembled = np.zeros(lay.psi_pad, np.uint16)
+        for r in range(N):
+            mine = run.state(r)["param"]
+            off = 0
+            for (a, e) in lay.shard_ranges(code[0], r):
+                assembled[a:e] = mine[off:off + e - a]
+                off += e - a
+        if topo != "flat":               # flat ring: another (deterministic) reduction order
+            assert np.array_equal(assembled, p_full), code
         for b in range(len(lay.buckets)):
             s0, n = lay.buckets[b]
             out = run.pl.gather_window(0, b, slot=b % 2)
@@ -524,5 +534,5 @@ def test_gather_windows_return_full_parameters(topo, transport):
                 if r == 0:
                     assert ptr == out
                 got = d2h(ptr, n, np.uint16)
-                assert np.array_equal(got, p_full[s0:s0 + n]), (code, b, r)
+                assert np.array_equal(got, assembled[s0:s0 + n]), (code, b, r)
         run.close()
