@@ -276,8 +276,19 @@ __device__ __forceinline__ void adam_unit(const AdamSeg& sg, int64_t u, const Ad
   __stcs(reinterpret_cast<float4*>(sg.m) + 2 * u + 1, make_float4(m[4], m[5], m[6], m[7]));
   __stcs(reinterpret_cast<float4*>(sg.v) + 2 * u, make_float4(v[0], v[1], v[2], v[3]));
   __stcs(reinterpret_cast<float4*>(sg.v) + 2 * u + 1, make_float4(v[4], v[5], v[6], v[7]));
-  // the bf16 parameter goes straight into its all-gather / parameter slot
-  reinterpret_cast<uint4*>(sg.param)[u] = pack8(w);
+  // the bf16 parameter goes straight into its all-gather / parameter slot, and
+  // (fused all-gather) into the consumers' parameter buffers over NVLink
+  const uint4 pk = pack8(w);
+  reinterpret_cast<uint4*>(sg.param)[u] = pk;
+  for (int i = 0; i < sg.npush; ++i) __stcg(reinterpret_cast<uint4*>(sg.push[i]) + u, pk);
+}
+
+// after a fused all-gather, make this thread's remote stores visible system-wide
+// before the kernel ends (the step-end peer barrier then publishes them)
+__device__ __forceinline__ void push_fence(const AdamArgs& a) {
+  int any = 0;
+  for (int i = 0; i < a.nseg; ++i) any |= a.seg[i].npush;
+  if (any) __threadfence_system();
 }
 
 __device__ __forceinline__ float unscale_of(const AdamArgs& a) { return a.s_g_dev ? *a.s_g_dev : a.s_g; }
@@ -301,6 +312,7 @@ __global__ void __launch_bounds__(kAdamBlock, 3) adam_kernel(const AdamArgs a) {
     for (int64_t u = s + threadIdx.x; u < e; u += blockDim.x) adam_unit(sg, u, c, nsq, bad);
     base += n8;
   }
+  push_fence(a);
   // block reduction of the norm partial: warp shuffles, then one warp
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) nsq += __shfl_xor_sync(0xffffffffu, nsq, o);
@@ -447,11 +459,14 @@ __global__ void __launch_bounds__(kTmaThreads, 1) adam_tma_kernel(const AdamArgs
       __stcs(reinterpret_cast<float4*>(sg.m + o) + 1, make_float4(m[4], m[5], m[6], m[7]));
       __stcs(reinterpret_cast<float4*>(sg.v + o), make_float4(v[0], v[1], v[2], v[3]));
       __stcs(reinterpret_cast<float4*>(sg.v + o) + 1, make_float4(v[4], v[5], v[6], v[7]));
-      *reinterpret_cast<uint4*>(sg.param + o) = pack8(w);
+      const uint4 pk = pack8(w);
+      *reinterpret_cast<uint4*>(sg.param + o) = pk;
+      for (int i = 0; i < sg.npush; ++i) __stcg(reinterpret_cast<uint4*>(sg.push[i] + o), pk);
     }
     __syncthreads();   // every thread is done with stage s: refill it
     if (threadIdx.x == 0 && k + stages < mine) issue(k + stages);
   }
+  push_fence(a);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) nsq += __shfl_xor_sync(0xffffffffu, nsq, o);
   __shared__ double s_part[kTmaThreads / 32];

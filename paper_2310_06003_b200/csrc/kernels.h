@@ -62,6 +62,7 @@ struct RoundsArgs {
 };
 
 constexpr int kAdamMaxIn = 4;
+constexpr int kAdamMaxPush = 8;   // fused parameter all-gather: peers per store
 
 struct AdamSeg {
   // g_hat = fold(gin[0..gnin-1]) with the hop operator: 1 input = a
@@ -76,6 +77,8 @@ struct AdamSeg {
   int32_t gnin;
   uint32_t graw;     // bit i: gin[i] is a raw gradient -> RNE_bf16(g * alpha)
   int32_t in_norm;   // elements counted in the unique-element norm
+  int32_t npush;     // fused parameter all-gather: the bf16 output is also
+  uint16_t* push[kAdamMaxPush];   // stored at these peer addresses (NVLink)
 };
 
 struct AdamArgs {

@@ -481,6 +481,7 @@ void paro_opts_default(paro_opts_t* o) {
   o->clip_norm = 0.f;
   o->skip_nonfinite = 0;
   o->gather_windows = 0;
+  o->fuse_gather = 1;
   o->stream = nullptr;
 }
 
@@ -600,6 +601,7 @@ paro_status_t paro_plan(paro_ctx_t ctx, const char* strategy, const int64_t* par
   if (po.two_phase) po.fuse_final = false;   // g_hat is materialised for the norm pass
   if (o.gather_windows < 0 || o.gather_windows > 64) return fail(PARO_ERR_INVALID, "gather_windows must be in [0, 64]");
   po.windows = o.gather_windows;
+  po.fuse_gather = o.fuse_gather != 0 && !(o.inter_gbps > 0.f) && o.topology != PARO_TOPO_NCCL;
   auto* p = new PlanT();
   p->ctx = ctx;
   p->opts = o;
@@ -893,6 +895,13 @@ paro_status_t paro_step(paro_plan_t p, const void* const* grads, void* const* pa
   }
   CK(cudaMemsetAsync(p->d_nonfinite, 0, sizeof(int), ctx->comp));
   CK(cudaMemsetAsync(p->d_partials, 0, sizeof(double) * p->partials_cap, ctx->comp));
+  // fused parameter all-gather: Adam stores into peers' parameter buffers, so
+  // every peer must have entered this step (its reads of last step's
+  // parameters are stream-ordered before it) before the first update
+  if (!pl.sched.empty() && !pl.sched[0].param_push.empty()) {
+    paro_status_t s0 = all_peer_barrier(p, &launches);
+    if (s0 != PARO_OK) return s0;
+  }
 
   const int nb = (int)pl.buckets.size();
   const int grid = adam_grid();
@@ -928,6 +937,10 @@ paro_status_t paro_step(paro_plan_t p, const void* const* grads, void* const* pa
       sg.param = reinterpret_cast<uint16_t*>(data_ptr(p, S0.param[r].rank, S0.param[r].kind, S0.param[r].off));
       sg.n8 = len / 8;
       sg.in_norm = (uniq && (norm_only || !two)) ? 1 : 0;
+      sg.npush = 0;
+      if (!S0.param_push.empty())
+        for (const Ref& x : S0.param_push[r])
+          sg.push[sg.npush++] = reinterpret_cast<uint16_t*>(data_ptr(p, x.rank, x.kind, x.off));
     }
     aa.partials = p->d_partials + (int64_t)n_adam * grid;
     if (norm_only) {

@@ -766,6 +766,29 @@ void Planner::build_schedule() {
       }
       // ---- parameter restore
       Launch& Lg = S.gather;
+      // ---- fused parameter all-gather (B200 design: the bf16 cast lands in the
+      // consumers' buffers straight from the Adam kernel over NVLink).  Only
+      // where the restore is ONE ring, so bytes per link class are unchanged:
+      // AG_E (P = I, OS = G: the g-1 same-position ranks), AG_I (P = N, OS = I:
+      // the M-1 group members), HO_AG with M = 1 or g = 1 (all other ranks).
+      const bool one_ring = (OS == LV_G && P == LV_I) || (OS == LV_I && P == LV_N) ||
+                            (OS == LV_G && P == LV_N && (M == 1 || g == 1));
+      const int n_cons = (OS == LV_G && P == LV_I) ? g - 1 : ((OS == LV_I) ? M - 1 : N - 1);
+      if (opt.fuse_gather && one_ring && n_cons <= kMaxPush && n_cons > 0) {
+        S.param_push.assign(N, {});
+        for (int r = 0; r < N; ++r) {
+          const int j = grp(r), p = pos(r);
+          Ref mine = param_base(r);
+          if (P == LV_I) mine = at(mine, int64_t(j) * C);
+          else if (OS == LV_G) mine = at(mine, int64_t(seg(j, p)) * C);
+          else mine = at(mine, int64_t(p) * chunk);
+          for (int x = 0; x < N; ++x) {
+            if (x == r) continue;
+            const bool cons = (OS == LV_G && P == LV_I) ? (pos(x) == p) : (OS == LV_I ? grp(x) == j : true);
+            if (cons) S.param_push[r].push_back(Ref{x, BUF_PARAM, mine.off});
+          }
+        }
+      }
       // ---- forward/backward parameter all-gather into a window (P = I / G):
       // round 0 copies the own P shard into its place, then the ring AG in place
       // (P = I: AG_I, "intra-group all-gather"; P = G: the world AG)
@@ -780,9 +803,11 @@ void Planner::build_schedule() {
         else emit_world_ag(S.window, win, 1);
         S.window.final_barrier = true;   // peers are done reading the slot before it is reused
       }
-      if (OS == LV_G && P == LV_I) emit_ag_e(Lg, param_base, 0);
-      if (OS == LV_G && P == LV_N) emit_world_ag(Lg, param_base, 0);
-      if (OS == LV_I && P == LV_N) emit_ag_i(Lg, param_base, 0);
+      if (S.param_push.empty()) {
+        if (OS == LV_G && P == LV_I) emit_ag_e(Lg, param_base, 0);
+        if (OS == LV_G && P == LV_N) emit_world_ag(Lg, param_base, 0);
+        if (OS == LV_I && P == LV_N) emit_ag_i(Lg, param_base, 0);
+      }
       // drop rounds that ended up empty for every rank (degenerate splits)
       for (Launch* Lp : {&S.reduce, &S.gather, &S.accum, &S.reduce_acc, &S.window}) {
         const bool is_red = (Lp == &S.reduce || Lp == &S.reduce_acc);
@@ -920,6 +945,10 @@ void Planner::validate_refs() const {
       if (!ok(S.param[r], S.os_len)) throw std::logic_error("adam output out of range in bucket " + std::to_string(b));
       for (const Ref& x : S.ghat_in[r])
         if (!ok(x, S.os_len)) throw std::logic_error("adam input out of range in bucket " + std::to_string(b));
+      if (!S.param_push.empty())
+        for (const Ref& x : S.param_push[r])
+          if (!ok(x, S.os_len) || x.off != S.param[r].off || x.kind != BUF_PARAM)
+            throw std::logic_error("fused gather target out of range in bucket " + std::to_string(b));
       for (size_t i = 0; opt.accum && i < S.ghat_in_acc[r].size(); ++i)
         if (!ok(S.ghat_in_acc[r][i], S.os_len))
           throw std::logic_error("adam input out of range in bucket " + std::to_string(b));
@@ -931,7 +960,10 @@ void Planner::count_bytes() {
   // bytes each rank sends (pull: what peers read from it; push: what it stores
   // into peers) over a list of launches plus the fused-Adam peer reads
   auto count = [&](std::initializer_list<const Launch*> Ls, const std::vector<std::vector<Ref>>* gin,
-                   int64_t os_len, std::vector<int64_t>& si, std::vector<int64_t>& se) {
+                   int64_t os_len, std::vector<int64_t>& si, std::vector<int64_t>& se,
+                   const std::vector<std::vector<Ref>>* push = nullptr) {
+    for (int x = 0; push && x < N && (int)push->size() == N; ++x)   // fused gather: x stores into y
+      for (const Ref& y : (*push)[x]) (grp(x) == grp(y.rank) ? si[x] : se[x]) += 2 * os_len;
     for (const Launch* L : Ls)
       for (const auto& rnd : L->rounds)
         for (int x = 0; x < N; ++x)
@@ -965,11 +997,12 @@ void Planner::count_bytes() {
       ++n_comm_launches;
       n_rounds += (int)L->rounds.size();
     }
-    count({&S.reduce, &S.gather}, &S.ghat_in, S.os_len, send_intra, send_inter);
+    count({&S.reduce, &S.gather}, &S.ghat_in, S.os_len, send_intra, send_inter, &S.param_push);
     count({&S.window}, nullptr, 0, win_send_intra, win_send_inter);
     if (opt.accum) {
       count({&S.accum}, nullptr, 0, acc_send_intra, acc_send_inter);
-      count({&S.reduce_acc, &S.gather}, &S.ghat_in_acc, S.os_len, accstep_send_intra, accstep_send_inter);
+      count({&S.reduce_acc, &S.gather}, &S.ghat_in_acc, S.os_len, accstep_send_intra, accstep_send_inter,
+            &S.param_push);
     }
     // NCCL comparator: ring-algorithm volumes of each call (perf only)
     for (int r = 0; r < N && opt.topology == 4; ++r) {

@@ -35,7 +35,8 @@ enum BufKind : int {
 
 constexpr int kMaxIn = 16;   // max inputs of one fold task
 constexpr int kStageSets = 3;
-constexpr int kMaxAdamIn = 4;  // max fold inputs of the fused final hop in Adam  // rotation of per-bucket staging sets (reuse distance)
+constexpr int kMaxAdamIn = 4;
+constexpr int kMaxPush = 8;    // max peers one fused-gather Adam store goes to  // max fold inputs of the fused final hop in Adam  // rotation of per-bucket staging sets (reuse distance)
 
 struct Ref {
   int32_t rank = -1;
@@ -96,6 +97,10 @@ struct BucketSchedule {
   // forward/backward parameter all-gather of the whole bucket into window slot
   // 0; the engine shifts BUF_WIN refs to the slot used
   Launch window;
+  // fused parameter all-gather: Adam also stores its bf16 output into these
+  // peers' parameter buffers (same offset: the layouts are symmetric), which
+  // replaces the gather launch when the consumers are one ring's members
+  std::vector<std::vector<Ref>> param_push;
 };
 
 struct PlanOptions {
@@ -107,6 +112,7 @@ struct PlanOptions {
   bool accum = false;        // build the gradient-accumulation launches (s > 1)
   bool two_phase = false;    // clipping / skip: every bucket's g_hat stays resident until Adam (R28)
   int windows = 0;           // parameter-gather window slots (0: none)
+  bool fuse_gather = true;   // fold a one-ring parameter all-gather into Adam's stores
 };
 
 class Planner {

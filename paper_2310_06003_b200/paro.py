@@ -46,7 +46,8 @@ class paro_opts_t(C.Structure):
                 ("loss_scale", C.c_float), ("comm_ctas", C.c_int), ("pipeline_depth", C.c_int),
                 ("pull_transport", C.c_int), ("adam_impl", C.c_int), ("comm_impl", C.c_int),
                 ("inter_gbps", C.c_float), ("clip_norm", C.c_float), ("skip_nonfinite", C.c_int),
-                ("gather_windows", C.c_int), ("grad_accum", C.c_int), ("stream", C.c_void_p)]
+                ("fuse_gather", C.c_int), ("gather_windows", C.c_int), ("grad_accum", C.c_int),
+                ("stream", C.c_void_p)]
 
 
 class paro_plan_info_t(C.Structure):
@@ -135,7 +136,8 @@ def check(status):
 # ---------------------------------------------------------------- helpers
 def make_opts(bucket_elems=1 << 26, topology="ho", beta1=0.9, beta2=0.95, eps=1e-8, weight_decay=0.0,
               loss_scale=1.0, comm_ctas=148, pipeline_depth=2, stream=None, transport="pull", adam_impl="auto",
-              comm_impl="tma", inter_gbps=0.0, grad_accum=False, clip_norm=0.0, skip_nonfinite=False, gather_windows=0):
+              comm_impl="tma", inter_gbps=0.0, grad_accum=False, clip_norm=0.0, skip_nonfinite=False, gather_windows=0,
+              fuse_gather=True):
     o = paro_opts_t()
     paro_opts_default(C.byref(o))
     o.bucket_elems = int(bucket_elems)
@@ -151,6 +153,7 @@ def make_opts(bucket_elems=1 << 26, topology="ho", beta1=0.9, beta2=0.95, eps=1e
     o.clip_norm = float(clip_norm)
     o.skip_nonfinite = 1 if skip_nonfinite else 0
     o.gather_windows = int(gather_windows)
+    o.fuse_gather = 1 if fuse_gather else 0
     o.stream = stream
     return o
 
