@@ -47,7 +47,7 @@ def parse():
     ap.add_argument("--comm-ctas", type=int, default=148)
     ap.add_argument("--depth", type=int, default=2)
     ap.add_argument("--transport", default="pull", choices=["pull", "push"])
-    ap.add_argument("--adam-impl", default="auto", choices=["auto", "lsu"])
+    ap.add_argument("--adam-impl", default="auto", choices=["auto", "lsu", "tma_store"])
     ap.add_argument("--comm-impl", default="tma", choices=["tma", "lsu"])
     ap.add_argument("--no-fuse-gather", action="store_true",
                     help="run the parameter all-gather as its own launch instead of inside Adam")

@@ -87,7 +87,8 @@ typedef struct {
                           * successor's buffers (push).  Same bits either way.     */
   int adam_impl;         /* 0 (default): TMA bulk-copy pipeline (cp.async.bulk +    *
                           * mbarrier stages; also pulls NVLink-peer operands);      *
-                          * 1: the LSU (ld.global) kernel                           */
+                          * 1: the LSU (ld.global) kernel; 2: TMA both ways (the   *
+                          * results leave shared memory through bulk copies too)   */
   int comm_impl;         /* 0 (default): collective rounds move operands with TMA  *
                           * bulk copies into shared memory; 1: LSU kernel           */
   float inter_gbps;      /* > 0: emulate a slow inter-group link — each rank's     *

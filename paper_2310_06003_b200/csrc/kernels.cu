@@ -367,6 +367,21 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                : "memory");
 }
 
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
 struct TileRef {
   int seg;
   int64_t start;   // element offset inside the segment
@@ -388,6 +403,12 @@ __device__ __forceinline__ bool tile_of(const AdamArgs& a, int64_t t, TileRef& o
   return false;
 }
 
+// kStore = false: results are stored by the threads (st.global.cs);
+// kStore = true: results are written back into the stage in shared memory and
+// leave through bulk copies too (master, m, v, the bf16 parameter and, for the
+// fused all-gather, the peers' parameter buffers): the stage is refilled one
+// iteration later, once its stores have read it (wait_group.read 1).
+template <bool kStore>
 __global__ void __launch_bounds__(kTmaThreads, 1) adam_tma_kernel(const AdamArgs a, int gnin_max, int stages) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ uint64_t full_bar[4];
@@ -428,7 +449,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) adam_tma_kernel(const AdamArgs
     TileRef tr;
     tile_of(a, blockIdx.x + k * gridDim.x, tr);
     const AdamSeg& sg = a.seg[tr.seg];
-    const unsigned char* base = smem + s * stage_bytes;
+    unsigned char* base = smem + s * stage_bytes;
     const int e0 = threadIdx.x * 8;
     if (e0 < tr.n) {
       float g[8];
@@ -440,7 +461,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) adam_tma_kernel(const AdamArgs
         if ((sg.graw >> i) & 1u) scale_round8(x, c.alpha);
         hop8(g, x);
       }
-      const float* fw = reinterpret_cast<const float*>(base + gnin_max * g_bytes);
+      float* fw = reinterpret_cast<float*>(base + gnin_max * g_bytes);
       const float4 w0 = *reinterpret_cast<const float4*>(fw + e0), w1 = *reinterpret_cast<const float4*>(fw + e0 + 4);
       const float4 m0 = *reinterpret_cast<const float4*>(fw + kTmaTile + e0);
       const float4 m1 = *reinterpret_cast<const float4*>(fw + kTmaTile + e0 + 4);
@@ -452,21 +473,57 @@ __global__ void __launch_bounds__(kTmaThreads, 1) adam_tma_kernel(const AdamArgs
       const bool in_norm = sg.in_norm != 0;
 #pragma unroll
       for (int e = 0; e < 8; ++e) adam_elem(g[e], w[e], m[e], v[e], c, nsq, bad, in_norm);
-      const int64_t o = tr.start + e0;
-      __stcs(reinterpret_cast<float4*>(sg.master + o), make_float4(w[0], w[1], w[2], w[3]));
-      __stcs(reinterpret_cast<float4*>(sg.master + o) + 1, make_float4(w[4], w[5], w[6], w[7]));
-      __stcs(reinterpret_cast<float4*>(sg.m + o), make_float4(m[0], m[1], m[2], m[3]));
-      __stcs(reinterpret_cast<float4*>(sg.m + o) + 1, make_float4(m[4], m[5], m[6], m[7]));
-      __stcs(reinterpret_cast<float4*>(sg.v + o), make_float4(v[0], v[1], v[2], v[3]));
-      __stcs(reinterpret_cast<float4*>(sg.v + o) + 1, make_float4(v[4], v[5], v[6], v[7]));
       const uint4 pk = pack8(w);
-      *reinterpret_cast<uint4*>(sg.param + o) = pk;
-      for (int i = 0; i < sg.npush; ++i) __stcg(reinterpret_cast<uint4*>(sg.push[i] + o), pk);
+      if (kStore) {   // back into the stage, in place (each thread owns its 8 elements)
+        *reinterpret_cast<float4*>(fw + e0) = make_float4(w[0], w[1], w[2], w[3]);
+        *reinterpret_cast<float4*>(fw + e0 + 4) = make_float4(w[4], w[5], w[6], w[7]);
+        *reinterpret_cast<float4*>(fw + kTmaTile + e0) = make_float4(m[0], m[1], m[2], m[3]);
+        *reinterpret_cast<float4*>(fw + kTmaTile + e0 + 4) = make_float4(m[4], m[5], m[6], m[7]);
+        *reinterpret_cast<float4*>(fw + 2 * kTmaTile + e0) = make_float4(v[0], v[1], v[2], v[3]);
+        *reinterpret_cast<float4*>(fw + 2 * kTmaTile + e0 + 4) = make_float4(v[4], v[5], v[6], v[7]);
+        *reinterpret_cast<uint4*>(base + e0 * 2) = pk;   // over g_hat input 0 (consumed)
+      } else {
+        const int64_t o = tr.start + e0;
+        __stcs(reinterpret_cast<float4*>(sg.master + o), make_float4(w[0], w[1], w[2], w[3]));
+        __stcs(reinterpret_cast<float4*>(sg.master + o) + 1, make_float4(w[4], w[5], w[6], w[7]));
+        __stcs(reinterpret_cast<float4*>(sg.m + o), make_float4(m[0], m[1], m[2], m[3]));
+        __stcs(reinterpret_cast<float4*>(sg.m + o) + 1, make_float4(m[4], m[5], m[6], m[7]));
+        __stcs(reinterpret_cast<float4*>(sg.v + o), make_float4(v[0], v[1], v[2], v[3]));
+        __stcs(reinterpret_cast<float4*>(sg.v + o) + 1, make_float4(v[4], v[5], v[6], v[7]));
+        *reinterpret_cast<uint4*>(sg.param + o) = pk;
+        for (int i = 0; i < sg.npush; ++i) __stcg(reinterpret_cast<uint4*>(sg.push[i] + o), pk);
+      }
     }
-    __syncthreads();   // every thread is done with stage s: refill it
-    if (threadIdx.x == 0 && k + stages < mine) issue(k + stages);
+    if (kStore) {
+      fence_proxy_async_smem();   // this thread's smem writes -> visible to the bulk-copy engine
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const uint32_t gb = (uint32_t)tr.n * 2, fb = (uint32_t)tr.n * 4;
+        const unsigned char* fbase = base + gnin_max * g_bytes;
+        bulk_s2g(sg.master + tr.start, fbase, fb);
+        bulk_s2g(sg.m + tr.start, fbase + f_bytes, fb);
+        bulk_s2g(sg.v + tr.start, fbase + 2 * f_bytes, fb);
+        bulk_s2g(sg.param + tr.start, base, gb);
+        for (int i = 0; i < sg.npush; ++i) bulk_s2g(sg.push[i] + tr.start, base, gb);
+        bulk_commit();
+        // the previous tile's stores have read their stage: refill it
+        bulk_wait_read<1>();
+        if (k >= 1 && k - 1 + stages < mine) issue(k - 1 + stages);
+      }
+    } else {
+      __syncthreads();   // every thread is done with stage s: refill it
+      if (threadIdx.x == 0 && k + stages < mine) issue(k + stages);
+    }
   }
-  push_fence(a);
+  if (kStore) {
+    if (threadIdx.x == 0) {
+      bulk_wait_all();
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      __threadfence_system();
+    }
+  } else {
+    push_fence(a);
+  }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) nsq += __shfl_xor_sync(0xffffffffu, nsq, o);
   __shared__ double s_part[kTmaThreads / 32];
@@ -769,7 +826,7 @@ static cudaError_t set_carveouts() {
   static bool done = false;
   if (done) return cudaSuccess;
   const void* fns[] = {(const void*)rounds_kernel, (const void*)rounds_tma_kernel, (const void*)adam_kernel,
-                       (const void*)adam_tma_kernel};
+                       (const void*)adam_tma_kernel<false>, (const void*)adam_tma_kernel<true>};
   for (const void* f : fns) {
     cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout,
                                          (int)cudaSharedmemCarveoutMaxShared);
@@ -819,7 +876,7 @@ cudaError_t launch_adam(const AdamArgs& a, int grid, cudaStream_t s, int cap_two
 }
 
 // TMA pipeline: persistent grid (one CTA per SM); stages sized to ~200 KB.
-cudaError_t launch_adam_tma(const AdamArgs& a, int sms, cudaStream_t s, int smem_budget_kb) {
+cudaError_t launch_adam_tma(const AdamArgs& a, int sms, cudaStream_t s, int smem_budget_kb, int tma_store) {
   cudaError_t ec = set_carveouts();
   if (ec != cudaSuccess) return ec;
   int gmax = 1;
@@ -831,11 +888,15 @@ cudaError_t launch_adam_tma(const AdamArgs& a, int sms, cudaStream_t s, int smem
   const size_t smem = stage * stages;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(adam_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    cudaError_t e = cudaFuncSetAttribute(adam_tma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         220 * 1024);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(adam_tma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  adam_tma_kernel<<<sms, kTmaThreads, smem, s>>>(a, gmax, stages);
+  if (tma_store) adam_tma_kernel<true><<<sms, kTmaThreads, smem, s>>>(a, gmax, stages);
+  else adam_tma_kernel<false><<<sms, kTmaThreads, smem, s>>>(a, gmax, stages);
   return cudaGetLastError();
 }
 

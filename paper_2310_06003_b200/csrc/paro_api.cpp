@@ -957,7 +957,8 @@ paro_status_t paro_step(paro_plan_t p, const void* const* grads, void* const* pa
     // while collectives run beside it (real N > 1) Adam keeps ~120 KB of shared
     // memory per SM so the TMA collective kernel (<= 96 KB) fits on the same SM
     if (p->opts.adam_impl != 1)
-      CK(launch_adam_tma(aa, ctx->sm_count, ctx->comp, (ctx->mode == MODE_REAL && pl.N > 1) ? 120 : 200));
+      CK(launch_adam_tma(aa, ctx->sm_count, ctx->comp, (ctx->mode == MODE_REAL && pl.N > 1) ? 120 : 200,
+                         p->opts.adam_impl == 2 ? 1 : 0));
     else CK(launch_adam(aa, grid, ctx->comp, (ctx->mode == MODE_REAL && pl.N > 1) ? 1 : 0));
     prof_end(p, ctx->comp, pk);
     ++n_adam;

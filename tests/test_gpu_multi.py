@@ -59,7 +59,8 @@ def test_real_ranks_match_oracle(tmp_path, variant):
         cfg.update({"codes": ["NNN", "IIG", "GGG", "NIG"], "topos": ["ho", "flat"], "transports": ["pull"],
                     "inter_gbps": 50.0, "comm_impl": "lsu"})
     if variant == "accum":       # gradient accumulation, s = 3 micro-batches per step (NEXT-1)
-        cfg.update({"accum": 3, "topos": ["ho", "two_step"], "transports": ["pull", "push"], "windows": 2})
+        cfg.update({"accum": 3, "topos": ["ho", "two_step"], "transports": ["pull", "push"], "windows": 2,
+                    "adam_impl": "tma_store"})
     if variant == "clip":        # two-phase step with an active global-norm clip (NEXT-3)
         cfg.update({"clip_norm": 0.05, "topos": ["ho", "nccl"], "transports": ["pull"]})
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",

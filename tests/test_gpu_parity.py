@@ -132,7 +132,7 @@ def test_synth_generator_matches_host():
 
 
 # --------------------------------------------------------------------- N = 1
-@pytest.mark.parametrize("adam_impl", ["auto", "lsu"])
+@pytest.mark.parametrize("adam_impl", ["auto", "lsu", "tma_store"])
 @pytest.mark.parametrize("wd,ls", [(0.0, 1.0), (0.1, 4.0)])
 def test_n1_ten_steps_bit_exact(wd, ls, adam_impl):
     sizes = [50_000, 4096, 12_345, 3 * 4096 * 148 + 8]   # > one tile per CTA, ragged tail
@@ -206,7 +206,7 @@ def test_flat_ring_matches_oracle_flat_simulation(transport):
         run.close()
 
 
-@pytest.mark.parametrize("adam_impl", ["auto", "lsu"])
+@pytest.mark.parametrize("adam_impl", ["auto", "lsu", "tma_store"])
 @pytest.mark.parametrize("code", ["IIG", "NNN", "III", "GGG"])
 def test_4m_2x4_ten_steps(code, adam_impl):
     N, M = 8, 4
