@@ -338,8 +338,6 @@ __global__ void __launch_bounds__(kAdamBlock, 3) adam_kernel(const AdamArgs a) {
 // (up to ~170 KB per SM) in flight while 16 warps compute on the current one,
 // so memory-level parallelism no longer costs registers.  Persistent grid:
 // one CTA per SM, tiles dealt round-robin.  Inputs must be local memory.
-constexpr int kTmaThreads = 512;
-constexpr int kTmaTile = kTmaThreads * 8;   // elements per tile (8 per thread)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -388,14 +386,15 @@ struct TileRef {
   int n;           // elements in this tile (multiple of 8)
 };
 
+template <int kTile>
 __device__ __forceinline__ bool tile_of(const AdamArgs& a, int64_t t, TileRef& out) {
   for (int i = 0; i < a.nseg; ++i) {
     const int64_t n = a.seg[i].n8 * 8;
-    const int64_t nt = (n + kTmaTile - 1) / kTmaTile;
+    const int64_t nt = (n + kTile - 1) / kTile;
     if (t < nt) {
       out.seg = i;
-      out.start = t * kTmaTile;
-      out.n = (int)min((int64_t)kTmaTile, n - out.start);
+      out.start = t * kTile;
+      out.n = (int)min((int64_t)kTile, n - out.start);
       return true;
     }
     t -= nt;
@@ -408,8 +407,9 @@ __device__ __forceinline__ bool tile_of(const AdamArgs& a, int64_t t, TileRef& o
 // leave through bulk copies too (master, m, v, the bf16 parameter and, for the
 // fused all-gather, the peers' parameter buffers): the stage is refilled one
 // iteration later, once its stores have read it (wait_group.read 1).
-template <bool kStore>
-__global__ void __launch_bounds__(kTmaThreads, 1) adam_tma_kernel(const AdamArgs a, int gnin_max, int stages) {
+template <bool kStore, int kThr>
+__global__ void __launch_bounds__(kThr, 1) adam_tma_kernel(const AdamArgs a, int gnin_max, int stages) {
+  constexpr int kTmaTile = kThr * 8;   // elements per tile (8 per thread)
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ uint64_t full_bar[4];
   if (a.skip && *a.skip) return;   // two-phase step: non-finite gradients, update skipped
@@ -427,7 +427,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) adam_tma_kernel(const AdamArgs
   __syncthreads();
   auto issue = [&](int64_t k) {   // thread 0: load tile k of this CTA into stage k % stages
     TileRef tr;
-    tile_of(a, blockIdx.x + k * gridDim.x, tr);
+    tile_of<kTmaTile>(a, blockIdx.x + k * gridDim.x, tr);
     const AdamSeg& sg = a.seg[tr.seg];
     const int s = (int)(k % stages);
     unsigned char* base = smem + s * stage_bytes;
@@ -447,7 +447,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) adam_tma_kernel(const AdamArgs
     const int s = (int)(k % stages);
     mbar_wait(&full_bar[s], (uint32_t)((k / stages) & 1));
     TileRef tr;
-    tile_of(a, blockIdx.x + k * gridDim.x, tr);
+    tile_of<kTmaTile>(a, blockIdx.x + k * gridDim.x, tr);
     const AdamSeg& sg = a.seg[tr.seg];
     unsigned char* base = smem + s * stage_bytes;
     const int e0 = threadIdx.x * 8;
@@ -526,7 +526,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) adam_tma_kernel(const AdamArgs
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) nsq += __shfl_xor_sync(0xffffffffu, nsq, o);
-  __shared__ double s_part[kTmaThreads / 32];
+  __shared__ double s_part[kThr / 32];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   if (lane == 0) s_part[wid] = nsq;
   const int any_bad = __syncthreads_or(bad);
@@ -826,7 +826,8 @@ static cudaError_t set_carveouts() {
   static bool done = false;
   if (done) return cudaSuccess;
   const void* fns[] = {(const void*)rounds_kernel, (const void*)rounds_tma_kernel, (const void*)adam_kernel,
-                       (const void*)adam_tma_kernel<false>, (const void*)adam_tma_kernel<true>};
+                       (const void*)adam_tma_kernel<false, 512>, (const void*)adam_tma_kernel<true, 512>,
+                       (const void*)adam_tma_kernel<true, 256>};
   for (const void* f : fns) {
     cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout,
                                          (int)cudaSharedmemCarveoutMaxShared);
@@ -876,27 +877,40 @@ cudaError_t launch_adam(const AdamArgs& a, int grid, cudaStream_t s, int cap_two
 }
 
 // TMA pipeline: persistent grid (one CTA per SM); stages sized to ~200 KB.
+// TMA pipeline: persistent grid (one CTA per SM), stages sized to the budget.
+// The TMA-store variant refills a stage one iteration late (after its stores
+// have read it), so it keeps >= 3 stages: with a small budget (collectives
+// co-running) it switches to 2048-element tiles (256 threads).
 cudaError_t launch_adam_tma(const AdamArgs& a, int sms, cudaStream_t s, int smem_budget_kb, int tma_store) {
   cudaError_t ec = set_carveouts();
   if (ec != cudaSuccess) return ec;
   int gmax = 1;
   for (int i = 0; i < a.nseg; ++i) gmax = a.seg[i].gnin > gmax ? a.seg[i].gnin : gmax;
-  const size_t stage = (size_t)kTmaTile * (2 * gmax + 12);
-  int stages = (int)(((size_t)smem_budget_kb * 1024) / stage);
-  if (stages > 4) stages = 4;
-  if (stages < 2) stages = 2;
-  const size_t smem = stage * stages;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(adam_tma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         220 * 1024);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(adam_tma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    if (e != cudaSuccess) return e;
+    for (const void* f : {(const void*)adam_tma_kernel<false, 512>, (const void*)adam_tma_kernel<true, 512>,
+                          (const void*)adam_tma_kernel<true, 256>}) {
+      cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+      if (e != cudaSuccess) return e;
+    }
     attr_set = true;
   }
-  if (tma_store) adam_tma_kernel<true><<<sms, kTmaThreads, smem, s>>>(a, gmax, stages);
-  else adam_tma_kernel<false><<<sms, kTmaThreads, smem, s>>>(a, gmax, stages);
+  auto stages_for = [&](int tile) {
+    const size_t stage = (size_t)tile * (2 * gmax + 12);
+    int st = (int)(((size_t)smem_budget_kb * 1024) / stage);
+    return st > 4 ? 4 : (st < 2 ? 2 : st);
+  };
+  if (!tma_store) {
+    const int st = stages_for(4096);
+    adam_tma_kernel<false, 512><<<sms, 512, (size_t)4096 * (2 * gmax + 12) * st, s>>>(a, gmax, st);
+  } else if (stages_for(4096) >= 3) {
+    const int st = stages_for(4096);
+    adam_tma_kernel<true, 512><<<sms, 512, (size_t)4096 * (2 * gmax + 12) * st, s>>>(a, gmax, st);
+  } else {
+    int st = stages_for(2048);
+    if (st < 3) st = 3;
+    adam_tma_kernel<true, 256><<<sms, 256, (size_t)2048 * (2 * gmax + 12) * st, s>>>(a, gmax, st);
+  }
   return cudaGetLastError();
 }
 

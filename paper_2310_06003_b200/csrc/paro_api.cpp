@@ -956,10 +956,14 @@ paro_status_t paro_step(paro_plan_t p, const void* const* grads, void* const* pa
     // inputs: tools/tma_peer_test.cu measured 782 GB/s); LSU kernel on request.
     // while collectives run beside it (real N > 1) Adam keeps ~120 KB of shared
     // memory per SM so the TMA collective kernel (<= 96 KB) fits on the same SM
+    // (no collective rounds beside it, e.g. everything fused: the full budget)
+    bool corun = false;
+    if (ctx->mode == MODE_REAL && pl.N > 1)
+      for (size_t b = 0; b < p->red.size() && !corun; ++b)
+        corun = red[b].nrounds > 0 || p->gat[b].nrounds > 0;
     if (p->opts.adam_impl != 1)
-      CK(launch_adam_tma(aa, ctx->sm_count, ctx->comp, (ctx->mode == MODE_REAL && pl.N > 1) ? 120 : 200,
-                         p->opts.adam_impl == 2 ? 1 : 0));
-    else CK(launch_adam(aa, grid, ctx->comp, (ctx->mode == MODE_REAL && pl.N > 1) ? 1 : 0));
+      CK(launch_adam_tma(aa, ctx->sm_count, ctx->comp, corun ? 120 : 200, p->opts.adam_impl == 2 ? 1 : 0));
+    else CK(launch_adam(aa, grid, ctx->comp, corun ? 1 : 0));
     prof_end(p, ctx->comp, pk);
     ++n_adam;
     ++launches;
