@@ -86,9 +86,10 @@ typedef struct {
                           * over NVLink (pull); 0: ranks STORE into their          *
                           * successor's buffers (push).  Same bits either way.     */
   int adam_impl;         /* 0 (default): TMA bulk-copy pipeline (cp.async.bulk +    *
-                          * mbarrier stages; also pulls NVLink-peer operands);      *
-                          * 1: the LSU (ld.global) kernel; 2: TMA both ways (the   *
-                          * results leave shared memory through bulk copies too)   */
+                          * mbarrier stages; also pulls NVLink-peer operands); the *
+                          * results leave through bulk copies too when N = 1 (or   *
+                          * emulated), through thread stores otherwise;            *
+                          * 1: the LSU (ld.global) kernel; 2: TMA both ways always */
   int comm_impl;         /* 0 (default): collective rounds move operands with TMA  *
                           * bulk copies into shared memory; 1: LSU kernel           */
   float inter_gbps;      /* > 0: emulate a slow inter-group link — each rank's     *

@@ -961,8 +961,12 @@ paro_status_t paro_step(paro_plan_t p, const void* const* grads, void* const* pa
     if (ctx->mode == MODE_REAL && pl.N > 1)
       for (size_t b = 0; b < p->red.size() && !corun; ++b)
         corun = red[b].nrounds > 0 || p->gat[b].nrounds > 0;
+    // stores: bulk copies out of shared memory win when Adam has the GPU to itself
+    // and no NVLink operands (N = 1: 0.97 of the HBM peak vs 0.90, profiles/r01);
+    // beside collectives / with peer traffic the thread stores are faster
+    const bool tma_store = p->opts.adam_impl == 2 || (p->opts.adam_impl == 0 && (pl.N == 1 || ctx->mode == MODE_EMU));
     if (p->opts.adam_impl != 1)
-      CK(launch_adam_tma(aa, ctx->sm_count, ctx->comp, corun ? 120 : 200, p->opts.adam_impl == 2 ? 1 : 0));
+      CK(launch_adam_tma(aa, ctx->sm_count, ctx->comp, corun ? 120 : 200, tma_store ? 1 : 0));
     else CK(launch_adam(aa, grid, ctx->comp, corun ? 1 : 0));
     prof_end(p, ctx->comp, pk);
     ++n_adam;
