@@ -49,8 +49,8 @@ def parse():
     ap.add_argument("--transport", default="pull", choices=["pull", "push"])
     ap.add_argument("--adam-impl", default="auto", choices=["auto", "lsu", "tma_store"])
     ap.add_argument("--comm-impl", default="tma", choices=["tma", "lsu"])
-    ap.add_argument("--no-fuse-gather", action="store_true",
-                    help="run the parameter all-gather as its own launch instead of inside Adam")
+    ap.add_argument("--fuse-gather", default="auto", choices=["auto", "always", "never"],
+                    help="parameter all-gather inside Adam (one-ring restores)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -214,7 +214,7 @@ def run_ours(args):
     plan = paro.Plan(ctx, args.strategy, sizes, bucket_elems=args.bucket, topology=args.topology,
                      comm_ctas=args.comm_ctas, pipeline_depth=args.depth, stream=stream.cuda_stream,
                      transport=args.transport, adam_impl=args.adam_impl, comm_impl=args.comm_impl,
-                     fuse_gather=not args.no_fuse_gather)
+                     fuse_gather=args.fuse_gather)
     info = plan.info()
     st = [torch.empty(info["os_numel"], dtype=torch.float32, device="cuda") for _ in range(3)]
     ptrs = [[t.data_ptr() for t in st]]
@@ -344,7 +344,7 @@ def run_ours(args):
                        "topology": args.topology, "bucket_elems": info["bucket_elems"],
                        "n_buckets": info["n_buckets"], "comm_ctas": args.comm_ctas, "pipeline_depth": args.depth,
                        "transport": args.transport, "adam_impl": args.adam_impl, "comm_impl": args.comm_impl,
-                       "fuse_gather": not args.no_fuse_gather,
+                       "fuse_gather": args.fuse_gather,
                        "l2": "no flush: per-step inputs (13.5 GB grads + 81 GB/div(OS) state) >> 126 MB L2",
                        "intra_inter_gap": "not emulated: one NVSwitch box, intra/inter are labels"},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,

@@ -106,12 +106,14 @@ typedef struct {
                           * selects the two-phase step: every bucket is reduced    *
                           * and the norm all-reduced before the first update, and  *
                           * the reduced gradient stays resident (psi/div(OS) bf16) */
-  int fuse_gather;       /* 1 (default): when the parameter restore is one ring    *
-                          * (AG_E for P = I, OS = G; AG_I for P = N, OS = I; the   *
-                          * world ring when M = 1 or g = 1) the Adam kernel stores *
-                          * its bf16 output straight into the consumers' buffers   *
-                          * over NVLink instead of a separate all-gather launch;   *
-                          * same bits, same bytes per link class.  0: launch it.   */
+  int fuse_gather;       /* when the parameter restore is one ring (AG_E for P = I,*
+                          * OS = G; AG_I for P = N, OS = I; the world ring when    *
+                          * M = 1 or g = 1) the Adam kernel can store its bf16     *
+                          * output straight into the consumers' buffers over       *
+                          * NVLink instead of a separate all-gather launch (same   *
+                          * bits, same bytes per link class).  1 (default): only   *
+                          * when no collective rounds run beside Adam (the whole   *
+                          * reduction fused too); 2: always; 0: never.             */
   int gather_windows;    /* > 0: that many library window slots of bucket_elems    *
                           * bf16 each for paro_gather_window (P = I or G only).    */
   int grad_accum;        /* 1: enable paro_accumulate (gradient accumulation over  *

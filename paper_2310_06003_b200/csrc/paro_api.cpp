@@ -601,7 +601,8 @@ paro_status_t paro_plan(paro_ctx_t ctx, const char* strategy, const int64_t* par
   if (po.two_phase) po.fuse_final = false;   // g_hat is materialised for the norm pass
   if (o.gather_windows < 0 || o.gather_windows > 64) return fail(PARO_ERR_INVALID, "gather_windows must be in [0, 64]");
   po.windows = o.gather_windows;
-  po.fuse_gather = o.fuse_gather != 0 && !(o.inter_gbps > 0.f) && o.topology != PARO_TOPO_NCCL;
+  if (o.fuse_gather < 0 || o.fuse_gather > 2) return fail(PARO_ERR_INVALID, "fuse_gather must be 0, 1 or 2");
+  po.fuse_gather = (o.inter_gbps > 0.f || o.topology == PARO_TOPO_NCCL) ? 0 : o.fuse_gather;
   auto* p = new PlanT();
   p->ctx = ctx;
   p->opts = o;

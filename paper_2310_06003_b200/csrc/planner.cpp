@@ -774,7 +774,7 @@ void Planner::build_schedule() {
       const bool one_ring = (OS == LV_G && P == LV_I) || (OS == LV_I && P == LV_N) ||
                             (OS == LV_G && P == LV_N && (M == 1 || g == 1));
       const int n_cons = (OS == LV_G && P == LV_I) ? g - 1 : ((OS == LV_I) ? M - 1 : N - 1);
-      if (opt.fuse_gather && one_ring && n_cons <= kMaxPush && n_cons > 0) {
+      if (opt.fuse_gather > 0 && one_ring && n_cons <= kMaxPush && n_cons > 0) {
         S.param_push.assign(N, {});
         for (int r = 0; r < N; ++r) {
           const int j = grp(r), p = pos(r);
@@ -809,7 +809,7 @@ void Planner::build_schedule() {
         if (OS == LV_I && P == LV_N) emit_ag_i(Lg, param_base, 0);
       }
       // drop rounds that ended up empty for every rank (degenerate splits)
-      for (Launch* Lp : {&S.reduce, &S.gather, &S.accum, &S.reduce_acc, &S.window}) {
+      auto finish = [&](Launch* Lp) {
         const bool is_red = (Lp == &S.reduce || Lp == &S.reduce_acc);
         std::vector<std::vector<Ref>>& gin = (Lp == &S.reduce_acc) ? S.ghat_in_acc : S.ghat_in;
         std::vector<std::vector<std::vector<Task>>> kept;
@@ -859,6 +859,17 @@ void Planner::build_schedule() {
               if (t.dst.rank != r) Lp->final_barrier = true;
         }
         if (Lp->final_extra.empty()) Lp->final_extra.assign(N, 0);
+      };
+      for (Launch* Lp : {&S.reduce, &S.gather, &S.accum, &S.reduce_acc, &S.window}) finish(Lp);
+      // fused gather, auto mode: only when no collective rounds run beside Adam
+      // (the whole reduction fused too); beside a rounds kernel the separate
+      // all-gather launch measured faster (profiles/r01/sweep_fuse_4.jsonl)
+      if (opt.fuse_gather == 1 && !S.param_push.empty() && !S.reduce.rounds.empty()) {
+        S.param_push.clear();
+        if (OS == LV_G && P == LV_I) emit_ag_e(Lg, param_base, 0);
+        if (OS == LV_G && P == LV_N) emit_world_ag(Lg, param_base, 0);
+        if (OS == LV_I && P == LV_N) emit_ag_i(Lg, param_base, 0);
+        finish(&Lg);
       }
     } else if (N == 1 && opt.accum) {   // one rank: the accumulation is a local fold
       S.accum.add(0, 0, make_task(n, {grad(0, 0)}, Ref{0, acc_kind, s}));

@@ -112,7 +112,8 @@ struct PlanOptions {
   bool accum = false;        // build the gradient-accumulation launches (s > 1)
   bool two_phase = false;    // clipping / skip: every bucket's g_hat stays resident until Adam (R28)
   int windows = 0;           // parameter-gather window slots (0: none)
-  bool fuse_gather = true;   // fold a one-ring parameter all-gather into Adam's stores
+  int fuse_gather = 1;       // fold a one-ring parameter all-gather into Adam's stores:
+                             // 0 never, 1 when no collective rounds co-run, 2 always
 };
 
 class Planner {

@@ -137,7 +137,7 @@ def check(status):
 def make_opts(bucket_elems=1 << 26, topology="ho", beta1=0.9, beta2=0.95, eps=1e-8, weight_decay=0.0,
               loss_scale=1.0, comm_ctas=148, pipeline_depth=2, stream=None, transport="pull", adam_impl="auto",
               comm_impl="tma", inter_gbps=0.0, grad_accum=False, clip_norm=0.0, skip_nonfinite=False, gather_windows=0,
-              fuse_gather=True):
+              fuse_gather="auto"):
     o = paro_opts_t()
     paro_opts_default(C.byref(o))
     o.bucket_elems = int(bucket_elems)
@@ -153,7 +153,7 @@ def make_opts(bucket_elems=1 << 26, topology="ho", beta1=0.9, beta2=0.95, eps=1e
     o.clip_norm = float(clip_norm)
     o.skip_nonfinite = 1 if skip_nonfinite else 0
     o.gather_windows = int(gather_windows)
-    o.fuse_gather = 1 if fuse_gather else 0
+    o.fuse_gather = {"auto": 1, "always": 2, "never": 0, True: 2, False: 0}[fuse_gather]
     o.stream = stream
     return o
 

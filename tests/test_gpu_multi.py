@@ -62,7 +62,8 @@ def test_real_ranks_match_oracle(tmp_path, variant):
         cfg.update({"accum": 3, "topos": ["ho", "two_step"], "transports": ["pull", "push"], "windows": 2,
                     "adam_impl": "tma_store"})
     if variant == "clip":        # two-phase step with an active global-norm clip (NEXT-3)
-        cfg.update({"clip_norm": 0.05, "topos": ["ho", "nccl"], "transports": ["pull"]})
+        cfg.update({"clip_norm": 0.05, "topos": ["ho", "nccl"], "transports": ["pull", "push"],
+                    "fuse_gather": "always"})
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr=127.0.0.1", "--master-port=29517", os.path.join(ROOT, "tests", "dist_worker.py"),
            str(tmp_path), json.dumps(cfg)]

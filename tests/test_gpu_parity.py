@@ -33,7 +33,7 @@ class EmuRun:
 
     def __init__(self, N, M, code, sizes, B, topo="ho", depth=2, wd=0.0, loss_scale=1.0, transport="push",
                  adam_impl="auto", comm_impl="tma", grad_accum=False, mode="emulated", clip_norm=0.0,
-                 skip_nonfinite=False):
+                 skip_nonfinite=False, fuse_gather="auto"):
         paro = _paro()
         if mode == "emulated":
             self.ctx = paro.Context(N, M, mode="emulated", device=0)
@@ -42,7 +42,7 @@ class EmuRun:
         self.pl = paro.Plan(self.ctx, code, sizes, bucket_elems=B, topology=topo, pipeline_depth=depth,
                             weight_decay=wd, loss_scale=loss_scale, transport=transport, adam_impl=adam_impl,
                             comm_impl=comm_impl, grad_accum=grad_accum, clip_norm=clip_norm,
-                            skip_nonfinite=skip_nonfinite)
+                            skip_nonfinite=skip_nonfinite, fuse_gather=fuse_gather)
         self.info = self.pl.info()
         self.N, self.code, self.sizes = N, code, sizes
         n = self.info["os_numel"]
@@ -535,4 +535,29 @@ def test_gather_windows_return_full_parameters(topo, transport):
                     assert ptr == out
                 got = d2h(ptr, n, np.uint16)
                 assert np.array_equal(got, assembled[s0:s0 + n]), (code, b, r)
+        run.close()
+
+
+
+# --------------------------------------------------------------------- fused parameter all-gather
+@pytest.mark.parametrize("N,M", [(8, 4), (8, 2), (8, 1), (4, 4), (6, 3)])
+@pytest.mark.parametrize("transport,adam_impl", [("pull", "auto"), ("push", "lsu"), ("pull", "tma_store")])
+def test_fused_gather_every_strategy(N, M, transport, adam_impl):
+    """fuse_gather = always: the Adam kernel stores the bf16 parameters into the
+    consumers' buffers (AG_E / AG_I / one world ring); bits equal the DP definition
+    and the bytes per link class stay those of the ring."""
+    sizes = ragged_param_sizes() + [N * 64 * 20]
+    B = N * 64 * 6
+    lay = L.Layout(sizes, N, M, B)
+    ref = _dp_reference(lay, 2)
+    for code in S.paro_strategies():
+        run = EmuRun(N, M, code, sizes, B, transport=transport, adam_impl=adam_impl, fuse_gather="always")
+        plain = _paro().Plan(run.ctx, code, sizes, bucket_elems=B, transport=transport, fuse_gather="never")
+        for r in range(N):
+            assert run.pl.send_bytes(r) == plain.send_bytes(r), (code, r)
+        plain.close()
+        for t in (1, 2):
+            run.set_grads(t)
+            run.step(t)
+        _check_against_dp(run, lay, ref)
         run.close()
