@@ -114,6 +114,12 @@ typedef struct {
                           * bits, same bytes per link class).  1 (default): only   *
                           * when no collective rounds run beside Adam (the whole   *
                           * reduction fused too); 2: always; 0: never.             */
+  int copy_engine;       /* 1: collective launches that only copy bits (parameter  *
+                          * all-gathers) run on the copy engines: per round a peer *
+                          * barrier, then cudaMemcpyAsync over NVLink (bidirectional *
+                          * ring traffic measured 770 GB/s/dir for the copy engines *
+                          * vs 660 for SM loads, profiles/r01/p2p_bidir.jsonl).     *
+                          * 0 (default): the rounds kernel.                         */
   int gather_windows;    /* > 0: that many library window slots of bucket_elems    *
                           * bf16 each for paro_gather_window (P = I or G only).    */
   int grad_accum;        /* 1: enable paro_accumulate (gradient accumulation over  *

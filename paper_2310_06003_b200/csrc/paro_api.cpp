@@ -41,13 +41,25 @@ struct paro_ctx {
   int mode = MODE_PLANNER;
   int N = 1, M = 1, rank = 0, device = -1;
   cudaStream_t main = nullptr, comm = nullptr, comp = nullptr;
+  cudaStream_t dma = nullptr;   // copy-engine transfers of pure-copy launches
   ncclComm_t world = nullptr, intra = nullptr, inter = nullptr;
   paro_status_t sticky = PARO_OK;
   std::string sticky_msg;
   int sm_count = 148;
 };
 
+struct CopyOp {
+  void* dst;
+  const void* src;
+  size_t bytes;
+};
+
 struct DevLaunch {
+  // pure-copy launch run by the copy engines (opts.copy_engine): per round a
+  // 1-CTA barrier kernel on the second barrier channel, then cudaMemcpyAsync
+  bool dma = false;
+  std::vector<std::vector<CopyOp>> copies;   // [round] local rank(s)' copies
+  std::vector<uint64_t> round_peers;         // [round] barrier peers before it
   int max_in = 1;          // largest fold input count (TMA stage sizing)
   int64_t bytes = 0;       // bytes the local rank(s) send in this launch
   int64_t round_off = 0;   // index into the plan's DRound array
@@ -64,6 +76,10 @@ struct paro_plan {
   std::vector<char*> region;              // per local rank: device region base
   std::vector<char*> peer_base;           // [N] base as addressable from this process
   uint64_t** d_peer_slot = nullptr;       // real mode
+  uint64_t** d_peer_slot2 = nullptr;      // second barrier channel (copy-engine launches)
+  uint64_t serial2 = 1;
+  unsigned long long arrive_base2 = 0;
+  cudaEvent_t ev_dma = nullptr;
   DRound* d_rounds = nullptr;
   DTask* d_tasks = nullptr;
   std::vector<DevLaunch> red, gat;        // per bucket
@@ -244,6 +260,26 @@ paro_status_t upload_schedule(PlanT* p) {
           if (t.dst.rank != x && (ctx->mode != MODE_REAL || x == ctx->rank)) dl.bytes += 2 * t.n;
         }
     dl.final_peers = (ctx->mode == MODE_REAL) ? L.barrier_peers(R, ctx->rank) : 0;
+    // copy engines: every task a plain 1-input bit copy
+    bool pure = p->opts.copy_engine != 0 && R > 0;
+    for (int r = 0; r < R && pure; ++r)
+      for (int x = 0; x < pl.N && pure; ++x)
+        for (const Task& t : L.rounds[r][x]) pure = pure && t.nin == 1 && t.in[0].kind != BUF_GRAD;
+    if (pure) {
+      dl.dma = true;
+      dl.copies.assign(R, {});
+      dl.round_peers.assign(R, 0);
+      for (int r = 0; r < R; ++r) {
+        for (int x = 0; x < pl.N; ++x) {
+          if (ctx->mode == MODE_REAL && x != ctx->rank) continue;
+          for (const Task& t : L.rounds[r][x]) {
+            const DTask d = resolve(p, t, x, -1, win_shift);
+            dl.copies[r].push_back({d.dst, d.in[0], (size_t)t.n * 2});
+          }
+        }
+        dl.round_peers[r] = (ctx->mode == MODE_REAL) ? L.barrier_peers(r, ctx->rank) : 0;
+      }
+    }
     return dl;
   };
   p->red.clear();
@@ -298,9 +334,46 @@ int comm_grid(const PlanT* p) {
   return g;
 }
 
+// 1-CTA peer barrier on the second channel (stream s), for copy-engine launches.
+paro_status_t barrier2(PlanT* p, uint64_t peers, cudaStream_t s, int* nlaunch) {
+  paro_ctx* ctx = p->ctx;
+  if (ctx->mode != MODE_REAL || !peers) return PARO_OK;
+  char* hdr = p->region[0];
+  RoundsArgs a{};
+  a.nrounds = 0;
+  a.final_barrier = 1;
+  a.final_peers = peers;
+  a.serial = p->serial2++;
+  a.arrive_base = p->arrive_base2;
+  a.bar.peer_slot = p->d_peer_slot2;
+  a.bar.my_flags = reinterpret_cast<uint64_t*>(hdr + 1024);
+  a.bar.arrive = reinterpret_cast<unsigned long long*>(hdr + 1536);
+  a.bar.err = reinterpret_cast<int*>(hdr + 520);
+  p->arrive_base2 += 1;
+  CK(launch_rounds(a, 1, 32, s));
+  ++*nlaunch;
+  return PARO_OK;
+}
+
+// A pure-copy launch on the copy engines: barrier with the round's peers, then
+// one cudaMemcpyAsync per copy (peer memory is mapped: NVLink P2P DMA).
+paro_status_t run_dma_launch(PlanT* p, const DevLaunch& dl, cudaStream_t s, int* nlaunch) {
+  paro_ctx* ctx = p->ctx;
+  for (size_t r = 0; r < dl.copies.size(); ++r) {
+    paro_status_t st = barrier2(p, dl.round_peers[r], s, nlaunch);
+    if (st != PARO_OK) return st;
+    const int k = prof_begin(p, s, 1, r == 0 ? dl.bytes : 0);
+    for (const CopyOp& c : dl.copies[r]) CK(cudaMemcpyAsync(c.dst, c.src, c.bytes, cudaMemcpyDeviceToDevice, s));
+    prof_end(p, s, k);
+  }
+  if (dl.final_barrier) return barrier2(p, dl.final_peers, s, nlaunch);
+  return PARO_OK;
+}
+
 // Launch one collective (reduce or gather of one bucket) on the comm stream.
 paro_status_t run_launch(PlanT* p, const DevLaunch& dl, int* nlaunch) {
   paro_ctx* ctx = p->ctx;
+  if (dl.dma) return run_dma_launch(p, dl, ctx->comm, nlaunch);
   if (dl.nrounds == 0 && (!dl.final_barrier || ctx->mode != MODE_REAL)) return PARO_OK;
   const int grid = comm_grid(p);
   RoundsArgs a{};
@@ -420,6 +493,7 @@ void destroy_plan(PlanT* p) {
     }
     for (char* r : p->region) cudaFree(r);
     cudaFree(p->d_peer_slot);
+    cudaFree(p->d_peer_slot2);
     cudaFree(p->d_rounds);
     cudaFree(p->d_tasks);
     cudaFree(p->d_partials);
@@ -429,7 +503,7 @@ void destroy_plan(PlanT* p) {
     cudaFree(p->d_skip);
     cudaFree(p->d_pack);
     if (p->h_pack) cudaFreeHost(p->h_pack);
-    for (cudaEvent_t e : {p->ev_fork, p->ev_comm, p->ev_comp, p->ev_pack_staged, p->ev_unpack_staged})
+    for (cudaEvent_t e : {p->ev_fork, p->ev_comm, p->ev_comp, p->ev_pack_staged, p->ev_unpack_staged, p->ev_dma})
       if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : p->prof_ev) cudaEventDestroy(e);
     cudaFree(p->d_trace);
@@ -449,6 +523,7 @@ paro_status_t make_streams(paro_ctx* ctx) {
   CK(cudaStreamCreateWithFlags(&ctx->main, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithPriority(&ctx->comm, cudaStreamNonBlocking, hi));  // collectives first
   CK(cudaStreamCreateWithFlags(&ctx->comp, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithPriority(&ctx->dma, cudaStreamNonBlocking, hi));
   return PARO_OK;
 }
 
@@ -482,6 +557,7 @@ void paro_opts_default(paro_opts_t* o) {
   o->skip_nonfinite = 0;
   o->gather_windows = 0;
   o->fuse_gather = 1;
+  o->copy_engine = 0;
   o->stream = nullptr;
 }
 
@@ -569,7 +645,7 @@ paro_status_t paro_finalize(paro_ctx_t ctx) {
     if (ctx->intra) ncclCommDestroy(ctx->intra);
     if (ctx->inter) ncclCommDestroy(ctx->inter);
     if (ctx->world) ncclCommDestroy(ctx->world);
-    for (cudaStream_t s : {ctx->main, ctx->comm, ctx->comp})
+    for (cudaStream_t s : {ctx->main, ctx->comm, ctx->comp, ctx->dma})
       if (s) cudaStreamDestroy(s);
   }
   delete ctx;
@@ -665,6 +741,9 @@ paro_status_t paro_plan(paro_ctx_t ctx, const char* strategy, const int64_t* par
     for (int x = 0; x < N; ++x) slots[x] = reinterpret_cast<uint64_t*>(p->peer_base[x]) + ctx->rank;
     PCK(cudaMalloc(&p->d_peer_slot, 64 * sizeof(uint64_t*)));
     PCK(cudaMemcpy(p->d_peer_slot, slots.data(), 64 * sizeof(uint64_t*), cudaMemcpyHostToDevice));
+    for (int x = 0; x < N; ++x) slots[x] = reinterpret_cast<uint64_t*>(p->peer_base[x] + 1024) + ctx->rank;
+    PCK(cudaMalloc(&p->d_peer_slot2, 64 * sizeof(uint64_t*)));
+    PCK(cudaMemcpy(p->d_peer_slot2, slots.data(), 64 * sizeof(uint64_t*), cudaMemcpyHostToDevice));
   }
   {
     paro_status_t s2 = upload_schedule(p);
@@ -683,7 +762,8 @@ paro_status_t paro_plan(paro_ctx_t ctx, const char* strategy, const int64_t* par
   p->pack_cap = std::max(1, n_params) * (int)p->local.size();
   PCK(cudaMalloc(&p->d_pack, 2 * sizeof(PackEntry) * p->pack_cap));   // [pack | unpack]
   PCK(cudaHostAlloc(&p->h_pack, 2 * sizeof(PackEntry) * p->pack_cap, cudaHostAllocDefault));
-  for (cudaEvent_t* e : {&p->ev_fork, &p->ev_comm, &p->ev_comp, &p->ev_pack_staged, &p->ev_unpack_staged})
+  for (cudaEvent_t* e : {&p->ev_fork, &p->ev_comm, &p->ev_comp, &p->ev_pack_staged, &p->ev_unpack_staged,
+                        &p->ev_dma})
     PCK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
   p->ev_red.resize(nb);
   p->ev_adam.resize(nb);
@@ -1008,7 +1088,13 @@ paro_status_t paro_step(paro_plan_t p, const void* const* grads, void* const* pa
   } else {
     const int D = std::max(1, p->opts.pipeline_depth);
     const bool nccl = pl.opt.topology == PARO_TOPO_NCCL;
+    bool dma_used = false;
     auto do_gather = [&](int b) -> paro_status_t {
+      if (p->gat[b].dma) {   // copy engines, off the comm stream: overlaps the next reductions
+        CK(cudaStreamWaitEvent(ctx->dma, p->ev_adam[b], 0));
+        dma_used = true;
+        return run_dma_launch(p, p->gat[b], ctx->dma, &launches);
+      }
       CK(cudaStreamWaitEvent(ctx->comm, p->ev_adam[b], 0));
       if (nccl) {
         const int k = prof_begin(p, ctx->comm, 1, 0);
@@ -1071,6 +1157,10 @@ paro_status_t paro_step(paro_plan_t p, const void* const* grads, void* const* pa
     for (int b = std::max(0, nb - D); b < nb; ++b) {
       paro_status_t s5 = do_gather(b);
       if (s5 != PARO_OK) return s5;
+    }
+    if (dma_used) {   // the step-end barrier comes after every copy-engine transfer
+      CK(cudaEventRecord(p->ev_dma, ctx->dma));
+      CK(cudaStreamWaitEvent(ctx->comm, p->ev_dma, 0));
     }
     if (!two) {
       paro_status_t s6 = norm_reduce();

@@ -46,7 +46,7 @@ class paro_opts_t(C.Structure):
                 ("loss_scale", C.c_float), ("comm_ctas", C.c_int), ("pipeline_depth", C.c_int),
                 ("pull_transport", C.c_int), ("adam_impl", C.c_int), ("comm_impl", C.c_int),
                 ("inter_gbps", C.c_float), ("clip_norm", C.c_float), ("skip_nonfinite", C.c_int),
-                ("fuse_gather", C.c_int), ("gather_windows", C.c_int), ("grad_accum", C.c_int),
+                ("fuse_gather", C.c_int), ("copy_engine", C.c_int), ("gather_windows", C.c_int), ("grad_accum", C.c_int),
                 ("stream", C.c_void_p)]
 
 
@@ -137,7 +137,7 @@ def check(status):
 def make_opts(bucket_elems=1 << 26, topology="ho", beta1=0.9, beta2=0.95, eps=1e-8, weight_decay=0.0,
               loss_scale=1.0, comm_ctas=148, pipeline_depth=2, stream=None, transport="pull", adam_impl="auto",
               comm_impl="tma", inter_gbps=0.0, grad_accum=False, clip_norm=0.0, skip_nonfinite=False, gather_windows=0,
-              fuse_gather="auto"):
+              fuse_gather="auto", copy_engine=False):
     o = paro_opts_t()
     paro_opts_default(C.byref(o))
     o.bucket_elems = int(bucket_elems)
@@ -154,6 +154,7 @@ def make_opts(bucket_elems=1 << 26, topology="ho", beta1=0.9, beta2=0.95, eps=1e
     o.skip_nonfinite = 1 if skip_nonfinite else 0
     o.gather_windows = int(gather_windows)
     o.fuse_gather = {"auto": 1, "always": 2, "never": 0, True: 2, False: 0}[fuse_gather]
+    o.copy_engine = 1 if copy_engine else 0
     o.stream = stream
     return o
 

@@ -42,6 +42,7 @@ def main():
     windows = cfg.get("windows", 0)      # > 0: also gather every bucket through paro_gather_window
     adam_impl = cfg.get("adam_impl", "auto")
     fuse_gather = cfg.get("fuse_gather", "auto")
+    copy_engine = cfg.get("copy_engine", False)
     for M in splits:
         uid = paro.unique_id() if rank == 0 else bytes(128)
         t = torch.tensor(list(uid), dtype=torch.uint8)
@@ -51,7 +52,8 @@ def main():
             if True:
                 pl = paro.Plan(ctx, code, sizes, bucket_elems=B, topology=topo, transport=tr, comm_impl=comm_impl,
                                inter_gbps=inter_gbps, grad_accum=accum > 0, clip_norm=clip,
-                               gather_windows=windows, adam_impl=adam_impl, fuse_gather=fuse_gather)
+                               gather_windows=windows, adam_impl=adam_impl, fuse_gather=fuse_gather,
+                               copy_engine=copy_engine)
                 info = pl.info()
                 st = [torch.empty(info["os_numel"], dtype=torch.float32, device="cuda") for _ in range(3)]
                 ptrs = [[x.data_ptr() for x in st]]

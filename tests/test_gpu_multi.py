@@ -49,7 +49,7 @@ CODES = ["NNN", "NNI", "NNG", "NII", "NIG", "NGG", "INI", "ING", "III", "IIG", "
 
 
 @pytest.mark.skipif(_ngpu() < 2, reason="needs >= 2 GPUs")
-@pytest.mark.parametrize("variant", ["default", "paced_lsu", "accum", "clip"])
+@pytest.mark.parametrize("variant", ["default", "paced_lsu", "accum", "clip", "copy_engine"])
 def test_real_ranks_match_oracle(tmp_path, variant):
     world = min(_ngpu(), 4)
     splits = [m for m in range(1, world + 1) if world % m == 0]
@@ -61,6 +61,9 @@ def test_real_ranks_match_oracle(tmp_path, variant):
     if variant == "accum":       # gradient accumulation, s = 3 micro-batches per step (NEXT-1)
         cfg.update({"accum": 3, "topos": ["ho", "two_step"], "transports": ["pull", "push"], "windows": 2,
                     "adam_impl": "tma_store"})
+    if variant == "copy_engine":   # all-gathers on the copy engines (barrier kernel + cudaMemcpyAsync)
+        cfg.update({"topos": ["ho", "two_step", "h_ring"], "transports": ["pull"], "fuse_gather": "never",
+                    "copy_engine": True, "windows": 2})
     if variant == "clip":        # two-phase step with an active global-norm clip (NEXT-3)
         cfg.update({"clip_norm": 0.05, "topos": ["ho", "nccl"], "transports": ["pull", "push"],
                     "fuse_gather": "always"})

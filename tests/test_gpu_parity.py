@@ -33,7 +33,7 @@ class EmuRun:
 
     def __init__(self, N, M, code, sizes, B, topo="ho", depth=2, wd=0.0, loss_scale=1.0, transport="push",
                  adam_impl="auto", comm_impl="tma", grad_accum=False, mode="emulated", clip_norm=0.0,
-                 skip_nonfinite=False, fuse_gather="auto"):
+                 skip_nonfinite=False, fuse_gather="auto", copy_engine=False):
         paro = _paro()
         if mode == "emulated":
             self.ctx = paro.Context(N, M, mode="emulated", device=0)
@@ -42,7 +42,7 @@ class EmuRun:
         self.pl = paro.Plan(self.ctx, code, sizes, bucket_elems=B, topology=topo, pipeline_depth=depth,
                             weight_decay=wd, loss_scale=loss_scale, transport=transport, adam_impl=adam_impl,
                             comm_impl=comm_impl, grad_accum=grad_accum, clip_norm=clip_norm,
-                            skip_nonfinite=skip_nonfinite, fuse_gather=fuse_gather)
+                            skip_nonfinite=skip_nonfinite, fuse_gather=fuse_gather, copy_engine=copy_engine)
         self.info = self.pl.info()
         self.N, self.code, self.sizes = N, code, sizes
         n = self.info["os_numel"]
@@ -559,5 +559,26 @@ def test_fused_gather_every_strategy(N, M, transport, adam_impl):
         for t in (1, 2):
             run.set_grads(t)
             run.step(t)
+        _check_against_dp(run, lay, ref)
+        run.close()
+
+
+
+# --------------------------------------------------------------------- copy-engine all-gathers
+@pytest.mark.parametrize("topo", ["ho", "two_step", "h_ring", "flat"])
+def test_copy_engine_gathers_every_strategy(topo):
+    N, M = 8, 4
+    sizes = ragged_param_sizes() + [N * 64 * 20]
+    B = N * 64 * 6
+    lay = L.Layout(sizes, N, M, B)
+    ref = _dp_reference(lay, 2)
+    for code in S.paro_strategies():
+        run = EmuRun(N, M, code, sizes, B, topo=topo, transport="pull", fuse_gather="never", copy_engine=True)
+        for t in (1, 2):
+            run.set_grads(t)
+            run.step(t)
+        if topo == "flat":
+            run.close()
+            continue
         _check_against_dp(run, lay, ref)
         run.close()

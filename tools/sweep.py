@@ -31,7 +31,8 @@ def main():
                     help="time paro_collective(reduce) + paro_collective(gather) per step, no Adam")
     a = ap.parse_args()
     grid = {"strategy": ["IIG"], "topology": ["ho"], "transport": ["pull"], "comm_ctas": [148],
-            "bucket": [1 << 26], "depth": [2], "adam_impl": ["auto"], "comm_impl": ["tma"], "fuse_gather": ["auto"]}
+            "bucket": [1 << 26], "depth": [2], "adam_impl": ["auto"], "comm_impl": ["tma"], "fuse_gather": ["auto"],
+            "copy_engine": [0]}
     grid.update(json.loads(a.grid))
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -59,7 +60,8 @@ def main():
             plan = paro.Plan(ctx, cfg["strategy"], sizes, bucket_elems=cfg["bucket"], topology=cfg["topology"],
                              comm_ctas=cfg["comm_ctas"], pipeline_depth=cfg["depth"], stream=stream.cuda_stream,
                              transport=cfg["transport"], adam_impl=cfg["adam_impl"],
-                             comm_impl=cfg["comm_impl"], fuse_gather={1: "always", 0: "never"}.get(cfg["fuse_gather"], cfg["fuse_gather"]))
+                             comm_impl=cfg["comm_impl"], fuse_gather={1: "always", 0: "never"}.get(cfg["fuse_gather"], cfg["fuse_gather"]),
+                             copy_engine=bool(cfg["copy_engine"]))
         except Exception as e:  # noqa: BLE001
             if rank == 0:
                 print(json.dumps({"cfg": cfg, "error": str(e)}), flush=True)
