@@ -85,6 +85,8 @@ struct paro_plan {
   std::vector<DevLaunch> red, gat;        // per bucket
   std::vector<DevLaunch> acc_first, acc_next, red_acc;   // gradient accumulation (per bucket)
   std::vector<std::vector<DevLaunch>> win;  // [window slot][bucket]: forward/backward parameter gather
+  std::vector<DevLaunch> red_pre, acc_pre;  // copy-engine raw-chunk copies before reduce / accum (per bucket)
+  std::vector<cudaEvent_t> ev_pre;
   int64_t acc_count = 0;                  // micro-batches accumulated since the last step
   bool last_step_acc = false;             // the last step consumed an accumulator
   double* d_partials = nullptr;
@@ -201,7 +203,7 @@ DTask resolve(const PlanT* p, const Task& t, int executing_rank, int acc_kind, i
   const int M = p->pl->M;
   for (int i = 0; i < t.nin; ++i) {
     d.in[i] = reinterpret_cast<const uint16_t*>(ptr_of(t.in[i]));
-    if (t.in[i].kind == BUF_GRAD) d.rawmask |= 1u << i;
+    if (t.in[i].is_raw()) d.rawmask |= 1u << i;
     if (t.in[i].rank / M != executing_rank / M) d.inter += 1;
   }
   d.dst = reinterpret_cast<uint16_t*>(ptr_of(t.dst));
@@ -282,6 +284,25 @@ paro_status_t upload_schedule(PlanT* p) {
     }
     return dl;
   };
+  // copies of raw gradient chunks (no round barriers: the data is immutable in a step)
+  auto build_copies = [&](const Launch& L) {
+    DevLaunch dl;
+    dl.dma = true;
+    dl.copies.assign(L.rounds.size(), {});
+    dl.round_peers.assign(L.rounds.size(), 0);
+    for (size_t r = 0; r < L.rounds.size(); ++r)
+      for (int x = 0; x < pl.N; ++x) {
+        if (ctx->mode == MODE_REAL && x != ctx->rank) continue;
+        for (const Task& t : L.rounds[r][x]) {
+          const DTask d = resolve(p, t, x, -1);
+          dl.copies[r].push_back({d.dst, d.in[0], (size_t)t.n * 2});
+          if (t.in[0].rank != x) dl.bytes += 2 * t.n;
+        }
+      }
+    return dl;
+  };
+  p->red_pre.clear();
+  p->acc_pre.clear();
   p->red.clear();
   p->gat.clear();
   p->acc_first.clear();
@@ -292,6 +313,8 @@ paro_status_t upload_schedule(PlanT* p) {
     p->red.push_back(build(S.reduce, -1));
     p->gat.push_back(build(S.gather, -1));
     for (int w = 0; w < (int)p->win.size(); ++w) p->win[w].push_back(build(S.window, -1, int64_t(w) * pl.B));
+    if (!S.reduce_pre.rounds.empty()) p->red_pre.push_back(build_copies(S.reduce_pre));
+    if (!S.accum_pre.rounds.empty()) p->acc_pre.push_back(build_copies(S.accum_pre));
     if (pl.opt.accum) {
       p->acc_first.push_back(build(S.accum, -1));
       p->acc_next.push_back(build(S.accum, pl.acc_kind));
@@ -508,6 +531,7 @@ void destroy_plan(PlanT* p) {
     for (cudaEvent_t e : p->prof_ev) cudaEventDestroy(e);
     cudaFree(p->d_trace);
     for (cudaEvent_t e : p->ev_red) cudaEventDestroy(e);
+    for (cudaEvent_t e : p->ev_pre) cudaEventDestroy(e);
     for (cudaEvent_t e : p->ev_adam) cudaEventDestroy(e);
   }
   delete p;
@@ -679,6 +703,10 @@ paro_status_t paro_plan(paro_ctx_t ctx, const char* strategy, const int64_t* par
   po.windows = o.gather_windows;
   if (o.fuse_gather < 0 || o.fuse_gather > 2) return fail(PARO_ERR_INVALID, "fuse_gather must be 0, 1 or 2");
   po.fuse_gather = (o.inter_gbps > 0.f || o.topology == PARO_TOPO_NCCL) ? 0 : o.fuse_gather;
+  // paced (emulated-gap) runs keep every transfer in the rounds kernel, which
+  // paces them; the NCCL comparator has no copy-engine path
+  if (o.inter_gbps > 0.f || o.topology == PARO_TOPO_NCCL) o.copy_engine = 0;
+  po.ce_reduce = o.copy_engine != 0;
   auto* p = new PlanT();
   p->ctx = ctx;
   p->opts = o;
@@ -767,8 +795,10 @@ paro_status_t paro_plan(paro_ctx_t ctx, const char* strategy, const int64_t* par
     PCK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
   p->ev_red.resize(nb);
   p->ev_adam.resize(nb);
+  p->ev_pre.resize(nb);
   for (int b = 0; b < nb; ++b) {
     PCK(cudaEventCreateWithFlags(&p->ev_red[b], cudaEventDisableTiming));
+    PCK(cudaEventCreateWithFlags(&p->ev_pre[b], cudaEventDisableTiming));
     PCK(cudaEventCreateWithFlags(&p->ev_adam[b], cudaEventDisableTiming));
   }
   PCK(cudaDeviceSynchronize());
@@ -979,7 +1009,9 @@ paro_status_t paro_step(paro_plan_t p, const void* const* grads, void* const* pa
   // fused parameter all-gather: Adam stores into peers' parameter buffers, so
   // every peer must have entered this step (its reads of last step's
   // parameters are stream-ordered before it) before the first update
-  if (!pl.sched.empty() && !pl.sched[0].param_push.empty()) {
+  // (also before copy-engine reads of the peers' raw gradient chunks)
+  const bool pre_on = !p->red_pre.empty() && n_acc == 0;
+  if ((!pl.sched.empty() && !pl.sched[0].param_push.empty()) || pre_on) {
     paro_status_t s0 = all_peer_barrier(p, &launches);
     if (s0 != PARO_OK) return s0;
   }
@@ -1010,7 +1042,7 @@ paro_status_t paro_step(paro_plan_t p, const void* const* grads, void* const* pa
       for (int i = 0; i < sg.gnin; ++i) {
         const Ref& x = gin[i];
         sg.gin[i] = reinterpret_cast<const uint16_t*>(data_ptr(p, x.rank, x.kind, x.off));
-        if (x.kind == BUF_GRAD) sg.graw |= 1u << i;
+        if (x.is_raw()) sg.graw |= 1u << i;
       }
       sg.master = opt_state[li].master + S0.os_off[r];
       sg.m = opt_state[li].m + S0.os_off[r];
@@ -1089,6 +1121,24 @@ paro_status_t paro_step(paro_plan_t p, const void* const* grads, void* const* pa
     const int D = std::max(1, p->opts.pipeline_depth);
     const bool nccl = pl.opt.topology == PARO_TOPO_NCCL;
     bool dma_used = false;
+    // copy-engine raw-chunk copies of bucket b into landing set b % kStageSets
+    // (after the step-start barrier; set reuse waits for the reduce that read it)
+    auto issue_pre = [&](int b) -> paro_status_t {
+      if (b >= kStageSets) CK(cudaStreamWaitEvent(ctx->dma, p->ev_red[b - kStageSets], 0));
+      paro_status_t st = run_dma_launch(p, p->red_pre[b], ctx->dma, &launches);
+      if (st != PARO_OK) return st;
+      CK(cudaEventRecord(p->ev_pre[b], ctx->dma));
+      dma_used = true;
+      return PARO_OK;
+    };
+    if (pre_on) {
+      CK(cudaEventRecord(p->ev_comm, ctx->comm));
+      CK(cudaStreamWaitEvent(ctx->dma, p->ev_comm, 0));
+      for (int b = 0; b < std::min(kStageSets, nb); ++b) {
+        paro_status_t st = issue_pre(b);
+        if (st != PARO_OK) return st;
+      }
+    }
     auto do_gather = [&](int b) -> paro_status_t {
       if (p->gat[b].dma) {   // copy engines, off the comm stream: overlaps the next reductions
         CK(cudaStreamWaitEvent(ctx->dma, p->ev_adam[b], 0));
@@ -1107,6 +1157,7 @@ paro_status_t paro_step(paro_plan_t p, const void* const* grads, void* const* pa
       return run_launch(p, p->gat[b], &launches);
     };
     auto do_reduce = [&](int b) -> paro_status_t {
+      if (pre_on) CK(cudaStreamWaitEvent(ctx->comm, p->ev_pre[b], 0));
       if (nccl) {
         const int k = prof_begin(p, ctx->comm, 1, 0);
         paro_status_t s3 = run_nccl(p, pl.sched[b].nccl_reduce[ctx->rank]);
@@ -1119,6 +1170,7 @@ paro_status_t paro_step(paro_plan_t p, const void* const* grads, void* const* pa
       }
       CK(cudaEventRecord(p->ev_red[b], ctx->comm));
       CK(cudaStreamWaitEvent(ctx->comp, p->ev_red[b], 0));
+      if (pre_on && b + kStageSets < nb) return issue_pre(b + kStageSets);
       return PARO_OK;
     };
     if (two) {
@@ -1245,7 +1297,16 @@ paro_status_t paro_accumulate(paro_plan_t p, const void* const* grads) {
     if (sp != PARO_OK) return sp;
   }
   const std::vector<DevLaunch>& acc = (p->acc_count == 0) ? p->acc_first : p->acc_next;
+  const bool pre_on = !p->acc_pre.empty();
+  if (pre_on) {   // copy-engine reads of the peers' raw chunks: every peer has its micro-batch in place
+    paro_status_t s0 = all_peer_barrier(p, &launches);
+    if (s0 != PARO_OK) return s0;
+  }
   for (size_t b = 0; b < pl.buckets.size(); ++b) {
+    if (pre_on) {   // serial on the comm stream: the landing set is reused three buckets later
+      paro_status_t s2 = run_dma_launch(p, p->acc_pre[b], ctx->comm, &launches);
+      if (s2 != PARO_OK) return s2;
+    }
     paro_status_t s3 = run_launch(p, acc[b], &launches);
     if (s3 != PARO_OK) return s3;
   }

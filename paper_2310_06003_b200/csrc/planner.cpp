@@ -330,7 +330,8 @@ void Planner::layout() {
   buf_len[BUF_STAGE_E] = (N > 1) ? 2 * kStageSets * stage_e_len : 0;
   buf_len[BUF_P1] = (N > 1) ? kStageSets * p1_len : 0;
   buf_len[BUF_SOWN] = (N > 1) ? kStageSets * sown_len : 0;
-  buf_len[BUF_LAND] = (N > 1 && opt.topology == 3 && opt.push) ? kStageSets * land_len : 0;
+  buf_len[BUF_LAND] = (N > 1 && ((opt.topology == 3 && opt.push) || (opt.ce_reduce && G == LV_I)))
+                          ? kStageSets * land_len : 0;
   buf_len[BUF_GACC] = (opt.accum && G == LV_N) ? psi_pad : 0;
   buf_len[BUF_WIN] = (opt.windows > 0 && P != LV_N && N > 1) ? int64_t(opt.windows) * B : 0;
   acc_kind = !opt.accum ? -1 : (G == LV_N ? BUF_GACC : BUF_GSHARD);
@@ -712,7 +713,30 @@ void Planner::build_schedule() {
     };
 
     // RS_I of the gradients into the G residency.  Returns rounds used.
-    auto emit_rs_i = [&](Launch& L, int round0) -> int {
+    // Copy-engine variant (opt.ce_reduce, pull): the M-1 group peers' raw chunks
+    // are copied into landing slots (`pre`, run by the copy engines: raw
+    // gradients do not change during a step, so no round barrier is needed),
+    // then one local fold in the canonical order R_M(p; y_{p+1}, ..., y_p).
+    auto emit_rs_i = [&](Launch& L, int round0, Launch* pre = nullptr) -> int {
+      if (pre && opt.ce_reduce && M > 1) {
+        pre->n_ranks = N;
+        for (int r = 0; r < N; ++r) {
+          const int j = grp(r), p = pos(r);
+          Task t;
+          t.n = chunk;
+          t.nin = M;
+          for (int i = 0; i < M - 1; ++i) {
+            Ref land = land_i(r, i);
+            land.raw = true;
+            pre->add(0, r, make_task(chunk, {grad(rank_of(j, (p + 1 + i) % M), int64_t(p) * chunk)}, land));
+            t.in[i] = land;
+          }
+          t.in[M - 1] = grad(r, int64_t(p) * chunk);
+          t.dst = gshard(r, 0);
+          L.add(round0, r, t);
+        }
+        return 1;
+      }
       int r1 = 0;
       for (int j = 0; j < g; ++j) {
         auto gr = group_ranks(j);
@@ -745,7 +769,7 @@ void Planner::build_schedule() {
     if (N > 1 && topo != 4) {
       Launch& L = S.reduce;
       if (G == LV_I) {
-        emit_rs_e(L, emit_rs_i(L, 0));
+        emit_rs_e(L, emit_rs_i(L, 0, &S.reduce_pre));
       } else {
         emit_world_reduce(L);
       }
@@ -755,7 +779,7 @@ void Planner::build_schedule() {
         if (G == LV_G) {
           emit_world_rs(S.accum, 0);          // lands in the G residency (dest_seg)
         } else if (G == LV_I) {
-          emit_rs_i(S.accum, 0);
+          emit_rs_i(S.accum, 0, &S.accum_pre);
           emit_rs_e(S.reduce_acc, 0);
         } else {
           for (int r = 0; r < N; ++r) S.accum.add(0, r, make_task(n, {grad(r, 0)}, Ref{r, BUF_GACC, s}));
@@ -941,7 +965,7 @@ void Planner::validate_refs() const {
   };
   for (size_t b = 0; b < sched.size(); ++b) {
     const BucketSchedule& S = sched[b];
-    for (const Launch* L : {&S.reduce, &S.gather, &S.accum, &S.reduce_acc, &S.window})
+    for (const Launch* L : {&S.reduce, &S.gather, &S.accum, &S.reduce_acc, &S.window, &S.reduce_pre, &S.accum_pre})
       for (const auto& rnd : L->rounds)
         for (const auto& v : rnd)
           for (const Task& t : v) {
@@ -1008,10 +1032,10 @@ void Planner::count_bytes() {
       ++n_comm_launches;
       n_rounds += (int)L->rounds.size();
     }
-    count({&S.reduce, &S.gather}, &S.ghat_in, S.os_len, send_intra, send_inter, &S.param_push);
+    count({&S.reduce_pre, &S.reduce, &S.gather}, &S.ghat_in, S.os_len, send_intra, send_inter, &S.param_push);
     count({&S.window}, nullptr, 0, win_send_intra, win_send_inter);
     if (opt.accum) {
-      count({&S.accum}, nullptr, 0, acc_send_intra, acc_send_inter);
+      count({&S.accum_pre, &S.accum}, nullptr, 0, acc_send_intra, acc_send_inter);
       count({&S.reduce_acc, &S.gather}, &S.ghat_in_acc, S.os_len, accstep_send_intra, accstep_send_inter,
             &S.param_push);
     }

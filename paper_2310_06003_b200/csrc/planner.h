@@ -42,6 +42,8 @@ struct Ref {
   int32_t rank = -1;
   int32_t kind = -1;
   int64_t off = 0;           // element offset inside the buffer kind
+  bool raw = false;          // holds raw gradient bits (copied): scaled 1/N when read
+  bool is_raw() const { return raw || kind == BUF_GRAD; }
 };
 
 // dst = (((in0 (+) in1) (+) in2) ...), (+) = RNE_bf16(fp32 + fp32); inputs
@@ -101,6 +103,9 @@ struct BucketSchedule {
   // peers' parameter buffers (same offset: the layouts are symmetric), which
   // replaces the gather launch when the consumers are one ring's members
   std::vector<std::vector<Ref>> param_push;
+  // copy-engine transport (opt.ce_reduce): raw gradient chunks of the group
+  // peers copied into landing slots before `reduce` / `accum` fold them locally
+  Launch reduce_pre, accum_pre;
 };
 
 struct PlanOptions {
@@ -112,6 +117,7 @@ struct PlanOptions {
   bool accum = false;        // build the gradient-accumulation launches (s > 1)
   bool two_phase = false;    // clipping / skip: every bucket's g_hat stays resident until Adam (R28)
   int windows = 0;           // parameter-gather window slots (0: none)
+  bool ce_reduce = false;    // G = I: RS_I as copy-engine copies of raw chunks + one local fold
   int fuse_gather = 1;       // fold a one-ring parameter all-gather into Adam's stores:
                              // 0 never, 1 when no collective rounds co-run, 2 always
 };

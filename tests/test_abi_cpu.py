@@ -99,8 +99,9 @@ def test_send_bytes_match_oracle_simulator(N, M):
     w0 = master_f32(0, lay.psi)
     ctx = paro.Context(N, M)
     for code in S.paro_strategies():
-        for topo, tr in [(a, b) for a in ("ho", "two_step", "flat", "h_ring") for b in ("push", "pull")]:
-            pl = paro.Plan(ctx, code, sizes, bucket_elems=B, topology=topo, transport=tr)
+        for topo, tr, ce in [(a, b, c) for a in ("ho", "two_step", "flat", "h_ring") for b in ("push", "pull")
+                             for c in (False, True)]:
+            pl = paro.Plan(ctx, code, sizes, bucket_elems=B, topology=topo, transport=tr, copy_engine=ce)
             res = ST.strategy_step(code, lay, grads, ST.init_state(w0, lay, code), nm.AdamScalars(1e-3, 1),
                                    topology=topo)
             for r in range(N):
@@ -149,8 +150,10 @@ def test_accumulation_bytes_match_oracle_simulator(N, M):
     zero = [np.zeros(lay.psi, np.uint16) for _ in range(N)]
     ctx = paro.Context(N, M)
     for code in S.paro_strategies():
-        for topo, tr in [("ho", "pull"), ("ho", "push"), ("two_step", "pull"), ("flat", "pull"), ("direct", "push")]:
-            pl = paro.Plan(ctx, code, sizes, bucket_elems=B, topology=topo, transport=tr, grad_accum=True)
+        for topo, tr, ce in [("ho", "pull", False), ("ho", "push", False), ("two_step", "pull", False),
+                             ("flat", "pull", False), ("direct", "push", False), ("ho", "pull", True)]:
+            pl = paro.Plan(ctx, code, sizes, bucket_elems=B, topology=topo, transport=tr, grad_accum=True,
+                           copy_engine=ce)
             for s in (1, 3):
                 res = ST.strategy_accum_step(code, lay, [zero] * s, ST.init_state(w0, lay, code),
                                              nm.AdamScalars(1e-3, 1, accum_steps=s),

@@ -321,7 +321,7 @@ def _run_accum(run, steps, s):
 
 
 @pytest.mark.parametrize("topo,transport", [("ho", "pull"), ("ho", "push"), ("two_step", "pull"),
-                                            ("direct", "pull")])
+                                            ("direct", "pull"), ("ho", "ce")])
 def test_accumulation_every_strategy_2x4(topo, transport):
     """BASELINE config 1 shape (2 groups x 4, 16 buckets) with s = 3 micro-batches,
     two mini-batch steps: every strategy bit-exact vs dp_accum_step (R27)."""
@@ -331,7 +331,9 @@ def test_accumulation_every_strategy_2x4(topo, transport):
     lay = L.Layout(sizes, N, M, B)
     refs = {gl: _accum_reference(lay, 2, s, gl) for gl in "NIG"}
     for code in S.paro_strategies():
-        run = EmuRun(N, M, code, sizes, B, topo=topo, transport=transport, grad_accum=True)
+        ce = transport == "ce"
+        run = EmuRun(N, M, code, sizes, B, topo=topo, transport="pull" if ce else transport, grad_accum=True,
+                     copy_engine=ce)
         stats = _run_accum(run, 2, s)
         ref = refs[code[1]]
         _check_against_dp(run, lay, ref)
