@@ -118,8 +118,11 @@ typedef struct {
                           * all-gathers) run on the copy engines: per round a peer *
                           * barrier, then cudaMemcpyAsync over NVLink (bidirectional *
                           * ring traffic measured 770 GB/s/dir for the copy engines *
-                          * vs 660 for SM loads, profiles/r01/p2p_bidir.jsonl).     *
-                          * 0 (default): the rounds kernel.                         */
+                          * vs 660 for SM loads, profiles/r01/p2p_bidir.jsonl);     *
+                          * 2: also G = I's intra reduce-scatter as copy-engine     *
+                          * copies of the peers' raw chunks + one local fold.       *
+                          * 0 (default): the rounds kernel (measured fastest in the *
+                          * full step at 2x2, profiles/r01/sweep_copy_engine_2x2). */
   int gather_windows;    /* > 0: that many library window slots of bucket_elems    *
                           * bf16 each for paro_gather_window (P = I or G only).    */
   int grad_accum;        /* 1: enable paro_accumulate (gradient accumulation over  *

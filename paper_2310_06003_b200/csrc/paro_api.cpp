@@ -706,7 +706,8 @@ paro_status_t paro_plan(paro_ctx_t ctx, const char* strategy, const int64_t* par
   // paced (emulated-gap) runs keep every transfer in the rounds kernel, which
   // paces them; the NCCL comparator has no copy-engine path
   if (o.inter_gbps > 0.f || o.topology == PARO_TOPO_NCCL) o.copy_engine = 0;
-  po.ce_reduce = o.copy_engine != 0;
+  if (o.copy_engine < 0 || o.copy_engine > 2) return fail(PARO_ERR_INVALID, "copy_engine must be 0, 1 or 2");
+  po.ce_reduce = o.copy_engine == 2;
   auto* p = new PlanT();
   p->ctx = ctx;
   p->opts = o;

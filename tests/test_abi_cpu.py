@@ -100,7 +100,7 @@ def test_send_bytes_match_oracle_simulator(N, M):
     ctx = paro.Context(N, M)
     for code in S.paro_strategies():
         for topo, tr, ce in [(a, b, c) for a in ("ho", "two_step", "flat", "h_ring") for b in ("push", "pull")
-                             for c in (False, True)]:
+                             for c in (False, "gathers", "all")]:
             pl = paro.Plan(ctx, code, sizes, bucket_elems=B, topology=topo, transport=tr, copy_engine=ce)
             res = ST.strategy_step(code, lay, grads, ST.init_state(w0, lay, code), nm.AdamScalars(1e-3, 1),
                                    topology=topo)
@@ -151,9 +151,9 @@ def test_accumulation_bytes_match_oracle_simulator(N, M):
     ctx = paro.Context(N, M)
     for code in S.paro_strategies():
         for topo, tr, ce in [("ho", "pull", False), ("ho", "push", False), ("two_step", "pull", False),
-                             ("flat", "pull", False), ("direct", "push", False), ("ho", "pull", True)]:
+                             ("flat", "pull", False), ("direct", "push", False), ("ho", "pull", "all")]:
             pl = paro.Plan(ctx, code, sizes, bucket_elems=B, topology=topo, transport=tr, grad_accum=True,
-                           copy_engine=ce)
+                           copy_engine="all" if ce else False)
             for s in (1, 3):
                 res = ST.strategy_accum_step(code, lay, [zero] * s, ST.init_state(w0, lay, code),
                                              nm.AdamScalars(1e-3, 1, accum_steps=s),

@@ -63,7 +63,7 @@ def test_real_ranks_match_oracle(tmp_path, variant):
                     "adam_impl": "tma_store"})
     if variant == "copy_engine":   # all-gathers on the copy engines (barrier kernel + cudaMemcpyAsync)
         cfg.update({"topos": ["ho", "two_step", "h_ring"], "transports": ["pull"], "fuse_gather": "never",
-                    "copy_engine": True, "windows": 2})
+                    "copy_engine": "all", "windows": 2})
     if variant == "clip":        # two-phase step with an active global-norm clip (NEXT-3)
         cfg.update({"clip_norm": 0.05, "topos": ["ho", "nccl"], "transports": ["pull", "push"],
                     "fuse_gather": "always"})

@@ -333,7 +333,7 @@ def test_accumulation_every_strategy_2x4(topo, transport):
     for code in S.paro_strategies():
         ce = transport == "ce"
         run = EmuRun(N, M, code, sizes, B, topo=topo, transport="pull" if ce else transport, grad_accum=True,
-                     copy_engine=ce)
+                     copy_engine="all" if ce else False)
         stats = _run_accum(run, 2, s)
         ref = refs[code[1]]
         _check_against_dp(run, lay, ref)
@@ -567,15 +567,16 @@ def test_fused_gather_every_strategy(N, M, transport, adam_impl):
 
 
 # --------------------------------------------------------------------- copy-engine all-gathers
+@pytest.mark.parametrize("ce", ["gathers", "all"])
 @pytest.mark.parametrize("topo", ["ho", "two_step", "h_ring", "flat"])
-def test_copy_engine_gathers_every_strategy(topo):
+def test_copy_engine_gathers_every_strategy(topo, ce):
     N, M = 8, 4
     sizes = ragged_param_sizes() + [N * 64 * 20]
     B = N * 64 * 6
     lay = L.Layout(sizes, N, M, B)
     ref = _dp_reference(lay, 2)
     for code in S.paro_strategies():
-        run = EmuRun(N, M, code, sizes, B, topo=topo, transport="pull", fuse_gather="never", copy_engine=True)
+        run = EmuRun(N, M, code, sizes, B, topo=topo, transport="pull", fuse_gather="never", copy_engine=ce)
         for t in (1, 2):
             run.set_grads(t)
             run.step(t)
