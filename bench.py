@@ -33,7 +33,7 @@ METRIC = "params/s per sync+update step"
 LR = 3e-4
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
@@ -54,7 +54,15 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    return ap.parse_args()
+    return ap.parse_args(argv)
+
+
+def plan_kwargs(args, stream):
+    """paro.Plan options of the timed launch configuration (shared with the
+    full-size parity tests, so they check exactly what is timed)."""
+    return dict(bucket_elems=args.bucket, topology=args.topology, comm_ctas=args.comm_ctas,
+                pipeline_depth=args.depth, stream=stream, transport=args.transport, adam_impl=args.adam_impl,
+                comm_impl=args.comm_impl, fuse_gather=args.fuse_gather)
 
 
 def default_group(N):
@@ -211,10 +219,7 @@ def run_ours(args):
     sizes = llama_param_sizes(args.model)
     stream = torch.cuda.Stream()          # a real (non-legacy) stream the steps are ordered on
     torch.cuda.set_stream(stream)
-    plan = paro.Plan(ctx, args.strategy, sizes, bucket_elems=args.bucket, topology=args.topology,
-                     comm_ctas=args.comm_ctas, pipeline_depth=args.depth, stream=stream.cuda_stream,
-                     transport=args.transport, adam_impl=args.adam_impl, comm_impl=args.comm_impl,
-                     fuse_gather=args.fuse_gather)
+    plan = paro.Plan(ctx, args.strategy, sizes, **plan_kwargs(args, stream.cuda_stream))
     info = plan.info()
     st = [torch.empty(info["os_numel"], dtype=torch.float32, device="cuda") for _ in range(3)]
     ptrs = [[t.data_ptr() for t in st]]

@@ -343,6 +343,43 @@ const char* paro_last_error(void);
 /* Library version string ("paro-b200 <semver> sm_100a"). */
 const char* paro_version(void);
 
+/* ---- strategy advisor (NEXT-4; reading R29) ----------------------
+ * Table 1 marks the codes recommended for each training type;
+ * §3.1 trades memory (Table 2; P, G, OS take 2Psi, 2Psi',
+ * 12Psi' bytes) against communication (Table 3).  paro_advise evaluates all 14
+ * strategies for one task and returns them ranked: recommended-and-fitting
+ * first, then by modeled communication time, memory, code. */
+typedef struct {
+  int n_gpus, group_size;     /* N and M (M divides N)                                 */
+  int64_t psi;                /* model parameters Psi                           */
+  int64_t psi_trainable;      /* trainable parameters Psi' (0 < Psi' <= Psi)     */
+  int accum_steps;            /* s micro-batches per mini-batch, >= 1           */
+  int peft;                   /* 1: PEFT task (Table 1's last column, Psi' << Psi)      */
+  double mem_budget_bytes;    /* model-state bytes available per GPU                    */
+  double bw_intra_gbs;        /* per-rank intra-group link bandwidth, GB/s              */
+  double bw_inter_gbs;        /* per-rank inter-group link bandwidth, GB/s              */
+} paro_advise_in_t;
+
+typedef struct {
+  char code[4];               /* "IIG", NUL-terminated                                  */
+  int32_t recommended;        /* Table 1 mark in the task's column                      */
+  int32_t fits;               /* mem_bytes <= mem_budget_bytes                          */
+  int64_t mem_bytes;          /* 2Psi/div(P) + 2Psi'/div(G) + 12Psi'/div(OS), padded R21 */
+  int64_t intra_bytes;        /* bytes the busiest rank sends per mini-batch: s x       */
+  int64_t inter_bytes;        /*   (fwd + bwd param gather + micro-batch reduction) +   *
+                               *   the update-stage ops, counted from the library's own *
+                               *   plans (HO-Ring topology)                             */
+  double t_comm_s;            /* intra / bw_intra + inter / bw_inter                    */
+} paro_advice_t;
+
+/* Table 1 column of a task: 0 Psi' = Psi, 1 Psi' >= Psi/6, 2 Psi' < Psi/6, 3 PEFT. */
+int paro_table1_column(int64_t psi, int64_t psi_trainable, int peft);
+
+/* Fill out[0..13] (cap >= 14) with every PaRO strategy, best first; *n_out = 14.
+ * Host only (no context needed).  PARO_ERR_INVALID on a bad cluster shape,
+ * sizes, accum_steps < 1 or non-positive bandwidths. */
+paro_status_t paro_advise(const paro_advise_in_t* in, paro_advice_t* out, int cap, int* n_out);
+
 #ifdef __cplusplus
 }
 #endif

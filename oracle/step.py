@@ -76,6 +76,24 @@ def dp_reduce(lay: Layout, grads):
     return ghat
 
 
+def dp_reduce_window(lay: Layout, grad_of, a, b):
+    """dp_reduce restricted to flat elements [a, b) (sampled parity at full size).
+
+    The definition is elementwise, so a window needs only its own inputs:
+    grad_of(r, a, n) returns rank r's bf16 gradient bits for [a, a + n).  The
+    window must lie inside one global segment (the fold order depends on the
+    owner (j, p) of the segment, R1/R2).  Pinned against dp_reduce.
+    """
+    N = lay.N
+    geo = C.Geometry(N, lay.M)
+    j, p = lay.owner_segment(a)
+    if lay.owner_segment(b - 1) != (j, p):
+        raise ValueError("window crosses a segment boundary")
+    X = [pack(np.asarray(grad_of(r, a, b - a), np.uint16), 1.0 / N) for r in range(N)]
+    S = [canonical_fold([X[geo.r(jj, pp)] for pp in range(lay.M)], p) for jj in range(geo.g)]
+    return canonical_fold(S, j)
+
+
 def dp_step(lay: Layout, grads, master, m, v, sc: AdamScalars):
     """Unsharded data parallel with the canonical order (full-length arrays, Psi_pad).
 

@@ -37,6 +37,10 @@ enum Mode { MODE_REAL = 0, MODE_EMU = 1, MODE_PLANNER = 2 };
 
 }  // namespace
 
+namespace paro {
+paro_status_t api_fail(paro_status_t st, const std::string& msg) { return fail(st, msg); }
+}  // namespace paro
+
 struct paro_ctx {
   int mode = MODE_PLANNER;
   int N = 1, M = 1, rank = 0, device = -1;

@@ -73,6 +73,17 @@ class paro_profile_t(C.Structure):
                 ("traced_barrier_ms", C.c_double), ("traced_work_ms", C.c_double), ("traced_final_ms", C.c_double)]
 
 
+class paro_advise_in_t(C.Structure):
+    _fields_ = [("n_gpus", C.c_int), ("group_size", C.c_int), ("psi", C.c_int64), ("psi_trainable", C.c_int64),
+                ("accum_steps", C.c_int), ("peft", C.c_int), ("mem_budget_bytes", C.c_double),
+                ("bw_intra_gbs", C.c_double), ("bw_inter_gbs", C.c_double)]
+
+
+class paro_advice_t(C.Structure):
+    _fields_ = [("code", C.c_char * 4), ("recommended", C.c_int32), ("fits", C.c_int32), ("mem_bytes", C.c_int64),
+                ("intra_bytes", C.c_int64), ("inter_bytes", C.c_int64), ("t_comm_s", C.c_double)]
+
+
 _vp = C.c_void_p
 _i64 = C.c_int64
 _st = C.c_int
@@ -115,6 +126,9 @@ paro_plan_destroy = _sig("paro_plan_destroy", _st, _vp)
 paro_collective = _sig("paro_collective", _st, _vp, C.c_int)
 paro_profile_start = _sig("paro_profile_start", _st, _vp, C.c_int)
 paro_profile_stop = _sig("paro_profile_stop", _st, _vp, C.POINTER(paro_profile_t))
+paro_table1_column = _sig("paro_table1_column", C.c_int, _i64, _i64, C.c_int)
+paro_advise = _sig("paro_advise", _st, C.POINTER(paro_advise_in_t), C.POINTER(paro_advice_t), C.c_int,
+                   C.POINTER(C.c_int))
 paro_last_error = _sig("paro_last_error", C.c_char_p)
 paro_version = _sig("paro_version", C.c_char_p)
 
@@ -124,7 +138,8 @@ EXPORTED = ["paro_opts_default", "paro_get_unique_id", "paro_init", "paro_init_e
             "paro_opt_state_init_synth", "paro_synth_grads", "paro_step", "paro_step_stats",
             "paro_plan_destroy", "paro_last_error", "paro_version", "paro_profile_start",
             "paro_profile_stop", "paro_collective", "paro_accumulate",
-            "paro_rank_accum_send_bytes", "paro_gather_window", "paro_rank_gather_send_bytes"]
+            "paro_rank_accum_send_bytes", "paro_gather_window", "paro_rank_gather_send_bytes",
+            "paro_table1_column", "paro_advise"]
 
 
 def check(status):
@@ -157,6 +172,22 @@ def make_opts(bucket_elems=1 << 26, topology="ho", beta1=0.9, beta2=0.95, eps=1e
     o.copy_engine = {False: 0, True: 1, "gathers": 1, "all": 2, 0: 0, 1: 1, 2: 2}[copy_engine]
     o.stream = stream
     return o
+
+
+def advise(n_gpus, group_size, psi, psi_trainable, accum_steps, mem_budget_bytes, bw_intra_gbs, bw_inter_gbs,
+           peft=False):
+    """paro_advise: the 14 strategies ranked for one training task (list of dicts, best first)."""
+    a = paro_advise_in_t(int(n_gpus), int(group_size), int(psi), int(psi_trainable), int(accum_steps),
+                         1 if peft else 0, float(mem_budget_bytes), float(bw_intra_gbs), float(bw_inter_gbs))
+    out = (paro_advice_t * 14)()
+    n = C.c_int()
+    check(paro_advise(C.byref(a), out, 14, C.byref(n)))
+    rows = []
+    for x in out[:n.value]:
+        rows.append({"code": x.code.decode(), "recommended": bool(x.recommended), "fits": bool(x.fits),
+                     "mem_bytes": x.mem_bytes, "intra_bytes": x.intra_bytes, "inter_bytes": x.inter_bytes,
+                     "t_s": x.t_comm_s})
+    return rows
 
 
 def unique_id():

@@ -22,9 +22,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def test_exports_every_declared_symbol():
     hdr = open(os.path.join(ROOT, "include", "paro.h")).read()
-    declared = set(re.findall(r"\b(paro_[a-z_]+)\s*\(", hdr))
+    declared = set(re.findall(r"\b(paro_[a-z0-9_]+)\s*\(", hdr))
     out = subprocess.run(["nm", "-D", "--defined-only", paro.LIB_PATH], capture_output=True, text=True).stdout
-    exported = set(re.findall(r" T (paro_[a-z_]+)$", out, re.M))
+    exported = set(re.findall(r" T (paro_[a-z0-9_]+)$", out, re.M))
     assert declared, "no declarations parsed"
     assert declared <= exported, declared - exported
     assert set(paro.EXPORTED) == declared

@@ -128,3 +128,46 @@ def test_norm_matches_fsum():
         res = ST.strategy_step(code, lay, grads, ST.init_state(w0, lay, code), sc)
         ref = math.fsum((float(x) * 0.25) ** 2 for x in nm.f32_from_bf16_bits(gh))
         assert abs(res.norm_sq - ref) <= 1e-12 * ref
+
+
+@pytest.mark.parametrize("N,M", [(8, 4), (4, 2), (2, 1), (6, 3)])
+def test_reduce_window_equals_full_reduction(N, M):
+    """dp_reduce_window (used by the full-size sampled parity tests) is the
+    elementwise restriction of dp_reduce: every segment window, and ragged
+    sub-windows, give the same bits; a window crossing a segment is refused."""
+    sizes = [N * 64 * 5 + 17, 300]
+    lay = L.Layout(sizes, N, M, N * 64 * 2)
+    grads = [grad_bits(r, 3, 0, lay.psi) for r in range(N)]
+    full = ST.dp_reduce(lay, grads)
+
+    def grad_of(r, a, n):
+        return ST.pad_flat(grads[r], lay.psi_pad, np.uint16)[a:a + n]
+
+    rng = np.random.default_rng(N * 10 + M)
+    for b in range(len(lay.buckets)):
+        for k in range(N):
+            a, e = lay.segment(b, k)
+            assert np.array_equal(ST.dp_reduce_window(lay, grad_of, a, e), full[a:e])
+            x = int(rng.integers(a, e - 1))
+            y = int(rng.integers(x + 1, e + 1))
+            assert np.array_equal(ST.dp_reduce_window(lay, grad_of, x, y), full[x:y])
+    a, e = lay.segment(0, 0)
+    with pytest.raises(ValueError):
+        ST.dp_reduce_window(lay, grad_of, e - 3, e + 3)
+
+
+def test_reduce_window_smallint_mean_at_llama_scale():
+    """At the LLaMA-7B layout (2x4, 2^28 buckets) a window of small-integer
+    gradients reduces to the exact mean (the sum is exact in any order)."""
+    from paro_synth import edge_grad_bits, llama_param_sizes
+    lay = L.Layout(llama_param_sizes("7B"), 8, 4, 1 << 28)
+    b = len(lay.buckets) // 2
+    a, e = lay.segment(b, 5)
+    a, e = a + 1000, a + 1000 + 512
+
+    def grad_of(r, s, n):
+        return edge_grad_bits("smallint", n, rank=r, step=s % 97)
+
+    got = nm.f32_from_bf16_bits(ST.dp_reduce_window(lay, grad_of, a, e)).astype(np.float64)
+    ints = sum(nm.f32_from_bf16_bits(grad_of(r, a, e - a)).astype(np.float64) for r in range(8))
+    assert np.array_equal(got, ints / 8)   # |sum| <= 24: every partial is exact in bf16
