@@ -129,6 +129,16 @@ typedef struct {
                           * s > 1 micro-batches); G = N plans then own  *
                           * a psi_pad bf16 accumulator.  0 (default): off.         */
   void* stream;          /* cudaStream_t the step is ordered on; NULL = ctx stream */
+  int frozen;            /* 1: a frozen-parameter plan (partial / PEFT training:  *
+                          * Psi' < Psi trainable; the frozen tensors keep  *
+                          * only their parameters, 2 bytes each).  It owns *
+                          * the P residency of its tensors and serves            *
+                          * paro_gather_window; paro_step, paro_accumulate,       *
+                          * paro_synth_grads and paro_collective return           *
+                          * PARO_ERR_STATE; paro_opt_state_init* take st = NULL   *
+                          * and only fill the parameter buffer.  Pair it with a   *
+                          * plan of the trainable tensors (paro_plan_masked).    *
+                          * 0 (default).                                          */
 } paro_opts_t;
 
 typedef struct {
@@ -194,6 +204,19 @@ paro_status_t paro_finalize(paro_ctx_t ctx);
  * parameter buffer, G-residency buffer, staging).  Collective in real mode. */
 paro_status_t paro_plan(paro_ctx_t ctx, const char* strategy, const int64_t* param_sizes,
                         int n_params, const paro_opts_t* opts, paro_plan_t* out);
+
+/* Partial / PEFT training ("full, partial, and PEFT"; P:172 Psi' trainable
+ * parameters; P:225 memory 2Psi, 2Psi', 12Psi'): trainable[i] != 0 marks tensor
+ * i trainable.  Creates *out_trainable = paro_plan over the trainable tensors
+ * (in their declaration order; the sync + update step runs on Psi' elements)
+ * and *out_frozen = a frozen-parameter plan (opts->frozen = 1) over the others
+ * (NULL when every tensor is trainable).  Both use `strategy`'s P level, so
+ * every parameter is resident at P and gathered the same way; G and OS exist
+ * for the trainable tensors only.  Collective in real mode.  Errors as
+ * paro_plan; PARO_ERR_INVALID if no tensor is trainable. */
+paro_status_t paro_plan_masked(paro_ctx_t ctx, const char* strategy, const int64_t* param_sizes,
+                               const uint8_t* trainable, int n_params, const paro_opts_t* opts,
+                               paro_plan_t* out_trainable, paro_plan_t* out_frozen);
 
 paro_status_t paro_plan_info(paro_plan_t plan, paro_plan_info_t* out);
 

@@ -587,6 +587,7 @@ void paro_opts_default(paro_opts_t* o) {
   o->fuse_gather = 1;
   o->copy_engine = 0;
   o->stream = nullptr;
+  o->frozen = 0;
 }
 
 paro_status_t paro_get_unique_id(paro_uid_t* out) {
@@ -712,6 +713,7 @@ paro_status_t paro_plan(paro_ctx_t ctx, const char* strategy, const int64_t* par
   if (o.inter_gbps > 0.f || o.topology == PARO_TOPO_NCCL) o.copy_engine = 0;
   if (o.copy_engine < 0 || o.copy_engine > 2) return fail(PARO_ERR_INVALID, "copy_engine must be 0, 1 or 2");
   po.ce_reduce = o.copy_engine == 2;
+  po.params_only = o.frozen != 0;
   auto* p = new PlanT();
   p->ctx = ctx;
   p->opts = o;
@@ -812,6 +814,33 @@ paro_status_t paro_plan(paro_ctx_t ctx, const char* strategy, const int64_t* par
   return PARO_OK;
 }
 
+paro_status_t paro_plan_masked(paro_ctx_t ctx, const char* strategy, const int64_t* param_sizes,
+                               const uint8_t* trainable, int n_params, const paro_opts_t* opts,
+                               paro_plan_t* out_trainable, paro_plan_t* out_frozen) {
+  if (!out_trainable || !out_frozen || !trainable || (n_params > 0 && !param_sizes) || n_params < 0)
+    return fail(PARO_ERR_INVALID, "null argument");
+  *out_trainable = nullptr;
+  *out_frozen = nullptr;
+  std::vector<int64_t> tr, fr;
+  for (int i = 0; i < n_params; ++i) (trainable[i] ? tr : fr).push_back(param_sizes[i]);
+  if (tr.empty()) return fail(PARO_ERR_INVALID, "no trainable tensor");
+  paro_opts_t o;
+  if (opts) o = *opts;
+  else paro_opts_default(&o);
+  o.frozen = 0;
+  paro_status_t st = paro_plan(ctx, strategy, tr.data(), (int)tr.size(), &o, out_trainable);
+  if (st != PARO_OK || fr.empty()) return st;
+  o.frozen = 1;
+  st = paro_plan(ctx, strategy, fr.data(), (int)fr.size(), &o, out_frozen);
+  if (st != PARO_OK) {
+    const std::string msg = g_last_error;
+    paro_plan_destroy(*out_trainable);
+    *out_trainable = nullptr;
+    g_last_error = msg;
+  }
+  return st;
+}
+
 paro_status_t paro_plan_info(paro_plan_t p, paro_plan_info_t* out) {
   if (!p || !out) return fail(PARO_ERR_INVALID, "null argument");
   const Planner& pl = *p->pl;
@@ -898,7 +927,7 @@ paro_status_t paro_buffer(paro_plan_t p, int rank, int kind, void** ptr) {
   if (ctx->mode == MODE_PLANNER) return fail(PARO_ERR_STATE, "planning-only context has no buffers");
   if (!is_local(p, rank)) return fail(PARO_ERR_INVALID, "rank is not local to this process");
   const Planner& pl = *p->pl;
-  if (kind == 0) *ptr = data_ptr(p, rank, BUF_GRAD, 0);
+  if (kind == 0) *ptr = pl.opt.params_only ? nullptr : data_ptr(p, rank, BUF_GRAD, 0);
   else if (kind == 1) *ptr = data_ptr(p, rank, BUF_PARAM, 0);
   else if (kind == 2) *ptr = (pl.G == LV_N) ? nullptr : data_ptr(p, rank, BUF_GSHARD, 0);
   else if (kind == 3) *ptr = pl.buf_len[BUF_GHAT] ? data_ptr(p, rank, BUF_GHAT, 0) : nullptr;
@@ -914,9 +943,10 @@ static paro_status_t opt_init_impl(paro_plan_t p, int rank, const float* src, ui
   paro_status_t s = check_ctx(ctx);
   if (s != PARO_OK) return s;
   if (ctx->mode == MODE_PLANNER) return fail(PARO_ERR_STATE, "planning-only context");
-  if (!st || !st->master || !st->m || !st->v) return fail(PARO_ERR_INVALID, "null opt state");
-  if (!is_local(p, rank)) return fail(PARO_ERR_INVALID, "rank is not local to this process");
   const Planner& pl = *p->pl;
+  if (!pl.opt.params_only && (!st || !st->master || !st->m || !st->v))
+    return fail(PARO_ERR_INVALID, "null opt state");
+  if (!is_local(p, rank)) return fail(PARO_ERR_INVALID, "rank is not local to this process");
   uint16_t* pbuf = reinterpret_cast<uint16_t*>(data_ptr(p, rank, BUF_PARAM, 0));
   for (size_t b = 0; b < pl.buckets.size(); ++b) {
     int64_t ob, oe, pb, pe;
@@ -924,8 +954,9 @@ static paro_status_t opt_init_impl(paro_plan_t p, int rank, const float* src, ui
     pl.residency(pl.P, rank, b, &pb, &pe);
     const int64_t os_off = pl.buckets[b].first / pl.divl(pl.OS);
     const int64_t p_off = pl.buckets[b].first / pl.divl(pl.P);
-    CK(launch_init_range(src, key, ob, oe - ob, pl.psi, st->master + os_off, st->m + os_off, st->v + os_off,
-                         nullptr, ctx->main));
+    if (!pl.opt.params_only)
+      CK(launch_init_range(src, key, ob, oe - ob, pl.psi, st->master + os_off, st->m + os_off, st->v + os_off,
+                           nullptr, ctx->main));
     CK(launch_init_range(src, key, pb, pe - pb, pl.psi, nullptr, nullptr, nullptr, pbuf + p_off, ctx->main));
   }
   CK(cudaStreamSynchronize(ctx->main));
@@ -948,6 +979,7 @@ paro_status_t paro_synth_grads(paro_plan_t p, int rank, uint64_t seed, int64_t s
   paro_ctx* ctx = p->ctx;
   paro_status_t s = check_ctx(ctx);
   if (s != PARO_OK) return s;
+  if (p->pl->opt.params_only) return fail(PARO_ERR_STATE, "frozen-parameter plan has no gradients or optimizer state");
   if (ctx->mode == MODE_PLANNER) return fail(PARO_ERR_STATE, "planning-only context");
   if (!is_local(p, rank)) return fail(PARO_ERR_INVALID, "rank is not local to this process");
   uint16_t* g = reinterpret_cast<uint16_t*>(data_ptr(p, rank, BUF_GRAD, 0));
@@ -964,6 +996,7 @@ paro_status_t paro_step(paro_plan_t p, const void* const* grads, void* const* pa
   paro_status_t s = check_ctx(ctx);
   if (s != PARO_OK) return s;
   if (ctx->mode == MODE_PLANNER) return fail(PARO_ERR_STATE, "planning-only context cannot step");
+  if (p->pl->opt.params_only) return fail(PARO_ERR_STATE, "frozen-parameter plan has no gradients or optimizer state");
   if (step < 1) return fail(PARO_ERR_INVALID, "step must be >= 1");
   if (!opt_state) return fail(PARO_ERR_INVALID, "null opt_state");
   const Planner& pl = *p->pl;
@@ -1284,6 +1317,7 @@ paro_status_t paro_accumulate(paro_plan_t p, const void* const* grads) {
   paro_status_t s = check_ctx(ctx);
   if (s != PARO_OK) return s;
   if (ctx->mode == MODE_PLANNER) return fail(PARO_ERR_STATE, "planning-only context cannot accumulate");
+  if (p->pl->opt.params_only) return fail(PARO_ERR_STATE, "frozen-parameter plan has no gradients or optimizer state");
   const Planner& pl = *p->pl;
   if (!pl.opt.accum) return fail(PARO_ERR_STATE, "plan was created without grad_accum");
   const int nl = (int)p->local.size();
@@ -1364,6 +1398,7 @@ paro_status_t paro_collective(paro_plan_t p, int what) {
   paro_ctx* ctx = p->ctx;
   paro_status_t s = check_ctx(ctx);
   if (s != PARO_OK) return s;
+  if (p->pl->opt.params_only) return fail(PARO_ERR_STATE, "frozen-parameter plan has no gradients or optimizer state");
   if (ctx->mode == MODE_PLANNER) return fail(PARO_ERR_STATE, "planning-only context");
   if (what != 0 && what != 1) return fail(PARO_ERR_INVALID, "what must be 0 (reduce) or 1 (gather)");
   const Planner& pl = *p->pl;

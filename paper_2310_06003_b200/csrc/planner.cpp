@@ -267,8 +267,25 @@ Planner::Planner(int N_, int M_, const std::string& code_, const std::vector<int
     throw std::invalid_argument("gradient accumulation is not available with the NCCL comparator topology");
   if (opt.accum && opt.topology == 3 && (M >= kMaxIn || g >= kMaxIn))
     throw std::invalid_argument("gradient accumulation with the direct topology needs group_size and n_groups < 16");
+  if (opt.params_only) opt.accum = opt.two_phase = opt.ce_reduce = false;
   layout();
   build_schedule();
+  if (opt.params_only) {   // keep only the forward/backward parameter gathers
+    for (BucketSchedule& S : sched) {
+      BucketSchedule w;
+      w.window = S.window;
+      w.nccl_reduce.assign(N, {});
+      w.nccl_gather.assign(N, {});
+      w.ghat.assign(N, Ref{});
+      w.ghat_in.assign(N, {});
+      w.param = std::vector<Ref>(N, Ref{0, BUF_PARAM, 0});
+      w.os_off.assign(N, 0);
+      w.os_len = 0;
+      S = w;
+    }
+    grad_ops.clear();
+    rest_ops.clear();
+  }
   validate_refs();
   count_bytes();
 }
@@ -292,6 +309,7 @@ void Planner::residency(Level l, int r, int64_t b, int64_t* begin, int64_t* end)
 
 int64_t Planner::mem_bytes(int state) const {
   if (state == 0) return 2 * p_numel;
+  if (opt.params_only && state != 0) return 0;
   if (state == 1) return 2 * (G == LV_N ? psi_pad : g_numel);
   return 12 * os_numel;
 }
@@ -335,6 +353,12 @@ void Planner::layout() {
   buf_len[BUF_GACC] = (opt.accum && G == LV_N) ? psi_pad : 0;
   buf_len[BUF_WIN] = (opt.windows > 0 && P != LV_N && N > 1) ? int64_t(opt.windows) * B : 0;
   acc_kind = !opt.accum ? -1 : (G == LV_N ? BUF_GACC : BUF_GSHARD);
+  if (opt.params_only) {   // frozen tensors: no gradient, no optimizer state, no staging
+    for (int k = 0; k < BUF_NKINDS; ++k)
+      if (k != BUF_PARAM && k != BUF_WIN) buf_len[k] = 0;
+    g_numel = os_numel = 0;
+    acc_kind = -1;
+  }
   int64_t off = 0;
   for (int k = 0; k < BUF_NKINDS; ++k) {
     buf_off[k] = off;

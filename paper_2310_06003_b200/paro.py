@@ -47,7 +47,7 @@ class paro_opts_t(C.Structure):
                 ("pull_transport", C.c_int), ("adam_impl", C.c_int), ("comm_impl", C.c_int),
                 ("inter_gbps", C.c_float), ("clip_norm", C.c_float), ("skip_nonfinite", C.c_int),
                 ("fuse_gather", C.c_int), ("copy_engine", C.c_int), ("gather_windows", C.c_int), ("grad_accum", C.c_int),
-                ("stream", C.c_void_p)]
+                ("stream", C.c_void_p), ("frozen", C.c_int)]
 
 
 class paro_plan_info_t(C.Structure):
@@ -104,6 +104,8 @@ paro_init_planner = _sig("paro_init_planner", _st, C.c_int, C.c_int, C.POINTER(_
 paro_finalize = _sig("paro_finalize", _st, _vp)
 paro_plan = _sig("paro_plan", _st, _vp, C.c_char_p, C.POINTER(_i64), C.c_int, C.POINTER(paro_opts_t),
                  C.POINTER(_vp))
+paro_plan_masked = _sig("paro_plan_masked", _st, _vp, C.c_char_p, C.POINTER(_i64), C.POINTER(C.c_uint8), C.c_int,
+                        C.POINTER(paro_opts_t), C.POINTER(_vp), C.POINTER(_vp))
 paro_plan_info = _sig("paro_plan_info", _st, _vp, C.POINTER(paro_plan_info_t))
 paro_shard_range = _sig("paro_shard_range", _st, _vp, C.c_int, C.c_int, _i64, C.POINTER(_i64), C.POINTER(_i64))
 paro_bucket_range = _sig("paro_bucket_range", _st, _vp, _i64, C.POINTER(_i64), C.POINTER(_i64))
@@ -139,7 +141,7 @@ EXPORTED = ["paro_opts_default", "paro_get_unique_id", "paro_init", "paro_init_e
             "paro_plan_destroy", "paro_last_error", "paro_version", "paro_profile_start",
             "paro_profile_stop", "paro_collective", "paro_accumulate",
             "paro_rank_accum_send_bytes", "paro_gather_window", "paro_rank_gather_send_bytes",
-            "paro_table1_column", "paro_advise"]
+            "paro_table1_column", "paro_advise", "paro_plan_masked"]
 
 
 def check(status):
@@ -152,7 +154,7 @@ def check(status):
 def make_opts(bucket_elems=1 << 26, topology="ho", beta1=0.9, beta2=0.95, eps=1e-8, weight_decay=0.0,
               loss_scale=1.0, comm_ctas=148, pipeline_depth=2, stream=None, transport="pull", adam_impl="auto",
               comm_impl="tma", inter_gbps=0.0, grad_accum=False, clip_norm=0.0, skip_nonfinite=False, gather_windows=0,
-              fuse_gather="auto", copy_engine=False):
+              fuse_gather="auto", copy_engine=False, frozen=False):
     o = paro_opts_t()
     paro_opts_default(C.byref(o))
     o.bucket_elems = int(bucket_elems)
@@ -171,6 +173,7 @@ def make_opts(bucket_elems=1 << 26, topology="ho", beta1=0.9, beta2=0.95, eps=1e
     o.fuse_gather = {"auto": 1, "always": 2, "never": 0, True: 2, False: 0}[fuse_gather]
     o.copy_engine = {False: 0, True: 1, "gathers": 1, "all": 2, 0: 0, 1: 1, 2: 2}[copy_engine]
     o.stream = stream
+    o.frozen = 1 if frozen else 0
     return o
 
 
@@ -222,6 +225,27 @@ class Context:
 
 
 class Plan:
+    @classmethod
+    def masked(cls, ctx, strategy, param_sizes, trainable, **opts):
+        """paro_plan_masked: (plan of the trainable tensors, frozen-parameter plan or None)."""
+        sizes = [int(x) for x in param_sizes]
+        assert len(trainable) == len(sizes)
+        arr = (_i64 * max(1, len(sizes)))(*sizes)
+        msk = (C.c_uint8 * max(1, len(sizes)))(*[1 if t else 0 for t in trainable])
+        o = make_opts(**opts)
+        ht, hf = _vp(), _vp()
+        check(paro_plan_masked(ctx.h, strategy.encode(), arr, msk, len(sizes), C.byref(o), C.byref(ht), C.byref(hf)))
+        out = []
+        for h, sub in ((ht, [s for s, t in zip(sizes, trainable) if t]),
+                       (hf, [s for s, t in zip(sizes, trainable) if not t])):
+            if not h.value:
+                out.append(None)
+                continue
+            pl = cls.__new__(cls)
+            pl.ctx, pl.sizes, pl.opts, pl.h, pl.strategy = ctx, sub, o, h, strategy
+            out.append(pl)
+        return tuple(out)
+
     def __init__(self, ctx: Context, strategy: str, param_sizes, **opts):
         self.ctx = ctx
         self.sizes = [int(s) for s in param_sizes]
@@ -276,11 +300,12 @@ class Plan:
         return p.value
 
     def opt_state_init(self, rank, st, master_full_ptr=None, seed=None):
-        s = paro_opt_state_t(*st)
+        """st: (master, m, v) device pointers, or None for a frozen-parameter plan."""
+        sp = C.byref(paro_opt_state_t(*st)) if st is not None else None
         if master_full_ptr is not None:
-            check(paro_opt_state_init(self.h, rank, master_full_ptr, C.byref(s)))
+            check(paro_opt_state_init(self.h, rank, master_full_ptr, sp))
         else:
-            check(paro_opt_state_init_synth(self.h, rank, int(seed), C.byref(s)))
+            check(paro_opt_state_init_synth(self.h, rank, int(seed), sp))
 
     def synth_grads(self, rank, seed, step):
         check(paro_synth_grads(self.h, rank, int(seed), int(step)))

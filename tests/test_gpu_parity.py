@@ -585,3 +585,53 @@ def test_copy_engine_gathers_every_strategy(topo, ce):
             continue
         _check_against_dp(run, lay, ref)
         run.close()
+
+
+# --------------------------------------------------------------------- partial / PEFT training (NEXT-4)
+@pytest.mark.parametrize("N,M", [(8, 4), (4, 2), (8, 1), (1, 1)])
+def test_masked_plans_peft(N, M):
+    """paro_plan_masked: the trainable plan equals unsharded-DP Adam over the
+    trainable tensors alone (their own flat layout), the frozen tensors keep
+    their initial bf16 parameters bit for bit, and the parameter gathers of
+    both plans return the full bf16 model."""
+    paro = _paro()
+    u = N * 64
+    sizes = [u * 5 + 3, 1000, u * 9 + 17, 77, 4096, u * 2]
+    mask = [0, 1, 0, 1, 1, 0]
+    B = u * 4
+    tr = [s for s, t in zip(sizes, mask) if t]
+    fr = [s for s, t in zip(sizes, mask) if not t]
+    lay_t, lay_f = L.Layout(tr, N, M, B), L.Layout(fr, N, M, B)
+    w, m, v, p, _ = _dp_reference(lay_t, 3)
+    p_frozen = nm.bf16_bits_from_f32(ST.pad_flat(master_f32(0, lay_f.psi), lay_f.psi_pad, np.float32))
+    for code in S.paro_strategies():
+        ctx = paro.Context(N, M, mode="emulated", device=0) if N > 1 else \
+            paro.Context(1, 1, mode="real", rank=0, device=0, uid=paro.unique_id())
+        tp, fp = paro.Plan.masked(ctx, code, sizes, mask, bucket_elems=B, gather_windows=2)
+        n = tp.info()["os_numel"]
+        st = [tuple(torch.empty(n, dtype=torch.float32, device="cuda") for _ in range(3)) for _ in range(N)]
+        for r in range(N):
+            tp.opt_state_init(r, [x.data_ptr() for x in st[r]], seed=SEED)
+            fp.opt_state_init(r, None, seed=SEED)
+        for t in range(1, 4):
+            for r in range(N):
+                tp.synth_grads(r, SEED, t)
+            tp.step([[x.data_ptr() for x in s] for s in st], LR, t)
+        torch.cuda.synchronize()
+        for r in range(N):
+            _assert_same(st[r][0].cpu().numpy(), ST.shard_of(w, lay_t, code[2], r), f"{code} r{r} master")
+            _assert_same(st[r][1].cpu().numpy(), ST.shard_of(m, lay_t, code[2], r), f"{code} r{r} m")
+            _assert_same(st[r][2].cpu().numpy(), ST.shard_of(v, lay_t, code[2], r), f"{code} r{r} v")
+            pt = d2h(tp.buffer(r, 1), tp.info()["p_numel"], np.uint16)
+            assert np.array_equal(pt, ST.shard_of(p, lay_t, code[0], r)), (code, r)
+            pf = d2h(fp.buffer(r, 1), fp.info()["p_numel"], np.uint16)
+            assert np.array_equal(pf, ST.shard_of(p_frozen, lay_f, code[0], r)), (code, r)
+        for plan, lay, full in ((tp, lay_t, p), (fp, lay_f, p_frozen)):
+            for b, (s0, nb) in enumerate(lay.buckets):
+                out = plan.gather_window(0, b, slot=b % 2)
+                assert np.array_equal(d2h(out, nb, np.uint16), full[s0:s0 + nb]), (code, b)
+        with pytest.raises(paro.ParoError):
+            fp.step([[x.data_ptr() for x in s] for s in st], LR, 4)
+        fp.close()
+        tp.close()
+        ctx.close()

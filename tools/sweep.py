@@ -27,6 +27,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=2)
     ap.add_argument("--group-size", type=int, default=0)
     ap.add_argument("--grid", default="{}")
+    ap.add_argument("--mem-cap-gb", type=float, default=172.0,
+                    help="skip points whose per-rank HBM footprint (from a planning-only plan) exceeds this")
     ap.add_argument("--collective-only", action="store_true",
                     help="time paro_collective(reduce) + paro_collective(gather) per step, no Adam")
     a = ap.parse_args()
@@ -54,8 +56,22 @@ def main():
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     keys = list(grid.keys())
+    pctx = paro.Context(world, M)     # planning only: memory check before allocating
     for vals in itertools.product(*[grid[k] for k in keys]):
         cfg = dict(zip(keys, vals))
+        pp = paro.Plan(pctx, cfg["strategy"], sizes, bucket_elems=cfg["bucket"], topology=cfg["topology"],
+                       transport=cfg["transport"])
+        pi = pp.info()
+        pp.close()
+        foot = (2 * pi["psi_pad"] + pi["mem_p_bytes"] + (pi["mem_g_bytes"] if pi["g_numel"] > 0 else 0)
+                + pi["mem_os_bytes"] + pi["workspace_bytes"])
+        if foot > a.mem_cap_gb * 1e9:
+            if rank == 0:
+                print(json.dumps({"cfg": cfg, "groups": f"{world // M}x{M}", "skipped": "OOM",
+                                  "footprint_gb": round(foot / 1e9, 1),
+                                  "table2_gb": round((pi["mem_p_bytes"] + pi["mem_g_bytes"] + pi["mem_os_bytes"]) / 1e9, 1)}),
+                      flush=True)
+            continue
         try:
             plan = paro.Plan(ctx, cfg["strategy"], sizes, bucket_elems=cfg["bucket"], topology=cfg["topology"],
                              comm_ctas=cfg["comm_ctas"], pipeline_depth=cfg["depth"], stream=stream.cuda_stream,
@@ -106,12 +122,14 @@ def main():
                               "comm_GBps": round(prof["comm_bytes"] / max(1e-9, prof["comm_ms"]) / 1e6, 1),
                               "adam_GBps": round(28 * prof["adam_elems"] / max(1e-9, prof["adam_ms"]) / 1e6, 1),
                               "send_bytes": info["step_send_bytes_intra"] + info["step_send_bytes_inter"],
+                              "footprint_gb": round(foot / 1e9, 1),
                               "trace": {k: round(prof[k], 3) for k in ("traced_launches", "traced_barrier_ms",
                                                                       "traced_work_ms", "traced_final_ms")}}),
                   flush=True)
         del st
         plan.close()
         torch.cuda.empty_cache()
+    pctx.close()
     ctx.close()
     if world > 1:
         dist.destroy_process_group()
