@@ -139,6 +139,15 @@ typedef struct {
                           * and only fill the parameter buffer.  Pair it with a   *
                           * plan of the trainable tensors (paro_plan_masked).    *
                           * 0 (default).                                          */
+  int grad_slots;        /* K > 0: streamed gradients.  Instead of one psi_pad     *
+                          * flat gradient buffer (2 Psi bytes, which Table 2 does  *
+                          * not count for G = I / G), the plan keeps K bucket      *
+                          * slots (2 K B bytes) and paro_step_streamed has each    *
+                          * bucket's gradients produced into slot b % K just       *
+                          * before its reduction, so a rank's memory is Table 2's  *
+                          * P + G + OS plus staging.  paro_step and                *
+                          * paro_synth_grads then return PARO_ERR_STATE; not with  *
+                          * grad_accum; copy_engine is forced to 0.  0 (default).  */
 } paro_opts_t;
 
 typedef struct {
@@ -157,6 +166,8 @@ typedef struct {
    * paro_step that follows accumulation (0 otherwise)                         */
   int64_t accum_send_bytes_intra, accum_send_bytes_inter;
   int64_t accum_step_send_bytes_intra, accum_step_send_bytes_inter;
+  int64_t grad_buffer_bytes;           /* raw gradient buffer per rank: 2 psi_pad, or *
+                                        * 2 K B with grad_slots = K                    */
 } paro_plan_info_t;
 
 typedef struct {
@@ -306,6 +317,24 @@ paro_status_t paro_synth_grads(paro_plan_t plan, int rank, uint64_t seed, int64_
  *  accumulator ("grads must be NULL after paro_accumulate"). */
 paro_status_t paro_step(paro_plan_t plan, const void* const* grads, void* const* params,
                         const paro_opt_state_t* opt_state, float lr, int64_t step);
+
+/* Streamed step (plans with grad_slots = K > 0): the same step as paro_step,
+ * but bucket b's raw gradients are written into slot b % K while the step runs
+ * (ZeRO-style bucketed gradients: a rank never holds all of them, P:343-344,
+ * Table 2's G column).  For every bucket in order and every local rank, once
+ * every rank is done reading bucket b - K from that slot, the library calls
+ *   producer(user, rank, b, begin, end, dst, stream)
+ * from this host thread; it must enqueue, on `stream` (a cudaStream_t), writes
+ * of the bf16 gradients of flat elements [begin, end) (paro_bucket_range;
+ * zero past psi) into the device buffer dst (end - begin elements), and
+ * return.  producer NULL: the library's synthetic gradients of `seed` and
+ * `grad_step` (the paro_synth_grads values).  params, opt_state, lr, step:
+ * as paro_step.  Errors: PARO_ERR_STATE if the plan has no grad_slots. */
+typedef void (*paro_grad_producer_t)(void* user, int rank, int64_t bucket, int64_t begin, int64_t end,
+                                     void* dst, void* stream);
+paro_status_t paro_step_streamed(paro_plan_t plan, paro_grad_producer_t producer, void* user, uint64_t seed,
+                                 int64_t grad_step, void* const* params, const paro_opt_state_t* opt_state,
+                                 float lr, int64_t step);
 
 /* Gradient accumulation (§3.3; R27).  Adds one
  * micro-batch's gradients at the G residency: G = G reduces the micro-batch

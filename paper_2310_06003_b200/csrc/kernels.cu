@@ -778,13 +778,14 @@ __device__ __forceinline__ float synth_master(uint64_t key, uint64_t i) {
   return __uint_as_float((sign << 31) | (expo << 23) | mant);
 }
 
-__global__ void synth_grad_kernel(uint16_t* dst, int64_t psi, int64_t psi_pad, uint64_t key) {
+// dst[k] = gradient of flat element begin + k, k < n (n, begin multiples of 8)
+__global__ void synth_grad_kernel(uint16_t* dst, int64_t begin, int64_t n, int64_t psi, uint64_t key) {
   const int64_t nth = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < psi_pad / 8; u += nth) {
+  for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n / 8; u += nth) {
     uint16_t b[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
-      const int64_t i = u * 8 + e;
+      const int64_t i = begin + u * 8 + e;
       b[e] = (i < psi) ? synth_grad_bits(key, (uint64_t)i) : (uint16_t)0;
     }
     uint4 v;
@@ -941,7 +942,14 @@ cudaError_t launch_pack(const PackEntry* table, int n_entries, int64_t max_n, cu
 }
 
 cudaError_t launch_synth_grad(uint16_t* dst, int64_t psi, int64_t psi_pad, uint64_t key, cudaStream_t s) {
-  synth_grad_kernel<<<148 * 16, 256, 0, s>>>(dst, psi, psi_pad, key);
+  synth_grad_kernel<<<148 * 16, 256, 0, s>>>(dst, 0, psi_pad, psi, key);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_synth_grad_range(uint16_t* dst, int64_t begin, int64_t n, int64_t psi, uint64_t key,
+                                    cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  synth_grad_kernel<<<148 * 16, 256, 0, s>>>(dst, begin, n, psi, key);
   return cudaGetLastError();
 }
 

@@ -117,6 +117,9 @@ cudaError_t launch_clip_scale(const double* norm_sq, const int* nonfinite, doubl
                               int skip_nonfinite, float* s_g_out, int* skip_out, cudaStream_t s);
 cudaError_t launch_pack(const PackEntry* table, int n_entries, int64_t max_n, cudaStream_t s);
 cudaError_t launch_synth_grad(uint16_t* dst, int64_t psi, int64_t psi_pad, uint64_t key, cudaStream_t s);
+// gradients of flat elements [begin, begin + n) into dst (zero past psi)
+cudaError_t launch_synth_grad_range(uint16_t* dst, int64_t begin, int64_t n, int64_t psi, uint64_t key,
+                                    cudaStream_t s);
 // init master/m/v over flat range [begin, begin+n) into os arrays at os_ptrs and
 // params (bf16) at pdst (may be null); src == null => synthetic master from key
 cudaError_t launch_init_range(const float* src, uint64_t key, int64_t begin, int64_t n, int64_t psi,

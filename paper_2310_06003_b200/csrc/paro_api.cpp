@@ -91,6 +91,7 @@ struct paro_plan {
   std::vector<std::vector<DevLaunch>> win;  // [window slot][bucket]: forward/backward parameter gather
   std::vector<DevLaunch> red_pre, acc_pre;  // copy-engine raw-chunk copies before reduce / accum (per bucket)
   std::vector<cudaEvent_t> ev_pre;
+  std::vector<cudaEvent_t> ev_prod;       // streamed step: bucket b's gradients are in their slot
   int64_t acc_count = 0;                  // micro-batches accumulated since the last step
   bool last_step_acc = false;             // the last step consumed an accumulator
   double* d_partials = nullptr;
@@ -536,6 +537,7 @@ void destroy_plan(PlanT* p) {
     cudaFree(p->d_trace);
     for (cudaEvent_t e : p->ev_red) cudaEventDestroy(e);
     for (cudaEvent_t e : p->ev_pre) cudaEventDestroy(e);
+    for (cudaEvent_t e : p->ev_prod) if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : p->ev_adam) cudaEventDestroy(e);
   }
   delete p;
@@ -588,6 +590,7 @@ void paro_opts_default(paro_opts_t* o) {
   o->copy_engine = 0;
   o->stream = nullptr;
   o->frozen = 0;
+  o->grad_slots = 0;
 }
 
 paro_status_t paro_get_unique_id(paro_uid_t* out) {
@@ -714,6 +717,11 @@ paro_status_t paro_plan(paro_ctx_t ctx, const char* strategy, const int64_t* par
   if (o.copy_engine < 0 || o.copy_engine > 2) return fail(PARO_ERR_INVALID, "copy_engine must be 0, 1 or 2");
   po.ce_reduce = o.copy_engine == 2;
   po.params_only = o.frozen != 0;
+  if (o.grad_slots < 0) return fail(PARO_ERR_INVALID, "grad_slots must be >= 0");
+  if (o.grad_slots > 0 && o.grad_accum) return fail(PARO_ERR_INVALID, "grad_slots cannot be combined with grad_accum");
+  if (o.grad_slots > 0) o.copy_engine = 0;   // its stream and barrier channel produce the gradients
+  po.grad_slots = o.frozen ? 0 : o.grad_slots;
+  po.ce_reduce = o.copy_engine == 2;
   auto* p = new PlanT();
   p->ctx = ctx;
   p->opts = o;
@@ -785,7 +793,7 @@ paro_status_t paro_plan(paro_ctx_t ctx, const char* strategy, const int64_t* par
     if (s2 != PARO_OK) return bail(s2);
   }
   const int nb = (int)pl.buckets.size();
-  p->partials_cap = adam_grid() * (pl.N == 1 ? 1 : nb);
+  p->partials_cap = adam_grid() * ((pl.N == 1 && pl.opt.grad_slots == 0) ? 1 : nb);
   PCK(cudaMalloc(&p->d_partials, sizeof(double) * p->partials_cap));
   PCK(cudaMalloc(&p->d_norm, sizeof(double)));
   PCK(cudaMemset(p->d_norm, 0, sizeof(double)));
@@ -803,9 +811,11 @@ paro_status_t paro_plan(paro_ctx_t ctx, const char* strategy, const int64_t* par
   p->ev_red.resize(nb);
   p->ev_adam.resize(nb);
   p->ev_pre.resize(nb);
+  p->ev_prod.resize(nb);
   for (int b = 0; b < nb; ++b) {
     PCK(cudaEventCreateWithFlags(&p->ev_red[b], cudaEventDisableTiming));
     PCK(cudaEventCreateWithFlags(&p->ev_pre[b], cudaEventDisableTiming));
+    PCK(cudaEventCreateWithFlags(&p->ev_prod[b], cudaEventDisableTiming));
     PCK(cudaEventCreateWithFlags(&p->ev_adam[b], cudaEventDisableTiming));
   }
   PCK(cudaDeviceSynchronize());
@@ -858,6 +868,7 @@ paro_status_t paro_plan_info(paro_plan_t p, paro_plan_info_t* out) {
   int64_t ws = 0;
   for (int k = BUF_GHAT; k < BUF_NKINDS; ++k) ws += 2 * pl.buf_len[k];
   out->workspace_bytes = ws + kHeaderBytes;
+  out->grad_buffer_bytes = 2 * pl.buf_len[BUF_GRAD];
   const int me = p->ctx->mode == MODE_REAL ? p->ctx->rank : 0;
   out->step_send_bytes_intra = pl.send_intra[me];
   out->step_send_bytes_inter = pl.send_inter[me];
@@ -981,6 +992,8 @@ paro_status_t paro_synth_grads(paro_plan_t p, int rank, uint64_t seed, int64_t s
   if (s != PARO_OK) return s;
   if (p->pl->opt.params_only) return fail(PARO_ERR_STATE, "frozen-parameter plan has no gradients or optimizer state");
   if (ctx->mode == MODE_PLANNER) return fail(PARO_ERR_STATE, "planning-only context");
+  if (p->pl->opt.grad_slots > 0)
+    return fail(PARO_ERR_STATE, "plan has grad_slots: gradients are produced per bucket by paro_step_streamed");
   if (!is_local(p, rank)) return fail(PARO_ERR_INVALID, "rank is not local to this process");
   uint16_t* g = reinterpret_cast<uint16_t*>(data_ptr(p, rank, BUF_GRAD, 0));
   CK(launch_synth_grad(g, p->pl->psi, p->pl->psi_pad, synth_key(seed, kTagGrad, (uint64_t)rank, (uint64_t)step),
@@ -989,9 +1002,43 @@ paro_status_t paro_synth_grads(paro_plan_t p, int rank, uint64_t seed, int64_t s
   return PARO_OK;
 }
 
+namespace {
+// Gradient source of a streamed step (grad_slots > 0): producer(user, ...) or
+// the library's synthetic gradients (paro_synth hash, seed / grad_step).
+struct GradSource {
+  paro_grad_producer_t fn = nullptr;
+  void* user = nullptr;
+  uint64_t seed = 0;
+  int64_t gstep = 0;
+};
+paro_status_t step_impl(PlanT* p, const void* const* grads, void* const* params, const paro_opt_state_t* opt_state,
+                        float lr, int64_t step, const GradSource* src);
+}  // namespace
+
 paro_status_t paro_step(paro_plan_t p, const void* const* grads, void* const* params,
                         const paro_opt_state_t* opt_state, float lr, int64_t step) {
   if (!p) return fail(PARO_ERR_INVALID, "null plan");
+  if (p->pl->opt.grad_slots > 0)
+    return fail(PARO_ERR_STATE, "plan has grad_slots: its gradients stream in through paro_step_streamed");
+  return step_impl(p, grads, params, opt_state, lr, step, nullptr);
+}
+
+paro_status_t paro_step_streamed(paro_plan_t p, paro_grad_producer_t producer, void* user, uint64_t seed,
+                                 int64_t grad_step, void* const* params, const paro_opt_state_t* opt_state,
+                                 float lr, int64_t step) {
+  if (!p) return fail(PARO_ERR_INVALID, "null plan");
+  if (p->pl->opt.grad_slots <= 0) return fail(PARO_ERR_STATE, "plan was created without grad_slots");
+  GradSource src;
+  src.fn = producer;
+  src.user = user;
+  src.seed = seed;
+  src.gstep = grad_step;
+  return step_impl(p, nullptr, params, opt_state, lr, step, &src);
+}
+
+namespace {
+paro_status_t step_impl(PlanT* p, const void* const* grads, void* const* params, const paro_opt_state_t* opt_state,
+                        float lr, int64_t step, const GradSource* src) {
   paro_ctx* ctx = p->ctx;
   paro_status_t s = check_ctx(ctx);
   if (s != PARO_OK) return s;
@@ -1036,6 +1083,7 @@ paro_status_t paro_step(paro_plan_t p, const void* const* grads, void* const* pa
   CK(cudaEventRecord(p->ev_fork, S));
   CK(cudaStreamWaitEvent(ctx->comm, p->ev_fork, 0));
   CK(cudaStreamWaitEvent(ctx->comp, p->ev_fork, 0));
+  if (src) CK(cudaStreamWaitEvent(ctx->dma, p->ev_fork, 0));
 
   // ---- pack (per-parameter gradients -> flat gradient buffer)
   if (grads) {
@@ -1139,7 +1187,7 @@ paro_status_t paro_step(paro_plan_t p, const void* const* grads, void* const* pa
     return PARO_OK;
   };
 
-  if (pl.N == 1) {
+  if (pl.N == 1 && !src) {
     if (two) {
       paro_status_t s1 = adam_bucket(0, nb, true);
       if (s1 == PARO_OK) s1 = norm_reduce();
@@ -1194,7 +1242,45 @@ paro_status_t paro_step(paro_plan_t p, const void* const* grads, void* const* pa
       }
       return run_launch(p, p->gat[b], &launches);
     };
+    // streamed step: bucket b's gradients go into slot b % K once every rank is
+    // done reading bucket b - K from it (its reduce and, unless two-phase, the
+    // Adam that may fold it): local events, then a peer barrier on the second
+    // channel, on the producer stream (ctx->dma; no copy-engine launches here)
+    auto produce = [&](int b) -> paro_status_t {
+      cudaStream_t ps = ctx->dma;
+      const int K = pl.opt.grad_slots;
+      if (b >= K) {
+        CK(cudaStreamWaitEvent(ps, p->ev_red[b - K], 0));
+        if (!two) CK(cudaStreamWaitEvent(ps, p->ev_adam[b - K], 0));
+        uint64_t peers = 0;
+        for (int x = 0; x < pl.N && ctx->mode == MODE_REAL; ++x)
+          if (x != ctx->rank) peers |= uint64_t(1) << x;
+        paro_status_t sb = barrier2(p, peers, ps, &launches);
+        if (sb != PARO_OK) return sb;
+      }
+      const int64_t b0 = pl.buckets[b].first, n = pl.buckets[b].second;
+      for (int li = 0; li < nl; ++li) {
+        const int r = p->local[li];
+        void* dst = data_ptr(p, r, BUF_GRAD, int64_t(b % K) * pl.B);
+        if (src->fn) {
+          src->fn(src->user, r, b, b0, b0 + n, dst, ps);
+        } else {
+          CK(launch_synth_grad_range(static_cast<uint16_t*>(dst), b0, n, pl.psi,
+                                     synth_key(src->seed, kTagGrad, (uint64_t)r, (uint64_t)src->gstep), ps));
+          ++launches;
+        }
+      }
+      CK(cudaGetLastError());
+      CK(cudaEventRecord(p->ev_prod[b], ps));
+      CK(cudaStreamWaitEvent(ctx->comm, p->ev_prod[b], 0));
+      CK(cudaStreamWaitEvent(ctx->comp, p->ev_prod[b], 0));
+      return PARO_OK;
+    };
     auto do_reduce = [&](int b) -> paro_status_t {
+      if (src) {
+        paro_status_t sp = produce(b);
+        if (sp != PARO_OK) return sp;
+      }
       if (pre_on) CK(cudaStreamWaitEvent(ctx->comm, p->ev_pre[b], 0));
       if (nccl) {
         const int k = prof_begin(p, ctx->comm, 1, 0);
@@ -1310,6 +1396,8 @@ paro_status_t paro_step(paro_plan_t p, const void* const* grads, void* const* pa
   }
   return PARO_OK;
 }
+
+}  // namespace
 
 paro_status_t paro_accumulate(paro_plan_t p, const void* const* grads) {
   if (!p) return fail(PARO_ERR_INVALID, "null plan");

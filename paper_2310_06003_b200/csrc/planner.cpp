@@ -268,6 +268,9 @@ Planner::Planner(int N_, int M_, const std::string& code_, const std::vector<int
   if (opt.accum && opt.topology == 3 && (M >= kMaxIn || g >= kMaxIn))
     throw std::invalid_argument("gradient accumulation with the direct topology needs group_size and n_groups < 16");
   if (opt.params_only) opt.accum = opt.two_phase = opt.ce_reduce = false;
+  if (opt.grad_slots < 0) throw std::invalid_argument("grad_slots must be >= 0");
+  if (opt.grad_slots > 0 && (opt.accum || opt.ce_reduce))
+    throw std::invalid_argument("grad_slots cannot be combined with grad_accum or copy_engine = 2");
   layout();
   build_schedule();
   if (opt.params_only) {   // keep only the forward/backward parameter gathers
@@ -340,7 +343,7 @@ void Planner::layout() {
   p1_len = B / M;
   sown_len = C;
   land_len = int64_t(M - 1) * (B / M) + int64_t(g - 1) * C;
-  buf_len[BUF_GRAD] = psi_pad;
+  buf_len[BUF_GRAD] = opt.grad_slots > 0 ? std::min<int64_t>(psi_pad, int64_t(opt.grad_slots) * B) : psi_pad;
   buf_len[BUF_PARAM] = p_numel;
   buf_len[BUF_GSHARD] = g_numel;
   buf_len[BUF_GHAT] = int64_t(nslots) * ghat_slot;
@@ -393,7 +396,9 @@ void Planner::build_schedule() {
     S.nccl_gather.assign(N, {});
 
     int src_kind = BUF_GRAD;   // BUF_GACC while emitting the G = N post-accumulation reduction
-    auto grad = [&](int r, int64_t o) { return Ref{r, src_kind, s + o}; };
+    // raw gradients: the flat buffer, or bucket slot b % K of a streamed step
+    const int64_t gbase = opt.grad_slots > 0 ? int64_t(b % opt.grad_slots) * B : s;
+    auto grad = [&](int r, int64_t o) { return Ref{r, src_kind, (src_kind == BUF_GRAD ? gbase : s) + o}; };
     auto gshard = [&](int r, int64_t o) { return Ref{r, BUF_GSHARD, s / divl(G) + o}; };
     auto ghat_base = [&](int r) {
       if (G == OS && G != LV_N) return Ref{r, BUF_GSHARD, s / divl(G)};

@@ -118,6 +118,8 @@ struct PlanOptions {
   bool two_phase = false;    // clipping / skip: every bucket's g_hat stays resident until Adam (R28)
   int windows = 0;           // parameter-gather window slots (0: none)
   bool ce_reduce = false;    // G = I: RS_I as copy-engine copies of raw chunks + one local fold
+  int grad_slots = 0;        // > 0: raw gradients live in this many bucket slots (slot b % K)
+                             // filled by a producer as the step streams, not in one psi_pad buffer
   bool params_only = false;  // frozen tensors (partial / PEFT training): only
                              // the parameter residency and its forward/backward gathers
   int fuse_gather = 1;       // fold a one-ring parameter all-gather into Adam's stores:

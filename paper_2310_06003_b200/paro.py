@@ -47,7 +47,7 @@ class paro_opts_t(C.Structure):
                 ("pull_transport", C.c_int), ("adam_impl", C.c_int), ("comm_impl", C.c_int),
                 ("inter_gbps", C.c_float), ("clip_norm", C.c_float), ("skip_nonfinite", C.c_int),
                 ("fuse_gather", C.c_int), ("copy_engine", C.c_int), ("gather_windows", C.c_int), ("grad_accum", C.c_int),
-                ("stream", C.c_void_p), ("frozen", C.c_int)]
+                ("stream", C.c_void_p), ("frozen", C.c_int), ("grad_slots", C.c_int)]
 
 
 class paro_plan_info_t(C.Structure):
@@ -58,7 +58,8 @@ class paro_plan_info_t(C.Structure):
                 ("step_send_bytes_intra", C.c_int64), ("step_send_bytes_inter", C.c_int64),
                 ("n_rounds", C.c_int32), ("n_comm_launches", C.c_int32),
                 ("accum_send_bytes_intra", C.c_int64), ("accum_send_bytes_inter", C.c_int64),
-                ("accum_step_send_bytes_intra", C.c_int64), ("accum_step_send_bytes_inter", C.c_int64)]
+                ("accum_step_send_bytes_intra", C.c_int64), ("accum_step_send_bytes_inter", C.c_int64),
+                ("grad_buffer_bytes", C.c_int64)]
 
 
 class paro_step_stats_t(C.Structure):
@@ -122,6 +123,9 @@ paro_opt_state_init_synth = _sig("paro_opt_state_init_synth", _st, _vp, C.c_int,
 paro_synth_grads = _sig("paro_synth_grads", _st, _vp, C.c_int, C.c_uint64, _i64)
 paro_step = _sig("paro_step", _st, _vp, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(paro_opt_state_t),
                  C.c_float, _i64)
+PRODUCER = C.CFUNCTYPE(None, C.c_void_p, C.c_int, _i64, _i64, _i64, C.c_void_p, C.c_void_p)
+paro_step_streamed = _sig("paro_step_streamed", _st, _vp, PRODUCER, C.c_void_p, C.c_uint64, _i64, C.POINTER(_vp),
+                          C.POINTER(paro_opt_state_t), C.c_float, _i64)
 paro_accumulate = _sig("paro_accumulate", _st, _vp, C.POINTER(_vp))
 paro_step_stats = _sig("paro_step_stats", _st, _vp, C.POINTER(paro_step_stats_t))
 paro_plan_destroy = _sig("paro_plan_destroy", _st, _vp)
@@ -141,7 +145,7 @@ EXPORTED = ["paro_opts_default", "paro_get_unique_id", "paro_init", "paro_init_e
             "paro_plan_destroy", "paro_last_error", "paro_version", "paro_profile_start",
             "paro_profile_stop", "paro_collective", "paro_accumulate",
             "paro_rank_accum_send_bytes", "paro_gather_window", "paro_rank_gather_send_bytes",
-            "paro_table1_column", "paro_advise", "paro_plan_masked"]
+            "paro_table1_column", "paro_advise", "paro_plan_masked", "paro_step_streamed"]
 
 
 def check(status):
@@ -154,7 +158,7 @@ def check(status):
 def make_opts(bucket_elems=1 << 26, topology="ho", beta1=0.9, beta2=0.95, eps=1e-8, weight_decay=0.0,
               loss_scale=1.0, comm_ctas=148, pipeline_depth=2, stream=None, transport="pull", adam_impl="auto",
               comm_impl="tma", inter_gbps=0.0, grad_accum=False, clip_norm=0.0, skip_nonfinite=False, gather_windows=0,
-              fuse_gather="auto", copy_engine=False, frozen=False):
+              fuse_gather="auto", copy_engine=False, frozen=False, grad_slots=0):
     o = paro_opts_t()
     paro_opts_default(C.byref(o))
     o.bucket_elems = int(bucket_elems)
@@ -174,6 +178,7 @@ def make_opts(bucket_elems=1 << 26, topology="ho", beta1=0.9, beta2=0.95, eps=1e
     o.copy_engine = {False: 0, True: 1, "gathers": 1, "all": 2, 0: 0, 1: 1, 2: 2}[copy_engine]
     o.stream = stream
     o.frozen = 1 if frozen else 0
+    o.grad_slots = int(grad_slots)
     return o
 
 
@@ -318,6 +323,21 @@ class Plan:
         gp = (_vp * len(grads))(*grads) if grads is not None else None
         pp = (_vp * len(params))(*params) if params is not None else None
         check(paro_step(self.h, gp, pp, sts, float(lr), int(step)))
+
+    def step_streamed(self, opt_states, lr, step, seed=None, grad_step=None, producer=None, params=None):
+        """paro_step_streamed (grad_slots plans).  producer(rank, bucket, begin, end, dst_ptr, stream_ptr)
+        enqueues bucket `bucket`'s bf16 gradients into dst on that CUDA stream; None = the library's
+        synthetic gradients of (seed, grad_step)."""
+        n = len(opt_states)
+        sts = (paro_opt_state_t * n)(*[paro_opt_state_t(*s) for s in opt_states])
+        pp = (_vp * len(params))(*params) if params is not None else None
+        if producer is None:
+            cb = C.cast(None, PRODUCER)
+        else:
+            cb = PRODUCER(lambda _u, r, b, b0, b1, dst, stream: producer(r, b, b0, b1, dst, stream))
+        self._producer_ref = cb      # kept alive: the library calls it from this thread during the call
+        check(paro_step_streamed(self.h, cb, None, int(seed or 0), int(grad_step or 0), pp, sts, float(lr),
+                                 int(step)))
 
     def accumulate(self, grads=None):
         """paro_accumulate: add one micro-batch (grads: None = the flat gradient

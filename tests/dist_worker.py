@@ -43,6 +43,8 @@ def main():
     adam_impl = cfg.get("adam_impl", "auto")
     fuse_gather = cfg.get("fuse_gather", "auto")
     copy_engine = cfg.get("copy_engine", False)
+    mask = cfg.get("mask")               # partial / PEFT training: paro_plan_masked (NEXT-4)
+    slots = cfg.get("grad_slots", 0)     # > 0: streamed gradients (paro_step_streamed)
     for M in splits:
         uid = paro.unique_id() if rank == 0 else bytes(128)
         t = torch.tensor(list(uid), dtype=torch.uint8)
@@ -50,10 +52,16 @@ def main():
         ctx = paro.Context(world, M, mode="real", rank=rank, device=local, uid=bytes(t.tolist()))
         for code, topo, tr in [(c, t_, x) for c in codes for t_ in topos for x in transports]:
             if True:
-                pl = paro.Plan(ctx, code, sizes, bucket_elems=B, topology=topo, transport=tr, comm_impl=comm_impl,
-                               inter_gbps=inter_gbps, grad_accum=accum > 0, clip_norm=clip,
-                               gather_windows=windows, adam_impl=adam_impl, fuse_gather=fuse_gather,
-                               copy_engine=copy_engine)
+                kw = dict(bucket_elems=B, topology=topo, transport=tr, comm_impl=comm_impl,
+                          inter_gbps=inter_gbps, grad_accum=accum > 0, clip_norm=clip,
+                          gather_windows=windows, adam_impl=adam_impl, fuse_gather=fuse_gather,
+                          copy_engine=copy_engine, grad_slots=slots)
+                fz = None
+                if mask:
+                    pl, fz = paro.Plan.masked(ctx, code, sizes, mask, **kw)
+                    fz.opt_state_init(rank, None, seed=SEED)
+                else:
+                    pl = paro.Plan(ctx, code, sizes, **kw)
                 info = pl.info()
                 st = [torch.empty(info["os_numel"], dtype=torch.float32, device="cuda") for _ in range(3)]
                 ptrs = [[x.data_ptr() for x in st]]
@@ -64,9 +72,12 @@ def main():
                         for k in range(accum):
                             pl.synth_grads(rank, SEED, (s << 8) | (k + 1))
                             pl.accumulate()
+                    elif slots:
+                        pl.step_streamed(ptrs, 3e-4, s, seed=SEED, grad_step=s)
                     else:
                         pl.synth_grads(rank, SEED, s)
-                    pl.step(ptrs, 3e-4, s)
+                    if not slots:
+                        pl.step(ptrs, 3e-4, s)
                     stats = pl.stats()
                 torch.cuda.synchronize()
                 pbuf = torch.empty(info["p_numel"], dtype=torch.int16, device="cuda")
@@ -83,6 +94,21 @@ def main():
                         _copy(wb, ptr)
                         parts.append(wb.cpu().numpy().view(np.uint16))
                     extra["full"] = np.concatenate(parts)
+                if fz is not None:      # frozen parameters: residency and gathered windows
+                    fi = fz.info()
+                    fb = torch.empty(fi["p_numel"], dtype=torch.int16, device="cuda")
+                    _copy(fb, fz.buffer(rank, 1))
+                    extra["frozen_param"] = fb.cpu().numpy().view(np.uint16)
+                    parts = []
+                    for b in range(fi["n_buckets"]):
+                        b0, b1 = fz.bucket_range(b)
+                        ptr = fz.gather_window(rank, b, slot=b % max(1, windows))
+                        torch.cuda.synchronize()
+                        wb = torch.empty(b1 - b0, dtype=torch.int16, device="cuda")
+                        _copy(wb, ptr)
+                        parts.append(wb.cpu().numpy().view(np.uint16))
+                    extra["frozen_full"] = np.concatenate(parts)
+                    fz.close()
                 np.savez(os.path.join(out, tag + ".npz"), master=st[0].cpu().numpy(), m=st[1].cpu().numpy(),
                          v=st[2].cpu().numpy(), param=pbuf.cpu().numpy().view(np.uint16), **extra)
                 with open(os.path.join(out, tag + ".json"), "w") as f:

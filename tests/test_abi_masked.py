@@ -56,3 +56,34 @@ def test_frozen_plan_rejects_step_calls_on_planner_ctx():
         fp.step([[0, 0, 0]], 1e-3, 1)
     fp.close()
     ctx.close()
+
+
+# --------------------------------------------------------------------- streamed gradients (grad_slots)
+@pytest.mark.parametrize("N,M", [(8, 4), (4, 2), (1, 1)])
+def test_grad_slots_shrink_the_gradient_buffer_only(N, M):
+    """grad_slots = K keeps K bucket slots of raw gradients (2 K B bytes)
+    instead of the 2 psi_pad flat buffer; shard map, bytes and Table 2
+    accounting are unchanged."""
+    u = N * 64
+    sizes = [u * 37 + 5, 999, u * 11]
+    B = u * 4
+    ctx = paro.Context(N, M)
+    for code in S.paro_strategies():
+        a = paro.Plan(ctx, code, sizes, bucket_elems=B)
+        for K in (1, 2, 3):
+            b = paro.Plan(ctx, code, sizes, bucket_elems=B, grad_slots=K)
+            ia, ib = a.info(), b.info()
+            assert ia["grad_buffer_bytes"] == 2 * ia["psi_pad"]
+            assert ib["grad_buffer_bytes"] == 2 * min(ia["psi_pad"], K * ib["bucket_elems"])
+            for k in ("psi_pad", "p_numel", "g_numel", "os_numel", "mem_p_bytes", "mem_g_bytes", "mem_os_bytes",
+                      "step_send_bytes_intra", "step_send_bytes_inter", "n_rounds", "n_comm_launches"):
+                assert ia[k] == ib[k], (code, K, k)
+            for r in range(N):
+                assert a.send_bytes(r) == b.send_bytes(r)
+            b.close()
+        a.close()
+    with pytest.raises(paro.ParoError):
+        paro.Plan(ctx, "IIG", sizes, grad_slots=2, grad_accum=True)
+    with pytest.raises(paro.ParoError):
+        paro.Plan(ctx, "IIG", sizes, grad_slots=-1)
+    ctx.close()

@@ -49,7 +49,7 @@ CODES = ["NNN", "NNI", "NNG", "NII", "NIG", "NGG", "INI", "ING", "III", "IIG", "
 
 
 @pytest.mark.skipif(_ngpu() < 2, reason="needs >= 2 GPUs")
-@pytest.mark.parametrize("variant", ["default", "paced_lsu", "accum", "clip", "copy_engine"])
+@pytest.mark.parametrize("variant", ["default", "paced_lsu", "accum", "clip", "copy_engine", "masked", "slots"])
 def test_real_ranks_match_oracle(tmp_path, variant):
     world = min(_ngpu(), 4)
     splits = [m for m in range(1, world + 1) if world % m == 0]
@@ -67,13 +67,23 @@ def test_real_ranks_match_oracle(tmp_path, variant):
     if variant == "clip":        # two-phase step with an active global-norm clip (NEXT-3)
         cfg.update({"clip_norm": 0.05, "topos": ["ho", "nccl"], "transports": ["pull", "push"],
                     "fuse_gather": "always"})
+    if variant == "slots":       # streamed gradients: one bucket slot, reused by every bucket
+        cfg.update({"grad_slots": 1, "topos": ["ho", "two_step", "direct"], "transports": ["pull", "push"]})
+    if variant == "masked":      # partial / PEFT training: trainable plan + frozen-parameter plan
+        cfg.update({"sizes": [world * 64 * 40 + 24, 333, world * 64 * 9 + 5, 4096], "mask": [0, 1, 0, 1],
+                    "topos": ["ho", "two_step"], "transports": ["pull"], "windows": 2})
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr=127.0.0.1", "--master-port=29517", os.path.join(ROOT, "tests", "dist_worker.py"),
            str(tmp_path), json.dumps(cfg)]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    mask = cfg.get("mask")
+    tsizes = [x for x, t in zip(cfg["sizes"], mask) if t] if mask else cfg["sizes"]
     for M in splits:
-        lay = L.Layout(cfg["sizes"], world, M, cfg["bucket"])
+        lay = L.Layout(tsizes, world, M, cfg["bucket"])
+        if mask:
+            lay_f = L.Layout([x for x, t in zip(cfg["sizes"], mask) if not t], world, M, cfg["bucket"])
+            p_frozen = nm.bf16_bits_from_f32(ST.pad_flat(master_f32(0, lay_f.psi), lay_f.psi_pad, np.float32))
         refs = {gl: _dp(lay, 2, cfg.get("accum", 0), gl, cfg.get("clip_norm", 0.0)) for gl in "NIG"}
         for code in cfg["codes"]:
             w, m, v, p, norm = refs[code[1]]
@@ -92,3 +102,6 @@ def test_real_ranks_match_oracle(tmp_path, variant):
                     assert abs(meta["stats"]["grad_norm"] ** 2 - norm) <= 1e-12 * norm, tag
                     if "full" in d:      # forward/backward parameter gather: the full bf16 model
                         assert np.array_equal(d["full"], p), tag
+                    if mask:             # frozen tensors: untouched residency, full windows
+                        assert np.array_equal(d["frozen_param"], ST.shard_of(p_frozen, lay_f, code[0], rank)), tag
+                        assert np.array_equal(d["frozen_full"], p_frozen), tag

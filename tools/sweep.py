@@ -34,7 +34,7 @@ def main():
     a = ap.parse_args()
     grid = {"strategy": ["IIG"], "topology": ["ho"], "transport": ["pull"], "comm_ctas": [148],
             "bucket": [1 << 26], "depth": [2], "adam_impl": ["auto"], "comm_impl": ["tma"], "fuse_gather": ["auto"],
-            "copy_engine": [0]}
+            "copy_engine": [0], "grad_slots": [0]}
     grid.update(json.loads(a.grid))
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -60,10 +60,10 @@ def main():
     for vals in itertools.product(*[grid[k] for k in keys]):
         cfg = dict(zip(keys, vals))
         pp = paro.Plan(pctx, cfg["strategy"], sizes, bucket_elems=cfg["bucket"], topology=cfg["topology"],
-                       transport=cfg["transport"])
+                       transport=cfg["transport"], grad_slots=cfg["grad_slots"])
         pi = pp.info()
         pp.close()
-        foot = (2 * pi["psi_pad"] + pi["mem_p_bytes"] + (pi["mem_g_bytes"] if pi["g_numel"] > 0 else 0)
+        foot = (pi["grad_buffer_bytes"] + pi["mem_p_bytes"] + (pi["mem_g_bytes"] if pi["g_numel"] > 0 else 0)
                 + pi["mem_os_bytes"] + pi["workspace_bytes"])
         if foot > a.mem_cap_gb * 1e9:
             if rank == 0:
@@ -77,7 +77,7 @@ def main():
                              comm_ctas=cfg["comm_ctas"], pipeline_depth=cfg["depth"], stream=stream.cuda_stream,
                              transport=cfg["transport"], adam_impl=cfg["adam_impl"],
                              comm_impl=cfg["comm_impl"], fuse_gather={1: "always", 0: "never"}.get(cfg["fuse_gather"], cfg["fuse_gather"]),
-                             copy_engine=bool(cfg["copy_engine"]))
+                             copy_engine=bool(cfg["copy_engine"]), grad_slots=cfg["grad_slots"])
         except Exception as e:  # noqa: BLE001
             if rank == 0:
                 print(json.dumps({"cfg": cfg, "error": str(e)}), flush=True)
@@ -86,12 +86,15 @@ def main():
         st = [torch.empty(info["os_numel"], dtype=torch.float32, device="cuda") for _ in range(3)]
         ptrs = [[x.data_ptr() for x in st]]
         plan.opt_state_init(rank, ptrs[0], seed=SEED)
-        plan.synth_grads(rank, SEED, 1)
+        if not cfg["grad_slots"]:
+            plan.synth_grads(rank, SEED, 1)
         s = 0
         def one_step(s):
             if a.collective_only:
                 plan.collective(0)
                 plan.collective(1)
+            elif cfg["grad_slots"]:   # gradients produced per bucket inside the step (2 B/param written)
+                plan.step_streamed(ptrs, 3e-4, s, seed=SEED, grad_step=1)
             else:
                 plan.step(ptrs, 3e-4, s)
         for _ in range(a.warmup):
