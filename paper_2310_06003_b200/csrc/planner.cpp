@@ -272,6 +272,10 @@ Planner::Planner(int N_, int M_, const std::string& code_, const std::vector<int
   if (opt.grad_slots > 0 && (opt.accum || opt.ce_reduce))
     throw std::invalid_argument("grad_slots cannot be combined with grad_accum or copy_engine = 2");
   layout();
+  if (N == 1 && opt.two_phase && opt.grad_slots > 0 && opt.grad_slots < (int64_t)buckets.size())
+    throw std::invalid_argument(
+        "a two-phase step (clip_norm / skip_nonfinite) at N = 1 updates from the raw gradients after the norm "
+        "pass: grad_slots must be 0 or >= the number of buckets");
   build_schedule();
   if (opt.params_only) {   // keep only the forward/backward parameter gathers
     for (BucketSchedule& S : sched) {

@@ -87,3 +87,8 @@ def test_grad_slots_shrink_the_gradient_buffer_only(N, M):
     with pytest.raises(paro.ParoError):
         paro.Plan(ctx, "IIG", sizes, grad_slots=-1)
     ctx.close()
+    one = paro.Context(1, 1)     # N = 1 two-phase updates from the raw gradients: all must stay resident
+    with pytest.raises(paro.ParoError, match="two-phase"):
+        paro.Plan(one, "NNN", sizes, bucket_elems=64 * 4, grad_slots=2, clip_norm=1.0)
+    paro.Plan(one, "NNN", sizes, bucket_elems=64 * 4, grad_slots=1000, clip_norm=1.0).close()
+    one.close()

@@ -702,3 +702,29 @@ def test_streamed_step_python_producer():
     assert len(calls) == 2 * N * len(lay.buckets)
     _check_against_dp(run, lay, ref)
     run.close()
+
+
+@pytest.mark.parametrize("N,M", [(8, 4), (4, 2)])
+def test_streamed_step_with_clipping(N, M):
+    """Two-phase step (global-norm clipping) with one gradient slot: phase 1
+    reduces every bucket as it is produced, the slot is reused once the
+    reduction read it (no Adam reads raw slots in two-phase mode at N > 1)."""
+    paro = _paro()
+    sizes = [N * 64 * 40 + 24, 1000]
+    B = N * 64 * 8
+    lay = L.Layout(sizes, N, M, B)
+    clip = 0.05
+    ref, per = _clip_reference(lay, 3, clip)
+    for code in S.paro_strategies():
+        run = EmuRun(N, M, code, sizes, B)
+        run.pl.close()
+        run.pl = paro.Plan(run.ctx, code, sizes, bucket_elems=B, grad_slots=1, clip_norm=clip)
+        run.info = run.pl.info()
+        for r in range(N):
+            run.pl.opt_state_init(r, [t.data_ptr() for t in run.st[r]], seed=SEED)
+        for t in range(1, 4):
+            run.pl.step_streamed(run.ptrs(), LR, t, seed=SEED, grad_step=t)
+            st = run.pl.stats()
+            assert abs(st["grad_norm"] ** 2 - per[t - 1][5]) <= 1e-12 * per[t - 1][5]
+        _check_against_dp(run, lay, ref)
+        run.close()

@@ -20,6 +20,16 @@ import torch.distributed as dist  # noqa: E402
 from paro_synth import SEED, llama_param_sizes  # noqa: E402
 
 
+def _cudart():
+    import ctypes
+    import glob
+    import nvidia.cuda_runtime as cr
+    rt = ctypes.CDLL(glob.glob(os.path.join(list(cr.__path__)[0], "lib", "libcudart.so*"))[0])
+    rt.cudaMemcpyAsync.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_void_p]
+    rt.cudaMemcpyAsync.restype = ctypes.c_int
+    return rt
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--model", default="7B")
@@ -34,7 +44,7 @@ def main():
     a = ap.parse_args()
     grid = {"strategy": ["IIG"], "topology": ["ho"], "transport": ["pull"], "comm_ctas": [148],
             "bucket": [1 << 26], "depth": [2], "adam_impl": ["auto"], "comm_impl": ["tma"], "fuse_gather": ["auto"],
-            "copy_engine": [0], "grad_slots": [0]}
+            "copy_engine": [0], "grad_slots": [0], "producer": ["synth"]}
     grid.update(json.loads(a.grid))
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -88,13 +98,22 @@ def main():
         plan.opt_state_init(rank, ptrs[0], seed=SEED)
         if not cfg["grad_slots"]:
             plan.synth_grads(rank, SEED, 1)
+        producer = None
+        if cfg["grad_slots"] and cfg["producer"] == "copy":
+            # the "backward" hands over each bucket from one resident bucket-sized buffer
+            # (2 B read + 2 B written per element, like a real backward's gradient write)
+            srcbuf = torch.empty(info["bucket_elems"], dtype=torch.int16, device="cuda").random_(-32768, 32767)
+            rt = _cudart()
+
+            def producer(r, b, b0, b1, dst, strm, srcbuf=srcbuf, rt=rt):
+                rt.cudaMemcpyAsync(dst, srcbuf.data_ptr(), 2 * (b1 - b0), 3, strm)
         s = 0
         def one_step(s):
             if a.collective_only:
                 plan.collective(0)
                 plan.collective(1)
             elif cfg["grad_slots"]:   # gradients produced per bucket inside the step (2 B/param written)
-                plan.step_streamed(ptrs, 3e-4, s, seed=SEED, grad_step=1)
+                plan.step_streamed(ptrs, 3e-4, s, seed=SEED, grad_step=1, producer=producer)
             else:
                 plan.step(ptrs, 3e-4, s)
         for _ in range(a.warmup):
