@@ -268,17 +268,20 @@ def run_ours(args):
     comm_ms = prof["comm_ms"] / max(1, prof["comm_launches"])
     if prof["adam_ms"] >= prof["comm_ms"] or prof["comm_launches"] == 0:
         elems_per_launch = prof["adam_elems"] / max(1, prof["adam_launches"])
-        alg = 28.0 * elems_per_launch
+        # 28 B/elem, plus 2 B per extra g_hat input of a fused final hop and per fused-gather push
+        alg = prof["adam_hbm_bytes"] / max(1, prof["adam_launches"])
         ach = alg / (adam_ms / 1000.0) / 1e9
         peak = float(peaks["hbm_gbs"])
         # which Adam kernel ran: TMA pipeline when every operand is local (N = 1, push), else LSU
         kname = "adam_tma_kernel" if args.adam_impl == "auto" else "adam_kernel"
-        tr = traffic.get(kname)
+        # the committed capture is single-GPU (ncu never runs multi-rank): it matches the N = 1 kernel only
+        tr = traffic.get(kname) if N == 1 else None
         roof = {"bound": "hbm", "kernel": f"{kname} (fused unscale+Adam+bf16 cast+norm)", "achieved": ach,
                 "peak": peak, "unit": "GB/s", "frac": ach / peak,
                 "traffic": (tr["dram_bytes_per_elem"] * elems_per_launch) if tr else None,
                 "traffic_source": tr["source"] if tr else None,
-                "algorithmic_bytes_per_launch": alg, "launch_ms": adam_ms, "peak_source": peak_kind,
+                "algorithmic_bytes_per_launch": alg, "bytes_per_elem": alg / max(1.0, elems_per_launch),
+                "launch_ms": adam_ms, "peak_source": peak_kind,
                 "share_of_step": prof["adam_ms"] / max(1e-9, ms * args.steps)}
     else:
         alg = prof["comm_bytes"] / max(1, prof["comm_launches"])
@@ -290,6 +293,17 @@ def run_ours(args):
                 "traffic": None, "algorithmic_bytes_per_launch": alg,
                 "launch_ms": comm_ms, "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s/dir",
                 "share_of_step": prof["comm_ms"] / max(1e-9, ms * args.steps)}
+
+    # ---- the step as a whole against max(HBM, NVLink) (B200_PROFILING.md: the slower of
+    # the two bounds; HBM at the measured copy peak, NVLink at the measured 770 GB/s/dir)
+    hbm_step = (prof["adam_hbm_bytes"] + prof["comm_hbm_bytes"]) / args.steps
+    nvl_step = float(info["step_send_bytes_intra"] + info["step_send_bytes_inter"])
+    t_hbm, t_nvl = hbm_step / (float(peaks["hbm_gbs"]) * 1e6), nvl_step / (770.0 * 1e6)
+    step_roof = {"hbm_bytes": hbm_step, "nvlink_bytes": nvl_step, "t_hbm_ms": t_hbm, "t_nvlink_ms": t_nvl,
+                 "bound": "hbm" if t_hbm >= t_nvl else "nvlink", "t_bound_ms": max(t_hbm, t_nvl),
+                 "frac": max(t_hbm, t_nvl) / ms,
+                 "note": "algorithmic bytes of this rank's launches (Adam + collective tasks) per step; "
+                         "NVLink = bytes this rank sends per step (each direction)"}
 
     # ---- end to end: gradients from pinned host memory each step (read by the
     # pack kernel over PCIe), device->host read of the step's norm/flag
@@ -352,7 +366,7 @@ def run_ours(args):
                        "fuse_gather": args.fuse_gather,
                        "l2": "no flush: per-step inputs (13.5 GB grads + 81 GB/div(OS) state) >> 126 MB L2",
                        "intra_inter_gap": "not emulated: one NVSwitch box, intra/inter are labels"},
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roof, "step_roofline": step_roof, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(prof["kernel_launches"]),
             "clocks": clk,
             "per_step": {"sent_intra_bytes": stats["sent_intra"], "sent_inter_bytes": stats["sent_inter"],

@@ -378,6 +378,10 @@ typedef struct {
    * in the rounds' data movement, and in the launch-final barrier */
   int64_t traced_launches;
   double traced_barrier_ms, traced_work_ms, traced_final_ms;
+  /* algorithmic HBM bytes of this GPU in the timed launches: Adam = 26 B +
+   * 2 B per g_hat input (fused final hop) + 2 B per fused-gather push, per
+   * element; collectives = 2 B per task input + 2 B per output element */
+  int64_t adam_hbm_bytes, comm_hbm_bytes;
 } paro_profile_t;
 
 paro_status_t paro_profile_start(paro_plan_t plan, int max_launches);

@@ -66,6 +66,9 @@ struct DevLaunch {
   std::vector<uint64_t> round_peers;         // [round] barrier peers before it
   int max_in = 1;          // largest fold input count (TMA stage sizing)
   int64_t bytes = 0;       // bytes the local rank(s) send in this launch
+  int64_t hbm = 0;         // algorithmic HBM bytes of the local rank(s)' tasks: each input
+                           // read once (a peer's input is read from its HBM; by symmetry
+                           // the same bytes a peer reads here) + the output written
   int64_t round_off = 0;   // index into the plan's DRound array
   int nrounds = 0;
   int final_barrier = 0;
@@ -116,6 +119,7 @@ struct paro_plan {
   std::vector<cudaEvent_t> prof_ev;       // 2 per launch
   std::vector<int> prof_kind;             // 0 adam, 1 comm
   std::vector<int64_t> prof_amount;       // adam: elements; comm: bytes sent
+  std::vector<int64_t> prof_hbm;          // algorithmic HBM bytes of the launch (this GPU)
   int prof_used = 0;
   int64_t prof_steps = 0, prof_launches = 0;
   uint64_t* d_trace = nullptr;            // [kTraceLaunches][grid][kTraceSlots]
@@ -266,6 +270,11 @@ paro_status_t upload_schedule(PlanT* p) {
           }
           if (t.dst.rank != x && (ctx->mode != MODE_REAL || x == ctx->rank)) dl.bytes += 2 * t.n;
         }
+    for (int r = 0; r < R; ++r)
+      for (int x = 0; x < pl.N; ++x) {
+        if (ctx->mode == MODE_REAL && x != ctx->rank) continue;
+        for (const Task& t : L.rounds[r][x]) dl.hbm += 2 * t.n * (t.nin + 1);
+      }
     dl.final_peers = (ctx->mode == MODE_REAL) ? L.barrier_peers(R, ctx->rank) : 0;
     // copy engines: every task a plain 1-input bit copy
     bool pure = p->opts.copy_engine != 0 && R > 0;
@@ -302,6 +311,7 @@ paro_status_t upload_schedule(PlanT* p) {
           const DTask d = resolve(p, t, x, -1);
           dl.copies[r].push_back({d.dst, d.in[0], (size_t)t.n * 2});
           if (t.in[0].rank != x) dl.bytes += 2 * t.n;
+          dl.hbm += 4 * t.n;
         }
       }
     return dl;
@@ -338,11 +348,12 @@ paro_status_t upload_schedule(PlanT* p) {
 }
 
 // Record the start event of a timed launch; returns the slot or -1.
-int prof_begin(PlanT* p, cudaStream_t s, int kind, int64_t amount) {
+int prof_begin(PlanT* p, cudaStream_t s, int kind, int64_t amount, int64_t hbm = 0) {
   if (!p->prof || 2 * (p->prof_used + 1) > (int)p->prof_ev.size()) return -1;
   const int k = p->prof_used++;
   p->prof_kind[k] = kind;
   p->prof_amount[k] = amount;
+  p->prof_hbm[k] = hbm;
   cudaEventRecord(p->prof_ev[2 * k], s);
   return k;
 }
@@ -390,7 +401,7 @@ paro_status_t run_dma_launch(PlanT* p, const DevLaunch& dl, cudaStream_t s, int*
   for (size_t r = 0; r < dl.copies.size(); ++r) {
     paro_status_t st = barrier2(p, dl.round_peers[r], s, nlaunch);
     if (st != PARO_OK) return st;
-    const int k = prof_begin(p, s, 1, r == 0 ? dl.bytes : 0);
+    const int k = prof_begin(p, s, 1, r == 0 ? dl.bytes : 0, r == 0 ? dl.hbm : 0);
     for (const CopyOp& c : dl.copies[r]) CK(cudaMemcpyAsync(c.dst, c.src, c.bytes, cudaMemcpyDeviceToDevice, s));
     prof_end(p, s, k);
   }
@@ -424,7 +435,7 @@ paro_status_t run_launch(PlanT* p, const DevLaunch& dl, int* nlaunch) {
     a.bar.arrive = reinterpret_cast<unsigned long long*>(hdr + 512);
     a.bar.err = reinterpret_cast<int*>(hdr + 520);
     p->arrive_base += (unsigned long long)(dl.nrounds + dl.final_barrier) * grid;
-    const int k = prof_begin(p, ctx->comm, 1, dl.bytes);
+    const int k = prof_begin(p, ctx->comm, 1, dl.bytes, dl.hbm);
     if (p->prof && p->d_trace && (int)p->trace_nrounds.size() < kTraceLaunches) {
       a.trace = p->d_trace + (size_t)p->trace_nrounds.size() * grid * kTraceSlots;
       p->trace_nrounds.push_back(dl.nrounds);
@@ -438,7 +449,7 @@ paro_status_t run_launch(PlanT* p, const DevLaunch& dl, int* nlaunch) {
     for (int r = 0; r < dl.nrounds; ++r) {
       a.rounds = p->d_rounds + dl.round_off + r;
       a.nrounds = 1;
-      const int k = prof_begin(p, ctx->comm, 1, r == 0 ? dl.bytes : 0);
+      const int k = prof_begin(p, ctx->comm, 1, r == 0 ? dl.bytes : 0, r == 0 ? dl.hbm : 0);
       if (p->opts.comm_impl == 0) CK(launch_rounds_tma(a, grid, dl.max_in, ctx->comm));
       else CK(launch_rounds(a, grid, 0, ctx->comm));
       prof_end(p, ctx->comm, k);
@@ -1148,9 +1159,15 @@ paro_status_t step_impl(PlanT* p, const void* const* grads, void* const* params,
       ++launches;
       return PARO_OK;
     }
-    int64_t elems = 0;
-    for (int i = 0; i < aa.nseg; ++i) elems += 8 * aa.seg[i].n8;
-    const int pk = prof_begin(p, ctx->comp, 0, elems);
+    int64_t elems = 0, hbm = 0;
+    for (int i = 0; i < aa.nseg; ++i) {
+      elems += 8 * aa.seg[i].n8;
+      // master/m/v read + written (24 B), bf16 parameter written (2 B), every
+      // g_hat input read once (2 B each: local, or by symmetry served to a peer),
+      // every fused-gather push (2 B: by symmetry, a peer's push lands here)
+      hbm += 8 * aa.seg[i].n8 * (26 + 2 * aa.seg[i].gnin + 2 * aa.seg[i].npush);
+    }
+    const int pk = prof_begin(p, ctx->comp, 0, elems, hbm);
     // TMA-pipelined Adam (bulk copies also pull the fused hop's NVLink-peer
     // inputs: tools/tma_peer_test.cu measured 782 GB/s); LSU kernel on request.
     // while collectives run beside it (real N > 1) Adam keeps ~120 KB of shared
@@ -1530,6 +1547,7 @@ paro_status_t paro_profile_start(paro_plan_t p, int max_launches) {
   for (auto& e : p->prof_ev) CK(cudaEventCreate(&e));
   p->prof_kind.assign(max_launches, 0);
   p->prof_amount.assign(max_launches, 0);
+  p->prof_hbm.assign(max_launches, 0);
   p->prof_used = 0;
   p->prof_steps = 0;
   p->prof_launches = 0;
@@ -1555,10 +1573,12 @@ paro_status_t paro_profile_stop(paro_plan_t p, paro_profile_t* out) {
       out->adam_ms += ms;
       out->adam_launches += 1;
       out->adam_elems += p->prof_amount[k];
+      out->adam_hbm_bytes += p->prof_hbm[k];
     } else {
       out->comm_ms += ms;
       out->comm_launches += 1;
       out->comm_bytes += p->prof_amount[k];
+      out->comm_hbm_bytes += p->prof_hbm[k];
     }
   }
   out->steps = p->prof_steps;

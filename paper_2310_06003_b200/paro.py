@@ -71,7 +71,8 @@ class paro_profile_t(C.Structure):
     _fields_ = [("adam_ms", C.c_double), ("comm_ms", C.c_double), ("adam_launches", C.c_int64),
                 ("comm_launches", C.c_int64), ("adam_elems", C.c_int64), ("comm_bytes", C.c_int64),
                 ("steps", C.c_int64), ("kernel_launches", C.c_int64), ("traced_launches", C.c_int64),
-                ("traced_barrier_ms", C.c_double), ("traced_work_ms", C.c_double), ("traced_final_ms", C.c_double)]
+                ("traced_barrier_ms", C.c_double), ("traced_work_ms", C.c_double), ("traced_final_ms", C.c_double),
+                ("adam_hbm_bytes", C.c_int64), ("comm_hbm_bytes", C.c_int64)]
 
 
 class paro_advise_in_t(C.Structure):
