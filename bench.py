@@ -52,6 +52,10 @@ def parse(argv=None):
     ap.add_argument("--fuse-gather", default="auto", choices=["auto", "always", "never"],
                     help="parameter all-gather inside Adam (one-ring restores)")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-mode", default="stream", choices=["stream", "pack"],
+                    help="stream: a grad_slots plan whose producer copies each bucket host->device on the "
+                         "copy engines while the step runs (paro_step_streamed); pack: per-tensor pinned "
+                         "host pointers read by the pack kernel (paro_step)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args(argv)
@@ -323,6 +327,19 @@ def run_ours(args):
         for s in sizes:
             gptrs.append(host.data_ptr() + 2 * ((o % span) // 8 * 8))
             o += s
+        eplan, producer = plan, None
+        if args.e2e_mode == "stream":
+            # same strategy / split / kernels, gradients streamed bucket by bucket from pinned host
+            # memory by the copy engines, overlapped with the reductions and updates of earlier buckets
+            plan.close()
+            eplan = paro.Plan(ctx, args.strategy, sizes, grad_slots=4, **plan_kwargs(args, stream.cuda_stream))
+            eplan.opt_state_init(rank, ptrs[0], seed=SEED)
+            rt = _cudart()
+            bspan = max(8, cap - info["bucket_elems"])
+
+            def producer(r, b, b0, b1, dst, strm):
+                src = host.data_ptr() + 2 * ((b0 % bspan) // 8 * 8)
+                assert rt.cudaMemcpyAsync(dst, src, 2 * (b1 - b0), 1, strm) == 0
         barrier()
         torch.cuda.synchronize()
         t0 = torch.cuda.Event(enable_timing=True)
@@ -330,8 +347,11 @@ def run_ours(args):
         t0.record(stream)
         for _ in range(args.e2e_steps):
             step += 1
-            plan.step(ptrs, LR, step, grads=gptrs)
-            plan.stats()           # D2H of the step's grad norm + nonfinite flag (12 B)
+            if producer is not None:
+                eplan.step_streamed(ptrs, LR, step, producer=producer)
+            else:
+                eplan.step(ptrs, LR, step, grads=gptrs)
+            eplan.stats()          # D2H of the step's grad norm + nonfinite flag (12 B)
         t1.record(stream)
         torch.cuda.synchronize()
         ems = t0.elapsed_time(t1) / args.e2e_steps
@@ -341,8 +361,13 @@ def run_ours(args):
             ems = float(tt.item())
         e2e = {"value": info["psi"] / (ems / 1000.0), "unit": "params/s", "h2d_bytes_per_step": 2 * info["psi"],
                "d2h_bytes_per_step": 12, "ms_per_step": ems,
-               "path": "paro_step with per-tensor pinned-host gradient pointers (zero-copy pack kernel "
-                       "over PCIe from a <=2 GiB pinned staging area) + paro_step_stats read-back"}
+               "path": ("paro_step_streamed (grad_slots = 4): each bucket's gradients copied host->device "
+                                "by the copy engines from a <=2 GiB pinned staging area while earlier buckets "
+                                "reduce and update, + paro_step_stats read-back") if producer is not None else
+                               ("paro_step with per-tensor pinned-host gradient pointers (zero-copy pack kernel "
+                                "over PCIe from a <=2 GiB pinned staging area) + paro_step_stats read-back")}
+        if eplan is not plan:
+            plan = eplan
         del host
 
     cpu = None
@@ -379,6 +404,16 @@ def run_ours(args):
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def _cudart():
+    import ctypes
+    import glob
+    import nvidia.cuda_runtime as cr
+    rt = ctypes.CDLL(glob.glob(os.path.join(list(cr.__path__)[0], "lib", "libcudart.so*"))[0])
+    rt.cudaMemcpyAsync.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_void_p]
+    rt.cudaMemcpyAsync.restype = ctypes.c_int
+    return rt
 
 
 def _copy_from_ptr(dst_tensor, src_ptr):

@@ -966,7 +966,7 @@ static paro_status_t opt_init_impl(paro_plan_t p, int rank, const float* src, ui
   if (s != PARO_OK) return s;
   if (ctx->mode == MODE_PLANNER) return fail(PARO_ERR_STATE, "planning-only context");
   const Planner& pl = *p->pl;
-  if (!pl.opt.params_only && (!st || !st->master || !st->m || !st->v))
+  if (!pl.opt.params_only && pl.os_numel > 0 && (!st || !st->master || !st->m || !st->v))
     return fail(PARO_ERR_INVALID, "null opt state");
   if (!is_local(p, rank)) return fail(PARO_ERR_INVALID, "rank is not local to this process");
   uint16_t* pbuf = reinterpret_cast<uint16_t*>(data_ptr(p, rank, BUF_PARAM, 0));
@@ -1060,7 +1060,7 @@ paro_status_t step_impl(PlanT* p, const void* const* grads, void* const* params,
   const Planner& pl = *p->pl;
   const int nl = (int)p->local.size();
   const int np = (int)pl.param_sizes.size();
-  for (int i = 0; i < nl; ++i)
+  for (int i = 0; i < nl && pl.os_numel > 0; ++i)   // an empty model (psi = 0) has no state
     if (!opt_state[i].master || !opt_state[i].m || !opt_state[i].v)
       return fail(PARO_ERR_INVALID, "null opt_state array");
   if (grads) {
@@ -1124,6 +1124,7 @@ paro_status_t step_impl(PlanT* p, const void* const* grads, void* const* params,
   aa.skip = two ? p->d_skip : nullptr;
   auto adam_bucket = [&](int b0, int b1, bool norm_only = false) -> paro_status_t {
     // one Adam (or phase-1 norm) launch over buckets [b0, b1) and every local rank
+    if (b0 >= b1) return PARO_OK;   // empty model
     aa.nseg = 0;
     for (int li = 0; li < nl; ++li) {
       const int r = p->local[li];

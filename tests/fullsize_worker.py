@@ -55,15 +55,20 @@ def main():
     sizes = llama_param_sizes(args.model)
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
-    plan = paro.Plan(ctx, args.strategy, sizes, **bench.plan_kwargs(args, stream.cuda_stream))
+    slots = cfg.get("grad_slots", 0)          # > 0: streamed gradients (largest models)
+    plan = paro.Plan(ctx, args.strategy, sizes, grad_slots=slots, **bench.plan_kwargs(args, stream.cuda_stream))
     info = plan.info()
     st = [torch.empty(info["os_numel"], dtype=torch.float32, device="cuda") for _ in range(3)]
     ptrs = [[x.data_ptr() for x in st]]
     plan.opt_state_init(rank, ptrs[0], seed=SEED)
-    plan.synth_grads(rank, SEED, 1)           # bench: gradients of step 1 stay resident
+    if not slots:
+        plan.synth_grads(rank, SEED, 1)       # bench: gradients of step 1 stay resident
     steps = cfg.get("steps", 2)
     for s in range(1, steps + 1):
-        plan.step(ptrs, bench.LR, s)
+        if slots:
+            plan.step_streamed(ptrs, bench.LR, s, seed=SEED, grad_step=1)
+        else:
+            plan.step(ptrs, bench.LR, s)
     stats = plan.stats()
     torch.cuda.synchronize()
 
@@ -71,7 +76,7 @@ def main():
     buckets = sorted(set(cfg.get("buckets", [0, nb // 2, nb - 1])))
     W = cfg.get("window", 2048)
     pbuf = plan.buffer(rank, 1)
-    res = {"M": M, "strategy": args.strategy, "bucket_elems": info["bucket_elems"], "n_buckets": nb,
+    res = {"M": M, "strategy": args.strategy, "model": args.model, "bucket_elems": info["bucket_elems"], "n_buckets": nb,
            "psi_pad": info["psi_pad"], "stats": stats, "send": plan.send_bytes(rank), "os": [], "p": [],
            "bucket_ranges": [plan.bucket_range(b) for b in range(nb)],
            "os_ranges": [plan.shard_range("OS", rank, b) for b in range(nb)],

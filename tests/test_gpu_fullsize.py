@@ -84,7 +84,7 @@ def _run(tmp_path, world, cfg):
         res = json.load(open(tmp_path / f"r{rank}.json"))
         d = np.load(tmp_path / f"r{rank}.npz")
         code, M = res["strategy"], res["M"]
-        lay = L.Layout(llama_param_sizes("7B"), world, M, res["bucket_elems"])
+        lay = L.Layout(llama_param_sizes(res["model"]), world, M, res["bucket_elems"])
         # shard map and layout, every bucket, bit-exact
         assert res["psi_pad"] == lay.psi_pad and res["n_buckets"] == len(lay.buckets)
         assert [tuple(x) for x in res["bucket_ranges"]] == [(s, s + n) for (s, n) in lay.buckets]
@@ -121,3 +121,12 @@ def test_fullsize_7b_multi_gpu(tmp_path):
     """N = 2 / 4 (2x1 / 2x2): `bench.py --gpus N` under torchrun."""
     world = 4 if _ngpu() >= 4 else 2
     _run(tmp_path, world, {"steps": 2})
+
+
+@pytest.mark.skipif(_ngpu() < 4, reason="needs 4 GPUs")
+def test_fullsize_30b_streamed_gradients(tmp_path):
+    """The largest workload (BASELINE config 4's LLaMA-30B list, OS = G
+    strategy GGG at 2x2, 136 GB per rank) with streamed gradients (4 slots):
+    sampled windows bit-exact, shard map and bytes exact."""
+    _run(tmp_path, 4, {"steps": 2, "grad_slots": 4,
+                       "bench_args": ["--model", "30B", "--strategy", "GGG", "--group-size", "2"]})

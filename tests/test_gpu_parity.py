@@ -728,3 +728,40 @@ def test_streamed_step_with_clipping(N, M):
             assert abs(st["grad_norm"] ** 2 - per[t - 1][5]) <= 1e-12 * per[t - 1][5]
         _check_against_dp(run, lay, ref)
         run.close()
+
+
+# --------------------------------------------------------------------- empty / zero-size inputs
+@pytest.mark.parametrize("sizes", [[], [0], [0, 5, 0, 77, 0]])
+def test_empty_model_and_zero_size_tensors(sizes):
+    """An empty parameter list or zero-size tensors: the plan and step run
+    (nothing to do for psi = 0; zero-size tensors take no room and may have
+    NULL pointers), and the rest still matches unsharded DP."""
+    paro = _paro()
+    N, M, B = 8, 4, 8 * 64 * 2
+    lay = L.Layout(sizes, N, M, B)
+    ref = _dp_reference(lay, 2) if lay.psi else None
+    for code in ("NNN", "IIG", "GGG", "NIG"):
+        run = EmuRun(N, M, code, sizes, B)
+        assert run.info["psi"] == sum(sizes)
+        for t in range(1, 3):
+            if lay.psi:
+                run.set_grads(t)
+                st = run.step(t)
+            else:
+                run.pl.step([[0, 0, 0]] * N, LR, t)
+                st = run.pl.stats()
+                assert st["grad_norm"] == 0.0 and st["nonfinite"] == 0
+        if lay.psi:
+            _check_against_dp(run, lay, ref)
+            # per-tensor pointers with NULL for the zero-size tensors (pack path)
+            ptrs = []
+            for r in range(N):
+                g = torch.from_numpy(grad_bits(r, 3, 0, lay.psi).view(np.int16)).cuda()
+                o = 0
+                for s in sizes:
+                    ptrs.append(g.data_ptr() + 2 * o if s else 0)
+                    o += s
+                run.__dict__.setdefault("_keep", []).append(g)
+            run.pl.step(run.ptrs(), LR, 3, grads=ptrs)
+            torch.cuda.synchronize()
+        run.close()
