@@ -43,9 +43,9 @@ def parse(argv=None):
     ap.add_argument("--strategy", default="IIG")
     ap.add_argument("--group-size", type=int, default=0, help="M; default N/2 for N>=4, else 1")
     ap.add_argument("--topology", default="ho", choices=["ho", "two_step", "flat", "direct", "nccl"])
-    ap.add_argument("--bucket", type=int, default=1 << 28)
+    ap.add_argument("--bucket", type=int, default=1 << 29)
     ap.add_argument("--comm-ctas", type=int, default=148)
-    ap.add_argument("--depth", type=int, default=2)
+    ap.add_argument("--depth", type=int, default=1)
     ap.add_argument("--transport", default="pull", choices=["pull", "push"])
     ap.add_argument("--adam-impl", default="auto", choices=["auto", "lsu", "tma_store"])
     ap.add_argument("--comm-impl", default="tma", choices=["tma", "lsu"])
