@@ -58,6 +58,7 @@ def parse(argv=None):
                          "host pointers read by the pack kernel (paro_step)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-ho-ring", action="store_true", help="skip the 1 GiB HO-Ring all-reduce busbw (N > 1)")
     return ap.parse_args(argv)
 
 
@@ -309,6 +310,13 @@ def run_ours(args):
                  "note": "algorithmic bytes of this rank's launches (Adam + collective tasks) per step; "
                          "NVLink = bytes this rank sends per step (each direction)"}
 
+    # ---- HO-Ring bus bandwidth (BASELINE metric's second half, config 5): a 1 GiB bf16
+    # all-reduce through the library (NNN plan: hierarchical HO-RS + HO-AG with the bf16 hop
+    # arithmetic, paro_collective) beside NCCL's all_reduce on the same bytes, N > 1 only
+    ho = None
+    if world > 1 and not args.no_ho_ring:
+        ho = ho_ring_busbw(paro, ctx, stream, dist, world, M, rank, args)
+
     # ---- end to end: gradients from pinned host memory each step (read by the
     # pack kernel over PCIe), device->host read of the step's norm/flag
     e2e = None
@@ -391,7 +399,7 @@ def run_ours(args):
                        "fuse_gather": args.fuse_gather,
                        "l2": "no flush: per-step inputs (13.5 GB grads + 81 GB/div(OS) state) >> 126 MB L2",
                        "intra_inter_gap": "not emulated: one NVSwitch box, intra/inter are labels"},
-            "roofline": roof, "step_roofline": step_roof, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roof, "step_roofline": step_roof, "ho_ring": ho, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(prof["kernel_launches"]),
             "clocks": clk,
             "per_step": {"sent_intra_bytes": stats["sent_intra"], "sent_inter_bytes": stats["sent_inter"],
@@ -404,6 +412,43 @@ def run_ours(args):
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def ho_ring_busbw(paro, ctx, stream, dist, world, M, rank, args, nbytes=1 << 30, iters=10):
+    """busbw = S * 2(N-1)/N / t (nccl-tests convention), t = max over ranks of the CUDA-event time."""
+    import torch
+    elems = nbytes // 2
+
+    def timeit(fn):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(iters):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = torch.tensor([e0.elapsed_time(e1) / iters], dtype=torch.float64, device="cuda")
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        return float(ms.item())
+
+    factor = 2 * (world - 1) / world
+    pl = paro.Plan(ctx, "NNN", [elems], bucket_elems=min(elems, 1 << 28), topology="ho",
+                   stream=stream.cuda_stream, transport=args.transport, comm_impl=args.comm_impl,
+                   fuse_gather="never")
+    pl.synth_grads(rank, SEED, 1)
+    ms = timeit(lambda: pl.collective(0))
+    pl.close()
+    x = torch.ones(elems, dtype=torch.bfloat16, device="cuda")
+    ms_nccl = timeit(lambda: dist.all_reduce(x))
+    del x
+    bw = nbytes * factor / (ms / 1e3) / 1e9
+    return {"op": "all-reduce (HO-RS + HO-AG, bf16 hops in canonical order)", "bytes": nbytes,
+            "groups": f"{world // M}x{M}", "ms": ms, "busbw_GBps": bw, "peak_GBps": 770.0, "frac": bw / 770.0,
+            "nccl_allreduce_busbw_GBps": nbytes * factor / (ms_nccl / 1e3) / 1e9,
+            "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s per direction"}
 
 
 def _cudart():
