@@ -42,6 +42,7 @@ struct BarrierCtx {
   uint64_t* const* peer_slot;   // [N] device array: &flags_of_peer_x[me]
   uint64_t* my_flags;           // NULL => emulated mode (no barriers)
   unsigned long long* arrive;
+  unsigned long long* go;       // opened by the last-arriving CTA once the peers' flags are in
   int* err;
 };
 
@@ -58,6 +59,7 @@ struct RoundsArgs {
   double inter_bytes_per_ns;    // per-CTA pacing of inter-group tiles (0 = off)
   uint64_t serial;              // launch serial (same sequence on every rank)
   unsigned long long arrive_base;
+  int sys_fence_all;            // every CTA fences at sys scope (launch stores into peer memory)
   BarrierCtx bar;
 };
 

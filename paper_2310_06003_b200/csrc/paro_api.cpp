@@ -387,6 +387,7 @@ paro_status_t barrier2(PlanT* p, uint64_t peers, cudaStream_t s, int* nlaunch) {
   a.bar.peer_slot = p->d_peer_slot2;
   a.bar.my_flags = reinterpret_cast<uint64_t*>(hdr + 1024);
   a.bar.arrive = reinterpret_cast<unsigned long long*>(hdr + 1536);
+  a.bar.go = reinterpret_cast<unsigned long long*>(hdr + 1544);
   a.bar.err = reinterpret_cast<int*>(hdr + 520);
   p->arrive_base2 += 1;
   CK(launch_rounds(a, 1, 32, s));
@@ -433,7 +434,9 @@ paro_status_t run_launch(PlanT* p, const DevLaunch& dl, int* nlaunch) {
     a.bar.peer_slot = p->d_peer_slot;
     a.bar.my_flags = reinterpret_cast<uint64_t*>(hdr);
     a.bar.arrive = reinterpret_cast<unsigned long long*>(hdr + 512);
+    a.bar.go = reinterpret_cast<unsigned long long*>(hdr + 528);
     a.bar.err = reinterpret_cast<int*>(hdr + 520);
+    a.sys_fence_all = p->pl->opt.push ? 1 : 0;
     p->arrive_base += (unsigned long long)(dl.nrounds + dl.final_barrier) * grid;
     const int k = prof_begin(p, ctx->comm, 1, dl.bytes, dl.hbm);
     if (p->prof && p->d_trace && (int)p->trace_nrounds.size() < kTraceLaunches) {

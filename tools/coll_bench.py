@@ -26,6 +26,8 @@ def main():
     ap.add_argument("--transport", default="pull")
     ap.add_argument("--comm-impl", default="tma")
     ap.add_argument("--inter-gbps", type=float, default=0.0, help="emulated inter-group link (0 = off)")
+    ap.add_argument("--trace", action="store_true",
+                    help="per-launch device trace of the collective (barrier / work / final-barrier us)")
     ap.add_argument("--op", default="ar", choices=["ar", "ag"],
                     help="ar: gradient all-reduce (NNN plan, reduce launches); ag: parameter all-gather "
                          "(NNG plan, gather launches) as in the paper's section 4.4")
@@ -58,8 +60,8 @@ def main():
         dist.all_reduce(ms, op=dist.ReduceOp.MAX)
         return float(ms.item())
 
-    for mb in [int(x) for x in a.sizes_mb.split(",")]:
-        nbytes = mb << 20
+    for mb in [float(x) for x in a.sizes_mb.split(",")]:
+        nbytes = int(mb * (1 << 20))
         elems = nbytes // 2
         row = {"bytes": nbytes, "groups": f"{world // M}x{M}", "n_gpus": world, "inter_gbps": a.inter_gbps}
         factor = 2 * (world - 1) / world if a.op == "ar" else (world - 1) / world
@@ -72,6 +74,18 @@ def main():
             pl.synth_grads(rank, 1234, 1)
             ms = timeit(lambda: pl.collective(what))
             row[topo] = {"ms": round(ms, 4), "busbw_GBps": round(nbytes * factor / (ms / 1e3) / 1e9, 1)}
+            if a.trace:
+                pl.profile_start(64)
+                for _ in range(4):
+                    pl.collective(what)
+                torch.cuda.synchronize()
+                pr = pl.profile_stop()
+                nl = max(1, pr["traced_launches"])
+                row[topo]["trace_us_per_launch"] = {
+                    "event": round(1000 * pr["comm_ms"] / max(1, pr["comm_launches"]), 2),
+                    "barrier": round(1000 * pr["traced_barrier_ms"] / nl, 2),
+                    "work": round(1000 * pr["traced_work_ms"] / nl, 2),
+                    "final": round(1000 * pr["traced_final_ms"] / nl, 2)}
             pl.close()
         x = torch.ones(elems, dtype=torch.bfloat16, device="cuda")
         if a.op == "ar":
