@@ -1599,12 +1599,17 @@ paro_status_t paro_profile_stop(paro_plan_t p, paro_profile_t* out) {
       auto mn = [&](int slot) { uint64_t m = ~0ull; for (int b = 0; b < G; ++b) m = std::min(m, t[b * kTraceSlots + slot]); return m; };
       uint64_t prev = mn(0);
       const int R = std::min(p->trace_nrounds[l], (kTraceSlots - 2) / 2);
+      const bool dump = std::getenv("PARO_TRACE_DUMP") != nullptr;
+      if (dump) std::fprintf(stderr, "[paro trace] rank %d launch %zu: cta start spread %.2f us", p->ctx->rank, l,
+                             1e-3 * (double)(mx(0) - mn(0)));
       for (int r = 0; r < R; ++r) {
         const uint64_t be = mx(1 + 2 * r), we = mx(2 + 2 * r);
         bar += (double)(be - prev);
         work += (double)(we - be);
+        if (dump) std::fprintf(stderr, " | r%d bar %.2f work %.2f", r, 1e-3 * (double)(be - prev), 1e-3 * (double)(we - be));
         prev = we;
       }
+      if (dump) std::fprintf(stderr, " | end %.2f\n", 1e-3 * (double)(mx(kTraceSlots - 1) - prev));
       fin += (double)(mx(kTraceSlots - 1) - prev);
     }
     out->traced_launches = (int64_t)p->trace_nrounds.size();
