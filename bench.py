@@ -48,7 +48,7 @@ def parse(argv=None):
     ap.add_argument("--depth", type=int, default=1)
     ap.add_argument("--transport", default="pull", choices=["pull", "push"])
     ap.add_argument("--adam-impl", default="auto", choices=["auto", "lsu", "tma_store"])
-    ap.add_argument("--comm-impl", default="tma", choices=["tma", "lsu"])
+    ap.add_argument("--comm-impl", default="tma_store", choices=["tma", "lsu", "tma_store"])
     ap.add_argument("--fuse-gather", default="auto", choices=["auto", "always", "never"],
                     help="parameter all-gather inside Adam (one-ring restores)")
     ap.add_argument("--e2e-steps", type=int, default=3)
@@ -292,8 +292,8 @@ def run_ours(args):
         alg = prof["comm_bytes"] / max(1, prof["comm_launches"])
         ach = alg / (comm_ms / 1000.0) / 1e9
         peak = 770.0
-        roof = {"bound": "nvlink", "kernel": ("rounds_tma_kernel" if args.comm_impl == "tma" else "rounds_kernel")
-                + " (collective rounds: NVLink pull + hop)",
+        roof = {"bound": "nvlink", "kernel": {"tma": "rounds_tma_kernel<false>", "tma_store": "rounds_tma_kernel<true>"}.get(
+                    args.comm_impl, "rounds_kernel") + " (collective rounds: NVLink pull + hop)",
                 "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
                 "traffic": None, "algorithmic_bytes_per_launch": alg,
                 "launch_ms": comm_ms, "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s/dir",

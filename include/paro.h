@@ -90,8 +90,13 @@ typedef struct {
                           * results leave through bulk copies too when N = 1 (or   *
                           * emulated), through thread stores otherwise;            *
                           * 1: the LSU (ld.global) kernel; 2: TMA both ways always */
-  int comm_impl;         /* 0 (default): collective rounds move operands with TMA  *
-                          * bulk copies into shared memory; 1: LSU kernel           */
+  int comm_impl;         /* 2 (default): collective rounds move operands with TMA  *
+                          * bulk copies into shared memory and the folded tile     *
+                          * leaves through a bulk copy too (measured 1-10 % faster *
+                          * in the full step at 2x1 / 2x2, profiles/r01/           *
+                          * sweep_comm_store_*.jsonl); 0: TMA loads, thread        *
+                          * stores; 1: LSU kernel.  Same bits.  Other values:      *
+                          * PARO_ERR_INVALID.                                      */
   float inter_gbps;      /* > 0: emulate a slow inter-group link — each rank's     *
                           * inter-group transfers are paced to this many GB/s (TMA *
                           * rounds kernel; the final hop is then not fused into    *

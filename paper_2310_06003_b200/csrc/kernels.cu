@@ -594,6 +594,13 @@ __device__ __forceinline__ bool rt_tile(const RoundsArgs& a, const DRound& rd, i
   return false;
 }
 
+// kBulk: the folded tile goes back into its shared-memory stage (in place over
+// input 0) and leaves through one cp.async.bulk global<-shared per tile (the
+// bulk-copy engine keeps the NVLink stores of the push transport in flight
+// without LSU slots); the stage is refilled one tile later, after
+// wait_group.read, and every bulk store has completed before the next peer
+// barrier publishes the round.
+template <bool kBulk>
 __global__ void __launch_bounds__(kRtThreads) rounds_tma_kernel(const RoundsArgs a, int max_in) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ uint64_t bars[kRtStages];
@@ -646,14 +653,14 @@ __global__ void __launch_bounds__(kRtThreads) rounds_tma_kernel(const RoundsArgs
       int64_t e0;
       int ne;
       rt_tile(a, rd, blockIdx.x + k * gridDim.x, tk, e0, ne);
-      const unsigned char* base = smem + slot * stage_bytes;
+      unsigned char* base = smem + slot * stage_bytes;
       const int nin = tk->nin;
       const uint32_t raw = tk->rawmask;
       uint4* dst = reinterpret_cast<uint4*>(tk->dst + e0);
       for (int u = threadIdx.x; u < ne / 8; u += kRtThreads) {
         const uint4 v0 = reinterpret_cast<const uint4*>(base)[u];
-        if (nin == 1 && !(raw & 1u)) {
-          __stcg(dst + u, v0);
+        if (nin == 1 && !(raw & 1u)) {   // plain copy: the stage already holds the result
+          if (!kBulk) __stcg(dst + u, v0);
           continue;
         }
         float acc[8];
@@ -665,12 +672,28 @@ __global__ void __launch_bounds__(kRtThreads) rounds_tma_kernel(const RoundsArgs
           if ((raw >> i) & 1u) scale_round8(x, a.alpha);
           hop8(acc, x);
         }
-        __stcg(dst + u, pack8(acc));
+        if (kBulk) reinterpret_cast<uint4*>(base)[u] = pack8(acc);   // in place: this thread read it
+        else __stcg(dst + u, pack8(acc));
       }
-      __syncthreads();   // stage consumed by every thread: refill it
-      if (threadIdx.x == 0 && k + kRtStages < mine) issue(k + kRtStages);
+      if (kBulk) {
+        fence_proxy_async_smem();   // this thread's smem writes -> visible to the bulk-copy engine
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          bulk_s2g(tk->dst + e0, base, (uint32_t)ne * 2);
+          bulk_commit();
+          bulk_wait_read<1>();      // the previous tile's store has read its stage: refill it
+          if (k >= 1 && k - 1 + kRtStages < mine) issue(k - 1 + kRtStages);
+        }
+      } else {
+        __syncthreads();   // stage consumed by every thread: refill it
+        if (threadIdx.x == 0 && k + kRtStages < mine) issue(k + kRtStages);
+      }
     }
     cnt += (uint32_t)mine;
+    if (kBulk && threadIdx.x == 0) {   // the round's stores are complete (and the stages free)
+      bulk_wait_all();                 // before anyone reads them or the next round reuses
+      asm volatile("fence.proxy.async.global;" ::: "memory");   // the stages
+    }
     // tasks with many inputs: LSU path over the whole grid
     for (int ti = rd.t0; ti < rd.t1; ++ti)
       if (a.tasks[ti].nin > kRtMaxIn) run_task(a.tasks + ti, a.alpha);
@@ -847,7 +870,8 @@ int adam_block() { return kAdamBlock; }
 static cudaError_t set_carveouts() {
   static bool done = false;
   if (done) return cudaSuccess;
-  const void* fns[] = {(const void*)rounds_kernel, (const void*)rounds_tma_kernel, (const void*)adam_kernel,
+  const void* fns[] = {(const void*)rounds_kernel, (const void*)rounds_tma_kernel<false>,
+                       (const void*)rounds_tma_kernel<true>, (const void*)adam_kernel,
                        (const void*)adam_tma_kernel<false, 512>, (const void*)adam_tma_kernel<true, 512>,
                        (const void*)adam_tma_kernel<true, 256>};
   for (const void* f : fns) {
@@ -866,19 +890,23 @@ cudaError_t launch_rounds(const RoundsArgs& a, int grid, int block, cudaStream_t
   return cudaGetLastError();
 }
 
-cudaError_t launch_rounds_tma(const RoundsArgs& a, int grid, int max_in, cudaStream_t s) {
+cudaError_t launch_rounds_tma(const RoundsArgs& a, int grid, int max_in, cudaStream_t s, int bulk_store) {
   cudaError_t ec = set_carveouts();
   if (ec != cudaSuccess) return ec;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(rounds_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         kRtStages * kRtMaxIn * kRtTileB);
-    if (e != cudaSuccess) return e;
+    for (const void* f : {(const void*)rounds_tma_kernel<false>, (const void*)rounds_tma_kernel<true>}) {
+      cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           kRtStages * kRtMaxIn * kRtTileB);
+      if (e != cudaSuccess) return e;
+    }
     attr_set = true;
   }
   if (max_in < 1) max_in = 1;
   if (max_in > kRtMaxIn) max_in = kRtMaxIn;
-  rounds_tma_kernel<<<grid, kRtThreads, (size_t)kRtStages * max_in * kRtTileB, s>>>(a, max_in);
+  const size_t sm = (size_t)kRtStages * max_in * kRtTileB;
+  if (bulk_store) rounds_tma_kernel<true><<<grid, kRtThreads, sm, s>>>(a, max_in);
+  else rounds_tma_kernel<false><<<grid, kRtThreads, sm, s>>>(a, max_in);
   return cudaGetLastError();
 }
 

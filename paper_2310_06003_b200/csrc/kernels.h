@@ -108,7 +108,7 @@ struct PackEntry {     // one tensor slice: src/dst element pointers + count
 cudaError_t launch_rounds(const RoundsArgs& a, int grid, int block, cudaStream_t s);
 cudaError_t launch_adam(const AdamArgs& a, int grid, cudaStream_t s, int cap_two_per_sm);
 cudaError_t launch_adam_tma(const AdamArgs& a, int sms, cudaStream_t s, int smem_budget_kb, int tma_store);
-cudaError_t launch_rounds_tma(const RoundsArgs& a, int grid, int max_in, cudaStream_t s);
+cudaError_t launch_rounds_tma(const RoundsArgs& a, int grid, int max_in, cudaStream_t s, int bulk_store);
 cudaError_t launch_norm_finalize(const double* partials, int n, double* out, cudaStream_t s);
 // phase 1 of the two-phase step: block partials of sum (fold(gin) * s_g)^2 and
 // the non-finite flag, 2 bytes read per element, no update

@@ -444,7 +444,7 @@ paro_status_t run_launch(PlanT* p, const DevLaunch& dl, int* nlaunch) {
       p->trace_nrounds.push_back(dl.nrounds);
       p->trace_grid = grid;
     }
-    if (p->opts.comm_impl == 0) CK(launch_rounds_tma(a, grid, dl.max_in, ctx->comm));
+    if (p->opts.comm_impl != 1) CK(launch_rounds_tma(a, grid, dl.max_in, ctx->comm, p->opts.comm_impl == 2));
     else CK(launch_rounds(a, grid, 0, ctx->comm));
     prof_end(p, ctx->comm, k);
     ++*nlaunch;
@@ -453,7 +453,7 @@ paro_status_t run_launch(PlanT* p, const DevLaunch& dl, int* nlaunch) {
       a.rounds = p->d_rounds + dl.round_off + r;
       a.nrounds = 1;
       const int k = prof_begin(p, ctx->comm, 1, r == 0 ? dl.bytes : 0, r == 0 ? dl.hbm : 0);
-      if (p->opts.comm_impl == 0) CK(launch_rounds_tma(a, grid, dl.max_in, ctx->comm));
+      if (p->opts.comm_impl != 1) CK(launch_rounds_tma(a, grid, dl.max_in, ctx->comm, p->opts.comm_impl == 2));
       else CK(launch_rounds(a, grid, 0, ctx->comm));
       prof_end(p, ctx->comm, k);
       ++*nlaunch;
@@ -594,7 +594,7 @@ void paro_opts_default(paro_opts_t* o) {
   o->pipeline_depth = 2;
   o->pull_transport = 1;
   o->adam_impl = 0;
-  o->comm_impl = 0;
+  o->comm_impl = 2;
   o->inter_gbps = 0.f;
   o->grad_accum = 0;
   o->clip_norm = 0.f;
@@ -724,6 +724,7 @@ paro_status_t paro_plan(paro_ctx_t ctx, const char* strategy, const int64_t* par
   if (o.gather_windows < 0 || o.gather_windows > 64) return fail(PARO_ERR_INVALID, "gather_windows must be in [0, 64]");
   po.windows = o.gather_windows;
   if (o.fuse_gather < 0 || o.fuse_gather > 2) return fail(PARO_ERR_INVALID, "fuse_gather must be 0, 1 or 2");
+  if (o.comm_impl < 0 || o.comm_impl > 2) return fail(PARO_ERR_INVALID, "comm_impl must be 0, 1 or 2");
   po.fuse_gather = (o.inter_gbps > 0.f || o.topology == PARO_TOPO_NCCL) ? 0 : o.fuse_gather;
   // paced (emulated-gap) runs keep every transfer in the rounds kernel, which
   // paces them; the NCCL comparator has no copy-engine path

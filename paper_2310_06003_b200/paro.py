@@ -158,7 +158,7 @@ def check(status):
 # ---------------------------------------------------------------- helpers
 def make_opts(bucket_elems=1 << 26, topology="ho", beta1=0.9, beta2=0.95, eps=1e-8, weight_decay=0.0,
               loss_scale=1.0, comm_ctas=148, pipeline_depth=2, stream=None, transport="pull", adam_impl="auto",
-              comm_impl="tma", inter_gbps=0.0, grad_accum=False, clip_norm=0.0, skip_nonfinite=False, gather_windows=0,
+              comm_impl="tma_store", inter_gbps=0.0, grad_accum=False, clip_norm=0.0, skip_nonfinite=False, gather_windows=0,
               fuse_gather="auto", copy_engine=False, frozen=False, grad_slots=0):
     o = paro_opts_t()
     paro_opts_default(C.byref(o))
@@ -169,7 +169,7 @@ def make_opts(bucket_elems=1 << 26, topology="ho", beta1=0.9, beta2=0.95, eps=1e
     o.comm_ctas, o.pipeline_depth = int(comm_ctas), int(pipeline_depth)
     o.pull_transport = {"push": 0, "pull": 1}[transport]
     o.adam_impl = {"auto": 0, "lsu": 1, "tma_store": 2}[adam_impl]
-    o.comm_impl = {"tma": 0, "lsu": 1}[comm_impl]
+    o.comm_impl = {"tma": 0, "lsu": 1, "tma_store": 2}[comm_impl]
     o.inter_gbps = float(inter_gbps)
     o.grad_accum = 1 if grad_accum else 0
     o.clip_norm = float(clip_norm)

@@ -32,7 +32,7 @@ def main():
     codes = cfg.get("codes", ["NNN", "IIG", "NIG", "IGG", "GGG", "III", "INI", "NNG"])
     topos = cfg.get("topos", ["ho", "two_step", "direct"])
     transports = cfg.get("transports", ["push"])
-    comm_impl = cfg.get("comm_impl", "tma")
+    comm_impl = cfg.get("comm_impl", "tma_store")
     inter_gbps = cfg.get("inter_gbps", 0.0)
     sizes = cfg.get("sizes", [world * 64 * 40 + 24, 333])
     B = cfg.get("bucket", world * 64 * 12)

@@ -49,7 +49,8 @@ CODES = ["NNN", "NNI", "NNG", "NII", "NIG", "NGG", "INI", "ING", "III", "IIG", "
 
 
 @pytest.mark.skipif(_ngpu() < 2, reason="needs >= 2 GPUs")
-@pytest.mark.parametrize("variant", ["default", "paced_lsu", "accum", "clip", "copy_engine", "masked", "slots"])
+@pytest.mark.parametrize("variant", ["default", "paced_lsu", "accum", "clip", "copy_engine", "masked", "slots",
+                                     "tma_thread_store"])
 def test_real_ranks_match_oracle(tmp_path, variant):
     world = min(_ngpu(), 4)
     splits = [m for m in range(1, world + 1) if world % m == 0]
@@ -69,6 +70,8 @@ def test_real_ranks_match_oracle(tmp_path, variant):
                     "fuse_gather": "always"})
     if variant == "slots":       # streamed gradients: one bucket slot, reused by every bucket
         cfg.update({"grad_slots": 1, "topos": ["ho", "two_step", "direct"], "transports": ["pull", "push"]})
+    if variant == "tma_thread_store":   # rounds kernel with thread stores (comm_impl 0; the default bulk-copies out)
+        cfg.update({"topos": ["ho", "two_step", "direct"], "transports": ["push", "pull"], "comm_impl": "tma"})
     if variant == "masked":      # partial / PEFT training: trainable plan + frozen-parameter plan
         cfg.update({"sizes": [world * 64 * 40 + 24, 333, world * 64 * 9 + 5, 4096], "mask": [0, 1, 0, 1],
                     "topos": ["ho", "two_step"], "transports": ["pull"], "windows": 2})

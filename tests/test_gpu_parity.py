@@ -32,7 +32,7 @@ class EmuRun:
     """All ranks of one split on cuda:0 through the C ABI."""
 
     def __init__(self, N, M, code, sizes, B, topo="ho", depth=2, wd=0.0, loss_scale=1.0, transport="push",
-                 adam_impl="auto", comm_impl="tma", grad_accum=False, mode="emulated", clip_norm=0.0,
+                 adam_impl="auto", comm_impl="tma_store", grad_accum=False, mode="emulated", clip_norm=0.0,
                  skip_nonfinite=False, fuse_gather="auto", copy_engine=False):
         paro = _paro()
         if mode == "emulated":
@@ -151,7 +151,7 @@ def test_n1_ten_steps_bit_exact(wd, ls, adam_impl):
 CONFIG_4M = dict(sizes=[1 << 22], B=1 << 18)   # BASELINE config 1: 2^22 params, 16 buckets
 
 
-@pytest.mark.parametrize("comm_impl", ["tma", "lsu"])
+@pytest.mark.parametrize("comm_impl", ["tma", "lsu", "tma_store"])
 @pytest.mark.parametrize("transport", ["push", "pull"])
 @pytest.mark.parametrize("topo", ["ho", "two_step", "direct", "h_ring"])
 def test_4m_2x4_every_strategy_one_step(topo, transport, comm_impl):

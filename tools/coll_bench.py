@@ -24,7 +24,7 @@ def main():
     ap.add_argument("--iters", type=int, default=10)
     ap.add_argument("--comm-ctas", type=int, default=148)
     ap.add_argument("--transport", default="pull")
-    ap.add_argument("--comm-impl", default="tma")
+    ap.add_argument("--comm-impl", default="tma_store")
     ap.add_argument("--inter-gbps", type=float, default=0.0, help="emulated inter-group link (0 = off)")
     ap.add_argument("--trace", action="store_true",
                     help="per-launch device trace of the collective (barrier / work / final-barrier us)")

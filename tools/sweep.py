@@ -43,7 +43,7 @@ def main():
                     help="time paro_collective(reduce) + paro_collective(gather) per step, no Adam")
     a = ap.parse_args()
     grid = {"strategy": ["IIG"], "topology": ["ho"], "transport": ["pull"], "comm_ctas": [148],
-            "bucket": [1 << 26], "depth": [2], "adam_impl": ["auto"], "comm_impl": ["tma"], "fuse_gather": ["auto"],
+            "bucket": [1 << 26], "depth": [2], "adam_impl": ["auto"], "comm_impl": ["tma_store"], "fuse_gather": ["auto"],
             "copy_engine": [0], "grad_slots": [0], "producer": ["synth"]}
     grid.update(json.loads(a.grid))
     rank = int(os.environ.get("RANK", "0"))
