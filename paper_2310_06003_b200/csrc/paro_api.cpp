@@ -605,6 +605,7 @@ void paro_opts_default(paro_opts_t* o) {
   o->stream = nullptr;
   o->frozen = 0;
   o->grad_slots = 0;
+  o->fuse_allreduce = 1;
 }
 
 paro_status_t paro_get_unique_id(paro_uid_t* out) {
@@ -721,6 +722,7 @@ paro_status_t paro_plan(paro_ctx_t ctx, const char* strategy, const int64_t* par
   if (o.clip_norm < 0.f) return fail(PARO_ERR_INVALID, "clip_norm must be >= 0");
   po.two_phase = o.clip_norm > 0.f || o.skip_nonfinite != 0;
   if (po.two_phase) po.fuse_final = false;   // g_hat is materialised for the norm pass
+  po.fuse_ar_e = po.fuse_final && o.fuse_allreduce != 0;
   if (o.gather_windows < 0 || o.gather_windows > 64) return fail(PARO_ERR_INVALID, "gather_windows must be in [0, 64]");
   po.windows = o.gather_windows;
   if (o.fuse_gather < 0 || o.fuse_gather > 2) return fail(PARO_ERR_INVALID, "fuse_gather must be 0, 1 or 2");

@@ -390,6 +390,14 @@ void Planner::build_schedule() {
   if (OS != P) rest_ops = {OS == LV_G ? (P == LV_I ? "AG_E" : "HO_AG") : "AG_I"};
 
   const bool push = opt.push;
+  // OS = I, G = I at g = 2 (R31): the inter all-reduce of the intra partials
+  // (RS_E + AG_E) runs inside the Adam kernel, which folds the
+  // same-position peer's partial (pulled over NVLink) with its own.  For g = 2
+  // R_2(j; S_0, S_1) = S_{j+1} (+) S_j is one bf16 add, commutative, so both
+  // segments of the chunk get the ring's bits; each rank's partial is read
+  // once by its peer: (g-1)/g * 2 * chunk = chunk elements, the ring's bytes.
+  const bool fuse_ar_e = opt.fuse_ar_e && !push && N > 1 && M > 1 && g == 2 && G == LV_I &&
+                         OS == LV_I && opt.topology != 4;
   for (size_t b = 0; b < buckets.size(); ++b) {
     BucketSchedule& S = sched[b];
     const int64_t s = buckets[b].first, n = buckets[b].second;
@@ -802,7 +810,8 @@ void Planner::build_schedule() {
     if (N > 1 && topo != 4) {
       Launch& L = S.reduce;
       if (G == LV_I) {
-        emit_rs_e(L, emit_rs_i(L, 0, &S.reduce_pre));
+        const int r1 = emit_rs_i(L, 0, &S.reduce_pre);
+        if (!fuse_ar_e) emit_rs_e(L, r1);
       } else {
         emit_world_reduce(L);
       }
@@ -918,6 +927,18 @@ void Planner::build_schedule() {
         if (Lp->final_extra.empty()) Lp->final_extra.assign(N, 0);
       };
       for (Launch* Lp : {&S.reduce, &S.gather, &S.accum, &S.reduce_acc, &S.window}) finish(Lp);
+      if (fuse_ar_e) {
+        // Adam reads [peer partial, own partial] over the whole chunk; the RS_I
+        // launch ends with a barrier that covers the inter peer it reads
+        S.ghat_in.assign(N, {});
+        S.reduce.final_extra.assign(N, 0);
+        for (int r = 0; r < N; ++r) {
+          const int y = rank_of(1 - grp(r), pos(r));
+          S.ghat_in[r] = {gshard(y, 0), gshard(r, 0)};
+          S.reduce.final_extra[r] |= uint64_t(1) << y;
+        }
+        S.reduce.final_barrier = true;
+      }
       // fused gather, auto mode: only when no collective rounds run beside Adam
       // (the whole reduction fused too); beside a rounds kernel the separate
       // all-gather launch measured faster (profiles/r01/sweep_fuse_4.jsonl)

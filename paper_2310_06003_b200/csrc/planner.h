@@ -114,6 +114,7 @@ struct PlanOptions {
   int pipeline_depth = 2;
   bool push = true;          // push (remote stores) or pull (remote loads) transport
   bool fuse_final = true;    // OS = G: fold the owner's last reduction hop into Adam
+  bool fuse_ar_e = true;     // OS = I, G = I, g = 2 (pull): AR_E folded into Adam (R31)
   bool accum = false;        // build the gradient-accumulation launches (s > 1)
   bool two_phase = false;    // clipping / skip: every bucket's g_hat stays resident until Adam (R28)
   int windows = 0;           // parameter-gather window slots (0: none)

@@ -47,7 +47,8 @@ class paro_opts_t(C.Structure):
                 ("pull_transport", C.c_int), ("adam_impl", C.c_int), ("comm_impl", C.c_int),
                 ("inter_gbps", C.c_float), ("clip_norm", C.c_float), ("skip_nonfinite", C.c_int),
                 ("fuse_gather", C.c_int), ("copy_engine", C.c_int), ("gather_windows", C.c_int), ("grad_accum", C.c_int),
-                ("stream", C.c_void_p), ("frozen", C.c_int), ("grad_slots", C.c_int)]
+                ("stream", C.c_void_p), ("frozen", C.c_int), ("grad_slots", C.c_int),
+                ("fuse_allreduce", C.c_int)]
 
 
 class paro_plan_info_t(C.Structure):
@@ -159,7 +160,7 @@ def check(status):
 def make_opts(bucket_elems=1 << 26, topology="ho", beta1=0.9, beta2=0.95, eps=1e-8, weight_decay=0.0,
               loss_scale=1.0, comm_ctas=148, pipeline_depth=2, stream=None, transport="pull", adam_impl="auto",
               comm_impl="tma_store", inter_gbps=0.0, grad_accum=False, clip_norm=0.0, skip_nonfinite=False, gather_windows=0,
-              fuse_gather="auto", copy_engine=False, frozen=False, grad_slots=0):
+              fuse_gather="auto", copy_engine=False, frozen=False, grad_slots=0, fuse_allreduce=True):
     o = paro_opts_t()
     paro_opts_default(C.byref(o))
     o.bucket_elems = int(bucket_elems)
@@ -180,6 +181,7 @@ def make_opts(bucket_elems=1 << 26, topology="ho", beta1=0.9, beta2=0.95, eps=1e
     o.stream = stream
     o.frozen = 1 if frozen else 0
     o.grad_slots = int(grad_slots)
+    o.fuse_allreduce = 1 if fuse_allreduce else 0
     return o
 
 

@@ -33,7 +33,7 @@ class EmuRun:
 
     def __init__(self, N, M, code, sizes, B, topo="ho", depth=2, wd=0.0, loss_scale=1.0, transport="push",
                  adam_impl="auto", comm_impl="tma_store", grad_accum=False, mode="emulated", clip_norm=0.0,
-                 skip_nonfinite=False, fuse_gather="auto", copy_engine=False):
+                 skip_nonfinite=False, fuse_gather="auto", copy_engine=False, fuse_allreduce=True):
         paro = _paro()
         if mode == "emulated":
             self.ctx = paro.Context(N, M, mode="emulated", device=0)
@@ -42,7 +42,8 @@ class EmuRun:
         self.pl = paro.Plan(self.ctx, code, sizes, bucket_elems=B, topology=topo, pipeline_depth=depth,
                             weight_decay=wd, loss_scale=loss_scale, transport=transport, adam_impl=adam_impl,
                             comm_impl=comm_impl, grad_accum=grad_accum, clip_norm=clip_norm,
-                            skip_nonfinite=skip_nonfinite, fuse_gather=fuse_gather, copy_engine=copy_engine)
+                            skip_nonfinite=skip_nonfinite, fuse_gather=fuse_gather, copy_engine=copy_engine,
+                            fuse_allreduce=fuse_allreduce)
         self.info = self.pl.info()
         self.N, self.code, self.sizes = N, code, sizes
         n = self.info["os_numel"]
@@ -218,6 +219,44 @@ def test_4m_2x4_ten_steps(code, adam_impl):
         run.step(t)
     _check_against_dp(run, lay, ref)
     run.close()
+
+
+@pytest.mark.parametrize("fuse", [True, False])
+@pytest.mark.parametrize("N,M", [(8, 4), (4, 2), (6, 3)])
+def test_fused_inter_allreduce_os_i(N, M, fuse):
+    """OS = I, G = I at g = 2 (R31): AR_E folded into Adam (the peer's intra
+    partial pulled beside the own one) gives the ring's bits, 3 steps, ragged."""
+    sizes = ragged_param_sizes() + [N * 64 * 7 + 3]
+    B = N * 64 * 3
+    lay = L.Layout(sizes, N, M, B)
+    ref = _dp_reference(lay, 3)
+    for code in ("III", "NII"):
+        for adam_impl in ("auto", "lsu"):
+            run = EmuRun(N, M, code, sizes, B, transport="pull", adam_impl=adam_impl, fuse_allreduce=fuse)
+            for t in (1, 2, 3):
+                run.set_grads(t)
+                stats = run.step(t)
+            assert abs(stats["grad_norm"] ** 2 - ref[4][2]) <= 1e-12 * ref[4][2]
+            _check_against_dp(run, lay, ref)
+            run.close()
+
+
+@pytest.mark.parametrize("kind", ["specials", "nearmax", "smallint"])
+def test_fused_inter_allreduce_edge_inputs(kind):
+    N, M = 4, 2
+    sizes = [N * 64 * 10 + 5]
+    B = N * 64 * 4
+    lay = L.Layout(sizes, N, M, B)
+    ref = _dp_reference(lay, 1, kind=kind)
+    gh = ST.dp_step(lay, _oracle_grads(N, lay.psi, 1, kind), *ref[:3], nm.AdamScalars(LR, 1))[4]
+    expect_nonfinite = int(not np.all(np.isfinite(nm.f32_from_bf16_bits(gh))))
+    for code in ("III", "NII"):
+        run = EmuRun(N, M, code, sizes, B, transport="pull")
+        run.set_grads(1, kind=kind)
+        stats = run.step(1)
+        assert stats["nonfinite"] == expect_nonfinite
+        _check_against_dp(run, lay, ref)
+        run.close()
 
 
 @pytest.mark.parametrize("kind", ["zeros", "smallint", "specials", "nearmax"])

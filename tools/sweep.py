@@ -44,7 +44,7 @@ def main():
     a = ap.parse_args()
     grid = {"strategy": ["IIG"], "topology": ["ho"], "transport": ["pull"], "comm_ctas": [148],
             "bucket": [1 << 26], "depth": [2], "adam_impl": ["auto"], "comm_impl": ["tma_store"], "fuse_gather": ["auto"],
-            "copy_engine": [0], "grad_slots": [0], "producer": ["synth"]}
+            "copy_engine": [0], "grad_slots": [0], "producer": ["synth"], "fuse_allreduce": [1]}
     grid.update(json.loads(a.grid))
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -87,7 +87,8 @@ def main():
                              comm_ctas=cfg["comm_ctas"], pipeline_depth=cfg["depth"], stream=stream.cuda_stream,
                              transport=cfg["transport"], adam_impl=cfg["adam_impl"],
                              comm_impl=cfg["comm_impl"], fuse_gather={1: "always", 0: "never"}.get(cfg["fuse_gather"], cfg["fuse_gather"]),
-                             copy_engine=bool(cfg["copy_engine"]), grad_slots=cfg["grad_slots"])
+                             copy_engine=bool(cfg["copy_engine"]), grad_slots=cfg["grad_slots"],
+                             fuse_allreduce=bool(cfg["fuse_allreduce"]))
         except Exception as e:  # noqa: BLE001
             if rank == 0:
                 print(json.dumps({"cfg": cfg, "error": str(e)}), flush=True)
