@@ -26,10 +26,17 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# stdout carries exactly one JSON line: NCCL's log lines go to stderr, and the
+# "NCCL version ..." banner NCCL_DEBUG=VERSION printf()s to stdout is turned off
+os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+if os.environ.get("NCCL_DEBUG", "").upper() == "VERSION":
+    os.environ["NCCL_DEBUG"] = "WARN"
 
 from paro_synth import SEED, llama_param_sizes  # noqa: E402
 
 METRIC = "params/s per sync+update step"
+# the 14 codes Principle 1 allows (Table 1)
+STRATEGIES = ("NNN", "NNI", "NNG", "NII", "NIG", "NGG", "INI", "ING", "III", "IIG", "IGG", "GNG", "GIG", "GGG")
 LR = 3e-4
 
 
@@ -59,6 +66,8 @@ def parse(argv=None):
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-ho-ring", action="store_true", help="skip the 1 GiB HO-Ring all-reduce busbw (N > 1)")
+    ap.add_argument("--strategy-steps", type=int, default=3,
+                    help="N > 1: timed steps per PaRO strategy in the per_strategy table (0 = skip the table)")
     return ap.parse_args(argv)
 
 
@@ -378,6 +387,16 @@ def run_ours(args):
             plan = eplan
         del host
 
+    # ---- the metric is "per PaRO strategy": every one of the 14 codes on the same
+    # workload, split and kernels (N > 1; at N = 1 every code is the same computation)
+    per_strategy = None
+    if world > 1 and args.strategy_steps > 0:
+        plan.close()
+        del st, ptrs
+        torch.cuda.empty_cache()
+        per_strategy = per_strategy_table(paro, ctx, stream, dist, world, M, rank, sizes, args)
+        plan = None
+
     cpu = None
     if rank == 0 and N == 1 and not args.no_cpu_baseline:
         v, spent, elems, n = oracle_params_per_s(1, 1, args.strategy, "ho", 12.0, 1 << 22)
@@ -399,7 +418,8 @@ def run_ours(args):
                        "fuse_gather": args.fuse_gather,
                        "l2": "no flush: per-step inputs (13.5 GB grads + 81 GB/div(OS) state) >> 126 MB L2",
                        "intra_inter_gap": "not emulated: one NVSwitch box, intra/inter are labels"},
-            "roofline": roof, "step_roofline": step_roof, "ho_ring": ho, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roof, "step_roofline": step_roof, "ho_ring": ho, "per_strategy": per_strategy,
+            "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(prof["kernel_launches"]),
             "clocks": clk,
             "per_step": {"sent_intra_bytes": stats["sent_intra"], "sent_inter_bytes": stats["sent_inter"],
@@ -407,11 +427,69 @@ def run_ours(args):
                          "comm_ms": prof["comm_ms"] / args.steps},
         }
         print(json.dumps(line), flush=True)
-    plan.close()
+    if plan is not None:
+        plan.close()
     ctx.close()
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def per_strategy_table(paro, ctx, stream, dist, world, M, rank, sizes, args):
+    """Params/s of every PaRO code (Table 1) on the bench's workload, split and
+    kernels: per code W' = 2 warm-up + args.strategy_steps timed paro_steps on resident
+    gradients, CUDA events on the step stream, max over ranks.  A code whose per-rank
+    footprint (Table 2 + gradients + workspace) does not fit is reported as OOM, as the
+    paper does."""
+    import torch
+    pctx = paro.Context(world, M)          # planning only: footprint before allocating
+    free, _ = torch.cuda.mem_get_info()
+    fl = torch.tensor([float(free)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(fl, op=dist.ReduceOp.MIN)
+    free = float(fl.item())
+    out = {}
+    step = 0
+    for code in STRATEGIES:
+        pp = paro.Plan(pctx, code, sizes, **plan_kwargs(args, None))
+        pi = pp.info()
+        pp.close()
+        foot = (pi["grad_buffer_bytes"] + pi["mem_p_bytes"] + (pi["mem_g_bytes"] if pi["g_numel"] > 0 else 0)
+                + pi["mem_os_bytes"] + pi["workspace_bytes"])
+        if foot > free - (4 << 30):
+            out[code] = {"oom": True, "footprint_gb": round(foot / 1e9, 1)}
+            continue
+        plan = paro.Plan(ctx, code, sizes, **plan_kwargs(args, stream.cuda_stream))
+        info = plan.info()
+        st = [torch.empty(info["os_numel"], dtype=torch.float32, device="cuda") for _ in range(3)]
+        ptrs = [[t.data_ptr() for t in st]]
+        plan.opt_state_init(rank, ptrs[0], seed=SEED)
+        plan.synth_grads(rank, SEED, 1)
+        for _ in range(2):
+            step += 1
+            plan.step(ptrs, LR, step)
+        torch.cuda.synchronize()
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.strategy_steps):
+            step += 1
+            plan.step(ptrs, LR, step)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        dist.barrier()
+        torch.cuda.synchronize()
+        tt = torch.tensor([e0.elapsed_time(e1) / args.strategy_steps], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+        out[code] = {"value": info["psi"] / (ms / 1000.0), "ms_per_step": round(ms, 3),
+                     "sent_bytes": int(info["step_send_bytes_intra"] + info["step_send_bytes_inter"]),
+                     "footprint_gb": round(foot / 1e9, 1)}
+        plan.close()
+        del st, ptrs
+        torch.cuda.empty_cache()
+    pctx.close()
+    return {"unit": "params/s", "steps": args.strategy_steps, "warmup": 2, "codes": out}
 
 
 def ho_ring_busbw(paro, ctx, stream, dist, world, M, rank, args, nbytes=1 << 30, iters=10):

@@ -194,6 +194,7 @@ std::vector<int> Launch::reads(int r, int rank) const {
 uint64_t Launch::barrier_peers(int r, int rank) const {
   uint64_t m = 0;
   if (r >= (int)rounds.size() && !final_extra.empty()) m |= final_extra[rank];
+  if (r == 0 && !first_extra.empty()) m |= first_extra[rank];
   for (int rr = r - 1; rr <= r; ++rr) {
     if (rr < 0 || rr >= (int)rounds.size()) continue;
     for (int x : reads(rr, rank)) m |= uint64_t(1) << x;
@@ -396,8 +397,13 @@ void Planner::build_schedule() {
   // R_2(j; S_0, S_1) = S_{j+1} (+) S_j is one bf16 add, commutative, so both
   // segments of the chunk get the ring's bits; each rank's partial is read
   // once by its peer: (g-1)/g * 2 * chunk = chunk elements, the ring's bytes.
-  const bool fuse_ar_e = opt.fuse_ar_e && !push && N > 1 && M > 1 && g == 2 && G == LV_I &&
-                         OS == LV_I && opt.topology != 4;
+  // G = N (NNI, INI): the same fold after an RS_I of the raw gradients into the
+  // g_hat slot (HO-RS at g = 2 minus its inter part; two-step and direct give the
+  // same bits); the slot is reused pipeline_depth + 1 buckets later, so that
+  // RS_I's round-0 barrier also waits for the inter peer (whose Adam read it).
+  const bool fuse_ar_e = opt.fuse_ar_e && !push && N > 1 && M > 1 && g == 2 && OS == LV_I &&
+                         (G == LV_I ? opt.topology != 4
+                                    : (opt.topology == 0 || opt.topology == 1 || opt.topology == 3));
   for (size_t b = 0; b < buckets.size(); ++b) {
     BucketSchedule& S = sched[b];
     const int64_t s = buckets[b].first, n = buckets[b].second;
@@ -758,7 +764,9 @@ void Planner::build_schedule() {
     // are copied into landing slots (`pre`, run by the copy engines: raw
     // gradients do not change during a step, so no round barrier is needed),
     // then one local fold in the canonical order R_M(p; y_{p+1}, ..., y_p).
-    auto emit_rs_i = [&](Launch& L, int round0, Launch* pre = nullptr) -> int {
+    auto emit_rs_i = [&](Launch& L, int round0, Launch* pre = nullptr,
+                         std::function<Ref(int)> out = nullptr) -> int {
+      if (!out) out = [&](int r) { return gshard(r, 0); };
       if (pre && opt.ce_reduce && M > 1) {
         pre->n_ranks = N;
         for (int r = 0; r < N; ++r) {
@@ -773,7 +781,7 @@ void Planner::build_schedule() {
             t.in[i] = land;
           }
           t.in[M - 1] = grad(r, int64_t(p) * chunk);
-          t.dst = gshard(r, 0);
+          t.dst = out(r);
           L.add(round0, r, t);
         }
         return 1;
@@ -784,7 +792,7 @@ void Planner::build_schedule() {
         r1 = ring_rs(L, push, gr, [&](int c) { return one(int64_t(c) * chunk, chunk); },
                      [&, gr](int q, int, const Piece& pc) { return grad(gr[q], pc.src_off); },
                      [&, gr](int q, int slot) { return stage_i(gr[q], slot); },
-                     [&, gr](int q) { return gshard(gr[q], 0); }, round0);
+                     [&, gr, out](int q) { return out(gr[q]); }, round0);
       }
       return r1;
     };
@@ -812,6 +820,8 @@ void Planner::build_schedule() {
       if (G == LV_I) {
         const int r1 = emit_rs_i(L, 0, &S.reduce_pre);
         if (!fuse_ar_e) emit_rs_e(L, r1);
+      } else if (fuse_ar_e) {
+        emit_rs_i(L, 0, nullptr, [&](int r) { return ghat_base(r); });
       } else {
         emit_world_reduce(L);
       }
@@ -930,12 +940,15 @@ void Planner::build_schedule() {
       if (fuse_ar_e) {
         // Adam reads [peer partial, own partial] over the whole chunk; the RS_I
         // launch ends with a barrier that covers the inter peer it reads
+        auto part = [&](int r) { return G == LV_I ? gshard(r, 0) : ghat_base(r); };
         S.ghat_in.assign(N, {});
         S.reduce.final_extra.assign(N, 0);
+        if (G == LV_N) S.reduce.first_extra.assign(N, 0);
         for (int r = 0; r < N; ++r) {
           const int y = rank_of(1 - grp(r), pos(r));
-          S.ghat_in[r] = {gshard(y, 0), gshard(r, 0)};
+          S.ghat_in[r] = {part(y), part(r)};
           S.reduce.final_extra[r] |= uint64_t(1) << y;
+          if (G == LV_N) S.reduce.first_extra[r] |= uint64_t(1) << y;
         }
         S.reduce.final_barrier = true;
       }

@@ -61,6 +61,8 @@ struct Launch {
   std::vector<std::vector<std::vector<Task>>> rounds;  // [round][rank][task]
   bool final_barrier = false;   // barrier with the peers touched in the last round
   std::vector<uint64_t> final_extra;  // per rank: extra final-barrier peers (fused Adam reads)
+  std::vector<uint64_t> first_extra;  // per rank: extra round-0 barrier peers (their fused Adam
+                                      // read the slot this launch overwrites)
   int n_ranks = 0;
   void add(int round, int rank, const Task& t);
   bool empty() const { return rounds.empty() && !final_barrier; }

@@ -204,13 +204,13 @@ def test_gather_window_bytes_match_oracle(N, M):
 
 @pytest.mark.parametrize("N,M", [(8, 4), (4, 2), (6, 3), (8, 2), (4, 1)])
 def test_fused_inter_allreduce_keeps_table3_bytes(N, M):
-    """R31: folding AR_E into Adam (OS = I, G = I, g = 2, pull) sends exactly the
+    """R31: folding AR_E into Adam (OS = I, g = 2, pull) sends exactly the
     ring's bytes per link class (Table 3 closed form), in fewer rounds; other
     splits (g != 2, M = 1) and push plans are unchanged."""
     ctx = paro.Context(N, M)
     sizes = [1 << 20, 4000037]
     g = N // M
-    for code in ("III", "NII", "IIG", "INI"):
+    for code in ("III", "NII", "IIG", "INI", "NNI", "NNG"):
         res = {}
         for transport in ("pull", "push"):
             for fuse in (True, False):
@@ -223,6 +223,6 @@ def test_fused_inter_allreduce_keeps_table3_bytes(N, M):
         full = 2 * psi_pad
         assert inter == 2 * (g - 1) * full // N          # AR_E or RS_E + AG_E: 2(g-1)Psi/N
         assert intra == (M - 1) * full // M * (2 if code[0] == "N" else 1)
-        fused = code in ("III", "NII") and g == 2 and M > 1
+        fused = code in ("III", "NII", "INI", "NNI") and g == 2 and M > 1
         assert (res["pull", True][2] < res["pull", False][2]) == fused
         assert res["push", True][2] == res["push", False][2]

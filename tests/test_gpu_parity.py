@@ -222,17 +222,20 @@ def test_4m_2x4_ten_steps(code, adam_impl):
 
 
 @pytest.mark.parametrize("fuse", [True, False])
+@pytest.mark.parametrize("topo", ["ho", "two_step", "direct"])
 @pytest.mark.parametrize("N,M", [(8, 4), (4, 2), (6, 3)])
-def test_fused_inter_allreduce_os_i(N, M, fuse):
-    """OS = I, G = I at g = 2 (R31): AR_E folded into Adam (the peer's intra
-    partial pulled beside the own one) gives the ring's bits, 3 steps, ragged."""
+def test_fused_inter_allreduce_os_i(N, M, topo, fuse):
+    """OS = I at g = 2 (R31): AR_E folded into Adam (the peer's intra partial
+    pulled beside the own one) gives the ring's bits, 3 steps (g_hat slots of
+    G = N reused), ragged, depth 1 and 2."""
     sizes = ragged_param_sizes() + [N * 64 * 7 + 3]
     B = N * 64 * 3
     lay = L.Layout(sizes, N, M, B)
     ref = _dp_reference(lay, 3)
-    for code in ("III", "NII"):
-        for adam_impl in ("auto", "lsu"):
-            run = EmuRun(N, M, code, sizes, B, transport="pull", adam_impl=adam_impl, fuse_allreduce=fuse)
+    for code in ("III", "NII", "INI", "NNI"):
+        for adam_impl, depth in (("auto", 1), ("lsu", 2)):
+            run = EmuRun(N, M, code, sizes, B, topo=topo, depth=depth, transport="pull", adam_impl=adam_impl,
+                         fuse_allreduce=fuse)
             for t in (1, 2, 3):
                 run.set_grads(t)
                 stats = run.step(t)
@@ -250,7 +253,7 @@ def test_fused_inter_allreduce_edge_inputs(kind):
     ref = _dp_reference(lay, 1, kind=kind)
     gh = ST.dp_step(lay, _oracle_grads(N, lay.psi, 1, kind), *ref[:3], nm.AdamScalars(LR, 1))[4]
     expect_nonfinite = int(not np.all(np.isfinite(nm.f32_from_bf16_bits(gh))))
-    for code in ("III", "NII"):
+    for code in ("III", "NII", "INI", "NNI"):
         run = EmuRun(N, M, code, sizes, B, transport="pull")
         run.set_grads(1, kind=kind)
         stats = run.step(1)
