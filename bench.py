@@ -306,7 +306,16 @@ def run_ours(args):
                 "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
                 "traffic": None, "algorithmic_bytes_per_launch": alg,
                 "launch_ms": comm_ms, "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s/dir",
-                "share_of_step": prof["comm_ms"] / max(1e-9, ms * args.steps)}
+                "share_of_step": prof["comm_ms"] / max(1e-9, ms * args.steps),
+                # the Adam kernel beside it pulls the fused final hop's operands over the same
+                # links, so the rounds launches carry only part of the step's NVLink bytes: the
+                # link as a whole moves these bytes during the collective launches' time
+                "link_achieved": (info["step_send_bytes_intra"] + info["step_send_bytes_inter"])
+                                 / (prof["comm_ms"] / args.steps / 1000.0) / 1e9,
+                "note": "achieved = bytes this rank sends in the rounds launches / their duration; "
+                        "link_achieved = all bytes this rank sends per step (rounds + fused-Adam pulls) / "
+                        "the collective launches' time per step; SM-transport ceiling 672 GB/s/dir "
+                        "(profiles/r01/p2p_tma_bidir.jsonl)"}
 
     # ---- the step as a whole against max(HBM, NVLink) (B200_PROFILING.md: the slower of
     # the two bounds; HBM at the measured copy peak, NVLink at the measured 770 GB/s/dir)
