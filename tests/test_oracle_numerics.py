@@ -72,6 +72,28 @@ def test_canonical_fold_exact_on_small_integers_any_owner():
             assert np.array_equal(out, ints.sum(0))
 
 
+def test_two_member_fold_is_owner_independent():
+    """Reading R31's premise: R_2(0; y) == R_2(1; y) bit for bit (one hop, and
+    IEEE fp32 addition is commutative), on random bf16 patterns including
+    +-0, subnormals, +-inf and NaN (NaN compared by class), while for k = 3 the
+    owner changes the bits (the hand case above), so the fused inter all-reduce
+    is only exact at g = 2."""
+    rng = np.random.default_rng(31)
+    bits = rng.integers(0, 1 << 16, size=(2, 1 << 16), dtype=np.uint32).astype(np.uint16)
+    bits[0, :6] = [0x0000, 0x8000, 0x0001, 0x7F80, 0xFF80, 0x7FC0]
+    bits[1, :6] = [0x8000, 0x0000, 0x8001, 0xFF80, 0x7F80, 0x3F80]
+    ys = [bits[0], bits[1]]
+    a, b = nm.canonical_fold(ys, 0), nm.canonical_fold(ys, 1)
+    fa, fb = nm.f32_from_bf16_bits(a), nm.f32_from_bf16_bits(b)
+    assert np.array_equal(np.isnan(fa), np.isnan(fb))
+    ok = ~np.isnan(fa)
+    assert np.array_equal(a[ok], b[ok])
+    # the same as a plain fp32 sum rounded once (torch), either order
+    t = (torch.from_numpy(nm.f32_from_bf16_bits(bits[1])) + torch.from_numpy(nm.f32_from_bf16_bits(bits[0])))
+    ref = t.to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16)
+    assert np.array_equal(a[ok], ref[ok])
+
+
 def test_pack_power_of_two_scale_is_exponent_shift():
     rng = np.random.default_rng(3)
     x = nm.bf16_bits_from_f32((rng.standard_normal(10_000) * 1e-3).astype(np.float32))
