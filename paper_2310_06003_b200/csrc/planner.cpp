@@ -401,9 +401,13 @@ void Planner::build_schedule() {
   // g_hat slot (HO-RS at g = 2 minus its inter part; two-step and direct give the
   // same bits); the slot is reused pipeline_depth + 1 buckets later, so that
   // RS_I's round-0 barrier also waits for the inter peer (whose Adam read it).
-  const bool fuse_ar_e = opt.fuse_ar_e && !push && N > 1 && M > 1 && g == 2 && OS == LV_I &&
-                         (G == LV_I ? opt.topology != 4
-                                    : (opt.topology == 0 || opt.topology == 1 || opt.topology == 3));
+  // M = 1 (groups of one GPU, I == N): the partials are the raw gradients
+  // themselves (scaled by 1/N on read), so Adam folds the peer's raw bucket
+  // with its own for every OS != G code: the whole all-reduce in the update.
+  const bool topo_ok = opt.topology == 0 || opt.topology == 1 || opt.topology == 3;
+  const bool fuse_ar_e = opt.fuse_ar_e && !push && N > 1 && g == 2 &&
+                         ((M > 1 && OS == LV_I && (G == LV_I ? opt.topology != 4 : topo_ok)) ||
+                          (M == 1 && OS != LV_G && topo_ok));
   for (size_t b = 0; b < buckets.size(); ++b) {
     BucketSchedule& S = sched[b];
     const int64_t s = buckets[b].first, n = buckets[b].second;
@@ -817,7 +821,9 @@ void Planner::build_schedule() {
 
     if (N > 1 && topo != 4) {
       Launch& L = S.reduce;
-      if (G == LV_I) {
+      if (fuse_ar_e && M == 1) {
+        // nothing to reduce inside a group of one
+      } else if (G == LV_I) {
         const int r1 = emit_rs_i(L, 0, &S.reduce_pre);
         if (!fuse_ar_e) emit_rs_e(L, r1);
       } else if (fuse_ar_e) {
@@ -940,15 +946,16 @@ void Planner::build_schedule() {
       if (fuse_ar_e) {
         // Adam reads [peer partial, own partial] over the whole chunk; the RS_I
         // launch ends with a barrier that covers the inter peer it reads
-        auto part = [&](int r) { return G == LV_I ? gshard(r, 0) : ghat_base(r); };
+        auto part = [&](int r) { return M == 1 ? grad(r, 0) : (G == LV_I ? gshard(r, 0) : ghat_base(r)); };
+        const bool slot_reuse = M > 1 && G == LV_N;
         S.ghat_in.assign(N, {});
         S.reduce.final_extra.assign(N, 0);
-        if (G == LV_N) S.reduce.first_extra.assign(N, 0);
+        if (slot_reuse) S.reduce.first_extra.assign(N, 0);
         for (int r = 0; r < N; ++r) {
           const int y = rank_of(1 - grp(r), pos(r));
           S.ghat_in[r] = {part(y), part(r)};
           S.reduce.final_extra[r] |= uint64_t(1) << y;
-          if (G == LV_N) S.reduce.first_extra[r] |= uint64_t(1) << y;
+          if (slot_reuse) S.reduce.first_extra[r] |= uint64_t(1) << y;
         }
         S.reduce.final_barrier = true;
       }

@@ -202,7 +202,7 @@ def test_gather_window_bytes_match_oracle(N, M):
     ctx.close()
 
 
-@pytest.mark.parametrize("N,M", [(8, 4), (4, 2), (6, 3), (8, 2), (4, 1)])
+@pytest.mark.parametrize("N,M", [(8, 4), (4, 2), (6, 3), (8, 2), (4, 1), (2, 1)])
 def test_fused_inter_allreduce_keeps_table3_bytes(N, M):
     """R31: folding AR_E into Adam (OS = I, g = 2, pull) sends exactly the
     ring's bytes per link class (Table 3 closed form), in fewer rounds; other
@@ -210,7 +210,7 @@ def test_fused_inter_allreduce_keeps_table3_bytes(N, M):
     ctx = paro.Context(N, M)
     sizes = [1 << 20, 4000037]
     g = N // M
-    for code in ("III", "NII", "IIG", "INI", "NNI", "NNG"):
+    for code in ("III", "NII", "IIG", "INI", "NNI", "NNG", "NNN"):
         res = {}
         for transport in ("pull", "push"):
             for fuse in (True, False):
@@ -223,6 +223,6 @@ def test_fused_inter_allreduce_keeps_table3_bytes(N, M):
         full = 2 * psi_pad
         assert inter == 2 * (g - 1) * full // N          # AR_E or RS_E + AG_E: 2(g-1)Psi/N
         assert intra == (M - 1) * full // M * (2 if code[0] == "N" else 1)
-        fused = code in ("III", "NII", "INI", "NNI") and g == 2 and M > 1
+        fused = g == 2 and ((M > 1 and code[2] == "I") or (M == 1 and code[2] != "G"))
         assert (res["pull", True][2] < res["pull", False][2]) == fused
         assert res["push", True][2] == res["push", False][2]

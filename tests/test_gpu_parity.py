@@ -223,7 +223,7 @@ def test_4m_2x4_ten_steps(code, adam_impl):
 
 @pytest.mark.parametrize("fuse", [True, False])
 @pytest.mark.parametrize("topo", ["ho", "two_step", "direct"])
-@pytest.mark.parametrize("N,M", [(8, 4), (4, 2), (6, 3)])
+@pytest.mark.parametrize("N,M", [(8, 4), (4, 2), (6, 3), (2, 1)])
 def test_fused_inter_allreduce_os_i(N, M, topo, fuse):
     """OS = I at g = 2 (R31): AR_E folded into Adam (the peer's intra partial
     pulled beside the own one) gives the ring's bits, 3 steps (g_hat slots of
@@ -232,7 +232,7 @@ def test_fused_inter_allreduce_os_i(N, M, topo, fuse):
     B = N * 64 * 3
     lay = L.Layout(sizes, N, M, B)
     ref = _dp_reference(lay, 3)
-    for code in ("III", "NII", "INI", "NNI"):
+    for code in ("III", "NII", "INI", "NNI") + (("NNN",) if M == 1 else ()):
         for adam_impl, depth in (("auto", 1), ("lsu", 2)):
             run = EmuRun(N, M, code, sizes, B, topo=topo, depth=depth, transport="pull", adam_impl=adam_impl,
                          fuse_allreduce=fuse)
@@ -244,16 +244,16 @@ def test_fused_inter_allreduce_os_i(N, M, topo, fuse):
             run.close()
 
 
+@pytest.mark.parametrize("N,M", [(4, 2), (2, 1)])
 @pytest.mark.parametrize("kind", ["specials", "nearmax", "smallint"])
-def test_fused_inter_allreduce_edge_inputs(kind):
-    N, M = 4, 2
+def test_fused_inter_allreduce_edge_inputs(kind, N, M):
     sizes = [N * 64 * 10 + 5]
     B = N * 64 * 4
     lay = L.Layout(sizes, N, M, B)
     ref = _dp_reference(lay, 1, kind=kind)
     gh = ST.dp_step(lay, _oracle_grads(N, lay.psi, 1, kind), *ref[:3], nm.AdamScalars(LR, 1))[4]
     expect_nonfinite = int(not np.all(np.isfinite(nm.f32_from_bf16_bits(gh))))
-    for code in ("III", "NII", "INI", "NNI"):
+    for code in ("III", "NII", "INI", "NNI", "NNN"):
         run = EmuRun(N, M, code, sizes, B, transport="pull")
         run.set_grads(1, kind=kind)
         stats = run.step(1)
