@@ -153,17 +153,20 @@ typedef struct {
                           * P + G + OS plus staging.  paro_step and                *
                           * paro_synth_grads then return PARO_ERR_STATE; not with  *
                           * grad_accum; copy_engine is forced to 0.  0 (default).  */
-  int fuse_allreduce;    /* OS = I, G = I with g = 2 groups (NII, III,     *
+  int fuse_allreduce;    /* OS = I with g = 2 groups (NII, III, INI, NNI,  *
                           * P:355 "all-reduce among groups"): 1 (default) folds    *
                           * the inter-group all-reduce AR_E into the Adam kernel,  *
                           * which reads the same-position peer's intra partial    *
                           * over NVLink beside its own (R31: at g = 2 the fold     *
                           * R_2 of both segments is one commutative bf16 add, so   *
                           * the bits equal the RS_E + AG_E ring; bytes per link    *
-                          * class are equal too: (g-1)/g * 2 B/M = B/M).  The G   *
-                          * residency then keeps the intra partial (R26).          *
-                          * Off with pull_transport = 0, clipping / skip and       *
-                          * inter_gbps pacing.  0: the ring.                       */
+                          * class are equal too: (g-1)/g * 2 B/M = B/M).  G = I:  *
+                          * the G residency then keeps the intra partial (R26);   *
+                          * G = N: RS_I lands in the g_hat slot.  M = 1 (2 x 1):   *
+                          * every OS != G code, the partials being the raw         *
+                          * gradients.  Topologies HO, two-step, direct (any for   *
+                          * G = I except NCCL).  Off with pull_transport = 0,      *
+                          * clipping / skip and inter_gbps pacing.  0: the ring.   */
 } paro_opts_t;
 
 typedef struct {
