@@ -387,6 +387,8 @@ def run_ours(args):
             ems = float(tt.item())
         e2e = {"value": info["psi"] / (ems / 1000.0), "unit": "params/s", "h2d_bytes_per_step": 2 * info["psi"],
                "d2h_bytes_per_step": 12, "ms_per_step": ems,
+               # the host link bounds it: H2D bytes per step / step time, per GPU
+               "h2d_GBps_per_gpu": 2 * info["psi"] / (ems / 1000.0) / 1e9,
                "path": ("paro_step_streamed (grad_slots = 4): each bucket's gradients copied host->device "
                                 "by the copy engines from a <=2 GiB pinned staging area while earlier buckets "
                                 "reduce and update, + paro_step_stats read-back") if producer is not None else
