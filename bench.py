@@ -405,8 +405,11 @@ def run_ours(args):
         plan.close()
         del st, ptrs
         torch.cuda.empty_cache()
-        per_strategy = per_strategy_table(paro, ctx, stream, dist, world, M, rank, sizes, args)
         plan = None
+        try:   # a failing code must not cost the headline line
+            per_strategy = per_strategy_table(paro, ctx, stream, dist, world, M, rank, sizes, args)
+        except Exception as e:  # noqa: BLE001
+            per_strategy = {"error": repr(e)[:300]}
 
     cpu = None
     if rank == 0 and N == 1 and not args.no_cpu_baseline:
