@@ -421,6 +421,7 @@ def run_ours(args):
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "params/s", "n_gpus": N, "steps": args.steps,
+            "value_per_gpu": value / N,     # also per GPU, Psi / (N * t_step)
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "bf16 wire/grads, f32 master",
             "data": "synthetic (paro_synth counter-hash bf16 gradients, fp32 masters), resident in HBM",
