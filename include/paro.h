@@ -88,9 +88,10 @@ typedef struct {
   int adam_impl;         /* 0 (default): TMA bulk-copy pipeline (cp.async.bulk +    *
                           * mbarrier stages; also pulls NVLink-peer operands); the *
                           * results leave through bulk copies too when N = 1 (or   *
-                          * emulated, or no collective rounds run beside Adam and  *
-                          * it stores nothing into peers), through thread stores   *
-                          * otherwise;                                             *
+                          * emulated, or the inter all-reduce is folded into Adam *
+                          * with no collective rounds beside it and no peer       *
+                          * stores: the 2 x 1 OS != G codes), through thread       *
+                          * stores otherwise;                                      *
                           * 1: the LSU (ld.global) kernel; 2: TMA both ways always */
   int comm_impl;         /* 2 (default): collective rounds move operands with TMA  *
                           * bulk copies into shared memory and the folded tile     *

@@ -1187,14 +1187,16 @@ paro_status_t step_impl(PlanT* p, const void* const* grads, void* const* params,
     // stores: bulk copies out of shared memory win when Adam has the GPU to itself
     // and no NVLink operands (N = 1: 0.97 of the HBM peak vs 0.90, profiles/r01);
     // beside collectives / with peer traffic the thread stores are faster
-    // (real N > 1: also when nothing runs beside Adam and it pushes nothing to
-    // peers, e.g. the fused all-reduce at 2x1: NNN 35.6 -> 34.0 ms,
+    // (real N > 1: also for the fused all-reduce when nothing runs beside Adam
+    // and it pushes nothing to peers, i.e. 2x1: NNN 35.6 -> 34.0 ms,
     // profiles/r01/sweep_adam_store_fused_2x1.jsonl; with fused-gather pushes
-    // the thread stores stay faster: IIG 2x1 20.0 vs 20.6 ms)
+    // (IIG 2x1 20.0 vs 20.6 ms) or a fused final hop only (GGG 2x1 17.2-17.8
+    // vs 17.8-18.7 ms) the thread stores stay faster)
     bool pushes = false;
     for (int i = 0; i < aa.nseg; ++i) pushes = pushes || aa.seg[i].npush > 0;
     const bool tma_store = p->opts.adam_impl == 2 ||
-                           (p->opts.adam_impl == 0 && (pl.N == 1 || ctx->mode == MODE_EMU || (!corun && !pushes)));
+                           (p->opts.adam_impl == 0 && (pl.N == 1 || ctx->mode == MODE_EMU ||
+                                                       (pl.fused_allreduce && !corun && !pushes)));
     if (p->opts.adam_impl != 1)
       CK(launch_adam_tma(aa, ctx->sm_count, ctx->comp, corun ? 120 : 200, tma_store ? 1 : 0));
     else CK(launch_adam(aa, grid, ctx->comp, corun ? 1 : 0));

@@ -408,6 +408,7 @@ void Planner::build_schedule() {
   const bool fuse_ar_e = opt.fuse_ar_e && !push && N > 1 && g == 2 &&
                          ((M > 1 && OS == LV_I && (G == LV_I ? opt.topology != 4 : topo_ok)) ||
                           (M == 1 && OS != LV_G && topo_ok));
+  fused_allreduce = fuse_ar_e;
   for (size_t b = 0; b < buckets.size(); ++b) {
     BucketSchedule& S = sched[b];
     const int64_t s = buckets[b].first, n = buckets[b].second;

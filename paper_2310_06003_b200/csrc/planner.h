@@ -140,6 +140,7 @@ class Planner {
   std::string code;
   PlanOptions opt;
   int64_t psi = 0, psi_pad = 0, B = 0;
+  bool fused_allreduce = false;   // the inter all-reduce runs inside Adam (R31)
   std::vector<std::pair<int64_t, int64_t>> buckets;   // (start, size)
   std::vector<int64_t> param_sizes, param_offsets;
   int64_t p_numel = 0, g_numel = 0, os_numel = 0;
