@@ -839,7 +839,7 @@ void Planner::build_schedule() {
           emit_world_rs(S.accum, 0);          // lands in the G residency (dest_seg)
         } else if (G == LV_I) {
           emit_rs_i(S.accum, 0, &S.accum_pre);
-          emit_rs_e(S.reduce_acc, 0);
+          if (!fuse_ar_e) emit_rs_e(S.reduce_acc, 0);   // else folded into Adam (below)
         } else {
           for (int r = 0; r < N; ++r) S.accum.add(0, r, make_task(n, {grad(r, 0)}, Ref{r, BUF_GACC, s}));
           src_kind = BUF_GACC;
@@ -959,6 +959,18 @@ void Planner::build_schedule() {
           if (slot_reuse) S.reduce.first_extra[r] |= uint64_t(1) << y;
         }
         S.reduce.final_barrier = true;
+        // gradient accumulation, G = I: the accumulated intra partials sit in the
+        // G residency; the step after the last micro-batch folds them in Adam too
+        if (opt.accum && G == LV_I) {
+          S.ghat_in_acc.assign(N, {});
+          S.reduce_acc.final_extra.assign(N, 0);
+          for (int r = 0; r < N; ++r) {
+            const int y = rank_of(1 - grp(r), pos(r));
+            S.ghat_in_acc[r] = {gshard(y, 0), gshard(r, 0)};
+            S.reduce_acc.final_extra[r] |= uint64_t(1) << y;
+          }
+          S.reduce_acc.final_barrier = true;
+        }
       }
       // fused gather, auto mode: only when no collective rounds run beside Adam
       // (the whole reduction fused too); beside a rounds kernel the separate
