@@ -161,3 +161,36 @@ def test_grad_sq_sum_matches_fsum():
     g = nm.bf16_bits_from_f32((rng.standard_normal(50_000) * 1e-3).astype(np.float32))
     ref = math.fsum(float(x) ** 2 for x in nm.f32_from_bf16_bits(g))
     assert abs(nm.grad_sq_sum(g) - ref) <= 1e-12 * ref
+
+
+@pytest.mark.parametrize("N", [3, 5, 6, 7, 9, 12])
+def test_pack_non_power_of_two_matches_torch(N):
+    """pack = RNE_bf16(fp32(g) * fp32(1/N)) (reading R4) pinned bit for bit to
+    torch's own float32 multiply and bfloat16 conversion on 10^6 bf16 patterns
+    drawn over every finite exponent, so products land in the normal range, the
+    fp32-subnormal range (bf16 subnormals) and underflow to zero; +-inf stay
+    inf.  It also equals torch's bf16 rounding of the double quotient g/N:
+    for N < 2^15 the exact g/N of an 8-bit-mantissa g is at least 1/(2N)
+    bf16-ulp away from a rounding tie, farther than fp32(1/N)'s 2^-16-ulp
+    error can move it, so the two fp32 roundings never change the result
+    (pack is the correctly rounded per-rank mean contribution).  A truncating
+    cast (a plausible mistake) gives other bits on this input set."""
+    rng = np.random.default_rng(100 + N)
+    bits = rng.integers(0, 1 << 16, size=1_000_000, dtype=np.uint32).astype(np.uint16)
+    bits = bits[(bits & 0x7F80) != 0x7F80]                      # finite
+    tiny = (rng.integers(0, 0x0300, size=50_000, dtype=np.uint32).astype(np.uint16)
+            | (rng.integers(0, 2, size=50_000).astype(np.uint16) << 15))   # |g| < 2^-120
+    bits = np.concatenate([bits, tiny, np.uint16([0x7F80, 0xFF80, 0x0000, 0x8000, 0x0001, 0x8001])])
+    g = torch.from_numpy(bits.view(np.int16)).view(torch.bfloat16).float()
+    alpha = torch.tensor(np.float32(1.0 / N))
+    prod = g * alpha
+    ref = prod.to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16)
+    got = nm.pack(bits, 1.0 / N)
+    assert np.array_equal(got, ref)
+    f = nm.f32_from_bf16_bits(got)
+    assert (np.abs(f[np.isfinite(f)]) < np.float32(2.0 ** -126)).sum() > 1000    # subnormal results covered
+    g64 = nm.f32_from_bf16_bits(bits).astype(np.float64) / N
+    dbl = torch.from_numpy(g64).to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16)
+    assert np.array_equal(dbl, ref)
+    trunc = (prod.numpy().view(np.uint32) >> np.uint32(16)).astype(np.uint16)
+    assert not np.array_equal(trunc, ref)

@@ -192,3 +192,52 @@ def test_step_units_match_simulator_bytes():
             a, b = A.step_units_per_rank(code, N, M, lay.psi_pad)
             for r in range(N):
                 assert tuple(res.sent[r]) == (a, b), (code, N, M, r)
+
+
+def _counted(geo, ops, n_seg):
+    """Cluster-total [intra, inter] units of a sequence of (collective, multiplier)
+    counted message by message by the round simulators (rank-order rings, A14)."""
+    N, M = geo.N, geo.M
+    add = lambda a, b: a + b
+    X = {r: [np.zeros(n_seg, np.int64) for _ in range(N)] for r in range(N)}
+    Z = {r: np.zeros(n_seg, np.int64) for r in range(N)}
+    tot = [0, 0]
+    for op, mult in ops:
+        tr = C.Trace(M)
+        if op == "flat_rs":
+            tr = C.rs_flat_ring(geo, X, add)[1]
+        elif op == "flat_ag":
+            tr = C.ag_flat_ring(geo, Z)[1]
+        elif op == "intra_ag":      # ZeRO++ secondary partition: a Psi/M block per rank, AG inside the group
+            tr.extend(C.ag_intra(geo, {r: np.zeros(n_seg * geo.g, np.int64) for r in range(N)})[1])
+        else:
+            raise ValueError(op)
+        a, b = tr.totals()
+        tot[0] += mult * a
+        tot[1] += mult * b
+    return tuple(tot)
+
+
+@pytest.mark.parametrize("N,M,s", [(8, 2, 1), (8, 4, 3), (12, 3, 2), (16, 4, 4)])
+def test_table3_zero_rows_equal_flat_ring_simulator(N, M, s):
+    """Table 3's ZeRO-1 / ZeRO-2 / ZeRO-3 / ZeRO++ cells are flat-world
+    rings; with rank-order rings (reading A14: rank r = jM + p sends to r + 1, an
+    inter link iff r mod M = M - 1) the simulators' counted messages give every
+    cell exactly, intra and inter separately, per stage.  ZeRO-1's update
+    all-reduce is a flat RS + flat AG; ZeRO++'s backward A-G(P)
+    gathers its secondary (intra-group) partition."""
+    geo = C.Geometry(N, M)
+    n_seg = 64 * 5
+    psi = N * n_seg
+    plans = {
+        "ZeRO-1": {"upd_rs_ar_g": [("flat_rs", 1), ("flat_ag", 1)], "upd_ag_p": [("flat_ag", 1)]},
+        "ZeRO-2": {"bwd_rs_g": [("flat_rs", s)], "upd_ag_p": [("flat_ag", 1)]},
+        "ZeRO-3": {"fwd_ag_p": [("flat_ag", s)], "bwd_ag_p": [("flat_ag", s)], "bwd_rs_g": [("flat_rs", s)]},
+        "ZeRO++": {"fwd_ag_p": [("flat_ag", s)], "bwd_ag_p": [("intra_ag", s)], "bwd_rs_g": [("flat_rs", s)]},
+    }
+    for meth, stages in plans.items():
+        t = A.table3(meth, N, M, s, psi)
+        for stage in A.STAGES:
+            want = t[stage]
+            got = _counted(geo, stages.get(stage, []), n_seg)
+            assert (Fr(got[0]), Fr(got[1])) == want, (meth, stage, got, want)
