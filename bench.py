@@ -65,7 +65,8 @@ def parse(argv=None):
                          "host pointers read by the pack kernel (paro_step)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-ho-ring", action="store_true", help="skip the 1 GiB HO-Ring all-reduce busbw (N > 1)")
+    ap.add_argument("--no-ho-ring", action="store_true",
+                    help="skip the 1 MiB - 4 GiB HO-Ring / flat / NCCL all-reduce busbw sweep (N > 1)")
     ap.add_argument("--strategy-steps", type=int, default=3,
                     help="N > 1: timed steps per PaRO strategy in the per_strategy table (0 = skip the table)")
     return ap.parse_args(argv)
@@ -286,11 +287,12 @@ def run_ours(args):
         alg = prof["adam_hbm_bytes"] / max(1, prof["adam_launches"])
         ach = alg / (adam_ms / 1000.0) / 1e9
         peak = float(peaks["hbm_gbs"])
-        # which Adam kernel ran: TMA pipeline when every operand is local (N = 1, push), else LSU
-        kname = "adam_tma_kernel" if args.adam_impl == "auto" else "adam_kernel"
+        # which Adam kernel ran (reported by the library for the last launch)
+        kname = paro.ADAM_VARIANTS.get(prof["adam_variant"]) or "adam_kernel"
         # the committed capture is single-GPU (ncu never runs multi-rank): it matches the N = 1 kernel only
-        tr = traffic.get(kname) if N == 1 else None
-        roof = {"bound": "hbm", "kernel": f"{kname} (fused unscale+Adam+bf16 cast+norm)", "achieved": ach,
+        tr = traffic.get(kname.split("<")[0]) if N == 1 else None
+        roof = {"bound": "hbm", "kernel": f"{kname} ({prof['adam_stages']} stages; fused unscale+Adam+bf16 "
+                                          f"cast+norm)", "achieved": ach,
                 "peak": peak, "unit": "GB/s", "frac": ach / peak,
                 "traffic": (tr["dram_bytes_per_elem"] * elems_per_launch) if tr else None,
                 "traffic_source": tr["source"] if tr else None,
@@ -317,6 +319,11 @@ def run_ours(args):
                         "the collective launches' time per step; SM-transport ceiling 672 GB/s/dir "
                         "(profiles/r01/p2p_tma_bidir.jsonl)"}
 
+    # a fraction far above 1 means the timed launches are not doing the work (B200_PROFILING.md)
+    invalid = roof["frac"] > 1.2
+    if invalid:
+        roof["error"] = "frac > 1.2 of the measured peak: the timed kernel is not doing the counted work"
+
     # ---- the step as a whole against max(HBM, NVLink) (B200_PROFILING.md: the slower of
     # the two bounds; HBM at the measured copy peak, NVLink at the measured 770 GB/s/dir)
     hbm_step = (prof["adam_hbm_bytes"] + prof["comm_hbm_bytes"]) / args.steps
@@ -328,12 +335,11 @@ def run_ours(args):
                  "note": "algorithmic bytes of this rank's launches (Adam + collective tasks) per step; "
                          "NVLink = bytes this rank sends per step (each direction)"}
 
-    # ---- HO-Ring bus bandwidth (BASELINE metric's second half, config 5): a 1 GiB bf16
-    # all-reduce through the library (NNN plan: hierarchical HO-RS + HO-AG with the bf16 hop
-    # arithmetic, paro_collective) beside NCCL's all_reduce on the same bytes, N > 1 only
+    # ---- HO-Ring bus bandwidth (BASELINE metric's second half, config 5): the 1 MiB - 4 GiB
+    # bf16 all-reduce sweep through the library (HO-Ring and flat ring) beside NCCL, N > 1 only
     ho = None
     if world > 1 and not args.no_ho_ring:
-        ho = ho_ring_busbw(paro, ctx, stream, dist, world, M, rank, args)
+        ho = allreduce_sweep(paro, ctx, stream, dist, world, M, rank, args)
 
     # ---- end to end: gradients from pinned host memory each step (read by the
     # pack kernel over PCIe), device->host read of the step's norm/flag
@@ -441,13 +447,15 @@ def run_ours(args):
                          "grad_norm": stats["grad_norm"], "adam_ms": prof["adam_ms"] / args.steps,
                          "comm_ms": prof["comm_ms"] / args.steps},
         }
+        if invalid:
+            line["invalid"] = roof["error"]
         print(json.dumps(line), flush=True)
     if plan is not None:
         plan.close()
     ctx.close()
     if world > 1:
         dist.destroy_process_group()
-    return 0
+    return 3 if invalid else 0
 
 
 def per_strategy_table(paro, ctx, stream, dist, world, M, rank, sizes, args):
@@ -507,12 +515,23 @@ def per_strategy_table(paro, ctx, stream, dist, world, M, rank, sizes, args):
     return {"unit": "params/s", "steps": args.strategy_steps, "warmup": 2, "codes": out}
 
 
-def ho_ring_busbw(paro, ctx, stream, dist, world, M, rank, args, nbytes=1 << 30, iters=10):
-    """busbw = S * 2(N-1)/N / t (nccl-tests convention), t = max over ranks of the CUDA-event time."""
-    import torch
-    elems = nbytes // 2
+SWEEP_MIB = (1, 4, 16, 64, 256, 1024, 4096)   # BASELINE config 5: 1 MB - 4 GB
 
-    def timeit(fn):
+
+def allreduce_sweep(paro, ctx, stream, dist, world, M, rank, args, sizes_mib=SWEEP_MIB):
+    """BASELINE config 5: bf16 gradient all-reduce, 1 MiB - 4 GiB, through the library
+    (paro_collective(0) of an NNN plan made with fuse_allreduce = 0, so the whole
+    reduction runs in the collective launches: HO-Ring = HO-RS + HO-AG, flat = one ring
+    over all ranks, both with the bf16 hop arithmetic in canonical order) beside NCCL's
+    all_reduce on the same bytes.  busbw = S * 2(N-1)/N / t (nccl-tests convention), t =
+    max over ranks of the CUDA-event time per call.  A fraction of the 770 GB/s measured
+    peer-copy peak above 1.2 means the timed code is not doing the work: such a point is
+    reported as an error, not a number."""
+    import torch
+    factor = 2 * (world - 1) / world
+    peak = 770.0
+
+    def timeit(fn, iters):
         for _ in range(3):
             fn()
         torch.cuda.synchronize()
@@ -527,21 +546,37 @@ def ho_ring_busbw(paro, ctx, stream, dist, world, M, rank, args, nbytes=1 << 30,
         dist.all_reduce(ms, op=dist.ReduceOp.MAX)
         return float(ms.item())
 
-    factor = 2 * (world - 1) / world
-    pl = paro.Plan(ctx, "NNN", [elems], bucket_elems=min(elems, 1 << 28), topology="ho",
-                   stream=stream.cuda_stream, transport=args.transport, comm_impl=args.comm_impl,
-                   fuse_gather="never")
-    pl.synth_grads(rank, SEED, 1)
-    ms = timeit(lambda: pl.collective(0))
-    pl.close()
-    x = torch.ones(elems, dtype=torch.bfloat16, device="cuda")
-    ms_nccl = timeit(lambda: dist.all_reduce(x))
-    del x
-    bw = nbytes * factor / (ms / 1e3) / 1e9
-    return {"op": "all-reduce (HO-RS + HO-AG, bf16 hops in canonical order)", "bytes": nbytes,
-            "groups": f"{world // M}x{M}", "ms": ms, "busbw_GBps": bw, "peak_GBps": 770.0, "frac": bw / 770.0,
-            "nccl_allreduce_busbw_GBps": nbytes * factor / (ms_nccl / 1e3) / 1e9,
-            "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s per direction"}
+    rows = []
+    for mib in sizes_mib:
+        nbytes = mib << 20
+        elems = nbytes // 2
+        iters = max(5, min(200, (64 << 20) // nbytes * 10))
+        row = {"bytes": nbytes, "iters": iters}
+        for topo in ("ho", "flat"):
+            pl = paro.Plan(ctx, "NNN", [elems], bucket_elems=min(elems, 1 << 28), topology=topo,
+                           stream=stream.cuda_stream, transport=args.transport, comm_impl=args.comm_impl,
+                           fuse_gather="never", fuse_allreduce=False)
+            pl.synth_grads(rank, SEED, 1)
+            ms = timeit(lambda: pl.collective(0), iters)
+            pl.close()
+            bw = nbytes * factor / (ms / 1e3) / 1e9
+            row[topo] = {"us": round(ms * 1e3, 2), "busbw_GBps": round(bw, 1), "frac": round(bw / peak, 4)}
+            if bw / peak > 1.2:
+                row[topo]["error"] = "busbw above 1.2 x the 770 GB/s peak: the timed launches do not do the work"
+        x = torch.ones(elems, dtype=torch.bfloat16, device="cuda")
+        ms = timeit(lambda: dist.all_reduce(x), iters)
+        del x
+        bw = nbytes * factor / (ms / 1e3) / 1e9
+        row["nccl"] = {"us": round(ms * 1e3, 2), "busbw_GBps": round(bw, 1), "frac": round(bw / peak, 4)}
+        rows.append(row)
+    torch.cuda.empty_cache()
+    one = next((r for r in rows if r["bytes"] == 1 << 30), rows[-1])
+    return {"op": "all-reduce bf16 (library: HO-RS + HO-AG / flat ring, canonical-order bf16 hops; nccl: "
+                  "torch.distributed all_reduce)", "groups": f"{world // M}x{M}",
+            "peak_GBps": peak, "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s per direction",
+            "at_1GiB": {"ho_busbw_GBps": one["ho"]["busbw_GBps"], "flat_busbw_GBps": one["flat"]["busbw_GBps"],
+                        "nccl_busbw_GBps": one["nccl"]["busbw_GBps"], "ho_frac": one["ho"]["frac"]},
+            "sweep": rows}
 
 
 def _cudart():

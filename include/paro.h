@@ -92,7 +92,9 @@ typedef struct {
                           * with no collective rounds beside it and no peer       *
                           * stores: the 2 x 1 OS != G codes), through thread       *
                           * stores otherwise;                                      *
-                          * 1: the LSU (ld.global) kernel; 2: TMA both ways always */
+                          * 1: the LSU (ld.global) kernel; 2: TMA both ways always; *
+                          * 3: TMA loads + thread stores always (the variant real  *
+                          * N > 1 steps use beside collectives).  Same bits.       */
   int comm_impl;         /* 2 (default): collective rounds move operands with TMA  *
                           * bulk copies into shared memory and the folded tile     *
                           * leaves through a bulk copy too (measured 1-10 % faster *
@@ -169,7 +171,16 @@ typedef struct {
                           * every OS != G code, the partials being the raw         *
                           * gradients.  Topologies HO, two-step, direct (any for   *
                           * G = I except NCCL).  Off with pull_transport = 0,      *
-                          * clipping / skip and inter_gbps pacing.  0: the ring.   */
+                          * clipping / skip and inter_gbps pacing.  0: the ring,   *
+                          * and no part of any reduction runs inside Adam (the     *
+                          * OS = G final hop stays in the rounds kernel too), so   *
+                          * paro_collective(0) performs the whole reduction.       */
+  int adam_smem_kb;      /* > 0: shared memory (KB) the TMA Adam kernel may use for *
+                          * its stages, overriding the automatic 200 KB alone /    *
+                          * ~120 KB beside collectives (so an emulated or N = 1    *
+                          * run executes the co-run variants: 4096- or 2048-elem   *
+                          * tiles, 2-4 stages).  0 (default): automatic.  Must be  *
+                          * <= 220.                                                 */
 } paro_opts_t;
 
 typedef struct {
@@ -376,10 +387,15 @@ paro_status_t paro_accumulate(paro_plan_t plan, const void* const* grads);
 
 /* Collective only (no optimizer): run the plan's gradient-reduction launches
  * (what = 0) or parameter all-gather launches (what = 1) for every bucket,
- * stream-ordered like paro_step.  With strategy NNN, what = 0 is a
- * hierarchical all-reduce of the flat gradient buffer (gradients pre-scaled by
- * 1/N, i.e. the average) on the plan's topology: the HO-Ring all-reduce of
- * BASELINE config 5.  Requires a real or emulated context. */
+ * stream-ordered like paro_step.  With strategy NNN and fuse_allreduce = 0,
+ * what = 0 is a hierarchical all-reduce of the flat gradient buffer
+ * (gradients pre-scaled by 1/N, i.e. the average) on the plan's topology: the
+ * HO-Ring all-reduce of BASELINE config 5 (bucket b's average lands in
+ * paro_buffer kind 3, slot b % (pipeline_depth + 1)).
+ * Requires a real or emulated context.  PARO_ERR_STATE for what = 0 on a plan
+ * that folds part of its reduction into the Adam kernel (fuse_allreduce = 1:
+ * the inter all-reduce at g = 2, or the final hop of OS = G): its reduce
+ * launches alone do not complete the reduction. */
 paro_status_t paro_collective(paro_plan_t plan, int what);
 
 /* Per-kernel timing over a region of steps (used by bench.py for the roofline):
@@ -404,6 +420,10 @@ typedef struct {
    * 2 B per g_hat input (fused final hop) + 2 B per fused-gather push, per
    * element; collectives = 2 B per task input + 2 B per output element */
   int64_t adam_hbm_bytes, comm_hbm_bytes;
+  /* the last Adam launch: 0 adam_kernel (LSU), 1 adam_tma_kernel<false,512>   *
+   * (bulk loads, thread stores), 2 <true,512> (bulk loads + stores), 3       *
+   * <true,256>, 4 <false,256>; -1 none; and its shared-memory stage count     */
+  int32_t adam_variant, adam_stages;
 } paro_profile_t;
 
 paro_status_t paro_profile_start(paro_plan_t plan, int max_launches);

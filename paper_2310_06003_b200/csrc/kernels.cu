@@ -12,6 +12,7 @@
 // intrinsic, so nvcc cannot contract them to FMA; bf16 rounding is cvt.rn.
 #include <cuda_bf16.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "kernels.h"
@@ -873,7 +874,7 @@ static cudaError_t set_carveouts() {
   const void* fns[] = {(const void*)rounds_kernel, (const void*)rounds_tma_kernel<false>,
                        (const void*)rounds_tma_kernel<true>, (const void*)adam_kernel,
                        (const void*)adam_tma_kernel<false, 512>, (const void*)adam_tma_kernel<true, 512>,
-                       (const void*)adam_tma_kernel<true, 256>};
+                       (const void*)adam_tma_kernel<true, 256>, (const void*)adam_tma_kernel<false, 256>};
   for (const void* f : fns) {
     cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout,
                                          (int)cudaSharedmemCarveoutMaxShared);
@@ -926,12 +927,17 @@ cudaError_t launch_adam(const AdamArgs& a, int grid, cudaStream_t s, int cap_two
   return cudaGetLastError();
 }
 
-// TMA pipeline: persistent grid (one CTA per SM); stages sized to ~200 KB.
 // TMA pipeline: persistent grid (one CTA per SM), stages sized to the budget.
-// The TMA-store variant refills a stage one iteration late (after its stores
-// have read it), so it keeps >= 3 stages: with a small budget (collectives
-// co-running) it switches to 2048-element tiles (256 threads).
-cudaError_t launch_adam_tma(const AdamArgs& a, int sms, cudaStream_t s, int smem_budget_kb, int tma_store) {
+// smem_budget_kb sets the stage count (2-4); hard_kb is what the SM can give
+// Adam beside the co-running collective CTA (its stages are the rest of the
+// 228 KB).  Thread stores (kStore = false) keep >= 2 stages of 4096-element
+// tiles (512 threads) when they fit hard_kb, else 2048-element tiles (256
+// threads).  The TMA-store variant refills a stage one iteration late (after
+// its stores have read it), so it keeps >= 3 stages: with a small budget it
+// switches to 2048-element tiles.  Returns the variant (AdamVariant) and stage
+// count through *variant / *stages.
+cudaError_t launch_adam_tma(const AdamArgs& a, int sms, cudaStream_t s, int smem_budget_kb, int tma_store,
+                            int hard_kb, int* variant, int* stages) {
   cudaError_t ec = set_carveouts();
   if (ec != cudaSuccess) return ec;
   int gmax = 1;
@@ -939,28 +945,38 @@ cudaError_t launch_adam_tma(const AdamArgs& a, int sms, cudaStream_t s, int smem
   static bool attr_set = false;
   if (!attr_set) {
     for (const void* f : {(const void*)adam_tma_kernel<false, 512>, (const void*)adam_tma_kernel<true, 512>,
-                          (const void*)adam_tma_kernel<true, 256>}) {
+                          (const void*)adam_tma_kernel<true, 256>, (const void*)adam_tma_kernel<false, 256>}) {
       cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
       if (e != cudaSuccess) return e;
     }
     attr_set = true;
   }
-  auto stages_for = [&](int tile) {
-    const size_t stage = (size_t)tile * (2 * gmax + 12);
-    int st = (int)(((size_t)smem_budget_kb * 1024) / stage);
-    return st > 4 ? 4 : (st < 2 ? 2 : st);
-  };
+  if (hard_kb <= 0 || hard_kb > 220) hard_kb = 220;
+  auto stage_bytes = [&](int tile) { return (size_t)tile * (2 * gmax + 12); };
+  auto raw = [&](int tile, int kb) { return (int)(((size_t)kb * 1024) / stage_bytes(tile)); };
+  auto clampst = [](int st, int lo) { return st > 4 ? 4 : (st < lo ? lo : st); };
+  int v = 0, st = 0;
   if (!tma_store) {
-    const int st = stages_for(4096);
-    adam_tma_kernel<false, 512><<<sms, 512, (size_t)4096 * (2 * gmax + 12) * st, s>>>(a, gmax, st);
-  } else if (stages_for(4096) >= 3) {
-    const int st = stages_for(4096);
-    adam_tma_kernel<true, 512><<<sms, 512, (size_t)4096 * (2 * gmax + 12) * st, s>>>(a, gmax, st);
+    st = clampst(raw(4096, smem_budget_kb), 2);
+    if ((size_t)st * stage_bytes(4096) <= (size_t)hard_kb * 1024) {
+      v = ADAM_TMA_LD_512;
+      adam_tma_kernel<false, 512><<<sms, 512, stage_bytes(4096) * st, s>>>(a, gmax, st);
+    } else {
+      st = clampst(std::min(raw(2048, smem_budget_kb), raw(2048, hard_kb)), 2);
+      v = ADAM_TMA_LD_256;
+      adam_tma_kernel<false, 256><<<sms, 256, stage_bytes(2048) * st, s>>>(a, gmax, st);
+    }
+  } else if (raw(4096, smem_budget_kb) >= 3) {
+    st = clampst(raw(4096, smem_budget_kb), 3);
+    v = ADAM_TMA_ST_512;
+    adam_tma_kernel<true, 512><<<sms, 512, stage_bytes(4096) * st, s>>>(a, gmax, st);
   } else {
-    int st = stages_for(2048);
-    if (st < 3) st = 3;
-    adam_tma_kernel<true, 256><<<sms, 256, (size_t)2048 * (2 * gmax + 12) * st, s>>>(a, gmax, st);
+    st = clampst(raw(2048, smem_budget_kb), 3);
+    v = ADAM_TMA_ST_256;
+    adam_tma_kernel<true, 256><<<sms, 256, stage_bytes(2048) * st, s>>>(a, gmax, st);
   }
+  if (variant) *variant = v;
+  if (stages) *stages = st;
   return cudaGetLastError();
 }
 

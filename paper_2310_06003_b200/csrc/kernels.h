@@ -107,7 +107,16 @@ struct PackEntry {     // one tensor slice: src/dst element pointers + count
 // launchers (return cudaGetLastError())
 cudaError_t launch_rounds(const RoundsArgs& a, int grid, int block, cudaStream_t s);
 cudaError_t launch_adam(const AdamArgs& a, int grid, cudaStream_t s, int cap_two_per_sm);
-cudaError_t launch_adam_tma(const AdamArgs& a, int sms, cudaStream_t s, int smem_budget_kb, int tma_store);
+// Adam kernel variants (reported by paro_profile_stop)
+enum AdamVariant : int {
+  ADAM_LSU = 0,          // adam_kernel (ld/st.global)
+  ADAM_TMA_LD_512 = 1,   // adam_tma_kernel<false, 512>: bulk-copy loads, thread stores, 4096-elem tiles
+  ADAM_TMA_ST_512 = 2,   // adam_tma_kernel<true, 512>: bulk-copy loads and stores
+  ADAM_TMA_ST_256 = 3,   // adam_tma_kernel<true, 256>: same, 2048-elem tiles (small budget)
+  ADAM_TMA_LD_256 = 4    // adam_tma_kernel<false, 256>: thread stores, 2048-elem tiles
+};
+cudaError_t launch_adam_tma(const AdamArgs& a, int sms, cudaStream_t s, int smem_budget_kb, int tma_store,
+                            int hard_kb, int* variant, int* stages);
 cudaError_t launch_rounds_tma(const RoundsArgs& a, int grid, int max_in, cudaStream_t s, int bulk_store);
 cudaError_t launch_norm_finalize(const double* partials, int n, double* out, cudaStream_t s);
 // phase 1 of the two-phase step: block partials of sum (fold(gin) * s_g)^2 and

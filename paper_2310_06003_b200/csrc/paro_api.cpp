@@ -122,6 +122,7 @@ struct paro_plan {
   std::vector<int64_t> prof_hbm;          // algorithmic HBM bytes of the launch (this GPU)
   int prof_used = 0;
   int64_t prof_steps = 0, prof_launches = 0;
+  int adam_variant = -1, adam_stages = 0;   // the last Adam launch (AdamVariant)
   uint64_t* d_trace = nullptr;            // [kTraceLaunches][grid][kTraceSlots]
   std::vector<int> trace_nrounds;         // rounds of each traced launch
   int trace_grid = 0;
@@ -606,6 +607,7 @@ void paro_opts_default(paro_opts_t* o) {
   o->frozen = 0;
   o->grad_slots = 0;
   o->fuse_allreduce = 1;
+  o->adam_smem_kb = 0;
 }
 
 paro_status_t paro_get_unique_id(paro_uid_t* out) {
@@ -723,10 +725,13 @@ paro_status_t paro_plan(paro_ctx_t ctx, const char* strategy, const int64_t* par
   po.two_phase = o.clip_norm > 0.f || o.skip_nonfinite != 0;
   if (po.two_phase) po.fuse_final = false;   // g_hat is materialised for the norm pass
   po.fuse_ar_e = po.fuse_final && o.fuse_allreduce != 0;
+  if (o.fuse_allreduce == 0) po.fuse_final = false;   // no part of the reduction inside Adam
   if (o.gather_windows < 0 || o.gather_windows > 64) return fail(PARO_ERR_INVALID, "gather_windows must be in [0, 64]");
   po.windows = o.gather_windows;
   if (o.fuse_gather < 0 || o.fuse_gather > 2) return fail(PARO_ERR_INVALID, "fuse_gather must be 0, 1 or 2");
   if (o.comm_impl < 0 || o.comm_impl > 2) return fail(PARO_ERR_INVALID, "comm_impl must be 0, 1 or 2");
+  if (o.adam_impl < 0 || o.adam_impl > 3) return fail(PARO_ERR_INVALID, "adam_impl must be 0, 1, 2 or 3");
+  if (o.adam_smem_kb < 0 || o.adam_smem_kb > 220) return fail(PARO_ERR_INVALID, "adam_smem_kb must be in [0, 220]");
   po.fuse_gather = (o.inter_gbps > 0.f || o.topology == PARO_TOPO_NCCL) ? 0 : o.fuse_gather;
   // paced (emulated-gap) runs keep every transfer in the rounds kernel, which
   // paces them; the NCCL comparator has no copy-engine path
@@ -1194,12 +1199,32 @@ paro_status_t step_impl(PlanT* p, const void* const* grads, void* const* params,
     // vs 17.8-18.7 ms) the thread stores stay faster)
     bool pushes = false;
     for (int i = 0; i < aa.nseg; ++i) pushes = pushes || aa.seg[i].npush > 0;
-    const bool tma_store = p->opts.adam_impl == 2 ||
-                           (p->opts.adam_impl == 0 && (pl.N == 1 || ctx->mode == MODE_EMU ||
-                                                       (pl.fused_allreduce && !corun && !pushes)));
-    if (p->opts.adam_impl != 1)
-      CK(launch_adam_tma(aa, ctx->sm_count, ctx->comp, corun ? 120 : 200, tma_store ? 1 : 0));
-    else CK(launch_adam(aa, grid, ctx->comp, corun ? 1 : 0));
+    const int ai = p->opts.adam_impl;
+    const bool tma_store = ai == 2 || (ai == 0 && (pl.N == 1 || ctx->mode == MODE_EMU ||
+                                                   (pl.fused_allreduce && !corun && !pushes)));
+    // shared memory: the stage count follows a budget of ~120 KB while
+    // collectives co-run (200 KB alone); the hard limit is what the SM has left
+    // beside the largest co-running TMA rounds CTA (4 stages x 8 KB per input,
+    // 228 KB per SM, 1 KB reserved per CTA).  adam_smem_kb > 0 forces both
+    // (emulated / N = 1 runs of the co-run configurations).
+    int budget = corun ? 120 : 200, hard = 220;
+    if (corun && p->opts.comm_impl != 1) {
+      int mx = 1;
+      for (size_t b = 0; b < red.size(); ++b) {
+        if (red[b].nrounds > 0) mx = std::max(mx, red[b].max_in);
+        if (p->gat[b].nrounds > 0) mx = std::max(mx, p->gat[b].max_in);
+      }
+      hard = 226 - 1 - 32 * mx;
+    }
+    if (p->opts.adam_smem_kb > 0) budget = hard = p->opts.adam_smem_kb;
+    if (ai != 1) {
+      CK(launch_adam_tma(aa, ctx->sm_count, ctx->comp, budget, tma_store ? 1 : 0, hard, &p->adam_variant,
+                         &p->adam_stages));
+    } else {
+      CK(launch_adam(aa, grid, ctx->comp, corun ? 1 : 0));
+      p->adam_variant = ADAM_LSU;
+      p->adam_stages = 0;
+    }
     prof_end(p, ctx->comp, pk);
     ++n_adam;
     ++launches;
@@ -1523,6 +1548,18 @@ paro_status_t paro_collective(paro_plan_t p, int what) {
   if (ctx->mode == MODE_PLANNER) return fail(PARO_ERR_STATE, "planning-only context");
   if (what != 0 && what != 1) return fail(PARO_ERR_INVALID, "what must be 0 (reduce) or 1 (gather)");
   const Planner& pl = *p->pl;
+  // a plan that folds part of its gradient reduction into the Adam kernel (the
+  // inter all-reduce, R31, or the owner's final hop for OS = G) has reduce
+  // launches that do not complete the reduction on their own
+  if (what == 0 && pl.N > 1 && pl.opt.topology != PARO_TOPO_NCCL) {
+    bool folded = pl.fused_allreduce;
+    for (const BucketSchedule& S0 : pl.sched)
+      for (const auto& gin : S0.ghat_in) folded = folded || gin.size() > 1;
+    if (folded)
+      return fail(PARO_ERR_STATE,
+                  "plan folds part of its reduction into the Adam kernel (fused inter all-reduce or final hop): "
+                  "paro_collective(0) needs a plan made with fuse_allreduce = 0");
+  }
   cudaStream_t S = p->opts.stream ? static_cast<cudaStream_t>(p->opts.stream) : ctx->main;
   int launches = 0;
   CK(cudaEventRecord(p->ev_fork, S));
@@ -1599,6 +1636,8 @@ paro_status_t paro_profile_stop(paro_plan_t p, paro_profile_t* out) {
   }
   out->steps = p->prof_steps;
   out->kernel_launches = p->prof_launches;
+  out->adam_variant = p->adam_variant;
+  out->adam_stages = p->adam_stages;
   // device-side trace of the first collective launches: where the time goes
   if (!p->trace_nrounds.empty()) {
     const int G = p->trace_grid;

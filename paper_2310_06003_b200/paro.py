@@ -48,7 +48,7 @@ class paro_opts_t(C.Structure):
                 ("inter_gbps", C.c_float), ("clip_norm", C.c_float), ("skip_nonfinite", C.c_int),
                 ("fuse_gather", C.c_int), ("copy_engine", C.c_int), ("gather_windows", C.c_int), ("grad_accum", C.c_int),
                 ("stream", C.c_void_p), ("frozen", C.c_int), ("grad_slots", C.c_int),
-                ("fuse_allreduce", C.c_int)]
+                ("fuse_allreduce", C.c_int), ("adam_smem_kb", C.c_int)]
 
 
 class paro_plan_info_t(C.Structure):
@@ -73,7 +73,11 @@ class paro_profile_t(C.Structure):
                 ("comm_launches", C.c_int64), ("adam_elems", C.c_int64), ("comm_bytes", C.c_int64),
                 ("steps", C.c_int64), ("kernel_launches", C.c_int64), ("traced_launches", C.c_int64),
                 ("traced_barrier_ms", C.c_double), ("traced_work_ms", C.c_double), ("traced_final_ms", C.c_double),
-                ("adam_hbm_bytes", C.c_int64), ("comm_hbm_bytes", C.c_int64)]
+                ("adam_hbm_bytes", C.c_int64), ("comm_hbm_bytes", C.c_int64),
+                ("adam_variant", C.c_int32), ("adam_stages", C.c_int32)]
+
+ADAM_VARIANTS = {-1: None, 0: "adam_kernel", 1: "adam_tma_kernel<false,512>", 2: "adam_tma_kernel<true,512>",
+                 3: "adam_tma_kernel<true,256>", 4: "adam_tma_kernel<false,256>"}
 
 
 class paro_advise_in_t(C.Structure):
@@ -160,7 +164,8 @@ def check(status):
 def make_opts(bucket_elems=1 << 26, topology="ho", beta1=0.9, beta2=0.95, eps=1e-8, weight_decay=0.0,
               loss_scale=1.0, comm_ctas=148, pipeline_depth=2, stream=None, transport="pull", adam_impl="auto",
               comm_impl="tma_store", inter_gbps=0.0, grad_accum=False, clip_norm=0.0, skip_nonfinite=False, gather_windows=0,
-              fuse_gather="auto", copy_engine=False, frozen=False, grad_slots=0, fuse_allreduce=True):
+              fuse_gather="auto", copy_engine=False, frozen=False, grad_slots=0, fuse_allreduce=True,
+              adam_smem_kb=0):
     o = paro_opts_t()
     paro_opts_default(C.byref(o))
     o.bucket_elems = int(bucket_elems)
@@ -169,7 +174,7 @@ def make_opts(bucket_elems=1 << 26, topology="ho", beta1=0.9, beta2=0.95, eps=1e
     o.weight_decay, o.loss_scale = weight_decay, loss_scale
     o.comm_ctas, o.pipeline_depth = int(comm_ctas), int(pipeline_depth)
     o.pull_transport = {"push": 0, "pull": 1}[transport]
-    o.adam_impl = {"auto": 0, "lsu": 1, "tma_store": 2}[adam_impl]
+    o.adam_impl = {"auto": 0, "lsu": 1, "tma_store": 2, "tma": 3}[adam_impl]
     o.comm_impl = {"tma": 0, "lsu": 1, "tma_store": 2}[comm_impl]
     o.inter_gbps = float(inter_gbps)
     o.grad_accum = 1 if grad_accum else 0
@@ -182,6 +187,7 @@ def make_opts(bucket_elems=1 << 26, topology="ho", beta1=0.9, beta2=0.95, eps=1e
     o.frozen = 1 if frozen else 0
     o.grad_slots = int(grad_slots)
     o.fuse_allreduce = 1 if fuse_allreduce else 0
+    o.adam_smem_kb = int(adam_smem_kb)
     return o
 
 

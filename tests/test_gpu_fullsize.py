@@ -9,8 +9,8 @@ Checked bit-exact after 2 steps: fp32 master / m / v and bf16 parameters in
 windows at the start, middle and end of the rank's residency in the first,
 middle and last bucket (the last is ragged); the whole shard map (every
 bucket's OS and P range) and the per-rank bytes sent (exact, Table 3 / the
-per-strategy closed form).  N = 1 in a subprocess; N = 2 / 4 under torchrun
-when the box has the GPUs.
+per-strategy closed form).  N = 1 in a subprocess; N = every visible GPU
+(2 / 4 / 8) under torchrun when the box has them.
 """
 import json
 import os
@@ -118,15 +118,17 @@ def test_fullsize_7b_single_gpu(tmp_path):
 
 @pytest.mark.skipif(_ngpu() < 2, reason="needs >= 2 GPUs")
 def test_fullsize_7b_multi_gpu(tmp_path):
-    """N = 2 / 4 (2x1 / 2x2): `bench.py --gpus N` under torchrun."""
-    world = 4 if _ngpu() >= 4 else 2
-    _run(tmp_path, world, {"steps": 2})
+    """Every visible GPU (2x1 / 2x2 / 2x4 at 2 / 4 / 8 GPUs, bench's default split):
+    `bench.py --gpus N` under torchrun."""
+    _run(tmp_path, _ngpu(), {"steps": 2})
 
 
 @pytest.mark.skipif(_ngpu() < 4, reason="needs 4 GPUs")
 def test_fullsize_30b_streamed_gradients(tmp_path):
     """The largest workload (BASELINE config 4's LLaMA-30B list, OS = G
-    strategy GGG at 2x2, 136 GB per rank) with streamed gradients (4 slots):
-    sampled windows bit-exact, shard map and bytes exact."""
-    _run(tmp_path, 4, {"steps": 2, "grad_slots": 4,
-                       "bench_args": ["--model", "30B", "--strategy", "GGG", "--group-size", "2"]})
+    strategy GGG at 2 x (N/2): 2x2 on 4 GPUs (136 GB per rank), 2x4 on 8) with
+    streamed gradients (4 slots): sampled windows bit-exact, shard map and bytes
+    exact."""
+    world = _ngpu()
+    _run(tmp_path, world, {"steps": 2, "grad_slots": 4,
+                           "bench_args": ["--model", "30B", "--strategy", "GGG", "--group-size", str(world // 2)]})

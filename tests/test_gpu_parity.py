@@ -33,7 +33,8 @@ class EmuRun:
 
     def __init__(self, N, M, code, sizes, B, topo="ho", depth=2, wd=0.0, loss_scale=1.0, transport="push",
                  adam_impl="auto", comm_impl="tma_store", grad_accum=False, mode="emulated", clip_norm=0.0,
-                 skip_nonfinite=False, fuse_gather="auto", copy_engine=False, fuse_allreduce=True):
+                 skip_nonfinite=False, fuse_gather="auto", copy_engine=False, fuse_allreduce=True,
+                 adam_smem_kb=0):
         paro = _paro()
         if mode == "emulated":
             self.ctx = paro.Context(N, M, mode="emulated", device=0)
@@ -43,7 +44,7 @@ class EmuRun:
                             weight_decay=wd, loss_scale=loss_scale, transport=transport, adam_impl=adam_impl,
                             comm_impl=comm_impl, grad_accum=grad_accum, clip_norm=clip_norm,
                             skip_nonfinite=skip_nonfinite, fuse_gather=fuse_gather, copy_engine=copy_engine,
-                            fuse_allreduce=fuse_allreduce)
+                            fuse_allreduce=fuse_allreduce, adam_smem_kb=adam_smem_kb)
         self.info = self.pl.info()
         self.N, self.code, self.sizes = N, code, sizes
         n = self.info["os_numel"]
@@ -207,18 +208,67 @@ def test_flat_ring_matches_oracle_flat_simulation(transport):
         run.close()
 
 
-@pytest.mark.parametrize("adam_impl", ["auto", "lsu", "tma_store"])
+# Adam kernels selected by (adam_impl, adam_smem_kb); emulated "auto" = TMA
+# stores.  g_hat inputs per element at 2x4: NNN 1, III 2 (AR_E folded into
+# Adam, R31), IIG / GGG 3 (HO-Ring final hop fused).  120 KB is the co-run
+# budget real N > 1 steps use; 60 KB forces 2048-element thread-store tiles.
+ADAM_CASES = [("auto", 0), ("lsu", 0), ("tma_store", 0), ("tma", 0), ("tma", 120), ("tma_store", 120),
+              ("tma", 60)]
+
+
+@pytest.mark.parametrize("adam_impl,smem", ADAM_CASES)
 @pytest.mark.parametrize("code", ["IIG", "NNN", "III", "GGG"])
-def test_4m_2x4_ten_steps(code, adam_impl):
+def test_4m_2x4_ten_steps(code, adam_impl, smem):
     N, M = 8, 4
     lay = L.Layout(CONFIG_4M["sizes"], N, M, CONFIG_4M["B"])
     ref = _dp_reference(lay, 10)
-    run = EmuRun(N, M, code, CONFIG_4M["sizes"], CONFIG_4M["B"], adam_impl=adam_impl)
+    run = EmuRun(N, M, code, CONFIG_4M["sizes"], CONFIG_4M["B"], adam_impl=adam_impl, adam_smem_kb=smem)
     for t in range(1, 11):
         run.set_grads(t)
+        if t == 10:
+            run.pl.profile_start(4096)
         run.step(t)
+    prof = run.pl.profile_stop()
     _check_against_dp(run, lay, ref)
+    v = _paro().ADAM_VARIANTS[prof["adam_variant"]]
+    if adam_impl == "lsu":
+        assert v == "adam_kernel"
+    elif adam_impl == "tma":
+        assert v in ("adam_tma_kernel<false,512>", "adam_tma_kernel<false,256>")
+        if smem == 60:
+            assert v == "adam_tma_kernel<false,256>"
+    else:
+        assert v.startswith("adam_tma_kernel<true,")
+        if smem == 120:
+            assert v == "adam_tma_kernel<true,256>"
     run.close()
+
+
+def test_adam_variant_selection_covers_corun_kernels():
+    """The co-run budget (120 KB) selects the kernels real N > 1 steps run:
+    thread stores with 4096-element tiles at 2 stages when they fit, 2048-element
+    tiles when two 4096-element stages of a 3-input fused hop do not; TMA stores
+    at 2048-element tiles.  Each is bit-exact vs the DP definition."""
+    N, M = 8, 4
+    sizes = [N * 64 * 40 + 24, 1000]
+    B = N * 64 * 8
+    lay = L.Layout(sizes, N, M, B)
+    ref = _dp_reference(lay, 2)
+    seen = set()
+    for code, impl, kb in (("NNN", "tma", 120), ("IIG", "tma", 120), ("GGG", "tma", 120), ("III", "tma", 120),
+                           ("IIG", "tma_store", 120), ("NIG", "tma", 0)):
+        run = EmuRun(N, M, code, sizes, B, adam_impl=impl, adam_smem_kb=kb, transport="pull")
+        run.pl.profile_start(1024)
+        for t in (1, 2):
+            run.set_grads(t)
+            run.step(t)
+        prof = run.pl.profile_stop()
+        seen.add((_paro().ADAM_VARIANTS[prof["adam_variant"]], prof["adam_stages"]))
+        _check_against_dp(run, lay, ref)
+        run.close()
+    names = {v for v, _ in seen}
+    assert {"adam_tma_kernel<false,512>", "adam_tma_kernel<false,256>", "adam_tma_kernel<true,256>"} <= names, seen
+    assert ("adam_tma_kernel<false,512>", 2) in seen, seen
 
 
 @pytest.mark.parametrize("fuse", [True, False])
@@ -233,9 +283,9 @@ def test_fused_inter_allreduce_os_i(N, M, topo, fuse):
     lay = L.Layout(sizes, N, M, B)
     ref = _dp_reference(lay, 3)
     for code in ("III", "NII", "INI", "NNI") + (("NNN",) if M == 1 else ()):
-        for adam_impl, depth in (("auto", 1), ("lsu", 2)):
+        for adam_impl, depth, kb in (("auto", 1, 0), ("lsu", 2, 0), ("tma", 1, 120)):
             run = EmuRun(N, M, code, sizes, B, topo=topo, depth=depth, transport="pull", adam_impl=adam_impl,
-                         fuse_allreduce=fuse)
+                         fuse_allreduce=fuse, adam_smem_kb=kb)
             for t in (1, 2, 3):
                 run.set_grads(t)
                 stats = run.step(t)
@@ -807,3 +857,42 @@ def test_empty_model_and_zero_size_tensors(sizes):
             run.pl.step(run.ptrs(), LR, 3, grads=ptrs)
             torch.cuda.synchronize()
         run.close()
+
+
+# --------------------------------------------------------------------- collective only (BASELINE config 5)
+@pytest.mark.parametrize("N,M", [(8, 4), (4, 2), (2, 1), (8, 1)])
+@pytest.mark.parametrize("topo", ["ho", "two_step", "flat"])
+def test_collective_allreduce_matches_oracle(N, M, topo):
+    """paro_collective(0) of an NNN plan made with fuse_allreduce = 0 is the bf16
+    gradient all-reduce the bench sweeps (config 5): every rank's g_hat slot holds
+    the canonical-order average (HO-Ring / two-step: dp_reduce; flat ring: the
+    oracle's flat-ring simulation), bucket by bucket; a plan that folds part of
+    the reduction into Adam is refused."""
+    paro = _paro()
+    B = N * 64 * 16
+    sizes = [3 * B - N * 64 * 5]          # 3 buckets (ragged last): every slot of depth 2 holds one
+    lay = L.Layout(sizes, N, M, B)
+    grads = _oracle_grads(N, lay.psi, 1)
+    if topo == "flat":
+        res = ST.strategy_step("NNN", lay, grads, ST.init_state(master_f32(0, lay.psi), lay, "NNN"),
+                               nm.AdamScalars(LR, 1), topology="flat")
+        want = {r: res.ghat_os[r] for r in range(N)}
+    else:
+        gh = ST.dp_reduce(lay, grads)
+        want = {r: gh for r in range(N)}
+    ctx = paro.Context(N, M, mode="emulated", device=0)
+    pl = paro.Plan(ctx, "NNN", sizes, bucket_elems=B, topology=topo, fuse_allreduce=False, transport="pull")
+    for r in range(N):
+        pl.synth_grads(r, SEED, 1)
+    pl.collective(0)
+    torch.cuda.synchronize()
+    for r in range(N):
+        for b, (s0, n) in enumerate(lay.buckets):
+            got = d2h(pl.buffer(r, 3) + 2 * (b % 3) * B, n, np.uint16)
+            assert np.array_equal(got, want[r][s0:s0 + n]), (topo, r, b)
+    pl.close()
+    fused = paro.Plan(ctx, "GGG", sizes, bucket_elems=B, topology=topo, transport="pull")   # final hop in Adam
+    with pytest.raises(paro.ParoError, match="fuse_allreduce = 0"):
+        fused.collective(0)
+    fused.close()
+    ctx.close()

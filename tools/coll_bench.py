@@ -73,7 +73,7 @@ def main():
             bucket = min(elems, 1 << 28)
             pl = paro.Plan(ctx, code, [elems], bucket_elems=bucket, topology=topo, comm_ctas=a.comm_ctas,
                            stream=stream.cuda_stream, transport=a.transport, comm_impl=a.comm_impl,
-                           inter_gbps=a.inter_gbps, fuse_gather="never")
+                           inter_gbps=a.inter_gbps, fuse_gather="never", fuse_allreduce=False)
             pl.synth_grads(rank, 1234, 1)
             ms = timeit(lambda: pl.collective(what))
             row[topo] = {"ms": round(ms, 4), "busbw_GBps": round(nbytes * factor / (ms / 1e3) / 1e9, 1)}

@@ -27,7 +27,7 @@ def main():
     code = sys.argv[2] if len(sys.argv) > 2 else "IIG"
     N, M = 4, 2
     ctx = paro.Context(N, M, mode="emulated", device=0)
-    pl = paro.Plan(ctx, code, [n], bucket_elems=n)
+    pl = paro.Plan(ctx, code, [n], bucket_elems=n, fuse_allreduce=False)   # whole reduction in the rounds kernel
     for r in range(N):
         pl.synth_grads(r, SEED, 1)
     for _ in range(3):

@@ -91,7 +91,7 @@ def main():
                              transport=cfg["transport"], adam_impl=cfg["adam_impl"],
                              comm_impl=cfg["comm_impl"], fuse_gather={1: "always", 0: "never"}.get(cfg["fuse_gather"], cfg["fuse_gather"]),
                              copy_engine=bool(cfg["copy_engine"]), grad_slots=cfg["grad_slots"],
-                             fuse_allreduce=bool(cfg["fuse_allreduce"]))
+                             fuse_allreduce=bool(cfg["fuse_allreduce"]) and not a.collective_only)
         except Exception as e:  # noqa: BLE001
             if rank == 0:
                 print(json.dumps({"cfg": cfg, "error": str(e)}), flush=True)
