@@ -78,6 +78,19 @@ def canonical_fold(ys, c: int, op=hop):
     return acc
 
 
+def hop_f32(a, b) -> np.ndarray:
+    """One reduction hop of the fp32 wire (SURVEY reading A3, wire_dtype = 1):
+    a plain IEEE fp32 addition of fp32 partials, no bf16 rounding."""
+    return (np.asarray(a, dtype=F32) + np.asarray(b, dtype=F32)).astype(F32)
+
+
+def pack_f32(grad_bits, alpha: float) -> np.ndarray:
+    """Pre-scaling on the fp32 wire: x = fp32(g) * fp32(alpha), one fp32
+    rounding (exact for power-of-two N), kept in fp32 (reading A3/A4)."""
+    with np.errstate(over="ignore", invalid="ignore"):
+        return (f32_from_bf16_bits(grad_bits) * F32(alpha)).astype(F32)
+
+
 def pack(grad_bits, alpha: float) -> np.ndarray:
     """Gradient pre-scaling before the reduction: x = RNE_bf16(fp32(g) * fp32(alpha)).
 
@@ -98,11 +111,13 @@ class AdamScalars:
     step_size = lr / (1 - beta1^t);  bc2s = sqrt(1 - beta2^t);
     decay = 1 - lr * weight_decay;  s_g = 1 / loss_scale (unscale, R4).
     With gradient accumulation over s micro-batches the accumulated sum is
-    turned into the mini-batch mean here: s_g = 1 / (loss_scale * s) (R27).
+    turned into the mini-batch mean here: s_g = 1 / (loss_scale * s) (R27);
+    without pre-division (predivide = 0) the rank average too:
+    s_g = 1 / (loss_scale * s * N).
     """
 
     def __init__(self, lr, step, beta1=0.9, beta2=0.95, eps=1e-8, weight_decay=0.0,
-                 loss_scale=1.0, clip_coef=1.0, accum_steps=1):
+                 loss_scale=1.0, clip_coef=1.0, accum_steps=1, post_div=1):
         if step < 1:
             raise ValueError("step must be >= 1")
         if accum_steps < 1:
@@ -119,14 +134,16 @@ class AdamScalars:
         self.eps = F32(eps)
         self.wd = float(weight_decay)
         self.decay = F32(1.0 - lr * float(weight_decay))
-        self.s_g = F32((1.0 / (float(loss_scale) * accum_steps)) * float(clip_coef))
+        # post_div = N when the 1/N average is not applied at pack time
+        # (predivide = 0): the sum is averaged here, in the same rounding
+        self.s_g = F32((1.0 / (float(loss_scale) * accum_steps * post_div)) * float(clip_coef))
 
 
 def adam_update(master, m, v, ghat_bits, sc: AdamScalars):
     """Canonical fp32 Adam on one owned shard (P:225 mixed-precision Adam; R5-R7).
 
     Inputs: fp32 arrays master, m, v (not modified) and the reduced gradient
-    as bf16 bits.  Returns (master', m', v', param_bf16_bits).  Every line is
+    as bf16 bits (uint16; bf16 wire) or as fp32 values (float32; fp32 wire).  Returns (master', m', v', param_bf16_bits).  Every line is
     one IEEE fp32 operation rounded to nearest; NumPy float32 array
     arithmetic never contracts to FMA.
 
@@ -144,7 +161,7 @@ def adam_update(master, m, v, ghat_bits, sc: AdamScalars):
     with np.errstate(invalid="ignore", over="ignore"):   # non-finite inputs propagate (R9)
         if sc.wd != 0.0:
             w = w * sc.decay
-        gr = f32_from_bf16_bits(ghat_bits) * sc.s_g
+        gr = _ghat_f32(ghat_bits) * sc.s_g
         m2 = sc.b1 * m + sc.omb1 * gr
         v2 = sc.b2 * v + sc.omb2 * (gr * gr)
         d = np.sqrt(v2) / sc.bc2s + sc.eps
@@ -152,7 +169,13 @@ def adam_update(master, m, v, ghat_bits, sc: AdamScalars):
     return w2.astype(F32), m2.astype(F32), v2.astype(F32), bf16_bits_from_f32(w2)
 
 
+def _ghat_f32(ghat):
+    """g_hat as fp32 values: bf16 bit patterns are widened exactly, fp32 kept."""
+    ghat = np.asarray(ghat)
+    return ghat.astype(F32) if ghat.dtype == F32 else f32_from_bf16_bits(ghat)
+
+
 def grad_sq_sum(ghat_bits, s_g=F32(1.0)) -> float:
     """sum_i (fp32(g_hat_i) * s_g)^2 in fp64 (norm reporting, R8)."""
-    gr = (f32_from_bf16_bits(ghat_bits) * F32(s_g)).astype(np.float64)
+    gr = (_ghat_f32(ghat_bits) * F32(s_g)).astype(np.float64)
     return float(np.sum(gr * gr))

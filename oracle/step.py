@@ -26,7 +26,7 @@ from . import collectives as C
 from .accounting import step_ops
 from .layout import Layout
 from .numerics import (F32, AdamScalars, adam_update, bf16_bits_from_f32, canonical_fold,
-                       f32_from_bf16_bits, hop, pack)
+                       f32_from_bf16_bits, hop, hop_f32, pack, pack_f32)
 from .strategy import validate
 
 
@@ -57,26 +57,40 @@ def init_state(master_full, lay: Layout, code, ranks=None):
     return out
 
 
-def dp_reduce(lay: Layout, grads):
-    """g_hat = CanonReduce(RNE_bf16(grad_r / N)) over the N ranks (R2, R4), as bf16 bits."""
+def wire_ops(N, wire="bf16", predivide=True):
+    """(pack, hop, dtype) of a wire (readings R2/R4, A3): bf16 wire: x =
+    RNE_bf16(g * alpha) and the bf16 hop; fp32 wire: x = fp32(g) * alpha kept in
+    fp32 and plain fp32 addition, g_hat in fp32.  alpha = 1/N with pre-division,
+    1 without (the average is then taken in Adam's unscale, AdamScalars post_div)."""
+    alpha = 1.0 / N if predivide else 1.0
+    if wire == "bf16":
+        return (lambda g: pack(g, alpha)), hop, np.uint16
+    if wire == "fp32":
+        return (lambda g: pack_f32(g, alpha)), hop_f32, F32
+    raise ValueError(wire)
+
+
+def dp_reduce(lay: Layout, grads, wire="bf16", predivide=True):
+    """g_hat = CanonReduce(pack(grad_r)) over the N ranks (R2, R4): bf16 bits on
+    the bf16 wire (pack = RNE_bf16(grad_r / N)), fp32 values on the fp32 wire."""
     N = lay.N
     geo = C.Geometry(N, lay.M)
-    alpha = 1.0 / N
-    X = [pack(pad_flat(gr, lay.psi_pad, np.uint16), alpha) for gr in grads]
-    ghat = np.zeros(lay.psi_pad, np.uint16)
+    pk, op, dt = wire_ops(N, wire, predivide)
+    X = [pk(pad_flat(gr, lay.psi_pad, np.uint16)) for gr in grads]
+    ghat = np.zeros(lay.psi_pad, dt)
     for (s, n) in lay.buckets:
         segn = n // N
         for r in range(N):
             j, p = geo.jp(r)
             k = geo.seg(j, p)
             a, b = s + k * segn, s + (k + 1) * segn
-            S = [canonical_fold([X[geo.r(jj, pp)][a:b] for pp in range(lay.M)], p)
+            S = [canonical_fold([X[geo.r(jj, pp)][a:b] for pp in range(lay.M)], p, op)
                  for jj in range(geo.g)]
-            ghat[a:b] = canonical_fold(S, j)
+            ghat[a:b] = canonical_fold(S, j, op)
     return ghat
 
 
-def dp_reduce_window(lay: Layout, grad_of, a, b):
+def dp_reduce_window(lay: Layout, grad_of, a, b, wire="bf16", predivide=True):
     """dp_reduce restricted to flat elements [a, b) (sampled parity at full size).
 
     The definition is elementwise, so a window needs only its own inputs:
@@ -89,18 +103,21 @@ def dp_reduce_window(lay: Layout, grad_of, a, b):
     j, p = lay.owner_segment(a)
     if lay.owner_segment(b - 1) != (j, p):
         raise ValueError("window crosses a segment boundary")
-    X = [pack(np.asarray(grad_of(r, a, b - a), np.uint16), 1.0 / N) for r in range(N)]
-    S = [canonical_fold([X[geo.r(jj, pp)] for pp in range(lay.M)], p) for jj in range(geo.g)]
-    return canonical_fold(S, j)
+    pk, op, _ = wire_ops(N, wire, predivide)
+    X = [pk(np.asarray(grad_of(r, a, b - a), np.uint16)) for r in range(N)]
+    S = [canonical_fold([X[geo.r(jj, pp)] for pp in range(lay.M)], p, op) for jj in range(geo.g)]
+    return canonical_fold(S, j, op)
 
 
-def dp_step(lay: Layout, grads, master, m, v, sc: AdamScalars):
+def dp_step(lay: Layout, grads, master, m, v, sc: AdamScalars, wire="bf16", predivide=True):
     """Unsharded data parallel with the canonical order (full-length arrays, Psi_pad).
 
-    grads: list of N flat bf16-bit arrays (length Psi or Psi_pad).
-    Returns (master, m, v, param_bits, g_hat_bits).
+    grads: list of N flat bf16-bit arrays (length Psi or Psi_pad).  wire /
+    predivide: see wire_ops (without pre-division sc must carry post_div = N).
+    Returns (master, m, v, param_bits, g_hat) -- g_hat as bf16 bits, or fp32
+    values on the fp32 wire.
     """
-    ghat = dp_reduce(lay, grads)
+    ghat = dp_reduce(lay, grads, wire, predivide)
     w2, m2, v2, pb = adam_update(master, m, v, ghat, sc)
     return w2, m2, v2, pb, ghat
 
@@ -210,7 +227,8 @@ def _add_trace(res, tr):
     res.rounds += tr.n_rounds()
 
 
-def strategy_step(code, lay: Layout, grads, state, sc: AdamScalars, topology="ho"):
+def strategy_step(code, lay: Layout, grads, state, sc: AdamScalars, topology="ho", wire="bf16",
+                  predivide=True):
     """One s = 1 step of strategy `code` on all N ranks.
 
     grads: list of N flat bf16-bit arrays.  state: from init_state (updated
@@ -220,8 +238,9 @@ def strategy_step(code, lay: Layout, grads, state, sc: AdamScalars, topology="ho
     "flat" (ring over all ranks, P:399 -- a different, still deterministic
     accumulation order) or "h_ring" (H-Ring all-gather with one leader per
     group, P:401-402 / S:378; its reduce-scatter is two-step).  G = I always runs RS_I then the inter op (Fig 2/3).
+    wire / predivide: see wire_ops (fp32 wire: every partial and g_hat in fp32).
     """
-    return _simulate(code, lay, [grads], state, sc, topology, accumulate=False)
+    return _simulate(code, lay, [grads], state, sc, topology, accumulate=False, wire=wire, predivide=predivide)
 
 
 def strategy_accum_step(code, lay: Layout, grads_mb, state, sc: AdamScalars, topology="ho"):
@@ -247,14 +266,14 @@ def strategy_accum_step(code, lay: Layout, grads_mb, state, sc: AdamScalars, top
     return _simulate(code, lay, grads_mb, state, sc, topology, accumulate=True)
 
 
-def _simulate(code, lay, grads_mb, state, sc, topology, accumulate):
+def _simulate(code, lay, grads_mb, state, sc, topology, accumulate, wire="bf16", predivide=True):
     pl, gl, ol = validate(code)
     N, M = lay.N, lay.M
     geo = C.Geometry(N, M)
-    alpha = 1.0 / N
+    pk, hop, _ = wire_ops(N, wire, predivide)
     grad_ops, rest_ops = step_ops(code)
     res = StepResult(N)
-    X_mb = [[pack(pad_flat(gr, lay.psi_pad, np.uint16), alpha) for gr in grads] for grads in grads_mb]
+    X_mb = [[pk(pad_flat(gr, lay.psi_pad, np.uint16)) for gr in grads] for grads in grads_mb]
     new = {r: {"master": [], "m": [], "v": [], "param": []} for r in range(N)}
     ghat_os = {r: [] for r in range(N)}
     gshard = {r: [] for r in range(N)}
@@ -384,7 +403,8 @@ def _simulate(code, lay, grads_mb, state, sc, topology, accumulate):
         uniq = [np.concatenate(ghat_os[geo.r(0, p)]) for p in range(M)]
     else:
         uniq = [np.concatenate(ghat_os[0])]
-    allg = f32_from_bf16_bits(np.concatenate(uniq)) * sc.s_g
+    u = np.concatenate(uniq)
+    allg = (u if u.dtype == F32 else f32_from_bf16_bits(u)) * sc.s_g
     res.norm_sq = float(np.sum(allg.astype(np.float64) ** 2))
     res.nonfinite = bool(not np.all(np.isfinite(allg)))
     for r in range(N):
