@@ -181,6 +181,19 @@ typedef struct {
                           * run executes the co-run variants: 4096- or 2048-elem   *
                           * tiles, 2-4 stages).  0 (default): automatic.  Must be  *
                           * <= 220.                                                 */
+  int wire_dtype;        /* 0 (default): bf16 wire (G is 2 bytes): every hop *
+                          * RNE_bf16(fp32 a + fp32 b), g_hat bf16.  1: fp32 wire   *
+                          * (reading A3): pre-scaled raw gradients, partials, the  *
+                          * G residency and g_hat are fp32 (4 B per element on the *
+                          * wire and in those buffers; bytes sent double), every   *
+                          * hop one fp32 add, g_hat never rounded to bf16, so the  *
+                          * result depends on the split / bucket only through fp32 *
+                          * summation order (<= 1e-5 after 10 steps, SURVEY        *
+                          * §8(c-4)).  Not with grad_accum or copy_engine = 2.     */
+  int predivide;         /* 1 (default): raw gradients are multiplied by 1/N when   *
+                          * first read (R4); 0: the raw sum is reduced and the 1/N *
+                          * average is applied in Adam's unscale, s_g = 1 /        *
+                          * (loss_scale * N) (reading A4; same bits for N = 2^k).  */
 } paro_opts_t;
 
 typedef struct {
@@ -310,9 +323,9 @@ paro_status_t paro_rank_gather_send_bytes(paro_plan_t plan, int rank, int64_t* i
  *           Writing gradients here and passing grads = NULL to paro_step is
  *           the zero-copy path.
  *   kind 1: parameter buffer, bf16, p_numel elements (P residency, bucket-major).
- *   kind 2: G-residency buffer, bf16, g_numel elements (NULL for G = N, whose
- *           gradient residency is the flat gradient buffer).
- *   kind 3: reduced-gradient slots (bf16; slot b % (pipeline_depth+1) holds
+ *   kind 2: G-residency buffer, bf16 (fp32 on the fp32 wire), g_numel elements
+ *           (NULL for G = N, whose gradient residency is the flat gradient buffer).
+ *   kind 3: reduced-gradient slots (bf16, fp32 on the fp32 wire; slot b % (pipeline_depth+1) holds
  *           bucket b's g_hat at the OS residency) or NULL when g_hat lives in
  *           the G-residency buffer or is consumed directly by Adam.
  *   kind 4: the G = N gradient accumulator (bf16, psi_pad elements; grad_accum

@@ -148,9 +148,10 @@ def dp_clip_step(lay: Layout, grads, master, m, v, lr, step, clip_norm=0.0, skip
 
 def clip_update(ghat, master, m, v, lr, step, clip_norm, skip_nonfinite, accum_steps, adam_kw):
     sc0 = AdamScalars(lr, step, accum_steps=accum_steps, **adam_kw)
-    g = f32_from_bf16_bits(ghat) * sc0.s_g
+    g32 = ghat if np.asarray(ghat).dtype == F32 else f32_from_bf16_bits(ghat)   # bf16 bits or fp32 wire
+    g = g32 * sc0.s_g
     norm_sq = float(np.sum(g.astype(np.float64) ** 2))
-    nonfinite = not bool(np.all(np.isfinite(f32_from_bf16_bits(ghat))))   # R9: a non-finite g_hat
+    nonfinite = not bool(np.all(np.isfinite(g32)))   # R9: a non-finite g_hat
     if skip_nonfinite and nonfinite:
         return (np.array(master, np.float32), np.array(m, np.float32), np.array(v, np.float32),
                 bf16_bits_from_f32(master), ghat, norm_sq, 1.0, True)

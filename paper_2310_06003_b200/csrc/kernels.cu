@@ -64,6 +64,28 @@ __device__ __forceinline__ void hop8(float acc[8], const float x[8]) {
   unpack8(p, acc);
 }
 
+// fp32 wire (reading A3): x <- fp32(x) * alpha, acc <- acc + x, no bf16 rounding
+__device__ __forceinline__ void mul8(float f[8], float alpha) {
+#pragma unroll
+  for (int e = 0; e < 8; ++e) f[e] = __fmul_rn(f[e], alpha);
+}
+__device__ __forceinline__ void add8(float acc[8], const float x[8]) {
+#pragma unroll
+  for (int e = 0; e < 8; ++e) acc[e] = __fadd_rn(acc[e], x[e]);
+}
+// a raw gradient's pre-scaling and one hop, on the wire of the task / segment
+__device__ __forceinline__ void pre8(float f[8], float alpha, bool wide) {
+  if (wide) mul8(f, alpha);
+  else scale_round8(f, alpha);
+}
+__device__ __forceinline__ void hopw8(float acc[8], const float x[8], bool wide) {
+  if (wide) add8(acc, x);
+  else hop8(acc, x);
+}
+__device__ __forceinline__ void f4x2(const float4& a, const float4& b, float f[8]) {
+  f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w; f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
+}
+
 // ------------------------------------------------------------- sync helpers
 __device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
   uint64_t v;
@@ -207,7 +229,41 @@ __device__ __noinline__ void run_fold_generic(const DTask* __restrict__ t, float
   }
 }
 
+// fp32 wire task (out_f32): inputs bf16 (raw gradients, pre-scaled in fp32) or
+// fp32 partials, fp32 additions in the task's (canonical) order, fp32 result.
+__device__ __noinline__ void run_fold_wide(const DTask* __restrict__ t, float alpha) {
+  const int nin = t->nin;
+  const uint32_t raw = t->rawmask, f32 = t->f32mask;
+  const int64_t n8 = t->n8;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  auto load = [&](int i, int64_t u, float f[8]) {
+    if ((f32 >> i) & 1u) {
+      const float4* p = reinterpret_cast<const float4*>(t->in[i]) + 2 * u;
+      f4x2(__ldcg(p), __ldcg(p + 1), f);
+    } else {
+      unpack8(__ldcg(reinterpret_cast<const uint4*>(t->in[i]) + u), f);
+      if ((raw >> i) & 1u) mul8(f, alpha);
+    }
+  };
+  for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n8; u += stride) {
+    float acc[8];
+    load(0, u, acc);
+    for (int i = 1; i < nin; ++i) {
+      float x[8];
+      load(i, u, x);
+      add8(acc, x);
+    }
+    float4* d = reinterpret_cast<float4*>(t->dst) + 2 * u;
+    __stcg(d, make_float4(acc[0], acc[1], acc[2], acc[3]));
+    __stcg(d + 1, make_float4(acc[4], acc[5], acc[6], acc[7]));
+  }
+}
+
 __device__ __forceinline__ void run_task(const DTask* __restrict__ t, float alpha) {
+  if (t->out_f32) {
+    run_fold_wide(t, alpha);
+    return;
+  }
   switch (t->nin) {
     case 1: run_fold<1, 2>(t, alpha); break;
     case 2: run_fold<2, 1>(t, alpha); break;
@@ -261,29 +317,54 @@ __device__ __forceinline__ float adam_elem(float g, float& w, float& m, float& v
   return w2;
 }
 
+// g_hat input i of an Adam segment at 8-element unit u, as fp32 (bf16 widened, or
+// fp32 on the fp32 wire); raw gradients pre-scaled on the segment's wire
+__device__ __forceinline__ void ld_gin8(const AdamSeg& sg, int i, int64_t u, float alpha, float f[8]) {
+  if ((sg.gf32 >> i) & 1u) {
+    const float4* p = reinterpret_cast<const float4*>(sg.gin[i]) + 2 * u;
+    f4x2(__ldcs(p), __ldcs(p + 1), f);
+  } else {
+    unpack8(__ldcs(reinterpret_cast<const uint4*>(sg.gin[i]) + u), f);
+    if ((sg.graw >> i) & 1u) pre8(f, alpha, sg.gwide != 0);
+  }
+}
+
 __device__ __forceinline__ void adam_unit(const AdamSeg& sg, int64_t u, const AdamScal& c, double& nsq,
                                           int& bad) {
-  uint4 gv[kAdamMaxIn];
-#pragma unroll
-  for (int i = 0; i < kAdamMaxIn; ++i)
-    if (i < sg.gnin) gv[i] = __ldcs(reinterpret_cast<const uint4*>(sg.gin[i]) + u);
+  float g[8];
   const float4* mp = reinterpret_cast<const float4*>(sg.master) + 2 * u;
   const float4* m1p = reinterpret_cast<const float4*>(sg.m) + 2 * u;
   const float4* v1p = reinterpret_cast<const float4*>(sg.v) + 2 * u;
-  const float4 w0 = __ldcs(mp), w1 = __ldcs(mp + 1);
-  const float4 m0 = __ldcs(m1p), m1 = __ldcs(m1p + 1);
-  const float4 v0 = __ldcs(v1p), v1 = __ldcs(v1p + 1);
-  // g_hat: fused final hop(s) of the reduction, canonical order (R2)
-  float g[8];
-  unpack8(gv[0], g);
-  if (sg.graw & 1u) scale_round8(g, c.alpha);
+  float4 w0, w1, m0, m1, v0, v1;
+  if (!sg.gwide) {
+    uint4 gv[kAdamMaxIn];
 #pragma unroll
-  for (int i = 1; i < kAdamMaxIn; ++i) {
-    if (i < sg.gnin) {
+    for (int i = 0; i < kAdamMaxIn; ++i)
+      if (i < sg.gnin) gv[i] = __ldcs(reinterpret_cast<const uint4*>(sg.gin[i]) + u);
+    w0 = __ldcs(mp), w1 = __ldcs(mp + 1);
+    m0 = __ldcs(m1p), m1 = __ldcs(m1p + 1);
+    v0 = __ldcs(v1p), v1 = __ldcs(v1p + 1);
+    // g_hat: fused final hop(s) of the reduction, canonical order (R2)
+    unpack8(gv[0], g);
+    if (sg.graw & 1u) scale_round8(g, c.alpha);
+#pragma unroll
+    for (int i = 1; i < kAdamMaxIn; ++i) {
+      if (i < sg.gnin) {
+        float x[8];
+        unpack8(gv[i], x);
+        if ((sg.graw >> i) & 1u) scale_round8(x, c.alpha);
+        hop8(g, x);
+      }
+    }
+  } else {   // fp32 wire: fp32 inputs / fp32 hops, g_hat stays fp32
+    w0 = __ldcs(mp), w1 = __ldcs(mp + 1);
+    m0 = __ldcs(m1p), m1 = __ldcs(m1p + 1);
+    v0 = __ldcs(v1p), v1 = __ldcs(v1p + 1);
+    ld_gin8(sg, 0, u, c.alpha, g);
+    for (int i = 1; i < sg.gnin; ++i) {
       float x[8];
-      unpack8(gv[i], x);
-      if ((sg.graw >> i) & 1u) scale_round8(x, c.alpha);
-      hop8(g, x);
+      ld_gin8(sg, i, u, c.alpha, x);
+      add8(g, x);
     }
   }
   float w[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
@@ -429,15 +510,17 @@ __device__ __forceinline__ bool tile_of(const AdamArgs& a, int64_t t, TileRef& o
 // leave through bulk copies too (master, m, v, the bf16 parameter and, for the
 // fused all-gather, the peers' parameter buffers): the stage is refilled one
 // iteration later, once its stores have read it (wait_group.read 1).
+// gsz: bytes per g_hat element in the stages (2 bf16; 4 when any input is fp32,
+// the fp32 wire).
 template <bool kStore, int kThr>
-__global__ void __launch_bounds__(kThr, 1) adam_tma_kernel(const AdamArgs a, int gnin_max, int stages) {
+__global__ void __launch_bounds__(kThr, 1) adam_tma_kernel(const AdamArgs a, int gnin_max, int stages, int gsz) {
   constexpr int kTmaTile = kThr * 8;   // elements per tile (8 per thread)
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ uint64_t full_bar[4];
   if (a.skip && *a.skip) return;   // two-phase step: non-finite gradients, update skipped
   const AdamScal c{a.b1, a.omb1, a.b2, a.omb2, a.step_size, a.bc2s, a.eps, a.decay, unscale_of(a), a.alpha,
                    a.has_wd};
-  const size_t g_bytes = (size_t)kTmaTile * 2, f_bytes = (size_t)kTmaTile * 4;
+  const size_t g_bytes = (size_t)kTmaTile * gsz, f_bytes = (size_t)kTmaTile * 4;
   const size_t stage_bytes = gnin_max * g_bytes + 3 * f_bytes;
   int64_t total = 0;
   for (int i = 0; i < a.nseg; ++i) total += (a.seg[i].n8 * 8 + kTmaTile - 1) / kTmaTile;
@@ -453,9 +536,15 @@ __global__ void __launch_bounds__(kThr, 1) adam_tma_kernel(const AdamArgs a, int
     const AdamSeg& sg = a.seg[tr.seg];
     const int s = (int)(k % stages);
     unsigned char* base = smem + s * stage_bytes;
-    const uint32_t gb = (uint32_t)tr.n * 2, fb = (uint32_t)tr.n * 4;
-    mbar_expect_tx(&full_bar[s], sg.gnin * gb + 3 * fb);
-    for (int i = 0; i < sg.gnin; ++i) bulk_g2s(base + i * g_bytes, sg.gin[i] + tr.start, gb, &full_bar[s]);
+    const uint32_t fb = (uint32_t)tr.n * 4;
+    uint32_t tx = 3 * fb;
+    for (int i = 0; i < sg.gnin; ++i) tx += (uint32_t)tr.n * (((sg.gf32 >> i) & 1u) ? 4 : 2);
+    mbar_expect_tx(&full_bar[s], tx);
+    for (int i = 0; i < sg.gnin; ++i) {
+      const int es = ((sg.gf32 >> i) & 1u) ? 4 : 2;
+      bulk_g2s(base + i * g_bytes, reinterpret_cast<const unsigned char*>(sg.gin[i]) + (size_t)tr.start * es,
+               (uint32_t)tr.n * es, &full_bar[s]);
+    }
     unsigned char* fbase = base + gnin_max * g_bytes;
     bulk_g2s(fbase, sg.master + tr.start, fb, &full_bar[s]);
     bulk_g2s(fbase + f_bytes, sg.m + tr.start, fb, &full_bar[s]);
@@ -473,30 +562,45 @@ __global__ void __launch_bounds__(kThr, 1) adam_tma_kernel(const AdamArgs a, int
     const AdamSeg& sg = a.seg[tr.seg];
     unsigned char* base = smem + s * stage_bytes;
     const int e0 = threadIdx.x * 8;
-    if (e0 < tr.n) {
+    const bool act = e0 < tr.n;
+    float* fw = reinterpret_cast<float*>(base + gnin_max * g_bytes);
+    float w[8], m[8], v[8];
+    uint4 pk = make_uint4(0, 0, 0, 0);
+    if (act) {
       float g[8];
-      unpack8(*reinterpret_cast<const uint4*>(base + e0 * 2), g);
-      if (sg.graw & 1u) scale_round8(g, c.alpha);
+      auto ld = [&](int i, float f[8]) {   // g_hat input i of this thread's 8 elements, from the stage
+        if ((sg.gf32 >> i) & 1u) {
+          const float4* q = reinterpret_cast<const float4*>(base + i * g_bytes + (size_t)e0 * 4);
+          f4x2(q[0], q[1], f);
+        } else {
+          unpack8(*reinterpret_cast<const uint4*>(base + i * g_bytes + (size_t)e0 * 2), f);
+          if ((sg.graw >> i) & 1u) pre8(f, c.alpha, sg.gwide != 0);
+        }
+      };
+      ld(0, g);
       for (int i = 1; i < sg.gnin; ++i) {
         float x[8];
-        unpack8(*reinterpret_cast<const uint4*>(base + i * g_bytes + e0 * 2), x);
-        if ((sg.graw >> i) & 1u) scale_round8(x, c.alpha);
-        hop8(g, x);
+        ld(i, x);
+        hopw8(g, x, sg.gwide != 0);
       }
-      float* fw = reinterpret_cast<float*>(base + gnin_max * g_bytes);
       const float4 w0 = *reinterpret_cast<const float4*>(fw + e0), w1 = *reinterpret_cast<const float4*>(fw + e0 + 4);
       const float4 m0 = *reinterpret_cast<const float4*>(fw + kTmaTile + e0);
       const float4 m1 = *reinterpret_cast<const float4*>(fw + kTmaTile + e0 + 4);
       const float4 v0 = *reinterpret_cast<const float4*>(fw + 2 * kTmaTile + e0);
       const float4 v1 = *reinterpret_cast<const float4*>(fw + 2 * kTmaTile + e0 + 4);
-      float w[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
-      float m[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
-      float v[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+      f4x2(w0, w1, w);
+      f4x2(m0, m1, m);
+      f4x2(v0, v1, v);
       const bool in_norm = sg.in_norm != 0;
 #pragma unroll
       for (int e = 0; e < 8; ++e) adam_elem(g[e], w[e], m[e], v[e], c, nsq, bad, in_norm);
-      const uint4 pk = pack8(w);
-      if (kStore) {   // back into the stage, in place (each thread owns its 8 elements)
+      pk = pack8(w);
+    }
+    if (kStore) {
+      // fp32 inputs: every thread has read its input-0 bytes before the bf16
+      // outputs (half their width) are written over them
+      if (gsz == 4) __syncthreads();
+      if (act) {   // back into the stage, in place (each thread owns its 8 elements)
         *reinterpret_cast<float4*>(fw + e0) = make_float4(w[0], w[1], w[2], w[3]);
         *reinterpret_cast<float4*>(fw + e0 + 4) = make_float4(w[4], w[5], w[6], w[7]);
         *reinterpret_cast<float4*>(fw + kTmaTile + e0) = make_float4(m[0], m[1], m[2], m[3]);
@@ -504,17 +608,17 @@ __global__ void __launch_bounds__(kThr, 1) adam_tma_kernel(const AdamArgs a, int
         *reinterpret_cast<float4*>(fw + 2 * kTmaTile + e0) = make_float4(v[0], v[1], v[2], v[3]);
         *reinterpret_cast<float4*>(fw + 2 * kTmaTile + e0 + 4) = make_float4(v[4], v[5], v[6], v[7]);
         *reinterpret_cast<uint4*>(base + e0 * 2) = pk;   // over g_hat input 0 (consumed)
-      } else {
-        const int64_t o = tr.start + e0;
-        __stcs(reinterpret_cast<float4*>(sg.master + o), make_float4(w[0], w[1], w[2], w[3]));
-        __stcs(reinterpret_cast<float4*>(sg.master + o) + 1, make_float4(w[4], w[5], w[6], w[7]));
-        __stcs(reinterpret_cast<float4*>(sg.m + o), make_float4(m[0], m[1], m[2], m[3]));
-        __stcs(reinterpret_cast<float4*>(sg.m + o) + 1, make_float4(m[4], m[5], m[6], m[7]));
-        __stcs(reinterpret_cast<float4*>(sg.v + o), make_float4(v[0], v[1], v[2], v[3]));
-        __stcs(reinterpret_cast<float4*>(sg.v + o) + 1, make_float4(v[4], v[5], v[6], v[7]));
-        *reinterpret_cast<uint4*>(sg.param + o) = pk;
-        for (int i = 0; i < sg.npush; ++i) __stcg(reinterpret_cast<uint4*>(sg.push[i] + o), pk);
       }
+    } else if (act) {
+      const int64_t o = tr.start + e0;
+      __stcs(reinterpret_cast<float4*>(sg.master + o), make_float4(w[0], w[1], w[2], w[3]));
+      __stcs(reinterpret_cast<float4*>(sg.master + o) + 1, make_float4(w[4], w[5], w[6], w[7]));
+      __stcs(reinterpret_cast<float4*>(sg.m + o), make_float4(m[0], m[1], m[2], m[3]));
+      __stcs(reinterpret_cast<float4*>(sg.m + o) + 1, make_float4(m[4], m[5], m[6], m[7]));
+      __stcs(reinterpret_cast<float4*>(sg.v + o), make_float4(v[0], v[1], v[2], v[3]));
+      __stcs(reinterpret_cast<float4*>(sg.v + o) + 1, make_float4(v[4], v[5], v[6], v[7]));
+      *reinterpret_cast<uint4*>(sg.param + o) = pk;
+      for (int i = 0; i < sg.npush; ++i) __stcg(reinterpret_cast<uint4*>(sg.push[i] + o), pk);
     }
     if (kStore) {
       fence_proxy_async_smem();   // this thread's smem writes -> visible to the bulk-copy engine
@@ -577,17 +681,22 @@ constexpr int kRtTileB = kRtTileE * 2;
 constexpr int kRtStages = 4;
 constexpr int kRtMaxIn = 3;
 
+// a stage slot holds kRtTileB bytes per input: 4096 bf16 elements, or 2048 on
+// the fp32 wire (out_f32 tasks, whose fp32 result goes back over input 0)
+__device__ __forceinline__ int rt_te(const DTask* tk) { return tk->out_f32 ? kRtTileE / 2 : kRtTileE; }
+
 __device__ __forceinline__ bool rt_tile(const RoundsArgs& a, const DRound& rd, int64_t t, const DTask*& task,
                                         int64_t& e0, int& ne) {
   for (int ti = rd.t0; ti < rd.t1; ++ti) {
     const DTask* tk = a.tasks + ti;
     if (tk->nin > kRtMaxIn) continue;
+    const int te = rt_te(tk);
     const int64_t n = tk->n8 * 8;
-    const int64_t nt = (n + kRtTileE - 1) / kRtTileE;
+    const int64_t nt = (n + te - 1) / te;
     if (t < nt) {
       task = tk;
-      e0 = t * kRtTileE;
-      ne = (int)min((int64_t)kRtTileE, n - e0);
+      e0 = t * te;
+      ne = (int)min((int64_t)te, n - e0);
       return true;
     }
     t -= nt;
@@ -624,7 +733,7 @@ __global__ void __launch_bounds__(kRtThreads) rounds_tma_kernel(const RoundsArgs
     int64_t total = 0;
     for (int ti = rd.t0; ti < rd.t1; ++ti) {
       const DTask* tk = a.tasks + ti;
-      if (tk->nin <= kRtMaxIn) total += (tk->n8 * 8 + kRtTileE - 1) / kRtTileE;
+      if (tk->nin <= kRtMaxIn) total += (tk->n8 * 8 + rt_te(tk) - 1) / rt_te(tk);
     }
     const int64_t mine = (total > blockIdx.x) ? (total - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
     const uint64_t t_round = globaltimer();
@@ -635,14 +744,19 @@ __global__ void __launch_bounds__(kRtThreads) rounds_tma_kernel(const RoundsArgs
       int ne;
       rt_tile(a, rd, blockIdx.x + k * gridDim.x, tk, e0, ne);
       if (tk->inter && a.inter_bytes_per_ns > 0.0) {   // token bucket: emulated slow inter link
-        inter_sent += (double)ne * 2.0 * (double)tk->inter;
+        inter_sent += (double)ne * (tk->out_f32 ? 4.0 : 2.0) * (double)tk->inter;
         while (inter_sent > (double)(globaltimer() - t_round) * a.inter_bytes_per_ns) __nanosleep(256);
       }
       const uint32_t slot = (cnt + (uint32_t)k) % kRtStages;
       unsigned char* base = smem + slot * stage_bytes;
-      const uint32_t bytes = (uint32_t)ne * 2;
-      mbar_expect_tx(&bars[slot], bytes * tk->nin);
-      for (int i = 0; i < tk->nin; ++i) bulk_g2s(base + i * kRtTileB, tk->in[i] + e0, bytes, &bars[slot]);
+      uint32_t tx = 0;
+      for (int i = 0; i < tk->nin; ++i) tx += (uint32_t)ne * (((tk->f32mask >> i) & 1u) ? 4 : 2);
+      mbar_expect_tx(&bars[slot], tx);
+      for (int i = 0; i < tk->nin; ++i) {
+        const int es = ((tk->f32mask >> i) & 1u) ? 4 : 2;
+        bulk_g2s(base + i * kRtTileB, reinterpret_cast<const unsigned char*>(tk->in[i]) + (size_t)e0 * es,
+                 (uint32_t)ne * es, &bars[slot]);
+      }
     };
     if (threadIdx.x == 0)
       for (int64_t k = 0; k < min((int64_t)kRtStages, mine); ++k) issue(k);
@@ -657,8 +771,46 @@ __global__ void __launch_bounds__(kRtThreads) rounds_tma_kernel(const RoundsArgs
       unsigned char* base = smem + slot * stage_bytes;
       const int nin = tk->nin;
       const uint32_t raw = tk->rawmask;
+      const int osz = tk->out_f32 ? 4 : 2;
+      if (tk->out_f32) {
+        // fp32 wire: 2048-element tile = one 8-element unit per thread; fp32
+        // inputs read as 2 x float4, raw bf16 gradients widened and pre-scaled
+        const int u = threadIdx.x;
+        const bool act = u < ne / 8;
+        float acc[8];
+        if (act) {
+          for (int i = 0; i < nin; ++i) {
+            float x[8];
+            if ((tk->f32mask >> i) & 1u) {
+              const float4* q = reinterpret_cast<const float4*>(base + i * kRtTileB) + 2 * u;
+              f4x2(q[0], q[1], x);
+            } else {
+              unpack8(reinterpret_cast<const uint4*>(base + i * kRtTileB)[u], x);
+              if ((raw >> i) & 1u) mul8(x, a.alpha);
+            }
+            if (i == 0) {
+#pragma unroll
+              for (int e = 0; e < 8; ++e) acc[e] = x[e];
+            } else {
+              add8(acc, x);
+            }
+          }
+        }
+        if (kBulk) {
+          __syncthreads();   // the fp32 result is wider than a bf16 input 0: all reads first
+          if (act) {
+            float4* q = reinterpret_cast<float4*>(base) + 2 * u;
+            q[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+            q[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+          }
+        } else if (act) {
+          float4* q = reinterpret_cast<float4*>(tk->dst) + (e0 / 8 + u) * 2;
+          __stcg(q, make_float4(acc[0], acc[1], acc[2], acc[3]));
+          __stcg(q + 1, make_float4(acc[4], acc[5], acc[6], acc[7]));
+        }
+      }
       uint4* dst = reinterpret_cast<uint4*>(tk->dst + e0);
-      for (int u = threadIdx.x; u < ne / 8; u += kRtThreads) {
+      for (int u = threadIdx.x; u < (tk->out_f32 ? 0 : ne / 8); u += kRtThreads) {
         const uint4 v0 = reinterpret_cast<const uint4*>(base)[u];
         if (nin == 1 && !(raw & 1u)) {   // plain copy: the stage already holds the result
           if (!kBulk) __stcg(dst + u, v0);
@@ -680,7 +832,7 @@ __global__ void __launch_bounds__(kRtThreads) rounds_tma_kernel(const RoundsArgs
         fence_proxy_async_smem();   // this thread's smem writes -> visible to the bulk-copy engine
         __syncthreads();
         if (threadIdx.x == 0) {
-          bulk_s2g(tk->dst + e0, base, (uint32_t)ne * 2);
+          bulk_s2g(reinterpret_cast<unsigned char*>(tk->dst) + (size_t)e0 * osz, base, (uint32_t)ne * osz);
           bulk_commit();
           bulk_wait_read<1>();      // the previous tile's store has read its stage: refill it
           if (k >= 1 && k - 1 + kRtStages < mine) issue(k - 1 + kRtStages);
@@ -724,13 +876,11 @@ __global__ void __launch_bounds__(kAdamBlock) grad_norm_kernel(const AdamArgs a)
     if (sg.in_norm) {
       for (int64_t u = s + threadIdx.x; u < e; u += blockDim.x) {
         float g[8];
-        unpack8(__ldcs(reinterpret_cast<const uint4*>(sg.gin[0]) + u), g);
-        if (sg.graw & 1u) scale_round8(g, a.alpha);
+        ld_gin8(sg, 0, u, a.alpha, g);
         for (int k = 1; k < sg.gnin; ++k) {
           float x[8];
-          unpack8(__ldcs(reinterpret_cast<const uint4*>(sg.gin[k]) + u), x);
-          if ((sg.graw >> k) & 1u) scale_round8(x, a.alpha);
-          hop8(g, x);
+          ld_gin8(sg, k, u, a.alpha, x);
+          hopw8(g, x, sg.gwide != 0);
         }
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
@@ -940,8 +1090,11 @@ cudaError_t launch_adam_tma(const AdamArgs& a, int sms, cudaStream_t s, int smem
                             int hard_kb, int* variant, int* stages) {
   cudaError_t ec = set_carveouts();
   if (ec != cudaSuccess) return ec;
-  int gmax = 1;
-  for (int i = 0; i < a.nseg; ++i) gmax = a.seg[i].gnin > gmax ? a.seg[i].gnin : gmax;
+  int gmax = 1, gsz = 2;
+  for (int i = 0; i < a.nseg; ++i) {
+    gmax = a.seg[i].gnin > gmax ? a.seg[i].gnin : gmax;
+    if (a.seg[i].gf32) gsz = 4;
+  }
   static bool attr_set = false;
   if (!attr_set) {
     for (const void* f : {(const void*)adam_tma_kernel<false, 512>, (const void*)adam_tma_kernel<true, 512>,
@@ -952,7 +1105,7 @@ cudaError_t launch_adam_tma(const AdamArgs& a, int sms, cudaStream_t s, int smem
     attr_set = true;
   }
   if (hard_kb <= 0 || hard_kb > 220) hard_kb = 220;
-  auto stage_bytes = [&](int tile) { return (size_t)tile * (2 * gmax + 12); };
+  auto stage_bytes = [&](int tile) { return (size_t)tile * (gsz * gmax + 12); };
   auto raw = [&](int tile, int kb) { return (int)(((size_t)kb * 1024) / stage_bytes(tile)); };
   auto clampst = [](int st, int lo) { return st > 4 ? 4 : (st < lo ? lo : st); };
   int v = 0, st = 0;
@@ -960,20 +1113,20 @@ cudaError_t launch_adam_tma(const AdamArgs& a, int sms, cudaStream_t s, int smem
     st = clampst(raw(4096, smem_budget_kb), 2);
     if ((size_t)st * stage_bytes(4096) <= (size_t)hard_kb * 1024) {
       v = ADAM_TMA_LD_512;
-      adam_tma_kernel<false, 512><<<sms, 512, stage_bytes(4096) * st, s>>>(a, gmax, st);
+      adam_tma_kernel<false, 512><<<sms, 512, stage_bytes(4096) * st, s>>>(a, gmax, st, gsz);
     } else {
       st = clampst(std::min(raw(2048, smem_budget_kb), raw(2048, hard_kb)), 2);
       v = ADAM_TMA_LD_256;
-      adam_tma_kernel<false, 256><<<sms, 256, stage_bytes(2048) * st, s>>>(a, gmax, st);
+      adam_tma_kernel<false, 256><<<sms, 256, stage_bytes(2048) * st, s>>>(a, gmax, st, gsz);
     }
   } else if (raw(4096, smem_budget_kb) >= 3) {
     st = clampst(raw(4096, smem_budget_kb), 3);
     v = ADAM_TMA_ST_512;
-    adam_tma_kernel<true, 512><<<sms, 512, stage_bytes(4096) * st, s>>>(a, gmax, st);
+    adam_tma_kernel<true, 512><<<sms, 512, stage_bytes(4096) * st, s>>>(a, gmax, st, gsz);
   } else {
     st = clampst(raw(2048, smem_budget_kb), 3);
     v = ADAM_TMA_ST_256;
-    adam_tma_kernel<true, 256><<<sms, 256, stage_bytes(2048) * st, s>>>(a, gmax, st);
+    adam_tma_kernel<true, 256><<<sms, 256, stage_bytes(2048) * st, s>>>(a, gmax, st, gsz);
   }
   if (variant) *variant = v;
   if (stages) *stages = st;

@@ -21,12 +21,14 @@ constexpr int kMaxAdamSegs = 16;  // emulated ranks per Adam launch
 constexpr int kHeaderBytes = 4096;   // per-rank region header: flags + counters
 
 struct DTask {
-  const uint16_t* in[kDevMaxIn];
+  const uint16_t* in[kDevMaxIn];   // element pointers (bf16, or fp32 where f32mask says so)
   uint16_t* dst;
-  int64_t n8;        // 8-element (16-byte) units
+  int64_t n8;        // 8-element units (16 B of bf16, 32 B of fp32)
   int32_t nin;
-  uint32_t rawmask;  // bit i: input i is a raw gradient -> RNE_bf16(g * alpha)
+  uint32_t rawmask;  // bit i: input i is a raw bf16 gradient -> g * alpha (RNE_bf16 on the bf16 wire)
   int32_t inter;     // operands (inputs + dst) on another group's GPU: paced by inter_gbps
+  uint32_t f32mask;  // bit i: input i holds fp32 values (fp32 wire, reading A3)
+  int32_t out_f32;   // 1: fp32 wire task: fp32 arithmetic (no bf16 rounding), fp32 result
   int32_t pad_;
 };
 
@@ -81,6 +83,8 @@ struct AdamSeg {
   int32_t in_norm;   // elements counted in the unique-element norm
   int32_t npush;     // fused parameter all-gather: the bf16 output is also
   uint16_t* push[kAdamMaxPush];   // stored at these peer addresses (NVLink)
+  uint32_t gf32;     // bit i: gin[i] holds fp32 values (fp32 wire)
+  int32_t gwide;     // 1: fp32 wire: raw inputs g * alpha and hops in fp32, g_hat never rounded to bf16
 };
 
 struct AdamArgs {

@@ -10,8 +10,14 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <nvtx3/nvToolsExt.h>
+
+#include <chrono>
 #include <cmath>
+#include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
+#include <thread>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -123,6 +129,7 @@ struct paro_plan {
   int prof_used = 0;
   int64_t prof_steps = 0, prof_launches = 0;
   int adam_variant = -1, adam_stages = 0;   // the last Adam launch (AdamVariant)
+  float alpha = 1.f;                        // pre-scaling of raw gradients: 1/N (predivide) or 1
   uint64_t* d_trace = nullptr;            // [kTraceLaunches][grid][kTraceSlots]
   std::vector<int> trace_nrounds;         // rounds of each traced launch
   int trace_grid = 0;
@@ -163,6 +170,34 @@ paro_status_t nccl_fail(paro_ctx* ctx, const char* what, ncclResult_t r) {
   return fail(PARO_ERR_NCCL, m);
 }
 
+// Synchronise `s` while polling the NCCL communicators' asynchronous error
+// state (a failed or aborted peer surfaces here instead of a silent hang);
+// after PARO_WATCH_S seconds (default 300) without completion the context is
+// marked timed out.  The in-kernel peer waits time out on their own (20 s).
+paro_status_t sync_watch(paro_ctx* ctx, cudaStream_t s) {
+  const double limit = std::getenv("PARO_WATCH_S") ? std::atof(std::getenv("PARO_WATCH_S")) : 300.0;
+  const auto t0 = std::chrono::steady_clock::now();
+  for (int it = 0;; ++it) {
+    cudaError_t q = cudaStreamQuery(s);
+    if (q == cudaSuccess) return PARO_OK;
+    if (q != cudaErrorNotReady) return cuda_fail(ctx, "cudaStreamQuery", q);
+    for (ncclComm_t c : {ctx->world, ctx->intra, ctx->inter}) {
+      if (!c) continue;
+      ncclResult_t ae = ncclSuccess;
+      ncclResult_t r = ncclCommGetAsyncError(c, &ae);
+      if (r != ncclSuccess) return nccl_fail(ctx, "ncclCommGetAsyncError", r);
+      if (ae != ncclSuccess && ae != ncclInProgress) return nccl_fail(ctx, "NCCL asynchronous error", ae);
+    }
+    const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (el > limit) {
+      ctx->sticky = PARO_ERR_TIMEOUT;
+      ctx->sticky_msg = "the step did not complete within PARO_WATCH_S seconds";
+      return fail(PARO_ERR_TIMEOUT, ctx->sticky_msg);
+    }
+    std::this_thread::sleep_for(std::chrono::microseconds(it < 100 ? 20 : 500));
+  }
+}
+
 paro_status_t check_ctx(paro_ctx* ctx) {
   if (!ctx) return fail(PARO_ERR_INVALID, "null context");
   if (ctx->sticky != PARO_OK) return fail(ctx->sticky, "sticky error: " + ctx->sticky_msg);
@@ -172,6 +207,20 @@ paro_status_t check_ctx(paro_ctx* ctx) {
   }
   return PARO_OK;
 }
+
+// NVTX range over the host-side enqueue of a step / bucket launch (visible to
+// Nsight tools when attached; a no-op otherwise, NVTX3 is header-only)
+struct NvtxRange {
+  explicit NvtxRange(const char* fmt, ...) {
+    char buf[96];
+    va_list ap;
+    va_start(ap, fmt);
+    std::vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    nvtxRangePushA(buf);
+  }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 bool is_local(const PlanT* p, int rank) {
   for (int r : p->local)
@@ -187,13 +236,13 @@ int local_index(const PlanT* p, int rank) {
 
 char* data_ptr(const PlanT* p, int rank, int kind, int64_t off) {
   const Planner& pl = *p->pl;
-  return p->peer_base[rank] + kHeaderBytes + 2 * (pl.buf_off[kind] + off);
+  return p->peer_base[rank] + kHeaderBytes + pl.buf_off[kind] + (int64_t)pl.esz[kind] * off;
 }
 
 // which rank's region a resolved device pointer belongs to (-1: none)
 int data_rank(const PlanT* p, const void* ptr) {
   const char* c = static_cast<const char*>(ptr);
-  const size_t bytes = kHeaderBytes + 2 * (size_t)p->pl->region_elems;
+  const size_t bytes = kHeaderBytes + (size_t)p->pl->region_bytes;
   for (int r = 0; r < (int)p->peer_base.size(); ++r)
     if (p->peer_base[r] && c >= p->peer_base[r] && c < p->peer_base[r] + bytes) return r;
   return -1;
@@ -210,15 +259,20 @@ DTask resolve(const PlanT* p, const Task& t, int executing_rank, int acc_kind, i
   d.n8 = t.n / 8;
   d.rawmask = 0;
   d.inter = 0;
-  const int M = p->pl->M;
+  d.f32mask = 0;
+  const Planner& pl = *p->pl;
+  d.out_f32 = pl.esz[t.dst.kind] == 4 ? 1 : 0;
+  const int M = pl.M;
   for (int i = 0; i < t.nin; ++i) {
     d.in[i] = reinterpret_cast<const uint16_t*>(ptr_of(t.in[i]));
     if (t.in[i].is_raw()) d.rawmask |= 1u << i;
+    else if (pl.esz[t.in[i].kind] == 4) d.f32mask |= 1u << i;
     if (t.in[i].rank / M != executing_rank / M) d.inter += 1;
   }
   d.dst = reinterpret_cast<uint16_t*>(ptr_of(t.dst));
   if (t.dst.rank / M != executing_rank / M) d.inter += 1;
   if (acc_kind >= 0 && t.dst.kind == acc_kind) {
+    if (d.out_f32) d.f32mask |= 1u << d.nin;
     d.in[d.nin++] = d.dst;
     if (t.dst.rank / M != executing_rank / M) d.inter += 1;
   }
@@ -267,21 +321,25 @@ paro_status_t upload_schedule(PlanT* p) {
         for (const Task& t : L.rounds[r][x]) {
           for (int i = 0; i < t.nin; ++i) {
             const int y = t.in[i].rank;
-            if (y != x && (ctx->mode != MODE_REAL || y == ctx->rank)) dl.bytes += 2 * t.n;
+            if (y != x && (ctx->mode != MODE_REAL || y == ctx->rank)) dl.bytes += pl.esz[t.in[i].kind] * t.n;
           }
-          if (t.dst.rank != x && (ctx->mode != MODE_REAL || x == ctx->rank)) dl.bytes += 2 * t.n;
+          if (t.dst.rank != x && (ctx->mode != MODE_REAL || x == ctx->rank)) dl.bytes += pl.esz[t.dst.kind] * t.n;
         }
     for (int r = 0; r < R; ++r)
       for (int x = 0; x < pl.N; ++x) {
         if (ctx->mode == MODE_REAL && x != ctx->rank) continue;
-        for (const Task& t : L.rounds[r][x]) dl.hbm += 2 * t.n * (t.nin + 1);
+        for (const Task& t : L.rounds[r][x]) {
+          dl.hbm += pl.esz[t.dst.kind] * t.n;
+          for (int i = 0; i < t.nin; ++i) dl.hbm += pl.esz[t.in[i].kind] * t.n;
+        }
       }
     dl.final_peers = (ctx->mode == MODE_REAL) ? L.barrier_peers(R, ctx->rank) : 0;
     // copy engines: every task a plain 1-input bit copy
     bool pure = p->opts.copy_engine != 0 && R > 0;
     for (int r = 0; r < R && pure; ++r)
       for (int x = 0; x < pl.N && pure; ++x)
-        for (const Task& t : L.rounds[r][x]) pure = pure && t.nin == 1 && t.in[0].kind != BUF_GRAD;
+        for (const Task& t : L.rounds[r][x])
+          pure = pure && t.nin == 1 && !t.in[0].is_raw() && pl.esz[t.in[0].kind] == pl.esz[t.dst.kind];
     if (pure) {
       dl.dma = true;
       dl.copies.assign(R, {});
@@ -291,7 +349,7 @@ paro_status_t upload_schedule(PlanT* p) {
           if (ctx->mode == MODE_REAL && x != ctx->rank) continue;
           for (const Task& t : L.rounds[r][x]) {
             const DTask d = resolve(p, t, x, -1, win_shift);
-            dl.copies[r].push_back({d.dst, d.in[0], (size_t)t.n * 2});
+            dl.copies[r].push_back({d.dst, d.in[0], (size_t)t.n * pl.esz[t.dst.kind]});
           }
         }
         dl.round_peers[r] = (ctx->mode == MODE_REAL) ? L.barrier_peers(r, ctx->rank) : 0;
@@ -419,7 +477,7 @@ paro_status_t run_launch(PlanT* p, const DevLaunch& dl, int* nlaunch) {
   const int grid = comm_grid(p);
   RoundsArgs a{};
   a.tasks = p->d_tasks;
-  a.alpha = (float)(1.0 / (double)p->pl->N);
+  a.alpha = p->alpha;
   // emulated intra/inter gap: this rank's inter-group transfers are paced to
   // inter_gbps, spread evenly over the CTAs (real mode, TMA rounds kernel)
   a.inter_bytes_per_ns = (ctx->mode == MODE_REAL && p->opts.inter_gbps > 0.f)
@@ -517,9 +575,15 @@ paro_status_t run_nccl(PlanT* p, const std::vector<NcclCall>& calls) {
     void* send = data_ptr(p, c.send.rank, c.send.kind, c.send.off);
     void* recv = data_ptr(p, c.recv.rank, c.recv.kind, c.recv.off);
     ncclComm_t cm = pick_comm(ctx, c.comm);
-    if (c.kind == NcclCall::RS) NK(ncclReduceScatter(send, recv, c.count, ncclBfloat16, ncclAvg, cm, ctx->comm));
-    else if (c.kind == NcclCall::AG) NK(ncclAllGather(send, recv, c.count, ncclBfloat16, cm, ctx->comm));
-    else NK(ncclAllReduce(send, recv, c.count, ncclBfloat16, ncclAvg, cm, ctx->comm));
+    // bf16 wire: NCCL averages the raw gradients (ncclAvg); fp32 wire: the
+    // bucket was pre-scaled into fp32 by the rounds kernel, NCCL sums; without
+    // pre-division NCCL sums the raw gradients and Adam takes the average
+    const bool f32 = p->pl->esz[c.send.kind] == 4;
+    const ncclDataType_t dt = f32 ? ncclFloat : ncclBfloat16;
+    const ncclRedOp_t op = (!f32 && p->pl->opt.predivide) ? ncclAvg : ncclSum;
+    if (c.kind == NcclCall::RS) NK(ncclReduceScatter(send, recv, c.count, dt, op, cm, ctx->comm));
+    else if (c.kind == NcclCall::AG) NK(ncclAllGather(send, recv, c.count, dt, cm, ctx->comm));
+    else NK(ncclAllReduce(send, recv, c.count, dt, op, cm, ctx->comm));
   }
   return PARO_OK;
 }
@@ -608,6 +672,8 @@ void paro_opts_default(paro_opts_t* o) {
   o->grad_slots = 0;
   o->fuse_allreduce = 1;
   o->adam_smem_kb = 0;
+  o->wire_dtype = 0;
+  o->predivide = 1;
 }
 
 paro_status_t paro_get_unique_id(paro_uid_t* out) {
@@ -744,9 +810,13 @@ paro_status_t paro_plan(paro_ctx_t ctx, const char* strategy, const int64_t* par
   if (o.grad_slots > 0) o.copy_engine = 0;   // its stream and barrier channel produce the gradients
   po.grad_slots = o.frozen ? 0 : o.grad_slots;
   po.ce_reduce = o.copy_engine == 2;
+  if (o.wire_dtype != 0 && o.wire_dtype != 1) return fail(PARO_ERR_INVALID, "wire_dtype must be 0 (bf16) or 1 (fp32)");
+  po.wire = o.wire_dtype == 1 ? 4 : 2;
+  po.predivide = o.predivide != 0;
   auto* p = new PlanT();
   p->ctx = ctx;
   p->opts = o;
+  p->alpha = po.predivide ? (float)(1.0 / (double)ctx->N) : 1.0f;
   try {
     p->pl.reset(new Planner(ctx->N, ctx->M, strategy, sizes, po));
   } catch (const std::exception& ex) {
@@ -759,7 +829,7 @@ paro_status_t paro_plan(paro_ctx_t ctx, const char* strategy, const int64_t* par
   }
   const Planner& pl = *p->pl;
   const int N = pl.N;
-  const size_t region_bytes = kHeaderBytes + 2 * (size_t)pl.region_elems;
+  const size_t region_bytes = kHeaderBytes + (size_t)pl.region_bytes;
   auto bail = [&](paro_status_t s) {
     destroy_plan(p);
     return s;
@@ -888,7 +958,7 @@ paro_status_t paro_plan_info(paro_plan_t p, paro_plan_info_t* out) {
   out->mem_g_bytes = pl.mem_bytes(1);
   out->mem_os_bytes = pl.mem_bytes(2);
   int64_t ws = 0;
-  for (int k = BUF_GHAT; k < BUF_NKINDS; ++k) ws += 2 * pl.buf_len[k];
+  for (int k = BUF_GHAT; k < BUF_NKINDS; ++k) ws += (int64_t)pl.esz[k] * pl.buf_len[k];
   out->workspace_bytes = ws + kHeaderBytes;
   out->grad_buffer_bytes = 2 * pl.buf_len[BUF_GRAD];
   const int me = p->ctx->mode == MODE_REAL ? p->ctx->rank : 0;
@@ -1084,11 +1154,12 @@ paro_status_t step_impl(PlanT* p, const void* const* grads, void* const* params,
   const std::vector<DevLaunch>& red = n_acc > 0 ? p->red_acc : p->red;
   cudaStream_t S = p->opts.stream ? static_cast<cudaStream_t>(p->opts.stream) : ctx->main;
   int launches = 0;
+  NvtxRange nr_step("paro_step %s t=%lld", pl.code.c_str(), (long long)step);
 
   // ---- host scalars of canonical Adam (double, rounded once: R6)
   const double b1 = p->opts.beta1, b2 = p->opts.beta2, dlr = lr;
   AdamArgs aa{};
-  aa.alpha = (float)(1.0 / (double)pl.N);
+  aa.alpha = p->alpha;
   aa.b1 = (float)b1;
   aa.omb1 = (float)(1.0 - b1);
   aa.b2 = (float)b2;
@@ -1098,7 +1169,10 @@ paro_status_t step_impl(PlanT* p, const void* const* grads, void* const* params,
   aa.eps = p->opts.eps;
   aa.has_wd = p->opts.weight_decay != 0.0f;
   aa.decay = (float)(1.0 - dlr * (double)p->opts.weight_decay);
-  const double sg_base = 1.0 / ((double)p->opts.loss_scale * (double)(n_acc > 0 ? n_acc : 1));
+  // unscale (R4), the mini-batch mean over accumulated micro-batches (R27) and,
+  // without pre-division, the rank average (reading A4): rounded once
+  const double sg_base = 1.0 / ((double)p->opts.loss_scale * (double)(n_acc > 0 ? n_acc : 1) *
+                                (pl.opt.predivide ? 1.0 : (double)pl.N));
   aa.s_g = (float)sg_base;
   aa.nonfinite = p->d_nonfinite;
 
@@ -1136,6 +1210,7 @@ paro_status_t step_impl(PlanT* p, const void* const* grads, void* const* params,
   auto adam_bucket = [&](int b0, int b1, bool norm_only = false) -> paro_status_t {
     // one Adam (or phase-1 norm) launch over buckets [b0, b1) and every local rank
     if (b0 >= b1) return PARO_OK;   // empty model
+    NvtxRange nr(norm_only ? "paro norm b%d-%d" : "paro adam b%d-%d", b0, b1 - 1);
     aa.nseg = 0;
     for (int li = 0; li < nl; ++li) {
       const int r = p->local[li];
@@ -1148,10 +1223,13 @@ paro_status_t step_impl(PlanT* p, const void* const* grads, void* const* params,
       const std::vector<Ref>& gin = (n_acc > 0) ? S0.ghat_in_acc[r] : S0.ghat_in[r];
       sg.gnin = (int)gin.size();
       sg.graw = 0;
+      sg.gf32 = 0;
+      sg.gwide = pl.opt.wire == 4 ? 1 : 0;
       for (int i = 0; i < sg.gnin; ++i) {
         const Ref& x = gin[i];
         sg.gin[i] = reinterpret_cast<const uint16_t*>(data_ptr(p, x.rank, x.kind, x.off));
         if (x.is_raw()) sg.graw |= 1u << i;
+        else if (pl.esz[x.kind] == 4) sg.gf32 |= 1u << i;
       }
       sg.master = opt_state[li].master + S0.os_off[r];
       sg.m = opt_state[li].m + S0.os_off[r];
@@ -1175,9 +1253,12 @@ paro_status_t step_impl(PlanT* p, const void* const* grads, void* const* params,
     for (int i = 0; i < aa.nseg; ++i) {
       elems += 8 * aa.seg[i].n8;
       // master/m/v read + written (24 B), bf16 parameter written (2 B), every
-      // g_hat input read once (2 B each: local, or by symmetry served to a peer),
-      // every fused-gather push (2 B: by symmetry, a peer's push lands here)
-      hbm += 8 * aa.seg[i].n8 * (26 + 2 * aa.seg[i].gnin + 2 * aa.seg[i].npush);
+      // g_hat input read once (2 B each, 4 on the fp32 wire: local, or by
+      // symmetry served to a peer), every fused-gather push (2 B: by symmetry,
+      // a peer's push lands here)
+      int gb = 0;
+      for (int k = 0; k < aa.seg[i].gnin; ++k) gb += ((aa.seg[i].gf32 >> k) & 1u) ? 4 : 2;
+      hbm += 8 * aa.seg[i].n8 * (26 + gb + 2 * aa.seg[i].npush);
     }
     const int pk = prof_begin(p, ctx->comp, 0, elems, hbm);
     // TMA-pipelined Adam (bulk copies also pull the fused hop's NVLink-peer
@@ -1284,6 +1365,7 @@ paro_status_t step_impl(PlanT* p, const void* const* grads, void* const* params,
       }
     }
     auto do_gather = [&](int b) -> paro_status_t {
+      NvtxRange nr("paro gather b%d", b);
       if (p->gat[b].dma) {   // copy engines, off the comm stream: overlaps the next reductions
         CK(cudaStreamWaitEvent(ctx->dma, p->ev_adam[b], 0));
         dma_used = true;
@@ -1335,12 +1417,17 @@ paro_status_t step_impl(PlanT* p, const void* const* grads, void* const* params,
       return PARO_OK;
     };
     auto do_reduce = [&](int b) -> paro_status_t {
+      NvtxRange nr("paro reduce b%d", b);
       if (src) {
         paro_status_t sp = produce(b);
         if (sp != PARO_OK) return sp;
       }
       if (pre_on) CK(cudaStreamWaitEvent(ctx->comm, p->ev_pre[b], 0));
       if (nccl) {
+        if (red[b].nrounds > 0) {   // fp32 wire: pre-scale the bucket into fp32 first (local round)
+          paro_status_t s2 = run_launch(p, red[b], &launches);
+          if (s2 != PARO_OK) return s2;
+        }
         const int k = prof_begin(p, ctx->comm, 1, 0);
         paro_status_t s3 = run_nccl(p, pl.sched[b].nccl_reduce[ctx->rank]);
         prof_end(p, ctx->comm, k);
@@ -1567,6 +1654,10 @@ paro_status_t paro_collective(paro_plan_t p, int what) {
   const bool nccl = pl.opt.topology == PARO_TOPO_NCCL;
   for (size_t b = 0; b < pl.buckets.size() && pl.N > 1; ++b) {
     if (nccl) {
+      if (what == 0 && p->red[b].nrounds > 0) {   // fp32 wire: pre-scale into fp32 first
+        paro_status_t s2 = run_launch(p, p->red[b], &launches);
+        if (s2 != PARO_OK) return s2;
+      }
       const auto& calls = what == 0 ? pl.sched[b].nccl_reduce[ctx->rank] : pl.sched[b].nccl_gather[ctx->rank];
       const int k = prof_begin(p, ctx->comm, 1, 0);
       paro_status_t s3 = run_nccl(p, calls);
@@ -1683,7 +1774,10 @@ paro_status_t paro_step_stats(paro_plan_t p, paro_step_stats_t* out) {
   if (ctx->mode == MODE_PLANNER) return fail(PARO_ERR_STATE, "planning-only context");
   std::memset(out, 0, sizeof(*out));
   if (!p->stepped) return fail(PARO_ERR_STATE, "no step has run on this plan");
-  CK(cudaStreamSynchronize(p->last_stream));
+  {
+    paro_status_t sw = sync_watch(ctx, p->last_stream);
+    if (sw != PARO_OK) return sw;
+  }
   for (char* r : p->region) {
     int err = 0;
     CK(cudaMemcpy(&err, r + 520, sizeof(int), cudaMemcpyDeviceToHost));

@@ -272,6 +272,9 @@ Planner::Planner(int N_, int M_, const std::string& code_, const std::vector<int
   if (opt.grad_slots < 0) throw std::invalid_argument("grad_slots must be >= 0");
   if (opt.grad_slots > 0 && (opt.accum || opt.ce_reduce))
     throw std::invalid_argument("grad_slots cannot be combined with grad_accum or copy_engine = 2");
+  if (opt.wire != 2 && opt.wire != 4) throw std::invalid_argument("wire_dtype must be 0 (bf16) or 1 (fp32)");
+  if (opt.wire == 4 && (opt.accum || opt.ce_reduce))
+    throw std::invalid_argument("wire_dtype = 1 (fp32) is not available with grad_accum or copy_engine = 2");
   layout();
   if (N == 1 && opt.two_phase && opt.grad_slots > 0 && opt.grad_slots < (int64_t)buckets.size())
     throw std::invalid_argument(
@@ -318,7 +321,7 @@ void Planner::residency(Level l, int r, int64_t b, int64_t* begin, int64_t* end)
 int64_t Planner::mem_bytes(int state) const {
   if (state == 0) return 2 * p_numel;
   if (opt.params_only && state != 0) return 0;
-  if (state == 1) return 2 * (G == LV_N ? psi_pad : g_numel);
+  if (state == 1) return G == LV_N ? 2 * psi_pad : int64_t(opt.wire) * g_numel;
   return 12 * os_numel;
 }
 
@@ -360,6 +363,7 @@ void Planner::layout() {
                           ? kStageSets * land_len : 0;
   buf_len[BUF_GACC] = (opt.accum && G == LV_N) ? psi_pad : 0;
   buf_len[BUF_WIN] = (opt.windows > 0 && P != LV_N && N > 1) ? int64_t(opt.windows) * B : 0;
+  buf_len[BUF_XW] = (opt.wire == 4 && opt.topology == 4 && N > 1) ? B : 0;
   acc_kind = !opt.accum ? -1 : (G == LV_N ? BUF_GACC : BUF_GSHARD);
   if (opt.params_only) {   // frozen tensors: no gradient, no optimizer state, no staging
     for (int k = 0; k < BUF_NKINDS; ++k)
@@ -367,12 +371,16 @@ void Planner::layout() {
     g_numel = os_numel = 0;
     acc_kind = -1;
   }
+  // raw gradients and parameters are bf16; every buffer that holds a
+  // reduction partial or g_hat carries the wire type
+  for (int k = 0; k < BUF_NKINDS; ++k) esz[k] = opt.wire;
+  esz[BUF_GRAD] = esz[BUF_PARAM] = esz[BUF_WIN] = 2;
   int64_t off = 0;
   for (int k = 0; k < BUF_NKINDS; ++k) {
     buf_off[k] = off;
-    off += round_up(buf_len[k], kAlignElems);
+    off += round_up(buf_len[k] * esz[k], 2 * kAlignElems);
   }
-  region_elems = off;
+  region_bytes = off;
 }
 
 void Planner::build_schedule() {
@@ -989,16 +997,21 @@ void Planner::build_schedule() {
       S.reduce.final_extra.assign(1, 0);
       S.gather.final_extra.assign(1, 0);
     } else if (N > 1 && topo == 4) {  // NCCL comparator
+      // fp32 wire: the raw bf16 gradients are first pre-scaled into an fp32
+      // bucket (a local round of the rounds kernel), which NCCL then reduces
+      auto xsrc = [&](int r) { return opt.wire == 4 ? Ref{r, BUF_XW, 0} : grad(r, 0); };
+      if (opt.wire == 4)
+        for (int r = 0; r < N; ++r) S.reduce.add(0, r, make_task(n, {grad(r, 0)}, xsrc(r)));
       for (int r = 0; r < N; ++r) {
         auto& red = S.nccl_reduce[r];
         auto& gat = S.nccl_gather[r];
         const int j = grp(r);
         if (G == LV_I) {
-          red.push_back({NcclCall::RS, NcclCall::INTRA, grad(r, 0), gshard(r, 0), chunk});
+          red.push_back({NcclCall::RS, NcclCall::INTRA, xsrc(r), gshard(r, 0), chunk});
           if (OS == LV_G) red.push_back({NcclCall::RS, NcclCall::INTER, gshard(r, 0), dest_seg(r), C});
           else red.push_back({NcclCall::AR, NcclCall::INTER, gshard(r, 0), gshard(r, 0), chunk});
         } else {
-          red.push_back({NcclCall::RS, NcclCall::INTRA, grad(r, 0), p1(r), chunk});
+          red.push_back({NcclCall::RS, NcclCall::INTRA, xsrc(r), p1(r), chunk});
           red.push_back({NcclCall::RS, NcclCall::INTER, p1(r), dest_seg(r), C});
           if (OS == LV_I) red.push_back({NcclCall::AG, NcclCall::INTER, dest_seg(r), ghat_base(r), C});
           if (OS == LV_N) {
@@ -1093,15 +1106,15 @@ void Planner::count_bytes() {
             for (int i = 0; i < t.nin; ++i) {   // pull: y's bytes travel to x
               const int y = t.in[i].rank;
               if (y == x) continue;
-              (grp(x) == grp(y) ? si[y] : se[y]) += 2 * t.n;
+              (grp(x) == grp(y) ? si[y] : se[y]) += esz[t.in[i].kind] * t.n;
             }
             const int z = t.dst.rank;            // push: x's bytes travel to z
-            if (z != x) (grp(x) == grp(z) ? si[x] : se[x]) += 2 * t.n;
+            if (z != x) (grp(x) == grp(z) ? si[x] : se[x]) += esz[t.dst.kind] * t.n;
           }
     // fused final hop: the Adam kernel reads these inputs (pull: over NVLink)
     for (int x = 0; gin && x < N && (int)gin->size() == N; ++x)
       for (const Ref& y : (*gin)[x])
-        if (y.rank != x) (grp(x) == grp(y.rank) ? si[y.rank] : se[y.rank]) += 2 * os_len;
+        if (y.rank != x) (grp(x) == grp(y.rank) ? si[y.rank] : se[y.rank]) += esz[y.kind] * os_len;
   };
   send_intra.assign(N, 0);
   send_inter.assign(N, 0);
@@ -1132,7 +1145,7 @@ void Planner::count_bytes() {
         for (const NcclCall& c : *calls) {
           const int k = (c.comm == NcclCall::INTRA) ? M : (c.comm == NcclCall::INTER ? g : N);
           const int64_t per = (c.kind == NcclCall::AR) ? 2 * (k - 1) * (c.count / k) : (k - 1) * c.count;
-          (c.comm == NcclCall::INTRA ? send_intra[r] : send_inter[r]) += 2 * per;
+          (c.comm == NcclCall::INTRA ? send_intra[r] : send_inter[r]) += esz[c.send.kind] * per;
         }
         if (!calls->empty()) ++n_comm_launches;
       }

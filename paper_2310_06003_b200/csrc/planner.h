@@ -30,13 +30,14 @@ enum BufKind : int {
   BUF_LAND,        // direct push landing slots: 2 parities x ((M-1) chunks + (g-1) segments)
   BUF_GACC,        // G = N gradient accumulator (psi_pad; only for grad_accum plans)
   BUF_WIN,         // forward/backward parameter gather windows: n_windows x B (P = I or G)
+  BUF_XW,          // NCCL comparator on the fp32 wire: the bucket's pre-scaled fp32 gradients (B)
   BUF_NKINDS
 };
 
-constexpr int kMaxIn = 16;   // max inputs of one fold task
-constexpr int kStageSets = 3;
-constexpr int kMaxAdamIn = 4;
-constexpr int kMaxPush = 8;    // max peers one fused-gather Adam store goes to  // max fold inputs of the fused final hop in Adam  // rotation of per-bucket staging sets (reuse distance)
+constexpr int kMaxIn = 16;     // max inputs of one fold task
+constexpr int kStageSets = 3;  // rotation of per-bucket staging sets (reuse distance)
+constexpr int kMaxAdamIn = 4;  // max fold inputs of the fused final hop in Adam
+constexpr int kMaxPush = 8;    // max peers one fused-gather Adam store goes to
 
 struct Ref {
   int32_t rank = -1;
@@ -127,6 +128,9 @@ struct PlanOptions {
                              // the parameter residency and its forward/backward gathers
   int fuse_gather = 1;       // fold a one-ring parameter all-gather into Adam's stores:
                              // 0 never, 1 when no collective rounds co-run, 2 always
+  int wire = 2;              // bytes per reduction element on the wire and in the G / g_hat /
+                             // staging buffers: 2 = bf16, 4 = fp32 (reading A3)
+  bool predivide = true;     // raw gradients scaled by 1/N when first read (R4); else in Adam
 };
 
 class Planner {
@@ -147,8 +151,9 @@ class Planner {
   int nslots = 0;                                      // BUF_GHAT slots
   int64_t ghat_slot = 0;                               // elements per slot
   int64_t buf_len[BUF_NKINDS] = {0};                   // elements per kind
-  int64_t buf_off[BUF_NKINDS] = {0};                   // element offset in the region
-  int64_t region_elems = 0;                            // symmetric region (bf16 elems)
+  int64_t buf_off[BUF_NKINDS] = {0};                   // BYTE offset of each kind in the region
+  int esz[BUF_NKINDS] = {0};                           // bytes per element of each kind
+  int64_t region_bytes = 0;                            // symmetric region (after the header)
   int64_t stage_i_len = 0, stage_e_len = 0, p1_len = 0, sown_len = 0, land_len = 0;
 
   std::vector<BucketSchedule> sched;

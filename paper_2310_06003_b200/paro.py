@@ -48,7 +48,8 @@ class paro_opts_t(C.Structure):
                 ("inter_gbps", C.c_float), ("clip_norm", C.c_float), ("skip_nonfinite", C.c_int),
                 ("fuse_gather", C.c_int), ("copy_engine", C.c_int), ("gather_windows", C.c_int), ("grad_accum", C.c_int),
                 ("stream", C.c_void_p), ("frozen", C.c_int), ("grad_slots", C.c_int),
-                ("fuse_allreduce", C.c_int), ("adam_smem_kb", C.c_int)]
+                ("fuse_allreduce", C.c_int), ("adam_smem_kb", C.c_int), ("wire_dtype", C.c_int),
+                ("predivide", C.c_int)]
 
 
 class paro_plan_info_t(C.Structure):
@@ -165,7 +166,7 @@ def make_opts(bucket_elems=1 << 26, topology="ho", beta1=0.9, beta2=0.95, eps=1e
               loss_scale=1.0, comm_ctas=148, pipeline_depth=2, stream=None, transport="pull", adam_impl="auto",
               comm_impl="tma_store", inter_gbps=0.0, grad_accum=False, clip_norm=0.0, skip_nonfinite=False, gather_windows=0,
               fuse_gather="auto", copy_engine=False, frozen=False, grad_slots=0, fuse_allreduce=True,
-              adam_smem_kb=0):
+              adam_smem_kb=0, wire_dtype="bf16", predivide=True):
     o = paro_opts_t()
     paro_opts_default(C.byref(o))
     o.bucket_elems = int(bucket_elems)
@@ -188,6 +189,8 @@ def make_opts(bucket_elems=1 << 26, topology="ho", beta1=0.9, beta2=0.95, eps=1e
     o.grad_slots = int(grad_slots)
     o.fuse_allreduce = 1 if fuse_allreduce else 0
     o.adam_smem_kb = int(adam_smem_kb)
+    o.wire_dtype = {"bf16": 0, "fp32": 1, 0: 0, 1: 1}[wire_dtype]
+    o.predivide = 1 if predivide else 0
     return o
 
 

@@ -45,6 +45,9 @@ def main():
     copy_engine = cfg.get("copy_engine", False)
     mask = cfg.get("mask")               # partial / PEFT training: paro_plan_masked (NEXT-4)
     slots = cfg.get("grad_slots", 0)     # > 0: streamed gradients (paro_step_streamed)
+    wire = cfg.get("wire", "bf16")       # wire_dtype (reading A3)
+    predivide = cfg.get("predivide", True)
+    adam_smem_kb = cfg.get("adam_smem_kb", 0)
     for M in splits:
         uid = paro.unique_id() if rank == 0 else bytes(128)
         t = torch.tensor(list(uid), dtype=torch.uint8)
@@ -55,7 +58,8 @@ def main():
                 kw = dict(bucket_elems=B, topology=topo, transport=tr, comm_impl=comm_impl,
                           inter_gbps=inter_gbps, grad_accum=accum > 0, clip_norm=clip,
                           gather_windows=windows, adam_impl=adam_impl, fuse_gather=fuse_gather,
-                          copy_engine=copy_engine, grad_slots=slots)
+                          copy_engine=copy_engine, grad_slots=slots, wire_dtype=wire, predivide=predivide,
+                          adam_smem_kb=adam_smem_kb)
                 fz = None
                 if mask:
                     pl, fz = paro.Plan.masked(ctx, code, sizes, mask, **kw)

@@ -231,3 +231,41 @@ def test_fused_inter_allreduce_keeps_table3_bytes(N, M):
         else:
             assert (res["pull", True][2] < res["pull", False][2]) == fused
             assert res["push", True][2] == res["push", False][2]
+
+
+@pytest.mark.parametrize("N,M", [(8, 4), (4, 2), (8, 1), (6, 3)])
+def test_fp32_wire_bytes_and_memory(N, M):
+    """wire_dtype = 1 (reading A3): reduction partials travel as fp32, the
+    parameter restore stays bf16.  Push transport and the NCCL comparator send
+    every reduction element at 4 B: per-rank bytes = 4 x (reduction units) + 2 x
+    (restore units), the per-strategy closed form at fp32 width.  Pull plans
+    read the raw bf16 gradients at a ring's first hop (the reader pre-scales),
+    so they send between the bf16 and the all-fp32 figure.  The G residency is
+    4 B per element; grad_accum and copy_engine = 2 are refused."""
+    ctx = paro.Context(N, M)
+    sizes = [1 << 20, 4000037]
+    for code in ("NNN", "NNI", "NIG", "INI", "IIG", "IGG", "GGG", "III"):
+        for topo, tr in (("ho", "push"), ("two_step", "push"), ("nccl", "pull"), ("ho", "pull"), ("direct", "pull")):
+            kw = dict(bucket_elems=1 << 17, topology=topo, transport=tr)
+            b16 = paro.Plan(ctx, code, sizes, **kw).info()
+            f32 = paro.Plan(ctx, code, sizes, wire_dtype="fp32", **kw).info()
+            grad, rest = A.step_ops(code)
+            units = lambda prims: [sum(x) for x in zip(*[A.primitive_units(pr, N, M, b16["psi_pad"])
+                                                         for pr in prims])] or [0, 0]
+            red, res = units(grad), units(rest)
+            full = (4 * red[0] + 2 * res[0], 4 * red[1] + 2 * res[1])
+            got = (f32["step_send_bytes_intra"], f32["step_send_bytes_inter"])
+            assert (b16["step_send_bytes_intra"], b16["step_send_bytes_inter"]) == (2 * red[0] + 2 * res[0],
+                                                                                  2 * red[1] + 2 * res[1])
+            if tr == "push" or topo == "nccl":
+                assert got == full, (code, topo, tr)
+            else:
+                assert all(b16[k] <= f32[k] for k in ("step_send_bytes_intra", "step_send_bytes_inter"))
+                assert got[0] <= full[0] and got[1] <= full[1], (code, topo, tr)
+            assert f32["mem_p_bytes"] == b16["mem_p_bytes"] and f32["mem_os_bytes"] == b16["mem_os_bytes"]
+            if code[1] == "G" or (code[1] == "I" and M > 1):   # (M = 1: I is N, the raw bf16 buffer)
+                assert f32["mem_g_bytes"] == 2 * b16["mem_g_bytes"]
+    for bad in (dict(grad_accum=True), dict(copy_engine="all")):
+        with pytest.raises(paro.ParoError, match="fp32"):
+            paro.Plan(ctx, "IIG", sizes, wire_dtype="fp32", **bad)
+    ctx.close()

@@ -34,7 +34,7 @@ class EmuRun:
     def __init__(self, N, M, code, sizes, B, topo="ho", depth=2, wd=0.0, loss_scale=1.0, transport="push",
                  adam_impl="auto", comm_impl="tma_store", grad_accum=False, mode="emulated", clip_norm=0.0,
                  skip_nonfinite=False, fuse_gather="auto", copy_engine=False, fuse_allreduce=True,
-                 adam_smem_kb=0):
+                 adam_smem_kb=0, wire="bf16", predivide=True):
         paro = _paro()
         if mode == "emulated":
             self.ctx = paro.Context(N, M, mode="emulated", device=0)
@@ -44,7 +44,8 @@ class EmuRun:
                             weight_decay=wd, loss_scale=loss_scale, transport=transport, adam_impl=adam_impl,
                             comm_impl=comm_impl, grad_accum=grad_accum, clip_norm=clip_norm,
                             skip_nonfinite=skip_nonfinite, fuse_gather=fuse_gather, copy_engine=copy_engine,
-                            fuse_allreduce=fuse_allreduce, adam_smem_kb=adam_smem_kb)
+                            fuse_allreduce=fuse_allreduce, adam_smem_kb=adam_smem_kb, wire_dtype=wire,
+                            predivide=predivide)
         self.info = self.pl.info()
         self.N, self.code, self.sizes = N, code, sizes
         n = self.info["os_numel"]
@@ -97,14 +98,15 @@ def _assert_same(got, ref, what):
     assert bad.size == 0, f"{what}: {bad.size} mismatches, first at {bad[0]}: {gf[ok][bad[0]]} vs {rf[ok][bad[0]]}"
 
 
-def _dp_reference(lay, steps, kind="synth", wd=0.0, loss_scale=1.0):
+def _dp_reference(lay, steps, kind="synth", wd=0.0, loss_scale=1.0, wire="bf16", predivide=True):
     w0 = master_f32(0, lay.psi)
     w = ST.pad_flat(w0, lay.psi_pad, np.float32)
     m, v = np.zeros_like(w), np.zeros_like(w)
     norms = []
     for t in range(1, steps + 1):
-        sc = nm.AdamScalars(LR, t, weight_decay=wd, loss_scale=loss_scale)
-        w, m, v, p, gh = ST.dp_step(lay, _oracle_grads(lay.N, lay.psi, t, kind), w, m, v, sc)
+        sc = nm.AdamScalars(LR, t, weight_decay=wd, loss_scale=loss_scale, post_div=1 if predivide else lay.N)
+        w, m, v, p, gh = ST.dp_step(lay, _oracle_grads(lay.N, lay.psi, t, kind), w, m, v, sc, wire=wire,
+                                    predivide=predivide)
         norms.append(nm.grad_sq_sum(gh, sc.s_g))
     return w, m, v, p, norms
 
@@ -896,3 +898,109 @@ def test_collective_allreduce_matches_oracle(N, M, topo):
         fused.collective(0)
     fused.close()
     ctx.close()
+
+
+# --------------------------------------------------------------------- fp32 wire / predivide
+@pytest.mark.parametrize("topo,transport", [("ho", "pull"), ("ho", "push"), ("two_step", "pull"), ("direct", "pull"),
+                                            ("direct", "push")])
+def test_fp32_wire_every_strategy_2x4(topo, transport):
+    """wire_dtype = 1: fp32 partials and fp32 g_hat through every strategy's
+    schedule (fused final hop, fused inter all-reduce, AG of fp32 g_hat) equal
+    the oracle's fp32-wire DP definition bit for bit (same split), 3 steps, with
+    the default Adam, the LSU Adam and the co-run thread-store Adam."""
+    N, M = 8, 4
+    sizes = [N * 64 * 40 + 24, 1000]
+    B = N * 64 * 8
+    lay = L.Layout(sizes, N, M, B)
+    ref = _dp_reference(lay, 3, wire="fp32")
+    for i, code in enumerate(S.paro_strategies()):
+        impl, kb = (("auto", 0), ("lsu", 0), ("tma", 120))[i % 3]
+        run = EmuRun(N, M, code, sizes, B, topo=topo, transport=transport, wire="fp32", adam_impl=impl,
+                     adam_smem_kb=kb)
+        for t in (1, 2, 3):
+            run.set_grads(t)
+            st = run.step(t)
+        assert abs(st["grad_norm"] ** 2 - ref[4][-1]) <= 1e-12 * ref[4][-1]
+        _check_against_dp(run, lay, ref)
+        run.close()
+
+
+def _a24(a, b):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    return float(np.max(np.abs(a - b) / np.maximum(np.abs(b), 1e-3)))
+
+
+def test_fp32_wire_cross_split_within_1e5():
+    """SURVEY 8(c-4) cross-split / cross-bucket pin: on the fp32 wire, 10 steps
+    at 8 ranks as 2x4, 4x2, 8x1, 1x8 and two bucket sizes each equal their own
+    split's oracle bit for bit and agree with the 2x4 reference within 1e-5
+    (A24 metric); fp32 masters and bf16 parameters both compared."""
+    N = 8
+    sizes = [1 << 16]
+    lay_ref = L.Layout(sizes, N, 4, 1 << 13)
+    w_ref = _dp_reference(lay_ref, 10, wire="fp32")[0][:sizes[0]]
+    worst = 0.0
+    for (M, B, code) in [(4, 1 << 13, "IIG"), (2, 1 << 13, "NIG"), (1, 1 << 13, "GGG"), (8, 1 << 13, "III"),
+                         (4, 1 << 11, "NNN"), (2, 3 * 1024, "IGG")]:
+        lay = L.Layout(sizes, N, M, B)
+        ref = _dp_reference(lay, 10, wire="fp32")
+        run = EmuRun(N, M, code, sizes, B, wire="fp32", transport="pull")
+        for t in range(1, 11):
+            run.set_grads(t)
+            run.step(t)
+        _check_against_dp(run, lay, ref)
+        full = np.zeros(lay.psi_pad, np.float32)
+        for r in range(N):
+            off = 0
+            st = run.state(r)
+            for (a, e) in lay.shard_ranges(code[2], r):
+                full[a:e] = st["master"][off:off + e - a]
+                off += e - a
+        worst = max(worst, _a24(full[:sizes[0]], w_ref))
+        run.close()
+    assert worst <= 1e-5, worst
+
+
+@pytest.mark.parametrize("wire", ["bf16", "fp32"])
+@pytest.mark.parametrize("N,M", [(8, 4), (6, 3), (4, 1)])
+def test_predivide_off_every_strategy(wire, N, M):
+    """predivide = 0: the raw gradients are summed and Adam takes the 1/N average
+    (s_g = 1/(loss_scale * N)), bit for bit the oracle with post_div = N."""
+    sizes = ragged_param_sizes() + [N * 64 * 7 + 3]
+    B = N * 64 * 3
+    lay = L.Layout(sizes, N, M, B)
+    ref = _dp_reference(lay, 2, wire=wire, predivide=False, loss_scale=2.0)
+    for code in S.paro_strategies():
+        run = EmuRun(N, M, code, sizes, B, transport="pull", wire=wire, predivide=False, loss_scale=2.0)
+        for t in (1, 2):
+            run.set_grads(t)
+            st = run.step(t)
+        assert abs(st["grad_norm"] ** 2 - ref[4][-1]) <= 1e-12 * ref[4][-1]
+        _check_against_dp(run, lay, ref)
+        run.close()
+
+
+@pytest.mark.parametrize("code,kw", [("IIG", {}), ("NNN", {"clip_norm": 0.05}), ("GGG", {"fuse_gather": "always"}),
+                                     ("IGG", {"copy_engine": "gathers"})])
+def test_fp32_wire_with_options(code, kw):
+    """fp32 wire with the two-phase clipped step, fused parameter gathers and
+    copy-engine all-gathers (4x2, 2 steps)."""
+    N, M = 4, 2
+    sizes = [N * 64 * 40 + 24, 1000]
+    B = N * 64 * 8
+    lay = L.Layout(sizes, N, M, B)
+    if "clip_norm" in kw:
+        w = ST.pad_flat(master_f32(0, lay.psi), lay.psi_pad, np.float32)
+        m, v = np.zeros_like(w), np.zeros_like(w)
+        for t in (1, 2):
+            gh = ST.dp_reduce(lay, _oracle_grads(N, lay.psi, t), wire="fp32")
+            w, m, v, p = ST.clip_update(gh, w, m, v, LR, t, kw["clip_norm"], False, 1, {})[:4]
+        ref = (w, m, v, p, None)
+    else:
+        ref = _dp_reference(lay, 2, wire="fp32")
+    run = EmuRun(N, M, code, sizes, B, transport="pull", wire="fp32", **kw)
+    for t in (1, 2):
+        run.set_grads(t)
+        run.step(t)
+    _check_against_dp(run, lay, ref)
+    run.close()
