@@ -194,6 +194,17 @@ typedef struct {
                           * first read (R4); 0: the raw sum is reduced and the 1/N *
                           * average is applied in Adam's unscale, s_g = 1 /        *
                           * (loss_scale * N) (reading A4; same bits for N = 2^k).  */
+  const int64_t* bucket_groups; /* layer-aligned buckets (NEXT-2): n     *
+                          * ascending tensor indices, the first 0; bucket k holds *
+                          * exactly tensors [bucket_groups[k], bucket_groups[k+1]) *
+                          * (dense, zero-padded at its end to a multiple of N*64), *
+                          * so paro_gather_window(b) returns one layer group and a *
+                          * caller can prefetch group b+1 while computing group b. *
+                          * bucket_elems is then ignored; the flat layout has     *
+                          * padding inside (paro_bucket_range, and per-tensor     *
+                          * offsets follow the groups).  Read during paro_plan    *
+                          * only.  NULL / 0 (default): dense layout, fixed buckets. */
+  int n_bucket_groups;
 } paro_opts_t;
 
 typedef struct {
@@ -318,6 +329,11 @@ paro_status_t paro_gather_window(paro_plan_t plan, int rank, int64_t bucket, int
 /* Bytes `rank` sends to gather every bucket once through paro_gather_window. */
 paro_status_t paro_rank_gather_send_bytes(paro_plan_t plan, int rank, int64_t* intra, int64_t* inter);
 
+/* Bytes `rank` sends in one paro_gather_window of bucket `bucket` (with
+ * bucket_groups: one layer group's forward or backward A-G(P), Table 3). */
+paro_status_t paro_bucket_gather_send_bytes(paro_plan_t plan, int rank, int64_t bucket, int64_t* intra,
+                                            int64_t* inter);
+
 /* Library-owned device buffers of `rank` (must be a local rank):
  *   kind 0: flat gradient buffer, bf16, psi_pad elements (zero-padded tail).
  *           Writing gradients here and passing grads = NULL to paro_step is
@@ -335,7 +351,9 @@ paro_status_t paro_rank_gather_send_bytes(paro_plan_t plan, int rank, int64_t* i
 paro_status_t paro_buffer(paro_plan_t plan, int rank, int kind, void** ptr);
 
 /* Initialise one local rank's optimizer state and parameter buffer from a full
- * fp32 master vector `master_full` (device, psi elements; padding = 0):
+ * fp32 master vector `master_full` (device, psi_pad elements in the plan's flat
+ * layout: param i at its flat offset, padding ignored; for the dense layout
+ * the first psi elements suffice):
  * master = its OS residency slice, m = v = 0, param buffer = RNE_bf16 of the P
  * residency slice.  Stream-ordered on the plan stream. */
 paro_status_t paro_opt_state_init(paro_plan_t plan, int rank, const float* master_full,
@@ -372,7 +390,7 @@ paro_status_t paro_step(paro_plan_t plan, const void* const* grads, void* const*
  *   producer(user, rank, b, begin, end, dst, stream)
  * from this host thread; it must enqueue, on `stream` (a cudaStream_t), writes
  * of the bf16 gradients of flat elements [begin, end) (paro_bucket_range;
- * zero past psi) into the device buffer dst (end - begin elements), and
+ * zero on padding) into the device buffer dst (end - begin elements), and
  * return.  producer NULL: the library's synthetic gradients of `seed` and
  * `grad_step` (the paro_synth_grads values).  params, opt_state, lr, step:
  * as paro_step.  Errors: PARO_ERR_STATE if the plan has no grad_slots. */

@@ -16,10 +16,20 @@ groups through an inter-group all-gather").
 
 Reading R21 (padding): each bucket is a multiple of N*64 elements; Psi is
 zero-padded to Psi_pad = ceil(Psi / (N*64)) * N*64.
+
+Layer-aligned buckets (NEXT-2, "obtains a complete replica of model
+parameters through the intra-group all-gather" layer by layer in the forward /
+backward pass): with `groups` (tensor indices at which a bucket starts; the
+first is 0) bucket k holds exactly tensors [groups[k], groups[k+1]), laid out
+densely and zero-padded at its end to a multiple of N*64, so one bucket's
+gather is one layer group's parameters.  Psi_pad is then the sum of the padded
+group sizes and the padding lies at the end of every bucket.
 """
 from __future__ import annotations
 
 from dataclasses import dataclass, field
+
+import numpy as np
 
 from .strategy import divisor, validate_cluster
 
@@ -36,6 +46,7 @@ class Layout:
     N: int
     M: int
     bucket_elems: int
+    groups: list = None                      # tensor indices starting a bucket (layer-aligned buckets)
     g: int = field(init=False)
     psi: int = field(init=False)
     psi_pad: int = field(init=False)
@@ -49,6 +60,9 @@ class Layout:
             raise ValueError("param sizes must be >= 0")
         unit = self.N * QUANTUM
         self.psi = int(sum(int(s) for s in self.param_sizes))
+        if self.groups is not None:
+            self._grouped(unit)
+            return
         self.psi_pad = _ceil_div(self.psi, unit) * unit
         self.B = max(unit, (int(self.bucket_elems) // unit) * unit)
         offs, o = [], 0
@@ -57,11 +71,46 @@ class Layout:
             o += int(s)
         self.param_offsets = offs
         self.buckets = []
+        self.real = []
         start = 0
         while start < self.psi_pad:
             size = min(self.B, self.psi_pad - start)
             self.buckets.append((start, size))
+            self.real.append((start, min(start + size, self.psi)))
             start += size
+
+    def _grouped(self, unit):
+        n = len(self.param_sizes)
+        gs = [int(x) for x in self.groups]
+        if not gs or gs[0] != 0 or any(b <= a for a, b in zip(gs, gs[1:])) or gs[-1] >= max(n, 1):
+            raise ValueError("bucket groups must start at tensor 0 and increase strictly below n_params")
+        bounds = gs + [n]
+        offs, o = [], 0
+        self.buckets, self.real = [], []
+        for k in range(len(gs)):
+            start = o
+            for t in range(bounds[k], bounds[k + 1]):
+                offs.append(o)
+                o += int(self.param_sizes[t])
+            size = _ceil_div(o - start, unit) * unit
+            if size:
+                self.buckets.append((start, size))
+                self.real.append((start, o))
+            o = start + size
+        self.param_offsets = offs
+        self.psi_pad = o
+        self.B = max([unit] + [n for _, n in self.buckets])
+
+    def expand(self, x, fill=0):
+        """Place a per-tensor concatenation (length Psi, declaration order) into
+        the flat layout (length Psi_pad), `fill` on the padding."""
+        x = np.asarray(x)
+        out = np.full(self.psi_pad, fill, dtype=x.dtype)
+        o = 0
+        for off, sz in zip(self.param_offsets, self.param_sizes):
+            out[off:off + int(sz)] = x[o:o + int(sz)]
+            o += int(sz)
+        return out
 
     # -- rank geometry -------------------------------------------------------
     def rank_jp(self, r):

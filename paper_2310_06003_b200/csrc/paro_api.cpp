@@ -674,6 +674,8 @@ void paro_opts_default(paro_opts_t* o) {
   o->adam_smem_kb = 0;
   o->wire_dtype = 0;
   o->predivide = 1;
+  o->bucket_groups = nullptr;
+  o->n_bucket_groups = 0;
 }
 
 paro_status_t paro_get_unique_id(paro_uid_t* out) {
@@ -813,6 +815,11 @@ paro_status_t paro_plan(paro_ctx_t ctx, const char* strategy, const int64_t* par
   if (o.wire_dtype != 0 && o.wire_dtype != 1) return fail(PARO_ERR_INVALID, "wire_dtype must be 0 (bf16) or 1 (fp32)");
   po.wire = o.wire_dtype == 1 ? 4 : 2;
   po.predivide = o.predivide != 0;
+  if (o.n_bucket_groups < 0 || (o.n_bucket_groups > 0 && !o.bucket_groups))
+    return fail(PARO_ERR_INVALID, "bucket_groups: null pointer or negative count");
+  for (int k = 0; k < o.n_bucket_groups; ++k) po.groups.push_back(o.bucket_groups[k]);
+  o.bucket_groups = nullptr;   // not kept: the planner holds its copy
+  o.n_bucket_groups = 0;
   auto* p = new PlanT();
   p->ctx = ctx;
   p->opts = o;
@@ -930,9 +937,30 @@ paro_status_t paro_plan_masked(paro_ctx_t ctx, const char* strategy, const int64
   if (opts) o = *opts;
   else paro_opts_default(&o);
   o.frozen = 0;
+  // layer-aligned buckets: a group boundary at tensor t becomes, in each
+  // sub-list, the number of that list's tensors before t (empty groups merge)
+  std::vector<int64_t> gt, gf;
+  if (o.n_bucket_groups > 0 && o.bucket_groups) {
+    for (int k = 0; k < o.n_bucket_groups; ++k) {
+      const int64_t t = o.bucket_groups[k];
+      if (t < 0 || t > n_params) return fail(PARO_ERR_INVALID, "bucket_groups: tensor index out of range");
+      int64_t a = 0, b = 0;
+      for (int64_t i = 0; i < t; ++i) (trainable[i] ? a : b) += 1;
+      if (a < (int64_t)tr.size() && (gt.empty() || gt.back() < a)) gt.push_back(a);
+      if (b < (int64_t)fr.size() && (gf.empty() || gf.back() < b)) gf.push_back(b);
+    }
+    if (gt.empty() || gt[0] != 0) gt.insert(gt.begin(), 0);
+    if (!fr.empty() && (gf.empty() || gf[0] != 0)) gf.insert(gf.begin(), 0);
+    o.bucket_groups = gt.data();
+    o.n_bucket_groups = (int)gt.size();
+  }
   paro_status_t st = paro_plan(ctx, strategy, tr.data(), (int)tr.size(), &o, out_trainable);
   if (st != PARO_OK || fr.empty()) return st;
   o.frozen = 1;
+  if (o.n_bucket_groups > 0) {
+    o.bucket_groups = gf.data();
+    o.n_bucket_groups = (int)gf.size();
+  }
   st = paro_plan(ctx, strategy, fr.data(), (int)fr.size(), &o, out_frozen);
   if (st != PARO_OK) {
     const std::string msg = g_last_error;
@@ -1024,6 +1052,15 @@ paro_status_t paro_rank_gather_send_bytes(paro_plan_t p, int rank, int64_t* intr
   return PARO_OK;
 }
 
+paro_status_t paro_bucket_gather_send_bytes(paro_plan_t p, int rank, int64_t bucket, int64_t* intra, int64_t* inter) {
+  if (!p || !intra || !inter) return fail(PARO_ERR_INVALID, "null argument");
+  if (rank < 0 || rank >= p->pl->N) return fail(PARO_ERR_INVALID, "rank out of range");
+  if (bucket < 0 || bucket >= (int64_t)p->pl->buckets.size()) return fail(PARO_ERR_INVALID, "bucket out of range");
+  *intra = p->pl->win_bucket_intra[bucket][rank];
+  *inter = p->pl->win_bucket_inter[bucket][rank];
+  return PARO_OK;
+}
+
 paro_status_t paro_buffer(paro_plan_t p, int rank, int kind, void** ptr) {
   if (!p || !ptr) return fail(PARO_ERR_INVALID, "null argument");
   paro_ctx* ctx = p->ctx;
@@ -1058,9 +1095,10 @@ static paro_status_t opt_init_impl(paro_plan_t p, int rank, const float* src, ui
     const int64_t os_off = pl.buckets[b].first / pl.divl(pl.OS);
     const int64_t p_off = pl.buckets[b].first / pl.divl(pl.P);
     if (!pl.opt.params_only)
-      CK(launch_init_range(src, key, ob, oe - ob, pl.psi, st->master + os_off, st->m + os_off, st->v + os_off,
+      CK(launch_init_range(src, key, ob, oe - ob, pl.bucket_real_end[b], st->master + os_off, st->m + os_off, st->v + os_off,
                            nullptr, ctx->main));
-    CK(launch_init_range(src, key, pb, pe - pb, pl.psi, nullptr, nullptr, nullptr, pbuf + p_off, ctx->main));
+    CK(launch_init_range(src, key, pb, pe - pb, pl.bucket_real_end[b], nullptr, nullptr, nullptr, pbuf + p_off,
+                         ctx->main));
   }
   CK(cudaStreamSynchronize(ctx->main));
   return PARO_OK;
@@ -1088,8 +1126,15 @@ paro_status_t paro_synth_grads(paro_plan_t p, int rank, uint64_t seed, int64_t s
     return fail(PARO_ERR_STATE, "plan has grad_slots: gradients are produced per bucket by paro_step_streamed");
   if (!is_local(p, rank)) return fail(PARO_ERR_INVALID, "rank is not local to this process");
   uint16_t* g = reinterpret_cast<uint16_t*>(data_ptr(p, rank, BUF_GRAD, 0));
-  CK(launch_synth_grad(g, p->pl->psi, p->pl->psi_pad, synth_key(seed, kTagGrad, (uint64_t)rank, (uint64_t)step),
-                       ctx->main));
+  const Planner& pl = *p->pl;
+  const uint64_t key = synth_key(seed, kTagGrad, (uint64_t)rank, (uint64_t)step);
+  if (pl.opt.groups.empty()) {   // dense layout: one launch, zero past psi
+    CK(launch_synth_grad(g, pl.psi, pl.psi_pad, key, ctx->main));
+  } else {                       // layer-aligned buckets: zero on every bucket's padded tail
+    for (size_t b = 0; b < pl.buckets.size(); ++b)
+      CK(launch_synth_grad_range(g + pl.buckets[b].first, pl.buckets[b].first, pl.buckets[b].second,
+                                 pl.bucket_real_end[b], key, ctx->main));
+  }
   CK(cudaStreamSynchronize(ctx->main));
   return PARO_OK;
 }
@@ -1405,7 +1450,7 @@ paro_status_t step_impl(PlanT* p, const void* const* grads, void* const* params,
         if (src->fn) {
           src->fn(src->user, r, b, b0, b0 + n, dst, ps);
         } else {
-          CK(launch_synth_grad_range(static_cast<uint16_t*>(dst), b0, n, pl.psi,
+          CK(launch_synth_grad_range(static_cast<uint16_t*>(dst), b0, n, pl.bucket_real_end[b],
                                      synth_key(src->seed, kTagGrad, (uint64_t)r, (uint64_t)src->gstep), ps));
           ++launches;
         }

@@ -329,14 +329,47 @@ void Planner::layout() {
   const int64_t unit = int64_t(N) * kQuantum;
   psi = 0;
   param_offsets.clear();
-  for (int64_t s : param_sizes) {
-    param_offsets.push_back(psi);
-    psi += s;
-  }
-  psi_pad = ceil_div(psi, unit) * unit;
-  B = std::max(unit, (opt.bucket_elems / unit) * unit);
   buckets.clear();
-  for (int64_t s = 0; s < psi_pad; s += B) buckets.push_back({s, std::min(B, psi_pad - s)});
+  bucket_real_end.clear();
+  if (!opt.groups.empty()) {
+    // layer-aligned buckets (NEXT-2): bucket k = tensors [groups[k], groups[k+1]),
+    // dense, zero-padded at its end to a multiple of N*64 (R21 per bucket)
+    const int n = (int)param_sizes.size();
+    const std::vector<int64_t>& gs = opt.groups;
+    bool ok = gs[0] == 0 && gs.back() < std::max(n, 1);
+    for (size_t k = 1; k < gs.size(); ++k) ok = ok && gs[k] > gs[k - 1];
+    if (!ok) throw std::invalid_argument("bucket groups must start at tensor 0 and increase strictly below n_params");
+    int64_t o = 0;
+    for (size_t k = 0; k < gs.size(); ++k) {
+      const int64_t start = o;
+      const int64_t t1 = (k + 1 < gs.size()) ? gs[k + 1] : n;
+      for (int64_t t = gs[k]; t < t1; ++t) {
+        param_offsets.push_back(o);
+        o += param_sizes[t];
+        psi += param_sizes[t];
+      }
+      const int64_t size = ceil_div(o - start, unit) * unit;
+      if (size > 0) {
+        buckets.push_back({start, size});
+        bucket_real_end.push_back(o);
+      }
+      o = start + size;
+    }
+    psi_pad = o;
+    B = unit;
+    for (const auto& bk : buckets) B = std::max(B, bk.second);
+  } else {
+    for (int64_t s : param_sizes) {
+      param_offsets.push_back(psi);
+      psi += s;
+    }
+    psi_pad = ceil_div(psi, unit) * unit;
+    B = std::max(unit, (opt.bucket_elems / unit) * unit);
+    for (int64_t s = 0; s < psi_pad; s += B) {
+      buckets.push_back({s, std::min(B, psi_pad - s)});
+      bucket_real_end.push_back(std::min(psi, s + std::min(B, psi_pad - s)));
+    }
+  }
   p_numel = psi_pad / divl(P);
   g_numel = (G == LV_N) ? 0 : psi_pad / divl(G);
   os_numel = psi_pad / divl(OS);
@@ -1124,6 +1157,8 @@ void Planner::count_bytes() {
   accstep_send_inter.assign(N, 0);
   win_send_intra.assign(N, 0);
   win_send_inter.assign(N, 0);
+  win_bucket_intra.assign(sched.size(), std::vector<int64_t>(N, 0));
+  win_bucket_inter.assign(sched.size(), std::vector<int64_t>(N, 0));
   n_rounds = 0;
   n_comm_launches = 0;
   for (const BucketSchedule& S : sched) {
@@ -1133,7 +1168,14 @@ void Planner::count_bytes() {
       n_rounds += (int)L->rounds.size();
     }
     count({&S.reduce_pre, &S.reduce, &S.gather}, &S.ghat_in, S.os_len, send_intra, send_inter, &S.param_push);
-    count({&S.window}, nullptr, 0, win_send_intra, win_send_inter);
+    {
+      const size_t b = &S - sched.data();
+      count({&S.window}, nullptr, 0, win_bucket_intra[b], win_bucket_inter[b]);
+      for (int r = 0; r < N; ++r) {
+        win_send_intra[r] += win_bucket_intra[b][r];
+        win_send_inter[r] += win_bucket_inter[b][r];
+      }
+    }
     if (opt.accum) {
       count({&S.accum_pre, &S.accum}, nullptr, 0, acc_send_intra, acc_send_inter);
       count({&S.reduce_acc, &S.gather}, &S.ghat_in_acc, S.os_len, accstep_send_intra, accstep_send_inter,

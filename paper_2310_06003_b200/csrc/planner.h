@@ -131,6 +131,8 @@ struct PlanOptions {
   int wire = 2;              // bytes per reduction element on the wire and in the G / g_hat /
                              // staging buffers: 2 = bf16, 4 = fp32 (reading A3)
   bool predivide = true;     // raw gradients scaled by 1/N when first read (R4); else in Adam
+  std::vector<int64_t> groups;   // layer-aligned buckets: tensor indices starting a bucket
+                                 // (first 0); each bucket padded at its end to N*64 (NEXT-2)
 };
 
 class Planner {
@@ -146,6 +148,7 @@ class Planner {
   int64_t psi = 0, psi_pad = 0, B = 0;
   bool fused_allreduce = false;   // the inter all-reduce runs inside Adam (R31)
   std::vector<std::pair<int64_t, int64_t>> buckets;   // (start, size)
+  std::vector<int64_t> bucket_real_end;               // end of the real (non-padding) elements per bucket
   std::vector<int64_t> param_sizes, param_offsets;
   int64_t p_numel = 0, g_numel = 0, os_numel = 0;
   int nslots = 0;                                      // BUF_GHAT slots
@@ -162,6 +165,7 @@ class Planner {
   std::vector<int64_t> acc_send_intra, acc_send_inter;        // per accumulated micro-batch
   std::vector<int64_t> accstep_send_intra, accstep_send_inter;  // per step after accumulation
   std::vector<int64_t> win_send_intra, win_send_inter;          // per gather of every bucket once
+  std::vector<std::vector<int64_t>> win_bucket_intra, win_bucket_inter;   // [bucket][rank]: one window gather
   int acc_kind = -1;                                  // accumulator buffer (GSHARD / GACC)
   int n_rounds = 0, n_comm_launches = 0;
 

@@ -49,7 +49,7 @@ class paro_opts_t(C.Structure):
                 ("fuse_gather", C.c_int), ("copy_engine", C.c_int), ("gather_windows", C.c_int), ("grad_accum", C.c_int),
                 ("stream", C.c_void_p), ("frozen", C.c_int), ("grad_slots", C.c_int),
                 ("fuse_allreduce", C.c_int), ("adam_smem_kb", C.c_int), ("wire_dtype", C.c_int),
-                ("predivide", C.c_int)]
+                ("predivide", C.c_int), ("bucket_groups", C.POINTER(C.c_int64)), ("n_bucket_groups", C.c_int)]
 
 
 class paro_plan_info_t(C.Structure):
@@ -123,6 +123,8 @@ paro_rank_accum_send_bytes = _sig("paro_rank_accum_send_bytes", _st, _vp, C.c_in
 paro_gather_window = _sig("paro_gather_window", _st, _vp, C.c_int, _i64, C.c_int, _vp, C.POINTER(_vp))
 paro_rank_gather_send_bytes = _sig("paro_rank_gather_send_bytes", _st, _vp, C.c_int, C.POINTER(_i64),
                                    C.POINTER(_i64))
+paro_bucket_gather_send_bytes = _sig("paro_bucket_gather_send_bytes", _st, _vp, C.c_int, _i64, C.POINTER(_i64),
+                                     C.POINTER(_i64))
 paro_buffer = _sig("paro_buffer", _st, _vp, C.c_int, C.c_int, C.POINTER(_vp))
 paro_opt_state_init = _sig("paro_opt_state_init", _st, _vp, C.c_int, _vp, C.POINTER(paro_opt_state_t))
 paro_opt_state_init_synth = _sig("paro_opt_state_init_synth", _st, _vp, C.c_int, C.c_uint64,
@@ -152,7 +154,8 @@ EXPORTED = ["paro_opts_default", "paro_get_unique_id", "paro_init", "paro_init_e
             "paro_plan_destroy", "paro_last_error", "paro_version", "paro_profile_start",
             "paro_profile_stop", "paro_collective", "paro_accumulate",
             "paro_rank_accum_send_bytes", "paro_gather_window", "paro_rank_gather_send_bytes",
-            "paro_table1_column", "paro_advise", "paro_plan_masked", "paro_step_streamed"]
+            "paro_table1_column", "paro_advise", "paro_plan_masked", "paro_step_streamed",
+            "paro_bucket_gather_send_bytes"]
 
 
 def check(status):
@@ -166,7 +169,7 @@ def make_opts(bucket_elems=1 << 26, topology="ho", beta1=0.9, beta2=0.95, eps=1e
               loss_scale=1.0, comm_ctas=148, pipeline_depth=2, stream=None, transport="pull", adam_impl="auto",
               comm_impl="tma_store", inter_gbps=0.0, grad_accum=False, clip_norm=0.0, skip_nonfinite=False, gather_windows=0,
               fuse_gather="auto", copy_engine=False, frozen=False, grad_slots=0, fuse_allreduce=True,
-              adam_smem_kb=0, wire_dtype="bf16", predivide=True):
+              adam_smem_kb=0, wire_dtype="bf16", predivide=True, bucket_groups=None):
     o = paro_opts_t()
     paro_opts_default(C.byref(o))
     o.bucket_elems = int(bucket_elems)
@@ -191,6 +194,11 @@ def make_opts(bucket_elems=1 << 26, topology="ho", beta1=0.9, beta2=0.95, eps=1e
     o.adam_smem_kb = int(adam_smem_kb)
     o.wire_dtype = {"bf16": 0, "fp32": 1, 0: 0, 1: 1}[wire_dtype]
     o.predivide = 1 if predivide else 0
+    if bucket_groups is not None:
+        arr = (_i64 * max(1, len(bucket_groups)))(*[int(x) for x in bucket_groups])
+        o._groups_keep = arr            # the library reads it during paro_plan only
+        o.bucket_groups = C.cast(arr, C.POINTER(C.c_int64))
+        o.n_bucket_groups = len(bucket_groups)
     return o
 
 
@@ -306,9 +314,13 @@ class Plan:
         check(paro_gather_window(self.h, rank, int(bucket), int(slot), stream, C.byref(out)))
         return out.value
 
-    def gather_send_bytes(self, rank):
+    def gather_send_bytes(self, rank, bucket=None):
+        """(intra, inter) bytes `rank` sends gathering every bucket once, or one bucket."""
         a, b = _i64(), _i64()
-        check(paro_rank_gather_send_bytes(self.h, rank, C.byref(a), C.byref(b)))
+        if bucket is None:
+            check(paro_rank_gather_send_bytes(self.h, rank, C.byref(a), C.byref(b)))
+        else:
+            check(paro_bucket_gather_send_bytes(self.h, rank, int(bucket), C.byref(a), C.byref(b)))
         return a.value, b.value
 
     def buffer(self, rank, kind):

@@ -2,8 +2,9 @@
 
 This module holds NO arithmetic of the PaRO method: it only assembles bit
 patterns from a counter-based hash.  The CUDA side implements the identical
-generator (paper_2310_06003_b200/csrc/synth.cu); a GPU test checks the two
-produce the same bits.
+generator (synth_grad_kernel / init_range_kernel in
+paper_2310_06003_b200/csrc/kernels.cu); a GPU test checks the two produce the
+same bits.
 
 Generator (DESIGN.md §5 "Input recipe"):
 
@@ -122,3 +123,26 @@ def llama_param_sizes(name, vocab=32000):
 def ragged_param_sizes():
     """Small ragged list exercising padding and unaligned parameter starts."""
     return [3, 64, 100, 7, 512, 1, 4096 + 5]
+
+
+# ----------------------------------------------------------------- padded flat layouts
+def grad_flat(rank, step, psi_pad, real, seed=SEED):
+    """Gradient bits over a flat layout of psi_pad elements whose real (non-padding)
+    ranges are `real` [(begin, end), ...]: element i carries grad_bits at index i,
+    padding is zero.  For the dense layout real = [(0, psi)]; with layer-aligned
+    buckets every bucket has its own padded tail.  (The library's generator writes
+    the same bits: paro_synth_grads.)"""
+    out = np.zeros(psi_pad, np.uint16)
+    for a, e in real:
+        if e > a:
+            out[a:e] = grad_bits(rank, step, a, e - a, seed)
+    return out
+
+
+def master_flat(psi_pad, real, seed=SEED):
+    """Initial fp32 masters over a padded flat layout (zero on the padding)."""
+    out = np.zeros(psi_pad, np.float32)
+    for a, e in real:
+        if e > a:
+            out[a:e] = master_f32(a, e - a, seed)
+    return out

@@ -269,3 +269,56 @@ def test_fp32_wire_bytes_and_memory(N, M):
         with pytest.raises(paro.ParoError, match="fp32"):
             paro.Plan(ctx, "IIG", sizes, wire_dtype="fp32", **bad)
     ctx.close()
+
+
+LAYERS = lambda d, f, L: [d * 3 + 5] + [d * d, d * d + 7, f * d, d] * L + [d * 3 + 5]
+
+
+@pytest.mark.parametrize("N,M", [(8, 4), (4, 2), (8, 1), (6, 3), (1, 1)])
+def test_layer_aligned_buckets_layout_and_window_bytes(N, M):
+    """bucket_groups (NEXT-2): bucket k holds exactly one layer group
+    (dense, padded at its end to N*64), identically in the library and the oracle
+    layout; one bucket's forward / backward gather sends Table 3's per-layer
+    A-G(P): P = I (IIG, IGG) the MiCS-style intra AG, cluster total N(M-1)/M x
+    the layer; P = G on the flat ring (GGG = ZeRO-3) the flat AG
+    split (rank-order attribution, A14); P = G on HO-Ring the HO_AG closed form."""
+    sizes = LAYERS(64, 176, 3)
+    groups = [0, 1, 5, 9, 13]      # embedding, three layers of 4 tensors, head
+    lay = L.Layout(sizes, N, M, 0, groups=groups)
+    unit = N * 64
+    for k, (s0, n) in enumerate(lay.buckets):
+        assert n % unit == 0 and s0 % unit == 0
+        t1 = groups[k + 1] if k + 1 < len(groups) else len(sizes)
+        real = sum(sizes[groups[k]:t1])
+        assert lay.real[k] == (s0, s0 + real) and n == -(-real // unit) * unit
+        for t in range(groups[k], t1):
+            assert s0 <= lay.param_offsets[t] and lay.param_offsets[t] + sizes[t] <= s0 + real
+    x = np.arange(1, lay.psi + 1, dtype=np.int64)
+    e = lay.expand(x)
+    assert e.sum() == x.sum() and all(not e[a:b].any() for (_, b), (a, _) in zip(lay.real, lay.buckets[1:]))
+    ctx = paro.Context(N, M)
+    for code, topo in (("IIG", "ho"), ("IGG", "ho"), ("GGG", "flat"), ("GGG", "ho"), ("NNG", "ho")):
+        pl = paro.Plan(ctx, code, sizes, bucket_groups=groups, topology=topo, gather_windows=2)
+        info = pl.info()
+        assert info["psi"] == lay.psi and info["psi_pad"] == lay.psi_pad and info["n_buckets"] == len(lay.buckets)
+        for b, (s0, n) in enumerate(lay.buckets):
+            assert pl.bucket_range(b) == (s0, s0 + n)
+            for r in range(N):
+                for st in ("P", "G", "OS"):
+                    assert pl.shard_range(st, r, b) == lay.residency({"P": code[0], "G": code[1], "OS": code[2]}[st],
+                                                                     r, b)
+            per = [pl.gather_send_bytes(r, b) for r in range(N)]
+            tot = (sum(a for a, _ in per), sum(c for _, c in per))
+            if code[0] == "N" or N == 1:
+                assert tot == (0, 0)
+            elif code[0] == "I" and M > 1 and N // M > 1:
+                cell = A.table3("PaRO-IIG", N, M, 1, n)["fwd_ag_p"]
+                assert tot == (2 * cell[0], 2 * cell[1]), (code, b)
+            elif topo == "flat":
+                cell = A.table3("ZeRO-3", N, M, 1, n)["fwd_ag_p"]
+                assert tot == (2 * cell[0], 2 * cell[1]), (code, b)
+            elif code[0] == "G":
+                u = A.primitive_units("HO_AG", N, M, n)
+                assert all(x == (2 * u[0], 2 * u[1]) for x in per), (code, b)
+        pl.close()
+    ctx.close()

@@ -15,7 +15,7 @@ import torch
 from oracle import layout as L
 from oracle import numerics as nm
 from oracle import step as ST
-from paro_synth import grad_bits, master_f32
+from paro_synth import grad_bits, grad_flat, master_f32, master_flat
 
 pytestmark = pytest.mark.gpu
 
@@ -27,13 +27,13 @@ def _ngpu():
 
 
 def _dp(lay, steps, accum=0, g_level="N", clip=0.0, wire="bf16", predivide=True):
-    w = ST.pad_flat(master_f32(0, lay.psi), lay.psi_pad, np.float32)
+    w = master_flat(lay.psi_pad, lay.real)
     m, v = np.zeros_like(w), np.zeros_like(w)
     for t in range(1, steps + 1):
-        if wire != "bf16" or not predivide:
+        if wire != "bf16" or not predivide or lay.groups is not None:
             sc = nm.AdamScalars(3e-4, t, post_div=1 if predivide else lay.N)
-            w, m, v, p, gh = ST.dp_step(lay, [grad_bits(r, t, 0, lay.psi) for r in range(lay.N)], w, m, v, sc,
-                                        wire=wire, predivide=predivide)
+            w, m, v, p, gh = ST.dp_step(lay, [grad_flat(r, t, lay.psi_pad, lay.real) for r in range(lay.N)], w, m,
+                                        v, sc, wire=wire, predivide=predivide)
             sg = sc.s_g
             continue
         if clip:
@@ -58,7 +58,7 @@ CODES = ["NNN", "NNI", "NNG", "NII", "NIG", "NGG", "INI", "ING", "III", "IIG", "
 
 @pytest.mark.skipif(_ngpu() < 2, reason="needs >= 2 GPUs")
 @pytest.mark.parametrize("variant", ["default", "paced_lsu", "accum", "clip", "copy_engine", "masked", "slots",
-                                     "tma_thread_store", "fp32_wire", "predivide_off"])
+                                     "tma_thread_store", "fp32_wire", "predivide_off", "layer_windows"])
 def test_real_ranks_match_oracle(tmp_path, variant):
     world = _ngpu()                  # every visible GPU: 2 (2x1, 1x2), 4 (4x1, 2x2, 1x4), 8 (8x1, 4x2, 2x4, 1x8)
     splits = [m for m in range(1, world + 1) if world % m == 0]
@@ -84,6 +84,11 @@ def test_real_ranks_match_oracle(tmp_path, variant):
         cfg.update({"wire": "fp32", "topos": ["ho", "two_step", "nccl"], "transports": ["pull", "push"]})
     if variant == "predivide_off":   # raw sums, 1/N in Adam; with the co-run Adam budget forced
         cfg.update({"predivide": False, "topos": ["ho", "direct"], "transports": ["pull"], "adam_smem_kb": 120})
+    if variant == "layer_windows":   # layer-aligned buckets + per-layer forward/backward gathers (NEXT-2)
+        d = world * 8
+        cfg.update({"sizes": [d * 3 + 5] + [d * d, d * d + 7, 3 * d * d, d] * 3 + [d * 3 + 5],
+                    "groups": [0, 1, 5, 9, 13], "topos": ["ho", "two_step"], "transports": ["pull", "push"],
+                    "windows": 2})
     if variant == "masked":      # partial / PEFT training: trainable plan + frozen-parameter plan
         cfg.update({"sizes": [world * 64 * 40 + 24, 333, world * 64 * 9 + 5, 4096], "mask": [0, 1, 0, 1],
                     "topos": ["ho", "two_step"], "transports": ["pull"], "windows": 2})
@@ -95,7 +100,7 @@ def test_real_ranks_match_oracle(tmp_path, variant):
     mask = cfg.get("mask")
     tsizes = [x for x, t in zip(cfg["sizes"], mask) if t] if mask else cfg["sizes"]
     for M in splits:
-        lay = L.Layout(tsizes, world, M, cfg["bucket"])
+        lay = L.Layout(tsizes, world, M, cfg["bucket"], groups=cfg.get("groups"))
         if mask:
             lay_f = L.Layout([x for x, t in zip(cfg["sizes"], mask) if not t], world, M, cfg["bucket"])
             p_frozen = nm.bf16_bits_from_f32(ST.pad_flat(master_f32(0, lay_f.psi), lay_f.psi_pad, np.float32))

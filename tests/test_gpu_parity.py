@@ -1004,3 +1004,67 @@ def test_fp32_wire_with_options(code, kw):
         run.step(t)
     _check_against_dp(run, lay, ref)
     run.close()
+
+
+# --------------------------------------------------------------------- layer-aligned buckets (NEXT-2 per layer)
+LAYERS = lambda d, f, L: [d * 3 + 5] + [d * d, d * d + 7, f * d, d] * L + [d * 3 + 5]
+
+
+@pytest.mark.parametrize("N,M,topo", [(8, 4, "ho"), (4, 2, "two_step"), (8, 1, "ho"), (6, 3, "flat")])
+def test_layer_windows_every_strategy(N, M, topo):
+    """bucket_groups: every bucket is one layer group (parameters
+    gathered layer by layer for the forward / backward pass).  After 2 steps the
+    state equals unsharded DP over the padded layer layout, and gathering layer
+    b + 1 on a side stream (prefetch) while layer b's window is read returns
+    each layer's full bf16 parameters, bit for bit, on every rank."""
+    from paro_synth import grad_flat, master_flat
+    paro = _paro()
+    sizes = LAYERS(64, 176, 3)
+    groups = [0, 1, 5, 9, 13]
+    lay = L.Layout(sizes, N, M, 0, groups=groups)
+    w = master_flat(lay.psi_pad, lay.real)
+    m, v = np.zeros_like(w), np.zeros_like(w)
+    for t in (1, 2):
+        w, m, v, p, _ = ST.dp_step(lay, [grad_flat(r, t, lay.psi_pad, lay.real) for r in range(N)], w, m, v,
+                                   nm.AdamScalars(LR, t))
+    ref = (w, m, v, p, None)
+    side = torch.cuda.Stream()
+    for code in S.paro_strategies():
+        ctx = paro.Context(N, M, mode="emulated", device=0)
+        pl = paro.Plan(ctx, code, sizes, bucket_groups=groups, topology=topo, gather_windows=2, transport="pull")
+        info = pl.info()
+        assert info["n_buckets"] == len(lay.buckets) and info["psi_pad"] == lay.psi_pad
+        st = [tuple(torch.empty(info["os_numel"], dtype=torch.float32, device="cuda") for _ in range(3))
+              for _ in range(N)]
+        run = type("R", (), {})()
+        run.N, run.code, run.pl, run.st, run.info = N, code, pl, st, info
+        run.state = lambda r, run=run: EmuRun.state(run, r)
+        for r in range(N):
+            pl.opt_state_init(r, [x.data_ptr() for x in st[r]], seed=SEED)
+        for t in (1, 2):
+            for r in range(N):
+                pl.synth_grads(r, SEED, t)
+            pl.step([[x.data_ptr() for x in s] for s in st], LR, t)
+        if topo != "flat":
+            _check_against_dp(run, lay, ref)
+        full = np.zeros(lay.psi_pad, np.uint16)
+        for r in range(N):       # the full model assembled from every rank's P shards (bit copies)
+            mine, off = run.state(r)["param"], 0
+            for (a, e) in lay.shard_ranges(code[0], r):
+                full[a:e] = mine[off:off + e - a]
+                off += e - a
+        if topo != "flat":
+            assert np.array_equal(full, p), code
+        nb = len(lay.buckets)
+        pl.gather_window(0, 0, slot=0)
+        for b in range(nb):
+            if b + 1 < nb:       # prefetch the next layer on a side stream
+                pl.gather_window(0, b + 1, slot=(b + 1) % 2, stream=side.cuda_stream)
+            s0, n = lay.buckets[b]
+            for r in range(N):
+                ptr = pl.buffer(r, 1) + 2 * s0 if code[0] == "N" else pl.buffer(r, 5) + 2 * (b % 2) * lay.B
+                got = d2h(ptr, n, np.uint16)
+                assert np.array_equal(got, full[s0:s0 + n]), (code, b, r)
+            torch.cuda.current_stream().wait_stream(side)
+        pl.close()
+        ctx.close()
