@@ -49,7 +49,7 @@ def parse(argv=None):
     ap.add_argument("--model", default="7B")
     ap.add_argument("--strategy", default="IIG")
     ap.add_argument("--group-size", type=int, default=0, help="M; default N/2 for N>=4, else 1")
-    ap.add_argument("--topology", default="ho", choices=["ho", "two_step", "flat", "direct", "nccl"])
+    ap.add_argument("--topology", default="ho", choices=["ho", "two_step", "flat", "direct", "nccl", "oneshot"])
     ap.add_argument("--bucket", type=int, default=1 << 29)
     ap.add_argument("--comm-ctas", type=int, default=148)
     ap.add_argument("--depth", type=int, default=1)
@@ -522,8 +522,9 @@ def allreduce_sweep(paro, ctx, stream, dist, world, M, rank, args, sizes_mib=SWE
     """BASELINE config 5: bf16 gradient all-reduce, 1 MiB - 4 GiB, through the library
     (paro_collective(0) of an NNN plan made with fuse_allreduce = 0, so the whole
     reduction runs in the collective launches: HO-Ring = HO-RS + HO-AG, flat = one ring
-    over all ranks, both with the bf16 hop arithmetic in canonical order) beside NCCL's
-    all_reduce on the same bytes.  busbw = S * 2(N-1)/N / t (nccl-tests convention), t =
+    over all ranks, oneshot = one round in which every rank folds the whole bucket from
+    every peer, all with the bf16 hop arithmetic; HO-Ring and one-shot in canonical
+    order) beside NCCL's all_reduce on the same bytes.  busbw = S * 2(N-1)/N / t (nccl-tests convention), t =
     max over ranks of the CUDA-event time per call.  A fraction of the 770 GB/s measured
     peer-copy peak above 1.2 means the timed code is not doing the work: such a point is
     reported as an error, not a number."""
@@ -552,10 +553,12 @@ def allreduce_sweep(paro, ctx, stream, dist, world, M, rank, args, sizes_mib=SWE
         elems = nbytes // 2
         iters = max(5, min(200, (64 << 20) // nbytes * 10))
         row = {"bytes": nbytes, "iters": iters}
-        for topo in ("ho", "flat"):
+        for topo in ("ho", "flat", "oneshot"):
+            if topo == "oneshot" and world > 15:
+                continue
             pl = paro.Plan(ctx, "NNN", [elems], bucket_elems=min(elems, 1 << 28), topology=topo,
-                           stream=stream.cuda_stream, transport=args.transport, comm_impl=args.comm_impl,
-                           fuse_gather="never", fuse_allreduce=False)
+                           stream=stream.cuda_stream, transport="pull" if topo == "oneshot" else args.transport,
+                           comm_impl=args.comm_impl, fuse_gather="never", fuse_allreduce=False)
             pl.synth_grads(rank, SEED, 1)
             ms = timeit(lambda: pl.collective(0), iters)
             pl.close()
@@ -568,10 +571,12 @@ def allreduce_sweep(paro, ctx, stream, dist, world, M, rank, args, sizes_mib=SWE
         del x
         bw = nbytes * factor / (ms / 1e3) / 1e9
         row["nccl"] = {"us": round(ms * 1e3, 2), "busbw_GBps": round(bw, 1), "frac": round(bw / peak, 4)}
+        lib = [t for t in ("ho", "flat", "oneshot") if t in row and "error" not in row[t]]
+        row["library_best"] = max(lib, key=lambda t: row[t]["busbw_GBps"]) if lib else None
         rows.append(row)
     torch.cuda.empty_cache()
     one = next((r for r in rows if r["bytes"] == 1 << 30), rows[-1])
-    return {"op": "all-reduce bf16 (library: HO-RS + HO-AG / flat ring, canonical-order bf16 hops; nccl: "
+    return {"op": "all-reduce bf16 (library: HO-RS + HO-AG / flat ring / one-shot, bf16 hops; nccl: "
                   "torch.distributed all_reduce)", "groups": f"{world // M}x{M}",
             "peak_GBps": peak, "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s per direction",
             "at_1GiB": {"ho_busbw_GBps": one["ho"]["busbw_GBps"], "flat_busbw_GBps": one["flat"]["busbw_GBps"],

@@ -69,8 +69,16 @@ enum {
   PARO_TOPO_DIRECT = 3,    /* NVSwitch one-shot hierarchical: same bits as 0 / 1 */
   PARO_TOPO_NCCL = 4,      /* NCCL collectives on split comms: perf comparator,
                               NOT bit-exact (NCCL's reduction order)              */
-  PARO_TOPO_H_RING = 5     /* H-Ring all-gather with one leader per group (P:146-147,
+  PARO_TOPO_H_RING = 5,    /* H-Ring all-gather with one leader per group (P:146-147,
                               P:401-402); its reduce-scatter runs two-step        */
+  PARO_TOPO_ONESHOT = 6    /* NVSwitch one-shot, pull only: every collective is ONE
+                              round (each rank reads what it needs from every peer
+                              at once; RS folds in the owner's canonical nested
+                              order, so same bits as 0 / 1 / 3; NNN's all-reduce
+                              folds the whole bucket on every rank).  Fewest
+                              barriers (small messages); more inter bytes than the
+                              rings (RS / AG: (N-M)C inter per rank and bucket,
+                              AR: (N-1)B).  n_gpus <= 15.                          */
 };
 
 typedef struct {

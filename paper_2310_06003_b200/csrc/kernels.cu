@@ -209,31 +209,15 @@ __device__ __forceinline__ void run_fold(const DTask* __restrict__ t, float alph
   }
 }
 
+// Any input count, flat or nested (nest > 1: nblk blocks of nest inputs, each
+// block folded in order, then the block results in order, then the rest), on
+// either wire.  Used for tasks beyond the specialised paths (> 3-4 inputs, the
+// one-shot topology's N-input folds, fp32-wire tasks).
 __device__ __noinline__ void run_fold_generic(const DTask* __restrict__ t, float alpha) {
-  uint4* dst = reinterpret_cast<uint4*>(t->dst);
-  const int nin = t->nin;
-  const uint32_t raw = t->rawmask;
-  const int64_t n8 = t->n8;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n8; u += stride) {
-    float acc[8];
-    unpack8(__ldcg(reinterpret_cast<const uint4*>(t->in[0]) + u), acc);
-    if (raw & 1u) scale_round8(acc, alpha);
-    for (int i = 1; i < nin; ++i) {
-      float x[8];
-      unpack8(__ldcg(reinterpret_cast<const uint4*>(t->in[i]) + u), x);
-      if ((raw >> i) & 1u) scale_round8(x, alpha);
-      hop8(acc, x);
-    }
-    __stcg(dst + u, pack8(acc));
-  }
-}
-
-// fp32 wire task (out_f32): inputs bf16 (raw gradients, pre-scaled in fp32) or
-// fp32 partials, fp32 additions in the task's (canonical) order, fp32 result.
-__device__ __noinline__ void run_fold_wide(const DTask* __restrict__ t, float alpha) {
   const int nin = t->nin;
   const uint32_t raw = t->rawmask, f32 = t->f32mask;
+  const bool wide = t->out_f32 != 0;
+  const int nest = t->nest > 1 ? t->nest : nin, nblk = t->nest > 1 ? t->nblk : 1;
   const int64_t n8 = t->n8;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   auto load = [&](int i, int64_t u, float f[8]) {
@@ -242,26 +226,45 @@ __device__ __noinline__ void run_fold_wide(const DTask* __restrict__ t, float al
       f4x2(__ldcg(p), __ldcg(p + 1), f);
     } else {
       unpack8(__ldcg(reinterpret_cast<const uint4*>(t->in[i]) + u), f);
-      if ((raw >> i) & 1u) mul8(f, alpha);
+      if ((raw >> i) & 1u) pre8(f, alpha, wide);
     }
   };
   for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n8; u += stride) {
     float acc[8];
-    load(0, u, acc);
-    for (int i = 1; i < nin; ++i) {
+    int i = 0;
+    for (int b = 0; b < nblk; ++b) {
+      float blk[8];
+      load(i++, u, blk);
+      for (int q = 1; q < nest; ++q) {
+        float x[8];
+        load(i++, u, x);
+        hopw8(blk, x, wide);
+      }
+      if (b == 0) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[e] = blk[e];
+      } else {
+        hopw8(acc, blk, wide);
+      }
+    }
+    for (; i < nin; ++i) {
       float x[8];
       load(i, u, x);
-      add8(acc, x);
+      hopw8(acc, x, wide);
     }
-    float4* d = reinterpret_cast<float4*>(t->dst) + 2 * u;
-    __stcg(d, make_float4(acc[0], acc[1], acc[2], acc[3]));
-    __stcg(d + 1, make_float4(acc[4], acc[5], acc[6], acc[7]));
+    if (wide) {
+      float4* d = reinterpret_cast<float4*>(t->dst) + 2 * u;
+      __stcg(d, make_float4(acc[0], acc[1], acc[2], acc[3]));
+      __stcg(d + 1, make_float4(acc[4], acc[5], acc[6], acc[7]));
+    } else {
+      __stcg(reinterpret_cast<uint4*>(t->dst) + u, pack8(acc));
+    }
   }
 }
 
 __device__ __forceinline__ void run_task(const DTask* __restrict__ t, float alpha) {
-  if (t->out_f32) {
-    run_fold_wide(t, alpha);
+  if (t->out_f32 || t->nest > 1) {
+    run_fold_generic(t, alpha);
     return;
   }
   switch (t->nin) {

@@ -29,7 +29,8 @@ struct DTask {
   int32_t inter;     // operands (inputs + dst) on another group's GPU: paced by inter_gbps
   uint32_t f32mask;  // bit i: input i holds fp32 values (fp32 wire, reading A3)
   int32_t out_f32;   // 1: fp32 wire task: fp32 arithmetic (no bf16 rounding), fp32 result
-  int32_t pad_;
+  int16_t nest, nblk;   // nested fold: nblk blocks of nest inputs, each folded, then the
+                        // block results, then the remaining inputs (one-shot topology)
 };
 
 struct DRound {

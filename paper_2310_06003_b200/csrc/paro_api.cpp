@@ -257,6 +257,8 @@ DTask resolve(const PlanT* p, const Task& t, int executing_rank, int acc_kind, i
   };
   d.nin = t.nin;
   d.n8 = t.n / 8;
+  d.nest = (int16_t)t.nest;
+  d.nblk = (int16_t)t.nblk;
   d.rawmask = 0;
   d.inter = 0;
   d.f32mask = 0;
@@ -393,6 +395,24 @@ paro_status_t upload_schedule(PlanT* p) {
       p->acc_first.push_back(build(S.accum, -1));
       p->acc_next.push_back(build(S.accum, pl.acc_kind));
       p->red_acc.push_back(build(S.reduce_acc, -1));
+    }
+  }
+  // bounds check of every resolved device span against the regions it must
+  // lie in (compute-sanitizer is closed on this pool: our own check, on the
+  // host, before any kernel can touch a bad address)
+  {
+    const size_t rb = kHeaderBytes + (size_t)pl.region_bytes;
+    auto inside = [&](const void* ptr, size_t bytes) {
+      const char* c = static_cast<const char*>(ptr);
+      for (char* base : p->peer_base)
+        if (base && c >= base + kHeaderBytes && c + bytes <= base + rb) return true;
+      return false;
+    };
+    for (const DTask& d : tasks) {
+      const size_t n = (size_t)d.n8 * 8;
+      bool ok = inside(d.dst, n * (d.out_f32 ? 4 : 2));
+      for (int i = 0; i < d.nin && ok; ++i) ok = inside(d.in[i], n * (((d.f32mask >> i) & 1u) ? 4 : 2));
+      if (!ok) return fail(PARO_ERR_INVALID, "internal error: a collective task addresses memory outside the plan's regions");
     }
   }
   if (!rounds.empty()) {

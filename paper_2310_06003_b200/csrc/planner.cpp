@@ -260,7 +260,10 @@ Planner::Planner(int N_, int M_, const std::string& code_, const std::vector<int
   OS = norm(OS);
   for (int64_t s : sizes)
     if (s < 0) throw std::invalid_argument("param sizes must be >= 0");
-  if (opt.topology < 0 || opt.topology > 5) throw std::invalid_argument("unknown topology");
+  if (opt.topology < 0 || opt.topology > 6) throw std::invalid_argument("unknown topology");
+  if (opt.topology == 6 && N > kMaxIn - 1)
+    throw std::invalid_argument("one-shot topology needs n_gpus <= 15");
+  if (opt.topology == 6 && opt.push) throw std::invalid_argument("one-shot topology is pull-only (transport = pull)");
   if (opt.topology == 3 && (M > kMaxIn || g > kMaxIn))
     throw std::invalid_argument("direct topology needs group_size and n_groups <= 16");
   if (opt.pipeline_depth < 1) opt.pipeline_depth = 1;
@@ -445,7 +448,7 @@ void Planner::build_schedule() {
   // M = 1 (groups of one GPU, I == N): the partials are the raw gradients
   // themselves (scaled by 1/N on read), so Adam folds the peer's raw bucket
   // with its own for every OS != G code: the whole all-reduce in the update.
-  const bool topo_ok = opt.topology == 0 || opt.topology == 1 || opt.topology == 3;
+  const bool topo_ok = opt.topology == 0 || opt.topology == 1 || opt.topology == 3 || opt.topology == 6;
   const bool fuse_ar_e = opt.fuse_ar_e && !push && N > 1 && g == 2 &&
                          ((M > 1 && OS == LV_I && (G == LV_I ? opt.topology != 4 : topo_ok)) ||
                           (M == 1 && OS != LV_G && topo_ok));
@@ -510,7 +513,28 @@ void Planner::build_schedule() {
 
     // ---- world-reaching RS producing g_hat segments at dest_seg (G in {N, G}).
     // Returns rounds used.
+    // one-shot (NVSwitch, pull): rank r folds segment k of every rank's raw
+    // gradients in one round, in the segment owner's canonical order (R2):
+    // blocks j' = owner-group + 1 .. owner-group, inside each the positions
+    // owner-position + 1 .. owner-position (a nested fold when g > 1 and M > 1)
+    auto oneshot_task = [&](int k, Ref dst) {
+      Task t;
+      t.n = C;
+      const int jo = k % g, po = k / g;   // segment k = p * g + j (R1)
+      for (int bj = 1; bj <= g; ++bj)
+        for (int bp = 1; bp <= M; ++bp) t.in[t.nin++] = grad(rank_of((jo + bj) % g, (po + bp) % M), int64_t(k) * C);
+      if (g > 1 && M > 1) {
+        t.nest = M;
+        t.nblk = g;
+      }
+      t.dst = dst;
+      return t;
+    };
     auto emit_world_rs = [&](Launch& L, int round0) -> int {
+      if (topo == 6) {
+        for (int r = 0; r < N; ++r) L.add(round0, r, oneshot_task(seg(grp(r), pos(r)), dest_seg(r)));
+        return 1;
+      }
       if (topo == 0) {  // HO-Ring RS (R16/R17)
         int R1 = 0;
         if (g > 1 && M > 1) {   // phase 1: intra ring RS of the foreign-group segments
@@ -671,6 +695,15 @@ void Planner::build_schedule() {
 
     // ---- world-reaching AG of segments in place in a bucket-layout buffer.  Returns rounds used.
     auto emit_world_ag = [&](Launch& L, const std::function<Ref(int)>& base, int round0) -> int {
+      if (topo == 6) {  // one-shot: every segment copied from its owner in one round
+        for (int r = 0; r < N; ++r)
+          for (int x = 0; x < N; ++x) {
+            if (x == r) continue;
+            const int64_t o = int64_t(seg(grp(x), pos(x))) * C;
+            L.add(round0, r, make_task(C, {at(base(x), o)}, at(base(r), o)));
+          }
+        return 1;
+      }
       if (topo == 0) {  // HO-Ring AG
         for (int j = 0; j < g; ++j) {
           auto gr = group_ranks(j);
@@ -787,6 +820,15 @@ void Planner::build_schedule() {
     };
     // AG_E in place in a chunk-layout buffer (segment j of chunk p at j*C)
     auto emit_ag_e = [&](Launch& L, const std::function<Ref(int)>& base, int round0) -> int {
+      if (topo == 6 && g > 1) {   // one-shot: the g-1 same-position peers' segments in one round
+        for (int r = 0; r < N; ++r)
+          for (int jj = 0; jj < g; ++jj)
+            if (jj != grp(r)) {
+              const int x = rank_of(jj, pos(r));
+              L.add(round0, r, make_task(C, {at(base(x), int64_t(jj) * C)}, at(base(r), int64_t(jj) * C)));
+            }
+        return 1;
+      }
       int used = 0;
       for (int p = 0; p < M; ++p) {
         auto pr = pos_ranks(p);
@@ -796,6 +838,15 @@ void Planner::build_schedule() {
       return used;
     };
     auto emit_ag_i = [&](Launch& L, const std::function<Ref(int)>& base, int round0) -> int {
+      if (topo == 6 && M > 1) {   // one-shot: the M-1 group peers' chunks in one round
+        for (int r = 0; r < N; ++r)
+          for (int pp = 0; pp < M; ++pp)
+            if (pp != pos(r)) {
+              const int x = rank_of(grp(r), pp);
+              L.add(round0, r, make_task(chunk, {at(base(x), int64_t(pp) * chunk)}, at(base(r), int64_t(pp) * chunk)));
+            }
+        return 1;
+      }
       int used = 0;
       for (int j = 0; j < g; ++j) {
         auto gr = group_ranks(j);
@@ -832,6 +883,17 @@ void Planner::build_schedule() {
         }
         return 1;
       }
+      if (topo == 6 && M > 1) {   // one-shot RS_I: the chunk of every group member, R_M(p; .) order
+        for (int r = 0; r < N; ++r) {
+          const int j = grp(r), p = pos(r);
+          Task t;
+          t.n = chunk;
+          for (int i = 1; i <= M; ++i) t.in[t.nin++] = grad(rank_of(j, (p + i) % M), int64_t(p) * chunk);
+          t.dst = out(r);
+          L.add(round0, r, t);
+        }
+        return 1;
+      }
       int r1 = 0;
       for (int j = 0; j < g; ++j) {
         auto gr = group_ranks(j);
@@ -844,6 +906,18 @@ void Planner::build_schedule() {
     };
     // RS_E from the G residency; in place + AG_E for OS = I (all-reduce)
     auto emit_rs_e = [&](Launch& L, int round0) {
+      if (topo == 6 && g > 1) {   // one-shot RS_E: segment j of the g same-position partials, R_g(j; .) order
+        for (int r = 0; r < N; ++r) {
+          const int j = grp(r), p = pos(r);
+          Task t;
+          t.n = C;
+          for (int i = 1; i <= g; ++i) t.in[t.nin++] = gshard(rank_of((j + i) % g, p), int64_t(j) * C);
+          t.dst = dest_seg(r);
+          L.add(round0, r, t);
+        }
+        if (OS == LV_I) emit_ag_e(L, [&](int r) { return ghat_base(r); }, round0 + 1);
+        return;
+      }
       int r2 = 0;
       for (int p = 0; p < M; ++p) {
         auto pr = pos_ranks(p);
@@ -856,6 +930,11 @@ void Planner::build_schedule() {
     };
     // G in {N, G}: world RS (+ AG_E / world AG of g_hat for OS = I / N)
     auto emit_world_reduce = [&](Launch& L) {
+      if (topo == 6 && OS == LV_N) {   // one-shot all-reduce: every rank folds every segment, one round
+        for (int r = 0; r < N; ++r)
+          for (int k = 0; k < N; ++k) L.add(0, r, oneshot_task(k, at(ghat_base(r), int64_t(k) * C)));
+        return;
+      }
       int used = emit_world_rs(L, 0);
       if (OS == LV_I) emit_ag_e(L, [&](int r) { return ghat_base(r); }, used);
       if (OS == LV_N) emit_world_ag(L, [&](int r) { return ghat_base(r); }, used);
@@ -957,7 +1036,7 @@ void Planner::build_schedule() {
             for (size_t i = 0; i < last[r].size(); ++i) {
               const Task& t = last[r][i];
               if (t.dst.rank == d.rank && t.dst.kind == d.kind && t.dst.off == d.off && t.n == C &&
-                  t.nin <= kMaxAdamIn) {
+                  t.nin <= kMaxAdamIn && t.nest <= 1) {
                 for (int k = 0; k < t.nin; ++k) gin[r].push_back(t.in[k]);
                 last[r].erase(last[r].begin() + i);
                 break;

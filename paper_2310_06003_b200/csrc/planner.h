@@ -55,6 +55,10 @@ struct Task {
   int32_t nin = 0;
   Ref in[kMaxIn];
   Ref dst;
+  // nested fold (one-shot topology): the first nest * nblk inputs are nblk
+  // blocks of nest; each block is folded in order, then the block results in
+  // order, then any further inputs: ((b_0 (+) b_1) ...) with b_k = fold(block k)
+  int32_t nest = 0, nblk = 0;
 };
 
 // One collective launch = rounds; round r holds, for every rank, its tasks.

@@ -21,7 +21,7 @@ _lib = C.CDLL(LIB_PATH)
 
 # ---------------------------------------------------------------- constants
 PARO_OK, PARO_ERR_INVALID, PARO_ERR_OOM, PARO_ERR_CUDA, PARO_ERR_NCCL, PARO_ERR_STATE, PARO_ERR_TIMEOUT = range(7)
-TOPO = {"ho": 0, "two_step": 1, "flat": 2, "direct": 3, "nccl": 4, "h_ring": 5}
+TOPO = {"ho": 0, "two_step": 1, "flat": 2, "direct": 3, "nccl": 4, "h_ring": 5, "oneshot": 6}
 STATE = {"P": 0, "G": 1, "OS": 2}
 
 

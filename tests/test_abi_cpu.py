@@ -322,3 +322,48 @@ def test_layer_aligned_buckets_layout_and_window_bytes(N, M):
                 assert all(x == (2 * u[0], 2 * u[1]) for x in per), (code, b)
         pl.close()
     ctx.close()
+
+
+@pytest.mark.parametrize("N,M", [(8, 4), (4, 2), (8, 1), (6, 3), (2, 1), (4, 4)])
+def test_oneshot_topology_rounds_and_bytes(N, M):
+    """PARO_TOPO_ONESHOT: every collective is one round; a rank reads its
+    segment C = B/N from each of the N - 1 peers (RS: (M-1)C intra + (N-M)C
+    inter per bucket, the AG the same), NNN's all-reduce reads the whole bucket
+    from every peer ((N-1)B, one round); G = I's RS_I / RS_E read the group /
+    position peers' chunk / segment ((M-1)B/M, (g-1)C: the ring's bytes).
+    Closed forms counted from the definition of the one-shot schedule."""
+    ctx = paro.Context(N, M)
+    g = N // M
+    B = N * 64 * 8
+    sizes = [B * 3]
+    for code in ("NNN", "GGG", "NNG", "IGG", "IIG", "III"):
+        pl = paro.Plan(ctx, code, sizes, bucket_elems=B, topology="oneshot", fuse_allreduce=False)
+        info = pl.info()
+        C, nb = B // N, info["n_buckets"]
+        if code == "NNN":
+            want = (2 * (M - 1) * B * nb, 2 * (N - M) * B * nb) if N > 1 else (0, 0)
+            rounds = nb
+        elif code in ("GGG", "NNG", "IGG"):
+            rs = ((M - 1) * C, (N - M) * C)
+            if code == "GGG":
+                ag = (0, 0)
+            elif code == "NNG":
+                ag = rs
+            else:                                    # IGG: P = I, restore AG_E over the g positions
+                ag = (0, (g - 1) * C)
+            want = (2 * (rs[0] + ag[0]) * nb, 2 * (rs[1] + ag[1]) * nb)
+            rounds = nb * ((1 if N > 1 else 0) + (1 if sum(ag) else 0))
+        else:                                        # IIG / III: RS_I + RS_E (+ AG_E of g_hat for III)
+            gi = M > 1 and g > 1
+            if not gi:
+                pl.close()
+                continue
+            want = (2 * (M - 1) * (B // M) * nb,
+                    2 * ((g - 1) * C + (g - 1) * C) * nb)   # RS_E + (IIG: AG_E of params | III: AG_E of g_hat)
+            rounds = 3 * nb     # RS_I, RS_E, then AG_E (IIG: of the parameters; III: of g_hat)
+        assert (info["step_send_bytes_intra"], info["step_send_bytes_inter"]) == want, code
+        assert info["n_rounds"] == rounds, (code, info["n_rounds"], rounds)
+        pl.close()
+    with pytest.raises(paro.ParoError, match="pull-only"):
+        paro.Plan(ctx, "IIG", sizes, topology="oneshot", transport="push")
+    ctx.close()

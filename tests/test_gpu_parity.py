@@ -1062,9 +1062,64 @@ def test_layer_windows_every_strategy(N, M, topo):
                 pl.gather_window(0, b + 1, slot=(b + 1) % 2, stream=side.cuda_stream)
             s0, n = lay.buckets[b]
             for r in range(N):
-                ptr = pl.buffer(r, 1) + 2 * s0 if code[0] == "N" else pl.buffer(r, 5) + 2 * (b % 2) * lay.B
+                resident = info["p_numel"] == lay.psi_pad      # P = N (or I with groups of one GPU)
+                ptr = pl.buffer(r, 1) + 2 * s0 if resident else pl.buffer(r, 5) + 2 * (b % 2) * lay.B
                 got = d2h(ptr, n, np.uint16)
                 assert np.array_equal(got, full[s0:s0 + n]), (code, b, r)
             torch.cuda.current_stream().wait_stream(side)
         pl.close()
         ctx.close()
+
+
+# --------------------------------------------------------------------- one-shot topology
+@pytest.mark.parametrize("N,M", [(8, 4), (4, 2), (8, 1), (6, 3), (2, 1), (9, 3), (4, 4)])
+def test_oneshot_every_strategy_ragged(N, M):
+    """PARO_TOPO_ONESHOT: one round per collective, nested N-input folds in the
+    owner's canonical order: every strategy bit-exact vs unsharded DP (same
+    bits as HO-Ring), 2 steps, ragged sizes; with and without the folds fused
+    into Adam; the fp32 wire too."""
+    sizes = ragged_param_sizes() + [N * 64 * 7 + 3]
+    B = N * 64 * 3
+    lay = L.Layout(sizes, N, M, B)
+    ref = _dp_reference(lay, 2)
+    ref32 = _dp_reference(lay, 2, wire="fp32")
+    for i, code in enumerate(S.paro_strategies()):
+        for fuse, wire in ((True, "bf16"), (False, "bf16"), (True, "fp32")):
+            if wire == "fp32" and i % 2:
+                continue
+            run = EmuRun(N, M, code, sizes, B, topo="oneshot", transport="pull", fuse_allreduce=fuse, wire=wire)
+            for t in (1, 2):
+                run.set_grads(t)
+                run.step(t)
+            _check_against_dp(run, lay, ref if wire == "bf16" else ref32)
+            run.close()
+
+
+@pytest.mark.parametrize("N,M", [(8, 4), (4, 2)])
+def test_oneshot_accumulation_and_collective(N, M):
+    """One-shot schedules with gradient accumulation (s = 3, the accumulator
+    hopped after the nested fold) and the NNN all-reduce through paro_collective."""
+    s = 3
+    sizes = [N * 64 * 40 + 24, 1000]
+    B = N * 64 * 8
+    lay = L.Layout(sizes, N, M, B)
+    refs = {gl: _accum_reference(lay, 2, s, gl) for gl in "NIG"}
+    for code in S.paro_strategies():
+        run = EmuRun(N, M, code, sizes, B, topo="oneshot", transport="pull", grad_accum=True)
+        _run_accum(run, 2, s)
+        _check_against_dp(run, lay, refs[code[1]])
+        run.close()
+    paro = _paro()
+    ctx = paro.Context(N, M, mode="emulated", device=0)
+    pl = paro.Plan(ctx, "NNN", [3 * B], bucket_elems=B, topology="oneshot", fuse_allreduce=False)
+    lay3 = L.Layout([3 * B], N, M, B)
+    gh = ST.dp_reduce(lay3, _oracle_grads(N, lay3.psi, 1))
+    for r in range(N):
+        pl.synth_grads(r, SEED, 1)
+    pl.collective(0)
+    torch.cuda.synchronize()
+    for r in range(N):
+        for b, (s0, n) in enumerate(lay3.buckets):
+            assert np.array_equal(d2h(pl.buffer(r, 3) + 2 * (b % 3) * B, n, np.uint16), gh[s0:s0 + n]), (r, b)
+    pl.close()
+    ctx.close()
