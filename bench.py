@@ -179,6 +179,29 @@ def oracle_params_per_s(N, M, strategy, topology, budget_s, sample, steps=None):
     return elems / spent, spent, elems, n
 
 
+def oracle_strategy_table(psi=1 << 22, N=8, M=4, bucket=1 << 18):
+    """SURVEY §8(d) CPU baseline: one full step of every PaRO code with all 8 ranks
+    simulated in one process (BASELINE configs[0]: 2^22 params, 2 groups x 4, 2^18
+    buckets), the oracle as it stands, one core.  params/s = Psi / t_step."""
+    from oracle import layout as L
+    from oracle import numerics as nm
+    from oracle import step as ST
+    from paro_synth import grad_bits, master_f32
+    lay = L.Layout([psi], N, M, bucket)
+    w0 = master_f32(0, lay.psi)
+    grads = [grad_bits(r, 1, 0, lay.psi) for r in range(N)]
+    sc = nm.AdamScalars(LR, 1)
+    out = {}
+    for code in STRATEGIES:
+        state = ST.init_state(w0, lay, code)
+        t0 = time.perf_counter()
+        ST.strategy_step(code, lay, grads, state, sc)
+        dt = time.perf_counter() - t0
+        out[code] = {"s_per_step": round(dt, 3), "params_per_s": lay.psi / dt}
+    return {"workload": f"{psi} params, {N} simulated ranks as {N // M}x{M}, {bucket}-element buckets "
+                        "(BASELINE configs[0])", "cores": 1, "kind": "oracle", "codes": out}
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -372,34 +395,55 @@ def run_ours(args):
             def producer(r, b, b0, b1, dst, strm):
                 src = host.data_ptr() + 2 * ((b0 % bspan) // 8 * 8)
                 assert rt.cudaMemcpyAsync(dst, src, 2 * (b1 - b0), 1, strm) == 0
-        barrier()
-        torch.cuda.synchronize()
-        t0 = torch.cuda.Event(enable_timing=True)
-        t1 = torch.cuda.Event(enable_timing=True)
-        t0.record(stream)
-        for _ in range(args.e2e_steps):
-            step += 1
-            if producer is not None:
-                eplan.step_streamed(ptrs, LR, step, producer=producer)
-            else:
-                eplan.step(ptrs, LR, step, grads=gptrs)
-            eplan.stats()          # D2H of the step's grad norm + nonfinite flag (12 B)
-        t1.record(stream)
-        torch.cuda.synchronize()
-        ems = t0.elapsed_time(t1) / args.e2e_steps
-        if world > 1:
-            tt = torch.tensor([ems], dtype=torch.float64, device="cuda")
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            ems = float(tt.item())
-        e2e = {"value": info["psi"] / (ems / 1000.0), "unit": "params/s", "h2d_bytes_per_step": 2 * info["psi"],
-               "d2h_bytes_per_step": 12, "ms_per_step": ems,
-               # the host link bounds it: H2D bytes per step / step time, per GPU
-               "h2d_GBps_per_gpu": 2 * info["psi"] / (ems / 1000.0) / 1e9,
-               "path": ("paro_step_streamed (grad_slots = 4): each bucket's gradients copied host->device "
-                                "by the copy engines from a <=2 GiB pinned staging area while earlier buckets "
-                                "reduce and update, + paro_step_stats read-back") if producer is not None else
-                               ("paro_step with per-tensor pinned-host gradient pointers (zero-copy pack kernel "
-                                "over PCIe from a <=2 GiB pinned staging area) + paro_step_stats read-back")}
+        # the step's result back on the host: the updated bf16 parameters of this rank's
+        # P residency (2 Psi / div(P) bytes) into pinned memory, plus the norm / flag
+        pbytes = 2 * eplan.info()["p_numel"]
+        hparams = torch.empty(pbytes // 2, dtype=torch.int16, pin_memory=True)
+        rt = _cudart()
+        pbuf = eplan.buffer(rank, 1)
+
+        def e2e_run(params_back):
+            nonlocal step
+            barrier()
+            torch.cuda.synchronize()
+            t0 = torch.cuda.Event(enable_timing=True)
+            t1 = torch.cuda.Event(enable_timing=True)
+            t0.record(stream)
+            for _ in range(args.e2e_steps):
+                step += 1
+                if producer is not None:
+                    eplan.step_streamed(ptrs, LR, step, producer=producer)
+                else:
+                    eplan.step(ptrs, LR, step, grads=gptrs)
+                if params_back:
+                    assert rt.cudaMemcpyAsync(hparams.data_ptr(), pbuf, pbytes, 2, stream.cuda_stream) == 0
+                eplan.stats()          # D2H of the step's grad norm + nonfinite flag (12 B)
+            t1.record(stream)
+            torch.cuda.synchronize()
+            ems = t0.elapsed_time(t1) / args.e2e_steps
+            if world > 1:
+                tt = torch.tensor([ems], dtype=torch.float64, device="cuda")
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                ems = float(tt.item())
+            return ems
+
+        path = (("paro_step_streamed (grad_slots = 4): each bucket's gradients copied host->device by the copy "
+                 "engines from a <=2 GiB pinned staging area while earlier buckets reduce and update")
+                if producer is not None else
+                ("paro_step with per-tensor pinned-host gradient pointers (zero-copy pack kernel over PCIe from "
+                 "a <=2 GiB pinned staging area)"))
+        ems_p = e2e_run(True)
+        ems_s = e2e_run(False)
+        e2e = {"value": info["psi"] / (ems_p / 1000.0), "unit": "params/s", "h2d_bytes_per_step": 2 * info["psi"],
+               "d2h_bytes_per_step": pbytes + 12, "ms_per_step": ems_p,
+               # the host link bounds it: bytes over PCIe per step / step time, per GPU
+               "pcie_GBps_per_gpu": (2 * info["psi"] + pbytes) / (ems_p / 1000.0) / 1e9,
+               "path": path + ", then the rank's updated bf16 parameters (P residency) device->host into pinned "
+                              "memory + paro_step_stats read-back",
+               "stats_only": {"value": info["psi"] / (ems_s / 1000.0), "ms_per_step": ems_s,
+                              "d2h_bytes_per_step": 12, "h2d_GBps_per_gpu": 2 * info["psi"] / (ems_s / 1000.0) / 1e9,
+                              "path": path + " + paro_step_stats read-back only"}}
+        del hparams
         if eplan is not plan:
             plan = eplan
         del host
@@ -422,7 +466,8 @@ def run_ours(args):
         v, spent, elems, n = oracle_params_per_s(1, 1, args.strategy, "ho", 12.0, 1 << 22)
         cpu = {"value": v, "unit": "params/s", "cores": 1, "kind": "oracle",
                "sample": f"{n} oracle steps of {1 << 22}-param slices of the {args.model} list "
-                         f"({spent:.1f} s, NumPy single thread; host has {os.cpu_count()} cores)"}
+                         f"({spent:.1f} s, NumPy single thread; host has {os.cpu_count()} cores)",
+               "per_strategy_2x4": oracle_strategy_table()}
 
     if rank == 0:
         line = {
@@ -481,35 +526,49 @@ def per_strategy_table(paro, ctx, stream, dist, world, M, rank, sizes, args):
         if foot > free - (4 << 30):
             out[code] = {"oom": True, "footprint_gb": round(foot / 1e9, 1)}
             continue
-        plan = paro.Plan(ctx, code, sizes, **plan_kwargs(args, stream.cuda_stream))
-        info = plan.info()
-        st = [torch.empty(info["os_numel"], dtype=torch.float32, device="cuda") for _ in range(3)]
-        ptrs = [[t.data_ptr() for t in st]]
-        plan.opt_state_init(rank, ptrs[0], seed=SEED)
-        plan.synth_grads(rank, SEED, 1)
-        for _ in range(2):
-            step += 1
-            plan.step(ptrs, LR, step)
-        torch.cuda.synchronize()
-        dist.barrier()
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(args.strategy_steps):
-            step += 1
-            plan.step(ptrs, LR, step)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        dist.barrier()
-        torch.cuda.synchronize()
-        tt = torch.tensor([e0.elapsed_time(e1) / args.strategy_steps], dtype=torch.float64, device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms = float(tt.item())
-        out[code] = {"value": info["psi"] / (ms / 1000.0), "ms_per_step": round(ms, 3),
-                     "sent_bytes": int(info["step_send_bytes_intra"] + info["step_send_bytes_inter"]),
-                     "footprint_gb": round(foot / 1e9, 1)}
-        plan.close()
-        del st, ptrs
+        plan, st, err, ms = None, None, None, None
+        try:   # one failing code is reported as such; the ranks agree before moving on
+            plan = paro.Plan(ctx, code, sizes, **plan_kwargs(args, stream.cuda_stream))
+            info = plan.info()
+            st = [torch.empty(info["os_numel"], dtype=torch.float32, device="cuda") for _ in range(3)]
+            ptrs = [[t.data_ptr() for t in st]]
+            plan.opt_state_init(rank, ptrs[0], seed=SEED)
+            plan.synth_grads(rank, SEED, 1)
+        except Exception as e:  # noqa: BLE001
+            err = repr(e)[:300]
+        ok = torch.tensor([0.0 if err else 1.0], dtype=torch.float64, device="cuda")
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if ok.item() == 1.0:
+            try:
+                for _ in range(2):
+                    step += 1
+                    plan.step(ptrs, LR, step)
+                torch.cuda.synchronize()
+                dist.barrier()
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                for _ in range(args.strategy_steps):
+                    step += 1
+                    plan.step(ptrs, LR, step)
+                e1.record(stream)
+                plan.stats()
+                torch.cuda.synchronize()
+                ms = e0.elapsed_time(e1) / args.strategy_steps
+            except Exception as e:  # noqa: BLE001
+                err = repr(e)[:300]
+            tt = torch.tensor([ms if ms is not None else float("inf")], dtype=torch.float64, device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ms = float(tt.item())
+        if err or ms is None or ms == float("inf"):
+            out[code] = {"error": err or "failed on another rank"}
+        else:
+            out[code] = {"value": info["psi"] / (ms / 1000.0), "ms_per_step": round(ms, 3),
+                         "sent_bytes": int(info["step_send_bytes_intra"] + info["step_send_bytes_inter"]),
+                         "footprint_gb": round(foot / 1e9, 1)}
+        if plan is not None:
+            plan.close()
+        del st
         torch.cuda.empty_cache()
     pctx.close()
     return {"unit": "params/s", "steps": args.strategy_steps, "warmup": 2, "codes": out}

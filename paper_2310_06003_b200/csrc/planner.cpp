@@ -1081,20 +1081,22 @@ void Planner::build_schedule() {
         S.reduce.final_barrier = true;
         // gradient accumulation, G = I: the accumulated intra partials sit in the
         // G residency; the step after the last micro-batch folds them in Adam too
+        // (no barrier launch: paro_accumulate ends with an all-peer barrier, which
+        // already orders every peer's accumulator writes before this step, and the
+        // step-end barrier orders Adam's peer reads before the next accumulation)
         if (opt.accum && G == LV_I) {
           S.ghat_in_acc.assign(N, {});
           S.reduce_acc.final_extra.assign(N, 0);
           for (int r = 0; r < N; ++r) {
             const int y = rank_of(1 - grp(r), pos(r));
             S.ghat_in_acc[r] = {gshard(y, 0), gshard(r, 0)};
-            S.reduce_acc.final_extra[r] |= uint64_t(1) << y;
           }
-          S.reduce_acc.final_barrier = true;
+          S.reduce_acc.final_barrier = false;
         }
       }
       // fused gather, auto mode: only when no collective rounds run beside Adam
       // (the whole reduction fused too); beside a rounds kernel the separate
-      // all-gather launch measured faster (profiles/r01/sweep_fuse_4.jsonl)
+      // all-gather launch measured faster (profiles/r01/sweep_fuse_gather_2x2*.jsonl)
       if (opt.fuse_gather == 1 && !S.param_push.empty() && !S.reduce.rounds.empty()) {
         S.param_push.clear();
         if (OS == LV_G && P == LV_I) emit_ag_e(Lg, param_base, 0);
