@@ -124,7 +124,7 @@ __device__ __forceinline__ void st_release_gpu(unsigned long long* p, unsigned l
 // transitive across the gpu-scope and sys-scope synchronisations).  Measured:
 // 1 MiB all-reduce at 2 GPUs 44 -> 37 us, 1 GiB unchanged (profiles/r01).
 // Returns false (and leaves a sticky error word) on timeout.
-__device__ bool grid_peer_barrier(const RoundsArgs& a, uint64_t peers, int bidx) {
+__device__ bool grid_peer_barrier(const RoundsArgs& a, uint64_t peers, int bidx, int narr) {
   __shared__ int s_ok;
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -132,7 +132,7 @@ __device__ bool grid_peer_barrier(const RoundsArgs& a, uint64_t peers, int bidx)
     volatile int* err = a.bar.err;
     if (a.sys_fence_all) __threadfence_system();   // remote NVLink stores visible system-wide
     else __threadfence();
-    const unsigned long long target = a.arrive_base + (unsigned long long)(bidx + 1) * gridDim.x;
+    const unsigned long long target = a.arrive_base + (unsigned long long)(narr + 1) * gridDim.x;
     const unsigned long long old = atomicAdd(a.bar.arrive, 1ull);
     const uint64_t val = a.serial * 256ull + (uint64_t)bidx + 1ull;
     const uint64_t t0 = globaltimer();
@@ -160,6 +160,51 @@ __device__ bool grid_peer_barrier(const RoundsArgs& a, uint64_t peers, int bidx)
   }
   __syncthreads();
   return s_ok != 0;
+}
+
+// The first barrier of a launch, before any of its work: every write it must
+// publish was made by earlier kernels (stream-ordered before this one), so no
+// grid arrival is needed: CTA 0 publishes to the peers (fence.acq_rel.sys, then
+// relaxed flag stores), waits for their flags and opens `go` for the others.
+// Removes the arrival of every CTA (and their launch skew) from the critical
+// path of latency-bound launches.
+__device__ bool entry_barrier(const RoundsArgs& a, uint64_t peers, int bidx) {
+  __shared__ int s_ok;
+  if (threadIdx.x == 0) {
+    int ok = 1;
+    volatile int* err = a.bar.err;
+    const uint64_t val = a.serial * 256ull + (uint64_t)bidx + 1ull;
+    const uint64_t t0 = globaltimer();
+    if (blockIdx.x == 0) {
+      asm volatile("fence.acq_rel.sys;" ::: "memory");
+      for (int x = 0; x < 64; ++x)
+        if ((peers >> x) & 1ull) st_relaxed_sys(a.bar.peer_slot[x], val);
+      for (int x = 0; x < 64 && ok; ++x) {
+        if (!((peers >> x) & 1ull)) continue;
+        while (ld_acquire_sys(&a.bar.my_flags[x]) < val) {
+          if (*err || globaltimer() - t0 > kTimeoutNs) { ok = 0; atomicExch((int*)err, 2); break; }
+        }
+      }
+      st_release_gpu(a.bar.go, (unsigned long long)val);
+    } else {
+      while (ld_acquire_gpu(a.bar.go) < (unsigned long long)val) {
+        if (*err || globaltimer() - t0 > kTimeoutNs) { ok = 0; atomicExch((int*)err, 2); break; }
+        __nanosleep(32);
+      }
+    }
+    if (*err) ok = 0;
+    s_ok = ok;
+  }
+  __syncthreads();
+  return s_ok != 0;
+}
+
+// barrier k of a launch (bidx counts every barrier, narr the grid arrivals)
+__device__ __forceinline__ bool launch_barrier(const RoundsArgs& a, uint64_t peers, int& bidx, int& narr) {
+  const bool ok = (bidx == 0 && a.entry_fast) ? entry_barrier(a, peers, bidx)
+                                              : grid_peer_barrier(a, peers, bidx, narr++);
+  ++bidx;
+  return ok;
 }
 
 // ------------------------------------------------------------- fold tasks
@@ -283,17 +328,17 @@ __device__ __forceinline__ void trace_stamp(const RoundsArgs& a, int slot) {
 
 __global__ void __maxnreg__(48) rounds_kernel(const RoundsArgs a) {
   if (a.bar.err && *(volatile int*)a.bar.err) return;   // sticky device error: do nothing
-  int bidx = 0;
+  int bidx = 0, narr = 0;
   trace_stamp(a, 0);
   for (int r = 0; r < a.nrounds; ++r) {
     const DRound rd = a.rounds[r];
-    if (a.bar.my_flags && !grid_peer_barrier(a, rd.peers_before, bidx++)) return;
+    if (a.bar.my_flags && !launch_barrier(a, rd.peers_before, bidx, narr)) return;
     trace_stamp(a, 1 + 2 * r);
     for (int ti = rd.t0; ti < rd.t1; ++ti) run_task(a.tasks + ti, a.alpha);
     __syncthreads();
     trace_stamp(a, 2 + 2 * r);
   }
-  if (a.bar.my_flags && a.final_barrier) grid_peer_barrier(a, a.final_peers, bidx++);
+  if (a.bar.my_flags && a.final_barrier) launch_barrier(a, a.final_peers, bidx, narr);
   trace_stamp(a, kTraceSlots - 1);
 }
 
@@ -725,11 +770,11 @@ __global__ void __launch_bounds__(kRtThreads) rounds_tma_kernel(const RoundsArgs
   __syncthreads();
   const size_t stage_bytes = (size_t)max_in * kRtTileB;
   uint32_t cnt = 0;   // tiles this CTA has consumed so far (stage = cnt % S, parity = cnt / S)
-  int bidx = 0;
+  int bidx = 0, narr = 0;
   trace_stamp(a, 0);
   for (int r = 0; r < a.nrounds; ++r) {
     const DRound rd = a.rounds[r];
-    if (a.bar.my_flags && !grid_peer_barrier(a, rd.peers_before, bidx++)) return;
+    if (a.bar.my_flags && !launch_barrier(a, rd.peers_before, bidx, narr)) return;
     // order the peers' released (generic-proxy) writes before our async-proxy reads
     if (threadIdx.x == 0) asm volatile("fence.proxy.async;" ::: "memory");
     trace_stamp(a, 1 + 2 * r);
@@ -856,7 +901,7 @@ __global__ void __launch_bounds__(kRtThreads) rounds_tma_kernel(const RoundsArgs
     __syncthreads();
     trace_stamp(a, 2 + 2 * r);
   }
-  if (a.bar.my_flags && a.final_barrier) grid_peer_barrier(a, a.final_peers, bidx++);
+  if (a.bar.my_flags && a.final_barrier) launch_barrier(a, a.final_peers, bidx, narr);
   trace_stamp(a, kTraceSlots - 1);
 }
 

@@ -63,6 +63,8 @@ struct RoundsArgs {
   uint64_t serial;              // launch serial (same sequence on every rank)
   unsigned long long arrive_base;
   int sys_fence_all;            // every CTA fences at sys scope (launch stores into peer memory)
+  int entry_fast;               // the launch's first barrier (no work of this launch before it) is
+                                // published by CTA 0 alone, without the grid arrival
   BarrierCtx bar;
 };
 

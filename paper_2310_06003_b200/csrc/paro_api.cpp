@@ -71,6 +71,7 @@ struct DevLaunch {
   std::vector<std::vector<CopyOp>> copies;   // [round] local rank(s)' copies
   std::vector<uint64_t> round_peers;         // [round] barrier peers before it
   int max_in = 1;          // largest fold input count (TMA stage sizing)
+  int64_t max_tiles = 0;   // largest round's 4096-element tiles of the local rank(s) (grid sizing)
   int64_t bytes = 0;       // bytes the local rank(s) send in this launch
   int64_t hbm = 0;         // algorithmic HBM bytes of the local rank(s)' tasks: each input
                            // read once (a peer's input is read from its HBM; by symmetry
@@ -132,7 +133,7 @@ struct paro_plan {
   float alpha = 1.f;                        // pre-scaling of raw gradients: 1/N (predivide) or 1
   uint64_t* d_trace = nullptr;            // [kTraceLaunches][grid][kTraceSlots]
   std::vector<int> trace_nrounds;         // rounds of each traced launch
-  int trace_grid = 0;
+  std::vector<int> trace_grids;           // CTAs of each traced launch (stride: sm_count)
 };
 // (the C API also declares a *function* named paro_plan, which hides the tag in C++)
 using PlanT = struct paro_plan;
@@ -311,7 +312,12 @@ paro_status_t upload_schedule(PlanT* p) {
         d.peers_before = 0;
       }
       d.t1 = (int32_t)tasks.size();
-      for (int ti = d.t0; ti < d.t1; ++ti) dl.max_in = std::max(dl.max_in, std::min(3, (int)tasks[ti].nin));
+      int64_t tiles = 0;
+      for (int ti = d.t0; ti < d.t1; ++ti) {
+        dl.max_in = std::max(dl.max_in, std::min(3, (int)tasks[ti].nin));
+        tiles += (tasks[ti].n8 * 8 + 4095) / 4096;
+      }
+      dl.max_tiles = std::max(dl.max_tiles, tiles);
       (void)acc_kind;
       rounds.push_back(d);
     }
@@ -442,14 +448,26 @@ void prof_end(PlanT* p, cudaStream_t s, int k) {
 
 constexpr int kTraceLaunches = 512;
 
-int comm_grid(const PlanT* p) {
-  int g = p->opts.comm_ctas > 0 ? p->opts.comm_ctas : 148;
+// CTAs of a collective launch: comm_ctas, or (0 = auto) enough for ~4 tiles of
+// its largest round per CTA, at least 8 and at most one per SM: small launches
+// then pay for fewer arrivals at every in-kernel barrier (latency-bound sizes)
+int comm_grid(const PlanT* p, const DevLaunch* dl = nullptr) {
+  int g = p->opts.comm_ctas > 0 ? p->opts.comm_ctas : p->ctx->sm_count;
+  if (p->opts.comm_ctas <= 0 && dl && dl->max_tiles > 0)
+    g = (int)std::min<int64_t>(g, std::max<int64_t>(8, (dl->max_tiles + 3) / 4));
   if (p->ctx->mode == MODE_REAL) {
     if (g > p->ctx->sm_count) g = p->ctx->sm_count;   // co-residency of all CTAs (barriers)
   } else {
     g = p->ctx->sm_count * 2;
   }
   return g;
+}
+
+// First barrier of a launch published by CTA 0 without a grid arrival (kernels.cu
+// entry_barrier); PARO_ENTRY_BARRIER=0 restores the all-CTA arrival (A/B runs).
+bool entry_fast_on() {
+  static const bool on = !(std::getenv("PARO_ENTRY_BARRIER") && std::atoi(std::getenv("PARO_ENTRY_BARRIER")) == 0);
+  return on;
 }
 
 // 1-CTA peer barrier on the second channel (stream s), for copy-engine launches.
@@ -463,12 +481,13 @@ paro_status_t barrier2(PlanT* p, uint64_t peers, cudaStream_t s, int* nlaunch) {
   a.final_peers = peers;
   a.serial = p->serial2++;
   a.arrive_base = p->arrive_base2;
+  a.entry_fast = entry_fast_on() ? 1 : 0;
   a.bar.peer_slot = p->d_peer_slot2;
   a.bar.my_flags = reinterpret_cast<uint64_t*>(hdr + 1024);
   a.bar.arrive = reinterpret_cast<unsigned long long*>(hdr + 1536);
   a.bar.go = reinterpret_cast<unsigned long long*>(hdr + 1544);
   a.bar.err = reinterpret_cast<int*>(hdr + 520);
-  p->arrive_base2 += 1;
+  p->arrive_base2 += a.entry_fast ? 0 : 1;
   CK(launch_rounds(a, 1, 32, s));
   ++*nlaunch;
   return PARO_OK;
@@ -494,7 +513,7 @@ paro_status_t run_launch(PlanT* p, const DevLaunch& dl, int* nlaunch) {
   paro_ctx* ctx = p->ctx;
   if (dl.dma) return run_dma_launch(p, dl, ctx->comm, nlaunch);
   if (dl.nrounds == 0 && (!dl.final_barrier || ctx->mode != MODE_REAL)) return PARO_OK;
-  const int grid = comm_grid(p);
+  const int grid = comm_grid(p, &dl);
   RoundsArgs a{};
   a.tasks = p->d_tasks;
   a.alpha = p->alpha;
@@ -510,18 +529,20 @@ paro_status_t run_launch(PlanT* p, const DevLaunch& dl, int* nlaunch) {
     a.final_peers = dl.final_peers;
     a.serial = p->serial++;
     a.arrive_base = p->arrive_base;
+    a.entry_fast = entry_fast_on() ? 1 : 0;
     a.bar.peer_slot = p->d_peer_slot;
     a.bar.my_flags = reinterpret_cast<uint64_t*>(hdr);
     a.bar.arrive = reinterpret_cast<unsigned long long*>(hdr + 512);
     a.bar.go = reinterpret_cast<unsigned long long*>(hdr + 528);
     a.bar.err = reinterpret_cast<int*>(hdr + 520);
     a.sys_fence_all = p->pl->opt.push ? 1 : 0;
-    p->arrive_base += (unsigned long long)(dl.nrounds + dl.final_barrier) * grid;
+    // grid arrivals this launch adds to the counter (the first barrier has none when entry_fast)
+    p->arrive_base += (unsigned long long)(dl.nrounds + dl.final_barrier - a.entry_fast) * grid;
     const int k = prof_begin(p, ctx->comm, 1, dl.bytes, dl.hbm);
     if (p->prof && p->d_trace && (int)p->trace_nrounds.size() < kTraceLaunches) {
-      a.trace = p->d_trace + (size_t)p->trace_nrounds.size() * grid * kTraceSlots;
+      a.trace = p->d_trace + (size_t)p->trace_nrounds.size() * ctx->sm_count * kTraceSlots;
       p->trace_nrounds.push_back(dl.nrounds);
-      p->trace_grid = grid;
+      p->trace_grids.push_back(grid);
     }
     if (p->opts.comm_impl != 1) CK(launch_rounds_tma(a, grid, dl.max_in, ctx->comm, p->opts.comm_impl == 2));
     else CK(launch_rounds(a, grid, 0, ctx->comm));
@@ -675,7 +696,7 @@ void paro_opts_default(paro_opts_t* o) {
   o->eps = 1e-8f;
   o->weight_decay = 0.0f;
   o->loss_scale = 1.0f;
-  o->comm_ctas = 148;
+  o->comm_ctas = 0;
   o->pipeline_depth = 2;
   o->pull_transport = 1;
   o->adam_impl = 0;
@@ -800,7 +821,7 @@ paro_status_t paro_plan(paro_ctx_t ctx, const char* strategy, const int64_t* par
   else paro_opts_default(&o);
   if (o.topology == PARO_TOPO_NCCL && ctx->mode == MODE_EMU)
     return fail(PARO_ERR_INVALID, "NCCL topology needs real ranks");
-  if (o.comm_ctas <= 0) o.comm_ctas = 148;
+  if (o.comm_ctas < 0) o.comm_ctas = 0;
   std::vector<int64_t> sizes(param_sizes, param_sizes + n_params);
   PlanOptions po;
   po.bucket_elems = o.bucket_elems > 0 ? o.bucket_elems : (int64_t(1) << 26);
@@ -1764,6 +1785,7 @@ paro_status_t paro_profile_start(paro_plan_t p, int max_launches) {
     CK(cudaMalloc(&p->d_trace, sizeof(uint64_t) * kTraceLaunches * ctx->sm_count * kTraceSlots));
   }
   p->trace_nrounds.clear();
+  p->trace_grids.clear();
   p->prof = true;
   return PARO_OK;
 }
@@ -1796,12 +1818,13 @@ paro_status_t paro_profile_stop(paro_plan_t p, paro_profile_t* out) {
   out->adam_stages = p->adam_stages;
   // device-side trace of the first collective launches: where the time goes
   if (!p->trace_nrounds.empty()) {
-    const int G = p->trace_grid;
-    std::vector<uint64_t> tr((size_t)p->trace_nrounds.size() * G * kTraceSlots);
+    const int S = p->ctx->sm_count;
+    std::vector<uint64_t> tr((size_t)p->trace_nrounds.size() * S * kTraceSlots);
     CK(cudaMemcpy(tr.data(), p->d_trace, tr.size() * sizeof(uint64_t), cudaMemcpyDeviceToHost));
     double bar = 0, work = 0, fin = 0;
     for (size_t l = 0; l < p->trace_nrounds.size(); ++l) {
-      const uint64_t* t = tr.data() + l * G * kTraceSlots;
+      const uint64_t* t = tr.data() + l * S * kTraceSlots;
+      const int G = p->trace_grids[l];
       auto mx = [&](int slot) { uint64_t m = 0; for (int b = 0; b < G; ++b) m = std::max(m, t[b * kTraceSlots + slot]); return m; };
       auto mn = [&](int slot) { uint64_t m = ~0ull; for (int b = 0; b < G; ++b) m = std::min(m, t[b * kTraceSlots + slot]); return m; };
       uint64_t prev = mn(0);

@@ -166,7 +166,7 @@ def check(status):
 
 # ---------------------------------------------------------------- helpers
 def make_opts(bucket_elems=1 << 26, topology="ho", beta1=0.9, beta2=0.95, eps=1e-8, weight_decay=0.0,
-              loss_scale=1.0, comm_ctas=148, pipeline_depth=2, stream=None, transport="pull", adam_impl="auto",
+              loss_scale=1.0, comm_ctas=0, pipeline_depth=2, stream=None, transport="pull", adam_impl="auto",
               comm_impl="tma_store", inter_gbps=0.0, grad_accum=False, clip_norm=0.0, skip_nonfinite=False, gather_windows=0,
               fuse_gather="auto", copy_engine=False, frozen=False, grad_slots=0, fuse_allreduce=True,
               adam_smem_kb=0, wire_dtype="bf16", predivide=True, bucket_groups=None):

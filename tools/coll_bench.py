@@ -25,7 +25,7 @@ def main():
     ap.add_argument("--topos", default="ho,flat,two_step,direct")
     ap.add_argument("--group-size", type=int, default=0)
     ap.add_argument("--iters", type=int, default=10)
-    ap.add_argument("--comm-ctas", type=int, default=148)
+    ap.add_argument("--comm-ctas", type=int, default=0)
     ap.add_argument("--transport", default="pull")
     ap.add_argument("--comm-impl", default="tma_store")
     ap.add_argument("--inter-gbps", type=float, default=0.0, help="emulated inter-group link (0 = off)")
