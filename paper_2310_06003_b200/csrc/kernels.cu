@@ -561,7 +561,7 @@ __device__ __forceinline__ bool tile_of(const AdamArgs& a, int64_t t, TileRef& o
 // gsz: bytes per g_hat element in the stages (2 bf16; 4 when any input is fp32,
 // the fp32 wire).
 template <bool kStore, int kThr>
-__global__ void __launch_bounds__(kThr, 1) adam_tma_kernel(const AdamArgs a, int gnin_max, int stages, int gsz) {
+__global__ void __maxnreg__(72) adam_tma_kernel(const AdamArgs a, int gnin_max, int stages, int gsz) {
   constexpr int kTmaTile = kThr * 8;   // elements per tile (8 per thread)
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ uint64_t full_bar[4];
@@ -717,39 +717,119 @@ __global__ void __launch_bounds__(kThr, 1) adam_tma_kernel(const AdamArgs a, int
 
 // ------------------------------------------------------------- rounds, TMA pipeline
 // The collective rounds with the operand streams moved by the bulk-copy engine:
-// for every tile (4096 elements) of a fold task, one thread issues
-// cp.async.bulk for each input — NVLink-peer or local — into a 4-stage
-// shared-memory ring (mbarrier complete_tx); 8 warps fold from shared memory
-// and store the result.  Memory-level parallelism no longer costs registers,
-// so the kernel keeps NVLink busy beside the Adam kernel.  Tasks with more
-// than kRtMaxIn inputs (direct topology, large M or g) use the LSU path.
+// for every tile of a fold task, one thread issues cp.async.bulk for each input
+// — NVLink-peer or local — into a 4-stage shared-memory ring (mbarrier
+// complete_tx); 8 warps fold from shared memory and store the result.
+// Memory-level parallelism no longer costs registers, so the kernel keeps
+// NVLink busy beside the Adam kernel.  A stage holds one slot of `slotb` bytes
+// per input: 8 KB (4096 bf16 / 2048 fp32 elements) for tasks of up to 3 inputs,
+// smaller slots for the N-input folds of the one-shot topology (the stages
+// stay within 96 KB).
 constexpr int kRtThreads = 256;
-constexpr int kRtTileE = 4096;
-constexpr int kRtTileB = kRtTileE * 2;
+constexpr int kRtSlotB = 8192;    // slot bytes per input for <= 3 inputs
 constexpr int kRtStages = 4;
-constexpr int kRtMaxIn = 3;
+constexpr int kRtMaxIn = kDevMaxIn;
+constexpr int kRtSmem = kRtStages * 3 * kRtSlotB;   // 96 KB
 
-// a stage slot holds kRtTileB bytes per input: 4096 bf16 elements, or 2048 on
-// the fp32 wire (out_f32 tasks, whose fp32 result goes back over input 0)
-__device__ __forceinline__ int rt_te(const DTask* tk) { return tk->out_f32 ? kRtTileE / 2 : kRtTileE; }
+// log2 of the slot bytes: 8 KB up to 3 inputs, else the largest power of two
+// with 4 stages x max_in slots <= 96 KB (4 KB for 4-6 inputs, 2 KB for 7-12, 1 KB)
+int rt_slot_lg(int max_in) {
+  if (max_in <= 3) return 13;
+  int lg = 13;
+  while (lg > 10 && (kRtStages * max_in) << lg > kRtSmem) --lg;
+  return lg;
+}
+int rt_slot_bytes(int max_in) { return 1 << rt_slot_lg(max_in); }
 
-__device__ __forceinline__ bool rt_tile(const RoundsArgs& a, const DRound& rd, int64_t t, const DTask*& task,
-                                        int64_t& e0, int& ne) {
+// log2 of the elements per tile: one slot of the task's widest operand (fp32
+// wire tasks have fp32 results, whose tile goes back over input 0's slot)
+__device__ __forceinline__ int rt_te_lg(const DTask* tk, int slot_lg) { return slot_lg - (tk->out_f32 ? 2 : 1); }
+
+__device__ __forceinline__ bool rt_tile(const RoundsArgs& a, const DRound& rd, int64_t t, int slot_lg,
+                                        const DTask*& task, int64_t& e0, int& ne) {
   for (int ti = rd.t0; ti < rd.t1; ++ti) {
     const DTask* tk = a.tasks + ti;
     if (tk->nin > kRtMaxIn) continue;
-    const int te = rt_te(tk);
+    const int lg = rt_te_lg(tk, slot_lg);
     const int64_t n = tk->n8 * 8;
-    const int64_t nt = (n + te - 1) / te;
+    const int64_t nt = (n + (1ll << lg) - 1) >> lg;
     if (t < nt) {
       task = tk;
-      e0 = t * te;
-      ne = (int)min((int64_t)te, n - e0);
+      e0 = t << lg;
+      ne = (int)min((int64_t)1 << lg, n - e0);
       return true;
     }
     t -= nt;
   }
   return false;
+}
+
+// One tile of an fp32-wire task (fp32 result) or a nested fold (one-shot
+// topology), from the stage `base`: nblk blocks of nest inputs, each folded in
+// order, then the block results, then the remaining inputs; on the task's wire
+// (fp32 adds, or the bf16 hop).  bulk: the result goes back over input 0's slot
+// (the fp32 result is wider than a bf16 input: every thread reads first).
+__device__ __forceinline__ void rt_fold_generic(const DTask* tk, unsigned char* base, int slotb, int ne, int64_t e0,
+                                                float alpha, bool bulk) {
+  const bool wide = tk->out_f32 != 0;
+  const int nin = tk->nin;
+  const uint32_t raw = tk->rawmask, f32 = tk->f32mask;
+  const int nest = tk->nest > 1 ? tk->nest : nin, nblk = tk->nest > 1 ? tk->nblk : 1;
+  const int nu = ne / 8;
+  for (int u0 = 0; u0 < nu; u0 += kRtThreads) {   // wide tiles: one pass (<= 256 units)
+    const int u = u0 + threadIdx.x;
+    const bool act = u < nu;
+    float acc[8];
+    if (act) {
+      auto ld = [&](int i, float x[8]) {
+        if ((f32 >> i) & 1u) {
+          const float4* q = reinterpret_cast<const float4*>(base + i * slotb) + 2 * u;
+          f4x2(q[0], q[1], x);
+        } else {
+          unpack8(reinterpret_cast<const uint4*>(base + i * slotb)[u], x);
+          if ((raw >> i) & 1u) pre8(x, alpha, wide);
+        }
+      };
+      int i = 0;
+      for (int b = 0; b < nblk; ++b) {
+        float blk[8];
+        ld(i++, blk);
+        for (int q = 1; q < nest; ++q) {
+          float x[8];
+          ld(i++, x);
+          hopw8(blk, x, wide);
+        }
+        if (b == 0) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) acc[e] = blk[e];
+        } else {
+          hopw8(acc, blk, wide);
+        }
+      }
+      for (; i < nin; ++i) {
+        float x[8];
+        ld(i, x);
+        hopw8(acc, x, wide);
+      }
+    }
+    if (wide) {
+      if (bulk) {
+        __syncthreads();
+        if (act) {
+          float4* q = reinterpret_cast<float4*>(base) + 2 * u;
+          q[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+          q[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+        }
+      } else if (act) {
+        float4* q = reinterpret_cast<float4*>(tk->dst) + (e0 / 8 + u) * 2;
+        __stcg(q, make_float4(acc[0], acc[1], acc[2], acc[3]));
+        __stcg(q + 1, make_float4(acc[4], acc[5], acc[6], acc[7]));
+      }
+    } else if (act) {
+      if (bulk) reinterpret_cast<uint4*>(base)[u] = pack8(acc);   // same width: in place, this thread read it
+      else __stcg(reinterpret_cast<uint4*>(tk->dst + e0) + u, pack8(acc));
+    }
+  }
 }
 
 // kBulk: the folded tile goes back into its shared-memory stage (in place over
@@ -758,8 +838,15 @@ __device__ __forceinline__ bool rt_tile(const RoundsArgs& a, const DRound& rd, i
 // without LSU slots); the stage is refilled one tile later, after
 // wait_group.read, and every bulk store has completed before the next peer
 // barrier publishes the round.
-template <bool kBulk>
-__global__ void __launch_bounds__(kRtThreads) rounds_tma_kernel(const RoundsArgs a, int max_in) {
+// <= 64 registers (launch bounds 256 x 4): a rounds CTA (256 x 64) must fit
+// beside a 512-thread Adam CTA (512 x 72, __maxnreg__) in the SM's 64 K
+// registers, so collectives and updates co-run
+// kGen: the launch has fp32-wire or nested (one-shot) tasks; their folds are
+// compiled into a separate instantiation so the common bf16 path keeps every
+// value in registers (<= 64, no spills).
+template <bool kBulk, bool kGen>
+__global__ void __launch_bounds__(kRtThreads, 4) rounds_tma_kernel(const RoundsArgs a, int max_in, int slot_lg) {
+  const int slotb = 1 << slot_lg;
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ uint64_t bars[kRtStages];
   if (a.bar.err && *(volatile int*)a.bar.err) return;   // sticky device error: do nothing
@@ -768,7 +855,7 @@ __global__ void __launch_bounds__(kRtThreads) rounds_tma_kernel(const RoundsArgs
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  const size_t stage_bytes = (size_t)max_in * kRtTileB;
+  const size_t stage_bytes = (size_t)max_in * slotb;
   uint32_t cnt = 0;   // tiles this CTA has consumed so far (stage = cnt % S, parity = cnt / S)
   int bidx = 0, narr = 0;
   trace_stamp(a, 0);
@@ -781,7 +868,10 @@ __global__ void __launch_bounds__(kRtThreads) rounds_tma_kernel(const RoundsArgs
     int64_t total = 0;
     for (int ti = rd.t0; ti < rd.t1; ++ti) {
       const DTask* tk = a.tasks + ti;
-      if (tk->nin <= kRtMaxIn) total += (tk->n8 * 8 + rt_te(tk) - 1) / rt_te(tk);
+      if (tk->nin <= kRtMaxIn) {
+        const int lg = rt_te_lg(tk, slot_lg);
+        total += (tk->n8 * 8 + (1ll << lg) - 1) >> lg;
+      }
     }
     const int64_t mine = (total > blockIdx.x) ? (total - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
     const uint64_t t_round = globaltimer();
@@ -790,7 +880,7 @@ __global__ void __launch_bounds__(kRtThreads) rounds_tma_kernel(const RoundsArgs
       const DTask* tk;
       int64_t e0;
       int ne;
-      rt_tile(a, rd, blockIdx.x + k * gridDim.x, tk, e0, ne);
+      rt_tile(a, rd, blockIdx.x + k * gridDim.x, slot_lg, tk, e0, ne);
       if (tk->inter && a.inter_bytes_per_ns > 0.0) {   // token bucket: emulated slow inter link
         inter_sent += (double)ne * (tk->out_f32 ? 4.0 : 2.0) * (double)tk->inter;
         while (inter_sent > (double)(globaltimer() - t_round) * a.inter_bytes_per_ns) __nanosleep(256);
@@ -802,7 +892,7 @@ __global__ void __launch_bounds__(kRtThreads) rounds_tma_kernel(const RoundsArgs
       mbar_expect_tx(&bars[slot], tx);
       for (int i = 0; i < tk->nin; ++i) {
         const int es = ((tk->f32mask >> i) & 1u) ? 4 : 2;
-        bulk_g2s(base + i * kRtTileB, reinterpret_cast<const unsigned char*>(tk->in[i]) + (size_t)e0 * es,
+        bulk_g2s(base + i * slotb, reinterpret_cast<const unsigned char*>(tk->in[i]) + (size_t)e0 * es,
                  (uint32_t)ne * es, &bars[slot]);
       }
     };
@@ -815,66 +905,33 @@ __global__ void __launch_bounds__(kRtThreads) rounds_tma_kernel(const RoundsArgs
       const DTask* tk;
       int64_t e0;
       int ne;
-      rt_tile(a, rd, blockIdx.x + k * gridDim.x, tk, e0, ne);
+      rt_tile(a, rd, blockIdx.x + k * gridDim.x, slot_lg, tk, e0, ne);
       unsigned char* base = smem + slot * stage_bytes;
       const int nin = tk->nin;
       const uint32_t raw = tk->rawmask;
       const int osz = tk->out_f32 ? 4 : 2;
-      if (tk->out_f32) {
-        // fp32 wire: 2048-element tile = one 8-element unit per thread; fp32
-        // inputs read as 2 x float4, raw bf16 gradients widened and pre-scaled
-        const int u = threadIdx.x;
-        const bool act = u < ne / 8;
-        float acc[8];
-        if (act) {
-          for (int i = 0; i < nin; ++i) {
+      if (kGen && (tk->out_f32 || tk->nest > 1)) {
+        rt_fold_generic(tk, base, slotb, ne, e0, a.alpha, kBulk);   // fp32-wire or nested tile
+      } else {
+        uint4* dst = reinterpret_cast<uint4*>(tk->dst + e0);
+        for (int u = threadIdx.x; u < ne / 8; u += kRtThreads) {
+          const uint4 v0 = reinterpret_cast<const uint4*>(base)[u];
+          if (nin == 1 && !(raw & 1u)) {   // plain copy: the stage already holds the result
+            if (!kBulk) __stcg(dst + u, v0);
+            continue;
+          }
+          float acc[8];
+          unpack8(v0, acc);
+          if (raw & 1u) scale_round8(acc, a.alpha);
+          for (int i = 1; i < nin; ++i) {
             float x[8];
-            if ((tk->f32mask >> i) & 1u) {
-              const float4* q = reinterpret_cast<const float4*>(base + i * kRtTileB) + 2 * u;
-              f4x2(q[0], q[1], x);
-            } else {
-              unpack8(reinterpret_cast<const uint4*>(base + i * kRtTileB)[u], x);
-              if ((raw >> i) & 1u) mul8(x, a.alpha);
-            }
-            if (i == 0) {
-#pragma unroll
-              for (int e = 0; e < 8; ++e) acc[e] = x[e];
-            } else {
-              add8(acc, x);
-            }
+            unpack8(reinterpret_cast<const uint4*>(base + i * slotb)[u], x);
+            if ((raw >> i) & 1u) scale_round8(x, a.alpha);
+            hop8(acc, x);
           }
+          if (kBulk) reinterpret_cast<uint4*>(base)[u] = pack8(acc);   // in place: this thread read it
+          else __stcg(dst + u, pack8(acc));
         }
-        if (kBulk) {
-          __syncthreads();   // the fp32 result is wider than a bf16 input 0: all reads first
-          if (act) {
-            float4* q = reinterpret_cast<float4*>(base) + 2 * u;
-            q[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
-            q[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
-          }
-        } else if (act) {
-          float4* q = reinterpret_cast<float4*>(tk->dst) + (e0 / 8 + u) * 2;
-          __stcg(q, make_float4(acc[0], acc[1], acc[2], acc[3]));
-          __stcg(q + 1, make_float4(acc[4], acc[5], acc[6], acc[7]));
-        }
-      }
-      uint4* dst = reinterpret_cast<uint4*>(tk->dst + e0);
-      for (int u = threadIdx.x; u < (tk->out_f32 ? 0 : ne / 8); u += kRtThreads) {
-        const uint4 v0 = reinterpret_cast<const uint4*>(base)[u];
-        if (nin == 1 && !(raw & 1u)) {   // plain copy: the stage already holds the result
-          if (!kBulk) __stcg(dst + u, v0);
-          continue;
-        }
-        float acc[8];
-        unpack8(v0, acc);
-        if (raw & 1u) scale_round8(acc, a.alpha);
-        for (int i = 1; i < nin; ++i) {
-          float x[8];
-          unpack8(reinterpret_cast<const uint4*>(base + i * kRtTileB)[u], x);
-          if ((raw >> i) & 1u) scale_round8(x, a.alpha);
-          hop8(acc, x);
-        }
-        if (kBulk) reinterpret_cast<uint4*>(base)[u] = pack8(acc);   // in place: this thread read it
-        else __stcg(dst + u, pack8(acc));
       }
       if (kBulk) {
         fence_proxy_async_smem();   // this thread's smem writes -> visible to the bulk-copy engine
@@ -895,9 +952,6 @@ __global__ void __launch_bounds__(kRtThreads) rounds_tma_kernel(const RoundsArgs
       bulk_wait_all();                 // before anyone reads them or the next round reuses
       asm volatile("fence.proxy.async.global;" ::: "memory");   // the stages
     }
-    // tasks with many inputs: LSU path over the whole grid
-    for (int ti = rd.t0; ti < rd.t1; ++ti)
-      if (a.tasks[ti].nin > kRtMaxIn) run_task(a.tasks + ti, a.alpha);
     __syncthreads();
     trace_stamp(a, 2 + 2 * r);
   }
@@ -1069,8 +1123,9 @@ int adam_block() { return kAdamBlock; }
 static cudaError_t set_carveouts() {
   static bool done = false;
   if (done) return cudaSuccess;
-  const void* fns[] = {(const void*)rounds_kernel, (const void*)rounds_tma_kernel<false>,
-                       (const void*)rounds_tma_kernel<true>, (const void*)adam_kernel,
+  const void* fns[] = {(const void*)rounds_kernel, (const void*)rounds_tma_kernel<false, false>,
+                       (const void*)rounds_tma_kernel<true, false>, (const void*)rounds_tma_kernel<false, true>,
+                       (const void*)rounds_tma_kernel<true, true>, (const void*)adam_kernel,
                        (const void*)adam_tma_kernel<false, 512>, (const void*)adam_tma_kernel<true, 512>,
                        (const void*)adam_tma_kernel<true, 256>, (const void*)adam_tma_kernel<false, 256>};
   for (const void* f : fns) {
@@ -1089,24 +1144,37 @@ cudaError_t launch_rounds(const RoundsArgs& a, int grid, int block, cudaStream_t
   return cudaGetLastError();
 }
 
-cudaError_t launch_rounds_tma(const RoundsArgs& a, int grid, int max_in, cudaStream_t s, int bulk_store) {
+cudaError_t launch_rounds_tma(const RoundsArgs& a, int grid, int max_in, cudaStream_t s, int bulk_store,
+                              int generic) {
   cudaError_t ec = set_carveouts();
   if (ec != cudaSuccess) return ec;
   static bool attr_set = false;
   if (!attr_set) {
-    for (const void* f : {(const void*)rounds_tma_kernel<false>, (const void*)rounds_tma_kernel<true>}) {
-      cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           kRtStages * kRtMaxIn * kRtTileB);
+    for (const void* f : {(const void*)rounds_tma_kernel<false, false>, (const void*)rounds_tma_kernel<true, false>,
+                          (const void*)rounds_tma_kernel<false, true>, (const void*)rounds_tma_kernel<true, true>}) {
+      cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, kRtSmem);
       if (e != cudaSuccess) return e;
     }
     attr_set = true;
   }
   if (max_in < 1) max_in = 1;
   if (max_in > kRtMaxIn) max_in = kRtMaxIn;
-  const size_t sm = (size_t)kRtStages * max_in * kRtTileB;
-  if (bulk_store) rounds_tma_kernel<true><<<grid, kRtThreads, sm, s>>>(a, max_in);
-  else rounds_tma_kernel<false><<<grid, kRtThreads, sm, s>>>(a, max_in);
+  const int lg = rt_slot_lg(max_in);
+  const size_t sm = (size_t)kRtStages * max_in << lg;
+  if (generic) {
+    if (bulk_store) rounds_tma_kernel<true, true><<<grid, kRtThreads, sm, s>>>(a, max_in, lg);
+    else rounds_tma_kernel<false, true><<<grid, kRtThreads, sm, s>>>(a, max_in, lg);
+  } else {
+    if (bulk_store) rounds_tma_kernel<true, false><<<grid, kRtThreads, sm, s>>>(a, max_in, lg);
+    else rounds_tma_kernel<false, false><<<grid, kRtThreads, sm, s>>>(a, max_in, lg);
+  }
   return cudaGetLastError();
+}
+
+int rounds_tma_smem_kb(int max_in) {
+  if (max_in < 1) max_in = 1;
+  if (max_in > kRtMaxIn) max_in = kRtMaxIn;
+  return (kRtStages * max_in * rt_slot_bytes(max_in) + 1023) / 1024;
 }
 
 cudaError_t launch_adam(const AdamArgs& a, int grid, cudaStream_t s, int cap_two_per_sm) {

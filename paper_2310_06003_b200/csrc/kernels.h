@@ -124,7 +124,10 @@ enum AdamVariant : int {
 };
 cudaError_t launch_adam_tma(const AdamArgs& a, int sms, cudaStream_t s, int smem_budget_kb, int tma_store,
                             int hard_kb, int* variant, int* stages);
-cudaError_t launch_rounds_tma(const RoundsArgs& a, int grid, int max_in, cudaStream_t s, int bulk_store);
+// generic: the launch has fp32-wire (out_f32) or nested (one-shot) tasks
+cudaError_t launch_rounds_tma(const RoundsArgs& a, int grid, int max_in, cudaStream_t s, int bulk_store,
+                              int generic);
+int rounds_tma_smem_kb(int max_in);   // dynamic shared memory of a TMA rounds CTA
 cudaError_t launch_norm_finalize(const double* partials, int n, double* out, cudaStream_t s);
 // phase 1 of the two-phase step: block partials of sum (fold(gin) * s_g)^2 and
 // the non-finite flag, 2 bytes read per element, no update

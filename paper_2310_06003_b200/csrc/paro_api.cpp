@@ -72,6 +72,7 @@ struct DevLaunch {
   std::vector<uint64_t> round_peers;         // [round] barrier peers before it
   int max_in = 1;          // largest fold input count (TMA stage sizing)
   int64_t max_tiles = 0;   // largest round's 4096-element tiles of the local rank(s) (grid sizing)
+  int generic = 0;         // has fp32-wire or nested (one-shot) tasks: the generic fold kernel
   int64_t bytes = 0;       // bytes the local rank(s) send in this launch
   int64_t hbm = 0;         // algorithmic HBM bytes of the local rank(s)' tasks: each input
                            // read once (a peer's input is read from its HBM; by symmetry
@@ -314,7 +315,8 @@ paro_status_t upload_schedule(PlanT* p) {
       d.t1 = (int32_t)tasks.size();
       int64_t tiles = 0;
       for (int ti = d.t0; ti < d.t1; ++ti) {
-        dl.max_in = std::max(dl.max_in, std::min(3, (int)tasks[ti].nin));
+        dl.max_in = std::max(dl.max_in, (int)tasks[ti].nin);
+        if (tasks[ti].out_f32 || tasks[ti].nest > 1) dl.generic = 1;
         tiles += (tasks[ti].n8 * 8 + 4095) / 4096;
       }
       dl.max_tiles = std::max(dl.max_tiles, tiles);
@@ -544,7 +546,7 @@ paro_status_t run_launch(PlanT* p, const DevLaunch& dl, int* nlaunch) {
       p->trace_nrounds.push_back(dl.nrounds);
       p->trace_grids.push_back(grid);
     }
-    if (p->opts.comm_impl != 1) CK(launch_rounds_tma(a, grid, dl.max_in, ctx->comm, p->opts.comm_impl == 2));
+    if (p->opts.comm_impl != 1) CK(launch_rounds_tma(a, grid, dl.max_in, ctx->comm, p->opts.comm_impl == 2, dl.generic));
     else CK(launch_rounds(a, grid, 0, ctx->comm));
     prof_end(p, ctx->comm, k);
     ++*nlaunch;
@@ -553,7 +555,7 @@ paro_status_t run_launch(PlanT* p, const DevLaunch& dl, int* nlaunch) {
       a.rounds = p->d_rounds + dl.round_off + r;
       a.nrounds = 1;
       const int k = prof_begin(p, ctx->comm, 1, r == 0 ? dl.bytes : 0, r == 0 ? dl.hbm : 0);
-      if (p->opts.comm_impl != 1) CK(launch_rounds_tma(a, grid, dl.max_in, ctx->comm, p->opts.comm_impl == 2));
+      if (p->opts.comm_impl != 1) CK(launch_rounds_tma(a, grid, dl.max_in, ctx->comm, p->opts.comm_impl == 2, dl.generic));
       else CK(launch_rounds(a, grid, 0, ctx->comm));
       prof_end(p, ctx->comm, k);
       ++*nlaunch;
@@ -1381,7 +1383,7 @@ paro_status_t step_impl(PlanT* p, const void* const* grads, void* const* params,
         if (red[b].nrounds > 0) mx = std::max(mx, red[b].max_in);
         if (p->gat[b].nrounds > 0) mx = std::max(mx, p->gat[b].max_in);
       }
-      hard = 226 - 1 - 32 * mx;
+      hard = 226 - 1 - rounds_tma_smem_kb(mx);
     }
     if (p->opts.adam_smem_kb > 0) budget = hard = p->opts.adam_smem_kb;
     if (ai != 1) {

@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--topos", default="ho,flat,two_step,direct")
     ap.add_argument("--group-size", type=int, default=0)
     ap.add_argument("--iters", type=int, default=10)
+    ap.add_argument("--no-nccl", action="store_true")
     ap.add_argument("--comm-ctas", type=int, default=0)
     ap.add_argument("--transport", default="pull")
     ap.add_argument("--comm-impl", default="tma_store")
@@ -66,13 +67,15 @@ def main():
     for mb in [float(x) for x in a.sizes_mb.split(",")]:
         nbytes = int(mb * (1 << 20))
         elems = nbytes // 2
-        row = {"bytes": nbytes, "groups": f"{world // M}x{M}", "n_gpus": world, "inter_gbps": a.inter_gbps}
+        row = {"bytes": nbytes, "groups": f"{world // M}x{M}", "n_gpus": world, "inter_gbps": a.inter_gbps,
+               "comm_ctas": a.comm_ctas, "entry_barrier": os.environ.get("PARO_ENTRY_BARRIER", "1")}
         factor = 2 * (world - 1) / world if a.op == "ar" else (world - 1) / world
         code, what = ("NNN", 0) if a.op == "ar" else ("NNG", 1)
         for topo in a.topos.split(","):
             bucket = min(elems, 1 << 28)
             pl = paro.Plan(ctx, code, [elems], bucket_elems=bucket, topology=topo, comm_ctas=a.comm_ctas,
-                           stream=stream.cuda_stream, transport=a.transport, comm_impl=a.comm_impl,
+                           stream=stream.cuda_stream, transport="pull" if topo == "oneshot" else a.transport,
+                           comm_impl=a.comm_impl,
                            inter_gbps=a.inter_gbps, fuse_gather="never", fuse_allreduce=False)
             pl.synth_grads(rank, 1234, 1)
             ms = timeit(lambda: pl.collective(what))
@@ -90,6 +93,10 @@ def main():
                     "work": round(1000 * pr["traced_work_ms"] / nl, 2),
                     "final": round(1000 * pr["traced_final_ms"] / nl, 2)}
             pl.close()
+        if a.no_nccl:
+            if rank == 0:
+                print(json.dumps(row), flush=True)
+            continue
         x = torch.ones(elems, dtype=torch.bfloat16, device="cuda")
         if a.op == "ar":
             ms = timeit(lambda: dist.all_reduce(x))
