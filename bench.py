@@ -494,6 +494,8 @@ def run_ours(args):
             "gpu_launches": int(prof["kernel_launches"]),
             "clocks": clk,
             "per_step": {"sent_intra_bytes": stats["sent_intra"], "sent_inter_bytes": stats["sent_inter"],
+                         # NVLink bytes counted on the device by the kernels that moved them (-1 at N = 1)
+                         "moved_intra_bytes": stats["moved_intra"], "moved_inter_bytes": stats["moved_inter"],
                          "grad_norm": stats["grad_norm"], "adam_ms": prof["adam_ms"] / args.steps,
                          "comm_ms": prof["comm_ms"] / args.steps},
         }

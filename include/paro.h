@@ -243,6 +243,14 @@ typedef struct {
   int32_t nonfinite;     /* 1 if any reduced gradient was inf/NaN (R9: flag only)   */
   int64_t sent_intra, sent_inter;  /* bytes this rank sent in the last step         */
   int32_t kernel_launches;         /* library kernels launched by the last step     */
+  /* NVLink bytes this rank's transfers moved since the last paro_step began, by  *
+   * link class: counted on the device by the kernels that move them (every tile *
+   * a CTA pulls from a peer or pushes into one; fused-hop pulls and fused-gather *
+   * pushes in Adam), plus copy-engine copies counted at enqueue.  In these       *
+   * rank-symmetric schedules it equals sent_intra / sent_inter (except H-Ring,   *
+   * whose leaders pull more than they are pulled: totals over ranks agree).      *
+   * Real mode only; -1 in emulated mode and for the NCCL comparator.             */
+  int64_t moved_intra, moved_inter;
 } paro_step_stats_t;
 
 /* Fill *o with the defaults listed above. */

@@ -207,6 +207,28 @@ __device__ __forceinline__ bool launch_barrier(const RoundsArgs& a, uint64_t pee
   return ok;
 }
 
+// NVLink bytes of one task / tile, split by link class: every peer input is
+// pulled, a peer destination pushed (device-counted "moved" bytes, reported by
+// paro_step_stats)
+__device__ __forceinline__ void count_moved(const DTask* tk, int64_t ne, unsigned long long& mi,
+                                            unsigned long long& me) {
+  const int osz = tk->out_f32 ? 4 : 2;
+  for (int i = 0; i < tk->nin; ++i)
+    if ((tk->peermask >> i) & 1u) {
+      const unsigned long long b = (unsigned long long)ne * (((tk->f32mask >> i) & 1u) ? 4 : 2);
+      if ((tk->intermask >> i) & 1u) me += b;
+      else mi += b;
+    }
+  if (tk->dst_peer == 1) mi += (unsigned long long)ne * osz;
+  if (tk->dst_peer == 2) me += (unsigned long long)ne * osz;
+}
+__device__ __forceinline__ void flush_moved(unsigned long long* moved, unsigned long long mi,
+                                            unsigned long long me) {
+  if (!moved) return;
+  if (mi) atomicAdd(moved, mi);
+  if (me) atomicAdd(moved + 1, me);
+}
+
 // ------------------------------------------------------------- fold tasks
 // Each task is spread over the whole grid, grid-stride interleaved (every
 // warp touches consecutive 16-byte units; measured on B200: interleaving beats
@@ -329,16 +351,21 @@ __device__ __forceinline__ void trace_stamp(const RoundsArgs& a, int slot) {
 __global__ void __maxnreg__(48) rounds_kernel(const RoundsArgs a) {
   if (a.bar.err && *(volatile int*)a.bar.err) return;   // sticky device error: do nothing
   int bidx = 0, narr = 0;
+  unsigned long long mi = 0, me = 0;
   trace_stamp(a, 0);
   for (int r = 0; r < a.nrounds; ++r) {
     const DRound rd = a.rounds[r];
     if (a.bar.my_flags && !launch_barrier(a, rd.peers_before, bidx, narr)) return;
     trace_stamp(a, 1 + 2 * r);
-    for (int ti = rd.t0; ti < rd.t1; ++ti) run_task(a.tasks + ti, a.alpha);
+    for (int ti = rd.t0; ti < rd.t1; ++ti) {
+      run_task(a.tasks + ti, a.alpha);
+      if (blockIdx.x == 0 && threadIdx.x == 0) count_moved(a.tasks + ti, a.tasks[ti].n8 * 8, mi, me);
+    }
     __syncthreads();
     trace_stamp(a, 2 + 2 * r);
   }
   if (a.bar.my_flags && a.final_barrier) launch_barrier(a, a.final_peers, bidx, narr);
+  if (threadIdx.x == 0) flush_moved(a.moved, mi, me);
   trace_stamp(a, kTraceSlots - 1);
 }
 
@@ -456,14 +483,22 @@ __global__ void __launch_bounds__(kAdamBlock, 3) adam_kernel(const AdamArgs a) {
   double nsq = 0.0;
   int bad = 0;
   int64_t base = 0;
+  unsigned long long mi = 0, me = 0;
   for (int i = 0; i < a.nseg && base < b1; ++i) {
     const AdamSeg& sg = a.seg[i];
     const int64_t n8 = sg.n8;
     const int64_t s = max(b0, base) - base, e = min(b1, base + n8) - base;
     for (int64_t u = s + threadIdx.x; u < e; u += blockDim.x) adam_unit(sg, u, c, nsq, bad);
+    if (threadIdx.x == 0 && e > s) {
+      for (int k = 0; k < sg.gnin; ++k)
+        if ((sg.gpeer >> k) & 1u) (((sg.ginter >> k) & 1u) ? me : mi) += (unsigned long long)(e - s) * 8 *
+                                                                          (((sg.gf32 >> k) & 1u) ? 4 : 2);
+      for (int k = 0; k < sg.npush; ++k) (((sg.pinter >> k) & 1u) ? me : mi) += (unsigned long long)(e - s) * 16;
+    }
     base += n8;
   }
   push_fence(a);
+  if (threadIdx.x == 0) flush_moved(a.moved, mi, me);
   // block reduction of the norm partial: warp shuffles, then one warp
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) nsq += __shfl_xor_sync(0xffffffffu, nsq, o);
@@ -570,6 +605,7 @@ __global__ void __maxnreg__(72) adam_tma_kernel(const AdamArgs a, int gnin_max, 
                    a.has_wd};
   const size_t g_bytes = (size_t)kTmaTile * gsz, f_bytes = (size_t)kTmaTile * 4;
   const size_t stage_bytes = gnin_max * g_bytes + 3 * f_bytes;
+  unsigned long long mi = 0, me = 0;   // NVLink bytes of this CTA's tiles (thread 0)
   int64_t total = 0;
   for (int i = 0; i < a.nseg; ++i) total += (a.seg[i].n8 * 8 + kTmaTile - 1) / kTmaTile;
   const int64_t mine = (total > blockIdx.x) ? (total - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
@@ -586,7 +622,12 @@ __global__ void __maxnreg__(72) adam_tma_kernel(const AdamArgs a, int gnin_max, 
     unsigned char* base = smem + s * stage_bytes;
     const uint32_t fb = (uint32_t)tr.n * 4;
     uint32_t tx = 3 * fb;
-    for (int i = 0; i < sg.gnin; ++i) tx += (uint32_t)tr.n * (((sg.gf32 >> i) & 1u) ? 4 : 2);
+    for (int i = 0; i < sg.gnin; ++i) {
+      const uint32_t b = (uint32_t)tr.n * (((sg.gf32 >> i) & 1u) ? 4 : 2);
+      tx += b;
+      if ((sg.gpeer >> i) & 1u) (((sg.ginter >> i) & 1u) ? me : mi) += b;   // fused hop: NVLink pull
+    }
+    for (int i = 0; i < sg.npush; ++i) (((sg.pinter >> i) & 1u) ? me : mi) += (unsigned long long)tr.n * 2;
     mbar_expect_tx(&full_bar[s], tx);
     for (int i = 0; i < sg.gnin; ++i) {
       const int es = ((sg.gf32 >> i) & 1u) ? 4 : 2;
@@ -698,6 +739,7 @@ __global__ void __maxnreg__(72) adam_tma_kernel(const AdamArgs a, int gnin_max, 
   } else {
     push_fence(a);
   }
+  if (threadIdx.x == 0) flush_moved(a.moved, mi, me);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) nsq += __shfl_xor_sync(0xffffffffu, nsq, o);
   __shared__ double s_part[kThr / 32];
@@ -858,6 +900,7 @@ __global__ void __launch_bounds__(kRtThreads, 4) rounds_tma_kernel(const RoundsA
   const size_t stage_bytes = (size_t)max_in * slotb;
   uint32_t cnt = 0;   // tiles this CTA has consumed so far (stage = cnt % S, parity = cnt / S)
   int bidx = 0, narr = 0;
+  unsigned long long mi = 0, me = 0;   // NVLink bytes of the tiles this CTA issued (thread 0)
   trace_stamp(a, 0);
   for (int r = 0; r < a.nrounds; ++r) {
     const DRound rd = a.rounds[r];
@@ -885,6 +928,7 @@ __global__ void __launch_bounds__(kRtThreads, 4) rounds_tma_kernel(const RoundsA
         inter_sent += (double)ne * (tk->out_f32 ? 4.0 : 2.0) * (double)tk->inter;
         while (inter_sent > (double)(globaltimer() - t_round) * a.inter_bytes_per_ns) __nanosleep(256);
       }
+      count_moved(tk, ne, mi, me);
       const uint32_t slot = (cnt + (uint32_t)k) % kRtStages;
       unsigned char* base = smem + slot * stage_bytes;
       uint32_t tx = 0;
@@ -956,6 +1000,7 @@ __global__ void __launch_bounds__(kRtThreads, 4) rounds_tma_kernel(const RoundsA
     trace_stamp(a, 2 + 2 * r);
   }
   if (a.bar.my_flags && a.final_barrier) launch_barrier(a, a.final_peers, bidx, narr);
+  if (threadIdx.x == 0) flush_moved(a.moved, mi, me);
   trace_stamp(a, kTraceSlots - 1);
 }
 

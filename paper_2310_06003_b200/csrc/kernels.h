@@ -31,6 +31,10 @@ struct DTask {
   int32_t out_f32;   // 1: fp32 wire task: fp32 arithmetic (no bf16 rounding), fp32 result
   int16_t nest, nblk;   // nested fold: nblk blocks of nest inputs, each folded, then the
                         // block results, then the remaining inputs (one-shot topology)
+  uint32_t peermask;    // bit i: input i lives on another rank (pulled over NVLink)
+  uint32_t intermask;   // bit i: ... on another group's rank
+  int32_t dst_peer;     // result stored into another rank: 1 same group, 2 other group (push)
+  int32_t pad2_;
 };
 
 struct DRound {
@@ -65,6 +69,7 @@ struct RoundsArgs {
   int sys_fence_all;            // every CTA fences at sys scope (launch stores into peer memory)
   int entry_fast;               // the launch's first barrier (no work of this launch before it) is
                                 // published by CTA 0 alone, without the grid arrival
+  unsigned long long* moved;    // [intra, inter] NVLink bytes this rank's CTAs pulled + pushed (or NULL)
   BarrierCtx bar;
 };
 
@@ -88,6 +93,8 @@ struct AdamSeg {
   uint16_t* push[kAdamMaxPush];   // stored at these peer addresses (NVLink)
   uint32_t gf32;     // bit i: gin[i] holds fp32 values (fp32 wire)
   int32_t gwide;     // 1: fp32 wire: raw inputs g * alpha and hops in fp32, g_hat never rounded to bf16
+  uint32_t gpeer, ginter;   // bit i: gin[i] on another rank / another group's rank (NVLink pulls)
+  uint32_t pinter;          // bit i: push[i] on another group's rank (else same group)
 };
 
 struct AdamArgs {
@@ -103,6 +110,7 @@ struct AdamArgs {
   // update is skipped entirely while *skip != 0
   const float* s_g_dev;
   const int* skip;
+  unsigned long long* moved;   // [intra, inter] NVLink bytes pulled (fused hop) + pushed (fused gather), or NULL
 };
 
 struct PackEntry {     // one tensor slice: src/dst element pointers + count

@@ -131,6 +131,8 @@ struct paro_plan {
   int prof_used = 0;
   int64_t prof_steps = 0, prof_launches = 0;
   int adam_variant = -1, adam_stages = 0;   // the last Adam launch (AdamVariant)
+  unsigned long long* d_moved = nullptr;    // [intra, inter] NVLink bytes moved by this rank's kernels
+  int64_t moved_host[2] = {0, 0};           // ... by its copy-engine transfers (counted at enqueue)
   float alpha = 1.f;                        // pre-scaling of raw gradients: 1/N (predivide) or 1
   uint64_t* d_trace = nullptr;            // [kTraceLaunches][grid][kTraceSlots]
   std::vector<int> trace_nrounds;         // rounds of each traced launch
@@ -273,6 +275,12 @@ DTask resolve(const PlanT* p, const Task& t, int executing_rank, int acc_kind, i
     else if (pl.esz[t.in[i].kind] == 4) d.f32mask |= 1u << i;
     if (t.in[i].rank / M != executing_rank / M) d.inter += 1;
   }
+  for (int i = 0; i < t.nin; ++i)
+    if (t.in[i].rank != executing_rank) {
+      d.peermask |= 1u << i;
+      if (t.in[i].rank / M != executing_rank / M) d.intermask |= 1u << i;
+    }
+  if (t.dst.rank != executing_rank) d.dst_peer = (t.dst.rank / M != executing_rank / M) ? 2 : 1;
   d.dst = reinterpret_cast<uint16_t*>(ptr_of(t.dst));
   if (t.dst.rank / M != executing_rank / M) d.inter += 1;
   if (acc_kind >= 0 && t.dst.kind == acc_kind) {
@@ -503,7 +511,15 @@ paro_status_t run_dma_launch(PlanT* p, const DevLaunch& dl, cudaStream_t s, int*
     paro_status_t st = barrier2(p, dl.round_peers[r], s, nlaunch);
     if (st != PARO_OK) return st;
     const int k = prof_begin(p, s, 1, r == 0 ? dl.bytes : 0, r == 0 ? dl.hbm : 0);
-    for (const CopyOp& c : dl.copies[r]) CK(cudaMemcpyAsync(c.dst, c.src, c.bytes, cudaMemcpyDeviceToDevice, s));
+    for (const CopyOp& c : dl.copies[r]) {
+      CK(cudaMemcpyAsync(c.dst, c.src, c.bytes, cudaMemcpyDeviceToDevice, s));
+      if (ctx->mode == MODE_REAL) {   // copy-engine transfer over NVLink: counted at enqueue
+        const int rs = data_rank(p, c.src), rd = data_rank(p, c.dst);
+        const int other = rs != ctx->rank ? rs : rd;
+        if (other >= 0 && other != ctx->rank)
+          p->moved_host[other / p->pl->M != ctx->rank / p->pl->M ? 1 : 0] += (int64_t)c.bytes;
+      }
+    }
     prof_end(p, s, k);
   }
   if (dl.final_barrier) return barrier2(p, dl.final_peers, s, nlaunch);
@@ -532,6 +548,7 @@ paro_status_t run_launch(PlanT* p, const DevLaunch& dl, int* nlaunch) {
     a.serial = p->serial++;
     a.arrive_base = p->arrive_base;
     a.entry_fast = entry_fast_on() ? 1 : 0;
+    a.moved = p->d_moved;
     a.bar.peer_slot = p->d_peer_slot;
     a.bar.my_flags = reinterpret_cast<uint64_t*>(hdr);
     a.bar.arrive = reinterpret_cast<unsigned long long*>(hdr + 512);
@@ -651,6 +668,7 @@ void destroy_plan(PlanT* p) {
     cudaFree(p->d_nonfinite);
     cudaFree(p->d_sg);
     cudaFree(p->d_skip);
+    cudaFree(p->d_moved);
     cudaFree(p->d_pack);
     if (p->h_pack) cudaFreeHost(p->h_pack);
     for (cudaEvent_t e : {p->ev_fork, p->ev_comm, p->ev_comp, p->ev_pack_staged, p->ev_unpack_staged, p->ev_dma})
@@ -944,6 +962,8 @@ paro_status_t paro_plan(paro_ctx_t ctx, const char* strategy, const int64_t* par
   PCK(cudaMalloc(&p->d_sg, sizeof(float)));
   PCK(cudaMalloc(&p->d_skip, sizeof(int)));
   PCK(cudaMemset(p->d_skip, 0, sizeof(int)));
+  PCK(cudaMalloc(&p->d_moved, 2 * sizeof(unsigned long long)));
+  PCK(cudaMemset(p->d_moved, 0, 2 * sizeof(unsigned long long)));
   p->pack_cap = std::max(1, n_params) * (int)p->local.size();
   PCK(cudaMalloc(&p->d_pack, 2 * sizeof(PackEntry) * p->pack_cap));   // [pack | unpack]
   PCK(cudaHostAlloc(&p->h_pack, 2 * sizeof(PackEntry) * p->pack_cap, cudaHostAllocDefault));
@@ -1263,7 +1283,10 @@ paro_status_t step_impl(PlanT* p, const void* const* grads, void* const* params,
                                 (pl.opt.predivide ? 1.0 : (double)pl.N));
   aa.s_g = (float)sg_base;
   aa.nonfinite = p->d_nonfinite;
+  aa.moved = ctx->mode == MODE_REAL ? p->d_moved : nullptr;
 
+  CK(cudaMemsetAsync(p->d_moved, 0, 2 * sizeof(unsigned long long), S));   // moved bytes of this step
+  p->moved_host[0] = p->moved_host[1] = 0;
   CK(cudaEventRecord(p->ev_fork, S));
   CK(cudaStreamWaitEvent(ctx->comm, p->ev_fork, 0));
   CK(cudaStreamWaitEvent(ctx->comp, p->ev_fork, 0));
@@ -1312,12 +1335,17 @@ paro_status_t step_impl(PlanT* p, const void* const* grads, void* const* params,
       sg.gnin = (int)gin.size();
       sg.graw = 0;
       sg.gf32 = 0;
+      sg.gpeer = sg.ginter = sg.pinter = 0;
       sg.gwide = pl.opt.wire == 4 ? 1 : 0;
       for (int i = 0; i < sg.gnin; ++i) {
         const Ref& x = gin[i];
         sg.gin[i] = reinterpret_cast<const uint16_t*>(data_ptr(p, x.rank, x.kind, x.off));
         if (x.is_raw()) sg.graw |= 1u << i;
         else if (pl.esz[x.kind] == 4) sg.gf32 |= 1u << i;
+        if (x.rank != r) {
+          sg.gpeer |= 1u << i;
+          if (x.rank / pl.M != r / pl.M) sg.ginter |= 1u << i;
+        }
       }
       sg.master = opt_state[li].master + S0.os_off[r];
       sg.m = opt_state[li].m + S0.os_off[r];
@@ -1327,8 +1355,10 @@ paro_status_t step_impl(PlanT* p, const void* const* grads, void* const* params,
       sg.in_norm = (uniq && (norm_only || !two)) ? 1 : 0;
       sg.npush = 0;
       if (!S0.param_push.empty())
-        for (const Ref& x : S0.param_push[r])
+        for (const Ref& x : S0.param_push[r]) {
+          if (x.rank / pl.M != r / pl.M) sg.pinter |= 1u << sg.npush;
           sg.push[sg.npush++] = reinterpret_cast<uint16_t*>(data_ptr(p, x.rank, x.kind, x.off));
+        }
     }
     aa.partials = p->d_partials + (int64_t)n_adam * grid;
     if (norm_only) {
@@ -1887,6 +1917,13 @@ paro_status_t paro_step_stats(paro_plan_t p, paro_step_stats_t* out) {
   out->sent_intra = p->last_step_acc ? p->pl->accstep_send_intra[me] : p->pl->send_intra[me];
   out->sent_inter = p->last_step_acc ? p->pl->accstep_send_inter[me] : p->pl->send_inter[me];
   out->kernel_launches = p->last_launches;
+  out->moved_intra = out->moved_inter = -1;
+  if (ctx->mode == MODE_REAL && p->pl->opt.topology != PARO_TOPO_NCCL) {
+    unsigned long long mv[2] = {0, 0};
+    CK(cudaMemcpy(mv, p->d_moved, sizeof(mv), cudaMemcpyDeviceToHost));
+    out->moved_intra = (int64_t)mv[0] + p->moved_host[0];
+    out->moved_inter = (int64_t)mv[1] + p->moved_host[1];
+  }
   return PARO_OK;
 }
 

@@ -17,6 +17,7 @@ namespace {
 
 constexpr int64_t kQuantum = 64;      // elements per shard granule (R21)
 constexpr int64_t kAlignElems = 128;  // 256-byte alignment of buffer kinds
+constexpr int64_t kOneRoundExtraBytes = int64_t(6) << 20;   // one-shot AR: extra bytes worth one barrier
 
 int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
@@ -930,7 +931,12 @@ void Planner::build_schedule() {
     };
     // G in {N, G}: world RS (+ AG_E / world AG of g_hat for OS = I / N)
     auto emit_world_reduce = [&](Launch& L) {
-      if (topo == 6 && OS == LV_N) {   // one-shot all-reduce: every rank folds every segment, one round
+      // one-shot all-reduce: every rank folds every segment in one round, reading
+      // (N-1) B instead of the 2(N-1)/N B of one-shot RS + AG (two rounds); worth
+      // it while the extra bytes cost less than a barrier (~10 us ~ 6 MB of
+      // NVLink): always at N = 2 (equal bytes), small buckets otherwise
+      const int64_t extra = (int64_t)(N - 1) * (N - 2) * n * opt.wire / N;
+      if (topo == 6 && OS == LV_N && (N == 2 || extra <= kOneRoundExtraBytes)) {
         for (int r = 0; r < N; ++r)
           for (int k = 0; k < N; ++k) L.add(0, r, oneshot_task(k, at(ghat_base(r), int64_t(k) * C)));
         return;

@@ -66,7 +66,8 @@ class paro_plan_info_t(C.Structure):
 
 class paro_step_stats_t(C.Structure):
     _fields_ = [("grad_norm", C.c_double), ("nonfinite", C.c_int32), ("sent_intra", C.c_int64),
-                ("sent_inter", C.c_int64), ("kernel_launches", C.c_int32)]
+                ("sent_inter", C.c_int64), ("kernel_launches", C.c_int32), ("moved_intra", C.c_int64),
+                ("moved_inter", C.c_int64)]
 
 
 class paro_profile_t(C.Structure):

@@ -367,3 +367,25 @@ def test_oneshot_topology_rounds_and_bytes(N, M):
     with pytest.raises(paro.ParoError, match="pull-only"):
         paro.Plan(ctx, "IIG", sizes, topology="oneshot", transport="push")
     ctx.close()
+
+
+@pytest.mark.parametrize("N,M", [(8, 4), (4, 2), (8, 1), (2, 1)])
+def test_oneshot_allreduce_one_or_two_rounds(N, M):
+    """One-shot NNN all-reduce: one round ((N-1)B read per rank) while the extra
+    bytes over one-shot RS + AG (two rounds, 2(N-1)/N B, the ring's volume) stay
+    under ~6 MB (a barrier's worth of NVLink time), always at N = 2; two rounds
+    with the ring's bytes for larger buckets."""
+    ctx = paro.Context(N, M)
+    for B in (N * 64 * 8, N * 64 * (1 << 14)):
+        pl = paro.Plan(ctx, "NNN", [2 * B], bucket_elems=B, topology="oneshot", fuse_allreduce=False)
+        info = pl.info()
+        C = B // N
+        one = N == 2 or (N - 1) * (N - 2) * B * 2 // N <= 6 << 20
+        if one:
+            want = (2 * (M - 1) * B * 2, 2 * (N - M) * B * 2)
+        else:
+            want = (2 * 2 * (M - 1) * C * 2, 2 * 2 * (N - M) * C * 2)
+        assert (info["step_send_bytes_intra"], info["step_send_bytes_inter"]) == want, (B, one)
+        assert info["n_rounds"] == 2 * (1 if one else 2)
+        pl.close()
+    ctx.close()

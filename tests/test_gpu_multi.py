@@ -135,6 +135,10 @@ def test_real_ranks_match_oracle(tmp_path, variant):
                     assert np.array_equal(d["v"], ST.shard_of(v, lay, code[2], rank)), tag
                     assert np.array_equal(d["param"], ST.shard_of(p, lay, code[0], rank)), tag
                     assert abs(meta["stats"]["grad_norm"] ** 2 - norm) <= 1e-12 * norm, tag
+                    # NVLink bytes counted on the device by the kernels that moved them equal the
+                    # plan's per-rank transfer list (rank-symmetric schedules; Table 3 accounting)
+                    st_ = meta["stats"]
+                    assert (st_["moved_intra"], st_["moved_inter"]) == (st_["sent_intra"], st_["sent_inter"]), tag
                     if "full" in d:      # forward/backward parameter gather: the full bf16 model
                         assert np.array_equal(d["full"], p), tag
                     if mask:             # frozen tensors: untouched residency, full windows
