@@ -49,15 +49,20 @@ def main():
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
 
+    host_us = {}
+
     def timeit(fn):
+        import time
         for _ in range(3):
             fn()
         torch.cuda.synchronize()
         dist.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
+        t0 = time.perf_counter()
         for _ in range(a.iters):
             fn()
+        host_us["last"] = (time.perf_counter() - t0) * 1e6 / a.iters   # enqueue cost per call (host)
         e1.record(stream)
         torch.cuda.synchronize()
         ms = torch.tensor([e0.elapsed_time(e1) / a.iters], dtype=torch.float64, device="cuda")
@@ -79,7 +84,8 @@ def main():
                            inter_gbps=a.inter_gbps, fuse_gather="never", fuse_allreduce=False)
             pl.synth_grads(rank, 1234, 1)
             ms = timeit(lambda: pl.collective(what))
-            row[topo] = {"ms": round(ms, 4), "busbw_GBps": round(nbytes * factor / (ms / 1e3) / 1e9, 1)}
+            row[topo] = {"ms": round(ms, 4), "busbw_GBps": round(nbytes * factor / (ms / 1e3) / 1e9, 1),
+                         "host_us_per_call": round(host_us["last"], 2)}
             if a.trace:
                 pl.profile_start(64)
                 for _ in range(4):
