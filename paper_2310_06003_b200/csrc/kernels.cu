@@ -124,7 +124,7 @@ __device__ __forceinline__ void st_release_gpu(unsigned long long* p, unsigned l
 // transitive across the gpu-scope and sys-scope synchronisations).  Measured:
 // 1 MiB all-reduce at 2 GPUs 44 -> 37 us, 1 GiB unchanged (profiles/r01).
 // Returns false (and leaves a sticky error word) on timeout.
-__device__ bool grid_peer_barrier(const RoundsArgs& a, uint64_t peers, int bidx, int narr) {
+__device__ bool grid_peer_barrier(const RoundsArgs& a, uint64_t peers, int bidx, int narr, uint64_t gen0) {
   __shared__ int s_ok;
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -132,9 +132,9 @@ __device__ bool grid_peer_barrier(const RoundsArgs& a, uint64_t peers, int bidx,
     volatile int* err = a.bar.err;
     if (a.sys_fence_all) __threadfence_system();   // remote NVLink stores visible system-wide
     else __threadfence();
-    const unsigned long long target = a.arrive_base + (unsigned long long)(narr + 1) * gridDim.x;
+    const unsigned long long target = (unsigned long long)(narr + 1) * gridDim.x;
     const unsigned long long old = atomicAdd(a.bar.arrive, 1ull);
-    const uint64_t val = a.serial * 256ull + (uint64_t)bidx + 1ull;
+    const uint64_t val = gen0 * 256ull + (uint64_t)bidx + 1ull;
     const uint64_t t0 = globaltimer();
     if (old + 1 == target) {          // last CTA of this GPU: publish to peers, wait for them
       // release pattern: one fence.acq_rel.sys, then relaxed sys-scope flag stores
@@ -168,12 +168,12 @@ __device__ bool grid_peer_barrier(const RoundsArgs& a, uint64_t peers, int bidx,
 // relaxed flag stores), waits for their flags and opens `go` for the others.
 // Removes the arrival of every CTA (and their launch skew) from the critical
 // path of latency-bound launches.
-__device__ bool entry_barrier(const RoundsArgs& a, uint64_t peers, int bidx) {
+__device__ bool entry_barrier(const RoundsArgs& a, uint64_t peers, int bidx, uint64_t gen0) {
   __shared__ int s_ok;
   if (threadIdx.x == 0) {
     int ok = 1;
     volatile int* err = a.bar.err;
-    const uint64_t val = a.serial * 256ull + (uint64_t)bidx + 1ull;
+    const uint64_t val = gen0 * 256ull + (uint64_t)bidx + 1ull;
     const uint64_t t0 = globaltimer();
     if (blockIdx.x == 0) {
       asm volatile("fence.acq_rel.sys;" ::: "memory");
@@ -199,12 +199,32 @@ __device__ bool entry_barrier(const RoundsArgs& a, uint64_t peers, int bidx) {
   return s_ok != 0;
 }
 
-// barrier k of a launch (bidx counts every barrier, narr the grid arrivals)
-__device__ __forceinline__ bool launch_barrier(const RoundsArgs& a, uint64_t peers, int& bidx, int& narr) {
-  const bool ok = (bidx == 0 && a.entry_fast) ? entry_barrier(a, peers, bidx)
-                                              : grid_peer_barrier(a, peers, bidx, narr++);
+// barrier k of a launch (bidx counts every barrier, narr the grid arrivals);
+// barrier values are gen0 * 256 + k + 1, gen0 = the channel's launch generation
+__device__ __forceinline__ bool launch_barrier(const RoundsArgs& a, uint64_t peers, int& bidx, int& narr,
+                                               uint64_t gen0) {
+  const bool ok = (bidx == 0 && a.entry_fast) ? entry_barrier(a, peers, bidx, gen0)
+                                              : grid_peer_barrier(a, peers, bidx, narr++, gen0);
   ++bidx;
   return ok;
+}
+
+// the channel's launch generation, read by every CTA at start: the previous
+// launch on this channel (same stream) has exited, so the value is stable
+__device__ __forceinline__ uint64_t launch_gen(const RoundsArgs& a) {
+  return a.bar.gen ? *reinterpret_cast<volatile unsigned long long*>(a.bar.gen) : 0ull;
+}
+
+// the last CTA to exit resets the arrival counter and advances the generation
+// (every CTA has read it and passed every barrier by then)
+__device__ __forceinline__ void launch_exit(const RoundsArgs& a, uint64_t gen0) {
+  if (!a.bar.my_flags || threadIdx.x != 0) return;
+  __threadfence();
+  if (atomicAdd(a.bar.exitc, 1u) + 1u == gridDim.x) {
+    atomicExch(a.bar.arrive, 0ull);
+    atomicExch(a.bar.exitc, 0u);
+    atomicExch(a.bar.gen, (unsigned long long)(gen0 + 1));
+  }
 }
 
 // NVLink bytes of one task / tile, split by link class: every peer input is
@@ -352,10 +372,11 @@ __global__ void __maxnreg__(48) rounds_kernel(const RoundsArgs a) {
   if (a.bar.err && *(volatile int*)a.bar.err) return;   // sticky device error: do nothing
   int bidx = 0, narr = 0;
   unsigned long long mi = 0, me = 0;
+  const uint64_t gen0 = launch_gen(a);
   trace_stamp(a, 0);
   for (int r = 0; r < a.nrounds; ++r) {
     const DRound rd = a.rounds[r];
-    if (a.bar.my_flags && !launch_barrier(a, rd.peers_before, bidx, narr)) return;
+    if (a.bar.my_flags && !launch_barrier(a, rd.peers_before, bidx, narr, gen0)) return;
     trace_stamp(a, 1 + 2 * r);
     for (int ti = rd.t0; ti < rd.t1; ++ti) {
       run_task(a.tasks + ti, a.alpha);
@@ -364,8 +385,9 @@ __global__ void __maxnreg__(48) rounds_kernel(const RoundsArgs a) {
     __syncthreads();
     trace_stamp(a, 2 + 2 * r);
   }
-  if (a.bar.my_flags && a.final_barrier) launch_barrier(a, a.final_peers, bidx, narr);
+  if (a.bar.my_flags && a.final_barrier && !launch_barrier(a, a.final_peers, bidx, narr, gen0)) return;
   if (threadIdx.x == 0) flush_moved(a.moved, mi, me);
+  launch_exit(a, gen0);
   trace_stamp(a, kTraceSlots - 1);
 }
 
@@ -901,10 +923,11 @@ __global__ void __launch_bounds__(kRtThreads, 4) rounds_tma_kernel(const RoundsA
   uint32_t cnt = 0;   // tiles this CTA has consumed so far (stage = cnt % S, parity = cnt / S)
   int bidx = 0, narr = 0;
   unsigned long long mi = 0, me = 0;   // NVLink bytes of the tiles this CTA issued (thread 0)
+  const uint64_t gen0 = launch_gen(a);
   trace_stamp(a, 0);
   for (int r = 0; r < a.nrounds; ++r) {
     const DRound rd = a.rounds[r];
-    if (a.bar.my_flags && !launch_barrier(a, rd.peers_before, bidx, narr)) return;
+    if (a.bar.my_flags && !launch_barrier(a, rd.peers_before, bidx, narr, gen0)) return;
     // order the peers' released (generic-proxy) writes before our async-proxy reads
     if (threadIdx.x == 0) asm volatile("fence.proxy.async;" ::: "memory");
     trace_stamp(a, 1 + 2 * r);
@@ -999,8 +1022,9 @@ __global__ void __launch_bounds__(kRtThreads, 4) rounds_tma_kernel(const RoundsA
     __syncthreads();
     trace_stamp(a, 2 + 2 * r);
   }
-  if (a.bar.my_flags && a.final_barrier) launch_barrier(a, a.final_peers, bidx, narr);
+  if (a.bar.my_flags && a.final_barrier && !launch_barrier(a, a.final_peers, bidx, narr, gen0)) return;
   if (threadIdx.x == 0) flush_moved(a.moved, mi, me);
+  launch_exit(a, gen0);
   trace_stamp(a, kTraceSlots - 1);
 }
 

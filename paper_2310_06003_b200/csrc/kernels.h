@@ -43,14 +43,20 @@ struct DRound {
   uint64_t peers_before; // barrier peer mask before this round (real mode)
 };
 
-// Region header layout (bytes): [0, 512) uint64 flags[64] indexed by sender;
-// [512] uint64 arrive counter; [520] int32 error word.
+// Region header layout (bytes), channel 0 (collective launches): [0, 512) uint64
+// flags[64] indexed by sender; [512] arrive; [520] int32 error word; [528] go;
+// [536] launch generation; [544] exit count.  Channel 2 (copy-engine barriers)
+// at [1024, 1536) flags, [1536] arrive, [1544] go, [1552] generation, [1560] exit.
 struct BarrierCtx {
   uint64_t* const* peer_slot;   // [N] device array: &flags_of_peer_x[me]
   uint64_t* my_flags;           // NULL => emulated mode (no barriers)
-  unsigned long long* arrive;
+  unsigned long long* arrive;   // grid arrivals of the running launch (reset to 0 when it exits)
   unsigned long long* go;       // opened by the last-arriving CTA once the peers' flags are in
   int* err;
+  unsigned long long* gen;      // launch generation of this channel: every launch reads it at start
+                                // and the last CTA to exit advances it (device-resident, so
+                                // launches need no host bookkeeping and can be graph-replayed)
+  unsigned int* exitc;          // CTAs of the running launch that have exited
 };
 
 constexpr int kTraceSlots = 64;   // per CTA per traced launch: start, (barrier exit, work end) x rounds, end
@@ -64,8 +70,7 @@ struct RoundsArgs {
   uint64_t final_peers;
   float alpha;
   double inter_bytes_per_ns;    // per-CTA pacing of inter-group tiles (0 = off)
-  uint64_t serial;              // launch serial (same sequence on every rank)
-  unsigned long long arrive_base;
+
   int sys_fence_all;            // every CTA fences at sys scope (launch stores into peer memory)
   int entry_fast;               // the launch's first barrier (no work of this launch before it) is
                                 // published by CTA 0 alone, without the grid arrival

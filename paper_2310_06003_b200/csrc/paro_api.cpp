@@ -92,8 +92,6 @@ struct paro_plan {
   std::vector<char*> peer_base;           // [N] base as addressable from this process
   uint64_t** d_peer_slot = nullptr;       // real mode
   uint64_t** d_peer_slot2 = nullptr;      // second barrier channel (copy-engine launches)
-  uint64_t serial2 = 1;
-  unsigned long long arrive_base2 = 0;
   cudaEvent_t ev_dma = nullptr;
   DRound* d_rounds = nullptr;
   DTask* d_tasks = nullptr;
@@ -117,8 +115,6 @@ struct paro_plan {
   cudaEvent_t ev_fork = nullptr, ev_comm = nullptr, ev_comp = nullptr, ev_pack_staged = nullptr,
               ev_unpack_staged = nullptr;
   std::vector<cudaEvent_t> ev_red, ev_adam;
-  uint64_t serial = 1;
-  unsigned long long arrive_base = 0;
   cudaStream_t last_stream = nullptr;
   int last_launches = 0;
   bool stepped = false;
@@ -489,15 +485,14 @@ paro_status_t barrier2(PlanT* p, uint64_t peers, cudaStream_t s, int* nlaunch) {
   a.nrounds = 0;
   a.final_barrier = 1;
   a.final_peers = peers;
-  a.serial = p->serial2++;
-  a.arrive_base = p->arrive_base2;
   a.entry_fast = entry_fast_on() ? 1 : 0;
   a.bar.peer_slot = p->d_peer_slot2;
   a.bar.my_flags = reinterpret_cast<uint64_t*>(hdr + 1024);
   a.bar.arrive = reinterpret_cast<unsigned long long*>(hdr + 1536);
   a.bar.go = reinterpret_cast<unsigned long long*>(hdr + 1544);
   a.bar.err = reinterpret_cast<int*>(hdr + 520);
-  p->arrive_base2 += a.entry_fast ? 0 : 1;
+  a.bar.gen = reinterpret_cast<unsigned long long*>(hdr + 1552);
+  a.bar.exitc = reinterpret_cast<unsigned int*>(hdr + 1560);
   CK(launch_rounds(a, 1, 32, s));
   ++*nlaunch;
   return PARO_OK;
@@ -545,8 +540,6 @@ paro_status_t run_launch(PlanT* p, const DevLaunch& dl, int* nlaunch) {
     a.nrounds = dl.nrounds;
     a.final_barrier = dl.final_barrier;
     a.final_peers = dl.final_peers;
-    a.serial = p->serial++;
-    a.arrive_base = p->arrive_base;
     a.entry_fast = entry_fast_on() ? 1 : 0;
     a.moved = p->d_moved;
     a.bar.peer_slot = p->d_peer_slot;
@@ -554,9 +547,9 @@ paro_status_t run_launch(PlanT* p, const DevLaunch& dl, int* nlaunch) {
     a.bar.arrive = reinterpret_cast<unsigned long long*>(hdr + 512);
     a.bar.go = reinterpret_cast<unsigned long long*>(hdr + 528);
     a.bar.err = reinterpret_cast<int*>(hdr + 520);
+    a.bar.gen = reinterpret_cast<unsigned long long*>(hdr + 536);
+    a.bar.exitc = reinterpret_cast<unsigned int*>(hdr + 544);
     a.sys_fence_all = p->pl->opt.push ? 1 : 0;
-    // grid arrivals this launch adds to the counter (the first barrier has none when entry_fast)
-    p->arrive_base += (unsigned long long)(dl.nrounds + dl.final_barrier - a.entry_fast) * grid;
     const int k = prof_begin(p, ctx->comm, 1, dl.bytes, dl.hbm);
     if (p->prof && p->d_trace && (int)p->trace_nrounds.size() < kTraceLaunches) {
       a.trace = p->d_trace + (size_t)p->trace_nrounds.size() * ctx->sm_count * kTraceSlots;

@@ -144,3 +144,28 @@ def test_real_ranks_match_oracle(tmp_path, variant):
                     if mask:             # frozen tensors: untouched residency, full windows
                         assert np.array_equal(d["frozen_param"], ST.shard_of(p_frozen, lay_f, code[0], rank)), tag
                         assert np.array_equal(d["frozen_full"], p_frozen), tag
+
+
+@pytest.mark.skipif(_ngpu() < 2, reason="needs >= 2 GPUs")
+def test_collective_graph_replay(tmp_path):
+    """The peer barriers keep their state on the device (per-channel launch
+    generation advanced by each launch's last CTA), so collective launches can
+    be captured once in a CUDA graph and replayed, also between eager calls:
+    every replay's all-reduce equals the oracle (HO-Ring and one-shot)."""
+    world = _ngpu()
+    M = world // 2 if world >= 4 else 1
+    B = world * 64 * 32
+    cfg = {"M": M, "bucket": B, "topos": ["ho", "oneshot"], "per_graph": 3, "replays": 4}
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr=127.0.0.1", "--master-port=29519", os.path.join(ROOT, "tests", "graph_worker.py"),
+           str(tmp_path), json.dumps(cfg)]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    lay = L.Layout([3 * B], world, M, B)
+    gh = ST.dp_reduce(lay, [grad_bits(r_, 1, 0, lay.psi) for r_ in range(world)])
+    for topo in cfg["topos"]:
+        for rank in range(world):
+            for k in range(cfg["replays"]):
+                got = np.load(tmp_path / f"{topo}_r{rank}_k{k}.npy")
+                for b, (s0, n) in enumerate(lay.buckets):   # bucket b's average in slot b % 3
+                    assert np.array_equal(got[b * B:b * B + n], gh[s0:s0 + n]), (topo, rank, k, b)
