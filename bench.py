@@ -613,6 +613,31 @@ def allreduce_sweep(paro, ctx, stream, dist, world, M, rank, args, sizes_mib=SWE
         dist.all_reduce(ms, op=dist.ReduceOp.MAX)
         return float(ms.item())
 
+    def graph_time(fn, inner, reps=5):
+        """Per-call device time of `inner` calls captured in one CUDA graph (no host
+        launch overhead in the timed region), max over ranks."""
+        fn()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            for _ in range(inner):
+                fn()
+        torch.cuda.synchronize()
+        dist.barrier()
+        g.replay()
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            g.replay()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        del g
+        ms = torch.tensor([e0.elapsed_time(e1) / (reps * inner)], dtype=torch.float64, device="cuda")
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        return float(ms.item())
+
     rows = []
     for mib in sizes_mib:
         nbytes = mib << 20
@@ -627,16 +652,32 @@ def allreduce_sweep(paro, ctx, stream, dist, world, M, rank, args, sizes_mib=SWE
                            comm_impl=args.comm_impl, fuse_gather="never", fuse_allreduce=False)
             pl.synth_grads(rank, SEED, 1)
             ms = timeit(lambda: pl.collective(0), iters)
-            pl.close()
             bw = nbytes * factor / (ms / 1e3) / 1e9
             row[topo] = {"us": round(ms * 1e3, 2), "busbw_GBps": round(bw, 1), "frac": round(bw / peak, 4)}
             if bw / peak > 1.2:
                 row[topo]["error"] = "busbw above 1.2 x the 770 GB/s peak: the timed launches do not do the work"
+            if topo == "oneshot" and nbytes <= (64 << 20):
+                try:   # the same calls captured in a CUDA graph (device-resident barrier state)
+                    gms = graph_time(lambda: pl.collective(0), 20)
+                    gbw = nbytes * factor / (gms / 1e3) / 1e9
+                    row["oneshot_graph"] = {"us": round(gms * 1e3, 2), "busbw_GBps": round(gbw, 1),
+                                            "frac": round(gbw / peak, 4)}
+                except Exception as e:  # noqa: BLE001
+                    row["oneshot_graph"] = {"error": repr(e)[:200]}
+            pl.close()
         x = torch.ones(elems, dtype=torch.bfloat16, device="cuda")
         ms = timeit(lambda: dist.all_reduce(x), iters)
-        del x
         bw = nbytes * factor / (ms / 1e3) / 1e9
         row["nccl"] = {"us": round(ms * 1e3, 2), "busbw_GBps": round(bw, 1), "frac": round(bw / peak, 4)}
+        if nbytes <= (64 << 20):
+            try:
+                gms = graph_time(lambda: dist.all_reduce(x), 20)
+                gbw = nbytes * factor / (gms / 1e3) / 1e9
+                row["nccl_graph"] = {"us": round(gms * 1e3, 2), "busbw_GBps": round(gbw, 1),
+                                     "frac": round(gbw / peak, 4)}
+            except Exception as e:  # noqa: BLE001
+                row["nccl_graph"] = {"error": repr(e)[:200]}
+        del x
         lib = [t for t in ("ho", "flat", "oneshot") if t in row and "error" not in row[t]]
         row["library_best"] = max(lib, key=lambda t: row[t]["busbw_GBps"]) if lib else None
         rows.append(row)
