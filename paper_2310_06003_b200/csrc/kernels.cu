@@ -573,6 +573,27 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                : "memory");
 }
 
+// the same copies with an L2 eviction-priority policy (createpolicy; evict_first
+// for operands Adam reads or writes exactly once)
+__device__ __forceinline__ uint64_t l2_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                              uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_s2g_hint(void* dst, const void* src, uint32_t bytes, uint64_t pol) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(dst),
+               "r"(smem_u32(src)), "r"(bytes), "l"(pol)
+               : "memory");
+}
+
 __device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
                "r"(bytes)
@@ -657,9 +678,16 @@ __global__ void __maxnreg__(72) adam_tma_kernel(const AdamArgs a, int gnin_max, 
                (uint32_t)tr.n * es, &full_bar[s]);
     }
     unsigned char* fbase = base + gnin_max * g_bytes;
-    bulk_g2s(fbase, sg.master + tr.start, fb, &full_bar[s]);
-    bulk_g2s(fbase + f_bytes, sg.m + tr.start, fb, &full_bar[s]);
-    bulk_g2s(fbase + 2 * f_bytes, sg.v + tr.start, fb, &full_bar[s]);
+    if (a.l2_hint) {   // master / m / v: read once per step, evict first
+      const uint64_t pol = l2_evict_first();
+      bulk_g2s_hint(fbase, sg.master + tr.start, fb, &full_bar[s], pol);
+      bulk_g2s_hint(fbase + f_bytes, sg.m + tr.start, fb, &full_bar[s], pol);
+      bulk_g2s_hint(fbase + 2 * f_bytes, sg.v + tr.start, fb, &full_bar[s], pol);
+    } else {
+      bulk_g2s(fbase, sg.master + tr.start, fb, &full_bar[s]);
+      bulk_g2s(fbase + f_bytes, sg.m + tr.start, fb, &full_bar[s]);
+      bulk_g2s(fbase + 2 * f_bytes, sg.v + tr.start, fb, &full_bar[s]);
+    }
   };
   if (threadIdx.x == 0)
     for (int64_t k = 0; k < min((int64_t)stages, mine); ++k) issue(k);
@@ -737,9 +765,16 @@ __global__ void __maxnreg__(72) adam_tma_kernel(const AdamArgs a, int gnin_max, 
       if (threadIdx.x == 0) {
         const uint32_t gb = (uint32_t)tr.n * 2, fb = (uint32_t)tr.n * 4;
         const unsigned char* fbase = base + gnin_max * g_bytes;
-        bulk_s2g(sg.master + tr.start, fbase, fb);
-        bulk_s2g(sg.m + tr.start, fbase + f_bytes, fb);
-        bulk_s2g(sg.v + tr.start, fbase + 2 * f_bytes, fb);
+        if (a.l2_hint) {
+          const uint64_t pol = l2_evict_first();
+          bulk_s2g_hint(sg.master + tr.start, fbase, fb, pol);
+          bulk_s2g_hint(sg.m + tr.start, fbase + f_bytes, fb, pol);
+          bulk_s2g_hint(sg.v + tr.start, fbase + 2 * f_bytes, fb, pol);
+        } else {
+          bulk_s2g(sg.master + tr.start, fbase, fb);
+          bulk_s2g(sg.m + tr.start, fbase + f_bytes, fb);
+          bulk_s2g(sg.v + tr.start, fbase + 2 * f_bytes, fb);
+        }
         bulk_s2g(sg.param + tr.start, base, gb);
         for (int i = 0; i < sg.npush; ++i) bulk_s2g(sg.push[i] + tr.start, base, gb);
         bulk_commit();
