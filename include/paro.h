@@ -419,6 +419,23 @@ paro_status_t paro_step_streamed(paro_plan_t plan, paro_grad_producer_t producer
                                  int64_t grad_step, void* const* params, const paro_opt_state_t* opt_state,
                                  float lr, int64_t step);
 
+/* Parameter consumer: after paro_set_param_consumer, every paro_step /
+ * paro_step_streamed calls, for each bucket b in order and every local rank,
+ *   consumer(user, rank, b, begin, end, src, stream)
+ * from the calling host thread; it must enqueue, on `stream` (a cudaStream_t
+ * that waits until bucket b's updated bf16 parameters are final on this rank:
+ * after its restore, or its Adam when there is none, and with fused gathers
+ * after every peer's Adam of b), reads of the rank's P residency of the bucket:
+ * flat elements [begin, end) (paro_shard_range(P)), `end - begin` bf16 at src.
+ * The step completes (on its stream) only once these reads have.  Use: copy
+ * each bucket device->host while later buckets still reduce / update (and, in
+ * a streamed step, while their gradients come in: PCIe is full duplex).
+ * consumer NULL unregisters.  Errors: PARO_ERR_STATE on a planning-only
+ * context or a frozen-parameter plan. */
+typedef void (*paro_param_consumer_t)(void* user, int rank, int64_t bucket, int64_t begin, int64_t end,
+                                      const void* src, void* stream);
+paro_status_t paro_set_param_consumer(paro_plan_t plan, paro_param_consumer_t consumer, void* user);
+
 /* Gradient accumulation (§3.3; R27).  Adds one
  * micro-batch's gradients at the G residency: G = G reduces the micro-batch
  * over all ranks (HO-Ring RS), G = I inside the group (RS_I, P:353,

@@ -52,6 +52,7 @@ struct paro_ctx {
   int N = 1, M = 1, rank = 0, device = -1;
   cudaStream_t main = nullptr, comm = nullptr, comp = nullptr;
   cudaStream_t dma = nullptr;   // copy-engine transfers of pure-copy launches
+  cudaStream_t sink = nullptr;  // parameter consumer (paro_set_param_consumer): per-bucket reads
   ncclComm_t world = nullptr, intra = nullptr, inter = nullptr;
   paro_status_t sticky = PARO_OK;
   std::string sticky_msg;
@@ -92,6 +93,11 @@ struct paro_plan {
   std::vector<char*> peer_base;           // [N] base as addressable from this process
   uint64_t** d_peer_slot = nullptr;       // real mode
   uint64_t** d_peer_slot2 = nullptr;      // second barrier channel (copy-engine launches)
+  uint64_t** d_peer_slot3 = nullptr;      // third channel (parameter consumer stream)
+  paro_param_consumer_t cons_fn = nullptr;  // per-bucket consumer of the updated parameters
+  void* cons_user = nullptr;
+  cudaEvent_t ev_cons = nullptr;
+  std::vector<cudaEvent_t> ev_pfinal;     // bucket b's parameters final on this rank
   cudaEvent_t ev_dma = nullptr;
   DRound* d_rounds = nullptr;
   DTask* d_tasks = nullptr;
@@ -483,20 +489,22 @@ int env_flag(const char* name, int dflt) {
 }
 
 // 1-CTA peer barrier on the second channel (stream s), for copy-engine launches.
-paro_status_t barrier2(PlanT* p, uint64_t peers, cudaStream_t s, int* nlaunch) {
+// channel 2 (hdr + 1024: copy-engine launches, the gradient producer) or 3
+// (hdr + 2048: the parameter consumer); each channel's launches run on one stream
+paro_status_t barrier2(PlanT* p, uint64_t peers, cudaStream_t s, int* nlaunch, int channel = 2) {
   paro_ctx* ctx = p->ctx;
   if (ctx->mode != MODE_REAL || !peers) return PARO_OK;
-  char* hdr = p->region[0];
+  char* hdr = p->region[0] + (channel == 3 ? 1024 : 0);
   RoundsArgs a{};
   a.nrounds = 0;
   a.final_barrier = 1;
   a.final_peers = peers;
   a.entry_fast = entry_fast_on() ? 1 : 0;
-  a.bar.peer_slot = p->d_peer_slot2;
+  a.bar.peer_slot = channel == 3 ? p->d_peer_slot3 : p->d_peer_slot2;
   a.bar.my_flags = reinterpret_cast<uint64_t*>(hdr + 1024);
   a.bar.arrive = reinterpret_cast<unsigned long long*>(hdr + 1536);
   a.bar.go = reinterpret_cast<unsigned long long*>(hdr + 1544);
-  a.bar.err = reinterpret_cast<int*>(hdr + 520);
+  a.bar.err = reinterpret_cast<int*>(p->region[0] + 520);
   a.bar.gen = reinterpret_cast<unsigned long long*>(hdr + 1552);
   a.bar.exitc = reinterpret_cast<unsigned int*>(hdr + 1560);
   CK(launch_rounds(a, 1, 32, s));
@@ -660,6 +668,9 @@ void destroy_plan(PlanT* p) {
     for (char* r : p->region) cudaFree(r);
     cudaFree(p->d_peer_slot);
     cudaFree(p->d_peer_slot2);
+    cudaFree(p->d_peer_slot3);
+    if (p->ev_cons) cudaEventDestroy(p->ev_cons);
+    for (cudaEvent_t e : p->ev_pfinal) if (e) cudaEventDestroy(e);
     cudaFree(p->d_rounds);
     cudaFree(p->d_tasks);
     cudaFree(p->d_partials);
@@ -693,6 +704,7 @@ paro_status_t make_streams(paro_ctx* ctx) {
   CK(cudaStreamCreateWithPriority(&ctx->comm, cudaStreamNonBlocking, hi));  // collectives first
   CK(cudaStreamCreateWithFlags(&ctx->comp, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithPriority(&ctx->dma, cudaStreamNonBlocking, hi));
+  CK(cudaStreamCreateWithFlags(&ctx->sink, cudaStreamNonBlocking));
   return PARO_OK;
 }
 
@@ -822,7 +834,7 @@ paro_status_t paro_finalize(paro_ctx_t ctx) {
     if (ctx->intra) ncclCommDestroy(ctx->intra);
     if (ctx->inter) ncclCommDestroy(ctx->inter);
     if (ctx->world) ncclCommDestroy(ctx->world);
-    for (cudaStream_t s : {ctx->main, ctx->comm, ctx->comp, ctx->dma})
+    for (cudaStream_t s : {ctx->main, ctx->comm, ctx->comp, ctx->dma, ctx->sink})
       if (s) cudaStreamDestroy(s);
   }
   delete ctx;
@@ -946,6 +958,9 @@ paro_status_t paro_plan(paro_ctx_t ctx, const char* strategy, const int64_t* par
     for (int x = 0; x < N; ++x) slots[x] = reinterpret_cast<uint64_t*>(p->peer_base[x] + 1024) + ctx->rank;
     PCK(cudaMalloc(&p->d_peer_slot2, 64 * sizeof(uint64_t*)));
     PCK(cudaMemcpy(p->d_peer_slot2, slots.data(), 64 * sizeof(uint64_t*), cudaMemcpyHostToDevice));
+    for (int x = 0; x < N; ++x) slots[x] = reinterpret_cast<uint64_t*>(p->peer_base[x] + 2048) + ctx->rank;
+    PCK(cudaMalloc(&p->d_peer_slot3, 64 * sizeof(uint64_t*)));
+    PCK(cudaMemcpy(p->d_peer_slot3, slots.data(), 64 * sizeof(uint64_t*), cudaMemcpyHostToDevice));
   }
   {
     paro_status_t s2 = upload_schedule(p);
@@ -973,10 +988,13 @@ paro_status_t paro_plan(paro_ctx_t ctx, const char* strategy, const int64_t* par
   p->ev_adam.resize(nb);
   p->ev_pre.resize(nb);
   p->ev_prod.resize(nb);
+  p->ev_pfinal.resize(nb);
+  PCK(cudaEventCreateWithFlags(&p->ev_cons, cudaEventDisableTiming));
   for (int b = 0; b < nb; ++b) {
     PCK(cudaEventCreateWithFlags(&p->ev_red[b], cudaEventDisableTiming));
     PCK(cudaEventCreateWithFlags(&p->ev_pre[b], cudaEventDisableTiming));
     PCK(cudaEventCreateWithFlags(&p->ev_prod[b], cudaEventDisableTiming));
+    PCK(cudaEventCreateWithFlags(&p->ev_pfinal[b], cudaEventDisableTiming));
     PCK(cudaEventCreateWithFlags(&p->ev_adam[b], cudaEventDisableTiming));
   }
   PCK(cudaDeviceSynchronize());
@@ -1214,6 +1232,15 @@ paro_status_t step_impl(PlanT* p, const void* const* grads, void* const* params,
                         float lr, int64_t step, const GradSource* src);
 }  // namespace
 
+paro_status_t paro_set_param_consumer(paro_plan_t p, paro_param_consumer_t consumer, void* user) {
+  if (!p) return fail(PARO_ERR_INVALID, "null plan");
+  if (p->ctx->mode == MODE_PLANNER) return fail(PARO_ERR_STATE, "planning-only context");
+  if (p->pl->opt.params_only) return fail(PARO_ERR_STATE, "frozen-parameter plan has no step");
+  p->cons_fn = consumer;
+  p->cons_user = user;
+  return PARO_OK;
+}
+
 paro_status_t paro_step(paro_plan_t p, const void* const* grads, void* const* params,
                         const paro_opt_state_t* opt_state, float lr, int64_t step) {
   if (!p) return fail(PARO_ERR_INVALID, "null plan");
@@ -1444,6 +1471,36 @@ paro_status_t step_impl(PlanT* p, const void* const* grads, void* const* params,
     return PARO_OK;
   };
 
+  // parameter consumer (paro_set_param_consumer): bucket b's P residency handed
+  // to the caller on the sink stream as soon as it is final, so e.g. its
+  // device->host copy overlaps the later buckets' work (and, in a streamed
+  // step, their host->device gradients: PCIe is full duplex).  With fused
+  // gathers a peer's Adam writes into our parameters: a channel-3 barrier with
+  // every peer (each reaches it after its own Adam of the bucket) comes first.
+  auto consume = [&](int b) -> paro_status_t {
+    cudaStream_t cs = ctx->sink;
+    CK(cudaStreamWaitEvent(cs, p->ev_pfinal[b], 0));
+    if (!pl.sched[b].param_push.empty()) {
+      uint64_t peers = 0;
+      for (int x = 0; x < pl.N && ctx->mode == MODE_REAL; ++x)
+        if (x != ctx->rank) peers |= uint64_t(1) << x;
+      paro_status_t sb = barrier2(p, peers, cs, &launches, 3);
+      if (sb != PARO_OK) return sb;
+    }
+    for (int li = 0; li < nl; ++li) {
+      const int r = p->local[li];
+      int64_t b0, b1;
+      pl.residency(pl.P, r, b, &b0, &b1);
+      void* src = data_ptr(p, r, BUF_PARAM, pl.buckets[b].first / pl.divl(pl.P));
+      p->cons_fn(p->cons_user, r, b, b0, b1, src, cs);
+    }
+    CK(cudaGetLastError());
+    return PARO_OK;
+  };
+  // streamed step: bucket b's gradients go into slot b % K once every rank is
+  // done reading bucket b - K from it (its reduce and, unless two-phase, the
+  // Adam that may fold it): local events, then a peer barrier on the second
+  // channel, on the producer stream (ctx->dma; no copy-engine launches here)
   if (pl.N == 1 && !src) {
     if (two) {
       paro_status_t s1 = adam_bucket(0, nb, true);
@@ -1456,6 +1513,14 @@ paro_status_t step_impl(PlanT* p, const void* const* grads, void* const* params,
     }
     paro_status_t s2 = adam_bucket(0, nb);   // contiguous: one launch over all buckets
     if (s2 != PARO_OK) return s2;
+    if (p->cons_fn) {   // every bucket final with the one launch
+      for (int b = 0; b < nb; ++b) {
+        CK(cudaEventRecord(p->ev_pfinal[b], ctx->comp));
+        paro_status_t sc = consume(b);
+        if (sc != PARO_OK) return sc;
+      }
+      CK(cudaEventRecord(p->ev_cons, ctx->sink));
+    }
     if (!two) {
       paro_status_t s3 = norm_reduce();
       if (s3 != PARO_OK) return s3;
@@ -1463,6 +1528,7 @@ paro_status_t step_impl(PlanT* p, const void* const* grads, void* const* params,
   } else {
     const int D = std::max(1, p->opts.pipeline_depth);
     const bool nccl = pl.opt.topology == PARO_TOPO_NCCL;
+    const int me = ctx->mode == MODE_REAL ? ctx->rank : 0;
     bool dma_used = false;
     // copy-engine raw-chunk copies of bucket b into landing set b % kStageSets
     // (after the step-start barrier; set reuse waits for the reduce that read it)
@@ -1482,28 +1548,30 @@ paro_status_t step_impl(PlanT* p, const void* const* grads, void* const* params,
         if (st != PARO_OK) return st;
       }
     }
+    // bucket b's parameters are final on this rank once its restore ran (or its
+    // Adam, when there is no gather launch); ev_pfinal[b] marks that point
     auto do_gather = [&](int b) -> paro_status_t {
       NvtxRange nr("paro gather b%d", b);
       if (p->gat[b].dma) {   // copy engines, off the comm stream: overlaps the next reductions
         CK(cudaStreamWaitEvent(ctx->dma, p->ev_adam[b], 0));
         dma_used = true;
-        return run_dma_launch(p, p->gat[b], ctx->dma, &launches);
+        paro_status_t sd = run_dma_launch(p, p->gat[b], ctx->dma, &launches);
+        if (sd == PARO_OK && p->cons_fn) CK(cudaEventRecord(p->ev_pfinal[b], ctx->dma));
+        return sd;
       }
       CK(cudaStreamWaitEvent(ctx->comm, p->ev_adam[b], 0));
+      paro_status_t s3 = PARO_OK;
       if (nccl) {
         const int k = prof_begin(p, ctx->comm, 1, 0);
-        paro_status_t s3 = run_nccl(p, pl.sched[b].nccl_gather[ctx->rank]);
+        s3 = run_nccl(p, pl.sched[b].nccl_gather[ctx->rank]);
         prof_end(p, ctx->comm, k);
-        if (s3 != PARO_OK) return s3;
-        if (!pl.sched[b].nccl_gather[ctx->rank].empty()) ++launches;
-        return PARO_OK;
+        if (s3 == PARO_OK && !pl.sched[b].nccl_gather[ctx->rank].empty()) ++launches;
+      } else {
+        s3 = run_launch(p, p->gat[b], &launches);
       }
-      return run_launch(p, p->gat[b], &launches);
+      if (s3 == PARO_OK && p->cons_fn) CK(cudaEventRecord(p->ev_pfinal[b], ctx->comm));
+      return s3;
     };
-    // streamed step: bucket b's gradients go into slot b % K once every rank is
-    // done reading bucket b - K from it (its reduce and, unless two-phase, the
-    // Adam that may fold it): local events, then a peer barrier on the second
-    // channel, on the producer stream (ctx->dma; no copy-engine launches here)
     auto produce = [&](int b) -> paro_status_t {
       cudaStream_t ps = ctx->dma;
       const int K = pl.opt.grad_slots;
@@ -1588,6 +1656,8 @@ paro_status_t step_impl(PlanT* p, const void* const* grads, void* const* params,
       paro_status_t s4 = adam_bucket(b, b + 1);
       if (s4 != PARO_OK) return s4;
       CK(cudaEventRecord(p->ev_adam[b], ctx->comp));
+      if (p->cons_fn && p->gat[b].nrounds == 0 && !p->gat[b].dma && (!nccl || pl.sched[b].nccl_gather[me].empty()))
+        CK(cudaEventRecord(p->ev_pfinal[b], ctx->comp));   // no restore launch: final after Adam
       if (b >= D) {
         paro_status_t s5 = do_gather(b - D);
         if (s5 != PARO_OK) return s5;
@@ -1596,6 +1666,13 @@ paro_status_t step_impl(PlanT* p, const void* const* grads, void* const* params,
     for (int b = std::max(0, nb - D); b < nb; ++b) {
       paro_status_t s5 = do_gather(b);
       if (s5 != PARO_OK) return s5;
+    }
+    if (p->cons_fn) {   // in bucket order, each as soon as its parameters are final
+      for (int b = 0; b < nb; ++b) {
+        paro_status_t sc = consume(b);
+        if (sc != PARO_OK) return sc;
+      }
+      CK(cudaEventRecord(p->ev_cons, ctx->sink));
     }
     if (dma_used) {   // the step-end barrier comes after every copy-engine transfer
       CK(cudaEventRecord(p->ev_dma, ctx->dma));
@@ -1648,6 +1725,7 @@ paro_status_t step_impl(PlanT* p, const void* const* grads, void* const* params,
   }
   CK(cudaEventRecord(p->ev_comm, ctx->comm));
   CK(cudaStreamWaitEvent(S, p->ev_comm, 0));
+  if (p->cons_fn) CK(cudaStreamWaitEvent(S, p->ev_cons, 0));   // the step includes the consumption
   p->last_stream = S;
   p->last_launches = launches;
   p->stepped = true;

@@ -137,6 +137,8 @@ PRODUCER = C.CFUNCTYPE(None, C.c_void_p, C.c_int, _i64, _i64, _i64, C.c_void_p, 
 paro_step_streamed = _sig("paro_step_streamed", _st, _vp, PRODUCER, C.c_void_p, C.c_uint64, _i64, C.POINTER(_vp),
                           C.POINTER(paro_opt_state_t), C.c_float, _i64)
 paro_accumulate = _sig("paro_accumulate", _st, _vp, C.POINTER(_vp))
+CONSUMER = C.CFUNCTYPE(None, C.c_void_p, C.c_int, _i64, _i64, _i64, C.c_void_p, C.c_void_p)
+paro_set_param_consumer = _sig("paro_set_param_consumer", _st, _vp, CONSUMER, C.c_void_p)
 paro_step_stats = _sig("paro_step_stats", _st, _vp, C.POINTER(paro_step_stats_t))
 paro_plan_destroy = _sig("paro_plan_destroy", _st, _vp)
 paro_collective = _sig("paro_collective", _st, _vp, C.c_int)
@@ -156,7 +158,7 @@ EXPORTED = ["paro_opts_default", "paro_get_unique_id", "paro_init", "paro_init_e
             "paro_profile_stop", "paro_collective", "paro_accumulate",
             "paro_rank_accum_send_bytes", "paro_gather_window", "paro_rank_gather_send_bytes",
             "paro_table1_column", "paro_advise", "paro_plan_masked", "paro_step_streamed",
-            "paro_bucket_gather_send_bytes"]
+            "paro_bucket_gather_send_bytes", "paro_set_param_consumer"]
 
 
 def check(status):
@@ -363,6 +365,17 @@ class Plan:
         self._producer_ref = cb      # kept alive: the library calls it from this thread during the call
         check(paro_step_streamed(self.h, cb, None, int(seed or 0), int(grad_step or 0), pp, sts, float(lr),
                                  int(step)))
+
+    def set_param_consumer(self, consumer):
+        """paro_set_param_consumer: consumer(rank, bucket, begin, end, src_ptr, stream_ptr) enqueues reads of
+        bucket `bucket`'s updated bf16 parameters (the rank's P residency [begin, end)) on that CUDA stream
+        during every following step; None unregisters."""
+        if consumer is None:
+            cb = C.cast(None, CONSUMER)
+        else:
+            cb = CONSUMER(lambda _u, r, b, b0, b1, src, stream: consumer(r, b, b0, b1, src, stream))
+        self._consumer_ref = cb       # kept alive: the library calls it during later steps
+        check(paro_set_param_consumer(self.h, cb, None))
 
     def accumulate(self, grads=None):
         """paro_accumulate: add one micro-batch (grads: None = the flat gradient

@@ -70,6 +70,16 @@ def main():
                 st = [torch.empty(info["os_numel"], dtype=torch.float32, device="cuda") for _ in range(3)]
                 ptrs = [[x.data_ptr() for x in st]]
                 pl.opt_state_init(rank, ptrs[0], seed=SEED)
+                consumed = None
+                if cfg.get("consumer"):   # per-bucket parameter consumer: copies into a side buffer
+                    consumed = torch.zeros(info["p_numel"], dtype=torch.int16, device="cuda")
+                    rt = _rt()
+                    pbase = pl.buffer(rank, 1)
+
+                    def _cons(r, b, b0, b1, src, stream, consumed=consumed, pbase=pbase, rt=rt):
+                        assert rt.cudaMemcpyAsync(consumed.data_ptr() + (src - pbase), src, 2 * (b1 - b0), 3,
+                                                  stream) == 0
+                    pl.set_param_consumer(_cons)
                 stats = None
                 for s in range(1, steps + 1):
                     if accum:
@@ -113,6 +123,8 @@ def main():
                         parts.append(wb.cpu().numpy().view(np.uint16))
                     extra["frozen_full"] = np.concatenate(parts)
                     fz.close()
+                if consumed is not None:
+                    extra["consumed"] = consumed.cpu().numpy().view(np.uint16)
                 np.savez(os.path.join(out, tag + ".npz"), master=st[0].cpu().numpy(), m=st[1].cpu().numpy(),
                          v=st[2].cpu().numpy(), param=pbuf.cpu().numpy().view(np.uint16), **extra)
                 with open(os.path.join(out, tag + ".json"), "w") as f:
@@ -121,6 +133,16 @@ def main():
         ctx.close()
         dist.barrier()
     dist.destroy_process_group()
+
+
+def _rt():
+    import ctypes
+    import glob
+    import nvidia.cuda_runtime as cr
+    rt = ctypes.CDLL(glob.glob(os.path.join(list(cr.__path__)[0], "lib", "libcudart.so*"))[0])
+    rt.cudaMemcpyAsync.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_void_p]
+    rt.cudaMemcpyAsync.restype = ctypes.c_int
+    return rt
 
 
 def _copy(dst, src_ptr):

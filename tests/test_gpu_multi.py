@@ -58,7 +58,7 @@ CODES = ["NNN", "NNI", "NNG", "NII", "NIG", "NGG", "INI", "ING", "III", "IIG", "
 
 @pytest.mark.skipif(_ngpu() < 2, reason="needs >= 2 GPUs")
 @pytest.mark.parametrize("variant", ["default", "paced_lsu", "accum", "clip", "copy_engine", "masked", "slots",
-                                     "tma_thread_store", "fp32_wire", "predivide_off", "layer_windows"])
+                                     "tma_thread_store", "fp32_wire", "predivide_off", "layer_windows", "consumer"])
 def test_real_ranks_match_oracle(tmp_path, variant):
     world = _ngpu()                  # every visible GPU: 2 (2x1, 1x2), 4 (4x1, 2x2, 1x4), 8 (8x1, 4x2, 2x4, 1x8)
     splits = [m for m in range(1, world + 1) if world % m == 0]
@@ -89,6 +89,9 @@ def test_real_ranks_match_oracle(tmp_path, variant):
         cfg.update({"sizes": [d * 3 + 5] + [d * d, d * d + 7, 3 * d * d, d] * 3 + [d * 3 + 5],
                     "groups": [0, 1, 5, 9, 13], "topos": ["ho", "two_step"], "transports": ["pull", "push"],
                     "windows": 2})
+    if variant == "consumer":    # per-bucket parameter consumer (incl. fused gathers: channel-3 barrier)
+        cfg.update({"consumer": True, "topos": ["ho", "oneshot"], "transports": ["pull"], "fuse_gather": "always",
+                    "grad_slots": 2})
     if variant == "masked":      # partial / PEFT training: trainable plan + frozen-parameter plan
         cfg.update({"sizes": [world * 64 * 40 + 24, 333, world * 64 * 9 + 5, 4096], "mask": [0, 1, 0, 1],
                     "topos": ["ho", "two_step"], "transports": ["pull"], "windows": 2})
@@ -139,6 +142,8 @@ def test_real_ranks_match_oracle(tmp_path, variant):
                     # plan's per-rank transfer list (rank-symmetric schedules; Table 3 accounting)
                     st_ = meta["stats"]
                     assert (st_["moved_intra"], st_["moved_inter"]) == (st_["sent_intra"], st_["sent_inter"]), tag
+                    if "consumed" in d:  # the consumer saw exactly the final parameters of every bucket
+                        assert np.array_equal(d["consumed"], d["param"]), tag
                     if "full" in d:      # forward/backward parameter gather: the full bf16 model
                         assert np.array_equal(d["full"], p), tag
                     if mask:             # frozen tensors: untouched residency, full windows

@@ -1123,3 +1123,55 @@ def test_oneshot_accumulation_and_collective(N, M):
             assert np.array_equal(d2h(pl.buffer(r, 3) + 2 * (b % 3) * B, n, np.uint16), gh[s0:s0 + n]), (r, b)
     pl.close()
     ctx.close()
+
+
+# --------------------------------------------------------------------- parameter consumer
+@pytest.mark.parametrize("N,M,slots", [(8, 4, 0), (4, 2, 2), (2, 1, 0), (1, 1, 2)])
+def test_param_consumer_every_strategy(N, M, slots):
+    """paro_set_param_consumer: each bucket's updated bf16 parameters (the rank's
+    P residency) are handed over on a side stream as soon as they are final; a
+    consumer that copies them out gets exactly the parameter buffer after the
+    step (= unsharded DP), every bucket once per step, in bucket order; also in
+    streamed steps (grad_slots) and at N = 1."""
+    import ctypes
+    from devmem import _cudart
+    paro = _paro()
+    rt = _cudart()
+    rt.cudaMemcpyAsync.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_void_p]
+    rt.cudaMemcpyAsync.restype = ctypes.c_int
+    sizes = [N * 64 * 40 + 24, 1000]
+    B = N * 64 * 8
+    lay = L.Layout(sizes, N, M, B)
+    ref = _dp_reference(lay, 2)
+    for code in S.paro_strategies():
+        mode = "emulated" if N > 1 else "real"
+        run = EmuRun(N, M, code, sizes, B, mode=mode, transport="pull")
+        if slots:
+            run.pl.close()
+            run.pl = paro.Plan(run.ctx, code, sizes, bucket_elems=B, grad_slots=slots, transport="pull")
+            run.info = run.pl.info()
+            for r in range(N):
+                run.pl.opt_state_init(r, [t.data_ptr() for t in run.st[r]], seed=SEED)
+        out = [torch.zeros(run.info["p_numel"], dtype=torch.int16, device="cuda") for _ in range(N)]
+        calls = []
+
+        def consumer(r, b, b0, b1, src, stream, out=out, calls=calls, run=run):
+            calls.append((r, b))
+            off = src - run.pl.buffer(r, 1)
+            assert rt.cudaMemcpyAsync(out[r].data_ptr() + off, src, 2 * (b1 - b0), 3, stream) == 0
+
+        run.pl.set_param_consumer(consumer)
+        for t in (1, 2):
+            if slots:
+                run.pl.step_streamed(run.ptrs(), LR, t, seed=SEED, grad_step=t)
+            else:
+                run.set_grads(t)
+                run.step(t)
+        torch.cuda.synchronize()
+        _check_against_dp(run, lay, ref)
+        nb = len(lay.buckets)
+        assert calls == [(r, b) for _ in range(2) for b in range(nb) for r in range(N)]
+        for r in range(N):
+            assert np.array_equal(out[r].cpu().numpy().view(np.uint16), run.state(r)["param"]), (code, r)
+        run.pl.set_param_consumer(None)
+        run.close()
