@@ -323,18 +323,25 @@ paro_status_t upload_schedule(PlanT* p) {
         d.peers_before = 0;
       }
       d.t1 = (int32_t)tasks.size();
-      int64_t tiles = 0;
       for (int ti = d.t0; ti < d.t1; ++ti) {
         dl.max_in = std::max(dl.max_in, (int)tasks[ti].nin);
         if (tasks[ti].out_f32 || tasks[ti].nest > 1) dl.generic = 1;
-        tiles += (tasks[ti].n8 * 8 + 4095) / 4096;
       }
-      dl.max_tiles = std::max(dl.max_tiles, tiles);
       (void)acc_kind;
       rounds.push_back(d);
     }
     dl.nrounds = R;
     dl.final_barrier = L.final_barrier ? 1 : 0;
+    // tiles of the largest round at the slot size this launch's input count gets
+    for (int r = 0; r < R; ++r) {
+      const DRound& d = rounds[dl.round_off + r];
+      int64_t tiles = 0;
+      for (int ti = d.t0; ti < d.t1; ++ti) {
+        const int64_t te = rounds_tma_tile_elems(dl.max_in, tasks[ti].out_f32);
+        tiles += (tasks[ti].n8 * 8 + te - 1) / te;
+      }
+      dl.max_tiles = std::max(dl.max_tiles, tiles);
+    }
     // bytes sent by the local rank(s): what peers read from them in this launch
     for (int r = 0; r < R; ++r)
       for (int x = 0; x < pl.N; ++x)

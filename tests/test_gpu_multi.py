@@ -139,9 +139,11 @@ def test_real_ranks_match_oracle(tmp_path, variant):
                     assert np.array_equal(d["param"], ST.shard_of(p, lay, code[0], rank)), tag
                     assert abs(meta["stats"]["grad_norm"] ** 2 - norm) <= 1e-12 * norm, tag
                     # NVLink bytes counted on the device by the kernels that moved them equal the
-                    # plan's per-rank transfer list (rank-symmetric schedules; Table 3 accounting)
+                    # plan's per-rank transfer list (rank-symmetric schedules; Table 3 accounting;
+                    # H-Ring's leaders pull more than they are pulled: its totals are checked below)
                     st_ = meta["stats"]
-                    assert (st_["moved_intra"], st_["moved_inter"]) == (st_["sent_intra"], st_["sent_inter"]), tag
+                    if topo != "h_ring":
+                        assert (st_["moved_intra"], st_["moved_inter"]) == (st_["sent_intra"], st_["sent_inter"]), tag
                     if "consumed" in d:  # the consumer saw exactly the final parameters of every bucket
                         assert np.array_equal(d["consumed"], d["param"]), tag
                     if "full" in d:      # forward/backward parameter gather: the full bf16 model
@@ -149,6 +151,12 @@ def test_real_ranks_match_oracle(tmp_path, variant):
                     if mask:             # frozen tensors: untouched residency, full windows
                         assert np.array_equal(d["frozen_param"], ST.shard_of(p_frozen, lay_f, code[0], rank)), tag
                         assert np.array_equal(d["frozen_full"], p_frozen), tag
+                if topo == "h_ring":
+                    tot = np.zeros(4, np.int64)
+                    for rank in range(world):
+                        st_ = json.load(open(tmp_path / f"{M}_{code}_{topo}_{tr}_r{rank}.json"))["stats"]
+                        tot += [st_["moved_intra"], st_["moved_inter"], st_["sent_intra"], st_["sent_inter"]]
+                    assert (tot[0], tot[1]) == (tot[2], tot[3]), (M, code, topo, tr)
 
 
 @pytest.mark.skipif(_ngpu() < 2, reason="needs >= 2 GPUs")
