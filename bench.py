@@ -58,6 +58,9 @@ def parse(argv=None):
     ap.add_argument("--comm-impl", default="tma_store", choices=["tma", "lsu", "tma_store"])
     ap.add_argument("--fuse-gather", default="auto", choices=["auto", "always", "never"],
                     help="parameter all-gather inside Adam (one-ring restores)")
+    ap.add_argument("--copy-engine", default="gathers", choices=["off", "gathers", "all"],
+                    help="parameter all-gathers (pure bit copies) on the copy engines: measured 2x2 IIG "
+                         "20.43 vs 21.10 ms (profiles/r02/sweep_copy_engine_iig_2x2.jsonl)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--e2e-mode", default="stream", choices=["stream", "pack"],
                     help="stream: a grad_slots plan whose producer copies each bucket host->device on the "
@@ -77,7 +80,8 @@ def plan_kwargs(args, stream):
     full-size parity tests, so they check exactly what is timed)."""
     return dict(bucket_elems=args.bucket, topology=args.topology, comm_ctas=args.comm_ctas,
                 pipeline_depth=args.depth, stream=stream, transport=args.transport, adam_impl=args.adam_impl,
-                comm_impl=args.comm_impl, fuse_gather=args.fuse_gather)
+                comm_impl=args.comm_impl, fuse_gather=args.fuse_gather,
+                copy_engine={"off": False, "gathers": "gathers", "all": "all"}[args.copy_engine])
 
 
 def default_group(N):
@@ -494,7 +498,7 @@ def run_ours(args):
                        "topology": args.topology, "bucket_elems": info["bucket_elems"],
                        "n_buckets": info["n_buckets"], "comm_ctas": args.comm_ctas, "pipeline_depth": args.depth,
                        "transport": args.transport, "adam_impl": args.adam_impl, "comm_impl": args.comm_impl,
-                       "fuse_gather": args.fuse_gather,
+                       "fuse_gather": args.fuse_gather, "copy_engine": args.copy_engine,
                        "l2": "no flush: per-step inputs (13.5 GB grads + 81 GB/div(OS) state) >> 126 MB L2",
                        "intra_inter_gap": "not emulated: one NVSwitch box, intra/inter are labels"},
             "roofline": roof, "step_roofline": step_roof, "ho_ring": ho, "per_strategy": per_strategy,

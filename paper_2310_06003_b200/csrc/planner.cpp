@@ -18,6 +18,7 @@ namespace {
 constexpr int64_t kQuantum = 64;      // elements per shard granule (R21)
 constexpr int64_t kAlignElems = 128;  // 256-byte alignment of buffer kinds
 constexpr int64_t kOneRoundExtraBytes = int64_t(6) << 20;   // one-shot AR: extra bytes worth one barrier
+constexpr int64_t kOneShotMaxBytes = int64_t(32) << 20;     // one-shot topology: larger buckets use HO-Ring
 
 int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
@@ -422,7 +423,7 @@ void Planner::layout() {
 
 void Planner::build_schedule() {
   sched.assign(buckets.size(), BucketSchedule());
-  const int topo = opt.topology;
+  int topo = opt.topology;   // per bucket: the one-shot topology hands large buckets to HO-Ring
   // primitive names (reporting; mirrors oracle.accounting.step_ops)
   grad_ops.clear();
   rest_ops.clear();
@@ -457,6 +458,11 @@ void Planner::build_schedule() {
   for (size_t b = 0; b < buckets.size(); ++b) {
     BucketSchedule& S = sched[b];
     const int64_t s = buckets[b].first, n = buckets[b].second;
+    // one-shot collectives pay off while latency-bound; on one NVSwitch box the
+    // all-to-all pulls move less than a ring once a bucket is large (measured:
+    // 2x2 all-reduce 408 vs 627 GB/s busbw at 1 GiB, profiles/r02), so larger
+    // buckets run the HO-Ring schedules (the same canonical bits)
+    topo = (opt.topology == 6 && n * opt.wire > kOneShotMaxBytes) ? 0 : opt.topology;
     const int64_t C = n / N, chunk = n / M;
     const int par = int(b % kStageSets);
     S.reduce.n_ranks = S.gather.n_ranks = S.accum.n_ranks = S.reduce_acc.n_ranks = S.window.n_ranks = N;
