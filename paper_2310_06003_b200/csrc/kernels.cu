@@ -14,6 +14,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "kernels.h"
 
@@ -826,7 +827,8 @@ __global__ void __maxnreg__(72) adam_tma_kernel(const AdamArgs a, int gnin_max, 
 // stay within 96 KB).
 constexpr int kRtThreads = 256;
 constexpr int kRtSlotB = 8192;    // slot bytes per input for <= 3 inputs
-constexpr int kRtStages = 4;
+constexpr int kRtStages = 4;      // stages for <= 3 inputs (8 KB slots)
+constexpr int kRtMaxStages = 8;
 constexpr int kRtMaxIn = kDevMaxIn;
 constexpr int kRtSmem = kRtStages * 3 * kRtSlotB;   // 96 KB
 
@@ -839,6 +841,14 @@ int rt_slot_lg(int max_in) {
   return lg;
 }
 int rt_slot_bytes(int max_in) { return 1 << rt_slot_lg(max_in); }
+// stages: 4 for <= 3 inputs (the tuned 8 KB-slot pipeline), else as many as
+// fit the 96 KB (up to 8); PARO_RT_STAGES overrides both (A/B runs)
+int rt_stages(int max_in) {
+  static const int env = std::getenv("PARO_RT_STAGES") ? std::atoi(std::getenv("PARO_RT_STAGES")) : 0;
+  int st = max_in <= 3 ? kRtStages : kRtSmem / (max_in << rt_slot_lg(max_in));
+  if (env >= 2) st = std::min(env, kRtSmem / (max_in << rt_slot_lg(max_in)));
+  return std::max(2, std::min(kRtMaxStages, st));
+}
 
 // log2 of the elements per tile: one slot of the task's widest operand (fp32
 // wire tasks have fp32 results, whose tile goes back over input 0's slot)
@@ -944,13 +954,14 @@ __device__ __forceinline__ void rt_fold_generic(const DTask* tk, unsigned char* 
 // compiled into a separate instantiation so the common bf16 path keeps every
 // value in registers (<= 64, no spills).
 template <bool kBulk, bool kGen>
-__global__ void __launch_bounds__(kRtThreads, 4) rounds_tma_kernel(const RoundsArgs a, int max_in, int slot_lg) {
+__global__ void __launch_bounds__(kRtThreads, 4) rounds_tma_kernel(const RoundsArgs a, int max_in, int slot_lg,
+                                                                   int nst) {
   const int slotb = 1 << slot_lg;
   extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ uint64_t bars[kRtStages];
+  __shared__ uint64_t bars[kRtMaxStages];
   if (a.bar.err && *(volatile int*)a.bar.err) return;   // sticky device error: do nothing
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kRtStages; ++s) mbar_init(&bars[s], 1);
+    for (int s = 0; s < nst; ++s) mbar_init(&bars[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -987,7 +998,7 @@ __global__ void __launch_bounds__(kRtThreads, 4) rounds_tma_kernel(const RoundsA
         while (inter_sent > (double)(globaltimer() - t_round) * a.inter_bytes_per_ns) __nanosleep(256);
       }
       count_moved(tk, ne, mi, me);
-      const uint32_t slot = (cnt + (uint32_t)k) % kRtStages;
+      const uint32_t slot = (cnt + (uint32_t)k) % nst;
       unsigned char* base = smem + slot * stage_bytes;
       uint32_t tx = 0;
       for (int i = 0; i < tk->nin; ++i) tx += (uint32_t)ne * (((tk->f32mask >> i) & 1u) ? 4 : 2);
@@ -999,11 +1010,11 @@ __global__ void __launch_bounds__(kRtThreads, 4) rounds_tma_kernel(const RoundsA
       }
     };
     if (threadIdx.x == 0)
-      for (int64_t k = 0; k < min((int64_t)kRtStages, mine); ++k) issue(k);
+      for (int64_t k = 0; k < min((int64_t)nst, mine); ++k) issue(k);
     for (int64_t k = 0; k < mine; ++k) {
       const uint32_t c = cnt + (uint32_t)k;
-      const uint32_t slot = c % kRtStages;
-      mbar_wait(&bars[slot], (c / kRtStages) & 1u);
+      const uint32_t slot = c % nst;
+      mbar_wait(&bars[slot], (c / nst) & 1u);
       const DTask* tk;
       int64_t e0;
       int ne;
@@ -1042,11 +1053,11 @@ __global__ void __launch_bounds__(kRtThreads, 4) rounds_tma_kernel(const RoundsA
           bulk_s2g(reinterpret_cast<unsigned char*>(tk->dst) + (size_t)e0 * osz, base, (uint32_t)ne * osz);
           bulk_commit();
           bulk_wait_read<1>();      // the previous tile's store has read its stage: refill it
-          if (k >= 1 && k - 1 + kRtStages < mine) issue(k - 1 + kRtStages);
+          if (k >= 1 && k - 1 + nst < mine) issue(k - 1 + nst);
         }
       } else {
         __syncthreads();   // stage consumed by every thread: refill it
-        if (threadIdx.x == 0 && k + kRtStages < mine) issue(k + kRtStages);
+        if (threadIdx.x == 0 && k + nst < mine) issue(k + nst);
       }
     }
     cnt += (uint32_t)mine;
@@ -1264,13 +1275,14 @@ cudaError_t launch_rounds_tma(const RoundsArgs& a, int grid, int max_in, cudaStr
   if (max_in < 1) max_in = 1;
   if (max_in > kRtMaxIn) max_in = kRtMaxIn;
   const int lg = rt_slot_lg(max_in);
-  const size_t sm = (size_t)kRtStages * max_in << lg;
+  const int nst = rt_stages(max_in);
+  const size_t sm = (size_t)nst * max_in << lg;
   if (generic) {
-    if (bulk_store) rounds_tma_kernel<true, true><<<grid, kRtThreads, sm, s>>>(a, max_in, lg);
-    else rounds_tma_kernel<false, true><<<grid, kRtThreads, sm, s>>>(a, max_in, lg);
+    if (bulk_store) rounds_tma_kernel<true, true><<<grid, kRtThreads, sm, s>>>(a, max_in, lg, nst);
+    else rounds_tma_kernel<false, true><<<grid, kRtThreads, sm, s>>>(a, max_in, lg, nst);
   } else {
-    if (bulk_store) rounds_tma_kernel<true, false><<<grid, kRtThreads, sm, s>>>(a, max_in, lg);
-    else rounds_tma_kernel<false, false><<<grid, kRtThreads, sm, s>>>(a, max_in, lg);
+    if (bulk_store) rounds_tma_kernel<true, false><<<grid, kRtThreads, sm, s>>>(a, max_in, lg, nst);
+    else rounds_tma_kernel<false, false><<<grid, kRtThreads, sm, s>>>(a, max_in, lg, nst);
   }
   return cudaGetLastError();
 }
@@ -1284,7 +1296,7 @@ int rounds_tma_tile_elems(int max_in, int out_f32) {
 int rounds_tma_smem_kb(int max_in) {
   if (max_in < 1) max_in = 1;
   if (max_in > kRtMaxIn) max_in = kRtMaxIn;
-  return (kRtStages * max_in * rt_slot_bytes(max_in) + 1023) / 1024;
+  return (rt_stages(max_in) * max_in * rt_slot_bytes(max_in) + 1023) / 1024;
 }
 
 cudaError_t launch_adam(const AdamArgs& a, int grid, cudaStream_t s, int cap_two_per_sm) {

@@ -8,6 +8,7 @@
 #include "planner.h"
 
 #include <algorithm>
+#include <cstdlib>
 #include <functional>
 #include <stdexcept>
 
@@ -19,6 +20,12 @@ constexpr int64_t kQuantum = 64;      // elements per shard granule (R21)
 constexpr int64_t kAlignElems = 128;  // 256-byte alignment of buffer kinds
 constexpr int64_t kOneRoundExtraBytes = int64_t(6) << 20;   // one-shot AR: extra bytes worth one barrier
 constexpr int64_t kOneShotMaxBytes = int64_t(32) << 20;     // one-shot topology: larger buckets use HO-Ring
+
+// PARO_ONESHOT_MAX_MB overrides the threshold (measurement runs)
+int64_t oneshot_max_bytes() {
+  const char* v = std::getenv("PARO_ONESHOT_MAX_MB");
+  return v ? int64_t(std::atoll(v)) << 20 : kOneShotMaxBytes;
+}
 
 int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
@@ -462,7 +469,7 @@ void Planner::build_schedule() {
     // all-to-all pulls move less than a ring once a bucket is large (measured:
     // 2x2 all-reduce 408 vs 627 GB/s busbw at 1 GiB, profiles/r02), so larger
     // buckets run the HO-Ring schedules (the same canonical bits)
-    topo = (opt.topology == 6 && n * opt.wire > kOneShotMaxBytes) ? 0 : opt.topology;
+    topo = (opt.topology == 6 && n * opt.wire > oneshot_max_bytes()) ? 0 : opt.topology;
     const int64_t C = n / N, chunk = n / M;
     const int par = int(b % kStageSets);
     S.reduce.n_ranks = S.gather.n_ranks = S.accum.n_ranks = S.reduce_acc.n_ranks = S.window.n_ranks = N;
