@@ -574,27 +574,6 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                : "memory");
 }
 
-// the same copies with an L2 eviction-priority policy (createpolicy; evict_first
-// for operands Adam reads or writes exactly once)
-__device__ __forceinline__ uint64_t l2_evict_first() {
-  uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-  return pol;
-}
-__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
-                                              uint64_t pol) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_s2g_hint(void* dst, const void* src, uint32_t bytes, uint64_t pol) {
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(dst),
-               "r"(smem_u32(src)), "r"(bytes), "l"(pol)
-               : "memory");
-}
-
 __device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
                "r"(bytes)
@@ -637,19 +616,21 @@ __device__ __forceinline__ bool tile_of(const AdamArgs& a, int64_t t, TileRef& o
 // leave through bulk copies too (master, m, v, the bf16 parameter and, for the
 // fused all-gather, the peers' parameter buffers): the stage is refilled one
 // iteration later, once its stores have read it (wait_group.read 1).
-// gsz: bytes per g_hat element in the stages (2 bf16; 4 when any input is fp32,
-// the fp32 wire).
-template <bool kStore, int kThr>
-__global__ void __maxnreg__(72) adam_tma_kernel(const AdamArgs a, int gnin_max, int stages, int gsz) {
+// kWide: the launch has fp32 g_hat inputs (the fp32 wire): 4-byte slots per
+// input, fp32 pre-scaling and hops; the bf16 instantiation keeps the
+// bf16-only arithmetic, constant slot sizes and fewer instructions.
+template <bool kStore, int kThr, bool kWide>
+__global__ void __maxnreg__(72) adam_tma_kernel(const AdamArgs a, int gnin_max, int stages) {
   constexpr int kTmaTile = kThr * 8;   // elements per tile (8 per thread)
+  constexpr int kGsz = kWide ? 4 : 2;  // bytes per g_hat element in a stage slot
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ uint64_t full_bar[4];
   if (a.skip && *a.skip) return;   // two-phase step: non-finite gradients, update skipped
   const AdamScal c{a.b1, a.omb1, a.b2, a.omb2, a.step_size, a.bc2s, a.eps, a.decay, unscale_of(a), a.alpha,
                    a.has_wd};
-  const size_t g_bytes = (size_t)kTmaTile * gsz, f_bytes = (size_t)kTmaTile * 4;
+  constexpr size_t g_bytes = (size_t)kTmaTile * kGsz, f_bytes = (size_t)kTmaTile * 4;
   const size_t stage_bytes = gnin_max * g_bytes + 3 * f_bytes;
-  unsigned long long mi = 0, me = 0;   // NVLink bytes of this CTA's tiles (thread 0)
+  int64_t done = 0;   // elements of this CTA's tiles (thread 0; moved-byte count at the end)
   int64_t total = 0;
   for (int i = 0; i < a.nseg; ++i) total += (a.seg[i].n8 * 8 + kTmaTile - 1) / kTmaTile;
   const int64_t mine = (total > blockIdx.x) ? (total - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
@@ -665,30 +646,25 @@ __global__ void __maxnreg__(72) adam_tma_kernel(const AdamArgs a, int gnin_max, 
     const int s = (int)(k % stages);
     unsigned char* base = smem + s * stage_bytes;
     const uint32_t fb = (uint32_t)tr.n * 4;
-    uint32_t tx = 3 * fb;
-    for (int i = 0; i < sg.gnin; ++i) {
-      const uint32_t b = (uint32_t)tr.n * (((sg.gf32 >> i) & 1u) ? 4 : 2);
-      tx += b;
-      if ((sg.gpeer >> i) & 1u) (((sg.ginter >> i) & 1u) ? me : mi) += b;   // fused hop: NVLink pull
-    }
-    for (int i = 0; i < sg.npush; ++i) (((sg.pinter >> i) & 1u) ? me : mi) += (unsigned long long)tr.n * 2;
-    mbar_expect_tx(&full_bar[s], tx);
-    for (int i = 0; i < sg.gnin; ++i) {
-      const int es = ((sg.gf32 >> i) & 1u) ? 4 : 2;
-      bulk_g2s(base + i * g_bytes, reinterpret_cast<const unsigned char*>(sg.gin[i]) + (size_t)tr.start * es,
-               (uint32_t)tr.n * es, &full_bar[s]);
+    done += tr.n;
+    if (kWide) {
+      uint32_t tx = 3 * fb;
+      for (int i = 0; i < sg.gnin; ++i) tx += (uint32_t)tr.n * (((sg.gf32 >> i) & 1u) ? 4 : 2);
+      mbar_expect_tx(&full_bar[s], tx);
+      for (int i = 0; i < sg.gnin; ++i) {
+        const int es = ((sg.gf32 >> i) & 1u) ? 4 : 2;
+        bulk_g2s(base + i * g_bytes, reinterpret_cast<const unsigned char*>(sg.gin[i]) + (size_t)tr.start * es,
+                 (uint32_t)tr.n * es, &full_bar[s]);
+      }
+    } else {
+      const uint32_t gb = (uint32_t)tr.n * 2;
+      mbar_expect_tx(&full_bar[s], sg.gnin * gb + 3 * fb);
+      for (int i = 0; i < sg.gnin; ++i) bulk_g2s(base + i * g_bytes, sg.gin[i] + tr.start, gb, &full_bar[s]);
     }
     unsigned char* fbase = base + gnin_max * g_bytes;
-    if (a.l2_hint) {   // master / m / v: read once per step, evict first
-      const uint64_t pol = l2_evict_first();
-      bulk_g2s_hint(fbase, sg.master + tr.start, fb, &full_bar[s], pol);
-      bulk_g2s_hint(fbase + f_bytes, sg.m + tr.start, fb, &full_bar[s], pol);
-      bulk_g2s_hint(fbase + 2 * f_bytes, sg.v + tr.start, fb, &full_bar[s], pol);
-    } else {
-      bulk_g2s(fbase, sg.master + tr.start, fb, &full_bar[s]);
-      bulk_g2s(fbase + f_bytes, sg.m + tr.start, fb, &full_bar[s]);
-      bulk_g2s(fbase + 2 * f_bytes, sg.v + tr.start, fb, &full_bar[s]);
-    }
+    bulk_g2s(fbase, sg.master + tr.start, fb, &full_bar[s]);
+    bulk_g2s(fbase + f_bytes, sg.m + tr.start, fb, &full_bar[s]);
+    bulk_g2s(fbase + 2 * f_bytes, sg.v + tr.start, fb, &full_bar[s]);
   };
   if (threadIdx.x == 0)
     for (int64_t k = 0; k < min((int64_t)stages, mine); ++k) issue(k);
@@ -708,20 +684,31 @@ __global__ void __maxnreg__(72) adam_tma_kernel(const AdamArgs a, int gnin_max, 
     uint4 pk = make_uint4(0, 0, 0, 0);
     if (act) {
       float g[8];
-      auto ld = [&](int i, float f[8]) {   // g_hat input i of this thread's 8 elements, from the stage
-        if ((sg.gf32 >> i) & 1u) {
-          const float4* q = reinterpret_cast<const float4*>(base + i * g_bytes + (size_t)e0 * 4);
-          f4x2(q[0], q[1], f);
-        } else {
-          unpack8(*reinterpret_cast<const uint4*>(base + i * g_bytes + (size_t)e0 * 2), f);
-          if ((sg.graw >> i) & 1u) pre8(f, c.alpha, sg.gwide != 0);
+      if (kWide) {
+        auto ld = [&](int i, float f[8]) {   // g_hat input i of this thread's 8 elements, from the stage
+          if ((sg.gf32 >> i) & 1u) {
+            const float4* q = reinterpret_cast<const float4*>(base + i * g_bytes + (size_t)e0 * 4);
+            f4x2(q[0], q[1], f);
+          } else {
+            unpack8(*reinterpret_cast<const uint4*>(base + i * g_bytes + (size_t)e0 * 2), f);
+            if ((sg.graw >> i) & 1u) mul8(f, c.alpha);
+          }
+        };
+        ld(0, g);
+        for (int i = 1; i < sg.gnin; ++i) {
+          float x[8];
+          ld(i, x);
+          add8(g, x);
         }
-      };
-      ld(0, g);
-      for (int i = 1; i < sg.gnin; ++i) {
-        float x[8];
-        ld(i, x);
-        hopw8(g, x, sg.gwide != 0);
+      } else {
+        unpack8(*reinterpret_cast<const uint4*>(base + e0 * 2), g);
+        if (sg.graw & 1u) scale_round8(g, c.alpha);
+        for (int i = 1; i < sg.gnin; ++i) {
+          float x[8];
+          unpack8(*reinterpret_cast<const uint4*>(base + i * g_bytes + e0 * 2), x);
+          if ((sg.graw >> i) & 1u) scale_round8(x, c.alpha);
+          hop8(g, x);
+        }
       }
       const float4 w0 = *reinterpret_cast<const float4*>(fw + e0), w1 = *reinterpret_cast<const float4*>(fw + e0 + 4);
       const float4 m0 = *reinterpret_cast<const float4*>(fw + kTmaTile + e0);
@@ -739,7 +726,7 @@ __global__ void __maxnreg__(72) adam_tma_kernel(const AdamArgs a, int gnin_max, 
     if (kStore) {
       // fp32 inputs: every thread has read its input-0 bytes before the bf16
       // outputs (half their width) are written over them
-      if (gsz == 4) __syncthreads();
+      if (kWide) __syncthreads();
       if (act) {   // back into the stage, in place (each thread owns its 8 elements)
         *reinterpret_cast<float4*>(fw + e0) = make_float4(w[0], w[1], w[2], w[3]);
         *reinterpret_cast<float4*>(fw + e0 + 4) = make_float4(w[4], w[5], w[6], w[7]);
@@ -766,16 +753,9 @@ __global__ void __maxnreg__(72) adam_tma_kernel(const AdamArgs a, int gnin_max, 
       if (threadIdx.x == 0) {
         const uint32_t gb = (uint32_t)tr.n * 2, fb = (uint32_t)tr.n * 4;
         const unsigned char* fbase = base + gnin_max * g_bytes;
-        if (a.l2_hint) {
-          const uint64_t pol = l2_evict_first();
-          bulk_s2g_hint(sg.master + tr.start, fbase, fb, pol);
-          bulk_s2g_hint(sg.m + tr.start, fbase + f_bytes, fb, pol);
-          bulk_s2g_hint(sg.v + tr.start, fbase + 2 * f_bytes, fb, pol);
-        } else {
-          bulk_s2g(sg.master + tr.start, fbase, fb);
-          bulk_s2g(sg.m + tr.start, fbase + f_bytes, fb);
-          bulk_s2g(sg.v + tr.start, fbase + 2 * f_bytes, fb);
-        }
+        bulk_s2g(sg.master + tr.start, fbase, fb);
+        bulk_s2g(sg.m + tr.start, fbase + f_bytes, fb);
+        bulk_s2g(sg.v + tr.start, fbase + 2 * f_bytes, fb);
         bulk_s2g(sg.param + tr.start, base, gb);
         for (int i = 0; i < sg.npush; ++i) bulk_s2g(sg.push[i] + tr.start, base, gb);
         bulk_commit();
@@ -797,7 +777,15 @@ __global__ void __maxnreg__(72) adam_tma_kernel(const AdamArgs a, int gnin_max, 
   } else {
     push_fence(a);
   }
-  if (threadIdx.x == 0) flush_moved(a.moved, mi, me);
+  if (threadIdx.x == 0 && a.moved && done > 0) {   // NVLink bytes of this CTA's tiles (real mode: one segment)
+    const AdamSeg& sg = a.seg[0];
+    unsigned long long mi = 0, me = 0;
+    for (int i = 0; i < sg.gnin; ++i)
+      if ((sg.gpeer >> i) & 1u)
+        (((sg.ginter >> i) & 1u) ? me : mi) += (unsigned long long)done * (((sg.gf32 >> i) & 1u) ? 4 : 2);
+    for (int i = 0; i < sg.npush; ++i) (((sg.pinter >> i) & 1u) ? me : mi) += (unsigned long long)done * 2;
+    flush_moved(a.moved, mi, me);
+  }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) nsq += __shfl_xor_sync(0xffffffffu, nsq, o);
   __shared__ double s_part[kThr / 32];
@@ -1241,8 +1229,10 @@ static cudaError_t set_carveouts() {
   const void* fns[] = {(const void*)rounds_kernel, (const void*)rounds_tma_kernel<false, false>,
                        (const void*)rounds_tma_kernel<true, false>, (const void*)rounds_tma_kernel<false, true>,
                        (const void*)rounds_tma_kernel<true, true>, (const void*)adam_kernel,
-                       (const void*)adam_tma_kernel<false, 512>, (const void*)adam_tma_kernel<true, 512>,
-                       (const void*)adam_tma_kernel<true, 256>, (const void*)adam_tma_kernel<false, 256>};
+                       (const void*)adam_tma_kernel<false, 512, false>, (const void*)adam_tma_kernel<true, 512, false>,
+                       (const void*)adam_tma_kernel<true, 256, false>, (const void*)adam_tma_kernel<false, 256, false>,
+                       (const void*)adam_tma_kernel<false, 512, true>, (const void*)adam_tma_kernel<true, 512, true>,
+                       (const void*)adam_tma_kernel<true, 256, true>, (const void*)adam_tma_kernel<false, 256, true>};
   for (const void* f : fns) {
     cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout,
                                          (int)cudaSharedmemCarveoutMaxShared);
@@ -1335,8 +1325,10 @@ cudaError_t launch_adam_tma(const AdamArgs& a, int sms, cudaStream_t s, int smem
   }
   static bool attr_set = false;
   if (!attr_set) {
-    for (const void* f : {(const void*)adam_tma_kernel<false, 512>, (const void*)adam_tma_kernel<true, 512>,
-                          (const void*)adam_tma_kernel<true, 256>, (const void*)adam_tma_kernel<false, 256>}) {
+    for (const void* f : {(const void*)adam_tma_kernel<false, 512, false>, (const void*)adam_tma_kernel<true, 512, false>,
+                          (const void*)adam_tma_kernel<true, 256, false>, (const void*)adam_tma_kernel<false, 256, false>,
+                          (const void*)adam_tma_kernel<false, 512, true>, (const void*)adam_tma_kernel<true, 512, true>,
+                          (const void*)adam_tma_kernel<true, 256, true>, (const void*)adam_tma_kernel<false, 256, true>}) {
       cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
       if (e != cudaSuccess) return e;
     }
@@ -1346,26 +1338,33 @@ cudaError_t launch_adam_tma(const AdamArgs& a, int sms, cudaStream_t s, int smem
   auto stage_bytes = [&](int tile) { return (size_t)tile * (gsz * gmax + 12); };
   auto raw = [&](int tile, int kb) { return (int)(((size_t)kb * 1024) / stage_bytes(tile)); };
   auto clampst = [](int st, int lo) { return st > 4 ? 4 : (st < lo ? lo : st); };
+  const bool wide = gsz == 4;
+#define PARO_ADAM_LAUNCH(KS, KT)                                                                    \
+  do {                                                                                              \
+    if (wide) adam_tma_kernel<KS, KT, true><<<sms, KT, stage_bytes(KT * 8) * st, s>>>(a, gmax, st); \
+    else adam_tma_kernel<KS, KT, false><<<sms, KT, stage_bytes(KT * 8) * st, s>>>(a, gmax, st);     \
+  } while (0)
   int v = 0, st = 0;
   if (!tma_store) {
     st = clampst(raw(4096, smem_budget_kb), 2);
     if ((size_t)st * stage_bytes(4096) <= (size_t)hard_kb * 1024) {
       v = ADAM_TMA_LD_512;
-      adam_tma_kernel<false, 512><<<sms, 512, stage_bytes(4096) * st, s>>>(a, gmax, st, gsz);
+      PARO_ADAM_LAUNCH(false, 512);
     } else {
       st = clampst(std::min(raw(2048, smem_budget_kb), raw(2048, hard_kb)), 2);
       v = ADAM_TMA_LD_256;
-      adam_tma_kernel<false, 256><<<sms, 256, stage_bytes(2048) * st, s>>>(a, gmax, st, gsz);
+      PARO_ADAM_LAUNCH(false, 256);
     }
   } else if (raw(4096, smem_budget_kb) >= 3) {
     st = clampst(raw(4096, smem_budget_kb), 3);
     v = ADAM_TMA_ST_512;
-    adam_tma_kernel<true, 512><<<sms, 512, stage_bytes(4096) * st, s>>>(a, gmax, st, gsz);
+    PARO_ADAM_LAUNCH(true, 512);
   } else {
     st = clampst(raw(2048, smem_budget_kb), 3);
     v = ADAM_TMA_ST_256;
-    adam_tma_kernel<true, 256><<<sms, 256, stage_bytes(2048) * st, s>>>(a, gmax, st, gsz);
+    PARO_ADAM_LAUNCH(true, 256);
   }
+#undef PARO_ADAM_LAUNCH
   if (variant) *variant = v;
   if (stages) *stages = st;
   return cudaGetLastError();

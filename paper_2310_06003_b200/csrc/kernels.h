@@ -116,7 +116,6 @@ struct AdamArgs {
   const float* s_g_dev;
   const int* skip;
   unsigned long long* moved;   // [intra, inter] NVLink bytes pulled (fused hop) + pushed (fused gather), or NULL
-  int l2_hint;                 // TMA Adam: evict_first L2 policy on the master / m / v streams
 };
 
 struct PackEntry {     // one tensor slice: src/dst element pointers + count

@@ -489,11 +489,6 @@ bool entry_fast_on() {
   return on;
 }
 
-// integer environment switch for A/B measurements (read once per name)
-int env_flag(const char* name, int dflt) {
-  const char* v = std::getenv(name);
-  return v ? std::atoi(v) : dflt;
-}
 
 // 1-CTA peer barrier on the second channel (stream s), for copy-engine launches.
 // channel 2 (hdr + 1024: copy-engine launches, the gradient producer) or 3
@@ -1317,7 +1312,6 @@ paro_status_t step_impl(PlanT* p, const void* const* grads, void* const* params,
   aa.s_g = (float)sg_base;
   aa.nonfinite = p->d_nonfinite;
   aa.moved = ctx->mode == MODE_REAL ? p->d_moved : nullptr;
-  aa.l2_hint = env_flag("PARO_L2_HINT", 0);
 
   CK(cudaMemsetAsync(p->d_moved, 0, 2 * sizeof(unsigned long long), S));   // moved bytes of this step
   p->moved_host[0] = p->moved_host[1] = 0;
