@@ -233,15 +233,8 @@ __device__ __forceinline__ void launch_exit(const RoundsArgs& a, uint64_t gen0) 
 // paro_step_stats)
 __device__ __forceinline__ void count_moved(const DTask* tk, int64_t ne, unsigned long long& mi,
                                             unsigned long long& me) {
-  const int osz = tk->out_f32 ? 4 : 2;
-  for (int i = 0; i < tk->nin; ++i)
-    if ((tk->peermask >> i) & 1u) {
-      const unsigned long long b = (unsigned long long)ne * (((tk->f32mask >> i) & 1u) ? 4 : 2);
-      if ((tk->intermask >> i) & 1u) me += b;
-      else mi += b;
-    }
-  if (tk->dst_peer == 1) mi += (unsigned long long)ne * osz;
-  if (tk->dst_peer == 2) me += (unsigned long long)ne * osz;
+  mi += (unsigned long long)ne * tk->mv_intra;   // per-element bytes precomputed from the peer masks
+  me += (unsigned long long)ne * tk->mv_inter;
 }
 __device__ __forceinline__ void flush_moved(unsigned long long* moved, unsigned long long mi,
                                             unsigned long long me) {

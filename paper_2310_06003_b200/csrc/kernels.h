@@ -34,7 +34,7 @@ struct DTask {
   uint32_t peermask;    // bit i: input i lives on another rank (pulled over NVLink)
   uint32_t intermask;   // bit i: ... on another group's rank
   int32_t dst_peer;     // result stored into another rank: 1 same group, 2 other group (push)
-  int32_t pad2_;
+  int16_t mv_intra, mv_inter;   // NVLink bytes per element this task moves (pulls + push), by link class
 };
 
 struct DRound {

@@ -283,6 +283,13 @@ DTask resolve(const PlanT* p, const Task& t, int executing_rank, int acc_kind, i
       if (t.in[i].rank / M != executing_rank / M) d.intermask |= 1u << i;
     }
   if (t.dst.rank != executing_rank) d.dst_peer = (t.dst.rank / M != executing_rank / M) ? 2 : 1;
+  for (int i = 0; i < t.nin; ++i)
+    if ((d.peermask >> i) & 1u) {
+      const int b = (!t.in[i].is_raw() && pl.esz[t.in[i].kind] == 4) ? 4 : 2;
+      if ((d.intermask >> i) & 1u) d.mv_inter += b;
+      else d.mv_intra += b;
+    }
+  if (d.dst_peer) (d.dst_peer == 2 ? d.mv_inter : d.mv_intra) += pl.esz[t.dst.kind];
   d.dst = reinterpret_cast<uint16_t*>(ptr_of(t.dst));
   if (t.dst.rank / M != executing_rank / M) d.inter += 1;
   if (acc_kind >= 0 && t.dst.kind == acc_kind) {
