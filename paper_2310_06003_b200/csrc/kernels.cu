@@ -613,7 +613,7 @@ __device__ __forceinline__ bool tile_of(const AdamArgs& a, int64_t t, TileRef& o
 // input, fp32 pre-scaling and hops; the bf16 instantiation keeps the
 // bf16-only arithmetic, constant slot sizes and fewer instructions.
 template <bool kStore, int kThr, bool kWide>
-__global__ void __maxnreg__(72) adam_tma_kernel(const AdamArgs a, int gnin_max, int stages) {
+__global__ void __launch_bounds__(kThr, 1) adam_tma_kernel(const AdamArgs a, int gnin_max, int stages) {
   constexpr int kTmaTile = kThr * 8;   // elements per tile (8 per thread)
   constexpr int kGsz = kWide ? 4 : 2;  // bytes per g_hat element in a stage slot
   extern __shared__ __align__(128) unsigned char smem[];
@@ -929,7 +929,7 @@ __device__ __forceinline__ void rt_fold_generic(const DTask* tk, unsigned char* 
 // wait_group.read, and every bulk store has completed before the next peer
 // barrier publishes the round.
 // <= 64 registers (launch bounds 256 x 4): a rounds CTA (256 x 64) must fit
-// beside a 512-thread Adam CTA (512 x 72, __maxnreg__) in the SM's 64 K
+// beside a 512-thread Adam CTA (512 x <= 84: launch bounds (512, 1)) in the SM's 64 K
 // registers, so collectives and updates co-run
 // kGen: the launch has fp32-wire or nested (one-shot) tasks; their folds are
 // compiled into a separate instantiation so the common bf16 path keeps every
