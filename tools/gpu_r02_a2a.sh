@@ -4,6 +4,8 @@ cd "$GRAFT_REPO_ROOT" 2>/dev/null || cd /root/repo
 mkdir -p gpurun_out
 NG=$(nvidia-smi -L | wc -l)
 python -c 'import __graft_entry__ as g; g.build()' > gpurun_out/build.log 2>&1 || { echo build failed; exit 1; }
+CUDA_VISIBLE_DEVICES=0 timeout 900 python bench.py --no-e2e --no-cpu-baseline > gpurun_out/bench_n1_c.json 2>/dev/null
+python -c "import json; d=json.load(open('gpurun_out/bench_n1_c.json')); print(d['ms_per_step'], d['roofline']['frac'], d['roofline']['kernel'], d['clocks'])"
 OUT=gpurun_out/a2a_${NG}gpu.jsonl
 : > $OUT
 run() { timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $NG --master-addr 127.0.0.1 --master-port 29651 tools/coll_bench.py "$@" >> $OUT 2>> gpurun_out/a2a.err; }
