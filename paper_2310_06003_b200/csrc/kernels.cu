@@ -813,12 +813,14 @@ constexpr int kRtMaxStages = 8;
 constexpr int kRtMaxIn = kDevMaxIn;
 constexpr int kRtSmem = kRtStages * 3 * kRtSlotB;   // 96 KB
 
-// log2 of the slot bytes: 8 KB up to 3 inputs, else the largest power of two
-// with 4 stages x max_in slots <= 96 KB (4 KB for 4-6 inputs, 2 KB for 7-12, 1 KB)
+// log2 of the slot bytes: 8 KB up to 4 inputs, else the largest power of two
+// with 3 stages x max_in slots <= 96 KB (4 KB for 5-8 inputs, 2 KB for 9-16)
 int rt_slot_lg(int max_in) {
   if (max_in <= 3) return 13;
-  int lg = 13;
-  while (lg > 10 && (kRtStages * max_in) << lg > kRtSmem) --lg;
+  static const int env = std::getenv("PARO_RT_SLOT_LG") ? std::atoi(std::getenv("PARO_RT_SLOT_LG")) : 0;
+  int lg = 13;   // the largest slot with >= 3 stages in 96 KB (larger bulk copies move more per request)
+  while (lg > 10 && (3 * max_in) << lg > kRtSmem) --lg;
+  if (env >= 10 && env <= 13 && (2 * max_in) << env <= kRtSmem) lg = env;
   return lg;
 }
 int rt_slot_bytes(int max_in) { return 1 << rt_slot_lg(max_in); }

@@ -710,9 +710,12 @@ void Planner::build_schedule() {
     // ---- world-reaching AG of segments in place in a bucket-layout buffer.  Returns rounds used.
     auto emit_world_ag = [&](Launch& L, const std::function<Ref(int)>& base, int round0) -> int {
       if (topo == 6) {  // one-shot: every segment copied from its owner in one round
+        // peers in rotated order (r+1, r+2, ...): tiles are dealt in task order, so
+        // at any moment every rank reads from a different peer (no egress hotspot;
+        // ascending order measured 1.8x slower at 2x2, profiles/r02/a2a_4gpu.jsonl)
         for (int r = 0; r < N; ++r)
-          for (int x = 0; x < N; ++x) {
-            if (x == r) continue;
+          for (int i = 1; i < N; ++i) {
+            const int x = (r + i) % N;
             const int64_t o = int64_t(seg(grp(x), pos(x))) * C;
             L.add(round0, r, make_task(C, {at(base(x), o)}, at(base(r), o)));
           }
@@ -834,13 +837,13 @@ void Planner::build_schedule() {
     };
     // AG_E in place in a chunk-layout buffer (segment j of chunk p at j*C)
     auto emit_ag_e = [&](Launch& L, const std::function<Ref(int)>& base, int round0) -> int {
-      if (topo == 6 && g > 1) {   // one-shot: the g-1 same-position peers' segments in one round
+      if (topo == 6 && g > 1) {   // one-shot: the g-1 same-position peers' segments in one round (rotated)
         for (int r = 0; r < N; ++r)
-          for (int jj = 0; jj < g; ++jj)
-            if (jj != grp(r)) {
-              const int x = rank_of(jj, pos(r));
-              L.add(round0, r, make_task(C, {at(base(x), int64_t(jj) * C)}, at(base(r), int64_t(jj) * C)));
-            }
+          for (int i = 1; i < g; ++i) {
+            const int jj = (grp(r) + i) % g;
+            const int x = rank_of(jj, pos(r));
+            L.add(round0, r, make_task(C, {at(base(x), int64_t(jj) * C)}, at(base(r), int64_t(jj) * C)));
+          }
         return 1;
       }
       int used = 0;
@@ -852,13 +855,13 @@ void Planner::build_schedule() {
       return used;
     };
     auto emit_ag_i = [&](Launch& L, const std::function<Ref(int)>& base, int round0) -> int {
-      if (topo == 6 && M > 1) {   // one-shot: the M-1 group peers' chunks in one round
+      if (topo == 6 && M > 1) {   // one-shot: the M-1 group peers' chunks in one round (rotated)
         for (int r = 0; r < N; ++r)
-          for (int pp = 0; pp < M; ++pp)
-            if (pp != pos(r)) {
-              const int x = rank_of(grp(r), pp);
-              L.add(round0, r, make_task(chunk, {at(base(x), int64_t(pp) * chunk)}, at(base(r), int64_t(pp) * chunk)));
-            }
+          for (int i = 1; i < M; ++i) {
+            const int pp = (pos(r) + i) % M;
+            const int x = rank_of(grp(r), pp);
+            L.add(round0, r, make_task(chunk, {at(base(x), int64_t(pp) * chunk)}, at(base(r), int64_t(pp) * chunk)));
+          }
         return 1;
       }
       int used = 0;
@@ -951,7 +954,10 @@ void Planner::build_schedule() {
       const int64_t extra = (int64_t)(N - 1) * (N - 2) * n * opt.wire / N;
       if (topo == 6 && OS == LV_N && (N == 2 || extra <= kOneRoundExtraBytes)) {
         for (int r = 0; r < N; ++r)
-          for (int k = 0; k < N; ++k) L.add(0, r, oneshot_task(k, at(ghat_base(r), int64_t(k) * C)));
+          for (int i = 0; i < N; ++i) {   // segments in rotated order, like the one-shot AG
+            const int k = (seg(grp(r), pos(r)) + i) % N;
+            L.add(0, r, oneshot_task(k, at(ghat_base(r), int64_t(k) * C)));
+          }
         return;
       }
       int used = emit_world_rs(L, 0);
