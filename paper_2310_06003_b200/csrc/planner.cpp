@@ -19,7 +19,7 @@ namespace {
 constexpr int64_t kQuantum = 64;      // elements per shard granule (R21)
 constexpr int64_t kAlignElems = 128;  // 256-byte alignment of buffer kinds
 constexpr int64_t kOneRoundExtraBytes = int64_t(6) << 20;   // one-shot AR: extra bytes worth one barrier
-constexpr int64_t kOneShotMaxBytes = int64_t(32) << 20;     // one-shot topology: larger buckets use HO-Ring
+constexpr int64_t kOneShotMaxBytes = int64_t(256) << 20;    // one-shot topology: larger buckets use HO-Ring
 
 // PARO_ONESHOT_MAX_MB overrides the threshold (measurement runs)
 int64_t oneshot_max_bytes() {
@@ -465,10 +465,10 @@ void Planner::build_schedule() {
   for (size_t b = 0; b < buckets.size(); ++b) {
     BucketSchedule& S = sched[b];
     const int64_t s = buckets[b].first, n = buckets[b].second;
-    // one-shot collectives pay off while latency-bound; on one NVSwitch box the
-    // all-to-all pulls move less than a ring once a bucket is large (measured:
-    // 2x2 all-reduce 408 vs 627 GB/s busbw at 1 GiB, profiles/r02), so larger
-    // buckets run the HO-Ring schedules (the same canonical bits)
+    // one-shot collectives win up to 256 MiB buckets at 2x2 (2 barriers instead
+    // of 4, rotated peer order: 666 vs 682 us at 256 MiB; 512 MiB buckets 2604 vs
+    // 2573 us, profiles/r02/oneshot_a2a_rotated_4gpu.jsonl), so larger buckets
+    // run the HO-Ring schedules (the same canonical bits)
     topo = (opt.topology == 6 && n * opt.wire > oneshot_max_bytes()) ? 0 : opt.topology;
     const int64_t C = n / N, chunk = n / M;
     const int par = int(b % kStageSets);

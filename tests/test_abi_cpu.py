@@ -394,12 +394,12 @@ def test_oneshot_allreduce_one_or_two_rounds(N, M):
 @pytest.mark.parametrize("N,M", [(8, 4), (4, 2)])
 def test_oneshot_large_buckets_run_ho_ring(N, M):
     """The one-shot topology keeps one-shot schedules while a bucket is small
-    (latency-bound, <= 32 MiB of payload) and hands larger buckets to the
+    (<= 256 MiB of payload) and hands larger buckets to the
     HO-Ring schedules (the same canonical bits; all-to-all pulls move less than
     a ring on one NVSwitch box): a large-bucket plan equals the HO-Ring plan in
     rounds and bytes."""
     ctx = paro.Context(N, M)
-    big = N * 64 * (1 << 16) * 4          # > 32 MiB of bf16 per bucket
+    big = N * 64 * (1 << 16) * 32         # > 256 MiB of bf16 per bucket
     for code in ("NNN", "IIG", "GGG", "NIG"):
         one = paro.Plan(ctx, code, [2 * big], bucket_elems=big, topology="oneshot", fuse_allreduce=False).info()
         ho = paro.Plan(ctx, code, [2 * big], bucket_elems=big, topology="ho", fuse_allreduce=False).info()
