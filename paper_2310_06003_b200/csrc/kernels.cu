@@ -796,6 +796,193 @@ __global__ void __launch_bounds__(kThr, 1) adam_tma_kernel(const AdamArgs a, int
   }
 }
 
+// ------------------------------------------------------------- Adam, warp-specialized TMA pipeline
+// The TMA-store Adam with a dedicated producer warp: the kThr compute threads
+// never wait for each other.  Per stage two mbarriers: `full` (the bulk loads
+// landed) and `done` (every compute thread wrote its results back into the
+// stage and fenced them for the async proxy).  The producer lane waits on
+// `done`, sends the tile's results out with bulk stores, and refills the stage
+// of the previous tile as soon as its stores have read it (wait_group.read 1).
+// Same arithmetic, bits and bytes as adam_tma_kernel<true, kThr, kWide>.
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+template <int kThr, bool kWide>
+__global__ void __launch_bounds__(kThr + 32, 1) adam_tma_ws_kernel(const AdamArgs a, int gnin_max, int stages) {
+  constexpr int kTmaTile = kThr * 8;
+  constexpr int kGsz = kWide ? 4 : 2;
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ uint64_t full_bar[4], done_bar[4];
+  if (a.skip && *a.skip) return;   // two-phase step: non-finite gradients, update skipped
+  const AdamScal c{a.b1, a.omb1, a.b2, a.omb2, a.step_size, a.bc2s, a.eps, a.decay, unscale_of(a), a.alpha,
+                   a.has_wd};
+  constexpr size_t g_bytes = (size_t)kTmaTile * kGsz, f_bytes = (size_t)kTmaTile * 4;
+  const size_t stage_bytes = gnin_max * g_bytes + 3 * f_bytes;
+  int64_t total = 0;
+  for (int i = 0; i < a.nseg; ++i) total += (a.seg[i].n8 * 8 + kTmaTile - 1) / kTmaTile;
+  const int64_t mine = (total > blockIdx.x) ? (total - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  const bool producer = threadIdx.x >= kThr;
+  if (threadIdx.x == kThr) {
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&done_bar[s], kThr);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  double nsq = 0.0;
+  int bad = 0;
+  if (producer) {
+    if (threadIdx.x == kThr) {
+      int64_t done = 0;
+      auto issue = [&](int64_t k) {   // load tile k of this CTA into stage k % stages
+        TileRef tr;
+        tile_of<kTmaTile>(a, blockIdx.x + k * gridDim.x, tr);
+        const AdamSeg& sg = a.seg[tr.seg];
+        const int s = (int)(k % stages);
+        unsigned char* base = smem + s * stage_bytes;
+        const uint32_t fb = (uint32_t)tr.n * 4;
+        done += tr.n;
+        if (kWide) {
+          uint32_t tx = 3 * fb;
+          for (int i = 0; i < sg.gnin; ++i) tx += (uint32_t)tr.n * (((sg.gf32 >> i) & 1u) ? 4 : 2);
+          mbar_expect_tx(&full_bar[s], tx);
+          for (int i = 0; i < sg.gnin; ++i) {
+            const int es = ((sg.gf32 >> i) & 1u) ? 4 : 2;
+            bulk_g2s(base + i * g_bytes, reinterpret_cast<const unsigned char*>(sg.gin[i]) + (size_t)tr.start * es,
+                     (uint32_t)tr.n * es, &full_bar[s]);
+          }
+        } else {
+          const uint32_t gb = (uint32_t)tr.n * 2;
+          mbar_expect_tx(&full_bar[s], sg.gnin * gb + 3 * fb);
+          for (int i = 0; i < sg.gnin; ++i) bulk_g2s(base + i * g_bytes, sg.gin[i] + tr.start, gb, &full_bar[s]);
+        }
+        unsigned char* fbase = base + gnin_max * g_bytes;
+        bulk_g2s(fbase, sg.master + tr.start, fb, &full_bar[s]);
+        bulk_g2s(fbase + f_bytes, sg.m + tr.start, fb, &full_bar[s]);
+        bulk_g2s(fbase + 2 * f_bytes, sg.v + tr.start, fb, &full_bar[s]);
+      };
+      for (int64_t k = 0; k < min((int64_t)stages, mine); ++k) issue(k);
+      for (int64_t k = 0; k < mine; ++k) {
+        const int s = (int)(k % stages);
+        mbar_wait(&done_bar[s], (uint32_t)((k / stages) & 1));   // the compute threads' results are in
+        TileRef tr;
+        tile_of<kTmaTile>(a, blockIdx.x + k * gridDim.x, tr);
+        const AdamSeg& sg = a.seg[tr.seg];
+        unsigned char* base = smem + s * stage_bytes;
+        const uint32_t gb = (uint32_t)tr.n * 2, fb = (uint32_t)tr.n * 4;
+        const unsigned char* fbase = base + gnin_max * g_bytes;
+        bulk_s2g(sg.master + tr.start, fbase, fb);
+        bulk_s2g(sg.m + tr.start, fbase + f_bytes, fb);
+        bulk_s2g(sg.v + tr.start, fbase + 2 * f_bytes, fb);
+        bulk_s2g(sg.param + tr.start, base, gb);
+        for (int i = 0; i < sg.npush; ++i) bulk_s2g(sg.push[i] + tr.start, base, gb);
+        bulk_commit();
+        bulk_wait_read<1>();   // the previous tile's stores have read their stage: refill it
+        if (k >= 1 && k - 1 + stages < mine) issue(k - 1 + stages);
+      }
+      bulk_wait_all();
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      __threadfence_system();
+      if (a.moved && done > 0) {   // NVLink bytes of this CTA's tiles (real mode: one segment)
+        const AdamSeg& sg = a.seg[0];
+        unsigned long long mi = 0, me = 0;
+        for (int i = 0; i < sg.gnin; ++i)
+          if ((sg.gpeer >> i) & 1u)
+            (((sg.ginter >> i) & 1u) ? me : mi) += (unsigned long long)done * (((sg.gf32 >> i) & 1u) ? 4 : 2);
+        for (int i = 0; i < sg.npush; ++i) (((sg.pinter >> i) & 1u) ? me : mi) += (unsigned long long)done * 2;
+        flush_moved(a.moved, mi, me);
+      }
+    }
+  } else {
+    for (int64_t k = 0; k < mine; ++k) {
+      const int s = (int)(k % stages);
+      mbar_wait(&full_bar[s], (uint32_t)((k / stages) & 1));
+      TileRef tr;
+      tile_of<kTmaTile>(a, blockIdx.x + k * gridDim.x, tr);
+      const AdamSeg& sg = a.seg[tr.seg];
+      unsigned char* base = smem + s * stage_bytes;
+      const int e0 = threadIdx.x * 8;
+      const bool act = e0 < tr.n;
+      float* fw = reinterpret_cast<float*>(base + gnin_max * g_bytes);
+      float w[8], m[8], v[8];
+      uint4 pk = make_uint4(0, 0, 0, 0);
+      if (act) {
+        float g[8];
+        if (kWide) {
+          auto ld = [&](int i, float f[8]) {
+            if ((sg.gf32 >> i) & 1u) {
+              const float4* q = reinterpret_cast<const float4*>(base + i * g_bytes + (size_t)e0 * 4);
+              f4x2(q[0], q[1], f);
+            } else {
+              unpack8(*reinterpret_cast<const uint4*>(base + i * g_bytes + (size_t)e0 * 2), f);
+              if ((sg.graw >> i) & 1u) mul8(f, c.alpha);
+            }
+          };
+          ld(0, g);
+          for (int i = 1; i < sg.gnin; ++i) {
+            float x[8];
+            ld(i, x);
+            add8(g, x);
+          }
+        } else {
+          unpack8(*reinterpret_cast<const uint4*>(base + e0 * 2), g);
+          if (sg.graw & 1u) scale_round8(g, c.alpha);
+          for (int i = 1; i < sg.gnin; ++i) {
+            float x[8];
+            unpack8(*reinterpret_cast<const uint4*>(base + i * g_bytes + e0 * 2), x);
+            if ((sg.graw >> i) & 1u) scale_round8(x, c.alpha);
+            hop8(g, x);
+          }
+        }
+        const float4 w0 = *reinterpret_cast<const float4*>(fw + e0), w1 = *reinterpret_cast<const float4*>(fw + e0 + 4);
+        const float4 m0 = *reinterpret_cast<const float4*>(fw + kTmaTile + e0);
+        const float4 m1 = *reinterpret_cast<const float4*>(fw + kTmaTile + e0 + 4);
+        const float4 v0 = *reinterpret_cast<const float4*>(fw + 2 * kTmaTile + e0);
+        const float4 v1 = *reinterpret_cast<const float4*>(fw + 2 * kTmaTile + e0 + 4);
+        f4x2(w0, w1, w);
+        f4x2(m0, m1, m);
+        f4x2(v0, v1, v);
+        const bool in_norm = sg.in_norm != 0;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) adam_elem(g[e], w[e], m[e], v[e], c, nsq, bad, in_norm);
+        pk = pack8(w);
+      }
+      // fp32 inputs: every compute thread has read its input-0 bytes before the
+      // bf16 outputs are written over them (named barrier of the compute threads)
+      if (kWide) asm volatile("bar.sync 1, %0;" ::"n"(kThr) : "memory");
+      if (act) {
+        *reinterpret_cast<float4*>(fw + e0) = make_float4(w[0], w[1], w[2], w[3]);
+        *reinterpret_cast<float4*>(fw + e0 + 4) = make_float4(w[4], w[5], w[6], w[7]);
+        *reinterpret_cast<float4*>(fw + kTmaTile + e0) = make_float4(m[0], m[1], m[2], m[3]);
+        *reinterpret_cast<float4*>(fw + kTmaTile + e0 + 4) = make_float4(m[4], m[5], m[6], m[7]);
+        *reinterpret_cast<float4*>(fw + 2 * kTmaTile + e0) = make_float4(v[0], v[1], v[2], v[3]);
+        *reinterpret_cast<float4*>(fw + 2 * kTmaTile + e0 + 4) = make_float4(v[4], v[5], v[6], v[7]);
+        *reinterpret_cast<uint4*>(base + e0 * 2) = pk;   // over g_hat input 0 (consumed)
+      }
+      fence_proxy_async_smem();   // this thread's smem writes -> visible to the bulk-copy engine
+      mbar_arrive(&done_bar[s]);
+    }
+  }
+  // norm partials (the producer warp contributes zeros)
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) nsq += __shfl_xor_sync(0xffffffffu, nsq, o);
+  __shared__ double s_part[(kThr + 32) / 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) s_part[wid] = nsq;
+  const int any_bad = __syncthreads_or(bad);
+  if (wid == 0) {
+    double x = (lane < (int)(blockDim.x / 32)) ? s_part[lane] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    if (lane == 0) {
+      a.partials[blockIdx.x] = x;
+      if (any_bad) atomicOr(a.nonfinite, 1);
+    }
+  }
+}
+
 // ------------------------------------------------------------- rounds, TMA pipeline
 // The collective rounds with the operand streams moved by the bulk-copy engine:
 // for every tile of a fold task, one thread issues cp.async.bulk for each input
@@ -1227,7 +1414,9 @@ static cudaError_t set_carveouts() {
                        (const void*)adam_tma_kernel<false, 512, false>, (const void*)adam_tma_kernel<true, 512, false>,
                        (const void*)adam_tma_kernel<true, 256, false>, (const void*)adam_tma_kernel<false, 256, false>,
                        (const void*)adam_tma_kernel<false, 512, true>, (const void*)adam_tma_kernel<true, 512, true>,
-                       (const void*)adam_tma_kernel<true, 256, true>, (const void*)adam_tma_kernel<false, 256, true>};
+                       (const void*)adam_tma_kernel<true, 256, true>, (const void*)adam_tma_kernel<false, 256, true>,
+                       (const void*)adam_tma_ws_kernel<512, false>, (const void*)adam_tma_ws_kernel<256, false>,
+                       (const void*)adam_tma_ws_kernel<512, true>, (const void*)adam_tma_ws_kernel<256, true>};
   for (const void* f : fns) {
     cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout,
                                          (int)cudaSharedmemCarveoutMaxShared);
@@ -1300,6 +1489,12 @@ cudaError_t launch_adam(const AdamArgs& a, int grid, cudaStream_t s, int cap_two
   return cudaGetLastError();
 }
 
+// warp-specialized TMA-store Adam (adam_tma_ws_kernel); PARO_ADAM_WS=0/1 for A/B
+bool adam_ws_on() {
+  static const int env = std::getenv("PARO_ADAM_WS") ? std::atoi(std::getenv("PARO_ADAM_WS")) : -1;
+  return env == 1;
+}
+
 // TMA pipeline: persistent grid (one CTA per SM), stages sized to the budget.
 // smem_budget_kb sets the stage count (2-4); hard_kb is what the SM can give
 // Adam beside the co-running collective CTA (its stages are the rest of the
@@ -1323,7 +1518,9 @@ cudaError_t launch_adam_tma(const AdamArgs& a, int sms, cudaStream_t s, int smem
     for (const void* f : {(const void*)adam_tma_kernel<false, 512, false>, (const void*)adam_tma_kernel<true, 512, false>,
                           (const void*)adam_tma_kernel<true, 256, false>, (const void*)adam_tma_kernel<false, 256, false>,
                           (const void*)adam_tma_kernel<false, 512, true>, (const void*)adam_tma_kernel<true, 512, true>,
-                          (const void*)adam_tma_kernel<true, 256, true>, (const void*)adam_tma_kernel<false, 256, true>}) {
+                          (const void*)adam_tma_kernel<true, 256, true>, (const void*)adam_tma_kernel<false, 256, true>,
+                          (const void*)adam_tma_ws_kernel<512, false>, (const void*)adam_tma_ws_kernel<256, false>,
+                          (const void*)adam_tma_ws_kernel<512, true>, (const void*)adam_tma_ws_kernel<256, true>}) {
       cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
       if (e != cudaSuccess) return e;
     }
@@ -1334,6 +1531,11 @@ cudaError_t launch_adam_tma(const AdamArgs& a, int sms, cudaStream_t s, int smem
   auto raw = [&](int tile, int kb) { return (int)(((size_t)kb * 1024) / stage_bytes(tile)); };
   auto clampst = [](int st, int lo) { return st > 4 ? 4 : (st < lo ? lo : st); };
   const bool wide = gsz == 4;
+#define PARO_ADAM_WS_LAUNCH(KT)                                                                          \
+  do {                                                                                                   \
+    if (wide) adam_tma_ws_kernel<KT, true><<<sms, KT + 32, stage_bytes(KT * 8) * st, s>>>(a, gmax, st);  \
+    else adam_tma_ws_kernel<KT, false><<<sms, KT + 32, stage_bytes(KT * 8) * st, s>>>(a, gmax, st);      \
+  } while (0)
 #define PARO_ADAM_LAUNCH(KS, KT)                                                                    \
   do {                                                                                              \
     if (wide) adam_tma_kernel<KS, KT, true><<<sms, KT, stage_bytes(KT * 8) * st, s>>>(a, gmax, st); \
@@ -1352,14 +1554,25 @@ cudaError_t launch_adam_tma(const AdamArgs& a, int sms, cudaStream_t s, int smem
     }
   } else if (raw(4096, smem_budget_kb) >= 3) {
     st = clampst(raw(4096, smem_budget_kb), 3);
-    v = ADAM_TMA_ST_512;
-    PARO_ADAM_LAUNCH(true, 512);
+    if (adam_ws_on()) {
+      v = ADAM_TMA_WS_512;
+      PARO_ADAM_WS_LAUNCH(512);
+    } else {
+      v = ADAM_TMA_ST_512;
+      PARO_ADAM_LAUNCH(true, 512);
+    }
   } else {
     st = clampst(raw(2048, smem_budget_kb), 3);
-    v = ADAM_TMA_ST_256;
-    PARO_ADAM_LAUNCH(true, 256);
+    if (adam_ws_on()) {
+      v = ADAM_TMA_WS_256;
+      PARO_ADAM_WS_LAUNCH(256);
+    } else {
+      v = ADAM_TMA_ST_256;
+      PARO_ADAM_LAUNCH(true, 256);
+    }
   }
 #undef PARO_ADAM_LAUNCH
+#undef PARO_ADAM_WS_LAUNCH
   if (variant) *variant = v;
   if (stages) *stages = st;
   return cudaGetLastError();

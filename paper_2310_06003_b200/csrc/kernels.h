@@ -133,7 +133,9 @@ enum AdamVariant : int {
   ADAM_TMA_LD_512 = 1,   // adam_tma_kernel<false, 512>: bulk-copy loads, thread stores, 4096-elem tiles
   ADAM_TMA_ST_512 = 2,   // adam_tma_kernel<true, 512>: bulk-copy loads and stores
   ADAM_TMA_ST_256 = 3,   // adam_tma_kernel<true, 256>: same, 2048-elem tiles (small budget)
-  ADAM_TMA_LD_256 = 4    // adam_tma_kernel<false, 256>: thread stores, 2048-elem tiles
+  ADAM_TMA_LD_256 = 4,   // adam_tma_kernel<false, 256>: thread stores, 2048-elem tiles
+  ADAM_TMA_WS_512 = 5,   // adam_tma_ws_kernel<512>: bulk loads + stores, dedicated producer warp
+  ADAM_TMA_WS_256 = 6    // adam_tma_ws_kernel<256>
 };
 cudaError_t launch_adam_tma(const AdamArgs& a, int sms, cudaStream_t s, int smem_budget_kb, int tma_store,
                             int hard_kb, int* variant, int* stages);

@@ -79,7 +79,8 @@ class paro_profile_t(C.Structure):
                 ("adam_variant", C.c_int32), ("adam_stages", C.c_int32)]
 
 ADAM_VARIANTS = {-1: None, 0: "adam_kernel", 1: "adam_tma_kernel<false,512>", 2: "adam_tma_kernel<true,512>",
-                 3: "adam_tma_kernel<true,256>", 4: "adam_tma_kernel<false,256>"}
+                 3: "adam_tma_kernel<true,256>", 4: "adam_tma_kernel<false,256>", 5: "adam_tma_ws_kernel<512>",
+                 6: "adam_tma_ws_kernel<256>"}
 
 
 class paro_advise_in_t(C.Structure):
