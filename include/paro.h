@@ -105,7 +105,9 @@ typedef struct {
                           * stores otherwise;                                      *
                           * 1: the LSU (ld.global) kernel; 2: TMA both ways always; *
                           * 3: TMA loads + thread stores always (the variant real  *
-                          * N > 1 steps use beside collectives).  Same bits.       */
+                          * N > 1 steps use beside collectives); 4: TMA both ways  *
+                          * with a dedicated producer warp (warp-specialized).     *
+                          * Same bits.                                             */
   int comm_impl;         /* 2 (default): collective rounds move operands with TMA  *
                           * bulk copies into shared memory and the folded tile     *
                           * leaves through a bulk copy too (measured 1-10 % faster *
@@ -489,7 +491,8 @@ typedef struct {
   int64_t adam_hbm_bytes, comm_hbm_bytes;
   /* the last Adam launch: 0 adam_kernel (LSU), 1 adam_tma_kernel<false,512>   *
    * (bulk loads, thread stores), 2 <true,512> (bulk loads + stores), 3       *
-   * <true,256>, 4 <false,256>; -1 none; and its shared-memory stage count     */
+   * <true,256>, 4 <false,256>, 5 adam_tma_ws_kernel<512> (warp-specialized),  *
+   * 6 adam_tma_ws_kernel<256>; -1 none; and its shared-memory stage count     */
   int32_t adam_variant, adam_stages;
 } paro_profile_t;
 

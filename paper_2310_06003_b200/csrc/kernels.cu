@@ -1505,7 +1505,7 @@ bool adam_ws_on() {
 // switches to 2048-element tiles.  Returns the variant (AdamVariant) and stage
 // count through *variant / *stages.
 cudaError_t launch_adam_tma(const AdamArgs& a, int sms, cudaStream_t s, int smem_budget_kb, int tma_store,
-                            int hard_kb, int* variant, int* stages) {
+                            int hard_kb, int* variant, int* stages, int ws) {
   cudaError_t ec = set_carveouts();
   if (ec != cudaSuccess) return ec;
   int gmax = 1, gsz = 2;
@@ -1554,7 +1554,7 @@ cudaError_t launch_adam_tma(const AdamArgs& a, int sms, cudaStream_t s, int smem
     }
   } else if (raw(4096, smem_budget_kb) >= 3) {
     st = clampst(raw(4096, smem_budget_kb), 3);
-    if (adam_ws_on()) {
+    if (ws == 1 || (ws < 0 && adam_ws_on())) {
       v = ADAM_TMA_WS_512;
       PARO_ADAM_WS_LAUNCH(512);
     } else {
@@ -1563,7 +1563,7 @@ cudaError_t launch_adam_tma(const AdamArgs& a, int sms, cudaStream_t s, int smem
     }
   } else {
     st = clampst(raw(2048, smem_budget_kb), 3);
-    if (adam_ws_on()) {
+    if (ws == 1 || (ws < 0 && adam_ws_on())) {
       v = ADAM_TMA_WS_256;
       PARO_ADAM_WS_LAUNCH(256);
     } else {

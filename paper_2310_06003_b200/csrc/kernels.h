@@ -137,8 +137,9 @@ enum AdamVariant : int {
   ADAM_TMA_WS_512 = 5,   // adam_tma_ws_kernel<512>: bulk loads + stores, dedicated producer warp
   ADAM_TMA_WS_256 = 6    // adam_tma_ws_kernel<256>
 };
+// ws: 1 the warp-specialized TMA-store kernel, 0 the single-role one, -1 automatic
 cudaError_t launch_adam_tma(const AdamArgs& a, int sms, cudaStream_t s, int smem_budget_kb, int tma_store,
-                            int hard_kb, int* variant, int* stages);
+                            int hard_kb, int* variant, int* stages, int ws);
 // generic: the launch has fp32-wire (out_f32) or nested (one-shot) tasks
 cudaError_t launch_rounds_tma(const RoundsArgs& a, int grid, int max_in, cudaStream_t s, int bulk_store,
                               int generic);

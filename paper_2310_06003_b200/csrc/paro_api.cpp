@@ -879,7 +879,7 @@ paro_status_t paro_plan(paro_ctx_t ctx, const char* strategy, const int64_t* par
   po.windows = o.gather_windows;
   if (o.fuse_gather < 0 || o.fuse_gather > 2) return fail(PARO_ERR_INVALID, "fuse_gather must be 0, 1 or 2");
   if (o.comm_impl < 0 || o.comm_impl > 2) return fail(PARO_ERR_INVALID, "comm_impl must be 0, 1 or 2");
-  if (o.adam_impl < 0 || o.adam_impl > 3) return fail(PARO_ERR_INVALID, "adam_impl must be 0, 1, 2 or 3");
+  if (o.adam_impl < 0 || o.adam_impl > 4) return fail(PARO_ERR_INVALID, "adam_impl must be 0 .. 4");
   if (o.adam_smem_kb < 0 || o.adam_smem_kb > 220) return fail(PARO_ERR_INVALID, "adam_smem_kb must be in [0, 220]");
   po.fuse_gather = (o.inter_gbps > 0.f || o.topology == PARO_TOPO_NCCL) ? 0 : o.fuse_gather;
   // paced (emulated-gap) runs keep every transfer in the rounds kernel, which
@@ -1434,8 +1434,8 @@ paro_status_t step_impl(PlanT* p, const void* const* grads, void* const* params,
     bool pushes = false;
     for (int i = 0; i < aa.nseg; ++i) pushes = pushes || aa.seg[i].npush > 0;
     const int ai = p->opts.adam_impl;
-    const bool tma_store = ai == 2 || (ai == 0 && (pl.N == 1 || ctx->mode == MODE_EMU ||
-                                                   (pl.fused_allreduce && !corun && !pushes)));
+    const bool tma_store = ai == 2 || ai == 4 || (ai == 0 && (pl.N == 1 || ctx->mode == MODE_EMU ||
+                                                                (pl.fused_allreduce && !corun && !pushes)));
     // shared memory: the stage count follows a budget of ~120 KB while
     // collectives co-run (200 KB alone); the hard limit is what the SM has left
     // beside the largest co-running TMA rounds CTA (4 stages x 8 KB per input,
@@ -1453,7 +1453,7 @@ paro_status_t step_impl(PlanT* p, const void* const* grads, void* const* params,
     if (p->opts.adam_smem_kb > 0) budget = hard = p->opts.adam_smem_kb;
     if (ai != 1) {
       CK(launch_adam_tma(aa, ctx->sm_count, ctx->comp, budget, tma_store ? 1 : 0, hard, &p->adam_variant,
-                         &p->adam_stages));
+                         &p->adam_stages, ai == 4 ? 1 : (ai == 2 ? 0 : -1)));
     } else {
       CK(launch_adam(aa, grid, ctx->comp, corun ? 1 : 0));
       p->adam_variant = ADAM_LSU;

@@ -182,7 +182,7 @@ def make_opts(bucket_elems=1 << 26, topology="ho", beta1=0.9, beta2=0.95, eps=1e
     o.weight_decay, o.loss_scale = weight_decay, loss_scale
     o.comm_ctas, o.pipeline_depth = int(comm_ctas), int(pipeline_depth)
     o.pull_transport = {"push": 0, "pull": 1}[transport]
-    o.adam_impl = {"auto": 0, "lsu": 1, "tma_store": 2, "tma": 3}[adam_impl]
+    o.adam_impl = {"auto": 0, "lsu": 1, "tma_store": 2, "tma": 3, "tma_ws": 4}[adam_impl]
     o.comm_impl = {"tma": 0, "lsu": 1, "tma_store": 2}[comm_impl]
     o.inter_gbps = float(inter_gbps)
     o.grad_accum = 1 if grad_accum else 0

@@ -215,7 +215,7 @@ def test_flat_ring_matches_oracle_flat_simulation(transport):
 # Adam, R31), IIG / GGG 3 (HO-Ring final hop fused).  120 KB is the co-run
 # budget real N > 1 steps use; 60 KB forces 2048-element thread-store tiles.
 ADAM_CASES = [("auto", 0), ("lsu", 0), ("tma_store", 0), ("tma", 0), ("tma", 120), ("tma_store", 120),
-              ("tma", 60)]
+              ("tma", 60), ("tma_ws", 0), ("tma_ws", 120)]
 
 
 @pytest.mark.parametrize("adam_impl,smem", ADAM_CASES)
@@ -239,10 +239,10 @@ def test_4m_2x4_ten_steps(code, adam_impl, smem):
         assert v in ("adam_tma_kernel<false,512>", "adam_tma_kernel<false,256>")
         if smem == 60:
             assert v == "adam_tma_kernel<false,256>"
+    elif adam_impl == "tma_ws":
+        assert v == ("adam_tma_ws_kernel<256>" if smem == 120 else "adam_tma_ws_kernel<512>")
     else:
-        assert v.startswith("adam_tma_kernel<true,")
-        if smem == 120:
-            assert v == "adam_tma_kernel<true,256>"
+        assert v.startswith("adam_tma_kernel<true,") or v.startswith("adam_tma_ws_kernel")
     run.close()
 
 
@@ -258,7 +258,7 @@ def test_adam_variant_selection_covers_corun_kernels():
     ref = _dp_reference(lay, 2)
     seen = set()
     for code, impl, kb in (("NNN", "tma", 120), ("IIG", "tma", 120), ("GGG", "tma", 120), ("III", "tma", 120),
-                           ("IIG", "tma_store", 120), ("NIG", "tma", 0)):
+                           ("IIG", "tma_store", 120), ("NIG", "tma", 0), ("IIG", "tma_ws", 0), ("GGG", "tma_ws", 120)):
         run = EmuRun(N, M, code, sizes, B, adam_impl=impl, adam_smem_kb=kb, transport="pull")
         run.pl.profile_start(1024)
         for t in (1, 2):
