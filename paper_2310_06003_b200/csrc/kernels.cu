@@ -1511,7 +1511,9 @@ cudaError_t launch_adam_tma(const AdamArgs& a, int sms, cudaStream_t s, int smem
   int gmax = 1, gsz = 2;
   for (int i = 0; i < a.nseg; ++i) {
     gmax = a.seg[i].gnin > gmax ? a.seg[i].gnin : gmax;
-    if (a.seg[i].gf32) gsz = 4;
+    // fp32 wire: fp32 arithmetic even when every input is a raw bf16 gradient
+    // (a fused one-shot hop or the fused all-reduce at M = 1), 4-byte slots
+    if (a.seg[i].gf32 || a.seg[i].gwide) gsz = 4;
   }
   static bool attr_set = false;
   if (!attr_set) {

@@ -3,7 +3,7 @@
 cd "$GRAFT_REPO_ROOT" 2>/dev/null || cd /root/repo
 mkdir -p gpurun_out
 python -c 'import __graft_entry__ as g; g.build()' > gpurun_out/build.log 2>&1 || { echo build failed; exit 1; }
-PARO_ADAM_WS=1 timeout 1200 python -m pytest tests -m gpu -q -k "n1_ten or 4m_2x4_ten or fp32_wire_every or consumer or streamed_step_every" > gpurun_out/pytest_ws.log 2>&1; echo "pytest_ws rc=$?" >> gpurun_out/pytest_ws.log
+PARO_ADAM_WS=1 timeout 1200 python -m pytest tests -m gpu -q -k "n1_ten or 4m_2x4_ten or variant_selection or fp32 or oneshot or consumer or streamed_step_every" > gpurun_out/pytest_ws.log 2>&1; echo "pytest_ws rc=$?" >> gpurun_out/pytest_ws.log
 tail -3 gpurun_out/pytest_ws.log
 : > gpurun_out/ws_ab.jsonl
 for i in 1 2 3; do
