@@ -341,6 +341,10 @@ def run_ours(args):
                 # link as a whole moves these bytes during the collective launches' time
                 "link_achieved": (info["step_send_bytes_intra"] + info["step_send_bytes_inter"])
                                  / (prof["comm_ms"] / args.steps / 1000.0) / 1e9,
+                # device trace of the first traced launches: time in peer barriers vs data movement
+                "trace_per_launch_ms": {"barrier": prof["traced_barrier_ms"] / max(1, prof["traced_launches"]),
+                                        "work": prof["traced_work_ms"] / max(1, prof["traced_launches"]),
+                                        "launches": prof["traced_launches"]},
                 "note": "achieved = bytes this rank sends in the rounds launches / their duration; "
                         "link_achieved = all bytes this rank sends per step (rounds + fused-Adam pulls) / "
                         "the collective launches' time per step; SM-transport ceiling 672 GB/s/dir "

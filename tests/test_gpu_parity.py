@@ -239,8 +239,10 @@ def test_4m_2x4_ten_steps(code, adam_impl, smem):
         assert v in ("adam_tma_kernel<false,512>", "adam_tma_kernel<false,256>")
         if smem == 60:
             assert v == "adam_tma_kernel<false,256>"
-    elif adam_impl == "tma_ws":
-        assert v == ("adam_tma_ws_kernel<256>" if smem == 120 else "adam_tma_ws_kernel<512>")
+    elif adam_impl == "tma_ws":   # 4096- or 2048-element tiles, by the stages that fit the budget
+        assert v in ("adam_tma_ws_kernel<512>", "adam_tma_ws_kernel<256>")
+        if smem == 120:
+            assert v == "adam_tma_ws_kernel<256>"
     else:
         assert v.startswith("adam_tma_kernel<true,") or v.startswith("adam_tma_ws_kernel")
     run.close()
