@@ -406,3 +406,14 @@ def test_oneshot_large_buckets_run_ho_ring(N, M):
         for k in ("step_send_bytes_intra", "step_send_bytes_inter", "n_rounds", "n_comm_launches"):
             assert one[k] == ho[k], (code, k)
     ctx.close()
+
+
+def test_param_consumer_needs_a_device_context():
+    """paro_set_param_consumer registers a per-bucket consumer for device plans;
+    a planning-only context has no steps (PARO_ERR_STATE)."""
+    ctx = paro.Context(4, 2)
+    pl = paro.Plan(ctx, "IIG", [1 << 16], bucket_elems=1 << 14)
+    with pytest.raises(paro.ParoError, match="planning-only"):
+        pl.set_param_consumer(lambda *a: None)
+    pl.close()
+    ctx.close()
