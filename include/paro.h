@@ -88,10 +88,7 @@ typedef struct {
   float eps;             /* 1e-8                                                   */
   float weight_decay;    /* 0.0 (AdamW form, R5)                                   */
   float loss_scale;      /* 1.0; gradients are unscaled by 1/loss_scale in Adam    */
-  int comm_ctas;         /* CTAs of the collective kernels; 0 (default): per launch, *
-                          * enough for ~4 tiles of its largest round per CTA (at   *
-                          * least 8, at most one per SM: 148 for large buckets,    *
-                          * fewer barrier arrivals for small ones)                  */
+  int comm_ctas;         /* CTAs of the collective kernels; 0 (default): one per SM */
   int pipeline_depth;    /* buckets in flight between reduce and gather (def. 2)  */
   int pull_transport;    /* 1 (default): ranks LOAD their ring predecessor's data   *
                           * over NVLink (pull); 0: ranks STORE into their          *

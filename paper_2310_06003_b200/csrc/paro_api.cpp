@@ -474,13 +474,14 @@ void prof_end(PlanT* p, cudaStream_t s, int k) {
 
 constexpr int kTraceLaunches = 512;
 
-// CTAs of a collective launch: comm_ctas, or (0 = auto) enough for ~4 tiles of
-// its largest round per CTA, at least 8 and at most one per SM: small launches
-// then pay for fewer arrivals at every in-kernel barrier (latency-bound sizes)
+// CTAs of a collective launch: comm_ctas, or (0) one per SM.  Sizing small
+// launches down (~4 tiles per CTA) was measured slower at every size (1 MiB
+// all-reduce, 2 GPUs: one-shot 21.2 vs 19.2 us, HO 35.9 vs 31.9 us; 4 GPUs the
+// same direction, profiles/r02/latency_*): more CTAs put more loads in flight
+// and the entry barrier has no grid arrival
 int comm_grid(const PlanT* p, const DevLaunch* dl = nullptr) {
+  (void)dl;
   int g = p->opts.comm_ctas > 0 ? p->opts.comm_ctas : p->ctx->sm_count;
-  if (p->opts.comm_ctas <= 0 && dl && dl->max_tiles > 0)
-    g = (int)std::min<int64_t>(g, std::max<int64_t>(8, (dl->max_tiles + 3) / 4));
   if (p->ctx->mode == MODE_REAL) {
     if (g > p->ctx->sm_count) g = p->ctx->sm_count;   // co-residency of all CTAs (barriers)
   } else {
