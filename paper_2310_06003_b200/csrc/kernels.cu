@@ -1461,12 +1461,6 @@ cudaError_t launch_rounds_tma(const RoundsArgs& a, int grid, int max_in, cudaStr
   return cudaGetLastError();
 }
 
-int rounds_tma_tile_elems(int max_in, int out_f32) {
-  if (max_in < 1) max_in = 1;
-  if (max_in > kRtMaxIn) max_in = kRtMaxIn;
-  return rt_slot_bytes(max_in) / (out_f32 ? 4 : 2);
-}
-
 int rounds_tma_smem_kb(int max_in) {
   if (max_in < 1) max_in = 1;
   if (max_in > kRtMaxIn) max_in = kRtMaxIn;

@@ -144,7 +144,6 @@ cudaError_t launch_adam_tma(const AdamArgs& a, int sms, cudaStream_t s, int smem
 cudaError_t launch_rounds_tma(const RoundsArgs& a, int grid, int max_in, cudaStream_t s, int bulk_store,
                               int generic);
 int rounds_tma_smem_kb(int max_in);   // dynamic shared memory of a TMA rounds CTA
-int rounds_tma_tile_elems(int max_in, int out_f32);   // elements per tile of a TMA rounds launch
 cudaError_t launch_norm_finalize(const double* partials, int n, double* out, cudaStream_t s);
 // phase 1 of the two-phase step: block partials of sum (fold(gin) * s_g)^2 and
 // the non-finite flag, 2 bytes read per element, no update

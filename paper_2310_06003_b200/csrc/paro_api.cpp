@@ -72,7 +72,6 @@ struct DevLaunch {
   std::vector<std::vector<CopyOp>> copies;   // [round] local rank(s)' copies
   std::vector<uint64_t> round_peers;         // [round] barrier peers before it
   int max_in = 1;          // largest fold input count (TMA stage sizing)
-  int64_t max_tiles = 0;   // largest round's 4096-element tiles of the local rank(s) (grid sizing)
   int generic = 0;         // has fp32-wire or nested (one-shot) tasks: the generic fold kernel
   int64_t bytes = 0;       // bytes the local rank(s) send in this launch
   int64_t hbm = 0;         // algorithmic HBM bytes of the local rank(s)' tasks: each input
@@ -339,16 +338,6 @@ paro_status_t upload_schedule(PlanT* p) {
     }
     dl.nrounds = R;
     dl.final_barrier = L.final_barrier ? 1 : 0;
-    // tiles of the largest round at the slot size this launch's input count gets
-    for (int r = 0; r < R; ++r) {
-      const DRound& d = rounds[dl.round_off + r];
-      int64_t tiles = 0;
-      for (int ti = d.t0; ti < d.t1; ++ti) {
-        const int64_t te = rounds_tma_tile_elems(dl.max_in, tasks[ti].out_f32);
-        tiles += (tasks[ti].n8 * 8 + te - 1) / te;
-      }
-      dl.max_tiles = std::max(dl.max_tiles, tiles);
-    }
     // bytes sent by the local rank(s): what peers read from them in this launch
     for (int r = 0; r < R; ++r)
       for (int x = 0; x < pl.N; ++x)
@@ -479,8 +468,7 @@ constexpr int kTraceLaunches = 512;
 // all-reduce, 2 GPUs: one-shot 21.2 vs 19.2 us, HO 35.9 vs 31.9 us; 4 GPUs the
 // same direction, profiles/r02/latency_*): more CTAs put more loads in flight
 // and the entry barrier has no grid arrival
-int comm_grid(const PlanT* p, const DevLaunch* dl = nullptr) {
-  (void)dl;
+int comm_grid(const PlanT* p) {
   int g = p->opts.comm_ctas > 0 ? p->opts.comm_ctas : p->ctx->sm_count;
   if (p->ctx->mode == MODE_REAL) {
     if (g > p->ctx->sm_count) g = p->ctx->sm_count;   // co-residency of all CTAs (barriers)
@@ -550,7 +538,7 @@ paro_status_t run_launch(PlanT* p, const DevLaunch& dl, int* nlaunch) {
   paro_ctx* ctx = p->ctx;
   if (dl.dma) return run_dma_launch(p, dl, ctx->comm, nlaunch);
   if (dl.nrounds == 0 && (!dl.final_barrier || ctx->mode != MODE_REAL)) return PARO_OK;
-  const int grid = comm_grid(p, &dl);
+  const int grid = comm_grid(p);
   RoundsArgs a{};
   a.tasks = p->d_tasks;
   a.alpha = p->alpha;
