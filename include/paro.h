@@ -199,7 +199,8 @@ typedef struct {
                           * hop one fp32 add, g_hat never rounded to bf16, so the  *
                           * result depends on the split / bucket only through fp32 *
                           * summation order (<= 1e-5 after 10 steps, SURVEY        *
-                          * §8(c-4)).  Not with grad_accum or copy_engine = 2.     */
+                          * §8(c-4)); gradient accumulators are fp32 too.  Not     *
+                          * with copy_engine = 2.                                  */
   int predivide;         /* 1 (default): raw gradients are multiplied by 1/N when   *
                           * first read (R4); 0: the raw sum is reduced and the 1/N *
                           * average is applied in Adam's unscale, s_g = 1 /        *

@@ -161,7 +161,7 @@ def clip_update(ghat, master, m, v, lr, step, clip_norm, skip_nonfinite, accum_s
     return w2, m2, v2, pb, ghat, norm_sq, coef, False
 
 
-def dp_accum_step(lay: Layout, grads_mb, master, m, v, sc: AdamScalars, g_level):
+def dp_accum_step(lay: Layout, grads_mb, master, m, v, sc: AdamScalars, g_level, wire="bf16"):
     """Unsharded data parallel with gradient accumulation (plain definition, R27).
 
     grads_mb[k][r]: rank r's flat bf16 gradient of micro-batch k (k = 1..s).
@@ -171,21 +171,23 @@ def dp_accum_step(lay: Layout, grads_mb, master, m, v, sc: AdamScalars, g_level)
       G = I: S_j'  = Acc_k R_M(p; x_(j', 0..M-1), k);  g_hat = R_g(j; S_0..S_{g-1})
       G = N: y_r   = Acc_k x_(r, k);                    g_hat = CanonReduce(y)
     with Acc_k y_k = ((y_1 (+) y_2) (+) ...) (+) y_s and x = RNE_bf16(g / N).
-    Then canonical Adam with sc built with accum_steps = s.
+    Then canonical Adam with sc built with accum_steps = s.  wire = "fp32":
+    x = fp32(g) / N, every (+) and the accumulator in fp32 (R32).
     """
     N, M = lay.N, lay.M
     geo = C.Geometry(N, M)
-    X_mb = [[pack(pad_flat(gr, lay.psi_pad, np.uint16), 1.0 / N) for gr in grads] for grads in grads_mb]
+    pk, op, dt = wire_ops(N, wire)
+    X_mb = [[pk(pad_flat(gr, lay.psi_pad, np.uint16)) for gr in grads] for grads in grads_mb]
 
     def acc(ys):
         out = ys[0]
         for y in ys[1:]:
-            out = hop(out, y)
+            out = op(out, y)
         return out
 
     if g_level == "N":
         Y = [acc([X[r] for X in X_mb]) for r in range(N)]
-    ghat = np.zeros(lay.psi_pad, np.uint16)
+    ghat = np.zeros(lay.psi_pad, dt)
     for (s, n) in lay.buckets:
         segn = n // N
         for r in range(N):
@@ -195,16 +197,16 @@ def dp_accum_step(lay: Layout, grads_mb, master, m, v, sc: AdamScalars, g_level)
             if g_level == "G":
                 per_mb = []
                 for X in X_mb:
-                    S = [canonical_fold([X[geo.r(jj, pp)][a:b] for pp in range(M)], p) for jj in range(geo.g)]
-                    per_mb.append(canonical_fold(S, j))
+                    S = [canonical_fold([X[geo.r(jj, pp)][a:b] for pp in range(M)], p, op) for jj in range(geo.g)]
+                    per_mb.append(canonical_fold(S, j, op))
                 ghat[a:b] = acc(per_mb)
             elif g_level == "I":
-                S = [acc([canonical_fold([X[geo.r(jj, pp)][a:b] for pp in range(M)], p) for X in X_mb])
+                S = [acc([canonical_fold([X[geo.r(jj, pp)][a:b] for pp in range(M)], p, op) for X in X_mb])
                      for jj in range(geo.g)]
-                ghat[a:b] = canonical_fold(S, j)
+                ghat[a:b] = canonical_fold(S, j, op)
             else:
-                S = [canonical_fold([Y[geo.r(jj, pp)][a:b] for pp in range(M)], p) for jj in range(geo.g)]
-                ghat[a:b] = canonical_fold(S, j)
+                S = [canonical_fold([Y[geo.r(jj, pp)][a:b] for pp in range(M)], p, op) for jj in range(geo.g)]
+                ghat[a:b] = canonical_fold(S, j, op)
     w2, m2, v2, pb = adam_update(master, m, v, ghat, sc)
     return w2, m2, v2, pb, ghat
 
@@ -244,7 +246,7 @@ def strategy_step(code, lay: Layout, grads, state, sc: AdamScalars, topology="ho
     return _simulate(code, lay, [grads], state, sc, topology, accumulate=False, wire=wire, predivide=predivide)
 
 
-def strategy_accum_step(code, lay: Layout, grads_mb, state, sc: AdamScalars, topology="ho"):
+def strategy_accum_step(code, lay: Layout, grads_mb, state, sc: AdamScalars, topology="ho", wire="bf16"):
     """One mini-batch step with gradient accumulation over s = len(grads_mb)
     micro-batches (§3.3; "each GPU maintains a gradient shard
     that accumulates gradients generated by each micro-batch").
@@ -264,7 +266,7 @@ def strategy_accum_step(code, lay: Layout, grads_mb, state, sc: AdamScalars, top
     strategy_step.  The mean over micro-batches is folded into the unscale
     factor: pass AdamScalars(..., accum_steps=s).
     """
-    return _simulate(code, lay, grads_mb, state, sc, topology, accumulate=True)
+    return _simulate(code, lay, grads_mb, state, sc, topology, accumulate=True, wire=wire)
 
 
 def _simulate(code, lay, grads_mb, state, sc, topology, accumulate, wire="bf16", predivide=True):

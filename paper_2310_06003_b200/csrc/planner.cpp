@@ -285,8 +285,8 @@ Planner::Planner(int N_, int M_, const std::string& code_, const std::vector<int
   if (opt.grad_slots > 0 && (opt.accum || opt.ce_reduce))
     throw std::invalid_argument("grad_slots cannot be combined with grad_accum or copy_engine = 2");
   if (opt.wire != 2 && opt.wire != 4) throw std::invalid_argument("wire_dtype must be 0 (bf16) or 1 (fp32)");
-  if (opt.wire == 4 && (opt.accum || opt.ce_reduce))
-    throw std::invalid_argument("wire_dtype = 1 (fp32) is not available with grad_accum or copy_engine = 2");
+  if (opt.wire == 4 && opt.ce_reduce)
+    throw std::invalid_argument("wire_dtype = 1 (fp32) is not available with copy_engine = 2");
   layout();
   if (N == 1 && opt.two_phase && opt.grad_slots > 0 && opt.grad_slots < (int64_t)buckets.size())
     throw std::invalid_argument(

@@ -393,14 +393,14 @@ def _mb_id(t, k):
     return (t << 8) | (k + 1)     # synthetic-gradient counter of micro-batch k of step t
 
 
-def _accum_reference(lay, steps, s, g_level, loss_scale=1.0):
+def _accum_reference(lay, steps, s, g_level, loss_scale=1.0, wire="bf16"):
     w = ST.pad_flat(master_f32(0, lay.psi), lay.psi_pad, np.float32)
     m, v = np.zeros_like(w), np.zeros_like(w)
     norms = []
     for t in range(1, steps + 1):
         mb = [[grad_bits(r, _mb_id(t, k), 0, lay.psi) for r in range(lay.N)] for k in range(s)]
         sc = nm.AdamScalars(LR, t, loss_scale=loss_scale, accum_steps=s)
-        w, m, v, p, gh = ST.dp_accum_step(lay, mb, w, m, v, sc, g_level)
+        w, m, v, p, gh = ST.dp_accum_step(lay, mb, w, m, v, sc, g_level, wire=wire)
         norms.append(nm.grad_sq_sum(gh, sc.s_g))
     return w, m, v, p, norms
 
@@ -1176,4 +1176,22 @@ def test_param_consumer_every_strategy(N, M, slots):
         for r in range(N):
             assert np.array_equal(out[r].cpu().numpy().view(np.uint16), run.state(r)["param"]), (code, r)
         run.pl.set_param_consumer(None)
+        run.close()
+
+
+@pytest.mark.parametrize("N,M,topo", [(8, 4, "ho"), (4, 2, "two_step"), (2, 1, "ho"), (8, 4, "oneshot")])
+def test_fp32_wire_accumulation_every_strategy(N, M, topo):
+    """Gradient accumulation on the fp32 wire: fp32 accumulators at the G
+    residency (s = 3 micro-batches, 2 steps), every strategy bit-exact vs
+    dp_accum_step(wire = fp32)."""
+    s = 3
+    sizes = [N * 64 * 40 + 24, 1000]
+    B = N * 64 * 8
+    lay = L.Layout(sizes, N, M, B)
+    refs = {gl: _accum_reference(lay, 2, s, gl, wire="fp32") for gl in "NIG"}
+    for code in S.paro_strategies():
+        run = EmuRun(N, M, code, sizes, B, topo=topo, transport="pull", grad_accum=True, wire="fp32")
+        stats = _run_accum(run, 2, s)
+        _check_against_dp(run, lay, refs[code[1]])
+        assert abs(stats[-1]["grad_norm"] ** 2 - refs[code[1]][4][-1]) <= 1e-12 * refs[code[1]][4][-1]
         run.close()

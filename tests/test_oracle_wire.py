@@ -152,3 +152,34 @@ def test_predivide_off_equals_on_at_power_of_two_N():
     # (2^-9 relative) of partials bounded by sum_r |g_r|
     gsum = np.sum([np.abs(nm.f32_from_bf16_bits(ST.pad_flat(g, lay.psi_pad, np.uint16))) for g in grads], axis=0)
     assert np.all(np.abs(a - b) <= 2 * N * 2.0 ** -9 * gsum)
+
+
+@pytest.mark.parametrize("N,M", [(8, 4), (4, 2), (6, 3)])
+def test_fp32_wire_accumulation(N, M):
+    """Gradient accumulation on the fp32 wire (R27 + R32): every strategy's
+    simulated accumulating step equals dp_accum_step(wire = fp32) bit for bit;
+    small integers accumulate to the exact sum; and the three G levels agree
+    with each other far closer than on the bf16 wire (only fp32 order differs)."""
+    s = 3
+    lay = L.Layout([N * 64 * 6 + 5], N, M, N * 64 * 2)
+    mb = [[grad_bits(r, (1 << 8) | (k + 1), 0, lay.psi) for r in range(N)] for k in range(s)]
+    w0 = master_f32(0, lay.psi)
+    wp = ST.pad_flat(w0, lay.psi_pad, np.float32)
+    z = np.zeros_like(wp)
+    sc = nm.AdamScalars(LR, 1, accum_steps=s)
+    refs = {gl: ST.dp_accum_step(lay, mb, wp, z, z, sc, gl, wire="fp32") for gl in "NIG"}
+    for code in S.paro_strategies():
+        res = ST.strategy_accum_step(code, lay, mb, ST.init_state(w0, lay, code), sc, wire="fp32")
+        w = refs[code[1]][0]
+        for r in range(N):
+            assert np.array_equal(res.state[r]["master"].view(np.uint32),
+                                  ST.shard_of(w, lay, code[2], r).view(np.uint32)), (code, r)
+    gh = {gl: refs[gl][4].astype(np.float64) for gl in "NIG"}
+    scale = np.abs(gh["G"]).max()
+    assert max(np.abs(gh["N"] - gh["G"]).max(), np.abs(gh["I"] - gh["G"]).max()) <= 1e-6 * scale
+    ints = np.random.default_rng(N).integers(-3, 4, size=(s, N, lay.psi)).astype(np.float32)
+    mbi = [[nm.bf16_bits_from_f32(ints[k, r]) for r in range(N)] for k in range(s)]
+    for gl in "NIG":
+        gi = ST.dp_accum_step(lay, mbi, wp, z, z, sc, gl, wire="fp32")[4]
+        if N & (N - 1) == 0:
+            assert np.array_equal(gi[:lay.psi], ints.sum((0, 1)) / N), gl
