@@ -345,9 +345,16 @@ def run_ours(args):
                 "trace_per_launch_ms": {"barrier": prof["traced_barrier_ms"] / max(1, prof["traced_launches"]),
                                         "work": prof["traced_work_ms"] / max(1, prof["traced_launches"]),
                                         "launches": prof["traced_launches"]},
-                "note": "achieved = bytes this rank sends in the rounds launches / their duration; "
-                        "link_achieved = all bytes this rank sends per step (rounds + fused-Adam pulls) / "
-                        "the collective launches' time per step; SM-transport ceiling 672 GB/s/dir "
+                # the link over the whole step: every byte this rank sends (SM rounds, fused-Adam
+                # pulls, copy-engine gathers) / the step time
+                "step_link_GBps": (info["step_send_bytes_intra"] + info["step_send_bytes_inter"])
+                                  / (ms / 1000.0) / 1e9,
+                "note": "achieved = bytes this rank sends in the rounds launches / their duration; the "
+                        "launches of consecutive buckets overlap (share_of_step > 1) and share the link "
+                        "with the copy-engine parameter gathers, so a launch's duration includes time the "
+                        "link spends on other engines' bytes; link_achieved = all bytes this rank sends "
+                        "per step / the collective launches' time per step; step_link_GBps = the same "
+                        "bytes / the step time; SM-transport ceiling 672 GB/s/dir "
                         "(profiles/r01/p2p_tma_bidir.jsonl)"}
 
     # a fraction far above 1 means the timed launches are not doing the work (B200_PROFILING.md)
