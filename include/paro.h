@@ -141,8 +141,10 @@ typedef struct {
                           * vs 660 for SM loads, profiles/r01/p2p_bidir.jsonl);     *
                           * 2: also G = I's intra reduce-scatter as copy-engine     *
                           * copies of the peers' raw chunks + one local fold.       *
-                          * 0 (default): the rounds kernel (measured fastest in the *
-                          * full step at 2x2, profiles/r01/sweep_copy_engine_2x2). */
+                          * 0 (default): the rounds kernel.  Measured in the full  *
+                          * 7B IIG step at 2x2 (profiles/r02/                      *
+                          * sweep_copy_engine_iig_2x2.jsonl): 0 / 1 / 2 = 21.10 /  *
+                          * 20.43 / 20.49 ms; bench.py runs 1.                     */
   int gather_windows;    /* > 0: that many library window slots of bucket_elems    *
                           * bf16 each for paro_gather_window (P = I or G only).    */
   int grad_accum;        /* 1: enable paro_accumulate (gradient accumulation over  *
