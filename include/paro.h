@@ -141,6 +141,11 @@ typedef struct {
                           * vs 660 for SM loads, profiles/r01/p2p_bidir.jsonl);     *
                           * 2: also G = I's intra reduce-scatter as copy-engine     *
                           * copies of the peers' raw chunks + one local fold.       *
+                          * 3: 1, and the trailing copy-only rounds of a reduce    *
+                          * launch (the all-gather half of an all-reduce: OS = N,  *
+                          * or AG_E for G = N, OS = I) leave the rounds kernel for *
+                          * the copy engines, on a second stream: the kernels of   *
+                          * later buckets run beside them (real mode only).        *
                           * 0 (default): the rounds kernel.  Measured in the full  *
                           * 7B IIG step at 2x2 (profiles/r02/                      *
                           * sweep_copy_engine_iig_2x2.jsonl): 0 / 1 / 2 = 21.10 /  *

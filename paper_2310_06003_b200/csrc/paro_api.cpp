@@ -81,6 +81,9 @@ struct DevLaunch {
   int nrounds = 0;
   int final_barrier = 0;
   uint64_t final_peers = 0;
+  // copy-engine tail (opts.copy_engine = 3): the launch's trailing pure-copy
+  // rounds, run by the copy engines after the kernel's rounds [0, nrounds)
+  std::vector<DevLaunch> tail;
 };
 
 struct paro_plan {
@@ -98,6 +101,7 @@ struct paro_plan {
   cudaEvent_t ev_cons = nullptr;
   std::vector<cudaEvent_t> ev_pfinal;     // bucket b's parameters final on this rank
   cudaEvent_t ev_dma = nullptr;
+  cudaEvent_t ev_tail = nullptr;          // comm -> dma hand-over of a copy-engine tail
   DRound* d_rounds = nullptr;
   DTask* d_tasks = nullptr;
   std::vector<DevLaunch> red, gat;        // per bucket
@@ -305,7 +309,7 @@ paro_status_t upload_schedule(PlanT* p) {
   const Planner& pl = *p->pl;
   std::vector<DRound> rounds;
   std::vector<DTask> tasks;
-  auto build = [&](const Launch& L, int acc_kind, int64_t win_shift = 0) {
+  auto build = [&](const Launch& L, int acc_kind, int64_t win_shift = 0, bool allow_tail = false) {
     DevLaunch dl;
     dl.round_off = (int64_t)rounds.size();
     if (L.empty()) return dl;
@@ -339,30 +343,80 @@ paro_status_t upload_schedule(PlanT* p) {
     dl.nrounds = R;
     dl.final_barrier = L.final_barrier ? 1 : 0;
     // bytes sent by the local rank(s): what peers read from them in this launch
+    std::vector<int64_t> bytes_r(R, 0), hbm_r(R, 0);
     for (int r = 0; r < R; ++r)
       for (int x = 0; x < pl.N; ++x)
         for (const Task& t : L.rounds[r][x]) {
           for (int i = 0; i < t.nin; ++i) {
             const int y = t.in[i].rank;
-            if (y != x && (ctx->mode != MODE_REAL || y == ctx->rank)) dl.bytes += pl.esz[t.in[i].kind] * t.n;
+            if (y != x && (ctx->mode != MODE_REAL || y == ctx->rank)) bytes_r[r] += pl.esz[t.in[i].kind] * t.n;
           }
-          if (t.dst.rank != x && (ctx->mode != MODE_REAL || x == ctx->rank)) dl.bytes += pl.esz[t.dst.kind] * t.n;
+          if (t.dst.rank != x && (ctx->mode != MODE_REAL || x == ctx->rank)) bytes_r[r] += pl.esz[t.dst.kind] * t.n;
         }
     for (int r = 0; r < R; ++r)
       for (int x = 0; x < pl.N; ++x) {
         if (ctx->mode == MODE_REAL && x != ctx->rank) continue;
         for (const Task& t : L.rounds[r][x]) {
-          dl.hbm += pl.esz[t.dst.kind] * t.n;
-          for (int i = 0; i < t.nin; ++i) dl.hbm += pl.esz[t.in[i].kind] * t.n;
+          hbm_r[r] += pl.esz[t.dst.kind] * t.n;
+          for (int i = 0; i < t.nin; ++i) hbm_r[r] += pl.esz[t.in[i].kind] * t.n;
         }
       }
+    for (int r = 0; r < R; ++r) {
+      dl.bytes += bytes_r[r];
+      dl.hbm += hbm_r[r];
+    }
     dl.final_peers = (ctx->mode == MODE_REAL) ? L.barrier_peers(R, ctx->rank) : 0;
-    // copy engines: every task a plain 1-input bit copy
-    bool pure = p->opts.copy_engine != 0 && R > 0;
-    for (int r = 0; r < R && pure; ++r)
-      for (int x = 0; x < pl.N && pure; ++x)
+    // copy engines: every task of round r (of every rank: the decision is the
+    // same on all ranks, their barrier channels stay in step) a plain 1-input bit copy
+    auto pure_round = [&](int r) {
+      bool ok = true;
+      for (int x = 0; x < pl.N && ok; ++x)
         for (const Task& t : L.rounds[r][x])
-          pure = pure && t.nin == 1 && !t.in[0].is_raw() && pl.esz[t.in[0].kind] == pl.esz[t.dst.kind];
+          ok = ok && t.nin == 1 && !t.in[0].is_raw() && pl.esz[t.in[0].kind] == pl.esz[t.dst.kind];
+      return ok;
+    };
+    bool pure = p->opts.copy_engine != 0 && R > 0;
+    for (int r = 0; r < R && pure; ++r) pure = pure_round(r);
+    // copy-engine tail (copy_engine = 3, real mode, reduce launches): the trailing
+    // pure-copy rounds (an all-reduce's all-gather half) leave the rounds kernel
+    // for the copy engines (bidirectional ring traffic 770 vs 660 GB/s/dir for SM
+    // loads, profiles/r01/p2p_bidir.jsonl).  The kernel keeps rounds [0, k)
+    // without a final barrier: the tail's first barrier (the peers of rounds k-1
+    // and k, as inside the kernel) publishes them.  Tail tasks read and write the
+    // reduction's result buffers only (no staging sets), so the kernels of later
+    // buckets may run beside the tail.
+    if (!pure && allow_tail && p->opts.copy_engine == 3 && ctx->mode == MODE_REAL) {
+      int k = R;
+      while (k > 0 && pure_round(k - 1)) --k;
+      bool ok = k > 0 && k < R;
+      auto result_buf = [](int kind) { return kind == BUF_GHAT || kind == BUF_GSHARD; };
+      for (int r = k; r < R && ok; ++r)
+        for (int x = 0; x < pl.N && ok; ++x)
+          for (const Task& t : L.rounds[r][x]) ok = ok && result_buf(t.dst.kind) && result_buf(t.in[0].kind);
+      if (ok) {
+        DevLaunch tl;
+        tl.dma = true;
+        tl.copies.assign(R - k, {});
+        tl.round_peers.assign(R - k, 0);
+        for (int r = k; r < R; ++r) {
+          for (const Task& t : L.rounds[r][ctx->rank]) {
+            const DTask d = resolve(p, t, ctx->rank, -1, win_shift);
+            tl.copies[r - k].push_back({d.dst, d.in[0], (size_t)t.n * pl.esz[t.dst.kind]});
+          }
+          tl.round_peers[r - k] = L.barrier_peers(r, ctx->rank);
+          tl.bytes += bytes_r[r];
+          tl.hbm += hbm_r[r];
+        }
+        tl.final_barrier = dl.final_barrier;
+        tl.final_peers = dl.final_peers;
+        dl.nrounds = k;
+        dl.final_barrier = 0;
+        dl.final_peers = 0;
+        dl.bytes -= tl.bytes;
+        dl.hbm -= tl.hbm;
+        dl.tail.push_back(std::move(tl));
+      }
+    }
     if (pure) {
       dl.dma = true;
       dl.copies.assign(R, {});
@@ -407,7 +461,7 @@ paro_status_t upload_schedule(PlanT* p) {
   p->red_acc.clear();
   p->win.assign(pl.buf_len[BUF_WIN] > 0 ? pl.opt.windows : 0, {});
   for (const BucketSchedule& S : pl.sched) {
-    p->red.push_back(build(S.reduce, -1));
+    p->red.push_back(build(S.reduce, -1, 0, true));
     p->gat.push_back(build(S.gather, -1));
     for (int w = 0; w < (int)p->win.size(); ++w) p->win[w].push_back(build(S.window, -1, int64_t(w) * pl.B));
     if (!S.reduce_pre.rounds.empty()) p->red_pre.push_back(build_copies(S.reduce_pre));
@@ -533,10 +587,33 @@ paro_status_t run_dma_launch(PlanT* p, const DevLaunch& dl, cudaStream_t s, int*
   return PARO_OK;
 }
 
+paro_status_t run_launch_kernel(PlanT* p, const DevLaunch& dl, int* nlaunch);
+
 // Launch one collective (reduce or gather of one bucket) on the comm stream.
-paro_status_t run_launch(PlanT* p, const DevLaunch& dl, int* nlaunch) {
+// A copy-engine tail follows on the dma stream: with `tail_on_dma` the caller
+// orders the consumers after the dma stream itself (*tail_on_dma = true), else
+// the comm stream waits for the tail here.
+paro_status_t run_launch(PlanT* p, const DevLaunch& dl, int* nlaunch, bool* tail_on_dma = nullptr) {
   paro_ctx* ctx = p->ctx;
   if (dl.dma) return run_dma_launch(p, dl, ctx->comm, nlaunch);
+  paro_status_t s = run_launch_kernel(p, dl, nlaunch);
+  if (s != PARO_OK || dl.tail.empty()) return s;
+  CK(cudaEventRecord(p->ev_tail, ctx->comm));
+  CK(cudaStreamWaitEvent(ctx->dma, p->ev_tail, 0));
+  s = run_dma_launch(p, dl.tail[0], ctx->dma, nlaunch);
+  if (s != PARO_OK) return s;
+  if (tail_on_dma) {
+    *tail_on_dma = true;
+  } else {
+    CK(cudaEventRecord(p->ev_tail, ctx->dma));
+    CK(cudaStreamWaitEvent(ctx->comm, p->ev_tail, 0));
+  }
+  return PARO_OK;
+}
+
+// The rounds-kernel part of a launch, on the comm stream.
+paro_status_t run_launch_kernel(PlanT* p, const DevLaunch& dl, int* nlaunch) {
+  paro_ctx* ctx = p->ctx;
   if (dl.nrounds == 0 && (!dl.final_barrier || ctx->mode != MODE_REAL)) return PARO_OK;
   const int grid = comm_grid(p);
   RoundsArgs a{};
@@ -679,7 +756,8 @@ void destroy_plan(PlanT* p) {
     cudaFree(p->d_moved);
     cudaFree(p->d_pack);
     if (p->h_pack) cudaFreeHost(p->h_pack);
-    for (cudaEvent_t e : {p->ev_fork, p->ev_comm, p->ev_comp, p->ev_pack_staged, p->ev_unpack_staged, p->ev_dma})
+    for (cudaEvent_t e : {p->ev_fork, p->ev_comm, p->ev_comp, p->ev_pack_staged, p->ev_unpack_staged, p->ev_dma,
+                          p->ev_tail})
       if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : p->prof_ev) cudaEventDestroy(e);
     cudaFree(p->d_trace);
@@ -874,7 +952,7 @@ paro_status_t paro_plan(paro_ctx_t ctx, const char* strategy, const int64_t* par
   // paced (emulated-gap) runs keep every transfer in the rounds kernel, which
   // paces them; the NCCL comparator has no copy-engine path
   if (o.inter_gbps > 0.f || o.topology == PARO_TOPO_NCCL) o.copy_engine = 0;
-  if (o.copy_engine < 0 || o.copy_engine > 2) return fail(PARO_ERR_INVALID, "copy_engine must be 0, 1 or 2");
+  if (o.copy_engine < 0 || o.copy_engine > 3) return fail(PARO_ERR_INVALID, "copy_engine must be 0 .. 3");
   po.ce_reduce = o.copy_engine == 2;
   po.params_only = o.frozen != 0;
   if (o.grad_slots < 0) return fail(PARO_ERR_INVALID, "grad_slots must be >= 0");
@@ -980,7 +1058,7 @@ paro_status_t paro_plan(paro_ctx_t ctx, const char* strategy, const int64_t* par
   PCK(cudaMalloc(&p->d_pack, 2 * sizeof(PackEntry) * p->pack_cap));   // [pack | unpack]
   PCK(cudaHostAlloc(&p->h_pack, 2 * sizeof(PackEntry) * p->pack_cap, cudaHostAllocDefault));
   for (cudaEvent_t* e : {&p->ev_fork, &p->ev_comm, &p->ev_comp, &p->ev_pack_staged, &p->ev_unpack_staged,
-                        &p->ev_dma})
+                        &p->ev_dma, &p->ev_tail})
     PCK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
   p->ev_red.resize(nb);
   p->ev_adam.resize(nb);
@@ -1617,8 +1695,16 @@ paro_status_t step_impl(PlanT* p, const void* const* grads, void* const* params,
         if (s3 != PARO_OK) return s3;
         ++launches;
       } else {
-        paro_status_t s3 = run_launch(p, red[b], &launches);
+        bool tail = false;   // copy-engine tail: the reduction completes on the dma stream
+        paro_status_t s3 = run_launch(p, red[b], &launches, &tail);
         if (s3 != PARO_OK) return s3;
+        if (tail) {
+          dma_used = true;
+          CK(cudaEventRecord(p->ev_red[b], ctx->dma));
+          CK(cudaStreamWaitEvent(ctx->comp, p->ev_red[b], 0));
+          if (pre_on && b + kStageSets < nb) return issue_pre(b + kStageSets);
+          return PARO_OK;
+        }
       }
       CK(cudaEventRecord(p->ev_red[b], ctx->comm));
       CK(cudaStreamWaitEvent(ctx->comp, p->ev_red[b], 0));
@@ -1842,6 +1928,7 @@ paro_status_t paro_collective(paro_plan_t p, int what) {
   }
   cudaStream_t S = p->opts.stream ? static_cast<cudaStream_t>(p->opts.stream) : ctx->main;
   int launches = 0;
+  bool tails = false;
   CK(cudaEventRecord(p->ev_fork, S));
   CK(cudaStreamWaitEvent(ctx->comm, p->ev_fork, 0));
   const bool nccl = pl.opt.topology == PARO_TOPO_NCCL;
@@ -1858,9 +1945,13 @@ paro_status_t paro_collective(paro_plan_t p, int what) {
       if (s3 != PARO_OK) return s3;
       ++launches;
     } else {
-      paro_status_t s3 = run_launch(p, what == 0 ? p->red[b] : p->gat[b], &launches);
+      paro_status_t s3 = run_launch(p, what == 0 ? p->red[b] : p->gat[b], &launches, &tails);
       if (s3 != PARO_OK) return s3;
     }
+  }
+  if (tails) {   // copy-engine tails (the later buckets' kernels ran beside them)
+    CK(cudaEventRecord(p->ev_dma, ctx->dma));
+    CK(cudaStreamWaitEvent(ctx->comm, p->ev_dma, 0));
   }
   CK(cudaEventRecord(p->ev_comm, ctx->comm));
   CK(cudaStreamWaitEvent(S, p->ev_comm, 0));

@@ -190,7 +190,7 @@ def make_opts(bucket_elems=1 << 26, topology="ho", beta1=0.9, beta2=0.95, eps=1e
     o.skip_nonfinite = 1 if skip_nonfinite else 0
     o.gather_windows = int(gather_windows)
     o.fuse_gather = {"auto": 1, "always": 2, "never": 0, True: 2, False: 0}[fuse_gather]
-    o.copy_engine = {False: 0, True: 1, "gathers": 1, "all": 2, 0: 0, 1: 1, 2: 2}[copy_engine]
+    o.copy_engine = {False: 0, True: 1, "gathers": 1, "all": 2, "tails": 3, 0: 0, 1: 1, 2: 2, 3: 3}[copy_engine]
     o.stream = stream
     o.frozen = 1 if frozen else 0
     o.grad_slots = int(grad_slots)

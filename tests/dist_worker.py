@@ -59,7 +59,8 @@ def main():
                           inter_gbps=inter_gbps, grad_accum=accum > 0, clip_norm=clip,
                           gather_windows=windows, adam_impl=adam_impl, fuse_gather=fuse_gather,
                           copy_engine=copy_engine, grad_slots=slots, wire_dtype=wire, predivide=predivide,
-                          adam_smem_kb=adam_smem_kb, bucket_groups=cfg.get("groups"))
+                          adam_smem_kb=adam_smem_kb, bucket_groups=cfg.get("groups"),
+                          fuse_allreduce=cfg.get("fuse_allreduce", True))
                 fz = None
                 if mask:
                     pl, fz = paro.Plan.masked(ctx, code, sizes, mask, **kw)

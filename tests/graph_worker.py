@@ -34,10 +34,12 @@ def main():
     dist.broadcast(t, 0)
     ctx = paro.Context(world, M, mode="real", rank=rank, device=local, uid=bytes(t.tolist()))
     B = cfg["bucket"]
-    for topo in cfg["topos"]:
+    for name in cfg["topos"]:
+        # "<topo>+ce": copy_engine = 3 (the all-reduce's all-gather half on the copy engines, second stream)
+        topo, ce = (name[:-3], "tails") if name.endswith("+ce") else (name, False)
         s = torch.cuda.Stream()
         pl = paro.Plan(ctx, "NNN", [3 * B], bucket_elems=B, topology=topo, fuse_allreduce=False,
-                       stream=s.cuda_stream)
+                       stream=s.cuda_stream, copy_engine=ce)
         pl.synth_grads(rank, SEED, 1)
         with torch.cuda.stream(s):
             pl.collective(0)            # eager warm-up (kernel attributes, lazy peer access)
@@ -58,7 +60,7 @@ def main():
             torch.cuda.synchronize()
             buf = torch.empty(3 * B, dtype=torch.int16, device="cuda")
             _copy(buf, ghat)
-            np.save(os.path.join(out, f"{topo}_r{rank}_k{k}.npy"), buf.cpu().numpy().view(np.uint16))
+            np.save(os.path.join(out, f"{name}_r{rank}_k{k}.npy"), buf.cpu().numpy().view(np.uint16))
         del g
         pl.close()
         dist.barrier()

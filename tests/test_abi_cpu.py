@@ -100,7 +100,7 @@ def test_send_bytes_match_oracle_simulator(N, M):
     ctx = paro.Context(N, M)
     for code in S.paro_strategies():
         for topo, tr, ce in [(a, b, c) for a in ("ho", "two_step", "flat", "h_ring") for b in ("push", "pull")
-                             for c in (False, "gathers", "all")]:
+                             for c in (False, "gathers", "all", "tails")]:
             pl = paro.Plan(ctx, code, sizes, bucket_elems=B, topology=topo, transport=tr, copy_engine=ce)
             res = ST.strategy_step(code, lay, grads, ST.init_state(w0, lay, code), nm.AdamScalars(1e-3, 1),
                                    topology=topo)

@@ -58,7 +58,8 @@ CODES = ["NNN", "NNI", "NNG", "NII", "NIG", "NGG", "INI", "ING", "III", "IIG", "
 
 @pytest.mark.skipif(_ngpu() < 2, reason="needs >= 2 GPUs")
 @pytest.mark.parametrize("variant", ["default", "paced_lsu", "accum", "clip", "copy_engine", "masked", "slots",
-                                     "tma_thread_store", "fp32_wire", "predivide_off", "layer_windows", "consumer"])
+                                     "tma_thread_store", "fp32_wire", "predivide_off", "layer_windows", "consumer",
+                                     "ce_tails"])
 def test_real_ranks_match_oracle(tmp_path, variant):
     world = _ngpu()                  # every visible GPU: 2 (2x1, 1x2), 4 (4x1, 2x2, 1x4), 8 (8x1, 4x2, 2x4, 1x8)
     splits = [m for m in range(1, world + 1) if world % m == 0]
@@ -92,6 +93,9 @@ def test_real_ranks_match_oracle(tmp_path, variant):
     if variant == "consumer":    # per-bucket parameter consumer (incl. fused gathers: channel-3 barrier)
         cfg.update({"consumer": True, "topos": ["ho", "oneshot"], "transports": ["pull"], "fuse_gather": "always",
                     "grad_slots": 2})
+    if variant == "ce_tails":    # copy_engine = 3: the all-reduce's all-gather rounds on the copy engines
+        cfg.update({"copy_engine": "tails", "fuse_allreduce": False, "topos": ["ho", "two_step", "direct", "oneshot"],
+                    "transports": ["pull"], "fuse_gather": "never"})
     if variant == "masked":      # partial / PEFT training: trainable plan + frozen-parameter plan
         cfg.update({"sizes": [world * 64 * 40 + 24, 333, world * 64 * 9 + 5, 4096], "mask": [0, 1, 0, 1],
                     "topos": ["ho", "two_step"], "transports": ["pull"], "windows": 2})
@@ -164,11 +168,12 @@ def test_collective_graph_replay(tmp_path):
     """The peer barriers keep their state on the device (per-channel launch
     generation advanced by each launch's last CTA), so collective launches can
     be captured once in a CUDA graph and replayed, also between eager calls:
-    every replay's all-reduce equals the oracle (HO-Ring and one-shot)."""
+    every replay's all-reduce equals the oracle (HO-Ring, one-shot, and HO-Ring
+    with its all-gather rounds on the copy engines, copy_engine = 3)."""
     world = _ngpu()
     M = world // 2 if world >= 4 else 1
     B = world * 64 * 32
-    cfg = {"M": M, "bucket": B, "topos": ["ho", "oneshot"], "per_graph": 3, "replays": 4}
+    cfg = {"M": M, "bucket": B, "topos": ["ho", "oneshot", "ho+ce"], "per_graph": 3, "replays": 4}
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr=127.0.0.1", "--master-port=29519", os.path.join(ROOT, "tests", "graph_worker.py"),
            str(tmp_path), json.dumps(cfg)]

@@ -76,15 +76,17 @@ def main():
                "comm_ctas": a.comm_ctas, "entry_barrier": os.environ.get("PARO_ENTRY_BARRIER", "1")}
         factor = 2 * (world - 1) / world if a.op == "ar" else (world - 1) / world
         code, what = ("NNN", 0) if a.op == "ar" else ("NNG", 1)
-        for topo in a.topos.split(","):
+        for name in a.topos.split(","):
+            # "<topo>+ce": copy_engine = 3 (the all-gather half of the all-reduce on the copy engines)
+            topo, ce = (name[:-3], "tails") if name.endswith("+ce") else (name, False)
             bucket = min(elems, 1 << 28)
             pl = paro.Plan(ctx, code, [elems], bucket_elems=bucket, topology=topo, comm_ctas=a.comm_ctas,
                            stream=stream.cuda_stream, transport="pull" if topo == "oneshot" else a.transport,
-                           comm_impl=a.comm_impl,
+                           comm_impl=a.comm_impl, copy_engine=ce,
                            inter_gbps=a.inter_gbps, fuse_gather="never", fuse_allreduce=False)
             pl.synth_grads(rank, 1234, 1)
             ms = timeit(lambda: pl.collective(what))
-            row[topo] = {"ms": round(ms, 4), "busbw_GBps": round(nbytes * factor / (ms / 1e3) / 1e9, 1),
+            row[name] = {"ms": round(ms, 4), "busbw_GBps": round(nbytes * factor / (ms / 1e3) / 1e9, 1),
                          "host_us_per_call": round(host_us["last"], 2)}
             if a.trace:
                 pl.profile_start(64)
@@ -93,7 +95,7 @@ def main():
                 torch.cuda.synchronize()
                 pr = pl.profile_stop()
                 nl = max(1, pr["traced_launches"])
-                row[topo]["trace_us_per_launch"] = {
+                row[name]["trace_us_per_launch"] = {
                     "event": round(1000 * pr["comm_ms"] / max(1, pr["comm_launches"]), 2),
                     "barrier": round(1000 * pr["traced_barrier_ms"] / nl, 2),
                     "work": round(1000 * pr["traced_work_ms"] / nl, 2),
