@@ -1001,16 +1001,8 @@ constexpr int kRtMaxIn = kDevMaxIn;
 constexpr int kRtSmem = kRtStages * 3 * kRtSlotB;   // 96 KB
 
 // log2 of the slot bytes: 8 KB up to 4 inputs, else the largest power of two
-// with 3 stages x max_in slots <= 96 KB (4 KB for 5-8 inputs, 2 KB for 9-16).
-// A launch with the SM to itself (budget_kb > 96: collective-only calls, no
-// Adam CTA beside it) takes up to 16 KB slots with >= 3 stages in its budget.
-constexpr int kRtSoloSmem = 200 * 1024;   // of the SM's 227 KB: static mbarriers + margin
-int rt_slot_lg(int max_in, int budget) {
-  if (budget > kRtSmem) {
-    int lg = 14;
-    while (lg > 10 && (3 * max_in) << lg > budget) --lg;
-    return lg;
-  }
+// with 3 stages x max_in slots <= 96 KB (4 KB for 5-8 inputs, 2 KB for 9-16)
+int rt_slot_lg(int max_in) {
   if (max_in <= 3) return 13;
   static const int env = std::getenv("PARO_RT_SLOT_LG") ? std::atoi(std::getenv("PARO_RT_SLOT_LG")) : 0;
   int lg = 13;   // the largest slot with >= 3 stages in 96 KB (larger bulk copies move more per request)
@@ -1018,15 +1010,13 @@ int rt_slot_lg(int max_in, int budget) {
   if (env >= 10 && env <= 13 && (2 * max_in) << env <= kRtSmem) lg = env;
   return lg;
 }
-int rt_slot_bytes(int max_in) { return 1 << rt_slot_lg(max_in, kRtSmem); }
+int rt_slot_bytes(int max_in) { return 1 << rt_slot_lg(max_in); }
 // stages: 4 for <= 3 inputs (the tuned 8 KB-slot pipeline), else as many as
-// fit the 96 KB (up to 8); PARO_RT_STAGES overrides both (A/B runs).  Solo
-// launches: as many as fit their budget (up to 8).
-int rt_stages(int max_in, int budget) {
-  if (budget > kRtSmem) return std::max(2, std::min(kRtMaxStages, budget / (max_in << rt_slot_lg(max_in, budget))));
+// fit the 96 KB (up to 8); PARO_RT_STAGES overrides both (A/B runs)
+int rt_stages(int max_in) {
   static const int env = std::getenv("PARO_RT_STAGES") ? std::atoi(std::getenv("PARO_RT_STAGES")) : 0;
-  int st = max_in <= 3 ? kRtStages : kRtSmem / (max_in << rt_slot_lg(max_in, kRtSmem));
-  if (env >= 2) st = std::min(env, kRtSmem / (max_in << rt_slot_lg(max_in, kRtSmem)));
+  int st = max_in <= 3 ? kRtStages : kRtSmem / (max_in << rt_slot_lg(max_in));
+  if (env >= 2) st = std::min(env, kRtSmem / (max_in << rt_slot_lg(max_in)));
   return std::max(2, std::min(kRtMaxStages, st));
 }
 
@@ -1065,10 +1055,7 @@ __device__ __forceinline__ void rt_fold_generic(const DTask* tk, unsigned char* 
   const uint32_t raw = tk->rawmask, f32 = tk->f32mask;
   const int nest = tk->nest > 1 ? tk->nest : nin, nblk = tk->nest > 1 ? tk->nblk : 1;
   const int nu = ne / 8;
-  // passes of 256 units, the last first: a bulk fp32 result (4 B per element)
-  // goes back over input 0's slot, where pass k's results cover bytes that a
-  // bf16 input 0 holds only for higher units (16 KB slots: two passes)
-  for (int u0 = ((nu - 1) / kRtThreads) * kRtThreads; u0 >= 0; u0 -= kRtThreads) {
+  for (int u0 = 0; u0 < nu; u0 += kRtThreads) {   // wide tiles: one pass (<= 256 units)
     const int u = u0 + threadIdx.x;
     const bool act = u < nu;
     float acc[8];
@@ -1447,23 +1434,22 @@ cudaError_t launch_rounds(const RoundsArgs& a, int grid, int block, cudaStream_t
 }
 
 cudaError_t launch_rounds_tma(const RoundsArgs& a, int grid, int max_in, cudaStream_t s, int bulk_store,
-                              int generic, int solo) {
+                              int generic) {
   cudaError_t ec = set_carveouts();
   if (ec != cudaSuccess) return ec;
   static bool attr_set = false;
   if (!attr_set) {
     for (const void* f : {(const void*)rounds_tma_kernel<false, false>, (const void*)rounds_tma_kernel<true, false>,
                           (const void*)rounds_tma_kernel<false, true>, (const void*)rounds_tma_kernel<true, true>}) {
-      cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, kRtSoloSmem);
+      cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, kRtSmem);
       if (e != cudaSuccess) return e;
     }
     attr_set = true;
   }
   if (max_in < 1) max_in = 1;
   if (max_in > kRtMaxIn) max_in = kRtMaxIn;
-  const int budget = solo ? kRtSoloSmem : kRtSmem;
-  const int lg = rt_slot_lg(max_in, budget);
-  const int nst = rt_stages(max_in, budget);
+  const int lg = rt_slot_lg(max_in);
+  const int nst = rt_stages(max_in);
   const size_t sm = (size_t)nst * max_in << lg;
   if (generic) {
     if (bulk_store) rounds_tma_kernel<true, true><<<grid, kRtThreads, sm, s>>>(a, max_in, lg, nst);
@@ -1478,7 +1464,7 @@ cudaError_t launch_rounds_tma(const RoundsArgs& a, int grid, int max_in, cudaStr
 int rounds_tma_smem_kb(int max_in) {
   if (max_in < 1) max_in = 1;
   if (max_in > kRtMaxIn) max_in = kRtMaxIn;
-  return (rt_stages(max_in, kRtSmem) * max_in * rt_slot_bytes(max_in) + 1023) / 1024;
+  return (rt_stages(max_in) * max_in * rt_slot_bytes(max_in) + 1023) / 1024;
 }
 
 cudaError_t launch_adam(const AdamArgs& a, int grid, cudaStream_t s, int cap_two_per_sm) {

@@ -140,11 +140,9 @@ enum AdamVariant : int {
 // ws: 1 the warp-specialized TMA-store kernel, 0 the single-role one, -1 automatic
 cudaError_t launch_adam_tma(const AdamArgs& a, int sms, cudaStream_t s, int smem_budget_kb, int tma_store,
                             int hard_kb, int* variant, int* stages, int ws);
-// generic: the launch has fp32-wire (out_f32) or nested (one-shot) tasks;
-// solo: no Adam CTA shares the SMs (collective-only calls): up to 200 KB of
-// stages (16 KB slots) instead of the 96 KB co-run budget
+// generic: the launch has fp32-wire (out_f32) or nested (one-shot) tasks
 cudaError_t launch_rounds_tma(const RoundsArgs& a, int grid, int max_in, cudaStream_t s, int bulk_store,
-                              int generic, int solo = 0);
+                              int generic);
 int rounds_tma_smem_kb(int max_in);   // dynamic shared memory of a TMA rounds CTA
 cudaError_t launch_norm_finalize(const double* partials, int n, double* out, cudaStream_t s);
 // phase 1 of the two-phase step: block partials of sum (fold(gin) * s_g)^2 and

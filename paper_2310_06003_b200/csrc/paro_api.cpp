@@ -81,7 +81,6 @@ struct DevLaunch {
   int nrounds = 0;
   int final_barrier = 0;
   uint64_t final_peers = 0;
-  int64_t max_round_elems = 0;   // the local rank's largest round (elements folded or copied)
   // copy-engine tail (opts.copy_engine = 3): the launch's trailing pure-copy
   // rounds, run by the copy engines after the kernel's rounds [0, nrounds)
   std::vector<DevLaunch> tail;
@@ -103,7 +102,6 @@ struct paro_plan {
   std::vector<cudaEvent_t> ev_pfinal;     // bucket b's parameters final on this rank
   cudaEvent_t ev_dma = nullptr;
   cudaEvent_t ev_tail = nullptr;          // comm -> dma hand-over of a copy-engine tail
-  bool solo = false;                      // inside paro_collective: no Adam CTA beside the rounds
   DRound* d_rounds = nullptr;
   DTask* d_tasks = nullptr;
   std::vector<DevLaunch> red, gat;        // per bucket
@@ -335,7 +333,6 @@ paro_status_t upload_schedule(PlanT* p) {
         d.peers_before = 0;
       }
       d.t1 = (int32_t)tasks.size();
-      dl.max_round_elems = std::max(dl.max_round_elems, (int64_t)d.units * 8);
       for (int ti = d.t0; ti < d.t1; ++ti) {
         dl.max_in = std::max(dl.max_in, (int)tasks[ti].nin);
         if (tasks[ti].out_f32 || tasks[ti].nest > 1) dl.generic = 1;
@@ -614,18 +611,6 @@ paro_status_t run_launch(PlanT* p, const DevLaunch& dl, int* nlaunch, bool* tail
   return PARO_OK;
 }
 
-// Collective-only calls (paro_collective) have the SMs to themselves: their
-// launches may take up to 200 KB of TMA stages (16 KB slots) instead of the
-// 96 KB that leaves room for an Adam CTA, once a round gives every CTA at
-// least one 16 KB-slot tile (PARO_RT_SOLO = 0 / 1: never / always, A/B runs).
-int solo_stages(const PlanT* p, const DevLaunch& dl) {
-  if (!p->solo) return 0;
-  const char* e = std::getenv("PARO_RT_SOLO");
-  const int env = e ? std::atoi(e) : -1;
-  if (env >= 0) return env ? 1 : 0;
-  return dl.max_round_elems >= (int64_t)p->ctx->sm_count * 8192 ? 1 : 0;
-}
-
 // The rounds-kernel part of a launch, on the comm stream.
 paro_status_t run_launch_kernel(PlanT* p, const DevLaunch& dl, int* nlaunch) {
   paro_ctx* ctx = p->ctx;
@@ -660,8 +645,7 @@ paro_status_t run_launch_kernel(PlanT* p, const DevLaunch& dl, int* nlaunch) {
       p->trace_nrounds.push_back(dl.nrounds);
       p->trace_grids.push_back(grid);
     }
-    if (p->opts.comm_impl != 1)
-      CK(launch_rounds_tma(a, grid, dl.max_in, ctx->comm, p->opts.comm_impl == 2, dl.generic, solo_stages(p, dl)));
+    if (p->opts.comm_impl != 1) CK(launch_rounds_tma(a, grid, dl.max_in, ctx->comm, p->opts.comm_impl == 2, dl.generic));
     else CK(launch_rounds(a, grid, 0, ctx->comm));
     prof_end(p, ctx->comm, k);
     ++*nlaunch;
@@ -670,8 +654,7 @@ paro_status_t run_launch_kernel(PlanT* p, const DevLaunch& dl, int* nlaunch) {
       a.rounds = p->d_rounds + dl.round_off + r;
       a.nrounds = 1;
       const int k = prof_begin(p, ctx->comm, 1, r == 0 ? dl.bytes : 0, r == 0 ? dl.hbm : 0);
-      if (p->opts.comm_impl != 1)
-        CK(launch_rounds_tma(a, grid, dl.max_in, ctx->comm, p->opts.comm_impl == 2, dl.generic, solo_stages(p, dl)));
+      if (p->opts.comm_impl != 1) CK(launch_rounds_tma(a, grid, dl.max_in, ctx->comm, p->opts.comm_impl == 2, dl.generic));
       else CK(launch_rounds(a, grid, 0, ctx->comm));
       prof_end(p, ctx->comm, k);
       ++*nlaunch;
@@ -1949,8 +1932,6 @@ paro_status_t paro_collective(paro_plan_t p, int what) {
   CK(cudaEventRecord(p->ev_fork, S));
   CK(cudaStreamWaitEvent(ctx->comm, p->ev_fork, 0));
   const bool nccl = pl.opt.topology == PARO_TOPO_NCCL;
-  p->solo = true;
-  struct SoloOff { PlanT* p; ~SoloOff() { p->solo = false; } } solo_off{p};
   for (size_t b = 0; b < pl.buckets.size() && pl.N > 1; ++b) {
     if (nccl) {
       if (what == 0 && p->red[b].nrounds > 0) {   // fp32 wire: pre-scale into fp32 first
