@@ -51,7 +51,7 @@ def parse(argv=None):
     ap.add_argument("--group-size", type=int, default=0, help="M; default N/2 for N>=4, else 1")
     ap.add_argument("--topology", default="ho", choices=["ho", "two_step", "flat", "direct", "nccl", "oneshot"])
     ap.add_argument("--bucket", type=int, default=1 << 29)
-    ap.add_argument("--comm-ctas", type=int, default=0, help="0: sized per launch by the library")
+    ap.add_argument("--comm-ctas", type=int, default=0, help="0: one collective CTA per SM")
     ap.add_argument("--depth", type=int, default=1)
     ap.add_argument("--transport", default="pull", choices=["pull", "push"])
     ap.add_argument("--adam-impl", default="auto", choices=["auto", "lsu", "tma_store"])
@@ -62,6 +62,8 @@ def parse(argv=None):
                     help="parameter all-gathers (pure bit copies) on the copy engines: measured 2x2 IIG "
                          "20.43 vs 21.10 ms (profiles/r02/sweep_copy_engine_iig_2x2.jsonl)")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-bucket", type=int, default=0,
+                    help="bucket elements of the e2e (streamed) plan; 0 = --bucket")
     ap.add_argument("--e2e-mode", default="stream", choices=["stream", "pack"],
                     help="stream: a grad_slots plan whose producer copies each bucket host->device on the "
                          "copy engines while the step runs (paro_step_streamed); pack: per-tensor pinned "
@@ -402,7 +404,10 @@ def run_ours(args):
             # same strategy / split / kernels, gradients streamed bucket by bucket from pinned host
             # memory by the copy engines, overlapped with the reductions and updates of earlier buckets
             plan.close()
-            eplan = paro.Plan(ctx, args.strategy, sizes, grad_slots=4, **plan_kwargs(args, stream.cuda_stream))
+            ekw = plan_kwargs(args, stream.cuda_stream)
+            if args.e2e_bucket > 0:   # smaller buckets: shorter pipeline fill / drain on the host link
+                ekw["bucket_elems"] = min(args.e2e_bucket, args.bucket)
+            eplan = paro.Plan(ctx, args.strategy, sizes, grad_slots=4, **ekw)
             eplan.opt_state_init(rank, ptrs[0], seed=SEED)
             rt = _cudart()
             bspan = max(8, cap - info["bucket_elems"])
@@ -462,6 +467,7 @@ def run_ours(args):
         ems_s = e2e_run(False)
         eplan.set_param_consumer(None)
         e2e = {"value": info["psi"] / (ems_p / 1000.0), "unit": "params/s", "h2d_bytes_per_step": 2 * info["psi"],
+               "bucket_elems": eplan.info()["bucket_elems"],
                "d2h_bytes_per_step": pbytes + 12, "ms_per_step": ems_p,
                # the host link bounds it: bytes over PCIe per step / step time, per GPU
                "pcie_GBps_per_gpu": (2 * info["psi"] + pbytes) / (ems_p / 1000.0) / 1e9,
