@@ -5,7 +5,7 @@ mkdir -p gpurun_out
 python -c 'import __graft_entry__ as g; g.build()' > gpurun_out/build.log 2>&1 || { echo build failed; exit 1; }
 OUT=gpurun_out/e2e_bucket_ab.jsonl
 : > $OUT
-for eb in 0 268435456 134217728 67108864; do
+for eb in ${EBS:-0 268435456 134217728 67108864}; do
 timeout 600 python bench.py --steps 3 --warmup 3 --no-cpu-baseline --e2e-bucket $eb > gpurun_out/b.json 2> gpurun_out/b.err
 python - "$eb" >> $OUT <<'PY'
 import json, sys
