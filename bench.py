@@ -62,8 +62,10 @@ def parse(argv=None):
                     help="parameter all-gathers (pure bit copies) on the copy engines: measured 2x2 IIG "
                          "20.43 vs 21.10 ms (profiles/r02/sweep_copy_engine_iig_2x2.jsonl)")
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--e2e-bucket", type=int, default=0,
-                    help="bucket elements of the e2e (streamed) plan; 0 = --bucket")
+    ap.add_argument("--e2e-bucket", type=int, default=1 << 26,
+                    help="bucket elements of the e2e (streamed) plan (0 = --bucket): smaller buckets shorten "
+                         "the host link's pipeline fill and drain, N = 1 params-back 2^29: 305 ms, 2^26: 276-293 "
+                         "(profiles/r02/e2e_bucket_ab_1gpu.jsonl)")
     ap.add_argument("--e2e-mode", default="stream", choices=["stream", "pack"],
                     help="stream: a grad_slots plan whose producer copies each bucket host->device on the "
                          "copy engines while the step runs (paro_step_streamed); pack: per-tensor pinned "
