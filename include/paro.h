@@ -243,9 +243,6 @@ typedef struct {
   int64_t accum_step_send_bytes_intra, accum_step_send_bytes_inter;
   int64_t grad_buffer_bytes;           /* raw gradient buffer per rank: 2 psi_pad, or *
                                         * 2 K B with grad_slots = K                    */
-  int32_t n_column_rounds;             /* real mode: rounds of the uploaded schedule   *
-                                        * entered through a column barrier (CTA c with *
-                                        * the peers' CTAs c), 0 otherwise   */
 } paro_plan_info_t;
 
 typedef struct {

@@ -210,45 +210,6 @@ __device__ __forceinline__ bool launch_barrier(const RoundsArgs& a, uint64_t pee
   return ok;
 }
 
-// Column barrier: CTA c publishes its own progress (everything it wrote in
-// the launch so far: thread stores ordered by the CTA barrier, bulk stores
-// completed by wait_group 0 before the caller's __syncthreads) with one
-// fence.acq_rel.sys and relaxed flag stores into the peers' column slots
-// [me][c], then waits for the peers' CTAs c only.  No grid arrival and no `go`
-// hand-off: a CTA waits for its own column, not for the slowest CTA.  As a
-// final barrier it is always sufficient (the launch completes when every
-// column has, so the union over columns is the full barrier); between rounds
-// the host marks it only where every cross-round conflict stays in one column.
-__device__ bool column_barrier(const RoundsArgs& a, uint64_t peers, int bidx, uint64_t gen0) {
-  __shared__ int s_ok;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int ok = 1;
-    volatile int* err = a.bar.err;
-    const uint64_t val = gen0 * 256ull + (uint64_t)bidx + 1ull;
-    const uint64_t t0 = globaltimer();
-    asm volatile("fence.acq_rel.sys;" ::: "memory");
-    for (int x = 0; x < 64; ++x)
-      if ((peers >> x) & 1ull) st_relaxed_sys(a.bar.col_peer[x] + blockIdx.x, val);
-    for (int x = 0; x < 64 && ok; ++x) {
-      if (!((peers >> x) & 1ull)) continue;
-      while (ld_acquire_sys(a.bar.col_my + (size_t)x * kColCtas + blockIdx.x) < val) {
-        if (*err || globaltimer() - t0 > kTimeoutNs) { ok = 0; atomicExch((int*)err, 2); break; }
-      }
-    }
-    if (*err) ok = 0;
-    s_ok = ok;
-  }
-  __syncthreads();
-  return s_ok != 0;
-}
-
-// the launch's final barrier: a column barrier where the host enabled it
-__device__ __forceinline__ bool final_barrier(const RoundsArgs& a, int& bidx, int& narr, uint64_t gen0) {
-  if (a.col_final && a.bar.col_my) return column_barrier(a, a.final_peers, bidx++, gen0);
-  return launch_barrier(a, a.final_peers, bidx, narr, gen0);
-}
-
 // the channel's launch generation, read by every CTA at start: the previous
 // launch on this channel (same stream) has exited, so the value is stable
 __device__ __forceinline__ uint64_t launch_gen(const RoundsArgs& a) {
@@ -418,7 +379,7 @@ __global__ void __maxnreg__(48) rounds_kernel(const RoundsArgs a) {
     __syncthreads();
     trace_stamp(a, 2 + 2 * r);
   }
-  if (a.bar.my_flags && a.final_barrier && !final_barrier(a, bidx, narr, gen0)) return;
+  if (a.bar.my_flags && a.final_barrier && !launch_barrier(a, a.final_peers, bidx, narr, gen0)) return;
   if (threadIdx.x == 0) flush_moved(a.moved, mi, me);
   launch_exit(a, gen0);
   trace_stamp(a, kTraceSlots - 1);
@@ -1063,29 +1024,6 @@ int rt_stages(int max_in) {
 // wire tasks have fp32 results, whose tile goes back over input 0's slot)
 __device__ __forceinline__ int rt_te_lg(const DTask* tk, int slot_lg) { return slot_lg - (tk->out_f32 ? 2 : 1); }
 
-// Column round: the k-th tile of CTA c is tile c + j * grid of some task (every
-// task's tiles dealt from CTA 0), so tile t of any task is always CTA t % grid's
-__device__ __forceinline__ bool rt_tile_col(const RoundsArgs& a, const DRound& rd, int64_t k, int slot_lg,
-                                            const DTask*& task, int64_t& e0, int& ne) {
-  const int64_t c = blockIdx.x, G = gridDim.x;
-  for (int ti = rd.t0; ti < rd.t1; ++ti) {
-    const DTask* tk = a.tasks + ti;
-    if (tk->nin > kRtMaxIn) continue;
-    const int lg = rt_te_lg(tk, slot_lg);
-    const int64_t n = tk->n8 * 8;
-    const int64_t nt = (n + (1ll << lg) - 1) >> lg;
-    const int64_t mine = nt > c ? (nt - c + G - 1) / G : 0;
-    if (k < mine) {
-      task = tk;
-      e0 = (c + k * G) << lg;
-      ne = (int)min((int64_t)1 << lg, n - e0);
-      return true;
-    }
-    k -= mine;
-  }
-  return false;
-}
-
 __device__ __forceinline__ bool rt_tile(const RoundsArgs& a, const DRound& rd, int64_t t, int slot_lg,
                                         const DTask*& task, int64_t& e0, int& ne) {
   for (int ti = rd.t0; ti < rd.t1; ++ti) {
@@ -1205,38 +1143,26 @@ __global__ void __launch_bounds__(kRtThreads, 4) rounds_tma_kernel(const RoundsA
   trace_stamp(a, 0);
   for (int r = 0; r < a.nrounds; ++r) {
     const DRound rd = a.rounds[r];
-    if (a.bar.my_flags) {
-      if (rd.col && r > 0 && a.bar.col_my) {
-        if (!column_barrier(a, rd.peers_before, bidx++, gen0)) return;
-      } else if (!launch_barrier(a, rd.peers_before, bidx, narr, gen0)) {
-        return;
-      }
-    }
+    if (a.bar.my_flags && !launch_barrier(a, rd.peers_before, bidx, narr, gen0)) return;
     // order the peers' released (generic-proxy) writes before our async-proxy reads
     if (threadIdx.x == 0) asm volatile("fence.proxy.async;" ::: "memory");
     trace_stamp(a, 1 + 2 * r);
-    int64_t mine = 0;
+    int64_t total = 0;
     for (int ti = rd.t0; ti < rd.t1; ++ti) {
       const DTask* tk = a.tasks + ti;
       if (tk->nin <= kRtMaxIn) {
         const int lg = rt_te_lg(tk, slot_lg);
-        const int64_t nt = (tk->n8 * 8 + (1ll << lg) - 1) >> lg;
-        if (rd.col) mine += nt > blockIdx.x ? (nt - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-        else mine += nt;
+        total += (tk->n8 * 8 + (1ll << lg) - 1) >> lg;
       }
     }
-    if (!rd.col) mine = (mine > blockIdx.x) ? (mine - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-    auto tile_of = [&](int64_t k, const DTask*& tk, int64_t& e0, int& ne) {
-      if (rd.col) rt_tile_col(a, rd, k, slot_lg, tk, e0, ne);
-      else rt_tile(a, rd, blockIdx.x + k * gridDim.x, slot_lg, tk, e0, ne);
-    };
+    const int64_t mine = (total > blockIdx.x) ? (total - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
     const uint64_t t_round = globaltimer();
     double inter_sent = 0.0;   // bytes of inter-group tiles this CTA has issued in this round
     auto issue = [&](int64_t k) {
       const DTask* tk;
       int64_t e0;
       int ne;
-      tile_of(k, tk, e0, ne);
+      rt_tile(a, rd, blockIdx.x + k * gridDim.x, slot_lg, tk, e0, ne);
       if (tk->inter && a.inter_bytes_per_ns > 0.0) {   // token bucket: emulated slow inter link
         inter_sent += (double)ne * (tk->out_f32 ? 4.0 : 2.0) * (double)tk->inter;
         while (inter_sent > (double)(globaltimer() - t_round) * a.inter_bytes_per_ns) __nanosleep(256);
@@ -1262,7 +1188,7 @@ __global__ void __launch_bounds__(kRtThreads, 4) rounds_tma_kernel(const RoundsA
       const DTask* tk;
       int64_t e0;
       int ne;
-      tile_of(k, tk, e0, ne);
+      rt_tile(a, rd, blockIdx.x + k * gridDim.x, slot_lg, tk, e0, ne);
       unsigned char* base = smem + slot * stage_bytes;
       const int nin = tk->nin;
       const uint32_t raw = tk->rawmask;
@@ -1312,7 +1238,7 @@ __global__ void __launch_bounds__(kRtThreads, 4) rounds_tma_kernel(const RoundsA
     __syncthreads();
     trace_stamp(a, 2 + 2 * r);
   }
-  if (a.bar.my_flags && a.final_barrier && !final_barrier(a, bidx, narr, gen0)) return;
+  if (a.bar.my_flags && a.final_barrier && !launch_barrier(a, a.final_peers, bidx, narr, gen0)) return;
   if (threadIdx.x == 0) flush_moved(a.moved, mi, me);
   launch_exit(a, gen0);
   trace_stamp(a, kTraceSlots - 1);
@@ -1533,12 +1459,6 @@ cudaError_t launch_rounds_tma(const RoundsArgs& a, int grid, int max_in, cudaStr
     else rounds_tma_kernel<false, false><<<grid, kRtThreads, sm, s>>>(a, max_in, lg, nst);
   }
   return cudaGetLastError();
-}
-
-int rounds_tma_tile_elems(int max_in, int out_f32) {
-  if (max_in < 1) max_in = 1;
-  if (max_in > kRtMaxIn) max_in = kRtMaxIn;
-  return 1 << (rt_slot_lg(max_in) - (out_f32 ? 2 : 1));
 }
 
 int rounds_tma_smem_kb(int max_in) {

@@ -18,12 +18,7 @@ namespace paro {
 
 constexpr int kDevMaxIn = 16;
 constexpr int kMaxAdamSegs = 16;  // emulated ranks per Adam launch
-// per-rank region header: flags + counters of the barrier channels, then the
-// column flags of channel 0 ([sender rank < kColRanks][CTA < kColCtas] uint64)
-constexpr int kColOff = 4096;
-constexpr int kColRanks = 64;
-constexpr int kColCtas = 256;
-constexpr int kHeaderBytes = kColOff + kColRanks * kColCtas * 8;
+constexpr int kHeaderBytes = 4096;   // per-rank region header: flags + counters
 
 struct DTask {
   const uint16_t* in[kDevMaxIn];   // element pointers (bf16, or fp32 where f32mask says so)
@@ -46,18 +41,12 @@ struct DRound {
   int32_t t0, t1;        // task range
   int64_t units;         // sum of n8
   uint64_t peers_before; // barrier peer mask before this round (real mode)
-  int32_t col;           // 1: column round: CTA c takes tiles t = c (mod grid) of every task, and
-                         // the barrier before it is a column barrier (CTA c with the peers'
-                         // CTAs c only); the host proved every cross-round conflict column-local
-  int32_t pad;
 };
 
 // Region header layout (bytes), channel 0 (collective launches): [0, 512) uint64
 // flags[64] indexed by sender; [512] arrive; [520] int32 error word; [528] go;
 // [536] launch generation; [544] exit count.  Channel 2 (copy-engine barriers)
-// at [1024, 1536) flags, [1536] arrive, [1544] go, [1552] generation, [1560] exit;
-// channel 3 (parameter consumer) the same at +2048.  [kColOff, kHeaderBytes):
-// channel 0's column flags.
+// at [1024, 1536) flags, [1536] arrive, [1544] go, [1552] generation, [1560] exit.
 struct BarrierCtx {
   uint64_t* const* peer_slot;   // [N] device array: &flags_of_peer_x[me]
   uint64_t* my_flags;           // NULL => emulated mode (no barriers)
@@ -68,8 +57,6 @@ struct BarrierCtx {
                                 // and the last CTA to exit advances it (device-resident, so
                                 // launches need no host bookkeeping and can be graph-replayed)
   unsigned int* exitc;          // CTAs of the running launch that have exited
-  uint64_t* const* col_peer;    // [N] device array: &column_flags_of_peer_x[me][0] (channel 0), or NULL
-  uint64_t* col_my;             // this rank's column flags [sender][CTA], or NULL
 };
 
 constexpr int kTraceSlots = 64;   // per CTA per traced launch: start, (barrier exit, work end) x rounds, end
@@ -88,9 +75,6 @@ struct RoundsArgs {
   int entry_fast;               // the launch's first barrier (no work of this launch before it) is
                                 // published by CTA 0 alone, without the grid arrival
   unsigned long long* moved;    // [intra, inter] NVLink bytes this rank's CTAs pulled + pushed (or NULL)
-  int col_final;                // the final barrier is a column barrier: CTA c publishes its own
-                                // completion and waits for the peers' CTAs c (the kernel completes
-                                // once every column has, so the union is the full barrier)
   BarrierCtx bar;
 };
 
@@ -156,8 +140,6 @@ enum AdamVariant : int {
 // ws: 1 the warp-specialized TMA-store kernel, 0 the single-role one, -1 automatic
 cudaError_t launch_adam_tma(const AdamArgs& a, int sms, cudaStream_t s, int smem_budget_kb, int tma_store,
                             int hard_kb, int* variant, int* stages, int ws);
-// elements per tile of a TMA rounds launch (host planning of column rounds)
-int rounds_tma_tile_elems(int max_in, int out_f32);
 // generic: the launch has fp32-wire (out_f32) or nested (one-shot) tasks
 cudaError_t launch_rounds_tma(const RoundsArgs& a, int grid, int max_in, cudaStream_t s, int bulk_store,
                               int generic);

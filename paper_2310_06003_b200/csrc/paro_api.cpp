@@ -96,8 +96,6 @@ struct paro_plan {
   uint64_t** d_peer_slot = nullptr;       // real mode
   uint64_t** d_peer_slot2 = nullptr;      // second barrier channel (copy-engine launches)
   uint64_t** d_peer_slot3 = nullptr;      // third channel (parameter consumer stream)
-  uint64_t** d_col_peer = nullptr;        // channel 0 column flags: [peer] -> its [me][0] slot
-  int n_col_rounds = 0;                   // uploaded rounds entered through a column barrier
   paro_param_consumer_t cons_fn = nullptr;  // per-bucket consumer of the updated parameters
   void* cons_user = nullptr;
   cudaEvent_t ev_cons = nullptr;
@@ -305,78 +303,6 @@ DTask resolve(const PlanT* p, const Task& t, int executing_rank, int acc_kind, i
   return d;
 }
 
-int comm_grid(const PlanT* p);
-
-// Column barrier / A-B switch (PARO_COL_BARRIER=0: every barrier of channel 0
-// is the grid-wide one, as in round 1)
-bool col_barrier_on() {
-  static const bool on = !(std::getenv("PARO_COL_BARRIER") && std::atoi(std::getenv("PARO_COL_BARRIER")) == 0);
-  return on;
-}
-
-// Rounds of launch L whose preceding barrier may be a column barrier (kernels.cu
-// column_barrier): CTA c of rank y waits only for the peers' CTAs c.  Valid for
-// round r (r >= 1, round r-1 not itself a column round) when every pair of
-// accesses that conflict across the two rounds (a write in one, any access in
-// the other, same rank's memory, overlapping bytes; any two ranks, including
-// the same one) is handled by the same column on both sides: round r deals
-// every task's tiles from CTA 0 (tile t -> CTA t % G), round r-1 must have one
-// task on the accessing rank (the same dealing), both accesses start at the
-// same element offset with the same tile size (so element e is tile e / te on
-// both sides), and the other rank is among the peers the barrier waits for.
-// Computed from the global schedule, so every rank takes the same decision.
-std::vector<int32_t> column_rounds(const PlanT* p, const Launch& L) {
-  const Planner& pl = *p->pl;
-  const int R = (int)L.rounds.size();
-  std::vector<int32_t> col(R, 0);
-  if (!col_barrier_on() || p->ctx->mode != MODE_REAL || p->opts.comm_impl == 1 || R < 2) return col;
-  if (pl.N > kColRanks || comm_grid(p) > kColCtas) return col;
-  std::vector<int> max_in(pl.N, 1);   // per rank, as the kernel launch of that rank sizes its tiles
-  for (int r = 0; r < R; ++r)
-    for (int x = 0; x < pl.N; ++x)
-      for (const Task& t : L.rounds[r][x]) max_in[x] = std::max(max_in[x], (int)t.nin);
-  struct Acc {
-    int rank, kind;
-    int64_t off, n;
-    bool write;
-    int te;
-  };
-  auto accesses = [&](const Task& t, int x) {
-    std::vector<Acc> v;
-    const int te = rounds_tma_tile_elems(max_in[x], pl.esz[t.dst.kind] == 4 ? 1 : 0);
-    for (int i = 0; i < t.nin; ++i) v.push_back({t.in[i].rank, t.in[i].kind, t.in[i].off, t.n, false, te});
-    v.push_back({t.dst.rank, t.dst.kind, t.dst.off, t.n, true, te});
-    return v;
-  };
-  for (int r = 1; r < R; ++r) {
-    if (col[r - 1]) continue;
-    bool ok = true;
-    for (int y = 0; y < pl.N && ok; ++y) {
-      const uint64_t peers = L.barrier_peers(r, y);
-      for (const Task& B : L.rounds[r][y]) {
-        for (const Acc& b : accesses(B, y)) {
-          for (int x = 0; x < pl.N && ok; ++x) {
-            for (const Task& A : L.rounds[r - 1][x]) {
-              for (const Acc& a : accesses(A, x)) {
-                if (a.rank != b.rank || a.kind != b.kind || !(a.write || b.write)) continue;
-                const int64_t es = pl.esz[a.kind];
-                const bool overlap = a.off * es < (b.off + b.n) * es && b.off * es < (a.off + a.n) * es;
-                if (!overlap) continue;
-                ok = ok && a.off == b.off && a.te == b.te && L.rounds[r - 1][x].size() == 1 &&
-                     (x == y || ((peers >> x) & 1ull));
-              }
-            }
-          }
-          if (!ok) break;
-        }
-        if (!ok) break;
-      }
-    }
-    col[r] = ok ? 1 : 0;
-  }
-  return col;
-}
-
 // Build device round/task arrays for every bucket's launches.
 paro_status_t upload_schedule(PlanT* p) {
   paro_ctx* ctx = p->ctx;
@@ -388,11 +314,8 @@ paro_status_t upload_schedule(PlanT* p) {
     dl.round_off = (int64_t)rounds.size();
     if (L.empty()) return dl;
     const int R = (int)L.rounds.size();
-    const std::vector<int32_t> col = (acc_kind < 0 && win_shift == 0) ? column_rounds(p, L) : std::vector<int32_t>(R, 0);
     for (int r = 0; r < R; ++r) {
       DRound d{};
-      d.col = col[r];
-      p->n_col_rounds += col[r];
       d.t0 = (int32_t)tasks.size();
       d.units = 0;
       if (ctx->mode == MODE_REAL) {
@@ -715,11 +638,6 @@ paro_status_t run_launch_kernel(PlanT* p, const DevLaunch& dl, int* nlaunch) {
     a.bar.err = reinterpret_cast<int*>(hdr + 520);
     a.bar.gen = reinterpret_cast<unsigned long long*>(hdr + 536);
     a.bar.exitc = reinterpret_cast<unsigned int*>(hdr + 544);
-    if (p->d_col_peer && col_barrier_on() && grid <= kColCtas && p->opts.comm_impl != 1) {
-      a.bar.col_peer = p->d_col_peer;
-      a.bar.col_my = reinterpret_cast<uint64_t*>(hdr + kColOff);
-      a.col_final = 1;
-    }
     a.sys_fence_all = p->pl->opt.push ? 1 : 0;
     const int k = prof_begin(p, ctx->comm, 1, dl.bytes, dl.hbm);
     if (p->prof && p->d_trace && (int)p->trace_nrounds.size() < kTraceLaunches) {
@@ -826,7 +744,6 @@ void destroy_plan(PlanT* p) {
     cudaFree(p->d_peer_slot);
     cudaFree(p->d_peer_slot2);
     cudaFree(p->d_peer_slot3);
-    cudaFree(p->d_col_peer);
     if (p->ev_cons) cudaEventDestroy(p->ev_cons);
     for (cudaEvent_t e : p->ev_pfinal) if (e) cudaEventDestroy(e);
     cudaFree(p->d_rounds);
@@ -1120,12 +1037,6 @@ paro_status_t paro_plan(paro_ctx_t ctx, const char* strategy, const int64_t* par
     for (int x = 0; x < N; ++x) slots[x] = reinterpret_cast<uint64_t*>(p->peer_base[x] + 2048) + ctx->rank;
     PCK(cudaMalloc(&p->d_peer_slot3, 64 * sizeof(uint64_t*)));
     PCK(cudaMemcpy(p->d_peer_slot3, slots.data(), 64 * sizeof(uint64_t*), cudaMemcpyHostToDevice));
-    if (N <= kColRanks) {
-      for (int x = 0; x < N; ++x)
-        slots[x] = reinterpret_cast<uint64_t*>(p->peer_base[x] + kColOff) + (size_t)ctx->rank * kColCtas;
-      PCK(cudaMalloc(&p->d_col_peer, 64 * sizeof(uint64_t*)));
-      PCK(cudaMemcpy(p->d_col_peer, slots.data(), 64 * sizeof(uint64_t*), cudaMemcpyHostToDevice));
-    }
   }
   {
     paro_status_t s2 = upload_schedule(p);
@@ -1239,7 +1150,6 @@ paro_status_t paro_plan_info(paro_plan_t p, paro_plan_info_t* out) {
   out->step_send_bytes_inter = pl.send_inter[me];
   out->n_rounds = pl.n_rounds;
   out->n_comm_launches = pl.n_comm_launches;
-  out->n_column_rounds = p->n_col_rounds;
   if (pl.opt.accum) {
     out->accum_send_bytes_intra = pl.acc_send_intra[me];
     out->accum_send_bytes_inter = pl.acc_send_inter[me];

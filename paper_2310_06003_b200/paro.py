@@ -61,7 +61,7 @@ class paro_plan_info_t(C.Structure):
                 ("n_rounds", C.c_int32), ("n_comm_launches", C.c_int32),
                 ("accum_send_bytes_intra", C.c_int64), ("accum_send_bytes_inter", C.c_int64),
                 ("accum_step_send_bytes_intra", C.c_int64), ("accum_step_send_bytes_inter", C.c_int64),
-                ("grad_buffer_bytes", C.c_int64), ("n_column_rounds", C.c_int32)]
+                ("grad_buffer_bytes", C.c_int64)]
 
 
 class paro_step_stats_t(C.Structure):
