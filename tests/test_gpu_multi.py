@@ -187,3 +187,36 @@ def test_collective_graph_replay(tmp_path):
                 got = np.load(tmp_path / f"{topo}_r{rank}_k{k}.npy")
                 for b, (s0, n) in enumerate(lay.buckets):   # bucket b's average in slot b % 3
                     assert np.array_equal(got[b * B:b * B + n], gh[s0:s0 + n]), (topo, rank, k, b)
+
+
+@pytest.mark.skipif(_ngpu() < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("comm_impl", ["tma_store", "tma"])
+def test_collective_allreduce_real_ranks(tmp_path, comm_impl):
+    """BASELINE config 5 through real ranks: two back-to-back paro_collective(0)
+    all-reduces per topology, at a bucket where the one-shot all-reduce runs as
+    reduce-scatter + all-gather, with the bulk-store and thread-store rounds
+    kernels, equal the oracle (HO-Ring / two-step / direct / one-shot:
+    dp_reduce; flat: the oracle's flat ring), bucket by bucket with a ragged
+    last bucket."""
+    world = _ngpu()
+    M = world // 2 if world >= 4 else 1
+    B = world * 64 * 9000                      # one-shot at N >= 3: RS + AG (extra bytes > 6 MiB)
+    n = 3 * B - world * 64 * 7                 # 3 buckets, ragged last
+    topos = ["ho", "two_step", "direct", "oneshot", "flat"]
+    cfg = {"M": M, "bucket": B, "n": n, "topos": topos, "comm_impl": comm_impl}
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr=127.0.0.1", "--master-port=29521", os.path.join(ROOT, "tests", "coll_worker.py"),
+           str(tmp_path), json.dumps(cfg)]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    lay = L.Layout([n], world, M, B)
+    grads = [grad_bits(r_, 1, 0, lay.psi) for r_ in range(world)]
+    gh = ST.dp_reduce(lay, grads)
+    res = ST.strategy_step("NNN", lay, grads, ST.init_state(master_f32(0, lay.psi), lay, "NNN"),
+                           nm.AdamScalars(3e-4, 1), topology="flat")
+    for topo in topos:
+        for rank in range(world):
+            want = res.ghat_os[rank] if topo == "flat" else gh
+            got = np.load(tmp_path / f"{topo}_r{rank}.npy")
+            for b, (s0, nn) in enumerate(lay.buckets):    # bucket b in slot b % 3 (3 buckets: one each)
+                assert np.array_equal(got[b * B:b * B + nn], want[s0:s0 + nn]), (topo, rank, b)
