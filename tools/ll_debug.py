@@ -43,7 +43,7 @@ def main():
         got = grab()
         bad = np.nonzero(got != ref)[0]
         out.append({"rank": rank, "tag": tag, "bad": int(bad.size), "first": bad[:8].tolist(),
-                    "err": pl.ctx.last_error() if hasattr(pl.ctx, "last_error") else None})
+                    "got": got[bad[:4]].tolist(), "want": ref[bad[:4]].tolist()})
 
     for k in range(4):
         with torch.cuda.stream(s):
@@ -60,6 +60,20 @@ def main():
         with torch.cuda.stream(s):
             pl.collective(0)
         check(f"eager_after_replay{k}")
+    for k in range(4):                 # no host sync between the replay and the eager call
+        g.replay()
+        with torch.cuda.stream(s):
+            pl.collective(0)
+        check(f"replay_then_eager_nosync{k}")
+    for k in range(4):
+        with torch.cuda.stream(s):
+            pl.collective(0)
+            pl.collective(0)
+        check(f"eager_eager_nosync{k}")
+    for k in range(4):
+        g.replay()
+        g.replay()
+        check(f"replay_replay_nosync{k}")
     for o in out:
         if o["bad"] or rank == 0:
             print(json.dumps(o), flush=True)
