@@ -1402,113 +1402,6 @@ __global__ void init_range_kernel(const float* src, uint64_t key, int64_t begin,
 int adam_grid() { return 148 * 8; }
 int adam_block() { return kAdamBlock; }
 
-// ------------------------------------------------------------- LL one-round all-reduce
-__device__ __forceinline__ void st_ll(unsigned char* p, uint32_t d0, uint32_t d1, uint32_t flag) {
-  asm volatile("st.volatile.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(d0), "r"(flag), "r"(d1),
-               "r"(flag)
-               : "memory");
-}
-__device__ __forceinline__ uint4 ld_ll(const unsigned char* p) {
-  uint4 v;
-  asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];"
-               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-               : "l"(p)
-               : "memory");
-  return v;
-}
-
-// One launch per bucket: phase 1 pushes this rank's raw bucket to every peer
-// (grid-stride over 16-byte lines: 4 bf16 payload + 2 flags), phase 2 folds
-// every output unit of 8 elements in the task's canonical (nested) order,
-// reading peer inputs from the local receive lines once both flags of each
-// line carry this launch's flag.  The receive slot alternates parity per
-// launch: a sender at launch e has consumed its peers' lines of launch e-1,
-// so the receiver is past launch e-2, the last user of that parity.
-__global__ void __launch_bounds__(256) ll_allreduce_kernel(const LLArgs a) {
-  if (*(volatile int*)a.err) return;
-  const unsigned int e = *(volatile unsigned int*)a.epoch;
-  const uint32_t flag = e + 1u;
-  const int64_t par = (e & 1u) ? a.parity_bytes : 0;
-  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, nth = (int64_t)gridDim.x * blockDim.x;
-  // phase 1: push
-  const uint2* src = reinterpret_cast<const uint2*>(a.src);
-  const int64_t lines = a.n / 4;
-  for (int64_t l = tid; l < lines; l += nth) {
-    const uint2 d = src[l];
-    for (int q = 0; q < a.npeers; ++q) st_ll(a.peer_slot[q] + par + l * 16, d.x, d.y, flag);
-  }
-  // phase 2: fold
-  const uint64_t t0 = globaltimer();
-  for (int ti = 0; ti < a.ntasks; ++ti) {
-    const DTask* tk = a.tasks + ti;
-    const int nin = tk->nin;
-    const uint32_t raw = tk->rawmask, pm = tk->peermask;
-    const int nest = tk->nest > 1 ? tk->nest : nin, nblk = tk->nest > 1 ? tk->nblk : 1;
-    for (int64_t u = tid; u < tk->n8; u += nth) {
-      auto ld = [&](int i, float x[8]) -> bool {
-        if ((pm >> i) & 1u) {
-          const unsigned char* p = reinterpret_cast<const unsigned char*>(tk->in[i]) + par + u * 32;
-          uint4 v0 = ld_ll(p), v1 = ld_ll(p + 16);
-          while (v0.y != flag || v0.w != flag || v1.y != flag || v1.w != flag) {
-            if (*(volatile int*)a.err || globaltimer() - t0 > kTimeoutNs) {
-              atomicExch(a.err, 2);
-              return false;
-            }
-            v0 = ld_ll(p);
-            v1 = ld_ll(p + 16);
-          }
-          unpack8(make_uint4(v0.x, v0.z, v1.x, v1.z), x);
-        } else {
-          unpack8(reinterpret_cast<const uint4*>(tk->in[i])[u], x);
-        }
-        if ((raw >> i) & 1u) scale_round8(x, a.alpha);
-        return true;
-      };
-      float acc[8];
-      int i = 0;
-      for (int b = 0; b < nblk; ++b) {
-        float blk[8];
-        if (!ld(i++, blk)) return;
-        for (int q = 1; q < nest; ++q) {
-          float x[8];
-          if (!ld(i++, x)) return;
-          hop8(blk, x);
-        }
-        if (b == 0) {
-#pragma unroll
-          for (int k = 0; k < 8; ++k) acc[k] = blk[k];
-        } else {
-          hop8(acc, blk);
-        }
-      }
-      for (; i < nin; ++i) {
-        float x[8];
-        if (!ld(i, x)) return;
-        hop8(acc, x);
-      }
-      __stcg(reinterpret_cast<uint4*>(tk->dst) + u, pack8(acc));
-    }
-  }
-  // payload bytes pushed, by link class; the last CTA out advances the epoch
-  if (threadIdx.x == 0) {
-    if (a.moved && blockIdx.x == 0) {
-      unsigned long long mi = 0, me = 0;
-      for (int q = 0; q < a.npeers; ++q) (a.peer_inter[q] ? me : mi) += (unsigned long long)a.n * 2;
-      flush_moved(a.moved, mi, me);
-    }
-    __threadfence();
-    if (atomicAdd(a.epoch + 1, 1u) + 1u == gridDim.x) {
-      atomicExch(a.epoch + 1, 0u);
-      atomicExch(a.epoch, e + 1u);
-    }
-  }
-}
-
-cudaError_t launch_ll_allreduce(const LLArgs& a, int grid, cudaStream_t s) {
-  ll_allreduce_kernel<<<grid, 256, 0, s>>>(a);
-  return cudaGetLastError();
-}
-
 // All kernels that may share an SM prefer the maximum shared-memory carveout,
 // so the SM never has to drain to re-split L1/shared between a collective CTA
 // and an Adam CTA.

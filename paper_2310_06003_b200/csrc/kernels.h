@@ -140,27 +140,6 @@ enum AdamVariant : int {
 // ws: 1 the warp-specialized TMA-store kernel, 0 the single-role one, -1 automatic
 cudaError_t launch_adam_tma(const AdamArgs& a, int sms, cudaStream_t s, int smem_budget_kb, int tma_store,
                             int hard_kb, int* variant, int* stages, int ws);
-// Flag-in-data one-round all-reduce (small one-shot buckets, real mode): every
-// rank pushes its raw bucket into each peer's LL receive slot as 16-byte lines
-// {d0, flag, d1, flag} (4 bf16 per line, each 8-byte half self-validating),
-// then folds every element from its own gradients and the peers' lines, polling
-// the flags.  No barriers: the lines carry the synchronisation (NCCL's LL idea).
-constexpr int kLLMaxPeers = 7;
-struct LLArgs {
-  const DTask* tasks;           // the one-round all-reduce tasks of this rank; peermask bit i: input
-  int ntasks;                   //   i is an LL line base (parity 0) in this rank's receive buffer
-  const uint16_t* src;          // this rank's raw bucket (n elements, n % 8 == 0)
-  int64_t n;
-  unsigned char* peer_slot[kLLMaxPeers];   // each peer's receive slot for this rank (parity 0)
-  int peer_inter[kLLMaxPeers];             // 1: that peer is in another group (moved-byte class)
-  int npeers;
-  int64_t parity_bytes;         // offset of parity 1 in every receive buffer
-  unsigned int* epoch;          // [0] launches so far (flag = epoch + 1, parity = epoch & 1), [1] exit count
-  int* err;                     // sticky device error word (timeout)
-  float alpha;
-  unsigned long long* moved;    // [intra, inter] payload bytes pushed (or NULL)
-};
-cudaError_t launch_ll_allreduce(const LLArgs& a, int grid, cudaStream_t s);
 // generic: the launch has fp32-wire (out_f32) or nested (one-shot) tasks
 cudaError_t launch_rounds_tma(const RoundsArgs& a, int grid, int max_in, cudaStream_t s, int bulk_store,
                               int generic);

@@ -84,14 +84,6 @@ struct DevLaunch {
   // copy-engine tail (opts.copy_engine = 3): the launch's trailing pure-copy
   // rounds, run by the copy engines after the kernel's rounds [0, nrounds)
   std::vector<DevLaunch> tail;
-  // flag-in-data one-round all-reduce (planner ll): tasks [ll_t0, ll_t0 + ll_nt) of
-  // the device task array, this rank's raw bucket, the peers' receive slots
-  bool ll = false;
-  int32_t ll_t0 = 0, ll_nt = 0;
-  void* ll_src = nullptr;
-  int64_t ll_n = 0, ll_parity = 0;
-  std::vector<unsigned char*> ll_peer;
-  std::vector<int> ll_inter;
 };
 
 struct paro_plan {
@@ -104,7 +96,6 @@ struct paro_plan {
   uint64_t** d_peer_slot = nullptr;       // real mode
   uint64_t** d_peer_slot2 = nullptr;      // second barrier channel (copy-engine launches)
   uint64_t** d_peer_slot3 = nullptr;      // third channel (parameter consumer stream)
-  unsigned int* d_ll_epoch = nullptr;     // flag-in-data all-reduce: [launches so far, exit count]
   paro_param_consumer_t cons_fn = nullptr;  // per-bucket consumer of the updated parameters
   void* cons_user = nullptr;
   cudaEvent_t ev_cons = nullptr;
@@ -441,48 +432,6 @@ paro_status_t upload_schedule(PlanT* p) {
         dl.round_peers[r] = (ctx->mode == MODE_REAL) ? L.barrier_peers(r, ctx->rank) : 0;
       }
     }
-    // flag-in-data one-round all-reduce (planner ll: one-shot NNN, small buckets):
-    // the peers' raw inputs are read from this rank's LL receive lines, which
-    // the peers fill by pushing their raw buckets (kernels.cu ll_allreduce_kernel)
-    if (allow_tail && pl.ll && ctx->mode == MODE_REAL && R == 1 && dl.tail.empty() && !dl.dma) {
-      const int me = ctx->rank;
-      bool ok = !L.rounds[0][me].empty();
-      int64_t g0 = INT64_MAX, g1 = 0;
-      for (const Task& t : L.rounds[0][me]) {
-        ok = ok && t.nin == pl.N && t.dst.rank == me && pl.esz[t.dst.kind] == 2;
-        for (int i = 0; i < t.nin && ok; ++i) {
-          ok = t.in[i].kind == BUF_GRAD;
-          g0 = std::min(g0, t.in[i].off);
-          g1 = std::max(g1, t.in[i].off + t.n);
-        }
-      }
-      ok = ok && g1 - g0 <= pl.B && g0 % 8 == 0 && (g1 - g0) % 8 == 0;
-      if (ok) {
-        const int64_t slot = int64_t(4) * pl.B;   // bytes per sender and parity
-        dl.ll = true;
-        dl.ll_src = data_ptr(p, me, BUF_GRAD, g0);
-        dl.ll_n = g1 - g0;
-        dl.ll_parity = slot * pl.N;
-        for (int q = 0; q < pl.N; ++q) {
-          if (q == me) continue;
-          dl.ll_peer.push_back(reinterpret_cast<unsigned char*>(data_ptr(p, q, BUF_LL, 0)) + slot * me);
-          dl.ll_inter.push_back(q / pl.M != me / pl.M ? 1 : 0);
-        }
-        unsigned char* mine = reinterpret_cast<unsigned char*>(data_ptr(p, me, BUF_LL, 0));
-        const int32_t t0 = rounds.back().t0;
-        dl.ll_t0 = t0;
-        dl.ll_nt = rounds.back().t1 - t0;
-        int k = 0;
-        for (const Task& t : L.rounds[0][me]) {
-          DTask& d = tasks[t0 + k++];
-          for (int i = 0; i < t.nin; ++i) {
-            const int q = t.in[i].rank;
-            if (q == me) continue;   // own raw gradients: read in place
-            d.in[i] = reinterpret_cast<const uint16_t*>(mine + slot * q + (t.in[i].off - g0) / 4 * 16);
-          }
-        }
-      }
-    }
     return dl;
   };
   // copies of raw gradient chunks (no round barriers: the data is immutable in a step)
@@ -665,28 +614,6 @@ paro_status_t run_launch(PlanT* p, const DevLaunch& dl, int* nlaunch, bool* tail
 // The rounds-kernel part of a launch, on the comm stream.
 paro_status_t run_launch_kernel(PlanT* p, const DevLaunch& dl, int* nlaunch) {
   paro_ctx* ctx = p->ctx;
-  if (dl.ll) {   // flag-in-data one-round all-reduce: no barriers
-    LLArgs a{};
-    a.tasks = p->d_tasks + dl.ll_t0;
-    a.ntasks = dl.ll_nt;
-    a.src = static_cast<const uint16_t*>(dl.ll_src);
-    a.n = dl.ll_n;
-    a.npeers = (int)dl.ll_peer.size();
-    for (int q = 0; q < a.npeers; ++q) {
-      a.peer_slot[q] = dl.ll_peer[q];
-      a.peer_inter[q] = dl.ll_inter[q];
-    }
-    a.parity_bytes = dl.ll_parity;
-    a.epoch = p->d_ll_epoch;
-    a.err = reinterpret_cast<int*>(p->region[0] + 520);
-    a.alpha = p->alpha;
-    a.moved = p->d_moved;
-    const int k = prof_begin(p, ctx->comm, 1, dl.bytes, dl.hbm);
-    CK(launch_ll_allreduce(a, comm_grid(p), ctx->comm));
-    prof_end(p, ctx->comm, k);
-    ++*nlaunch;
-    return PARO_OK;
-  }
   if (dl.nrounds == 0 && (!dl.final_barrier || ctx->mode != MODE_REAL)) return PARO_OK;
   const int grid = comm_grid(p);
   RoundsArgs a{};
@@ -817,7 +744,6 @@ void destroy_plan(PlanT* p) {
     cudaFree(p->d_peer_slot);
     cudaFree(p->d_peer_slot2);
     cudaFree(p->d_peer_slot3);
-    cudaFree(p->d_ll_epoch);
     if (p->ev_cons) cudaEventDestroy(p->ev_cons);
     for (cudaEvent_t e : p->ev_pfinal) if (e) cudaEventDestroy(e);
     cudaFree(p->d_rounds);
@@ -1111,8 +1037,6 @@ paro_status_t paro_plan(paro_ctx_t ctx, const char* strategy, const int64_t* par
     for (int x = 0; x < N; ++x) slots[x] = reinterpret_cast<uint64_t*>(p->peer_base[x] + 2048) + ctx->rank;
     PCK(cudaMalloc(&p->d_peer_slot3, 64 * sizeof(uint64_t*)));
     PCK(cudaMemcpy(p->d_peer_slot3, slots.data(), 64 * sizeof(uint64_t*), cudaMemcpyHostToDevice));
-    PCK(cudaMalloc(&p->d_ll_epoch, 2 * sizeof(unsigned int)));
-    PCK(cudaMemset(p->d_ll_epoch, 0, 2 * sizeof(unsigned int)));
   }
   {
     paro_status_t s2 = upload_schedule(p);

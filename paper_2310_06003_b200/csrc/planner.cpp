@@ -21,14 +21,6 @@ constexpr int64_t kAlignElems = 128;  // 256-byte alignment of buffer kinds
 constexpr int64_t kOneRoundExtraBytes = int64_t(6) << 20;   // one-shot AR: extra bytes worth one barrier
 constexpr int64_t kOneShotMaxBytes = int64_t(256) << 20;    // one-shot topology: larger buckets use HO-Ring
 
-// one-shot NNN all-reduce of buckets up to this many bytes: flag-in-data (LL) lines
-// instead of barriers (PARO_LL_MAX_KB overrides; 0 disables)
-constexpr int64_t kLLMaxBytes = int64_t(4) << 20;
-int64_t ll_max_bytes() {
-  const char* v = std::getenv("PARO_LL_MAX_KB");
-  return v ? int64_t(std::atoll(v)) << 10 : kLLMaxBytes;
-}
-
 // PARO_ONESHOT_MAX_MB overrides the threshold (measurement runs)
 int64_t oneshot_max_bytes() {
   const char* v = std::getenv("PARO_ONESHOT_MAX_MB");
@@ -417,13 +409,6 @@ void Planner::layout() {
   buf_len[BUF_GACC] = (opt.accum && G == LV_N) ? psi_pad : 0;
   buf_len[BUF_WIN] = (opt.windows > 0 && P != LV_N && N > 1) ? int64_t(opt.windows) * B : 0;
   buf_len[BUF_XW] = (opt.wire == 4 && opt.topology == 4 && N > 1) ? B : 0;
-  // the one-round one-shot all-reduce (emit_world_reduce) of small buckets, bf16 wire, pull
-  {
-    const int64_t extra = (int64_t)(N - 1) * (N - 2) * B * 2 / N;
-    ll = opt.topology == 6 && OS == LV_N && N > 1 && N <= 8 && opt.wire == 2 && !opt.push &&
-         !opt.params_only && 2 * B <= ll_max_bytes() && (N == 2 || extra <= kOneRoundExtraBytes);
-  }
-  buf_len[BUF_LL] = ll ? int64_t(4) * N * B : 0;
   acc_kind = !opt.accum ? -1 : (G == LV_N ? BUF_GACC : BUF_GSHARD);
   if (opt.params_only) {   // frozen tensors: no gradient, no optimizer state, no staging
     for (int k = 0; k < BUF_NKINDS; ++k)
@@ -434,7 +419,7 @@ void Planner::layout() {
   // raw gradients and parameters are bf16; every buffer that holds a
   // reduction partial or g_hat carries the wire type
   for (int k = 0; k < BUF_NKINDS; ++k) esz[k] = opt.wire;
-  esz[BUF_GRAD] = esz[BUF_PARAM] = esz[BUF_WIN] = esz[BUF_LL] = 2;
+  esz[BUF_GRAD] = esz[BUF_PARAM] = esz[BUF_WIN] = 2;
   int64_t off = 0;
   for (int k = 0; k < BUF_NKINDS; ++k) {
     buf_off[k] = off;

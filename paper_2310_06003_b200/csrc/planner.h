@@ -31,8 +31,6 @@ enum BufKind : int {
   BUF_GACC,        // G = N gradient accumulator (psi_pad; only for grad_accum plans)
   BUF_WIN,         // forward/backward parameter gather windows: n_windows x B (P = I or G)
   BUF_XW,          // NCCL comparator on the fp32 wire: the bucket's pre-scaled fp32 gradients (B)
-  BUF_LL,          // flag-in-data receive lines of the small one-shot all-reduce: 2 parities x N
-                   // senders x B/4 lines of 16 B (4 B per element; esz 2 => 4 N B units)
   BUF_NKINDS
 };
 
@@ -153,8 +151,6 @@ class Planner {
   PlanOptions opt;
   int64_t psi = 0, psi_pad = 0, B = 0;
   bool fused_allreduce = false;   // the inter all-reduce runs inside Adam (R31)
-  bool ll = false;                // one-shot NNN all-reduce of small buckets through the
-                                  // flag-in-data kernel (real mode; BUF_LL allocated)
   std::vector<std::pair<int64_t, int64_t>> buckets;   // (start, size)
   std::vector<int64_t> bucket_real_end;               // end of the real (non-padding) elements per bucket
   std::vector<int64_t> param_sizes, param_offsets;

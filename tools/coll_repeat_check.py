@@ -1,5 +1,8 @@
-"""Debug: repeated one-shot NNN all-reduces (flag-in-data kernel) eager and
-graph-replayed; every result is compared with the first eager call's."""
+"""Repeated NNN all-reduces (paro_collective(0)), eager and graph-replayed,
+with and without host synchronisation between calls (back-to-back launches
+race the device-resident barrier generations if anything is wrong); every
+result is compared with the first eager call's.  argv: bucket multiplier,
+topology."""
 import json
 import os
 import sys
@@ -24,7 +27,8 @@ def main():
     ctx = paro.Context(world, M, mode="real", rank=rank, device=rank, uid=bytes(t.tolist()))
     B = world * 64 * int(sys.argv[1] if len(sys.argv) > 1 else 32)
     s = torch.cuda.Stream()
-    pl = paro.Plan(ctx, "NNN", [3 * B], bucket_elems=B, topology="oneshot", fuse_allreduce=False, stream=s.cuda_stream)
+    topo = sys.argv[2] if len(sys.argv) > 2 else "oneshot"
+    pl = paro.Plan(ctx, "NNN", [3 * B], bucket_elems=B, topology=topo, fuse_allreduce=False, stream=s.cuda_stream)
     pl.synth_grads(rank, 1234, 1)
     ghat = pl.buffer(rank, 3)
 
@@ -74,9 +78,11 @@ def main():
         g.replay()
         g.replay()
         check(f"replay_replay_nosync{k}")
+    nbad = sum(o["bad"] > 0 for o in out)
     for o in out:
-        if o["bad"] or rank == 0:
+        if o["bad"]:
             print(json.dumps(o), flush=True)
+    print(json.dumps({"rank": rank, "topology": topo, "checks": len(out), "failed": nbad}), flush=True)
     pl.close()
     ctx.close()
     dist.destroy_process_group()
