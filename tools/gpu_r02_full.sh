@@ -16,3 +16,7 @@ if [ -z "$NO_BENCH" ]; then
   fi
   head -c 1500 gpurun_out/bench_n$NG.json
 fi
+if [ -n "$ALSO_N2" ] && [ "$NG" -ge 2 ]; then
+  CUDA_VISIBLE_DEVICES=0,1 timeout 1200 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29612 bench.py --gpus 2 ${BENCH_ARGS} > gpurun_out/bench_n2.json 2> gpurun_out/bench_n2.err; echo "bench n2 rc=$?"
+  head -c 600 gpurun_out/bench_n2.json
+fi
