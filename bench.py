@@ -337,7 +337,11 @@ def run_ours(args):
         roof = {"bound": "nvlink", "kernel": {"tma": "rounds_tma_kernel<false>", "tma_store": "rounds_tma_kernel<true>"}.get(
                     args.comm_impl, "rounds_kernel") + " (collective rounds: NVLink pull + hop)",
                 "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
-                "traffic": None, "algorithmic_bytes_per_launch": alg,
+                "traffic": None,
+                "traffic_note": "ncu replays one process's kernels; launches that wait on peer GPUs cannot be "
+                                "replayed under it, so this kernel's DRAM traffic comes from the emulated "
+                                "single-GPU capture (profiles/r02/ncu/prof_rounds_emulated_r02_*.csv)",
+                "algorithmic_bytes_per_launch": alg,
                 "launch_ms": comm_ms, "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s/dir",
                 "share_of_step": prof["comm_ms"] / max(1e-9, ms * args.steps),
                 # the Adam kernel beside it pulls the fused final hop's operands over the same
